@@ -1,0 +1,180 @@
+/*
+ * sfb200 — B200-native (sm_100a) P2ENet + Gaussian-splat render path, C ABI.
+ *
+ * The drop-in boundary of this repo. Every entry point takes plain pointers
+ * and sizes (no torch types); array arguments are DEVICE pointers unless the
+ * name says host, and are caller-owned (the library never frees them).
+ * Scratch comes from a per-context grow-only arena; all work is stream-ordered
+ * on the context's stream (sfb_set_stream). Calls return SFB_OK (0) or an
+ * error code; sfb_last_error(ctx) gives the message.
+ *
+ * Each entry cites the reference interface it replaces (paths relative to
+ * /root/reference/pkg/src/splatforge). Layouts follow the reference:
+ * float64 SoA splats (gaussians.py:28-84, quaternions w,x,y,z), camera
+ * p_cam = R p + t (gaussians.py:87-137), planes row-major (H, W[, 3]).
+ */
+#ifndef SFB200_H
+#define SFB200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum {
+    SFB_OK = 0,
+    SFB_ERR_ARG = 1,    /* invalid argument (the reference raises ValueError) */
+    SFB_ERR_OOM = 2,    /* device allocation failed */
+    SFB_ERR_CUDA = 3,   /* CUDA runtime / launch error */
+    SFB_ERR_STATE = 4,  /* e.g. network not loaded */
+};
+
+/* Render planes (bit mask for sfb_render). */
+enum { SFB_PLANE_RGB = 1, SFB_PLANE_NORMAL = 2, SFB_PLANE_DEPTH = 4 };
+
+/* P2ENet arithmetic: fp32 SIMT gather-GEMM, or tcgen05 (3xTF32, fp32-accurate). */
+enum { SFB_NET_SIMT_F32 = 0, SFB_NET_TC_TF32X3 = 1 };
+
+typedef struct sfb_ctx sfb_ctx;
+
+typedef struct {
+    double rot[9];      /* row-major; rows are the camera axes */
+    double trans[3];
+    double fx, fy, cx, cy;
+    int32_t width, height;
+} sfb_camera;
+
+typedef struct {        /* rasterizer.py:25-29 RenderOptions */
+    int32_t tile_size;  /* 16 */
+    int32_t early_termination;
+    double alpha_max;   /* 0.99 */
+} sfb_render_options;
+
+typedef struct {        /* gaussians.py:28-84 Splats, float64 SoA, device */
+    const double *centers;      /* (n,3) */
+    const double *scales;       /* (n,3) sigma, strictly positive */
+    const double *quaternions;  /* (n,4) w,x,y,z */
+    const double *opacities;    /* (n,) */
+    const double *colors;       /* (n,3) */
+    const double *normals;      /* (n,3) */
+    int64_t n;
+} sfb_splats;
+
+typedef struct {        /* per-call timing / size report (host struct) */
+    int64_t kept;       /* splats surviving the cull */
+    int64_t runs;       /* depth-ordered runs of identical geometry */
+    int64_t fine_entries, super_entries, global_entries;
+    int64_t voxels[8];  /* per-level voxel counts of the last network pass */
+} sfb_stats;
+
+/* ---- context ------------------------------------------------------------ */
+int sfb_ctx_create(int device, sfb_ctx **out);
+int sfb_ctx_destroy(sfb_ctx *ctx);
+const char *sfb_last_error(sfb_ctx *ctx);
+int sfb_set_stream(sfb_ctx *ctx, void *cuda_stream);     /* cudaStream_t */
+int sfb_get_stats(sfb_ctx *ctx, sfb_stats *out);         /* host out */
+int sfb_version(void);
+
+/* ---- voxelization (voxelgrid.py:125-168, voxelize_adaptive) ------------- */
+/* bbox of (n,3) device positions -> host lo_hi[6] = (lo xyz, hi xyz). The
+ * caller forms s = (n / prod(hi-lo)) ** (1/3) in host float64 exactly as
+ * voxelgrid.py:133-141 does, so the lattice scale is bit-identical. */
+int sfb_bbox(sfb_ctx *ctx, const double *positions, int64_t n, double *lo_hi_host);
+
+/* Density-1 voxelization at scale s. Outputs (capacity n / n+1):
+ * coords (M,3) int32 in canonical packed-key order, feats (M,9) float64
+ * [centroid/s, mean colour, clipped residual], keys (M,) int64 packed as
+ * voxelgrid.py:22-27, point_to_voxel (n,), source_order (n,),
+ * source_offsets (M+1,) int32; *m_host receives M. */
+int sfb_voxelize(sfb_ctx *ctx, const double *positions, const double *colors, int64_t n,
+                 double s, const double *lo_hi_host, int32_t *coords, double *feats,
+                 int64_t *keys, int32_t *point_to_voxel, int32_t *source_order,
+                 int32_t *source_offsets, int64_t *m_host);
+
+/* ---- kernel maps (sparsenet.py:178-214 lookups, voxelgrid.py:88-94) ------- */
+/* Neighbour rows of a canonical grid for a k^3 stride-s conv, (m, k^3) int32,
+ * -1 where empty; taps in lexicographic (dz,dy,dx) order. Bit-exact with the
+ * reference's searchsorted lookups. */
+int sfb_kernel_map(sfb_ctx *ctx, const int32_t *coords, int64_t m, int32_t stride,
+                   int32_t kernel, int32_t *map_out);
+/* Parent row (-1 = orphan) and child tap (dz*4+dy*2+dx) of each target
+ * (sparsenet.py:233-238). parent grid given by canonical coords. */
+int sfb_transposed_map(sfb_ctx *ctx, const int32_t *parent_coords, int64_t m_parent,
+                       int32_t parent_stride, const int32_t *targets, int64_t m_targets,
+                       int32_t *parent_out, int32_t *tap_out);
+/* pool_2x2x2 (voxelgrid.py:171-185) on float32 features: parent coords
+ * (canonical), means of occupied children in child-row order, child->parent. */
+int sfb_pool(sfb_ctx *ctx, const int32_t *coords, const float *feats, int64_t m, int32_t c,
+             int32_t stride, int32_t *parent_coords, float *parent_feats,
+             int32_t *child_to_parent, int64_t *m_parent_host);
+
+/* ---- P2ENet (sparsenet.py:187-287, 310-341) ------------------------------ */
+/* Parse a P2EN weight blob (host bytes, sparsenet.py:344-434 layout) and
+ * upload the packed per-layer operands; replaces load_weights/NetworkWeights. */
+int sfb_net_load(sfb_ctx *ctx, const void *p2en_blob_host, size_t nbytes);
+int sfb_net_set_mode(sfb_ctx *ctx, int mode);          /* SFB_NET_* */
+/* A standalone conv (kind 0) / transposed_conv (kind 1) layer from host
+ * float32 weights (k,k,k,in,out) and bias, addressed as layer -1 below
+ * (sparse_conv / transposed_conv_pruned take their own weights,
+ * sparsenet.py:187, 217). */
+int sfb_layer_set(sfb_ctx *ctx, int kind, int kernel, int cin, int cout, const float *w_host,
+                  const float *b_host);
+/* Single layers on caller tensors (float32 features); layer = index into the
+ * loaded network, or -1 for the standalone layer. */
+int sfb_sparse_conv(sfb_ctx *ctx, int layer, const int32_t *coords, const float *feats,
+                    int64_t m, int32_t stride, int relu, float *out);
+int sfb_transposed_conv(sfb_ctx *ctx, int layer, const int32_t *parent_coords,
+                        const float *parent_feats, int64_t m_parent, int32_t parent_stride,
+                        const int32_t *targets, int64_t m_targets, int relu, float *out);
+/* Full UNet + head on a voxelized cloud: raw (m0,14) float32 per voxel. */
+int sfb_unet_forward(sfb_ctx *ctx, const int32_t *coords, const double *feats9, int64_t m0,
+                     float *raw_out);
+/* activate_head per row (sparsenet.py:310-341), float64 outputs. */
+int sfb_activate_head(sfb_ctx *ctx, const float *raw, int64_t m, double voxel_scale,
+                      double *delta, double *sigma, double *quat, double *opacity,
+                      double *normal);
+
+/* ---- estimate_neural (estimators.py:214-231) ----------------------------- */
+/* Cloud -> per-point Splats (float64 SoA, caller buffers of n rows). colors
+ * are copied from the input. s as for sfb_voxelize. */
+int sfb_estimate_neural(sfb_ctx *ctx, const double *positions, const double *colors,
+                        int64_t n, double s, const double *lo_hi_host, double *centers,
+                        double *scales, double *quaternions, double *opacities,
+                        double *colors_out, double *normals);
+
+/* ---- render (rasterizer.py:152-166, _raster_kernels.py:20-201) ------------ */
+/* Tiled front-to-back splatting of any Splats batch. plane_mask selects the
+ * planes written in ONE pass (alpha/T do not depend on the attribute):
+ * rgb (H,W,3) = sum + T*bg, normal (H,W,3) renormalised, depth (H,W),
+ * trans (H,W) clipped to [0,1]; all float32, NULL for planes not requested. */
+int sfb_render(sfb_ctx *ctx, const sfb_splats *splats, const sfb_camera *cam,
+               const sfb_render_options *opts, int32_t plane_mask, const double *background3,
+               float *rgb, float *normal, float *depth, float *trans);
+
+/* project_kernel seam (_raster_kernels.py:20-105): per splat, float64. */
+int sfb_project(sfb_ctx *ctx, const sfb_splats *splats, const sfb_camera *cam, double z_near,
+                double dilation, double *sx, double *sy, double *depth, double *cov_a,
+                double *cov_b, double *cov_c, double *radius, uint8_t *keep);
+
+/* _prepare + bin_tiles seam (rasterizer.py:99-130, _raster_kernels.py:108-143):
+ * materialises the reference CSR for parity checks. source (capacity n)
+ * rank->splat, offsets (ntx*nty+1), ids (capacity ids_capacity); K and E out.
+ * If E > ids_capacity nothing is written to ids (call again with room). */
+int sfb_prepare_debug(sfb_ctx *ctx, const sfb_splats *splats, const sfb_camera *cam,
+                      int32_t tile_size, int64_t *source, double *radius, int64_t *offsets,
+                      int64_t *ids, int64_t ids_capacity, int64_t *k_host, int64_t *e_host);
+
+/* ---- fused frame: cloud -> P2ENet -> splat, no per-point splats ---------- */
+/* The bench hot path: voxelize, UNet, head, then render the per-voxel
+ * Gaussians broadcast to their points (colours per point) straight to planes. */
+int sfb_frame(sfb_ctx *ctx, const double *positions, const double *colors, int64_t n, double s,
+              const double *lo_hi_host, const sfb_camera *cam, const sfb_render_options *opts,
+              int32_t plane_mask, const double *background3, float *rgb, float *normal,
+              float *depth, float *trans);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -1,0 +1,151 @@
+"""ctypes binding of libsfb200.so (the C ABI declared in include/sfb200.h).
+
+There is no CPU fallback: if the shared library is missing or no CUDA device
+is present, every entry point raises. Device buffers come from torch
+(``tensor.data_ptr()``); launches go on torch's current CUDA stream so torch
+events and the library's kernels share one timeline.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import threading
+from pathlib import Path
+
+PKG = Path(__file__).resolve().parent
+LIB_PATH = PKG / "_build" / "libsfb200.so"
+
+SFB_OK, SFB_ERR_ARG, SFB_ERR_OOM, SFB_ERR_CUDA, SFB_ERR_STATE = 0, 1, 2, 3, 4
+PLANE_RGB, PLANE_NORMAL, PLANE_DEPTH = 1, 2, 4
+NET_SIMT_F32, NET_TC_TF32X3 = 0, 1
+
+P = ctypes.c_void_p
+I64 = ctypes.c_int64
+I32 = ctypes.c_int32
+D = ctypes.c_double
+
+
+class Camera_t(ctypes.Structure):
+    _fields_ = [("rot", D * 9), ("trans", D * 3), ("fx", D), ("fy", D), ("cx", D), ("cy", D),
+                ("width", I32), ("height", I32)]
+
+
+class RenderOptions_t(ctypes.Structure):
+    _fields_ = [("tile_size", I32), ("early_termination", I32), ("alpha_max", D)]
+
+
+class Splats_t(ctypes.Structure):
+    _fields_ = [("centers", P), ("scales", P), ("quaternions", P), ("opacities", P),
+                ("colors", P), ("normals", P), ("n", I64)]
+
+
+class Stats_t(ctypes.Structure):
+    _fields_ = [("kept", I64), ("runs", I64), ("fine_entries", I64), ("super_entries", I64),
+                ("global_entries", I64), ("voxels", I64 * 8)]
+
+
+# name -> argtypes (restype is always int)
+SIGNATURES = {
+    "sfb_ctx_create": [ctypes.c_int, ctypes.POINTER(P)],
+    "sfb_ctx_destroy": [P],
+    "sfb_last_error": [P],
+    "sfb_set_stream": [P, P],
+    "sfb_get_stats": [P, ctypes.POINTER(Stats_t)],
+    "sfb_version": [],
+    "sfb_bbox": [P, P, I64, P],
+    "sfb_voxelize": [P, P, P, I64, D, P, P, P, P, P, P, P, ctypes.POINTER(I64)],
+    "sfb_kernel_map": [P, P, I64, I32, I32, P],
+    "sfb_transposed_map": [P, P, I64, I32, P, I64, P, P],
+    "sfb_pool": [P, P, P, I64, I32, I32, P, P, P, ctypes.POINTER(I64)],
+    "sfb_net_load": [P, P, ctypes.c_size_t],
+    "sfb_net_set_mode": [P, ctypes.c_int],
+    "sfb_layer_set": [P, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int, P, P],
+    "sfb_sparse_conv": [P, ctypes.c_int, P, P, I64, I32, ctypes.c_int, P],
+    "sfb_transposed_conv": [P, ctypes.c_int, P, P, I64, I32, P, I64, ctypes.c_int, P],
+    "sfb_unet_forward": [P, P, P, I64, P],
+    "sfb_activate_head": [P, P, I64, D, P, P, P, P, P],
+    "sfb_estimate_neural": [P, P, P, I64, D, P, P, P, P, P, P, P],
+    "sfb_render": [P, ctypes.POINTER(Splats_t), ctypes.POINTER(Camera_t),
+                   ctypes.POINTER(RenderOptions_t), I32, P, P, P, P, P],
+    "sfb_project": [P, ctypes.POINTER(Splats_t), ctypes.POINTER(Camera_t), D, D] + [P] * 8,
+    "sfb_prepare_debug": [P, ctypes.POINTER(Splats_t), ctypes.POINTER(Camera_t), I32, P, P, P, P,
+                          I64, ctypes.POINTER(I64), ctypes.POINTER(I64)],
+    "sfb_frame": [P, P, P, I64, D, P, ctypes.POINTER(Camera_t), ctypes.POINTER(RenderOptions_t),
+                  I32, P, P, P, P, P],
+}
+
+_lib = None
+_lock = threading.Lock()
+_contexts = {}
+
+
+def load_library():
+    """dlopen libsfb200.so (no GPU needed to load) and declare every symbol."""
+    global _lib
+    if _lib is None:
+        if not LIB_PATH.exists():
+            raise ImportError(f"{LIB_PATH} is not built; run `python -c 'import __graft_entry__ as g; "
+                              f"g.build()'` (there is no CPU fallback)")
+        lib = ctypes.CDLL(str(LIB_PATH))
+        for name, args in SIGNATURES.items():
+            fn = getattr(lib, name)
+            fn.argtypes = args
+            fn.restype = ctypes.c_char_p if name == "sfb_last_error" else ctypes.c_int
+        _lib = lib
+    return _lib
+
+
+class SfbError(RuntimeError):
+    pass
+
+
+class Context:
+    """One library context per CUDA device (stream set per call)."""
+
+    def __init__(self, device: int):
+        import torch
+        if not torch.cuda.is_available():
+            raise RuntimeError("paper_2409_16504_b200 needs a CUDA device (B200); "
+                               "there is no CPU fallback")
+        self.lib = load_library()
+        self.device = device
+        h = P()
+        rc = self.lib.sfb_ctx_create(device, ctypes.byref(h))
+        if rc != SFB_OK:
+            raise SfbError(f"sfb_ctx_create failed ({rc})")
+        self.handle = h
+        self.lock = threading.RLock()
+        self.net_token = None
+
+    def call(self, name: str, *args):
+        import torch
+        stream = torch.cuda.current_stream(self.device).cuda_stream
+        self.lib.sfb_set_stream(self.handle, P(stream))
+        rc = getattr(self.lib, name)(self.handle, *args)
+        if rc != SFB_OK:
+            msg = self.lib.sfb_last_error(self.handle).decode(errors="replace")
+            if rc == SFB_ERR_ARG:
+                raise ValueError(msg)
+            raise SfbError(f"{name}: {msg} (code {rc})")
+
+    def stats(self) -> dict:
+        s = Stats_t()
+        self.lib.sfb_get_stats(self.handle, ctypes.byref(s))
+        return dict(kept=s.kept, runs=s.runs, fine_entries=s.fine_entries,
+                    super_entries=s.super_entries, global_entries=s.global_entries,
+                    voxels=list(s.voxels))
+
+
+def context(device=None) -> Context:
+    import torch
+    dev = torch.cuda.current_device() if device is None else int(device)
+    with _lock:
+        ctx = _contexts.get(dev)
+        if ctx is None:
+            ctx = _contexts[dev] = Context(dev)
+    return ctx
+
+
+def ptr(t) -> P:
+    """Device pointer of a torch tensor (None -> NULL)."""
+    return P(0) if t is None else P(t.data_ptr())

@@ -1,0 +1,240 @@
+// Shared runtime pieces of libsfb200: context, scratch arena, error plumbing.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <cstdio>
+#include <cstring>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/sfb200.h"
+
+namespace sfb {
+
+struct Error : std::runtime_error {
+    int code;
+    Error(int c, const std::string &m) : std::runtime_error(m), code(c) {}
+};
+
+#define SFB_CUDA(expr)                                                                      \
+    do {                                                                                    \
+        cudaError_t _e = (expr);                                                            \
+        if (_e != cudaSuccess)                                                              \
+            throw ::sfb::Error(_e == cudaErrorMemoryAllocation ? SFB_ERR_OOM : SFB_ERR_CUDA, \
+                               std::string(#expr) + ": " + cudaGetErrorString(_e));         \
+    } while (0)
+
+#define SFB_CHECK_LAUNCH() SFB_CUDA(cudaGetLastError())
+
+#define SFB_REQUIRE(cond, msg)                                    \
+    do {                                                          \
+        if (!(cond)) throw ::sfb::Error(SFB_ERR_ARG, (msg));      \
+    } while (0)
+
+// Grow-only device scratch: a list of chunks; a top-level call resets the
+// cursor, allocations bump through existing chunks and only allocate a new
+// chunk when none has room (so steady-state frames never call cudaMalloc).
+class Arena {
+  public:
+    ~Arena() {
+        for (auto &c : chunks_) cudaFree(c.ptr);
+    }
+    void reset() {
+        cur_ = 0;
+        off_ = 0;
+    }
+    template <class T>
+    T *alloc(size_t count) {
+        return static_cast<T *>(alloc_bytes(count * sizeof(T)));
+    }
+    void *alloc_bytes(size_t bytes) {
+        bytes = (bytes + 255) & ~size_t(255);
+        if (bytes == 0) bytes = 256;
+        while (cur_ < chunks_.size()) {
+            if (off_ + bytes <= chunks_[cur_].size) {
+                void *p = static_cast<char *>(chunks_[cur_].ptr) + off_;
+                off_ += bytes;
+                return p;
+            }
+            ++cur_;
+            off_ = 0;
+        }
+        size_t sz = bytes < (size_t(64) << 20) ? (size_t(64) << 20) : bytes;
+        void *p = nullptr;
+        SFB_CUDA(cudaMalloc(&p, sz));
+        chunks_.push_back({p, sz});
+        cur_ = chunks_.size() - 1;
+        off_ = bytes;
+        return p;
+    }
+    size_t reserved() const {
+        size_t s = 0;
+        for (auto &c : chunks_) s += c.size;
+        return s;
+    }
+
+  private:
+    struct Chunk {
+        void *ptr;
+        size_t size;
+    };
+    std::vector<Chunk> chunks_;
+    size_t cur_ = 0, off_ = 0;
+};
+
+struct NetLayer {
+    int kind;            // 0 conv, 1 transposed_conv, 2 mlp
+    int kernel, cin, cout, taps;
+    float *w = nullptr;  // device, [taps][cin][cout] float32 (reference order)
+    float *b = nullptr;  // device, [cout]
+    // tcgen05 operands (split tf32 hi/lo, K-major per tap, padded)
+    float *w_tc = nullptr;
+    int cin_pad = 0, cout_pad = 0;
+};
+
+struct Net {
+    bool loaded = false;
+    std::vector<int> enc, dec;
+    int head_hidden = 0, levels = 0;
+    std::vector<NetLayer> layers;
+    std::vector<void *> allocations;
+    void release() {
+        for (void *p : allocations) cudaFree(p);
+        allocations.clear();
+        layers.clear();
+        loaded = false;
+    }
+};
+
+}  // namespace sfb
+
+struct sfb_ctx {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    sfb::Arena arena;
+    sfb::Net net;
+    sfb::NetLayer adhoc;  // standalone layer for single-layer calls
+    int net_mode = SFB_NET_SIMT_F32;
+    int num_sms = 148;
+    std::string last_error;
+    sfb_stats stats{};
+    // pinned host staging for small D2H reads (sizes, bbox)
+    int64_t *pinned = nullptr;
+    ~sfb_ctx() {
+        net.release();
+        for (void *p : {(void *)adhoc.w, (void *)adhoc.b, (void *)adhoc.w_tc})
+            if (p) cudaFree(p);
+        if (pinned) cudaFreeHost(pinned);
+    }
+    // read `count` int64 values back from device (one sync)
+    void read_back(const void *dev, size_t bytes) {
+        SFB_CUDA(cudaMemcpyAsync(pinned, dev, bytes, cudaMemcpyDeviceToHost, stream));
+        SFB_CUDA(cudaStreamSynchronize(stream));
+    }
+};
+
+namespace sfb {
+
+inline unsigned grid_for(int64_t n, int block, int64_t cap = 1 << 20) {
+    int64_t g = (n + block - 1) / block;
+    if (g < 1) g = 1;
+    if (g > cap) g = cap;
+    return static_cast<unsigned>(g);
+}
+
+inline int bits_for(uint64_t range_inclusive_max) {
+    int b = 0;
+    while (b < 64 && (range_inclusive_max >> b) != 0) ++b;
+    return b;
+}
+
+// Packed voxel key of voxelgrid.py:22-27: ((z+B)<<42)|((y+B)<<21)|(x+B).
+__host__ __device__ inline int64_t pack_key(int64_t x, int64_t y, int64_t z) {
+    const int64_t B = int64_t(1) << 20;
+    return ((z + B) << 42) | ((y + B) << 21) | (x + B);
+}
+__host__ __device__ inline bool key_in_range(int64_t x, int64_t y, int64_t z) {
+    const int64_t L = int64_t(1) << 20;
+    return x > -L && x < L && y > -L && y < L && z > -L && z < L;
+}
+// Python floor division by a positive power of two
+__host__ __device__ inline int64_t floor_div(int64_t a, int64_t d) {
+    int64_t q = a / d;
+    return (a % d != 0 && a < 0) ? q - 1 : q;
+}
+
+// ---- cross-file launchers (defined in the .cu files) ----------------------
+
+// hashmap.cu
+struct HashTable {
+    unsigned long long *keys = nullptr;
+    int32_t *vals = nullptr;
+    uint32_t mask = 0;
+};
+HashTable hash_build(sfb_ctx *ctx, const int32_t *coords, int64_t m);
+void kernel_map_build(sfb_ctx *ctx, const HashTable &h, const int32_t *coords, int64_t m,
+                      int stride, int kernel, int32_t *map_tap_major);
+void transposed_lookup(sfb_ctx *ctx, const HashTable &h, int parent_stride,
+                       const int32_t *targets, int64_t m, int32_t *parent_out, int32_t *tap_out);
+// pooled parents in canonical order; returns parent count (one host sync)
+int64_t pool_build(sfb_ctx *ctx, const int32_t *coords, int64_t m, int stride, const float *feats,
+                   int c, int ld_in, int32_t *parent_coords, float *parent_feats, int ld_out,
+                   int32_t *child_to_parent);
+
+// voxelize.cu
+struct VoxelOut {
+    int32_t *coords;
+    double *feats;
+    int64_t *keys;
+    int32_t *p2v, *order, *offsets;
+    int64_t m;
+};
+void bbox_run(sfb_ctx *ctx, const double *pos, int64_t n, double *lo_hi_host);
+void voxelize_run(sfb_ctx *ctx, const double *pos, const double *col, int64_t n, double s,
+                  const double *lo_hi, VoxelOut &out);
+
+// net.cu
+void net_load(sfb_ctx *ctx, const void *blob, size_t n);
+// returns per-voxel raw head (m0 x 14) float32 in `raw`
+void unet_run(sfb_ctx *ctx, const int32_t *coords, const double *feats9, int64_t m0, float *raw);
+void activate_run(sfb_ctx *ctx, const float *raw, int64_t m, double scale, double *delta,
+                  double *sigma, double *quat, double *opac, double *normal);
+void conv_layer(sfb_ctx *ctx, const NetLayer &L, const float *in, int ld_in, const int32_t *nbr,
+                int64_t m, int relu, float *out, int ld_out);
+void tconv_layer(sfb_ctx *ctx, const NetLayer &L, const float *in, int ld_in,
+                 const int32_t *parent, const int32_t *tap, int64_t m, int relu, float *out,
+                 int ld_out);
+void layer_set(sfb_ctx *ctx, int kind, int kernel, int cin, int cout, const float *w_host,
+               const float *b_host);
+// per-voxel Gaussian parameters for the fused frame: centres, sigma, quat, opacity, normal
+void head_to_voxel_splats(sfb_ctx *ctx, const float *raw, const int32_t *coords,
+                          const double *feats9, int64_t m0, double scale, double *centers,
+                          double *sigma, double *quat, double *opac, double *normal);
+
+// render.cu
+struct RenderInputs {
+    // geometry, either per splat (n rows) or per voxel (geom rows) with a
+    // point->geometry map; attributes always per point
+    const double *centers, *scales, *quats, *opac;
+    int64_t n_geom;
+    const int32_t *point_to_geom;  // nullptr: identity (geometry per point)
+    const int32_t *geom_points;    // CSR points of each geometry (fused path), or nullptr
+    const int32_t *geom_offsets;
+    const double *colors, *normals;
+    int64_t n_points;
+};
+void render_run(sfb_ctx *ctx, const RenderInputs &in, const sfb_camera &cam,
+                const sfb_render_options &opts, int plane_mask, const double *bg, float *rgb,
+                float *normal, float *depth, float *trans);
+void project_run(sfb_ctx *ctx, const double *centers, const double *quats, const double *scales,
+                 int64_t n, const sfb_camera &cam, double z_near, double dilation, double *sx,
+                 double *sy, double *depth, double *ca, double *cb, double *cc, double *radius,
+                 uint8_t *keep);
+void prepare_debug_run(sfb_ctx *ctx, const RenderInputs &in, const sfb_camera &cam, int tile,
+                       int64_t *source, double *radius, int64_t *offsets, int64_t *ids,
+                       int64_t cap, int64_t *k_host, int64_t *e_host);
+
+}  // namespace sfb

@@ -1,0 +1,467 @@
+// P2ENet on the device: P2EN weight loading, gather-GEMM-scatter sparse
+// convolutions, pruned transposed convolutions, the fused 2-layer MLP head and
+// the head activations (reference: sparsenet.py:187-341, 390-434).
+//
+// Data layout in HBM, per level l (stride 2^l): canonical voxel coords
+// (M_l,3) int32, a tap-major kernel map (27, M_l) int32, and float32
+// row-major features. The decoder's skip concatenation [up, skip]
+// (sparsenet.py:278-282) is never materialised by a copy: the encoder conv of
+// level l writes its output straight into columns [C_up, C_up+C_skip) of the
+// level-l concat buffer, and the transposed conv later fills columns
+// [0, C_up) of the same rows.
+//
+// Arithmetic modes: SFB_NET_SIMT_F32 (fp32 FFMA gather-GEMM, the parity
+// anchor) and SFB_NET_TC_TF32X3 (tcgen05 tensor cores, tf32 hi/lo split
+// giving fp32-level accuracy; conv_tc.cu).
+#include <cmath>
+
+#include "common.cuh"
+
+namespace sfb {
+
+void conv_layer_tc(sfb_ctx *ctx, const NetLayer &L, const float *in, int ld_in, const int32_t *nbr,
+                   int64_t m, int relu, float *out, int ld_out);
+bool conv_tc_supported(const NetLayer &L);
+void prepare_tc_weights(sfb_ctx *ctx, NetLayer &L);
+
+// ------------------------------------------------------------ weight loading
+namespace {
+struct Cursor {
+    const uint8_t *p;
+    size_t n, pos = 0;
+    const uint8_t *take(size_t k) {
+        if (pos + k > n) throw Error(SFB_ERR_ARG, "weights: file ends inside a field");
+        const uint8_t *r = p + pos;
+        pos += k;
+        return r;
+    }
+    uint32_t u32() {
+        uint32_t v;
+        std::memcpy(&v, take(4), 4);
+        return v;
+    }
+    uint8_t u8() { return *take(1); }
+};
+}  // namespace
+
+void net_load(sfb_ctx *ctx, const void *blob, size_t nbytes) {
+    Cursor c{static_cast<const uint8_t *>(blob), nbytes};
+    if (std::memcmp(c.take(4), "P2EN", 4) != 0)
+        throw Error(SFB_ERR_ARG, "weights: not a weight file (bad magic)");
+    uint32_t version = c.u32();
+    if (version != 1) throw Error(SFB_ERR_ARG, "weights: unsupported version " + std::to_string(version));
+    uint32_t levels = c.u32();
+    std::vector<int> enc(c.u32()), dec;
+    for (auto &e : enc) e = (int)c.u32();
+    dec.resize(c.u32());
+    for (auto &d : dec) d = (int)c.u32();
+    int head_hidden = (int)c.u32();
+    uint32_t count = c.u32();
+    SFB_REQUIRE(enc.size() >= 3 && dec.size() == enc.size() - 2 && levels == dec.size(),
+                "weights: topology does not match its plan");
+    // expected layer chain (sparsenet.py:108-118)
+    struct Want { int kind, cin, cout; };
+    std::vector<Want> want;
+    for (size_t i = 0; i + 1 < enc.size(); ++i) want.push_back({0, enc[i], enc[i + 1]});
+    int width = enc.back();
+    for (size_t j = 0; j < dec.size(); ++j) {
+        want.push_back({1, width, dec[j]});
+        width = dec[j] + enc[enc.size() - 2 - j];
+    }
+    want.push_back({2, width, head_hidden});
+    want.push_back({2, head_hidden, 14});
+    SFB_REQUIRE(count == want.size(), "weights: layer count does not match the plan");
+
+    Net fresh;
+    try {
+        for (uint32_t i = 0; i < count; ++i) {
+            NetLayer L;
+            L.kind = c.u8();
+            L.kernel = c.u8();
+            L.cin = (int)c.u32();
+            L.cout = (int)c.u32();
+            SFB_REQUIRE(L.kind == want[i].kind && L.cin == want[i].cin && L.cout == want[i].cout,
+                        "weights: layer " + std::to_string(i) + " disagrees with the plan");
+            if (L.kind == 0) SFB_REQUIRE(L.kernel >= 1 && (L.kernel & 1), "weights: conv kernels must be odd");
+            if (L.kind == 1) SFB_REQUIRE(L.kernel == 2, "weights: transposed_conv kernel is fixed at 2");
+            if (L.kind == 2) SFB_REQUIRE(L.kernel == 1, "weights: mlp kernel is fixed at 1");
+            L.taps = L.kind == 2 ? 1 : L.kernel * L.kernel * L.kernel;
+            size_t nw = (size_t)L.taps * L.cin * L.cout;
+            const uint8_t *w = c.take(4 * nw);
+            const uint8_t *b = c.take(4 * (size_t)L.cout);
+            SFB_CUDA(cudaMalloc(&L.w, 4 * nw));
+            fresh.allocations.push_back(L.w);
+            SFB_CUDA(cudaMalloc(&L.b, 4 * (size_t)L.cout));
+            fresh.allocations.push_back(L.b);
+            SFB_CUDA(cudaMemcpyAsync(L.w, w, 4 * nw, cudaMemcpyHostToDevice, ctx->stream));
+            SFB_CUDA(cudaMemcpyAsync(L.b, b, 4 * (size_t)L.cout, cudaMemcpyHostToDevice, ctx->stream));
+            fresh.layers.push_back(L);
+        }
+        SFB_REQUIRE(c.pos == c.n, "weights: trailing bytes after last layer");
+        for (auto &L : fresh.layers)
+            if (L.kind == 0 && conv_tc_supported(L)) {
+                prepare_tc_weights(ctx, L);
+                fresh.allocations.push_back(L.w_tc);
+            }
+        SFB_CUDA(cudaStreamSynchronize(ctx->stream));
+    } catch (...) {
+        fresh.release();
+        throw;
+    }
+    ctx->net.release();
+    ctx->net = fresh;
+    ctx->net.enc = enc;
+    ctx->net.dec = dec;
+    ctx->net.head_hidden = head_hidden;
+    ctx->net.levels = (int)levels;
+    ctx->net.loaded = true;
+}
+
+// A standalone layer (sparse_conv / transposed_conv_pruned called with their
+// own weights, sparsenet.py:187, 217) kept in ctx->adhoc.
+void layer_set(sfb_ctx *ctx, int kind, int kernel, int cin, int cout, const float *w_host,
+               const float *b_host) {
+    SFB_REQUIRE(kind == 0 || kind == 1, "only conv / transposed_conv layers can be set");
+    SFB_REQUIRE(cin > 0 && cout > 0, "channel counts must be positive");
+    if (kind == 0) SFB_REQUIRE(kernel >= 1 && (kernel & 1), "conv kernels must be odd");
+    if (kind == 1) SFB_REQUIRE(kernel == 2, "transposed_conv kernel is fixed at 2");
+    NetLayer &L = ctx->adhoc;
+    for (void *p : {(void *)L.w, (void *)L.b, (void *)L.w_tc})
+        if (p) cudaFree(p);
+    L = NetLayer{};
+    L.kind = kind;
+    L.kernel = kernel;
+    L.cin = cin;
+    L.cout = cout;
+    L.taps = kernel * kernel * kernel;
+    size_t nw = (size_t)L.taps * cin * cout;
+    SFB_CUDA(cudaMalloc(&L.w, 4 * nw));
+    SFB_CUDA(cudaMalloc(&L.b, 4 * (size_t)cout));
+    SFB_CUDA(cudaMemcpyAsync(L.w, w_host, 4 * nw, cudaMemcpyHostToDevice, ctx->stream));
+    SFB_CUDA(cudaMemcpyAsync(L.b, b_host, 4 * (size_t)cout, cudaMemcpyHostToDevice, ctx->stream));
+    if (kind == 0 && conv_tc_supported(L)) prepare_tc_weights(ctx, L);
+    SFB_CUDA(cudaStreamSynchronize(ctx->stream));
+}
+
+// ------------------------------------------------------------ SIMT gather-GEMM
+// CTA = 32 output rows x all output channels. Per tap: gather the 32
+// neighbour rows (zeros where empty) and W[tap] into shared memory, then
+// every thread accumulates its outputs over the tap's input channels.
+constexpr int kRows = 32;
+constexpr int kThreads = 256;
+constexpr int kMaxOut = 16;  // kRows * cout / kThreads for cout <= 128
+
+__global__ void __launch_bounds__(kThreads)
+k_conv_simt(const float *__restrict__ in, int ld_in, const int32_t *__restrict__ nbr, int64_t m,
+            int taps, int cin, int cout, const float *__restrict__ w, const float *__restrict__ b,
+            int relu, float *__restrict__ out, int ld_out) {
+    extern __shared__ float sm[];
+    float *A = sm;                  // [kRows][cin]
+    float *W = sm + kRows * cin;    // [cin][cout]
+    int64_t r0 = (int64_t)blockIdx.x * kRows;
+    int nout = kRows * cout;
+    float acc[kMaxOut];
+#pragma unroll
+    for (int k = 0; k < kMaxOut; ++k) acc[k] = 0.f;
+    for (int t = 0; t < taps; ++t) {
+        int any = 0;
+        for (int i = threadIdx.x; i < kRows * cin; i += kThreads) {
+            int r = i / cin, ci = i % cin;
+            int64_t row = r0 + r;
+            int32_t src = row < m ? nbr[(int64_t)t * m + row] : -1;
+            any |= src >= 0;
+            A[i] = src >= 0 ? in[(int64_t)src * ld_in + ci] : 0.f;
+        }
+        if (!__syncthreads_or(any)) continue;
+        const float *wt = w + (size_t)t * cin * cout;
+        for (int i = threadIdx.x; i < cin * cout; i += kThreads) W[i] = wt[i];
+        __syncthreads();
+#pragma unroll
+        for (int k = 0; k < kMaxOut; ++k) {
+            int o = threadIdx.x + k * kThreads;
+            if (o < nout) {
+                int r = o / cout, co = o % cout;
+                float s = acc[k];
+                for (int ci = 0; ci < cin; ++ci) s = fmaf(A[r * cin + ci], W[ci * cout + co], s);
+                acc[k] = s;
+            }
+        }
+        __syncthreads();
+    }
+#pragma unroll
+    for (int k = 0; k < kMaxOut; ++k) {
+        int o = threadIdx.x + k * kThreads;
+        if (o < nout) {
+            int r = o / cout, co = o % cout;
+            int64_t row = r0 + r;
+            if (row < m) {
+                float v = acc[k] + b[co];
+                out[row * ld_out + co] = relu ? fmaxf(v, 0.f) : v;
+            }
+        }
+    }
+}
+
+void conv_layer(sfb_ctx *ctx, const NetLayer &L, const float *in, int ld_in, const int32_t *nbr,
+                int64_t m, int relu, float *out, int ld_out) {
+    if (m == 0) return;
+    if (ctx->net_mode == SFB_NET_TC_TF32X3 && L.w_tc) {
+        conv_layer_tc(ctx, L, in, ld_in, nbr, m, relu, out, ld_out);
+        return;
+    }
+    SFB_REQUIRE(kRows * L.cout <= kMaxOut * kThreads, "conv: cout > 128 unsupported");
+    size_t smem = sizeof(float) * ((size_t)kRows * L.cin + (size_t)L.cin * L.cout);
+    SFB_REQUIRE(smem <= 200 * 1024, "conv: channels too wide for one CTA");
+    static bool attr = false;
+    if (!attr) {
+        SFB_CUDA(cudaFuncSetAttribute(k_conv_simt, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      200 * 1024));
+        attr = true;
+    }
+    k_conv_simt<<<grid_for(m, kRows), kThreads, smem, ctx->stream>>>(
+        in, ld_in, nbr, m, L.taps, L.cin, L.cout, L.w, L.b, relu, out, ld_out);
+    SFB_CHECK_LAUNCH();
+}
+
+// transposed conv: out[r] = b + in[parent[r]] @ W[tap[r]]  (orphans: bias only)
+__global__ void k_tconv(const float *__restrict__ in, int ld_in, const int32_t *__restrict__ parent,
+                        const int32_t *__restrict__ tap, int64_t m, int cin, int cout,
+                        const float *__restrict__ w, const float *__restrict__ b, int relu,
+                        float *__restrict__ out, int ld_out) {
+    int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (idx >= m * cout) return;
+    int64_t r = idx / cout;
+    int co = (int)(idx % cout);
+    int32_t p = parent[r];
+    float s = 0.f;
+    if (p >= 0) {
+        const float *x = in + (int64_t)p * ld_in;
+        const float *wt = w + (size_t)tap[r] * cin * cout + co;
+        for (int ci = 0; ci < cin; ++ci) s = fmaf(x[ci], wt[(size_t)ci * cout], s);
+    }
+    float v = s + b[co];
+    out[r * ld_out + co] = relu ? fmaxf(v, 0.f) : v;
+}
+
+void tconv_layer(sfb_ctx *ctx, const NetLayer &L, const float *in, int ld_in,
+                 const int32_t *parent, const int32_t *tap, int64_t m, int relu, float *out,
+                 int ld_out) {
+    if (m == 0) return;
+    k_tconv<<<grid_for(m * L.cout, 256), 256, 0, ctx->stream>>>(in, ld_in, parent, tap, m, L.cin,
+                                                                 L.cout, L.w, L.b, relu, out, ld_out);
+    SFB_CHECK_LAUNCH();
+}
+
+// child tap from coordinates (child stride cs, parent stride 2cs)
+__global__ void k_child_tap(const int32_t *__restrict__ coords, int64_t m, int cs,
+                            int32_t *__restrict__ tap) {
+    int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (r >= m) return;
+    int64_t ps = 2 * (int64_t)cs;
+    int64_t d[3];
+    for (int a = 0; a < 3; ++a) {
+        int64_t c = coords[3 * r + a];
+        d[a] = (c - floor_div(c, ps) * ps) / cs;
+    }
+    tap[r] = (int32_t)(d[2] * 4 + d[1] * 2 + d[0]);
+}
+
+// ------------------------------------------------------------ MLP head
+constexpr int kHeadRows = 32;
+
+__global__ void k_head_mlp(const float *__restrict__ f, int ld, int64_t m, int cin, int hid,
+                           const float *__restrict__ w1, const float *__restrict__ b1,
+                           const float *__restrict__ w2, const float *__restrict__ b2,
+                           float *__restrict__ raw) {
+    extern __shared__ float sm[];
+    float *F = sm;                         // [rows][cin]
+    float *H = F + kHeadRows * cin;        // [rows][hid]
+    float *W1 = H + kHeadRows * hid;       // [cin][hid]
+    float *W2 = W1 + cin * hid;            // [hid][14]
+    int64_t r0 = (int64_t)blockIdx.x * kHeadRows;
+    for (int i = threadIdx.x; i < cin * hid; i += blockDim.x) W1[i] = w1[i];
+    for (int i = threadIdx.x; i < hid * 14; i += blockDim.x) W2[i] = w2[i];
+    for (int i = threadIdx.x; i < kHeadRows * cin; i += blockDim.x) {
+        int64_t row = r0 + i / cin;
+        F[i] = row < m ? f[row * ld + i % cin] : 0.f;
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < kHeadRows * hid; i += blockDim.x) {
+        int r = i / hid, j = i % hid;
+        float s = 0.f;
+        for (int c = 0; c < cin; ++c) s = fmaf(F[r * cin + c], W1[c * hid + j], s);
+        H[i] = fmaxf(s + b1[j], 0.f);
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < kHeadRows * 14; i += blockDim.x) {
+        int r = i / 14, k = i % 14;
+        int64_t row = r0 + r;
+        if (row >= m) continue;
+        float s = 0.f;
+        for (int c = 0; c < hid; ++c) s = fmaf(H[r * hid + c], W2[c * 14 + k], s);
+        raw[row * 14 + k] = s + b2[k];
+    }
+}
+
+// ------------------------------------------------------------ activations
+__device__ __forceinline__ double logaddexp0(double x) {
+    // numpy npy_logaddexp(0, x): larger + log1p(exp(-|difference|))
+    double tmp = 0.0 - x;
+    if (tmp > 0) return 0.0 + log1p(exp(-tmp));
+    if (tmp <= 0) return x + log1p(exp(tmp));
+    return tmp;  // NaN
+}
+
+__device__ __forceinline__ void activate_row(const float *r, double scale, double *delta,
+                                             double *sigma, double *q, double *opac,
+                                             double *normal) {
+    double x[14];
+#pragma unroll
+    for (int k = 0; k < 14; ++k) x[k] = (double)r[k];
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+        delta[a] = tanh(x[a]) * scale;
+        sigma[a] = fmax(logaddexp0(x[3 + a]), 1e-12) * scale;
+    }
+    double qq[4] = {x[6] + 1.0, x[7], x[8], x[9]};
+    double qn = sqrt(qq[0] * qq[0] + qq[1] * qq[1] + qq[2] * qq[2] + qq[3] * qq[3]);
+    if (qn < 1e-12) {
+        q[0] = 1.0;
+        q[1] = q[2] = q[3] = 0.0;
+    } else {
+        double d = fmax(qn, 1e-300);
+        for (int a = 0; a < 4; ++a) q[a] = qq[a] / d;
+    }
+    double o = x[10];
+    if (o >= 0) *opac = 1.0 / (1.0 + exp(-o));
+    else {
+        double e = exp(o);
+        *opac = e / (1.0 + e);
+    }
+    double nn = sqrt(x[11] * x[11] + x[12] * x[12] + x[13] * x[13]);
+    if (nn < 1e-8) {
+        normal[0] = normal[1] = 0.0;
+        normal[2] = 1.0;
+    } else {
+        double d = fmax(nn, 1e-300);
+        for (int a = 0; a < 3; ++a) normal[a] = x[11 + a] / d;
+    }
+}
+
+__global__ void k_activate(const float *__restrict__ raw, int64_t m, double scale, double *delta,
+                           double *sigma, double *quat, double *opac, double *normal) {
+    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= m) return;
+    activate_row(raw + 14 * i, scale, delta + 3 * i, sigma + 3 * i, quat + 4 * i, opac + i,
+                 normal + 3 * i);
+}
+
+void activate_run(sfb_ctx *ctx, const float *raw, int64_t m, double scale, double *delta,
+                  double *sigma, double *quat, double *opac, double *normal) {
+    SFB_REQUIRE(scale > 0, "voxel_scale must be positive");
+    if (m == 0) return;
+    k_activate<<<grid_for(m, 128), 128, 0, ctx->stream>>>(raw, m, scale, delta, sigma, quat, opac,
+                                                          normal);
+    SFB_CHECK_LAUNCH();
+}
+
+// Per-voxel Gaussian: centre = (coord + 0.5 + residual) * scale + delta
+// (voxelgrid.py:119-122 + estimators.py:223), then the activated fields.
+__global__ void k_voxel_splats(const float *__restrict__ raw, const int32_t *__restrict__ coords,
+                               const double *__restrict__ feats9, int64_t m, double scale,
+                               double *centers, double *sigma, double *quat, double *opac,
+                               double *normal) {
+    int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (v >= m) return;
+    double delta[3];
+    activate_row(raw + 14 * v, scale, delta, sigma + 3 * v, quat + 4 * v, opac + v, normal + 3 * v);
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+        double rec = __dmul_rn(__dadd_rn(__dadd_rn((double)coords[3 * v + a], 0.5), feats9[9 * v + 6 + a]),
+                               scale);
+        centers[3 * v + a] = __dadd_rn(rec, delta[a]);
+    }
+}
+
+void head_to_voxel_splats(sfb_ctx *ctx, const float *raw, const int32_t *coords,
+                          const double *feats9, int64_t m0, double scale, double *centers,
+                          double *sigma, double *quat, double *opac, double *normal) {
+    k_voxel_splats<<<grid_for(m0, 128), 128, 0, ctx->stream>>>(raw, coords, feats9, m0, scale,
+                                                               centers, sigma, quat, opac, normal);
+    SFB_CHECK_LAUNCH();
+}
+
+// ------------------------------------------------------------ UNet
+__global__ void k_feats_to_f32(const double *__restrict__ f, int64_t n, float *__restrict__ o) {
+    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i < n) o[i] = (float)f[i];
+}
+
+void unet_run(sfb_ctx *ctx, const int32_t *coords0, const double *feats9, int64_t m0, float *raw) {
+    Net &net = ctx->net;
+    SFB_REQUIRE(net.loaded, "network weights are not loaded");
+    const int L = net.levels;
+    const auto &enc = net.enc;
+    const auto &dec = net.dec;
+    SFB_REQUIRE(m0 > 0, "empty voxel grid");
+    cudaStream_t st = ctx->stream;
+    std::vector<int64_t> M(L + 1);
+    std::vector<const int32_t *> coords(L + 1);
+    std::vector<int32_t *> nbr(L + 1), c2p(L);
+    std::vector<float *> cat(L), pin(L + 1);
+    std::vector<int> width(L);
+    M[0] = m0;
+    coords[0] = coords0;
+    for (int l = 0; l < L; ++l) width[l] = dec[L - 1 - l] + enc[l + 1];
+    pin[0] = ctx->arena.alloc<float>((size_t)m0 * enc[0]);
+    k_feats_to_f32<<<grid_for(m0 * enc[0], 256), 256, 0, st>>>(feats9, m0 * enc[0], pin[0]);
+    SFB_CHECK_LAUNCH();
+    int layer = 0;
+    for (int l = 0; l <= L; ++l) {
+        int stride = 1 << l;
+        HashTable h = hash_build(ctx, coords[l], M[l]);
+        int kern = net.layers[layer].kernel, taps = kern * kern * kern;
+        nbr[l] = ctx->arena.alloc<int32_t>((size_t)taps * M[l]);
+        kernel_map_build(ctx, h, coords[l], M[l], stride, kern, nbr[l]);
+        if (l == L) break;
+        cat[l] = ctx->arena.alloc<float>((size_t)M[l] * width[l]);
+        int up = dec[L - 1 - l];
+        conv_layer(ctx, net.layers[layer++], pin[l], enc[l], nbr[l], M[l], 1, cat[l] + up, width[l]);
+        // pool the skip features into the next level's input
+        int32_t *pc = ctx->arena.alloc<int32_t>((size_t)M[l] * 3);
+        pin[l + 1] = ctx->arena.alloc<float>((size_t)M[l] * enc[l + 1]);
+        c2p[l] = ctx->arena.alloc<int32_t>(M[l]);
+        M[l + 1] = pool_build(ctx, coords[l], M[l], stride, cat[l] + up, enc[l + 1], width[l], pc,
+                              pin[l + 1], enc[l + 1], c2p[l]);
+        coords[l + 1] = pc;
+    }
+    // bottleneck
+    float *bott = ctx->arena.alloc<float>((size_t)M[L] * enc[L + 1]);
+    conv_layer(ctx, net.layers[layer++], pin[L], enc[L], nbr[L], M[L], 1, bott, enc[L + 1]);
+    const float *coarse = bott;
+    int ld_coarse = enc[L + 1];
+    for (int l = L - 1; l >= 0; --l) {
+        int32_t *tap = ctx->arena.alloc<int32_t>(M[l]);
+        k_child_tap<<<grid_for(M[l], 256), 256, 0, st>>>(coords[l], M[l], 1 << l, tap);
+        SFB_CHECK_LAUNCH();
+        tconv_layer(ctx, net.layers[layer++], coarse, ld_coarse, c2p[l], tap, M[l], 1, cat[l], width[l]);
+        coarse = cat[l];
+        ld_coarse = width[l];
+    }
+    const NetLayer &h1 = net.layers[layer], &h2 = net.layers[layer + 1];
+    size_t smem = sizeof(float) * ((size_t)kHeadRows * (h1.cin + h1.cout) + (size_t)h1.cin * h1.cout +
+                                   (size_t)h1.cout * 14);
+    static bool attr = false;
+    if (!attr) {
+        SFB_CUDA(cudaFuncSetAttribute(k_head_mlp, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      200 * 1024));
+        attr = true;
+    }
+    SFB_REQUIRE(smem <= 200 * 1024, "head MLP too wide");
+    k_head_mlp<<<grid_for(m0, kHeadRows), 128, smem, st>>>(cat[0], width[0], m0, h1.cin, h1.cout,
+                                                           h1.w, h1.b, h2.w, h2.b, raw);
+    SFB_CHECK_LAUNCH();
+    for (int l = 0; l <= L && l < 8; ++l) ctx->stats.voxels[l] = M[l];
+}
+
+}  // namespace sfb

@@ -1,0 +1,807 @@
+// Splatting pipeline on the device (compiled with -fmad=false).
+//
+// Reference: project_kernel / bin_tiles / forward_kernel
+// (_raster_kernels.py:20-201) and _prepare / _compose / render
+// (rasterizer.py:99-166). Contract kept bit-for-bit where the reference is
+// integer or IEEE-exact: projection, covariance and depth in float64 with the
+// numba expression order and no FMA contraction, blend order = stable sort of
+// (depth, input index), tile ranges floor((s -+ r)/tile) on the alpha-support
+// radius, per-pixel box/circle tests, "T < 1/255 is checked before each splat".
+//
+// B200 design:
+//   1. project per geometry row (per splat, or per voxel in the fused frame);
+//   2. compact kept points, stable LSD radix sort of float64 depth bits with
+//      the point index as payload -> rank order (ties by index);
+//   3. split the rank order into RUNS of consecutive points with identical
+//      geometry (a voxel's points share centre/cov/opacity, so P2ENet splats
+//      collapse ~33x); one alpha per (run, pixel), colours stay per point;
+//   4. bin runs into a three-level tile pyramid — 16 px tiles, 8x8-tile super
+//      tiles, one whole-image list — choosing per run the finest level with
+//      <= 16 entries, so the giant random-init splats never expand into
+//      billions of (tile, splat) keys;
+//   5. one CTA per tile walks the three rank-sorted lists as a merge (rank
+//      windows + a shared-memory bitmap), tests exact tile coverage, blends
+//      RGB + normal (+ depth) + T in float64 registers in ONE pass, and stops
+//      when every pixel of the tile has T < 1/255 — identical to the
+//      reference, whose per-pixel skip makes all later splats no-ops.
+#include <cub/cub.cuh>
+
+#include "common.cuh"
+
+namespace sfb {
+
+constexpr double kCutoff = 1.0 / 255.0;
+constexpr int kFineMax = 16;   // tiles per run at the fine level
+constexpr int kSuper = 8;      // tiles per super-tile edge
+constexpr int kSuperMax = 16;  // super tiles per run at the middle level
+constexpr int kWin = 2048;     // rank window of the merge
+constexpr int kCT = 256;       // compositor threads per CTA
+
+struct Cam {
+    double r[9], t[3], fx, fy, cx, cy;
+    int64_t w, h;
+};
+
+static Cam to_cam(const sfb_camera &c) {
+    Cam k;
+    for (int i = 0; i < 9; ++i) k.r[i] = c.rot[i];
+    for (int i = 0; i < 3; ++i) k.t[i] = c.trans[i];
+    k.fx = c.fx;
+    k.fy = c.fy;
+    k.cx = c.cx;
+    k.cy = c.cy;
+    k.w = c.width;
+    k.h = c.height;
+    return k;
+}
+
+// ------------------------------------------------------------ 1. projection
+__global__ void k_project(const double *__restrict__ centers, const double *__restrict__ quats,
+                          const double *__restrict__ scales, int64_t n, Cam C, double z_near,
+                          double dil, double *__restrict__ sx, double *__restrict__ sy,
+                          double *__restrict__ depth, double *__restrict__ ca,
+                          double *__restrict__ cb, double *__restrict__ cc,
+                          double *__restrict__ rad3, uint8_t *__restrict__ keep) {
+    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const double *p = centers + 3 * i;
+    const double *R = C.r;
+    double px = R[0] * p[0] + R[1] * p[1] + R[2] * p[2] + C.t[0];
+    double py = R[3] * p[0] + R[4] * p[1] + R[5] * p[2] + C.t[1];
+    double pz = R[6] * p[0] + R[7] * p[1] + R[8] * p[2] + C.t[2];
+    uint8_t ok = 0;
+    double o_sx = 0, o_sy = 0, o_d = 0, o_a = 0, o_b = 0, o_c = 0, o_r = 0;
+    if (pz > z_near) {
+        const double *q = quats + 4 * i;
+        double w = q[0], x = q[1], y = q[2], z = q[3];
+        double qn = sqrt(w * w + x * x + y * y + z * z);
+        w /= qn;
+        x /= qn;
+        y /= qn;
+        z /= qn;
+        double r[9] = {1.0 - 2.0 * (y * y + z * z), 2.0 * (x * y - w * z), 2.0 * (x * z + w * y),
+                       2.0 * (x * y + w * z), 1.0 - 2.0 * (x * x + z * z), 2.0 * (y * z - w * x),
+                       2.0 * (x * z - w * y), 2.0 * (y * z + w * x), 1.0 - 2.0 * (x * x + y * y)};
+        double u[9];
+#pragma unroll
+        for (int a = 0; a < 3; ++a)
+#pragma unroll
+            for (int b = 0; b < 3; ++b)
+                u[3 * a + b] = r[3 * a] * R[3 * b] + r[3 * a + 1] * R[3 * b + 1] + r[3 * a + 2] * R[3 * b + 2];
+        const double *s = scales + 3 * i;
+        double d0 = s[0] * s[0], d1 = s[1] * s[1], d2 = s[2] * s[2];
+#define SIG(j, k) (d0 * u[j] * u[k] + d1 * u[3 + j] * u[3 + k] + d2 * u[6 + j] * u[6 + k])
+        double s00 = SIG(0, 0), s01 = SIG(0, 1), s02 = SIG(0, 2);
+        double s11 = SIG(1, 1), s12 = SIG(1, 2), s22 = SIG(2, 2);
+#undef SIG
+        double jx = C.fx / pz, jy = C.fy / pz;
+        double jxz = -C.fx * px / (pz * pz), jyz = -C.fy * py / (pz * pz);
+        double a = jx * jx * s00 + 2.0 * jx * jxz * s02 + jxz * jxz * s22 + dil;
+        double b = jx * jy * s01 + jx * jyz * s02 + jxz * jy * s12 + jxz * jyz * s22;
+        double c = jy * jy * s11 + 2.0 * jy * jyz * s12 + jyz * jyz * s22 + dil;
+        double mid = 0.5 * (a + c);
+        double gap = sqrt(fmax(0.25 * (a - c) * (a - c) + b * b, 0.0));
+        double rr = 3.0 * sqrt(fmax(mid + gap, 0.0));
+        double csx = jx * px + C.cx, csy = jy * py + C.cy;
+        if (!(csx + rr < 0.0 || csx - rr > (double)C.w - 1.0 || csy + rr < 0.0 ||
+              csy - rr > (double)C.h - 1.0)) {
+            ok = 1;
+            o_sx = csx;
+            o_sy = csy;
+            o_d = pz;
+            o_a = a;
+            o_b = b;
+            o_c = c;
+            o_r = rr;
+        }
+    }
+    sx[i] = o_sx;
+    sy[i] = o_sy;
+    depth[i] = o_d;
+    ca[i] = o_a;
+    cb[i] = o_b;
+    cc[i] = o_c;
+    rad3[i] = o_r;
+    keep[i] = ok;
+}
+
+void project_run(sfb_ctx *ctx, const double *centers, const double *quats, const double *scales,
+                 int64_t n, const sfb_camera &cam, double z_near, double dilation, double *sx,
+                 double *sy, double *depth, double *ca, double *cb, double *cc, double *radius,
+                 uint8_t *keep) {
+    if (n == 0) return;
+    k_project<<<grid_for(n, 128), 128, 0, ctx->stream>>>(centers, quats, scales, n, to_cam(cam),
+                                                         z_near, dilation, sx, sy, depth, ca, cb,
+                                                         cc, radius, keep);
+    SFB_CHECK_LAUNCH();
+}
+
+// ------------------------------------------------------------ 2. depth order
+struct Proj {
+    double *sx, *sy, *depth, *a, *b, *c, *r3;
+    uint8_t *keep;
+};
+
+static Proj project_inputs(sfb_ctx *ctx, const RenderInputs &in, const sfb_camera &cam) {
+    Proj P;
+    int64_t n = in.n_geom;
+    double *blk = ctx->arena.alloc<double>(7 * (size_t)(n > 0 ? n : 1));
+    P.sx = blk;
+    P.sy = blk + n;
+    P.depth = blk + 2 * n;
+    P.a = blk + 3 * n;
+    P.b = blk + 4 * n;
+    P.c = blk + 5 * n;
+    P.r3 = blk + 6 * n;
+    P.keep = ctx->arena.alloc<uint8_t>(n > 0 ? n : 1);
+    project_run(ctx, in.centers, in.quats, in.scales, n, cam, 0.01, 0.3, P.sx, P.sy, P.depth, P.a,
+                P.b, P.c, P.r3, P.keep);
+    return P;
+}
+
+__global__ void k_point_keep(const uint8_t *__restrict__ keep, const int32_t *__restrict__ p2g,
+                             int64_t n, uint8_t *__restrict__ flag) {
+    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i < n) flag[i] = keep[p2g ? p2g[i] : i];
+}
+
+__global__ void k_depth_keys(const uint32_t *__restrict__ kept, const int32_t *__restrict__ num,
+                             const int32_t *__restrict__ p2g, const double *__restrict__ depth,
+                             unsigned long long *__restrict__ keys) {
+    int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (j >= *num) return;
+    uint32_t i = kept[j];
+    keys[j] = (unsigned long long)__double_as_longlong(depth[p2g ? p2g[i] : i]);
+}
+
+// returns K (host) and the rank -> point array `source`
+static int64_t depth_order(sfb_ctx *ctx, const RenderInputs &in, const Proj &P, uint32_t **source) {
+    cudaStream_t st = ctx->stream;
+    int64_t n = in.n_points;
+    if (n == 0) {
+        *source = nullptr;
+        return 0;
+    }
+    uint8_t *flag = ctx->arena.alloc<uint8_t>(n);
+    k_point_keep<<<grid_for(n, 256), 256, 0, st>>>(P.keep, in.point_to_geom, n, flag);
+    uint32_t *kept = ctx->arena.alloc<uint32_t>(n);
+    int32_t *num = ctx->arena.alloc<int32_t>(1);
+    cub::CountingInputIterator<uint32_t> iota(0);
+    size_t tb = 0;
+    cub::DeviceSelect::Flagged(nullptr, tb, iota, flag, kept, num, (int)n, st);
+    void *tmp = ctx->arena.alloc_bytes(tb);
+    SFB_CUDA(cub::DeviceSelect::Flagged(tmp, tb, iota, flag, kept, num, (int)n, st));
+    ctx->read_back(num, sizeof(int32_t));
+    int64_t K = *reinterpret_cast<int32_t *>(ctx->pinned);
+    if (K == 0) {
+        *source = nullptr;
+        return 0;
+    }
+    auto *keys = ctx->arena.alloc<unsigned long long>(K), *keys2 = ctx->arena.alloc<unsigned long long>(K);
+    uint32_t *src = ctx->arena.alloc<uint32_t>(K);
+    k_depth_keys<<<grid_for(K, 256), 256, 0, st>>>(kept, num, in.point_to_geom, P.depth, keys);
+    SFB_CHECK_LAUNCH();
+    tb = 0;
+    cub::DeviceRadixSort::SortPairs(nullptr, tb, keys, keys2, kept, src, (int)K, 0, 64, st);
+    tmp = ctx->arena.alloc_bytes(tb);
+    SFB_CUDA(cub::DeviceRadixSort::SortPairs(tmp, tb, keys, keys2, kept, src, (int)K, 0, 64, st));
+    *source = src;
+    return K;
+}
+
+// ------------------------------------------------------------ 3. runs
+// alpha-support radius of rasterizer.py:115-123 (gap uses square-then-scale)
+__device__ __forceinline__ double support_radius(double a, double b, double c, double op) {
+    double mid = 0.5 * (a + c);
+    double amc = a - c;
+    double gap = sqrt(fmax(0.25 * (amc * amc) + b * b, 0.0));
+    double lam = fmax(mid + gap, 0.0);
+    double sup = 2.0 * log(fmax(255.0 * op, 1e-300));
+    return sqrt(fmax(sup, 0.0) * lam) + 1e-9;
+}
+
+struct TileRect {
+    int32_t x0, x1, y0, y1;
+};
+
+__device__ __forceinline__ TileRect tile_rect(double sx, double sy, double r, double ft,
+                                              int64_t ntx, int64_t nty) {
+    // int(np.floor(v / tile)) clamped (_raster_kernels.py:123-130); clamp in
+    // double first so non-finite extents cannot overflow the integer cast
+    double lim = 4.0e9;
+    double fx0 = fmin(fmax(floor((sx - r) / ft), -1.0), lim);
+    double fx1 = fmin(fmax(floor((sx + r) / ft), -lim), (double)ntx);
+    double fy0 = fmin(fmax(floor((sy - r) / ft), -1.0), lim);
+    double fy1 = fmin(fmax(floor((sy + r) / ft), -lim), (double)nty);
+    TileRect t;
+    t.x0 = (int32_t)fmax(fx0, 0.0);
+    t.x1 = (int32_t)fmin(fx1, (double)(ntx - 1));
+    t.y0 = (int32_t)fmax(fy0, 0.0);
+    t.y1 = (int32_t)fmin(fy1, (double)(nty - 1));
+    return t;
+}
+
+__global__ void k_run_heads(const uint32_t *__restrict__ src, int64_t K, const int32_t *__restrict__ p2g,
+                            Proj P, const double *__restrict__ opac, int32_t *__restrict__ head) {
+    int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (j >= K) return;
+    int h = 1;
+    if (j > 0) {
+        uint32_t i = src[j], k = src[j - 1];
+        if (p2g) {
+            h = p2g[i] != p2g[k];
+        } else {
+            h = !(P.sx[i] == P.sx[k] && P.sy[i] == P.sy[k] && P.depth[i] == P.depth[k] &&
+                  P.a[i] == P.a[k] && P.b[i] == P.b[k] && P.c[i] == P.c[k] && opac[i] == opac[k]);
+        }
+    }
+    head[j] = h;
+}
+
+struct Runs {
+    int64_t R;
+    double *mx, *my, *rad, *ia, *ib, *ic, *op;
+    int32_t *start, *count;
+    int4 *rect;
+    uint8_t *level;  // 0 fine, 1 super, 2 global, 3 dead
+    int32_t *nf, *ns, *ng;  // per-run entry counts
+};
+
+__global__ void k_run_build(const uint32_t *__restrict__ src, int64_t K,
+                            const int32_t *__restrict__ incl, const int32_t *__restrict__ p2g, Proj P,
+                            const double *__restrict__ opac, double ft, int64_t ntx, int64_t nty,
+                            int64_t nsx, int64_t nsy, double alpha_max, Runs R) {
+    int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (j >= K) return;
+    int32_t r = incl[j] - 1;
+    bool head = j == 0 || incl[j - 1] != incl[j];
+    if (!head) return;
+    // run length: distance to the next head
+    int64_t e = j + 1;
+    while (e < K && incl[e] == incl[j]) ++e;
+    R.start[r] = (int32_t)j;
+    R.count[r] = (int32_t)(e - j);
+    uint32_t i = src[j];
+    int32_t g = p2g ? p2g[i] : (int32_t)i;
+    double a = P.a[g], b = P.b[g], c = P.c[g];
+    double op = opac[g];
+    double det = a * c - b * b;
+    R.mx[r] = P.sx[g];
+    R.my[r] = P.sy[g];
+    R.ia[r] = c / det;
+    R.ib[r] = -b / det;
+    R.ic[r] = a / det;
+    R.op[r] = op;
+    double rad = support_radius(a, b, c, op);
+    R.rad[r] = rad;
+    TileRect t = tile_rect(P.sx[g], P.sy[g], rad, ft, ntx, nty);
+    R.rect[r] = make_int4(t.x0, t.x1, t.y0, t.y1);
+    int lvl = 3;
+    int nf = 0, ns = 0, ng = 0;
+    bool live = !(op < kCutoff) && !(alpha_max < kCutoff) && t.x0 <= t.x1 && t.y0 <= t.y1;
+    if (live) {
+        int64_t cnt = (int64_t)(t.x1 - t.x0 + 1) * (t.y1 - t.y0 + 1);
+        if (cnt <= kFineMax) {
+            lvl = 0;
+            nf = (int)cnt;
+        } else {
+            int64_t scnt = (int64_t)(t.x1 / kSuper - t.x0 / kSuper + 1) * (t.y1 / kSuper - t.y0 / kSuper + 1);
+            if (scnt <= kSuperMax) {
+                lvl = 1;
+                ns = (int)scnt;
+            } else {
+                lvl = 2;
+                ng = 1;
+            }
+        }
+    }
+    (void)nsx;
+    (void)nsy;
+    R.level[r] = (uint8_t)lvl;
+    R.nf[r] = nf;
+    R.ns[r] = ns;
+    R.ng[r] = ng;
+}
+
+__global__ void k_emit(Runs R, const int32_t *__restrict__ fpos, const int32_t *__restrict__ spos,
+                       const int32_t *__restrict__ gpos, int64_t ntx, int64_t nsx,
+                       uint32_t *__restrict__ fkey, uint32_t *__restrict__ fval,
+                       uint32_t *__restrict__ skey, uint32_t *__restrict__ sval,
+                       uint32_t *__restrict__ glist) {
+    int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (r >= R.R) return;
+    int lvl = R.level[r];
+    int4 t = R.rect[r];
+    if (lvl == 0) {
+        int32_t p = fpos[r];
+        for (int y = t.z; y <= t.w; ++y)
+            for (int x = t.x; x <= t.y; ++x) {
+                fkey[p] = (uint32_t)(y * ntx + x);
+                fval[p++] = (uint32_t)r;
+            }
+    } else if (lvl == 1) {
+        int32_t p = spos[r];
+        for (int y = t.z / kSuper; y <= t.w / kSuper; ++y)
+            for (int x = t.x / kSuper; x <= t.y / kSuper; ++x) {
+                skey[p] = (uint32_t)(y * nsx + x);
+                sval[p++] = (uint32_t)r;
+            }
+    } else if (lvl == 2) {
+        glist[gpos[r]] = (uint32_t)r;
+    }
+}
+
+__global__ void k_histogram(const uint32_t *__restrict__ keys, int64_t n, int32_t *__restrict__ cnt) {
+    int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (j < n) atomicAdd(&cnt[keys[j]], 1);
+}
+
+// ------------------------------------------------------------ 5. compositor
+struct CompParams {
+    int64_t W, H, ntx, nty, nsx;
+    int tile;
+    int terminate;
+    double alpha_max;
+    int plane_mask;
+    double bg[3];
+    // lists
+    const int32_t *f_off;
+    const uint32_t *f_ids;
+    const int32_t *s_off;
+    const uint32_t *s_ids;
+    const uint32_t *g_ids;
+    int64_t G;
+    Runs R;
+    // points
+    const uint32_t *src;
+    const int32_t *p2g;
+    const double *colors, *normals, *gdepth;
+    // outputs
+    float *rgb, *normal, *depth, *trans;
+};
+
+template <int NPIX>
+__global__ void __launch_bounds__(kCT) k_composite(CompParams P) {
+    __shared__ uint32_t bitmap[kWin / 32];
+    __shared__ uint32_t list[kWin];
+    __shared__ int s_nlist;
+    __shared__ double r_mx[kCT], r_my[kCT], r_rad[kCT], r_ia[kCT], r_ib[kCT], r_ic[kCT], r_op[kCT];
+    __shared__ int32_t r_start[kCT], r_count[kCT];
+    __shared__ uint32_t s_cursor_add[3];
+
+    const int64_t t = blockIdx.x;
+    const int64_t tx = t % P.ntx, ty = t / P.ntx;
+    const int64_t st = (ty / kSuper) * P.nsx + tx / kSuper;
+    const int TS = P.tile;
+    const int64_t x_lo = tx * TS, y_lo = ty * TS;
+    const int64_t x_end = min(x_lo + TS, P.W), y_end = min(y_lo + TS, P.H);
+    const bool want_rgb = P.plane_mask & SFB_PLANE_RGB, want_n = P.plane_mask & SFB_PLANE_NORMAL;
+    const bool want_d = P.plane_mask & SFB_PLANE_DEPTH;
+
+    int64_t pxs[NPIX], pys[NPIX];
+    bool valid[NPIX];
+    double T[NPIX], c0[NPIX], c1[NPIX], c2[NPIX], n0[NPIX], n1[NPIX], n2[NPIX], dd[NPIX];
+#pragma unroll
+    for (int k = 0; k < NPIX; ++k) {
+        int p = threadIdx.x + k * kCT;
+        pxs[k] = x_lo + p % TS;
+        pys[k] = y_lo + p / TS;
+        valid[k] = p < TS * TS && pxs[k] < x_end && pys[k] < y_end;
+        T[k] = 1.0;
+        c0[k] = c1[k] = c2[k] = n0[k] = n1[k] = n2[k] = dd[k] = 0.0;
+    }
+
+    int64_t fc = P.f_off[t], fe = P.f_off[t + 1];
+    int64_t sc = P.s_off[st], se = P.s_off[st + 1];
+    int64_t gc = 0, ge = P.G;
+    bool done = false;
+    while (!done) {
+        uint32_t w0 = 0xffffffffu;
+        if (fc < fe) w0 = min(w0, P.f_ids[fc]);
+        if (sc < se) w0 = min(w0, P.s_ids[sc]);
+        if (gc < ge) w0 = min(w0, P.g_ids[gc]);
+        if (w0 == 0xffffffffu) break;
+        const uint32_t w1 = w0 + kWin;
+        for (int i = threadIdx.x; i < kWin / 32; i += kCT) bitmap[i] = 0;
+        if (threadIdx.x < 3) s_cursor_add[threadIdx.x] = 0;
+        __syncthreads();
+        // scan the three streams for ids inside [w0, w1)
+#pragma unroll
+        for (int s = 0; s < 3; ++s) {
+            const uint32_t *ids = s == 0 ? P.f_ids : (s == 1 ? P.s_ids : P.g_ids);
+            int64_t cur = s == 0 ? fc : (s == 1 ? sc : gc);
+            int64_t end = s == 0 ? fe : (s == 1 ? se : ge);
+            int cnt = 0;
+            for (int k = 0; k < kWin / kCT; ++k) {
+                int64_t idx = cur + k * kCT + threadIdx.x;
+                if (cur + k * kCT >= end) break;
+                if (idx < end) {
+                    uint32_t id = ids[idx];
+                    if (id < w1) {
+                        ++cnt;
+                        bool cover = true;
+                        if (s != 0) {
+                            int4 rc = P.R.rect[id];
+                            cover = tx >= rc.x && tx <= rc.y && ty >= rc.z && ty <= rc.w;
+                        }
+                        if (cover) atomicOr(&bitmap[(id - w0) >> 5], 1u << ((id - w0) & 31));
+                    }
+                }
+            }
+            if (cnt) atomicAdd(&s_cursor_add[s], (uint32_t)cnt);
+        }
+        __syncthreads();
+        fc += s_cursor_add[0];
+        sc += s_cursor_add[1];
+        gc += s_cursor_add[2];
+        // ordered compaction of the bitmap (warp 0; 64 words -> 2 per lane)
+        if (threadIdx.x < 32) {
+            int lane = threadIdx.x;
+            uint32_t wa = bitmap[2 * lane], wb = bitmap[2 * lane + 1];
+            int ca = __popc(wa), cb = __popc(wb);
+            int incl = ca + cb;
+            for (int o = 1; o < 32; o <<= 1) {
+                int v = __shfl_up_sync(0xffffffffu, incl, o);
+                if (lane >= o) incl += v;
+            }
+            int pos = incl - ca - cb;
+            while (wa) {
+                int b = __ffs(wa) - 1;
+                wa &= wa - 1;
+                list[pos++] = w0 + 64 * lane + b;
+            }
+            while (wb) {
+                int b = __ffs(wb) - 1;
+                wb &= wb - 1;
+                list[pos++] = w0 + 64 * lane + 32 + b;
+            }
+            if (lane == 31) s_nlist = incl;
+        }
+        __syncthreads();
+        const int nlist = s_nlist;
+        for (int base = 0; base < nlist && !done; base += kCT) {
+            int nb = min(kCT, nlist - base);
+            if (threadIdx.x < nb) {
+                uint32_t r = list[base + threadIdx.x];
+                r_mx[threadIdx.x] = P.R.mx[r];
+                r_my[threadIdx.x] = P.R.my[r];
+                r_rad[threadIdx.x] = P.R.rad[r];
+                r_ia[threadIdx.x] = P.R.ia[r];
+                r_ib[threadIdx.x] = P.R.ib[r];
+                r_ic[threadIdx.x] = P.R.ic[r];
+                r_op[threadIdx.x] = P.R.op[r];
+                r_start[threadIdx.x] = P.R.start[r];
+                r_count[threadIdx.x] = P.R.count[r];
+            }
+            __syncthreads();
+            for (int e = 0; e < nb; ++e) {
+                const double mx = r_mx[e], my = r_my[e];
+                const double rad = r_rad[e] + 1.0, rr = rad * rad;
+                const double fx0 = fmax((double)x_lo, ceil(mx - rad));
+                const double fx1 = fmin((double)(x_end - 1), floor(mx + rad));
+                const double fy0 = fmax((double)y_lo, ceil(my - rad));
+                const double fy1 = fmin((double)(y_end - 1), floor(my + rad));
+#pragma unroll
+                for (int k = 0; k < NPIX; ++k) {
+                    if (!valid[k]) continue;
+                    const double px = (double)pxs[k], py = (double)pys[k];
+                    if (px < fx0 || px > fx1 || py < fy0 || py > fy1) continue;
+                    if (P.terminate && T[k] < kCutoff) continue;
+                    const double dx = px - mx, dy = py - my;
+                    if (dx * dx + dy * dy > rr) continue;
+                    const double q = r_ia[e] * dx * dx + 2.0 * r_ib[e] * dx * dy + r_ic[e] * dy * dy;
+                    double alpha = r_op[e] * exp(-0.5 * q);
+                    if (alpha > P.alpha_max) alpha = P.alpha_max;
+                    if (alpha < kCutoff) continue;
+                    const double om = 1.0 - alpha;
+                    const int32_t b0 = r_start[e], b1 = b0 + r_count[e];
+                    for (int32_t j = b0; j < b1; ++j) {
+                        if (P.terminate && T[k] < kCutoff) break;
+                        const uint32_t i = P.src[j];
+                        const double w = T[k] * alpha;
+                        if (want_rgb) {
+                            const double *cc = P.colors + 3 * (size_t)i;
+                            c0[k] = c0[k] + w * cc[0];
+                            c1[k] = c1[k] + w * cc[1];
+                            c2[k] = c2[k] + w * cc[2];
+                        }
+                        if (want_n || want_d) {
+                            const int64_t g = P.p2g ? P.p2g[i] : (int64_t)i;
+                            if (want_n) {
+                                const double *nn = P.normals + 3 * g;
+                                n0[k] = n0[k] + w * nn[0];
+                                n1[k] = n1[k] + w * nn[1];
+                                n2[k] = n2[k] + w * nn[2];
+                            }
+                            if (want_d) dd[k] = dd[k] + w * P.gdepth[g];
+                        }
+                        T[k] = T[k] * om;
+                    }
+                }
+            }
+            if (P.terminate) {
+                int mine = 1;
+#pragma unroll
+                for (int k = 0; k < NPIX; ++k)
+                    if (valid[k] && !(T[k] < kCutoff)) mine = 0;
+                done = __syncthreads_and(mine);
+            } else {
+                __syncthreads();
+            }
+        }
+    }
+    // planes (rasterizer.py:140-149; FrameBuffer clips T to [0,1])
+#pragma unroll
+    for (int k = 0; k < NPIX; ++k) {
+        if (!valid[k]) continue;
+        const int64_t pix = pys[k] * P.W + pxs[k];
+        if (P.rgb) {
+            P.rgb[3 * pix + 0] = (float)(c0[k] + T[k] * P.bg[0]);
+            P.rgb[3 * pix + 1] = (float)(c1[k] + T[k] * P.bg[1]);
+            P.rgb[3 * pix + 2] = (float)(c2[k] + T[k] * P.bg[2]);
+        }
+        if (P.normal) {
+            double nrm = sqrt(n0[k] * n0[k] + n1[k] * n1[k] + n2[k] * n2[k]);
+            bool z = !(nrm > 0.0);
+            P.normal[3 * pix + 0] = z ? 0.f : (float)(n0[k] / nrm);
+            P.normal[3 * pix + 1] = z ? 0.f : (float)(n1[k] / nrm);
+            P.normal[3 * pix + 2] = z ? 0.f : (float)(n2[k] / nrm);
+        }
+        if (P.depth) P.depth[pix] = (float)dd[k];
+        if (P.trans) P.trans[pix] = (float)fmin(fmax(T[k], 0.0), 1.0);
+    }
+}
+
+// ------------------------------------------------------------ driver
+void render_run(sfb_ctx *ctx, const RenderInputs &in, const sfb_camera &cam,
+                const sfb_render_options &opts, int plane_mask, const double *bg, float *rgb,
+                float *normal, float *depth, float *trans) {
+    SFB_REQUIRE(cam.width >= 1 && cam.height >= 1, "image must have positive dimensions");
+    SFB_REQUIRE(opts.tile_size >= 1 && opts.tile_size <= 32, "tile_size must be in [1, 32]");
+    cudaStream_t st = ctx->stream;
+    const int TS = opts.tile_size;
+    const int64_t ntx = (cam.width + TS - 1) / TS, nty = (cam.height + TS - 1) / TS;
+    const int64_t nsx = (ntx + kSuper - 1) / kSuper, nsy = (nty + kSuper - 1) / kSuper;
+    Proj P = project_inputs(ctx, in, cam);
+    uint32_t *src = nullptr;
+    int64_t K = depth_order(ctx, in, P, &src);
+    ctx->stats.kept = K;
+
+    Runs R{};
+    R.R = 0;
+    int32_t *f_off = ctx->arena.alloc<int32_t>(ntx * nty + 1);
+    int32_t *s_off = ctx->arena.alloc<int32_t>(nsx * nsy + 1);
+    uint32_t *fval2 = nullptr, *sval2 = nullptr, *glist = nullptr;
+    int64_t Ef = 0, Es = 0, G = 0;
+    SFB_CUDA(cudaMemsetAsync(f_off, 0, sizeof(int32_t) * (ntx * nty + 1), st));
+    SFB_CUDA(cudaMemsetAsync(s_off, 0, sizeof(int32_t) * (nsx * nsy + 1), st));
+    if (K > 0) {
+        int32_t *head = ctx->arena.alloc<int32_t>(K), *incl = ctx->arena.alloc<int32_t>(K);
+        k_run_heads<<<grid_for(K, 256), 256, 0, st>>>(src, K, in.point_to_geom, P, in.opac, head);
+        size_t tb = 0;
+        cub::DeviceScan::InclusiveSum(nullptr, tb, head, incl, (int)K, st);
+        void *tmp = ctx->arena.alloc_bytes(tb);
+        SFB_CUDA(cub::DeviceScan::InclusiveSum(tmp, tb, head, incl, (int)K, st));
+        ctx->read_back(incl + K - 1, sizeof(int32_t));
+        R.R = *reinterpret_cast<int32_t *>(ctx->pinned);
+        int64_t nr = R.R;
+        double *blk = ctx->arena.alloc<double>(7 * nr);
+        R.mx = blk;
+        R.my = blk + nr;
+        R.rad = blk + 2 * nr;
+        R.ia = blk + 3 * nr;
+        R.ib = blk + 4 * nr;
+        R.ic = blk + 5 * nr;
+        R.op = blk + 6 * nr;
+        R.start = ctx->arena.alloc<int32_t>(nr);
+        R.count = ctx->arena.alloc<int32_t>(nr);
+        R.rect = ctx->arena.alloc<int4>(nr);
+        R.level = ctx->arena.alloc<uint8_t>(nr);
+        int32_t *cnts = ctx->arena.alloc<int32_t>(3 * (nr + 1));
+        R.nf = cnts;
+        R.ns = cnts + (nr + 1);
+        R.ng = cnts + 2 * (nr + 1);
+        SFB_CUDA(cudaMemsetAsync(cnts, 0, sizeof(int32_t) * 3 * (nr + 1), st));
+        k_run_build<<<grid_for(K, 256), 256, 0, st>>>(src, K, incl, in.point_to_geom, P, in.opac,
+                                                      (double)TS, ntx, nty, nsx, nsy,
+                                                      opts.alpha_max, R);
+        SFB_CHECK_LAUNCH();
+        // exclusive positions of every level's entries (+1 slot carries the total)
+        int32_t *pos = ctx->arena.alloc<int32_t>(3 * (nr + 1));
+        tb = 0;
+        cub::DeviceScan::ExclusiveSum(nullptr, tb, R.nf, pos, (int)(nr + 1), st);
+        tmp = ctx->arena.alloc_bytes(tb);
+        for (int l = 0; l < 3; ++l)
+            SFB_CUDA(cub::DeviceScan::ExclusiveSum(tmp, tb, cnts + l * (nr + 1), pos + l * (nr + 1),
+                                                   (int)(nr + 1), st));
+        int32_t *tot = ctx->arena.alloc<int32_t>(3);
+        for (int l = 0; l < 3; ++l)
+            SFB_CUDA(cudaMemcpyAsync(tot + l, pos + l * (nr + 1) + nr, sizeof(int32_t),
+                                     cudaMemcpyDeviceToDevice, st));
+        ctx->read_back(tot, 3 * sizeof(int32_t));
+        const int32_t *h = reinterpret_cast<const int32_t *>(ctx->pinned);
+        Ef = h[0];
+        Es = h[1];
+        G = h[2];
+        uint32_t *fkey = ctx->arena.alloc<uint32_t>(Ef + 1), *fval = ctx->arena.alloc<uint32_t>(Ef + 1);
+        uint32_t *skey = ctx->arena.alloc<uint32_t>(Es + 1), *sval = ctx->arena.alloc<uint32_t>(Es + 1);
+        glist = ctx->arena.alloc<uint32_t>(G + 1);
+        k_emit<<<grid_for(nr, 128), 128, 0, st>>>(R, pos, pos + (nr + 1), pos + 2 * (nr + 1), ntx,
+                                                  nsx, fkey, fval, skey, sval, glist);
+        SFB_CHECK_LAUNCH();
+        // stable sort by tile id keeps each tile's runs in rank order
+        uint32_t *fkey2 = ctx->arena.alloc<uint32_t>(Ef + 1), *skey2 = ctx->arena.alloc<uint32_t>(Es + 1);
+        fval2 = ctx->arena.alloc<uint32_t>(Ef + 1);
+        sval2 = ctx->arena.alloc<uint32_t>(Es + 1);
+        int fbits = bits_for((uint64_t)(ntx * nty)), sbits = bits_for((uint64_t)(nsx * nsy));
+        size_t tb1 = 0, tb2 = 0, tb3 = 0;
+        if (Ef) cub::DeviceRadixSort::SortPairs(nullptr, tb1, fkey, fkey2, fval, fval2, (int)Ef, 0, fbits, st);
+        if (Es) cub::DeviceRadixSort::SortPairs(nullptr, tb2, skey, skey2, sval, sval2, (int)Es, 0, sbits, st);
+        int64_t nt = ntx * nty, ns = nsx * nsy;
+        cub::DeviceScan::ExclusiveSum(nullptr, tb3, f_off, f_off, (int)(nt + 1), st);
+        size_t tbm = std::max(tb1, std::max(tb2, tb3));
+        size_t tb4 = 0;
+        cub::DeviceScan::ExclusiveSum(nullptr, tb4, s_off, s_off, (int)(ns + 1), st);
+        tbm = std::max(tbm, tb4);
+        tmp = ctx->arena.alloc_bytes(tbm);
+        if (Ef) {
+            SFB_CUDA(cub::DeviceRadixSort::SortPairs(tmp, tb1, fkey, fkey2, fval, fval2, (int)Ef, 0, fbits, st));
+            k_histogram<<<grid_for(Ef, 256), 256, 0, st>>>(fkey2, Ef, f_off);
+        }
+        if (Es) {
+            SFB_CUDA(cub::DeviceRadixSort::SortPairs(tmp, tb2, skey, skey2, sval, sval2, (int)Es, 0, sbits, st));
+            k_histogram<<<grid_for(Es, 256), 256, 0, st>>>(skey2, Es, s_off);
+        }
+        SFB_CHECK_LAUNCH();
+        SFB_CUDA(cub::DeviceScan::ExclusiveSum(tmp, tbm, f_off, f_off, (int)(nt + 1), st));
+        SFB_CUDA(cub::DeviceScan::ExclusiveSum(tmp, tbm, s_off, s_off, (int)(ns + 1), st));
+    }
+    ctx->stats.runs = R.R;
+    ctx->stats.fine_entries = Ef;
+    ctx->stats.super_entries = Es;
+    ctx->stats.global_entries = G;
+
+    CompParams C{};
+    C.W = cam.width;
+    C.H = cam.height;
+    C.ntx = ntx;
+    C.nty = nty;
+    C.nsx = nsx;
+    C.tile = TS;
+    C.terminate = opts.early_termination;
+    C.alpha_max = opts.alpha_max;
+    C.plane_mask = plane_mask;
+    for (int a = 0; a < 3; ++a) C.bg[a] = bg ? bg[a] : 0.0;
+    C.f_off = f_off;
+    C.f_ids = fval2;
+    C.s_off = s_off;
+    C.s_ids = sval2;
+    C.g_ids = glist;
+    C.G = G;
+    C.R = R;
+    C.src = src;
+    C.p2g = in.point_to_geom;
+    C.colors = in.colors;
+    C.normals = in.normals;
+    C.gdepth = P.depth;
+    C.rgb = (plane_mask & SFB_PLANE_RGB) ? rgb : nullptr;
+    C.normal = (plane_mask & SFB_PLANE_NORMAL) ? normal : nullptr;
+    C.depth = (plane_mask & SFB_PLANE_DEPTH) ? depth : nullptr;
+    C.trans = trans;
+    int64_t ntiles = ntx * nty;
+    if (TS * TS <= kCT) k_composite<1><<<(unsigned)ntiles, kCT, 0, st>>>(C);
+    else k_composite<4><<<(unsigned)ntiles, kCT, 0, st>>>(C);
+    SFB_CHECK_LAUNCH();
+}
+
+// ------------------------------------------------------------ debug CSR (bin_tiles parity)
+__global__ void k_rank_rects(const uint32_t *__restrict__ src, int64_t K, const int32_t *__restrict__ p2g,
+                             Proj P, const double *__restrict__ opac, double ft, int64_t ntx,
+                             int64_t nty, double *__restrict__ radius, int4 *__restrict__ rect,
+                             int32_t *__restrict__ cnt, int64_t *__restrict__ source) {
+    int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (j >= K) return;
+    uint32_t i = src[j];
+    int32_t g = p2g ? p2g[i] : (int32_t)i;
+    double r = support_radius(P.a[g], P.b[g], P.c[g], opac[g]);
+    radius[j] = r;
+    source[j] = i;
+    TileRect t = tile_rect(P.sx[g], P.sy[g], r, ft, ntx, nty);
+    rect[j] = make_int4(t.x0, t.x1, t.y0, t.y1);
+    cnt[j] = (t.x0 <= t.x1 && t.y0 <= t.y1) ? (t.x1 - t.x0 + 1) * (t.y1 - t.y0 + 1) : 0;
+}
+
+__global__ void k_rank_emit(const int4 *__restrict__ rect, const int64_t *__restrict__ pos, int64_t K,
+                            int64_t ntx, uint32_t *__restrict__ key, uint32_t *__restrict__ val) {
+    int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (j >= K) return;
+    int4 t = rect[j];
+    int64_t p = pos[j];
+    for (int y = t.z; y <= t.w; ++y)
+        for (int x = t.x; x <= t.y; ++x) {
+            key[p] = (uint32_t)(y * ntx + x);
+            val[p++] = (uint32_t)j;
+        }
+}
+
+__global__ void k_widen(const uint32_t *__restrict__ a, int64_t n, int64_t *__restrict__ b) {
+    int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (j < n) b[j] = a[j];
+}
+__global__ void k_widen32(const int32_t *__restrict__ a, int64_t n, int64_t *__restrict__ b) {
+    int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (j < n) b[j] = a[j];
+}
+
+void prepare_debug_run(sfb_ctx *ctx, const RenderInputs &in, const sfb_camera &cam, int tile,
+                       int64_t *source, double *radius, int64_t *offsets, int64_t *ids,
+                       int64_t cap, int64_t *k_host, int64_t *e_host) {
+    cudaStream_t st = ctx->stream;
+    const int64_t ntx = (cam.width + tile - 1) / tile, nty = (cam.height + tile - 1) / tile;
+    Proj P = project_inputs(ctx, in, cam);
+    uint32_t *src = nullptr;
+    int64_t K = depth_order(ctx, in, P, &src);
+    *k_host = K;
+    int64_t nt = ntx * nty;
+    int32_t *toff = ctx->arena.alloc<int32_t>(nt + 1);
+    SFB_CUDA(cudaMemsetAsync(toff, 0, sizeof(int32_t) * (nt + 1), st));
+    if (K == 0) {
+        *e_host = 0;
+        k_widen32<<<grid_for(nt + 1, 256), 256, 0, st>>>(toff, nt + 1, offsets);
+        return;
+    }
+    int4 *rect = ctx->arena.alloc<int4>(K);
+    int32_t *cnt = ctx->arena.alloc<int32_t>(K + 1);
+    int64_t *pos = ctx->arena.alloc<int64_t>(K + 1);
+    SFB_CUDA(cudaMemsetAsync(cnt, 0, sizeof(int32_t) * (K + 1), st));
+    k_rank_rects<<<grid_for(K, 256), 256, 0, st>>>(src, K, in.point_to_geom, P, in.opac,
+                                                   (double)tile, ntx, nty, radius, rect, cnt, source);
+    size_t tb = 0;
+    cub::DeviceScan::ExclusiveSum(nullptr, tb, cnt, pos, (int)(K + 1), st);
+    void *tmp = ctx->arena.alloc_bytes(tb);
+    SFB_CUDA(cub::DeviceScan::ExclusiveSum(tmp, tb, cnt, pos, (int)(K + 1), st));
+    ctx->read_back(pos + K, sizeof(int64_t));
+    int64_t E = ctx->pinned[0];
+    *e_host = E;
+    SFB_REQUIRE(E < (int64_t(1) << 31), "debug CSR larger than 2^31 entries");
+    uint32_t *key = ctx->arena.alloc<uint32_t>(E + 1), *val = ctx->arena.alloc<uint32_t>(E + 1);
+    uint32_t *key2 = ctx->arena.alloc<uint32_t>(E + 1), *val2 = ctx->arena.alloc<uint32_t>(E + 1);
+    k_rank_emit<<<grid_for(K, 256), 256, 0, st>>>(rect, pos, K, ntx, key, val);
+    tb = 0;
+    int bits = bits_for((uint64_t)nt);
+    if (E) cub::DeviceRadixSort::SortPairs(nullptr, tb, key, key2, val, val2, (int)E, 0, bits, st);
+    size_t tb2 = 0;
+    cub::DeviceScan::ExclusiveSum(nullptr, tb2, toff, toff, (int)(nt + 1), st);
+    size_t tbx = std::max(tb, tb2);
+    tmp = ctx->arena.alloc_bytes(tbx);
+    if (E) {
+        SFB_CUDA(cub::DeviceRadixSort::SortPairs(tmp, tb, key, key2, val, val2, (int)E, 0, bits, st));
+        k_histogram<<<grid_for(E, 256), 256, 0, st>>>(key2, E, toff);
+    }
+    SFB_CUDA(cub::DeviceScan::ExclusiveSum(tmp, tbx, toff, toff, (int)(nt + 1), st));
+    k_widen32<<<grid_for(nt + 1, 256), 256, 0, st>>>(toff, nt + 1, offsets);
+    if (E && E <= cap) k_widen<<<grid_for(E, 256), 256, 0, st>>>(val2, E, ids);
+    SFB_CHECK_LAUNCH();
+}
+
+}  // namespace sfb

@@ -1,0 +1,82 @@
+"""End-to-end: cloud -> P2ENet -> planes on the GPU vs the CPU oracle end to end,
+and the fused frame vs the two-step (estimate_neural, render) path."""
+import numpy as np
+import pytest
+import torch
+
+from oracle import net as ON
+from oracle import raster as OR
+from paper_2409_16504_b200 import netplan, scenes
+from paper_2409_16504_b200.estimators import EstimatorConfig, estimate_neural, run_estimator
+from paper_2409_16504_b200.gaussians import Camera
+from paper_2409_16504_b200.pcio import PointCloud
+from paper_2409_16504_b200.pipeline import render_frame, stats
+from paper_2409_16504_b200.rasterizer import render_planes
+
+pytestmark = pytest.mark.gpu
+TOL = 2e-3
+
+
+def np_(t):
+    return t.detach().cpu().numpy().astype(np.float64)
+
+
+@pytest.fixture(scope="module")
+def setup():
+    cloud, views = scenes.config1()
+    w = netplan.init_random(netplan.NetworkPlan(), 0)
+    return PointCloud(cloud.positions, cloud.colors), cloud, views[0], w
+
+
+def test_estimate_neural_params_vs_oracle(setup):
+    pc, cloud, view, w = setup
+    sp = estimate_neural(pc, w, EstimatorConfig())
+    ref = ON.estimate(cloud.positions, cloud.colors, w.as_oracle_layers(), 3)
+    scale = ref["vox"]["scale_to_world"]
+    d = np_(sp.centers) - ref["centers"]
+    assert (np.abs(d) <= 1e-3 * scale).all()
+    bound = 1e-3 * np.maximum(np.abs(ref["scales"]), 1e-3 * scale)
+    assert (np.abs(np_(sp.scales) - ref["scales"]) <= bound).all()
+    for k in ("quaternions", "opacities", "normals"):
+        assert np.abs(np_(getattr(sp, k)) - ref[k]).max() <= 1e-3, k
+    assert np.array_equal(np_(sp.colors), ref["colors"])
+
+
+def test_fused_frame_equals_two_step(setup):
+    pc, cloud, view, w = setup
+    cam = Camera.of(view)
+    fused = render_frame(pc, w, cam, ("rgb", "normal", "depth"))
+    two = render_planes(estimate_neural(pc, w), cam, ("rgb", "normal", "depth"))
+    for k in ("rgb", "normal", "depth", "transmittance"):
+        assert torch.equal(getattr(fused, k), getattr(two, k)), k
+    st = stats()
+    assert st["runs"] <= st["kept"]
+
+
+def test_end_to_end_vs_cpu_oracle(setup):
+    pc, cloud, view, w = setup
+    fb = render_frame(pc, w, Camera.of(view), ("rgb", "normal")).numpy()
+    est = ON.estimate(cloud.positions, cloud.colors, w.as_oracle_layers(), 3)
+    for mode in ("rgb", "normal"):
+        ref = OR.render(est, view, mode)
+        err = np.abs(fb[mode] - ref[mode])
+        over = int((err.max(axis=2) > TOL).sum())
+        print(f"e2e {mode}: max |d| {err.max():.3g}, pixels over 2e-3: {over}")
+        assert over <= 0.001 * err.shape[0] * err.shape[1], (mode, over, err.max())
+
+
+def test_run_estimator_default_weights(setup):
+    pc, cloud, view, w = setup
+    a = run_estimator(pc, EstimatorConfig(kind="neural"))
+    b = estimate_neural(pc, w)
+    assert torch.equal(a.centers, b.centers)
+    with pytest.raises(NotImplementedError):
+        run_estimator(pc, EstimatorConfig(kind="local_pca"))
+
+
+def test_device_resident_inputs(setup):
+    pc, cloud, view, w = setup
+    dev = PointCloud(torch.from_numpy(cloud.positions).cuda(), torch.from_numpy(cloud.colors).cuda())
+    a = render_frame(dev, w, Camera.of(view))
+    b = render_frame(pc, w, Camera.of(view))
+    assert torch.equal(a.rgb, b.rgb) and torch.equal(a.normal, b.normal)

@@ -1,0 +1,167 @@
+"""GPU P2ENet vs the float64 oracle, with the tolerances of SURVEY.md §8(a):
+raw head |d| <= 1e-3*max(|ref|, 1e-3*max|ref|); delta/sigma relative to
+max(|ref|, 1e-3*scale); quaternion/opacity/normal 1e-3 absolute."""
+import numpy as np
+import pytest
+import torch
+
+from oracle import net as ON
+from oracle import voxel as OV
+from paper_2409_16504_b200 import netplan, scenes, sparsenet
+from paper_2409_16504_b200.pcio import PointCloud
+from paper_2409_16504_b200.voxelgrid import SparseVoxelGrid, voxelize_adaptive
+
+pytestmark = pytest.mark.gpu
+TOL = 1e-3
+
+
+def np_(t):
+    return t.detach().cpu().numpy().astype(np.float64)
+
+
+def raw_close(got, ref):
+    bound = TOL * np.maximum(np.abs(ref), 1e-3 * np.abs(ref).max())
+    bad = np.abs(got - ref) > bound
+    assert not bad.any(), f"{bad.sum()} raw outputs out of tolerance; worst " \
+                          f"{(np.abs(got - ref) / np.maximum(bound, 1e-300)).max():.3g}x"
+
+
+@pytest.fixture(scope="module", params=["simt_f32", "tc_tf32x3"])
+def mode(request):
+    sparsenet.set_mode(request.param)
+    yield request.param
+    sparsenet.set_mode("simt_f32")
+
+
+def test_config1_raw_head_vs_reference_golden(c1_arrays, mode):
+    cloud, _ = scenes.config1()
+    w = netplan.init_random(netplan.NetworkPlan(), 0)
+    vox = voxelize_adaptive(PointCloud(cloud.positions, cloud.colors))
+    raw = np_(sparsenet.unet_forward_voxels(vox, w))
+    raw_close(raw, c1_arrays["raw_voxel"])
+
+
+def test_config1_gaussian_params(c1_arrays, mode):
+    cloud, _ = scenes.config1()
+    w = netplan.init_random(netplan.NetworkPlan(), 0)
+    vox = voxelize_adaptive(PointCloud(cloud.positions, cloud.colors))
+    scale = vox.grid.scale_to_world
+    head = sparsenet.activate_head(sparsenet.unet_forward_voxels(vox, w), scale)
+    ref = ON.activate(c1_arrays["raw_voxel"], scale)
+    for name, got, want in (("delta", head.delta, ref["delta"]), ("sigma", head.sigma, ref["sigma"])):
+        g = np_(got)
+        bound = TOL * np.maximum(np.abs(want), 1e-3 * scale)
+        assert (np.abs(g - want) <= bound).all(), name
+    for name, got, want in (("quat", head.quat, ref["quat"]), ("opacity", head.opacity, ref["opacity"]),
+                            ("normal", head.normal, ref["normal"])):
+        assert np.abs(np_(got) - want).max() <= TOL, name
+
+
+def dense_conv(coords, feats, stride, w, b):
+    """Dense cross-correlation oracle (reference test_sparsenet.py:47-62)."""
+    k = w.shape[0]
+    r = k // 2
+    g = coords.astype(np.int64) // stride
+    g = g - g.min(axis=0)
+    nx, ny, nz = g.max(axis=0) + 1
+    dense = np.zeros((nz + 2 * r, ny + 2 * r, nx + 2 * r, feats.shape[1]))
+    dense[g[:, 2] + r, g[:, 1] + r, g[:, 0] + r] = feats
+    acc = np.zeros((nz, ny, nx, w.shape[-1])) + b.astype(np.float64)
+    for a in range(k):
+        for bb in range(k):
+            for c in range(k):
+                acc += dense[a:a + nz, bb:bb + ny, c:c + nx] @ w[a, bb, c].astype(np.float64)
+    return acc[g[:, 2], g[:, 1], g[:, 0]]
+
+
+@pytest.mark.parametrize("kernel,stride,cin,cout", [(1, 1, 4, 8), (3, 1, 9, 16), (5, 1, 3, 5),
+                                                    (3, 2, 16, 32), (3, 8, 64, 128)])
+def test_sparse_conv_vs_dense_oracle(kernel, stride, cin, cout, mode):
+    rng = np.random.default_rng(kernel + 7 * stride + cin)
+    side = 10
+    lattice = np.stack(np.meshgrid(*[np.arange(side)] * 3, indexing="ij"), -1).reshape(-1, 3)
+    pick = rng.choice(lattice.shape[0], size=300, replace=False)
+    coords = (lattice[pick] * stride).astype(np.int32)
+    feats = rng.normal(size=(300, cin)).astype(np.float32)
+    spec = netplan.ConvLayerSpec("conv", cin, cout, kernel=kernel)
+    w = rng.uniform(-0.3, 0.3, size=spec.weight_shape).astype(np.float32)
+    b = rng.normal(size=cout).astype(np.float32)
+    grid = SparseVoxelGrid.from_host(coords, feats, stride=stride)
+    out = sparsenet.sparse_conv(grid, spec, w, b, relu=False)
+    c = np_(grid.coords).astype(np.int32)
+    ref = dense_conv(c, np_(grid.feats), stride, w, b)
+    np.testing.assert_allclose(np_(out.feats), ref, rtol=0, atol=1e-4)
+
+
+def test_transposed_conv_children_and_orphans():
+    rng = np.random.default_rng(3)
+    parents = np.array([[0, 0, 0], [2, 0, 0], [0, 4, 2]], dtype=np.int32)
+    pf = rng.normal(size=(3, 6)).astype(np.float32)
+    spec = netplan.ConvLayerSpec("transposed_conv", 6, 4)
+    w = rng.normal(size=spec.weight_shape).astype(np.float32)
+    b = rng.normal(size=4).astype(np.float32)
+    grid = SparseVoxelGrid.from_host(parents, pf, stride=2)
+    kids = np.array([[0, 0, 0], [1, 0, 0], [1, 1, 1], [3, 1, 0], [1, 5, 3], [9, 9, 9]])
+    out = sparsenet.transposed_conv_pruned(grid, spec, w, b, kids, relu=False)
+    pk = OV.pack(np_(grid.coords).astype(np.int32))
+    pidx, tap = OV.transposed_map(kids, pk, 2)
+    g = np_(grid.feats)
+    want = np.tile(b.astype(np.float64), (len(kids), 1))
+    for i in range(len(kids)):
+        if pidx[i] >= 0:
+            want[i] += g[pidx[i]] @ w.reshape(8, 6, 4)[tap[i]].astype(np.float64)
+    np.testing.assert_allclose(np_(out.feats), want, rtol=0, atol=1e-5)
+    np.testing.assert_allclose(np_(out.feats)[-1], b, rtol=0, atol=0)   # orphan -> bias
+
+
+def test_zero_weights_give_final_bias():
+    rng = np.random.default_rng(7)
+    plan = netplan.NetworkPlan()
+    layers = [(s, np.zeros(s.weight_shape, np.float32), rng.normal(size=s.out_channels).astype(np.float32))
+              for s in plan.layer_specs()]
+    w = netplan.NetworkWeights(plan, layers)
+    pos = rng.normal(size=(200, 3))
+    vox = voxelize_adaptive(PointCloud(pos, rng.random((200, 3))))
+    raw = np_(sparsenet.unet_forward(vox, w))
+    np.testing.assert_allclose(raw, np.broadcast_to(layers[-1][2], raw.shape), rtol=0, atol=1e-6)
+
+
+@pytest.mark.parametrize("plan", [netplan.NetworkPlan((9, 4, 6), (4,), 5),
+                                  netplan.NetworkPlan((9, 8, 12, 24, 40, 48), (40, 24, 12, 8), 16)])
+def test_custom_plans_vs_oracle(plan, mode):
+    rng = np.random.default_rng(9)
+    pos = rng.normal(size=(3000, 3)) * [1.0, 0.8, 1.3]
+    col = rng.random((3000, 3))
+    w = netplan.init_random(plan, 2)
+    vox = voxelize_adaptive(PointCloud(pos, col))
+    got = np_(sparsenet.unet_forward_voxels(vox, w))
+    ov = OV.voxelize(pos, col)
+    ref = ON.unet(ov, w.as_oracle_layers(), plan.levels, per_voxel=True)
+    raw_close(got, ref)
+
+
+def test_p2en_round_trip_on_device(tmp_path):
+    w = netplan.init_random(netplan.NetworkPlan(), 5)
+    p = tmp_path / "w.p2en"
+    netplan.save_weights(w, p)
+    w2 = netplan.load_weights(p)
+    cloud, _ = scenes.config1(n_dirs=3000)
+    vox = voxelize_adaptive(PointCloud(cloud.positions, cloud.colors))
+    a = np_(sparsenet.unet_forward_voxels(vox, w))
+    b = np_(sparsenet.unet_forward_voxels(vox, w2))
+    assert np.array_equal(a, b)
+
+
+def test_activate_head_closed_forms():
+    out = sparsenet.activate_head(np.zeros((2, 14)), voxel_scale=0.5)
+    np.testing.assert_allclose(np_(out.delta), 0.0, atol=0)
+    np.testing.assert_allclose(np_(out.sigma), np.log(2.0) * 0.5, rtol=1e-12)
+    assert np_(out.quat)[0].tolist() == [1.0, 0.0, 0.0, 0.0]
+    np.testing.assert_allclose(np_(out.opacity), 0.5, rtol=1e-15)
+    assert np_(out.normal)[0].tolist() == [0.0, 0.0, 1.0]
+    raw = np.zeros(14)
+    raw[6] = -1.0          # quaternion collapses to zero -> identity
+    raw[3:6] = -1e4        # softplus underflow -> 1e-12 floor
+    out = sparsenet.activate_head(raw, voxel_scale=2.0)
+    assert np_(out.quat).tolist() == [1.0, 0.0, 0.0, 0.0]
+    np.testing.assert_allclose(np_(out.sigma), 2e-12, rtol=1e-12)
