@@ -76,6 +76,12 @@ const char *sfb_last_error(sfb_ctx *ctx);
 int sfb_set_stream(sfb_ctx *ctx, void *cuda_stream);     /* cudaStream_t */
 int sfb_get_stats(sfb_ctx *ctx, sfb_stats *out);         /* host out */
 int sfb_version(void);
+/* Stage timing with CUDA events on the context stream (off by default):
+ * after a call, sfb_stage_times returns (stage id, ms) per completed stage:
+ * 1 voxelize, 2 unet, 3 head, 4 project, 5 depth sort, 6 runs+binning,
+ * 7 composite. Synchronises on the recorded events. */
+int sfb_set_timing(sfb_ctx *ctx, int on);
+int sfb_stage_times(sfb_ctx *ctx, int32_t *stage_ids, float *ms, int32_t cap, int32_t *n_out);
 
 /* ---- voxelization (voxelgrid.py:125-168, voxelize_adaptive) ------------- */
 /* bbox of (n,3) device positions -> host lo_hi[6] = (lo xyz, hi xyz). The

@@ -18,6 +18,8 @@ LIB_PATH = PKG / "_build" / "libsfb200.so"
 SFB_OK, SFB_ERR_ARG, SFB_ERR_OOM, SFB_ERR_CUDA, SFB_ERR_STATE = 0, 1, 2, 3, 4
 PLANE_RGB, PLANE_NORMAL, PLANE_DEPTH = 1, 2, 4
 NET_SIMT_F32, NET_TC_TF32X3 = 0, 1
+STAGES = {1: "voxelize", 2: "unet", 3: "head", 4: "project", 5: "sort", 6: "bin",
+          7: "composite"}
 
 P = ctypes.c_void_p
 I64 = ctypes.c_int64
@@ -52,6 +54,8 @@ SIGNATURES = {
     "sfb_set_stream": [P, P],
     "sfb_get_stats": [P, ctypes.POINTER(Stats_t)],
     "sfb_version": [],
+    "sfb_set_timing": [P, ctypes.c_int],
+    "sfb_stage_times": [P, P, P, I32, ctypes.POINTER(I32)],
     "sfb_bbox": [P, P, I64, P],
     "sfb_voxelize": [P, P, P, I64, D, P, P, P, P, P, P, P, ctypes.POINTER(I64)],
     "sfb_kernel_map": [P, P, I64, I32, I32, P],
@@ -127,6 +131,22 @@ class Context:
             if rc == SFB_ERR_ARG:
                 raise ValueError(msg)
             raise SfbError(f"{name}: {msg} (code {rc})")
+
+    def set_timing(self, on: bool) -> None:
+        self.lib.sfb_set_timing(self.handle, int(bool(on)))
+
+    def stage_times(self) -> dict:
+        """{stage name: ms} of the last call (needs set_timing(True))."""
+        ids = (I32 * 16)()
+        ms = (ctypes.c_float * 16)()
+        n = I32(0)
+        if self.lib.sfb_stage_times(self.handle, ids, ms, 16, ctypes.byref(n)) != SFB_OK:
+            raise SfbError("sfb_stage_times failed")
+        out = {}
+        for i in range(n.value):
+            name = STAGES.get(ids[i], str(ids[i]))
+            out[name] = out.get(name, 0.0) + ms[i]
+        return out
 
     def stats(self) -> dict:
         s = Stats_t()

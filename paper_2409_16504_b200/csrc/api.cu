@@ -13,6 +13,8 @@ int guard(sfb_ctx *ctx, F &&f) {
     try {
         SFB_CUDA(cudaSetDevice(ctx->device));
         ctx->arena.reset();
+        ctx->n_marks = 0;
+        ctx->mark(ST_BEGIN);
         f();
         ctx->last_error.clear();
         return SFB_OK;
@@ -72,9 +74,11 @@ VoxelSplats neural_voxels(sfb_ctx *ctx, const double *pos, const double *col, in
     o.order = ctx->arena.alloc<int32_t>(n);
     o.offsets = ctx->arena.alloc<int32_t>(n + 1);
     voxelize_run(ctx, pos, col, n, s, lo_hi, o);
+    ctx->mark(ST_VOXELIZE);
     int64_t m = o.m;
     float *raw = ctx->arena.alloc<float>(14 * m);
     unet_run(ctx, o.coords, o.feats, m, raw);
+    ctx->mark(ST_UNET);
     double *blk = ctx->arena.alloc<double>(14 * m);
     V.c = blk;
     V.s = blk + 3 * m;
@@ -82,6 +86,7 @@ VoxelSplats neural_voxels(sfb_ctx *ctx, const double *pos, const double *col, in
     V.o = blk + 10 * m;
     V.n = blk + 11 * m;
     head_to_voxel_splats(ctx, raw, o.coords, o.feats, m, 1.0 / s, V.c, V.s, V.q, V.o, V.n);
+    ctx->mark(ST_HEAD);
     return V;
 }
 
@@ -120,6 +125,27 @@ const char *sfb_last_error(sfb_ctx *ctx) { return ctx ? ctx->last_error.c_str() 
 int sfb_set_stream(sfb_ctx *ctx, void *stream) {
     if (!ctx) return SFB_ERR_ARG;
     ctx->stream = static_cast<cudaStream_t>(stream);
+    return SFB_OK;
+}
+
+int sfb_set_timing(sfb_ctx *ctx, int on) {
+    if (!ctx) return SFB_ERR_ARG;
+    ctx->timing = on != 0;
+    return SFB_OK;
+}
+
+int sfb_stage_times(sfb_ctx *ctx, int32_t *stage_ids, float *ms, int32_t cap, int32_t *n_out) {
+    if (!ctx || !n_out) return SFB_ERR_ARG;
+    int n = 0;
+    for (int i = 1; i < ctx->n_marks && n < cap; ++i) {
+        float t = 0.f;
+        if (cudaEventSynchronize(ctx->ev[i]) != cudaSuccess ||
+            cudaEventElapsedTime(&t, ctx->ev[i - 1], ctx->ev[i]) != cudaSuccess)
+            return SFB_ERR_CUDA;
+        stage_ids[n] = ctx->stage_id[i];
+        ms[n++] = t;
+    }
+    *n_out = n;
     return SFB_OK;
 }
 

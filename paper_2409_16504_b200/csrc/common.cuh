@@ -123,11 +123,25 @@ struct sfb_ctx {
     sfb_stats stats{};
     // pinned host staging for small D2H reads (sizes, bbox)
     int64_t *pinned = nullptr;
+    // optional stage timing: CUDA events recorded on the stream at stage ends
+    static constexpr int kMaxMarks = 16;
+    bool timing = false;
+    cudaEvent_t ev[kMaxMarks] = {};
+    int stage_id[kMaxMarks] = {};
+    int n_marks = 0;
+    void mark(int stage) {
+        if (!timing || n_marks >= kMaxMarks) return;
+        if (!ev[n_marks]) cudaEventCreate(&ev[n_marks]);
+        cudaEventRecord(ev[n_marks], stream);
+        stage_id[n_marks++] = stage;
+    }
     ~sfb_ctx() {
         net.release();
         for (void *p : {(void *)adhoc.w, (void *)adhoc.b, (void *)adhoc.w_tc})
             if (p) cudaFree(p);
         if (pinned) cudaFreeHost(pinned);
+        for (auto &e : ev)
+            if (e) cudaEventDestroy(e);
     }
     // read `count` int64 values back from device (one sync)
     void read_back(const void *dev, size_t bytes) {
@@ -137,6 +151,9 @@ struct sfb_ctx {
 };
 
 namespace sfb {
+
+// stage ids reported by sfb_stage_times
+enum Stage { ST_BEGIN = 0, ST_VOXELIZE, ST_UNET, ST_HEAD, ST_PROJECT, ST_SORT, ST_BIN, ST_COMPOSITE };
 
 inline unsigned grid_for(int64_t n, int block, int64_t cap = 1 << 20) {
     int64_t g = (n + block - 1) / block;

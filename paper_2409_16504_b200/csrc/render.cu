@@ -583,8 +583,10 @@ void render_run(sfb_ctx *ctx, const RenderInputs &in, const sfb_camera &cam,
     const int64_t ntx = (cam.width + TS - 1) / TS, nty = (cam.height + TS - 1) / TS;
     const int64_t nsx = (ntx + kSuper - 1) / kSuper, nsy = (nty + kSuper - 1) / kSuper;
     Proj P = project_inputs(ctx, in, cam);
+    ctx->mark(ST_PROJECT);
     uint32_t *src = nullptr;
     int64_t K = depth_order(ctx, in, P, &src);
+    ctx->mark(ST_SORT);
     ctx->stats.kept = K;
 
     Runs R{};
@@ -676,6 +678,7 @@ void render_run(sfb_ctx *ctx, const RenderInputs &in, const sfb_camera &cam,
         SFB_CUDA(cub::DeviceScan::ExclusiveSum(tmp, tbm, f_off, f_off, (int)(nt + 1), st));
         SFB_CUDA(cub::DeviceScan::ExclusiveSum(tmp, tbm, s_off, s_off, (int)(ns + 1), st));
     }
+    ctx->mark(ST_BIN);
     ctx->stats.runs = R.R;
     ctx->stats.fine_entries = Ef;
     ctx->stats.super_entries = Es;
@@ -712,6 +715,7 @@ void render_run(sfb_ctx *ctx, const RenderInputs &in, const sfb_camera &cam,
     if (TS * TS <= kCT) k_composite<1><<<(unsigned)ntiles, kCT, 0, st>>>(C);
     else k_composite<4><<<(unsigned)ntiles, kCT, 0, st>>>(C);
     SFB_CHECK_LAUNCH();
+    ctx->mark(ST_COMPOSITE);
 }
 
 // ------------------------------------------------------------ debug CSR (bin_tiles parity)
