@@ -46,12 +46,13 @@ UNIT = "frames/s"
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--steps", type=int, default=100)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
     ap.add_argument("--config", choices=("c2", "c1"), default="c2")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-profile", action="store_true", help="skip the CUPTI launch count")
     ap.add_argument("--cpu-rows", type=int, default=2, help="tile rows in the CPU sample")
     return ap.parse_args()
 
@@ -143,7 +144,7 @@ class ClockSampler:
              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
         try:
             self.p = subprocess.Popen(["nvidia-smi", "-i", str(gpu), f"--query-gpu={q}",
-                                       "--format=csv,noheader,nounits", "-lms", "100"],
+                                       "--format=csv,noheader,nounits", "-lms", "50"],
                                       stdout=self.f, stderr=subprocess.DEVNULL)
         except OSError:
             self.p = None
@@ -266,14 +267,17 @@ def run_ours(args):
 
     # ---- kernel launches of one frame (CUPTI via torch.profiler, outside the timed region)
     launches = None
-    try:
+    if args.no_profile:
+        launches = "not counted (--no-profile)"
+    else:
+      try:
         from torch.profiler import ProfilerActivity, profile
         with profile(activities=[ProfilerActivity.CUDA]) as prof:
             render_frame(dev_cloud, weights, view_of(0), planes, out=out)
             torch.cuda.synchronize()
         launches = sum(1 for e in prof.events() if e.device_type.name == "CUDA"
                        and "memcpy" not in e.name.lower() and "memset" not in e.name.lower())
-    except Exception as exc:  # pragma: no cover
+      except Exception as exc:  # pragma: no cover
         launches = f"unavailable: {exc}"
 
     # ---- roofline of the dominant stage

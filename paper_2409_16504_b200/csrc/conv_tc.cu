@@ -1,14 +1,365 @@
-// tcgen05 gather-GEMM for the P2ENet sparse convolutions (work in progress:
-// the SIMT path in net.cu is used until this lands).
+// tcgen05 gather-GEMM-scatter for the P2ENet sparse convolutions (sm_100a).
+//
+// Reference semantics: sparse_conv (sparsenet.py:187-214)
+//   out[v] = b + sum_{taps t} in[nbr(v,t)] @ W[t]   (ReLU)
+// as an implicit GEMM: M = output voxels, N = Cout, K = taps x Cin.
+//
+// B200 mapping:
+//  * CTA = 128 output rows (UMMA M=128, cta_group::1) x all Cout (UMMA N),
+//    accumulator in TMEM (fp32, N columns), one elected thread issues
+//    tcgen05.mma.kind::tf32 for the whole CTA.
+//  * fp32 accuracy with tf32 tensor cores ("3xTF32"): every operand x is split
+//    into hi = tf32(x) and lo = tf32(x - hi); D += Ahi*Bhi + Ahi*Blo + Alo*Bhi.
+//    This keeps the conv at ~1e-6 relative error (bf16 inputs would break the
+//    1e-3 Gaussian-parameter tolerance).
+//  * per tap: the weight tile W[t] (pre-split, pre-laid-out in the UMMA
+//    K-major canonical layout at load time) is staged by a TMA bulk copy
+//    (cp.async.bulk, mbarrier complete_tx); the 128 neighbour rows are
+//    gathered by the 128 threads (one row each, kernel map read coalesced),
+//    split hi/lo in registers and written in the same canonical layout.
+//    Two smem stages: the gather of tap t+1 overlaps the MMAs of tap t.
+//  * coarse levels have few 128-row tiles (e.g. 4 at the bottleneck), so the
+//    27 taps are split across CTAs (split-K) to fill the 148 SMs; partial
+//    tiles go to a workspace and a deterministic reduce kernel sums them in
+//    split order, adds the bias and applies ReLU (bitwise run-to-run stable).
 #include "common.cuh"
 
 namespace sfb {
 
-bool conv_tc_supported(const NetLayer &) { return false; }
-void prepare_tc_weights(sfb_ctx *, NetLayer &) {}
-void conv_layer_tc(sfb_ctx *, const NetLayer &, const float *, int, const int32_t *, int64_t, int,
-                   float *, int) {
-    throw Error(SFB_ERR_STATE, "tcgen05 conv path not built");
+namespace {
+
+constexpr int kM = 128;        // UMMA M / rows per CTA
+constexpr int kThreadsTC = 128;
+
+// canonical K-major SWIZZLE_NONE offset (floats) of element (row, k) in a
+// [rows x KP] tile: 8-row groups of KP*8 floats, 4-wide k chunks of 32 floats
+__host__ __device__ inline int core_off(int row, int k, int KP) {
+    return (row >> 3) * (KP * 8) + (k >> 2) * 32 + (row & 7) * 4 + (k & 3);
+}
+
+__device__ __forceinline__ float tf32_trunc(float x) {
+    return __uint_as_float(__float_as_uint(x) & 0xffffe000u);
+}
+
+__device__ __forceinline__ uint32_t smem_u32(const void *p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ uint64_t smem_desc(uint32_t addr, uint32_t lbo, uint32_t sbo) {
+    uint64_t d = 0;
+    d |= (uint64_t)((addr >> 4) & 0x3fff);
+    d |= (uint64_t)((lbo >> 4) & 0x3fff) << 16;
+    d |= (uint64_t)((sbo >> 4) & 0x3fff) << 32;
+    d |= (uint64_t)1 << 46;  // descriptor version (sm_100)
+    return d;                // base offset 0, lbo mode 0, SWIZZLE_NONE
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
+    uint32_t addr = smem_u32(bar);
+    asm volatile(
+        "{\n\t.reg .pred P;\n"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 P, [%0], %1;\n\t"
+        "@!P bra WAIT_%=;\n}" ::"r"(addr),
+        "r"(parity)
+        : "memory");
+}
+
+__device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+                 "r"(bytes)
+                 : "memory");
+}
+
+__device__ __forceinline__ void tma_bulk_g2s(void *dst, const void *src, uint32_t bytes,
+                                             uint64_t *bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
+            "r"(smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar))
+        : "memory");
+}
+
+__device__ __forceinline__ void mma_tf32(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t idesc,
+                                         uint32_t accumulate) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+        "l"(a), "l"(b), "r"(idesc), "r"(accumulate));
+}
+
+__device__ __forceinline__ void mma_commit(uint64_t *bar) {
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                     smem_u32(bar))
+                 : "memory");
+}
+
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, float *v) {
+    uint32_t r[16];
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,"
+        "%15}, [%16];"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+          "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
+          "=r"(r[14]), "=r"(r[15])
+        : "r"(taddr));
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+    for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+template <int KP, int NP>
+struct TcShape {
+    static constexpr int A_FLOATS = kM * KP;               // one of hi/lo
+    static constexpr int B_FLOATS = NP * KP;
+    static constexpr int STAGE_FLOATS = 2 * A_FLOATS + 2 * B_FLOATS;
+    static constexpr int STAGES = (STAGE_FLOATS * 4 * 2 <= 200 * 1024) ? 2 : 1;
+    static constexpr int SMEM = STAGES * STAGE_FLOATS * 4 + 1024 + 64;
+    static constexpr uint32_t TMEM_COLS = NP <= 32 ? 32 : (NP <= 64 ? 64 : (NP <= 128 ? 128 : 256));
+    static constexpr uint32_t IDESC = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(NP >> 3) << 17) |
+                                      ((uint32_t)(kM >> 4) << 24);
+};
+
+template <int KP, int NP>
+__global__ void __launch_bounds__(kThreadsTC)
+k_conv_tc(const float *__restrict__ in, int ld_in, int cin, const int32_t *__restrict__ nbr,
+          int64_t m, int taps, int taps_per_split, const float *__restrict__ wtc,
+          const float *__restrict__ bias, int cout, int relu, float *__restrict__ out, int ld_out,
+          float *__restrict__ partial) {
+    using S = TcShape<KP, NP>;
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    float *stage_base = reinterpret_cast<float *>(
+        (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint64_t *bar_full = reinterpret_cast<uint64_t *>(stage_base + S::STAGES * S::STAGE_FLOATS);
+    uint64_t *bar_done = bar_full + 2;
+    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(bar_done + 2);
+
+    const int tid = threadIdx.x, warp = tid >> 5;
+    const int64_t row0 = (int64_t)blockIdx.x * kM;
+    const int split = blockIdx.y;
+    const int t0 = split * taps_per_split;
+    const int t1 = min(taps, t0 + taps_per_split);
+
+    if (tid == 0) {
+        for (int s = 0; s < 2; ++s) {
+            mbar_init(&bar_full[s], 1);
+            mbar_init(&bar_done[s], 1);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (warp == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                         smem_u32(tmem_slot)),
+                     "r"(S::TMEM_COLS));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;");
+    const uint32_t tmem = *tmem_slot;
+
+    const int64_t row = row0 + tid;
+    int issued = 0;        // taps whose MMAs were issued (uniform)
+    for (int t = t0; t < t1; ++t) {
+        const int s = issued % S::STAGES;
+        const int use = issued / S::STAGES;
+        float *A_hi = stage_base + s * S::STAGE_FLOATS;
+        float *A_lo = A_hi + S::A_FLOATS;
+        float *B_hi = A_lo + S::A_FLOATS;
+        const int32_t src = row < m ? nbr[(int64_t)t * m + row] : -1;
+        if (!__syncthreads_or(src >= 0)) continue;   // empty tap for the whole tile
+        if (use > 0) mbar_wait(&bar_done[s], (use - 1) & 1);   // stage free again
+        if (tid == 0) {
+            const uint32_t bytes = (uint32_t)(2 * S::B_FLOATS * 4);
+            mbar_expect_tx(&bar_full[s], bytes);
+            tma_bulk_g2s(B_hi, wtc + (size_t)t * 2 * S::B_FLOATS, bytes, &bar_full[s]);
+        }
+        // gather my row of this tap, split into tf32 hi/lo, canonical layout
+        const float *x = src >= 0 ? in + (int64_t)src * ld_in : nullptr;
+#pragma unroll
+        for (int c = 0; c < KP / 4; ++c) {
+            float v[4];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                int k = 4 * c + q;
+                v[q] = (x && k < cin) ? __ldg(x + k) : 0.f;
+            }
+            float4 hi, lo;
+            hi.x = tf32_trunc(v[0]);
+            hi.y = tf32_trunc(v[1]);
+            hi.z = tf32_trunc(v[2]);
+            hi.w = tf32_trunc(v[3]);
+            lo.x = tf32_trunc(v[0] - hi.x);
+            lo.y = tf32_trunc(v[1] - hi.y);
+            lo.z = tf32_trunc(v[2] - hi.z);
+            lo.w = tf32_trunc(v[3] - hi.w);
+            const int off = core_off(tid, 4 * c, KP);
+            *reinterpret_cast<float4 *>(A_hi + off) = hi;
+            *reinterpret_cast<float4 *>(A_lo + off) = lo;
+        }
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        __syncthreads();
+        if (tid == 0) {
+            mbar_wait(&bar_full[s], use & 1);
+            asm volatile("tcgen05.fence::after_thread_sync;");
+            const float *B_lo = B_hi + S::B_FLOATS;
+            const uint32_t lbo = 128, sbo_a = KP * 32, sbo_b = KP * 32;
+#pragma unroll
+            for (int ks = 0; ks < KP / 8; ++ks) {
+                const uint64_t ahi = smem_desc(smem_u32(A_hi) + ks * 256, lbo, sbo_a);
+                const uint64_t alo = smem_desc(smem_u32(A_lo) + ks * 256, lbo, sbo_a);
+                const uint64_t bhi = smem_desc(smem_u32(B_hi) + ks * 256, lbo, sbo_b);
+                const uint64_t blo = smem_desc(smem_u32(B_lo) + ks * 256, lbo, sbo_b);
+                mma_tf32(tmem, ahi, bhi, S::IDESC, (issued > 0 || ks > 0) ? 1u : 0u);
+                mma_tf32(tmem, ahi, blo, S::IDESC, 1u);
+                mma_tf32(tmem, alo, bhi, S::IDESC, 1u);
+            }
+            mma_commit(&bar_done[s]);
+        }
+        ++issued;
+    }
+    // epilogue: TMEM -> registers -> bias/ReLU -> global (or split-K partials)
+    float acc[NP];
+    if (issued > 0) {
+        const int last = issued - 1;
+        mbar_wait(&bar_done[last % S::STAGES], (last / S::STAGES) & 1);
+        asm volatile("tcgen05.fence::after_thread_sync;");
+        const uint32_t lane_base = (uint32_t)(warp * 32) << 16;
+#pragma unroll
+        for (int c = 0; c < NP; c += 16) tmem_ld16(tmem + lane_base + c, acc + c);
+    } else {
+#pragma unroll
+        for (int c = 0; c < NP; ++c) acc[c] = 0.f;
+    }
+    if (row < m) {
+        if (partial) {
+            float *p = partial + ((size_t)split * m + row) * NP;
+#pragma unroll
+            for (int c = 0; c < NP; c += 4)
+                *reinterpret_cast<float4 *>(p + c) = make_float4(acc[c], acc[c + 1], acc[c + 2], acc[c + 3]);
+        } else {
+            float *o = out + row * (int64_t)ld_out;
+#pragma unroll
+            for (int c = 0; c < NP; ++c)
+                if (c < cout) {
+                    float v = acc[c] + bias[c];
+                    o[c] = relu ? fmaxf(v, 0.f) : v;
+                }
+        }
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;");
+    __syncthreads();
+    if (warp == 0)
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem),
+                     "r"(S::TMEM_COLS));
+}
+
+// deterministic split-K reduction: out = act(b + sum_s partial[s]) in split order
+__global__ void k_splitk_reduce(const float *__restrict__ partial, int splits, int64_t m, int np,
+                                const float *__restrict__ bias, int cout, int relu,
+                                float *__restrict__ out, int ld_out) {
+    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= m * cout) return;
+    int64_t r = i / cout;
+    int c = (int)(i % cout);
+    float s = 0.f;
+    for (int k = 0; k < splits; ++k) s += partial[((size_t)k * m + r) * np + c];
+    float v = s + bias[c];
+    out[r * ld_out + c] = relu ? fmaxf(v, 0.f) : v;
+}
+
+// W[t][ci][co] -> per tap [hi | lo] tiles of [NP x KP] in the canonical layout
+__global__ void k_prep_weights(const float *__restrict__ w, int taps, int cin, int cout, int KP,
+                               int NP, float *__restrict__ wtc) {
+    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    int64_t per = (int64_t)NP * KP;
+    if (i >= taps * per) return;
+    int t = (int)(i / per);
+    int rem = (int)(i % per);
+    int n = rem / KP, k = rem % KP;
+    float x = (n < cout && k < cin) ? w[((size_t)t * cin + k) * cout + n] : 0.f;
+    float hi = tf32_trunc(x), lo = tf32_trunc(x - hi);
+    float *base = wtc + (size_t)t * 2 * per;
+    int off = core_off(n, k, KP);
+    base[off] = hi;
+    base[per + off] = lo;
+}
+
+int pad_k(int c) { return c <= 16 ? 16 : (c <= 32 ? 32 : (c <= 64 ? 64 : 128)); }
+int pad_n(int c) { return c <= 16 ? 16 : (c <= 32 ? 32 : (c <= 64 ? 64 : (c <= 128 ? 128 : 256))); }
+
+template <int KP, int NP>
+void launch_tc(sfb_ctx *ctx, const NetLayer &L, const float *in, int ld_in, const int32_t *nbr,
+               int64_t m, int relu, float *out, int ld_out) {
+    using S = TcShape<KP, NP>;
+    static bool attr = false;
+    if (!attr) {
+        SFB_CUDA(cudaFuncSetAttribute(k_conv_tc<KP, NP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      S::SMEM));
+        attr = true;
+    }
+    const int64_t tiles = (m + kM - 1) / kM;
+    // split the taps across CTAs until ~2 CTAs per SM are in flight
+    int splits = 1;
+    const int cands[] = {1, 3, 9, 27};
+    for (int c : cands)
+        if (c <= L.taps && L.taps % c == 0) {
+            splits = c;
+            if (tiles * c >= 2 * ctx->num_sms) break;
+        }
+    const int tps = (L.taps + splits - 1) / splits;
+    float *partial = nullptr;
+    if (splits > 1) partial = ctx->arena.alloc<float>((size_t)splits * m * NP);
+    dim3 grid((unsigned)tiles, splits);
+    k_conv_tc<KP, NP><<<grid, kThreadsTC, S::SMEM, ctx->stream>>>(
+        in, ld_in, L.cin, nbr, m, L.taps, tps, L.w_tc, L.b, L.cout, relu, out, ld_out, partial);
+    SFB_CHECK_LAUNCH();
+    if (splits > 1) {
+        k_splitk_reduce<<<grid_for(m * L.cout, 256), 256, 0, ctx->stream>>>(
+            partial, splits, m, NP, L.b, L.cout, relu, out, ld_out);
+        SFB_CHECK_LAUNCH();
+    }
+}
+
+}  // namespace
+
+bool conv_tc_supported(const NetLayer &L) {
+    if (L.kind != 0) return false;
+    int kp = pad_k(L.cin), np = pad_n(L.cout);
+    if (L.cin > 128 || L.cout > 128) return false;
+    size_t stage = (size_t)(2 * kM * kp + 2 * np * kp) * 4;
+    return stage + 2048 <= 200 * 1024;
+}
+
+void prepare_tc_weights(sfb_ctx *ctx, NetLayer &L) {
+    L.cin_pad = pad_k(L.cin);
+    L.cout_pad = pad_n(L.cout);
+    size_t n = (size_t)L.taps * 2 * L.cin_pad * L.cout_pad;
+    SFB_CUDA(cudaMalloc(&L.w_tc, n * sizeof(float)));
+    int64_t total = (int64_t)L.taps * L.cin_pad * L.cout_pad;
+    k_prep_weights<<<grid_for(total, 256), 256, 0, ctx->stream>>>(L.w, L.taps, L.cin, L.cout,
+                                                                  L.cin_pad, L.cout_pad, L.w_tc);
+    SFB_CHECK_LAUNCH();
+}
+
+void conv_layer_tc(sfb_ctx *ctx, const NetLayer &L, const float *in, int ld_in, const int32_t *nbr,
+                   int64_t m, int relu, float *out, int ld_out) {
+#define SFB_TC_CASE(K, N)                                                 \
+    if (L.cin_pad == K && L.cout_pad == N) {                              \
+        launch_tc<K, N>(ctx, L, in, ld_in, nbr, m, relu, out, ld_out);    \
+        return;                                                           \
+    }
+    SFB_TC_CASE(16, 16) SFB_TC_CASE(16, 32) SFB_TC_CASE(16, 64) SFB_TC_CASE(16, 128)
+    SFB_TC_CASE(32, 16) SFB_TC_CASE(32, 32) SFB_TC_CASE(32, 64) SFB_TC_CASE(32, 128)
+    SFB_TC_CASE(64, 16) SFB_TC_CASE(64, 32) SFB_TC_CASE(64, 64) SFB_TC_CASE(64, 128)
+    SFB_TC_CASE(128, 16) SFB_TC_CASE(128, 32) SFB_TC_CASE(128, 64)
+#undef SFB_TC_CASE
+    throw Error(SFB_ERR_STATE, "tcgen05 conv: unsupported channel padding");
 }
 
 }  // namespace sfb

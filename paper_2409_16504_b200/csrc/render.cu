@@ -382,12 +382,15 @@ struct CompParams {
 
 template <int NPIX>
 __global__ void __launch_bounds__(kCT) k_composite(CompParams P) {
+    constexpr int KMAX = kWin / kCT;
+    constexpr uint32_t NONE = 0xffffffffu;
     __shared__ uint32_t bitmap[kWin / 32];
     __shared__ uint32_t list[kWin];
     __shared__ int s_nlist;
-    __shared__ double r_mx[kCT], r_my[kCT], r_rad[kCT], r_ia[kCT], r_ib[kCT], r_ic[kCT], r_op[kCT];
-    __shared__ int32_t r_start[kCT], r_count[kCT];
-    __shared__ uint32_t s_cursor_add[3];
+    __shared__ uint32_t s_add[3];
+    // the current chunk's run records (pixel box precomputed per run)
+    __shared__ double r_mx[kCT], r_my[kCT], r_rr[kCT], r_ia[kCT], r_ib[kCT], r_ic[kCT], r_op[kCT];
+    __shared__ int32_t r_x0[kCT], r_x1[kCT], r_y0[kCT], r_y1[kCT], r_start[kCT], r_count[kCT];
 
     const int64_t t = blockIdx.x;
     const int64_t tx = t % P.ntx, ty = t / P.ntx;
@@ -397,67 +400,84 @@ __global__ void __launch_bounds__(kCT) k_composite(CompParams P) {
     const int64_t x_end = min(x_lo + TS, P.W), y_end = min(y_lo + TS, P.H);
     const bool want_rgb = P.plane_mask & SFB_PLANE_RGB, want_n = P.plane_mask & SFB_PLANE_NORMAL;
     const bool want_d = P.plane_mask & SFB_PLANE_DEPTH;
+    const bool term = P.terminate;
 
-    int64_t pxs[NPIX], pys[NPIX];
+    int32_t pxs[NPIX], pys[NPIX];
     bool valid[NPIX];
     double T[NPIX], c0[NPIX], c1[NPIX], c2[NPIX], n0[NPIX], n1[NPIX], n2[NPIX], dd[NPIX];
 #pragma unroll
     for (int k = 0; k < NPIX; ++k) {
         int p = threadIdx.x + k * kCT;
-        pxs[k] = x_lo + p % TS;
-        pys[k] = y_lo + p / TS;
+        pxs[k] = (int32_t)(x_lo + p % TS);
+        pys[k] = (int32_t)(y_lo + p / TS);
         valid[k] = p < TS * TS && pxs[k] < x_end && pys[k] < y_end;
         T[k] = 1.0;
         c0[k] = c1[k] = c2[k] = n0[k] = n1[k] = n2[k] = dd[k] = 0.0;
     }
+    auto saturated = [&]() {
+        int mine = 1;
+#pragma unroll
+        for (int k = 0; k < NPIX; ++k)
+            if (valid[k] && !(T[k] < kCutoff)) mine = 0;
+        return mine;
+    };
 
-    int64_t fc = P.f_off[t], fe = P.f_off[t + 1];
-    int64_t sc = P.s_off[st], se = P.s_off[st + 1];
-    int64_t gc = 0, ge = P.G;
+    const uint32_t *ids[3] = {P.f_ids, P.s_ids, P.g_ids};
+    int64_t cur[3] = {P.f_off[t], P.s_off[st], 0};
+    const int64_t end[3] = {P.f_off[t + 1], P.s_off[st + 1], P.G};
+    int ws = kCT;  // rank window grows 256 -> 2048: most tiles saturate in the first
     bool done = false;
     while (!done) {
-        uint32_t w0 = 0xffffffffu;
-        if (fc < fe) w0 = min(w0, P.f_ids[fc]);
-        if (sc < se) w0 = min(w0, P.s_ids[sc]);
-        if (gc < ge) w0 = min(w0, P.g_ids[gc]);
-        if (w0 == 0xffffffffu) break;
-        const uint32_t w1 = w0 + kWin;
+        uint32_t head[3];
+#pragma unroll
+        for (int s = 0; s < 3; ++s) head[s] = cur[s] < end[s] ? ids[s][cur[s]] : NONE;
+        const uint32_t w0 = min(head[0], min(head[1], head[2]));
+        if (w0 == NONE) break;
+        const uint32_t w1 = w0 + (uint32_t)ws;
         for (int i = threadIdx.x; i < kWin / 32; i += kCT) bitmap[i] = 0;
-        if (threadIdx.x < 3) s_cursor_add[threadIdx.x] = 0;
+        if (threadIdx.x < 3) s_add[threadIdx.x] = 0;
+        // independent loads first (memory-level parallelism), then the tests
+        uint32_t id[3][KMAX];
+#pragma unroll
+        for (int s = 0; s < 3; ++s)
+#pragma unroll
+            for (int k = 0; k < KMAX; ++k) {
+                int64_t idx = cur[s] + k * kCT + threadIdx.x;
+                id[s][k] = (k * kCT < ws && idx < end[s]) ? ids[s][idx] : NONE;
+            }
+        int4 rc[2][KMAX];
+#pragma unroll
+        for (int s = 1; s < 3; ++s)
+#pragma unroll
+            for (int k = 0; k < KMAX; ++k)
+                if (id[s][k] < w1) rc[s - 1][k] = P.R.rect[id[s][k]];
         __syncthreads();
-        // scan the three streams for ids inside [w0, w1)
 #pragma unroll
         for (int s = 0; s < 3; ++s) {
-            const uint32_t *ids = s == 0 ? P.f_ids : (s == 1 ? P.s_ids : P.g_ids);
-            int64_t cur = s == 0 ? fc : (s == 1 ? sc : gc);
-            int64_t end = s == 0 ? fe : (s == 1 ? se : ge);
-            int cnt = 0;
-            for (int k = 0; k < kWin / kCT; ++k) {
-                int64_t idx = cur + k * kCT + threadIdx.x;
-                if (cur + k * kCT >= end) break;
-                if (idx < end) {
-                    uint32_t id = ids[idx];
-                    if (id < w1) {
-                        ++cnt;
-                        bool cover = true;
-                        if (s != 0) {
-                            int4 rc = P.R.rect[id];
-                            cover = tx >= rc.x && tx <= rc.y && ty >= rc.z && ty <= rc.w;
-                        }
-                        if (cover) atomicOr(&bitmap[(id - w0) >> 5], 1u << ((id - w0) & 31));
-                    }
+            uint32_t cnt = 0;
+#pragma unroll
+            for (int k = 0; k < KMAX; ++k) {
+                uint32_t r = id[s][k];
+                if (r >= w1) continue;
+                ++cnt;
+                bool cover = true;
+                if (s) {
+                    int4 q = rc[s - 1][k];
+                    cover = tx >= q.x && tx <= q.y && ty >= q.z && ty <= q.w;
                 }
+                if (cover) atomicOr(&bitmap[(r - w0) >> 5], 1u << ((r - w0) & 31));
             }
-            if (cnt) atomicAdd(&s_cursor_add[s], (uint32_t)cnt);
+            if (cnt) atomicAdd(&s_add[s], cnt);
         }
         __syncthreads();
-        fc += s_cursor_add[0];
-        sc += s_cursor_add[1];
-        gc += s_cursor_add[2];
-        // ordered compaction of the bitmap (warp 0; 64 words -> 2 per lane)
+#pragma unroll
+        for (int s = 0; s < 3; ++s) cur[s] += s_add[s];
+        // ordered compaction of the bitmap by warp 0 (2 words per lane)
         if (threadIdx.x < 32) {
-            int lane = threadIdx.x;
-            uint32_t wa = bitmap[2 * lane], wb = bitmap[2 * lane + 1];
+            const int lane = threadIdx.x;
+            const int nw = ws / 32;
+            uint32_t wa = 2 * lane < nw ? bitmap[2 * lane] : 0u;
+            uint32_t wb = 2 * lane + 1 < nw ? bitmap[2 * lane + 1] : 0u;
             int ca = __popc(wa), cb = __popc(wb);
             int incl = ca + cb;
             for (int o = 1; o < 32; o <<= 1) {
@@ -480,35 +500,41 @@ __global__ void __launch_bounds__(kCT) k_composite(CompParams P) {
         __syncthreads();
         const int nlist = s_nlist;
         for (int base = 0; base < nlist && !done; base += kCT) {
-            int nb = min(kCT, nlist - base);
+            const int nb = min(kCT, nlist - base);
             if (threadIdx.x < nb) {
-                uint32_t r = list[base + threadIdx.x];
-                r_mx[threadIdx.x] = P.R.mx[r];
-                r_my[threadIdx.x] = P.R.my[r];
-                r_rad[threadIdx.x] = P.R.rad[r];
-                r_ia[threadIdx.x] = P.R.ia[r];
-                r_ib[threadIdx.x] = P.R.ib[r];
-                r_ic[threadIdx.x] = P.R.ic[r];
-                r_op[threadIdx.x] = P.R.op[r];
-                r_start[threadIdx.x] = P.R.start[r];
-                r_count[threadIdx.x] = P.R.count[r];
+                const uint32_t r = list[base + threadIdx.x];
+                const int j = threadIdx.x;
+                const double mx = P.R.mx[r], my = P.R.my[r];
+                const double rad = P.R.rad[r] + 1.0;
+                r_mx[j] = mx;
+                r_my[j] = my;
+                r_rr[j] = rad * rad;
+                r_ia[j] = P.R.ia[r];
+                r_ib[j] = P.R.ib[r];
+                r_ic[j] = P.R.ic[r];
+                r_op[j] = P.R.op[r];
+                r_start[j] = P.R.start[r];
+                r_count[j] = P.R.count[r];
+                // pixel box of forward_kernel (_raster_kernels.py:178-181), clamped to the tile
+                r_x0[j] = (int32_t)fmin(fmax((double)x_lo, ceil(mx - rad)), (double)x_end);
+                r_x1[j] = (int32_t)fmax(fmin((double)(x_end - 1), floor(mx + rad)), (double)(x_lo - 1));
+                r_y0[j] = (int32_t)fmin(fmax((double)y_lo, ceil(my - rad)), (double)y_end);
+                r_y1[j] = (int32_t)fmax(fmin((double)(y_end - 1), floor(my + rad)), (double)(y_lo - 1));
             }
             __syncthreads();
             for (int e = 0; e < nb; ++e) {
-                const double mx = r_mx[e], my = r_my[e];
-                const double rad = r_rad[e] + 1.0, rr = rad * rad;
-                const double fx0 = fmax((double)x_lo, ceil(mx - rad));
-                const double fx1 = fmin((double)(x_end - 1), floor(mx + rad));
-                const double fy0 = fmax((double)y_lo, ceil(my - rad));
-                const double fy1 = fmin((double)(y_end - 1), floor(my + rad));
+                if (term && e && (e & 31) == 0 && __syncthreads_and(saturated())) {
+                    done = true;
+                    break;
+                }
 #pragma unroll
                 for (int k = 0; k < NPIX; ++k) {
                     if (!valid[k]) continue;
-                    const double px = (double)pxs[k], py = (double)pys[k];
-                    if (px < fx0 || px > fx1 || py < fy0 || py > fy1) continue;
-                    if (P.terminate && T[k] < kCutoff) continue;
-                    const double dx = px - mx, dy = py - my;
-                    if (dx * dx + dy * dy > rr) continue;
+                    if (term && T[k] < kCutoff) continue;
+                    if (pxs[k] < r_x0[e] || pxs[k] > r_x1[e] || pys[k] < r_y0[e] || pys[k] > r_y1[e])
+                        continue;
+                    const double dx = (double)pxs[k] - r_mx[e], dy = (double)pys[k] - r_my[e];
+                    if (dx * dx + dy * dy > r_rr[e]) continue;
                     const double q = r_ia[e] * dx * dx + 2.0 * r_ib[e] * dx * dy + r_ic[e] * dy * dy;
                     double alpha = r_op[e] * exp(-0.5 * q);
                     if (alpha > P.alpha_max) alpha = P.alpha_max;
@@ -516,7 +542,7 @@ __global__ void __launch_bounds__(kCT) k_composite(CompParams P) {
                     const double om = 1.0 - alpha;
                     const int32_t b0 = r_start[e], b1 = b0 + r_count[e];
                     for (int32_t j = b0; j < b1; ++j) {
-                        if (P.terminate && T[k] < kCutoff) break;
+                        if (term && T[k] < kCutoff) break;
                         const uint32_t i = P.src[j];
                         const double w = T[k] * alpha;
                         if (want_rgb) {
@@ -539,22 +565,17 @@ __global__ void __launch_bounds__(kCT) k_composite(CompParams P) {
                     }
                 }
             }
-            if (P.terminate) {
-                int mine = 1;
-#pragma unroll
-                for (int k = 0; k < NPIX; ++k)
-                    if (valid[k] && !(T[k] < kCutoff)) mine = 0;
-                done = __syncthreads_and(mine);
-            } else {
-                __syncthreads();
-            }
+            if (done) break;
+            if (term) done = __syncthreads_and(saturated());
+            else __syncthreads();
         }
+        ws = min(ws * 2, kWin);
     }
     // planes (rasterizer.py:140-149; FrameBuffer clips T to [0,1])
 #pragma unroll
     for (int k = 0; k < NPIX; ++k) {
         if (!valid[k]) continue;
-        const int64_t pix = pys[k] * P.W + pxs[k];
+        const int64_t pix = (int64_t)pys[k] * P.W + pxs[k];
         if (P.rgb) {
             P.rgb[3 * pix + 0] = (float)(c0[k] + T[k] * P.bg[0]);
             P.rgb[3 * pix + 1] = (float)(c1[k] + T[k] * P.bg[1]);

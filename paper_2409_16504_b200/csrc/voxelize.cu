@@ -29,40 +29,39 @@ __global__ void k_bbox_init(unsigned long long *mm) {
     else if (t < 6) mm[t] = 0ull;
 }
 
-__global__ void k_bbox(const double *__restrict__ pos, int64_t n, unsigned long long *mm) {
-    unsigned long long lo[3] = {~0ull, ~0ull, ~0ull}, hi[3] = {0, 0, 0};
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
-         i += (int64_t)gridDim.x * blockDim.x) {
-#pragma unroll
-        for (int a = 0; a < 3; ++a) {
-            unsigned long long u = ord_bits(pos[3 * i + a]);
-            lo[a] = u < lo[a] ? u : lo[a];
-            hi[a] = u > hi[a] ? u : hi[a];
-        }
+// Flat, coalesced grid-stride pass over the (n,3) array; the total thread
+// count is a multiple of 3 so each thread always sees the same axis. Shared
+// atomics combine a block, then one global atomic per value per block.
+constexpr int kBBoxThreads = 192;
+__global__ void __launch_bounds__(kBBoxThreads) k_bbox(const double *__restrict__ pos, int64_t n,
+                                                       unsigned long long *mm) {
+    __shared__ unsigned long long s_mm[6];
+    if (threadIdx.x < 3) s_mm[threadIdx.x] = ~0ull;
+    else if (threadIdx.x < 6) s_mm[threadIdx.x] = 0ull;
+    __syncthreads();
+    const int64_t total = 3 * n;
+    const int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    const int axis = (int)(g % 3);
+    unsigned long long lo = ~0ull, hi = 0ull;
+    for (int64_t j = g; j < total; j += stride) {
+        unsigned long long u = ord_bits(pos[j]);
+        lo = u < lo ? u : lo;
+        hi = u > hi ? u : hi;
     }
-#pragma unroll
-    for (int a = 0; a < 3; ++a) {
-        for (int o = 16; o; o >>= 1) {
-            unsigned long long l2 = __shfl_xor_sync(0xffffffffu, lo[a], o);
-            unsigned long long h2 = __shfl_xor_sync(0xffffffffu, hi[a], o);
-            lo[a] = l2 < lo[a] ? l2 : lo[a];
-            hi[a] = h2 > hi[a] ? h2 : hi[a];
-        }
-    }
-    if ((threadIdx.x & 31) == 0) {
-#pragma unroll
-        for (int a = 0; a < 3; ++a) {
-            atomicMin(&mm[a], lo[a]);
-            atomicMax(&mm[3 + a], hi[a]);
-        }
-    }
+    atomicMin(&s_mm[axis], lo);
+    atomicMax(&s_mm[3 + axis], hi);
+    __syncthreads();
+    if (threadIdx.x < 3) atomicMin(&mm[threadIdx.x], s_mm[threadIdx.x]);
+    else if (threadIdx.x < 6) atomicMax(&mm[threadIdx.x], s_mm[threadIdx.x]);
 }
 
 void bbox_run(sfb_ctx *ctx, const double *pos, int64_t n, double *lo_hi_host) {
     SFB_REQUIRE(n > 0, "empty cloud has no bbox");
     auto *mm = ctx->arena.alloc<unsigned long long>(6);
     k_bbox_init<<<1, 32, 0, ctx->stream>>>(mm);
-    k_bbox<<<grid_for(n, 256, ctx->num_sms * 8), 256, 0, ctx->stream>>>(pos, n, mm);
+    k_bbox<<<grid_for(3 * n, kBBoxThreads, ctx->num_sms * 4), kBBoxThreads, 0, ctx->stream>>>(
+        pos, n, mm);
     SFB_CHECK_LAUNCH();
     ctx->read_back(mm, 6 * sizeof(unsigned long long));
     for (int a = 0; a < 6; ++a) lo_hi_host[a] = unord_bits((unsigned long long)ctx->pinned[a]);
@@ -120,26 +119,37 @@ __global__ void k_segments(const K *__restrict__ keys, const uint32_t *__restric
     }
 }
 
-// One thread per voxel: ordered float64 sums over its points (ascending index).
+// One warp per voxel: lanes fetch 32 of the voxel's points at a time (in
+// ascending point index, the CSR order), lane 0 then adds them strictly in
+// that order — bit-identical to np.add.at, with the loads in parallel.
 __global__ void k_voxel_feats(const double *__restrict__ pos, const double *__restrict__ col,
                               const int32_t *__restrict__ order, const int32_t *__restrict__ offsets,
                               const int32_t *__restrict__ coords, int64_t m, double s,
                               double *__restrict__ feats) {
-    int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    const int64_t v = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
     if (v >= m) return;
-    int32_t b = offsets[v], e = offsets[v + 1];
-    double c0 = 0.0, c1 = 0.0, c2 = 0.0, r0 = 0.0, r1 = 0.0, r2 = 0.0;
-    for (int32_t j = b; j < e; ++j) {
-        int64_t i = order[j];
-        c0 = __dadd_rn(c0, __dmul_rn(pos[3 * i + 0], s));
-        c1 = __dadd_rn(c1, __dmul_rn(pos[3 * i + 1], s));
-        c2 = __dadd_rn(c2, __dmul_rn(pos[3 * i + 2], s));
-        r0 = __dadd_rn(r0, col[3 * i + 0]);
-        r1 = __dadd_rn(r1, col[3 * i + 1]);
-        r2 = __dadd_rn(r2, col[3 * i + 2]);
+    const int32_t b = offsets[v], e = offsets[v + 1];
+    double acc[6] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+    for (int32_t j0 = b; j0 < e; j0 += 32) {
+        const int32_t j = j0 + lane;
+        double val[6] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+        if (j < e) {
+            const int64_t i = order[j];
+#pragma unroll
+            for (int a = 0; a < 3; ++a) {
+                val[a] = __dmul_rn(pos[3 * i + a], s);
+                val[3 + a] = col[3 * i + a];
+            }
+        }
+        const int cnt = min(32, e - j0);
+        for (int q = 0; q < cnt; ++q)
+#pragma unroll
+            for (int a = 0; a < 6; ++a) acc[a] = __dadd_rn(acc[a], __shfl_sync(0xffffffffu, val[a], q));
     }
+    if (lane != 0) return;
     double cnt = (double)(e - b);
-    double cen[3] = {__ddiv_rn(c0, cnt), __ddiv_rn(c1, cnt), __ddiv_rn(c2, cnt)};
+    double cen[3] = {__ddiv_rn(acc[0], cnt), __ddiv_rn(acc[1], cnt), __ddiv_rn(acc[2], cnt)};
     double *f = feats + 9 * v;
 #pragma unroll
     for (int a = 0; a < 3; ++a) {
@@ -147,10 +157,8 @@ __global__ void k_voxel_feats(const double *__restrict__ pos, const double *__re
         res = fmin(fmax(res, -0.5), 0.5);
         f[a] = __ddiv_rn(cen[a], s);
         f[6 + a] = res;
+        f[3 + a] = __ddiv_rn(acc[3 + a], cnt);
     }
-    f[3] = __ddiv_rn(r0, cnt);
-    f[4] = __ddiv_rn(r1, cnt);
-    f[5] = __ddiv_rn(r2, cnt);
 }
 
 template <class K>
@@ -176,8 +184,8 @@ static void voxelize_typed(sfb_ctx *ctx, const double *pos, const double *col, i
     SFB_CHECK_LAUNCH();
     ctx->read_back(incl + (n - 1), sizeof(int32_t));
     out.m = *reinterpret_cast<int32_t *>(ctx->pinned);
-    k_voxel_feats<<<grid_for(out.m, 128), 128, 0, st>>>(pos, col, out.order, out.offsets,
-                                                        out.coords, out.m, s, out.feats);
+    k_voxel_feats<<<grid_for(32 * out.m, 256), 256, 0, st>>>(pos, col, out.order, out.offsets,
+                                                             out.coords, out.m, s, out.feats);
     SFB_CHECK_LAUNCH();
 }
 
