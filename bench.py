@@ -212,11 +212,14 @@ def run_ours(args):
     evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
            for _ in range(args.steps)]
     stage_acc = {}
+    host_s = 0.0
     barrier()
     for i in range(args.steps):
         flush.zero_()
         evs[i][0].record()
+        h0 = time.perf_counter()
         render_frame(dev_cloud, weights, view_of(i), planes, out=out)
+        host_s += time.perf_counter() - h0
         evs[i][1].record()
         for k, v in ctx.stage_times().items():
             stage_acc[k] = stage_acc.get(k, 0.0) + v
@@ -323,6 +326,7 @@ def run_ours(args):
                        "net_arithmetic": "fp32 gather-GEMM, fp64 geometry/compositing"},
             "e2e": e2e, "gpu_launches": launches, "roofline": roof, "cpu_baseline": cpu,
             "clocks": clk, "stages_ms": stage_ms, "stats": st,
+            "host_enqueue_ms_per_step": 1e3 * host_s / args.steps,
         }
         print(json.dumps(line), flush=True)
     if world > 1:

@@ -117,7 +117,7 @@ struct sfb_ctx {
     sfb::Arena arena;
     sfb::Net net;
     sfb::NetLayer adhoc;  // standalone layer for single-layer calls
-    int net_mode = SFB_NET_SIMT_F32;
+    int net_mode = SFB_NET_TC_TF32X3;
     int num_sms = 148;
     std::string last_error;
     sfb_stats stats{};

@@ -36,6 +36,7 @@ constexpr int kSuper = 8;      // tiles per super-tile edge
 constexpr int kSuperMax = 16;  // super tiles per run at the middle level
 constexpr int kWin = 2048;     // rank window of the merge
 constexpr int kCT = 256;       // compositor threads per CTA
+constexpr int kPre = 4;        // staged points per run
 
 struct Cam {
     double r[9], t[3], fx, fy, cx, cy;
@@ -274,13 +275,11 @@ __global__ void k_run_build(const uint32_t *__restrict__ src, int64_t K,
     int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (j >= K) return;
     int32_t r = incl[j] - 1;
+    const bool last = j == K - 1 || incl[j + 1] != incl[j];
+    if (last) R.count[r] = (int32_t)(j + 1);   // end of run r; start subtracted below
     bool head = j == 0 || incl[j - 1] != incl[j];
     if (!head) return;
-    // run length: distance to the next head
-    int64_t e = j + 1;
-    while (e < K && incl[e] == incl[j]) ++e;
     R.start[r] = (int32_t)j;
-    R.count[r] = (int32_t)(e - j);
     uint32_t i = src[j];
     int32_t g = p2g ? p2g[i] : (int32_t)i;
     double a = P.a[g], b = P.b[g], c = P.c[g];
@@ -330,6 +329,7 @@ __global__ void k_emit(Runs R, const int32_t *__restrict__ fpos, const int32_t *
                        uint32_t *__restrict__ glist) {
     int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (r >= R.R) return;
+    R.count[r] -= R.start[r];   // k_run_build stored the run's end
     int lvl = R.level[r];
     int4 t = R.rect[r];
     if (lvl == 0) {
@@ -391,6 +391,11 @@ __global__ void __launch_bounds__(kCT) k_composite(CompParams P) {
     // the current chunk's run records (pixel box precomputed per run)
     __shared__ double r_mx[kCT], r_my[kCT], r_rr[kCT], r_ia[kCT], r_ib[kCT], r_ic[kCT], r_op[kCT];
     __shared__ int32_t r_x0[kCT], r_x1[kCT], r_y0[kCT], r_y1[kCT], r_start[kCT], r_count[kCT];
+    // attributes of each run's first kPre points, staged so the blend loop
+    // does not chase src[] -> colours[] through global memory per pixel
+    extern __shared__ double dyn_smem[];
+    double (*r_col)[3][kCT] = reinterpret_cast<double (*)[3][kCT]>(dyn_smem);
+    double (*r_nrm)[3][kCT] = reinterpret_cast<double (*)[3][kCT]>(dyn_smem + kPre * 3 * kCT);
 
     const int64_t t = blockIdx.x;
     const int64_t tx = t % P.ntx, ty = t / P.ntx;
@@ -513,8 +518,28 @@ __global__ void __launch_bounds__(kCT) k_composite(CompParams P) {
                 r_ib[j] = P.R.ib[r];
                 r_ic[j] = P.R.ic[r];
                 r_op[j] = P.R.op[r];
-                r_start[j] = P.R.start[r];
-                r_count[j] = P.R.count[r];
+                const int32_t st0 = P.R.start[r], cnt0 = P.R.count[r];
+                r_start[j] = st0;
+                r_count[j] = cnt0;
+                uint32_t pi[kPre];
+#pragma unroll
+                for (int q = 0; q < kPre; ++q) pi[q] = q < cnt0 ? P.src[st0 + q] : 0u;
+#pragma unroll
+                for (int q = 0; q < kPre; ++q) {
+                    if (q >= cnt0) break;
+                    if (want_rgb) {
+                        const double *cc = P.colors + 3 * (size_t)pi[q];
+                        r_col[q][0][j] = cc[0];
+                        r_col[q][1][j] = cc[1];
+                        r_col[q][2][j] = cc[2];
+                    }
+                    if (want_n) {
+                        const double *nn = P.normals + 3 * (P.p2g ? (int64_t)P.p2g[pi[q]] : (int64_t)pi[q]);
+                        r_nrm[q][0][j] = nn[0];
+                        r_nrm[q][1][j] = nn[1];
+                        r_nrm[q][2][j] = nn[2];
+                    }
+                }
                 // pixel box of forward_kernel (_raster_kernels.py:178-181), clamped to the tile
                 r_x0[j] = (int32_t)fmin(fmax((double)x_lo, ceil(mx - rad)), (double)x_end);
                 r_x1[j] = (int32_t)fmax(fmin((double)(x_end - 1), floor(mx + rad)), (double)(x_lo - 1));
@@ -543,23 +568,41 @@ __global__ void __launch_bounds__(kCT) k_composite(CompParams P) {
                     const int32_t b0 = r_start[e], b1 = b0 + r_count[e];
                     for (int32_t j = b0; j < b1; ++j) {
                         if (term && T[k] < kCutoff) break;
-                        const uint32_t i = P.src[j];
+                        const int q = j - b0;
                         const double w = T[k] * alpha;
-                        if (want_rgb) {
-                            const double *cc = P.colors + 3 * (size_t)i;
-                            c0[k] = c0[k] + w * cc[0];
-                            c1[k] = c1[k] + w * cc[1];
-                            c2[k] = c2[k] + w * cc[2];
-                        }
-                        if (want_n || want_d) {
-                            const int64_t g = P.p2g ? P.p2g[i] : (int64_t)i;
-                            if (want_n) {
-                                const double *nn = P.normals + 3 * g;
-                                n0[k] = n0[k] + w * nn[0];
-                                n1[k] = n1[k] + w * nn[1];
-                                n2[k] = n2[k] + w * nn[2];
+                        if (q < kPre) {
+                            if (want_rgb) {
+                                c0[k] = c0[k] + w * r_col[q][0][e];
+                                c1[k] = c1[k] + w * r_col[q][1][e];
+                                c2[k] = c2[k] + w * r_col[q][2][e];
                             }
-                            if (want_d) dd[k] = dd[k] + w * P.gdepth[g];
+                            if (want_n) {
+                                n0[k] = n0[k] + w * r_nrm[q][0][e];
+                                n1[k] = n1[k] + w * r_nrm[q][1][e];
+                                n2[k] = n2[k] + w * r_nrm[q][2][e];
+                            }
+                            if (want_d) {
+                                const uint32_t i = P.src[j];
+                                dd[k] = dd[k] + w * P.gdepth[P.p2g ? P.p2g[i] : (int64_t)i];
+                            }
+                        } else {
+                            const uint32_t i = P.src[j];
+                            if (want_rgb) {
+                                const double *cc = P.colors + 3 * (size_t)i;
+                                c0[k] = c0[k] + w * cc[0];
+                                c1[k] = c1[k] + w * cc[1];
+                                c2[k] = c2[k] + w * cc[2];
+                            }
+                            if (want_n || want_d) {
+                                const int64_t g = P.p2g ? P.p2g[i] : (int64_t)i;
+                                if (want_n) {
+                                    const double *nn = P.normals + 3 * g;
+                                    n0[k] = n0[k] + w * nn[0];
+                                    n1[k] = n1[k] + w * nn[1];
+                                    n2[k] = n2[k] + w * nn[2];
+                                }
+                                if (want_d) dd[k] = dd[k] + w * P.gdepth[g];
+                            }
                         }
                         T[k] = T[k] * om;
                     }
@@ -733,8 +776,15 @@ void render_run(sfb_ctx *ctx, const RenderInputs &in, const sfb_camera &cam,
     C.depth = (plane_mask & SFB_PLANE_DEPTH) ? depth : nullptr;
     C.trans = trans;
     int64_t ntiles = ntx * nty;
-    if (TS * TS <= kCT) k_composite<1><<<(unsigned)ntiles, kCT, 0, st>>>(C);
-    else k_composite<4><<<(unsigned)ntiles, kCT, 0, st>>>(C);
+    const size_t dyn = sizeof(double) * 2 * kPre * 3 * kCT;
+    static bool attr = false;
+    if (!attr) {
+        SFB_CUDA(cudaFuncSetAttribute(k_composite<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn));
+        SFB_CUDA(cudaFuncSetAttribute(k_composite<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn));
+        attr = true;
+    }
+    if (TS * TS <= kCT) k_composite<1><<<(unsigned)ntiles, kCT, dyn, st>>>(C);
+    else k_composite<4><<<(unsigned)ntiles, kCT, dyn, st>>>(C);
     SFB_CHECK_LAUNCH();
     ctx->mark(ST_COMPOSITE);
 }

@@ -24,7 +24,7 @@ MODES = {"simt_f32": _lib.NET_SIMT_F32, "tc_tf32x3": _lib.NET_TC_TF32X3}
 
 
 def set_mode(mode: str) -> None:
-    """Select the conv arithmetic: 'simt_f32' (FFMA) or 'tc_tf32x3' (tcgen05)."""
+    """Select the conv arithmetic: 'tc_tf32x3' (tcgen05, the default) or 'simt_f32' (FFMA)."""
     if mode not in MODES:
         raise ValueError(f"unknown network mode {mode!r}; expected one of {tuple(MODES)}")
     ctx = _lib.context()

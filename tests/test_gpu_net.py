@@ -33,7 +33,7 @@ def raw_close(got, ref):
 def mode(request):
     sparsenet.set_mode(request.param)
     yield request.param
-    sparsenet.set_mode("simt_f32")
+    sparsenet.set_mode("tc_tf32x3")
 
 
 def test_config1_raw_head_vs_reference_golden(c1_arrays, mode):
