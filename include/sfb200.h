@@ -81,6 +81,9 @@ int sfb_version(void);
  * 1 voxelize, 2 unet, 3 head, 4 project, 5 depth sort, 6 runs+binning,
  * 7 composite. Synchronises on the recorded events. */
 int sfb_set_timing(sfb_ctx *ctx, int on);
+/* CUDA-graph replay of sfb_frame (default on): the first call of a shape runs
+ * eagerly, the second captures, later calls update parameters and replay. */
+int sfb_set_graphs(sfb_ctx *ctx, int on);
 int sfb_stage_times(sfb_ctx *ctx, int32_t *stage_ids, float *ms, int32_t cap, int32_t *n_out);
 
 /* ---- voxelization (voxelgrid.py:125-168, voxelize_adaptive) ------------- */

@@ -1,9 +1,22 @@
 // C ABI of libsfb200 (declared in include/sfb200.h): argument checks, error
 // codes, arena reset per call, and the fused pipelines built from the stages
-// in voxelize.cu / hashmap.cu / net.cu / render.cu.
+// in voxelize.cu / hashmap.cu / net.cu / conv_tc.cu / render.cu.
+//
+// Every stage keeps its data-dependent sizes in a DevCounts block on the
+// device, so a call is a pure stream of kernels. sfb_frame replays the whole
+// cloud -> P2ENet -> planes sequence as one CUDA graph: the first call with a
+// new shape runs eagerly (growing the arena), the second captures, later
+// calls update the parameter kernel node (lattice scale, key layout, camera,
+// background) and launch the graph.
+#include <algorithm>
+
 #include "common.cuh"
 
 using namespace sfb;
+
+namespace sfb {
+const void *write_params_func();
+}
 
 namespace {
 
@@ -27,32 +40,52 @@ int guard(sfb_ctx *ctx, F &&f) {
     }
 }
 
+DevCounts *new_counts(sfb_ctx *ctx) {
+    DevCounts *C = ctx->arena.alloc<DevCounts>(1);
+    SFB_CUDA(cudaMemsetAsync(C, 0, sizeof(DevCounts), ctx->stream));
+    ctx->last_counts = C;
+    return C;
+}
+
+FrameParams *params(sfb_ctx *ctx, const FrameParams &host) {
+    FrameParams *P = ctx->arena.alloc<FrameParams>(1);
+    write_params(ctx, host, P);
+    return P;
+}
+
+FrameParams camera_params(const sfb_camera *cam, const double *bg) {
+    FrameParams P{};
+    if (cam) P.cam = to_cam(*cam);
+    for (int a = 0; a < 3; ++a) P.bg[a] = bg ? bg[a] : 0.0;
+    return P;
+}
+
 __global__ void k_expand_splats(const int32_t *__restrict__ p2v, int64_t n,
                                 const double *__restrict__ vc, const double *__restrict__ vs,
                                 const double *__restrict__ vq, const double *__restrict__ vo,
                                 const double *__restrict__ vn, const double *__restrict__ col,
                                 double *centers, double *scales, double *quats, double *opac,
                                 double *colors, double *normals) {
-    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (i >= n) return;
-    int64_t v = p2v[i];
-    for (int a = 0; a < 3; ++a) {
-        centers[3 * i + a] = vc[3 * v + a];
-        scales[3 * i + a] = vs[3 * v + a];
-        normals[3 * i + a] = vn[3 * v + a];
-        if (colors) colors[3 * i + a] = col[3 * i + a];
+    SFB_FOR(i, n) {
+        const int64_t v = p2v[i];
+        for (int a = 0; a < 3; ++a) {
+            centers[3 * i + a] = vc[3 * v + a];
+            scales[3 * i + a] = vs[3 * v + a];
+            normals[3 * i + a] = vn[3 * v + a];
+            if (colors) colors[3 * i + a] = col[3 * i + a];
+        }
+        for (int a = 0; a < 4; ++a) quats[4 * i + a] = vq[4 * v + a];
+        opac[i] = vo[v];
     }
-    for (int a = 0; a < 4; ++a) quats[4 * i + a] = vq[4 * v + a];
-    opac[i] = vo[v];
 }
 
 __global__ void k_tap_transpose(const int32_t *__restrict__ tm, int64_t m, int taps,
                                 int32_t *__restrict__ out) {
-    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (i >= m * taps) return;
-    int64_t r = i / taps;
-    int t = (int)(i % taps);
-    out[i] = tm[(int64_t)t * m + r];
+    SFB_FOR(i, m * taps) {
+        const int64_t r = i / taps;
+        const int t = (int)(i % taps);
+        out[i] = tm[(int64_t)t * m + r];
+    }
 }
 
 struct VoxelSplats {
@@ -60,8 +93,9 @@ struct VoxelSplats {
     double *c, *s, *q, *o, *n;
 };
 
-VoxelSplats neural_voxels(sfb_ctx *ctx, const double *pos, const double *col, int64_t n, double s,
-                          const double *lo_hi) {
+// voxelize -> UNet -> head -> per-voxel Gaussians, all device-sized (bound n)
+VoxelSplats neural_voxels(sfb_ctx *ctx, const double *pos, const double *col, int64_t n,
+                          const FrameParams &host, const FrameParams *P, DevCounts *C) {
     SFB_REQUIRE(ctx->net.loaded, "network weights are not loaded");
     SFB_REQUIRE(ctx->net.enc[0] == 9, "input grid has 9 channels, plan expects " +
                                           std::to_string(ctx->net.enc[0]));
@@ -73,28 +107,82 @@ VoxelSplats neural_voxels(sfb_ctx *ctx, const double *pos, const double *col, in
     o.p2v = ctx->arena.alloc<int32_t>(n);
     o.order = ctx->arena.alloc<int32_t>(n);
     o.offsets = ctx->arena.alloc<int32_t>(n + 1);
-    voxelize_run(ctx, pos, col, n, s, lo_hi, o);
+    voxelize_run(ctx, pos, col, n, host, P, o, C);
     ctx->mark(ST_VOXELIZE);
-    int64_t m = o.m;
-    float *raw = ctx->arena.alloc<float>(14 * m);
-    unet_run(ctx, o.coords, o.feats, m, raw);
+    float *raw = ctx->arena.alloc<float>(14 * n);
+    unet_run(ctx, o.coords, o.feats, n, host, P, C, raw);
     ctx->mark(ST_UNET);
-    double *blk = ctx->arena.alloc<double>(14 * m);
+    double *blk = ctx->arena.alloc<double>(14 * n);
     V.c = blk;
-    V.s = blk + 3 * m;
-    V.q = blk + 6 * m;
-    V.o = blk + 10 * m;
-    V.n = blk + 11 * m;
-    head_to_voxel_splats(ctx, raw, o.coords, o.feats, m, 1.0 / s, V.c, V.s, V.q, V.o, V.n);
+    V.s = blk + 3 * n;
+    V.q = blk + 6 * n;
+    V.o = blk + 10 * n;
+    V.n = blk + 11 * n;
+    head_to_voxel_splats(ctx, raw, o.coords, o.feats, &C->m[0], n, P, V.c, V.s, V.q, V.o, V.n);
     ctx->mark(ST_HEAD);
     return V;
 }
 
+RenderInputs splat_inputs(const sfb_splats *s) {
+    RenderInputs in{};
+    in.centers = s->centers;
+    in.scales = s->scales;
+    in.quats = s->quaternions;
+    in.opac = s->opacities;
+    in.n_geom = s->n;
+    in.d_n_geom = nullptr;
+    in.colors = s->colors;
+    in.normals = s->normals;
+    in.n_points = s->n;
+    return in;
+}
+
+// enqueue the fused frame (eager or under capture)
+void enqueue_frame(sfb_ctx *ctx, const double *pos, const double *col, int64_t n,
+                   const FrameParams &host, FrameParams *P, const sfb_camera *cam,
+                   const sfb_render_options *opts, int mask, float *rgb, float *normal,
+                   float *depth, float *trans) {
+    write_params(ctx, host, P);
+    DevCounts *C = new_counts(ctx);
+    VoxelSplats V = neural_voxels(ctx, pos, col, n, host, P, C);
+    RenderInputs in{};
+    in.centers = V.c;
+    in.scales = V.s;
+    in.quats = V.q;
+    in.opac = V.o;
+    in.n_geom = n;
+    in.d_n_geom = &C->m[0];
+    in.point_to_geom = V.vox.p2v;
+    in.colors = col;
+    in.normals = V.n;
+    in.n_points = n;
+    render_run(ctx, in, P, cam->width, cam->height, *opts, mask, C, rgb, normal, depth, trans);
+}
+
 }  // namespace
+
+struct sfb_frame_graph {
+    // shape key: everything baked into the kernels' launch configuration
+    int64_t n;
+    int32_t width, height, tile, terminate, mask, key_bits;
+    double alpha_max;
+    const void *ptrs[6];
+    int net_mode;
+    uint64_t net_epoch;
+    int seen = 0;                     // eager runs with this key
+    cudaGraphExec_t exec = nullptr;
+    cudaGraph_t graph = nullptr;
+    cudaGraphNode_t param_node = nullptr;
+    FrameParams *dev_params = nullptr;
+    ~sfb_frame_graph() {
+        if (exec) cudaGraphExecDestroy(exec);
+        if (graph) cudaGraphDestroy(graph);
+    }
+};
 
 extern "C" {
 
-int sfb_version(void) { return 1; }
+int sfb_version(void) { return 2; }
 
 int sfb_ctx_create(int device, sfb_ctx **out) {
     if (!out) return SFB_ERR_ARG;
@@ -104,7 +192,9 @@ int sfb_ctx_create(int device, sfb_ctx **out) {
     ctx->device = device;
     if (cudaSetDevice(device) != cudaSuccess ||
         cudaDeviceGetAttribute(&ctx->num_sms, cudaDevAttrMultiProcessorCount, device) != cudaSuccess ||
-        cudaMallocHost(&ctx->pinned, 4096) != cudaSuccess) {
+        cudaMallocHost(&ctx->pinned, 4096) != cudaSuccess ||
+        cudaStreamCreateWithFlags(&ctx->capture_stream, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaEventCreateWithFlags(&ctx->fork_event, cudaEventDisableTiming) != cudaSuccess) {
         delete ctx;
         return SFB_ERR_CUDA;
     }
@@ -115,7 +205,9 @@ int sfb_ctx_create(int device, sfb_ctx **out) {
 int sfb_ctx_destroy(sfb_ctx *ctx) {
     if (!ctx) return SFB_ERR_ARG;
     cudaSetDevice(ctx->device);
-    if (ctx->stream) cudaStreamSynchronize(ctx->stream);
+    cudaDeviceSynchronize();
+    for (auto *g : ctx->graphs) delete g;
+    ctx->graphs.clear();
     delete ctx;
     return SFB_OK;
 }
@@ -131,6 +223,12 @@ int sfb_set_stream(sfb_ctx *ctx, void *stream) {
 int sfb_set_timing(sfb_ctx *ctx, int on) {
     if (!ctx) return SFB_ERR_ARG;
     ctx->timing = on != 0;
+    return SFB_OK;
+}
+
+int sfb_set_graphs(sfb_ctx *ctx, int on) {
+    if (!ctx) return SFB_ERR_ARG;
+    ctx->use_graphs = on != 0;
     return SFB_OK;
 }
 
@@ -151,6 +249,17 @@ int sfb_stage_times(sfb_ctx *ctx, int32_t *stage_ids, float *ms, int32_t cap, in
 
 int sfb_get_stats(sfb_ctx *ctx, sfb_stats *out) {
     if (!ctx || !out) return SFB_ERR_ARG;
+    if (ctx->last_counts) {
+        DevCounts c{};
+        if (cudaMemcpy(&c, ctx->last_counts, sizeof(c), cudaMemcpyDeviceToHost) != cudaSuccess)
+            return SFB_ERR_CUDA;
+        ctx->stats.kept = c.kept;
+        ctx->stats.runs = c.runs;
+        ctx->stats.fine_entries = c.ef;
+        ctx->stats.super_entries = c.es;
+        ctx->stats.global_entries = c.g;
+        for (int l = 0; l < 8; ++l) ctx->stats.voxels[l] = c.m[l];
+    }
     *out = ctx->stats;
     return SFB_OK;
 }
@@ -163,9 +272,14 @@ int sfb_voxelize(sfb_ctx *ctx, const double *positions, const double *colors, in
                  const double *lo_hi_host, int32_t *coords, double *feats, int64_t *keys,
                  int32_t *p2v, int32_t *order, int32_t *offsets, int64_t *m_host) {
     return guard(ctx, [&] {
-        VoxelOut o{coords, feats, keys, p2v, order, offsets, 0};
-        voxelize_run(ctx, positions, colors, n, s, lo_hi_host, o);
-        *m_host = o.m;
+        FrameParams host{};
+        voxel_layout(lo_hi_host, s, host);
+        FrameParams *P = params(ctx, host);
+        DevCounts *C = new_counts(ctx);
+        VoxelOut o{coords, feats, keys, p2v, order, offsets};
+        voxelize_run(ctx, positions, colors, n, host, P, o, C);
+        ctx->read_back(&C->m[0], sizeof(int64_t));
+        *m_host = ctx->pinned[0];
     });
 }
 
@@ -174,15 +288,13 @@ int sfb_kernel_map(sfb_ctx *ctx, const int32_t *coords, int64_t m, int32_t strid
     return guard(ctx, [&] {
         SFB_REQUIRE(kernel >= 1 && (kernel & 1), "conv kernels must be odd");
         SFB_REQUIRE(stride >= 1, "stride must be positive");
-        HashTable h = hash_build(ctx, coords, m);
-        int taps = kernel * kernel * kernel;
-        int32_t *tm = ctx->arena.alloc<int32_t>((size_t)taps * (m > 0 ? m : 1));
-        kernel_map_build(ctx, h, coords, m, stride, kernel, tm);
-        // (taps, m) -> (m, taps) for the caller
-        if (m > 0) {
-            k_tap_transpose<<<grid_for(m * taps, 256), 256, 0, ctx->stream>>>(tm, m, taps, map_out);
-            SFB_CHECK_LAUNCH();
-        }
+        if (m == 0) return;
+        HashTable h = hash_build(ctx, coords, nullptr, m);
+        const int taps = kernel * kernel * kernel;
+        int32_t *tm = ctx->arena.alloc<int32_t>((size_t)taps * m);
+        kernel_map_build(ctx, h, coords, nullptr, m, stride, kernel, tm);
+        k_tap_transpose<<<dgrid(m * taps, 256), 256, 0, ctx->stream>>>(tm, m, taps, map_out);
+        SFB_CHECK_LAUNCH();
     });
 }
 
@@ -192,8 +304,9 @@ int sfb_transposed_map(sfb_ctx *ctx, const int32_t *parent_coords, int64_t m_par
     return guard(ctx, [&] {
         SFB_REQUIRE(parent_stride >= 2 && (parent_stride & (parent_stride - 1)) == 0,
                     "transposed conv needs a stride >= 2 grid to subdivide");
-        HashTable h = hash_build(ctx, parent_coords, m_parent);
-        transposed_lookup(ctx, h, parent_stride, targets, m_targets, parent_out, tap_out);
+        if (m_targets == 0) return;
+        HashTable h = hash_build(ctx, parent_coords, nullptr, m_parent);
+        transposed_lookup(ctx, h, parent_stride, targets, nullptr, m_targets, parent_out, tap_out);
     });
 }
 
@@ -201,13 +314,25 @@ int sfb_pool(sfb_ctx *ctx, const int32_t *coords, const float *feats, int64_t m,
              int32_t stride, int32_t *parent_coords, float *parent_feats, int32_t *c2p,
              int64_t *m_parent_host) {
     return guard(ctx, [&] {
-        *m_parent_host = pool_build(ctx, coords, m, stride, feats, c, c, parent_coords,
-                                    parent_feats, c, c2p);
+        FrameParams host{};
+        coords_layout(ctx, coords, m, host);
+        FrameParams *P = params(ctx, host);
+        DevCounts *C = new_counts(ctx);
+        *reinterpret_cast<int64_t *>(ctx->pinned) = m;
+        SFB_CUDA(cudaMemcpyAsync(&C->m[0], ctx->pinned, sizeof(int64_t), cudaMemcpyHostToDevice,
+                                 ctx->stream));
+        pool_build(ctx, coords, &C->m[0], m, stride, host, P, feats, c, c, parent_coords,
+                   parent_feats, c, c2p, &C->m[1]);
+        ctx->read_back(&C->m[1], sizeof(int64_t));
+        *m_parent_host = ctx->pinned[0];
     });
 }
 
 int sfb_net_load(sfb_ctx *ctx, const void *blob, size_t nbytes) {
-    return guard(ctx, [&] { net_load(ctx, blob, nbytes); });
+    return guard(ctx, [&] {
+        net_load(ctx, blob, nbytes);
+        ++ctx->net_epoch;
+    });
 }
 
 int sfb_net_set_mode(sfb_ctx *ctx, int mode) {
@@ -236,10 +361,11 @@ int sfb_sparse_conv(sfb_ctx *ctx, int layer, const int32_t *coords, const float 
     return guard(ctx, [&] {
         const NetLayer &L = pick_layer(ctx, layer);
         SFB_REQUIRE(L.kind == 0, "expected a conv spec");
-        HashTable h = hash_build(ctx, coords, m);
-        int32_t *nbr = ctx->arena.alloc<int32_t>((size_t)L.taps * (m > 0 ? m : 1));
-        kernel_map_build(ctx, h, coords, m, stride, L.kernel, nbr);
-        conv_layer(ctx, L, feats, L.cin, nbr, m, relu, out, L.cout);
+        if (m == 0) return;
+        HashTable h = hash_build(ctx, coords, nullptr, m);
+        int32_t *nbr = ctx->arena.alloc<int32_t>((size_t)L.taps * m);
+        kernel_map_build(ctx, h, coords, nullptr, m, stride, L.kernel, nbr);
+        conv_layer(ctx, L, feats, L.cin, nbr, m, nullptr, m, relu, out, L.cout);
     });
 }
 
@@ -249,17 +375,29 @@ int sfb_transposed_conv(sfb_ctx *ctx, int layer, const int32_t *parent_coords,
     return guard(ctx, [&] {
         const NetLayer &L = pick_layer(ctx, layer);
         SFB_REQUIRE(L.kind == 1, "expected a transposed_conv spec");
-        HashTable h = hash_build(ctx, parent_coords, m_parent);
-        int32_t *parent = ctx->arena.alloc<int32_t>(m_targets + 1);
-        int32_t *tap = ctx->arena.alloc<int32_t>(m_targets + 1);
-        transposed_lookup(ctx, h, parent_stride, targets, m_targets, parent, tap);
-        tconv_layer(ctx, L, parent_feats, L.cin, parent, tap, m_targets, relu, out, L.cout);
+        if (m_targets == 0) return;
+        HashTable h = hash_build(ctx, parent_coords, nullptr, m_parent);
+        int32_t *parent = ctx->arena.alloc<int32_t>(m_targets);
+        int32_t *tap = ctx->arena.alloc<int32_t>(m_targets);
+        transposed_lookup(ctx, h, parent_stride, targets, nullptr, m_targets, parent, tap);
+        tconv_layer(ctx, L, parent_feats, L.cin, parent, tap, nullptr, m_targets, relu, out, L.cout);
     });
 }
 
 int sfb_unet_forward(sfb_ctx *ctx, const int32_t *coords, const double *feats9, int64_t m0,
                      float *raw_out) {
-    return guard(ctx, [&] { unet_run(ctx, coords, feats9, m0, raw_out); });
+    return guard(ctx, [&] {
+        SFB_REQUIRE(m0 > 0, "empty voxel grid");
+        FrameParams host{};
+        coords_layout(ctx, coords, m0, host);
+        FrameParams *P = params(ctx, host);
+        DevCounts *C = new_counts(ctx);
+        *reinterpret_cast<int64_t *>(ctx->pinned) = m0;
+        SFB_CUDA(cudaMemcpyAsync(&C->m[0], ctx->pinned, sizeof(int64_t), cudaMemcpyHostToDevice,
+                                 ctx->stream));
+        unet_run(ctx, coords, feats9, m0, host, P, C, raw_out);
+        SFB_CUDA(cudaStreamSynchronize(ctx->stream));   // pinned staging reused next call
+    });
 }
 
 int sfb_activate_head(sfb_ctx *ctx, const float *raw, int64_t m, double scale, double *delta,
@@ -272,25 +410,16 @@ int sfb_estimate_neural(sfb_ctx *ctx, const double *positions, const double *col
                         double *quaternions, double *opacities, double *colors_out,
                         double *normals) {
     return guard(ctx, [&] {
-        VoxelSplats V = neural_voxels(ctx, positions, colors, n, s, lo_hi_host);
-        k_expand_splats<<<grid_for(n, 256), 256, 0, ctx->stream>>>(
+        FrameParams host{};
+        voxel_layout(lo_hi_host, s, host);
+        FrameParams *P = params(ctx, host);
+        DevCounts *C = new_counts(ctx);
+        VoxelSplats V = neural_voxels(ctx, positions, colors, n, host, P, C);
+        k_expand_splats<<<dgrid(n, 256), 256, 0, ctx->stream>>>(
             V.vox.p2v, n, V.c, V.s, V.q, V.o, V.n, colors, centers, scales, quaternions, opacities,
             colors_out, normals);
         SFB_CHECK_LAUNCH();
     });
-}
-
-static RenderInputs splat_inputs(const sfb_splats *s) {
-    RenderInputs in{};
-    in.centers = s->centers;
-    in.scales = s->scales;
-    in.quats = s->quaternions;
-    in.opac = s->opacities;
-    in.n_geom = s->n;
-    in.colors = s->colors;
-    in.normals = s->normals;
-    in.n_points = s->n;
-    return in;
 }
 
 int sfb_render(sfb_ctx *ctx, const sfb_splats *splats, const sfb_camera *cam,
@@ -298,7 +427,10 @@ int sfb_render(sfb_ctx *ctx, const sfb_splats *splats, const sfb_camera *cam,
                float *normal, float *depth, float *trans) {
     return guard(ctx, [&] {
         SFB_REQUIRE(splats && cam && opts, "null argument");
-        render_run(ctx, splat_inputs(splats), *cam, *opts, plane_mask, bg, rgb, normal, depth, trans);
+        FrameParams *P = params(ctx, camera_params(cam, bg));
+        DevCounts *C = new_counts(ctx);
+        render_run(ctx, splat_inputs(splats), P, cam->width, cam->height, *opts, plane_mask, C, rgb,
+                   normal, depth, trans);
     });
 }
 
@@ -306,8 +438,9 @@ int sfb_project(sfb_ctx *ctx, const sfb_splats *s, const sfb_camera *cam, double
                 double dilation, double *sx, double *sy, double *depth, double *ca, double *cb,
                 double *cc, double *radius, uint8_t *keep) {
     return guard(ctx, [&] {
-        project_run(ctx, s->centers, s->quaternions, s->scales, s->n, *cam, z_near, dilation, sx,
-                    sy, depth, ca, cb, cc, radius, keep);
+        FrameParams *P = params(ctx, camera_params(cam, nullptr));
+        project_run(ctx, s->centers, s->quaternions, s->scales, nullptr, s->n, P, z_near, dilation,
+                    sx, sy, depth, ca, cb, cc, radius, keep);
     });
 }
 
@@ -316,8 +449,10 @@ int sfb_prepare_debug(sfb_ctx *ctx, const sfb_splats *s, const sfb_camera *cam, 
                       int64_t cap, int64_t *k_host, int64_t *e_host) {
     return guard(ctx, [&] {
         SFB_REQUIRE(tile >= 1, "tile_size must be positive");
-        prepare_debug_run(ctx, splat_inputs(s), *cam, tile, source, radius, offsets, ids, cap,
-                          k_host, e_host);
+        FrameParams *P = params(ctx, camera_params(cam, nullptr));
+        DevCounts *C = new_counts(ctx);
+        prepare_debug_run(ctx, splat_inputs(s), P, cam->width, cam->height, tile, C, source,
+                          radius, offsets, ids, cap, k_host, e_host);
     });
 }
 
@@ -327,18 +462,104 @@ int sfb_frame(sfb_ctx *ctx, const double *positions, const double *colors, int64
               float *trans) {
     return guard(ctx, [&] {
         SFB_REQUIRE(cam && opts, "null argument");
-        VoxelSplats V = neural_voxels(ctx, positions, colors, n, s, lo_hi_host);
-        RenderInputs in{};
-        in.centers = V.c;
-        in.scales = V.s;
-        in.quats = V.q;
-        in.opac = V.o;
-        in.n_geom = V.vox.m;
-        in.point_to_geom = V.vox.p2v;
-        in.colors = colors;
-        in.normals = V.n;
-        in.n_points = n;
-        render_run(ctx, in, *cam, *opts, plane_mask, bg, rgb, normal, depth, trans);
+        SFB_REQUIRE(n >= 2, "voxelization needs at least 2 points");
+        FrameParams host = camera_params(cam, bg);
+        voxel_layout(lo_hi_host, s, host);
+        const int key_bits = host.total <= 32 ? ((host.total + 7) / 8) * 8 : 64;
+        if (!ctx->use_graphs || ctx->timing) {
+            FrameParams *P = ctx->arena.alloc<FrameParams>(1);
+            enqueue_frame(ctx, positions, colors, n, host, P, cam, opts, plane_mask, rgb, normal,
+                          depth, trans);
+            return;
+        }
+        // ---- graph path: find / build the graph of this shape
+        sfb_frame_graph *G = nullptr;
+        const void *ptrs[6] = {positions, colors, rgb, normal, depth, trans};
+        for (auto *g : ctx->graphs)
+            if (g->n == n && g->width == cam->width && g->height == cam->height &&
+                g->tile == opts->tile_size && g->terminate == opts->early_termination &&
+                g->alpha_max == opts->alpha_max && g->mask == plane_mask && g->key_bits == key_bits &&
+                g->net_mode == ctx->net_mode && g->net_epoch == ctx->net_epoch &&
+                std::equal(ptrs, ptrs + 6, g->ptrs))
+                G = g;
+        if (!G) {
+            G = new sfb_frame_graph();
+            G->n = n;
+            G->width = cam->width;
+            G->height = cam->height;
+            G->tile = opts->tile_size;
+            G->terminate = opts->early_termination;
+            G->alpha_max = opts->alpha_max;
+            G->mask = plane_mask;
+            G->key_bits = key_bits;
+            G->net_mode = ctx->net_mode;
+            G->net_epoch = ctx->net_epoch;
+            std::copy(ptrs, ptrs + 6, G->ptrs);
+            if (ctx->graphs.size() >= 8) {
+                delete ctx->graphs.front();
+                ctx->graphs.erase(ctx->graphs.begin());
+            }
+            ctx->graphs.push_back(G);
+        }
+        if (!G->exec && G->seen == 0) {
+            // first call of this shape: eager run (grows the arena, sets kernel attributes)
+            FrameParams *P = ctx->arena.alloc<FrameParams>(1);
+            enqueue_frame(ctx, positions, colors, n, host, P, cam, opts, plane_mask, rgb, normal,
+                          depth, trans);
+            G->seen = 1;
+            return;
+        }
+        if (!G->exec) {
+            // capture on the library's own stream; the caller's stream replays it
+            cudaStream_t user = ctx->stream;
+            SFB_CUDA(cudaStreamSynchronize(user));
+            ctx->stream = ctx->capture_stream;
+            FrameParams *P = ctx->arena.alloc<FrameParams>(1);
+            G->dev_params = P;
+            SFB_CUDA(cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeThreadLocal));
+            try {
+                enqueue_frame(ctx, positions, colors, n, host, P, cam, opts, plane_mask, rgb,
+                              normal, depth, trans);
+            } catch (...) {
+                cudaGraph_t junk = nullptr;
+                cudaStreamEndCapture(ctx->stream, &junk);
+                if (junk) cudaGraphDestroy(junk);
+                ctx->stream = user;
+                throw;
+            }
+            cudaError_t e = cudaStreamEndCapture(ctx->stream, &G->graph);
+            ctx->stream = user;
+            SFB_CUDA(e);
+            SFB_CUDA(cudaGraphInstantiate(&G->exec, G->graph, 0));
+            size_t nn = 0;
+            SFB_CUDA(cudaGraphGetNodes(G->graph, nullptr, &nn));
+            std::vector<cudaGraphNode_t> nodes(nn);
+            SFB_CUDA(cudaGraphGetNodes(G->graph, nodes.data(), &nn));
+            for (auto nd : nodes) {
+                cudaGraphNodeType ty;
+                SFB_CUDA(cudaGraphNodeGetType(nd, &ty));
+                if (ty != cudaGraphNodeTypeKernel) continue;
+                cudaKernelNodeParams kp;
+                SFB_CUDA(cudaGraphKernelNodeGetParams(nd, &kp));
+                if (kp.func == write_params_func()) {
+                    G->param_node = nd;
+                    break;
+                }
+            }
+            SFB_REQUIRE(G->param_node, "frame graph has no parameter node");
+            ctx->graph_nodes = (int64_t)nn;
+        }
+        // replay: new parameters into the first node, then the whole frame
+        cudaKernelNodeParams kp{};
+        FrameParams *dst = G->dev_params;
+        void *args[2] = {&host, &dst};
+        kp.func = const_cast<void *>(write_params_func());
+        kp.gridDim = dim3(1);
+        kp.blockDim = dim3(1);
+        kp.sharedMemBytes = 0;
+        kp.kernelParams = args;
+        SFB_CUDA(cudaGraphExecKernelNodeSetParams(G->exec, G->param_node, &kp));
+        SFB_CUDA(cudaGraphLaunch(G->exec, ctx->stream));
     });
 }
 

@@ -109,7 +109,10 @@ struct Net {
     }
 };
 
+struct DevCounts;
 }  // namespace sfb
+
+struct sfb_frame_graph;
 
 struct sfb_ctx {
     int device = 0;
@@ -118,6 +121,14 @@ struct sfb_ctx {
     sfb::Net net;
     sfb::NetLayer adhoc;  // standalone layer for single-layer calls
     int net_mode = SFB_NET_TC_TF32X3;
+    uint64_t net_epoch = 0;
+    // CUDA graphs of the fused frame, keyed by shape (api.cu)
+    bool use_graphs = true;
+    cudaStream_t capture_stream = nullptr;
+    cudaEvent_t fork_event = nullptr;
+    std::vector<sfb_frame_graph *> graphs;
+    int64_t graph_nodes = 0;
+    sfb::DevCounts *last_counts = nullptr;   // device counts of the last call
     int num_sms = 148;
     std::string last_error;
     sfb_stats stats{};
@@ -142,6 +153,8 @@ struct sfb_ctx {
         if (pinned) cudaFreeHost(pinned);
         for (auto &e : ev)
             if (e) cudaEventDestroy(e);
+        if (capture_stream) cudaStreamDestroy(capture_stream);
+        if (fork_event) cudaEventDestroy(fork_event);
     }
     // read `count` int64 values back from device (one sync)
     void read_back(const void *dev, size_t bytes) {
@@ -183,23 +196,79 @@ __host__ __device__ inline int64_t floor_div(int64_t a, int64_t d) {
     return (a % d != 0 && a < 0) ? q - 1 : q;
 }
 
+// grid-stride loop over a count that may live in device memory
+#define SFB_FOR(i, n)                                                              \
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < (n);    \
+         i += (int64_t)gridDim.x * blockDim.x)
+
+// grid for a grid-stride kernel: enough CTAs for `bound` items, capped
+inline unsigned dgrid(int64_t bound, int block, int per_sm = 8) {
+    int64_t g = (bound + block - 1) / block;
+    int64_t cap = 148 * per_sm;
+    if (g > cap) g = cap;
+    if (g < 1) g = 1;
+    return (unsigned)g;
+}
+
+// Device-resident sizes of one pipeline call (all data-dependent counts).
+struct DevCounts {
+    int64_t n;          // points
+    int64_t m[9];       // voxels per UNet level (m[0] = M0)
+    int64_t kept;       // points surviving the cull
+    int64_t runs;       // depth-ordered runs of identical geometry
+    int64_t runs1;      // runs + 1
+    int64_t ef, es, g;  // fine / super / global pyramid entries
+    int64_t scratch[4];
+};
+
+struct Cam {
+    double r[9], t[3], fx, fy, cx, cy;
+    int64_t w, h;
+};
+Cam to_cam(const sfb_camera &c);
+
+// Per-call parameters that change frame to frame (lattice scale, key layout,
+// camera, background). Written to device memory by the first kernel of a
+// call, so a captured CUDA graph replays with new values after a single
+// kernel-node parameter update.
+struct FrameParams {
+    double s, inv_s;
+    int64_t lo[3];
+    int32_t bits[3];
+    int32_t total;
+    Cam cam;
+    double bg[3];
+};
+
+// devprims.cu
+void dscan(sfb_ctx *ctx, const int32_t *in, int32_t *out, const int64_t *d_n, int64_t n_fixed,
+           int64_t *total_out, bool inclusive);
+template <class K>
+int dsort_pairs(sfb_ctx *ctx, K *k0, uint32_t *v0, K *k1, uint32_t *v1, const int64_t *d_n,
+                int64_t n_fixed, int bits);
+void write_params(sfb_ctx *ctx, const FrameParams &host, FrameParams *dev);
+
 // ---- cross-file launchers (defined in the .cu files) ----------------------
 
 // hashmap.cu
 struct HashTable {
     unsigned long long *keys = nullptr;
     int32_t *vals = nullptr;
-    uint32_t mask = 0;
+    uint32_t *mask = nullptr;  // device: capacity - 1, sized from the device count
 };
-HashTable hash_build(sfb_ctx *ctx, const int32_t *coords, int64_t m);
-void kernel_map_build(sfb_ctx *ctx, const HashTable &h, const int32_t *coords, int64_t m,
-                      int stride, int kernel, int32_t *map_tap_major);
+// counts: device pointer d_m (or nullptr -> m_bound is the exact count)
+HashTable hash_build(sfb_ctx *ctx, const int32_t *coords, const int64_t *d_m, int64_t m_bound);
+void kernel_map_build(sfb_ctx *ctx, const HashTable &h, const int32_t *coords, const int64_t *d_m,
+                      int64_t m_bound, int stride, int kernel, int32_t *map_tap_major);
 void transposed_lookup(sfb_ctx *ctx, const HashTable &h, int parent_stride,
-                       const int32_t *targets, int64_t m, int32_t *parent_out, int32_t *tap_out);
-// pooled parents in canonical order; returns parent count (one host sync)
-int64_t pool_build(sfb_ctx *ctx, const int32_t *coords, int64_t m, int stride, const float *feats,
-                   int c, int ld_in, int32_t *parent_coords, float *parent_feats, int ld_out,
-                   int32_t *child_to_parent);
+                       const int32_t *targets, const int64_t *d_m, int64_t m_bound,
+                       int32_t *parent_out, int32_t *tap_out);
+// pooled parents in canonical order; parent count -> *d_mp (device)
+void pool_build(sfb_ctx *ctx, const int32_t *coords, const int64_t *d_m, int64_t m_bound,
+                int stride, const FrameParams &host, const FrameParams *P, const float *feats,
+                int c, int ld_in, int32_t *parent_coords, float *parent_feats, int ld_out,
+                int32_t *child_to_parent, int64_t *d_mp);
+void coords_layout(sfb_ctx *ctx, const int32_t *coords, int64_t m, FrameParams &P);
 
 // voxelize.cu
 struct VoxelOut {
@@ -207,51 +276,55 @@ struct VoxelOut {
     double *feats;
     int64_t *keys;
     int32_t *p2v, *order, *offsets;
-    int64_t m;
 };
 void bbox_run(sfb_ctx *ctx, const double *pos, int64_t n, double *lo_hi_host);
-void voxelize_run(sfb_ctx *ctx, const double *pos, const double *col, int64_t n, double s,
-                  const double *lo_hi, VoxelOut &out);
+void voxel_layout(const double *lo_hi, double s, FrameParams &P);
+// voxel count lands in C->m[0] (device)
+void voxelize_run(sfb_ctx *ctx, const double *pos, const double *col, int64_t n,
+                  const FrameParams &host, const FrameParams *P, VoxelOut &out, DevCounts *C);
 
 // net.cu
 void net_load(sfb_ctx *ctx, const void *blob, size_t n);
-// returns per-voxel raw head (m0 x 14) float32 in `raw`
-void unet_run(sfb_ctx *ctx, const int32_t *coords, const double *feats9, int64_t m0, float *raw);
+// per-voxel raw head (M0 x 14) float32 into `raw`; M0 = C->m[0] (device), bound m_bound
+void unet_run(sfb_ctx *ctx, const int32_t *coords, const double *feats9, int64_t m_bound,
+              const FrameParams &host, const FrameParams *P, DevCounts *C, float *raw);
 void activate_run(sfb_ctx *ctx, const float *raw, int64_t m, double scale, double *delta,
                   double *sigma, double *quat, double *opac, double *normal);
 void conv_layer(sfb_ctx *ctx, const NetLayer &L, const float *in, int ld_in, const int32_t *nbr,
-                int64_t m, int relu, float *out, int ld_out);
+                int64_t nbr_ld, const int64_t *d_m, int64_t m_bound, int relu, float *out,
+                int ld_out);
 void tconv_layer(sfb_ctx *ctx, const NetLayer &L, const float *in, int ld_in,
-                 const int32_t *parent, const int32_t *tap, int64_t m, int relu, float *out,
-                 int ld_out);
+                 const int32_t *parent, const int32_t *tap, const int64_t *d_m, int64_t m_bound,
+                 int relu, float *out, int ld_out);
 void layer_set(sfb_ctx *ctx, int kind, int kernel, int cin, int cout, const float *w_host,
                const float *b_host);
-// per-voxel Gaussian parameters for the fused frame: centres, sigma, quat, opacity, normal
+// per-voxel Gaussians for the fused frame: centres, sigma, quat, opacity, normal
 void head_to_voxel_splats(sfb_ctx *ctx, const float *raw, const int32_t *coords,
-                          const double *feats9, int64_t m0, double scale, double *centers,
-                          double *sigma, double *quat, double *opac, double *normal);
+                          const double *feats9, const int64_t *d_m, int64_t m_bound,
+                          const FrameParams *P, double *centers, double *sigma, double *quat,
+                          double *opac, double *normal);
 
 // render.cu
 struct RenderInputs {
-    // geometry, either per splat (n rows) or per voxel (geom rows) with a
-    // point->geometry map; attributes always per point
+    // geometry, either per splat (n rows) or per voxel (geometry rows) with a
+    // point->geometry map; attributes: colours per point, normals per geometry
     const double *centers, *scales, *quats, *opac;
-    int64_t n_geom;
-    const int32_t *point_to_geom;  // nullptr: identity (geometry per point)
-    const int32_t *geom_points;    // CSR points of each geometry (fused path), or nullptr
-    const int32_t *geom_offsets;
+    int64_t n_geom;                 // host bound on geometry rows
+    const int64_t *d_n_geom;        // device count of geometry rows (nullptr: n_geom exact)
+    const int32_t *point_to_geom;   // nullptr: identity (geometry per point)
     const double *colors, *normals;
-    int64_t n_points;
+    int64_t n_points;               // exact, host
 };
-void render_run(sfb_ctx *ctx, const RenderInputs &in, const sfb_camera &cam,
-                const sfb_render_options &opts, int plane_mask, const double *bg, float *rgb,
-                float *normal, float *depth, float *trans);
+void render_run(sfb_ctx *ctx, const RenderInputs &in, const FrameParams *FP, int64_t width,
+                int64_t height, const sfb_render_options &opts, int plane_mask, DevCounts *C,
+                float *rgb, float *normal, float *depth, float *trans);
 void project_run(sfb_ctx *ctx, const double *centers, const double *quats, const double *scales,
-                 int64_t n, const sfb_camera &cam, double z_near, double dilation, double *sx,
-                 double *sy, double *depth, double *ca, double *cb, double *cc, double *radius,
-                 uint8_t *keep);
-void prepare_debug_run(sfb_ctx *ctx, const RenderInputs &in, const sfb_camera &cam, int tile,
-                       int64_t *source, double *radius, int64_t *offsets, int64_t *ids,
-                       int64_t cap, int64_t *k_host, int64_t *e_host);
+                 const int64_t *d_n, int64_t n_bound, const FrameParams *FP, double z_near,
+                 double dilation, double *sx, double *sy, double *depth, double *ca, double *cb,
+                 double *cc, double *radius, uint8_t *keep);
+void prepare_debug_run(sfb_ctx *ctx, const RenderInputs &in, const FrameParams *FP, int64_t width,
+                       int64_t height, int tile, DevCounts *C, int64_t *source, double *radius,
+                       int64_t *offsets, int64_t *ids, int64_t cap, int64_t *k_host,
+                       int64_t *e_host);
 
 }  // namespace sfb

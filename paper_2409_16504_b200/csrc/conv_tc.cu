@@ -125,12 +125,26 @@ struct TcShape {
                                       ((uint32_t)(kM >> 4) << 24);
 };
 
+// split-K factor for a level: the smallest divisor c (<= 32) of the tap count
+// with tiles*c >= target work items (else the largest such divisor)
+__host__ __device__ inline int choose_splits(int64_t tiles, int taps, int target) {
+    int best = 1;
+    for (int c = 1; c <= taps && c <= 32; ++c) {
+        if (taps % c) continue;
+        best = c;
+        if (tiles * c >= target) break;
+    }
+    return best;
+}
+constexpr int kSplitTarget = 2 * 148;
+constexpr int64_t kMaxPartialRows = 1480 * 128;
+
 template <int KP, int NP>
 __global__ void __launch_bounds__(kThreadsTC)
 k_conv_tc(const float *__restrict__ in, int ld_in, int cin, const int32_t *__restrict__ nbr,
-          int64_t m, int taps, int taps_per_split, const float *__restrict__ wtc,
-          const float *__restrict__ bias, int cout, int relu, float *__restrict__ out, int ld_out,
-          float *__restrict__ partial) {
+          int64_t nbr_ld, const int64_t *__restrict__ d_m, int64_t m_fixed, int taps,
+          const float *__restrict__ wtc, const float *__restrict__ bias, int cout, int relu,
+          float *__restrict__ out, int ld_out, float *__restrict__ partial) {
     using S = TcShape<KP, NP>;
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     float *stage_base = reinterpret_cast<float *>(
@@ -140,10 +154,12 @@ k_conv_tc(const float *__restrict__ in, int ld_in, int cin, const int32_t *__res
     uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(bar_done + 2);
 
     const int tid = threadIdx.x, warp = tid >> 5;
-    const int64_t row0 = (int64_t)blockIdx.x * kM;
-    const int split = blockIdx.y;
-    const int t0 = split * taps_per_split;
-    const int t1 = min(taps, t0 + taps_per_split);
+    const int64_t m = d_m ? *d_m : m_fixed;
+    const int64_t tiles = (m + kM - 1) / kM;
+    const int splits = choose_splits(tiles, taps, kSplitTarget);
+    const int tps = (taps + splits - 1) / splits;
+    const int64_t work = tiles * splits;
+    if ((int64_t)blockIdx.x >= work) return;   // uniform per CTA, before any collective
 
     if (tid == 0) {
         for (int s = 0; s < 2; ++s) {
@@ -163,114 +179,126 @@ k_conv_tc(const float *__restrict__ in, int ld_in, int cin, const int32_t *__res
     asm volatile("tcgen05.fence::after_thread_sync;");
     const uint32_t tmem = *tmem_slot;
 
-    const int64_t row = row0 + tid;
-    int issued = 0;        // taps whose MMAs were issued (uniform)
-    for (int t = t0; t < t1; ++t) {
-        const int s = issued % S::STAGES;
-        const int use = issued / S::STAGES;
-        float *A_hi = stage_base + s * S::STAGE_FLOATS;
-        float *A_lo = A_hi + S::A_FLOATS;
-        float *B_hi = A_lo + S::A_FLOATS;
-        const int32_t src = row < m ? nbr[(int64_t)t * m + row] : -1;
-        if (!__syncthreads_or(src >= 0)) continue;   // empty tap for the whole tile
-        if (use > 0) mbar_wait(&bar_done[s], (use - 1) & 1);   // stage free again
-        if (tid == 0) {
-            const uint32_t bytes = (uint32_t)(2 * S::B_FLOATS * 4);
-            mbar_expect_tx(&bar_full[s], bytes);
-            tma_bulk_g2s(B_hi, wtc + (size_t)t * 2 * S::B_FLOATS, bytes, &bar_full[s]);
-        }
-        // gather my row of this tap, split into tf32 hi/lo, canonical layout
-        const float *x = src >= 0 ? in + (int64_t)src * ld_in : nullptr;
-#pragma unroll
-        for (int c = 0; c < KP / 4; ++c) {
-            float v[4];
-#pragma unroll
-            for (int q = 0; q < 4; ++q) {
-                int k = 4 * c + q;
-                v[q] = (x && k < cin) ? __ldg(x + k) : 0.f;
+    int issued = 0;  // MMA batches issued by this CTA so far (drives stage/phase)
+    for (int64_t wi = blockIdx.x; wi < work; wi += gridDim.x) {
+        const int64_t row0 = (wi / splits) * kM;
+        const int split = (int)(wi % splits);
+        const int t0 = split * tps, t1 = min(taps, t0 + tps);
+        const int64_t row = row0 + tid;
+        int item_issued = 0;
+        for (int t = t0; t < t1; ++t) {
+            const int s = issued % S::STAGES;
+            const int use = issued / S::STAGES;
+            float *A_hi = stage_base + s * S::STAGE_FLOATS;
+            float *A_lo = A_hi + S::A_FLOATS;
+            float *B_hi = A_lo + S::A_FLOATS;
+            const int32_t src = row < m ? nbr[(int64_t)t * nbr_ld + row] : -1;
+            if (!__syncthreads_or(src >= 0)) continue;   // empty tap for the whole tile
+            if (use > 0) mbar_wait(&bar_done[s], (use - 1) & 1);   // stage free again
+            if (tid == 0) {
+                const uint32_t bytes = (uint32_t)(2 * S::B_FLOATS * 4);
+                mbar_expect_tx(&bar_full[s], bytes);
+                tma_bulk_g2s(B_hi, wtc + (size_t)t * 2 * S::B_FLOATS, bytes, &bar_full[s]);
             }
-            float4 hi, lo;
-            hi.x = tf32_trunc(v[0]);
-            hi.y = tf32_trunc(v[1]);
-            hi.z = tf32_trunc(v[2]);
-            hi.w = tf32_trunc(v[3]);
-            lo.x = tf32_trunc(v[0] - hi.x);
-            lo.y = tf32_trunc(v[1] - hi.y);
-            lo.z = tf32_trunc(v[2] - hi.z);
-            lo.w = tf32_trunc(v[3] - hi.w);
-            const int off = core_off(tid, 4 * c, KP);
-            *reinterpret_cast<float4 *>(A_hi + off) = hi;
-            *reinterpret_cast<float4 *>(A_lo + off) = lo;
-        }
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        __syncthreads();
-        if (tid == 0) {
-            mbar_wait(&bar_full[s], use & 1);
-            asm volatile("tcgen05.fence::after_thread_sync;");
-            const float *B_lo = B_hi + S::B_FLOATS;
-            const uint32_t lbo = 128, sbo_a = KP * 32, sbo_b = KP * 32;
+            // gather my row of this tap, split into tf32 hi/lo, canonical layout
+            const float *x = src >= 0 ? in + (int64_t)src * ld_in : nullptr;
 #pragma unroll
-            for (int ks = 0; ks < KP / 8; ++ks) {
-                const uint64_t ahi = smem_desc(smem_u32(A_hi) + ks * 256, lbo, sbo_a);
-                const uint64_t alo = smem_desc(smem_u32(A_lo) + ks * 256, lbo, sbo_a);
-                const uint64_t bhi = smem_desc(smem_u32(B_hi) + ks * 256, lbo, sbo_b);
-                const uint64_t blo = smem_desc(smem_u32(B_lo) + ks * 256, lbo, sbo_b);
-                mma_tf32(tmem, ahi, bhi, S::IDESC, (issued > 0 || ks > 0) ? 1u : 0u);
-                mma_tf32(tmem, ahi, blo, S::IDESC, 1u);
-                mma_tf32(tmem, alo, bhi, S::IDESC, 1u);
-            }
-            mma_commit(&bar_done[s]);
-        }
-        ++issued;
-    }
-    // epilogue: TMEM -> registers -> bias/ReLU -> global (or split-K partials)
-    float acc[NP];
-    if (issued > 0) {
-        const int last = issued - 1;
-        mbar_wait(&bar_done[last % S::STAGES], (last / S::STAGES) & 1);
-        asm volatile("tcgen05.fence::after_thread_sync;");
-        const uint32_t lane_base = (uint32_t)(warp * 32) << 16;
+            for (int c = 0; c < KP / 4; ++c) {
+                float v[4];
 #pragma unroll
-        for (int c = 0; c < NP; c += 16) tmem_ld16(tmem + lane_base + c, acc + c);
-    } else {
-#pragma unroll
-        for (int c = 0; c < NP; ++c) acc[c] = 0.f;
-    }
-    if (row < m) {
-        if (partial) {
-            float *p = partial + ((size_t)split * m + row) * NP;
-#pragma unroll
-            for (int c = 0; c < NP; c += 4)
-                *reinterpret_cast<float4 *>(p + c) = make_float4(acc[c], acc[c + 1], acc[c + 2], acc[c + 3]);
-        } else {
-            float *o = out + row * (int64_t)ld_out;
-#pragma unroll
-            for (int c = 0; c < NP; ++c)
-                if (c < cout) {
-                    float v = acc[c] + bias[c];
-                    o[c] = relu ? fmaxf(v, 0.f) : v;
+                for (int q = 0; q < 4; ++q) {
+                    int k = 4 * c + q;
+                    v[q] = (x && k < cin) ? __ldg(x + k) : 0.f;
                 }
+                float4 hi, lo;
+                hi.x = tf32_trunc(v[0]);
+                hi.y = tf32_trunc(v[1]);
+                hi.z = tf32_trunc(v[2]);
+                hi.w = tf32_trunc(v[3]);
+                lo.x = tf32_trunc(v[0] - hi.x);
+                lo.y = tf32_trunc(v[1] - hi.y);
+                lo.z = tf32_trunc(v[2] - hi.z);
+                lo.w = tf32_trunc(v[3] - hi.w);
+                const int off = core_off(tid, 4 * c, KP);
+                *reinterpret_cast<float4 *>(A_hi + off) = hi;
+                *reinterpret_cast<float4 *>(A_lo + off) = lo;
+            }
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            __syncthreads();
+            if (tid == 0) {
+                mbar_wait(&bar_full[s], use & 1);
+                asm volatile("tcgen05.fence::after_thread_sync;");
+                const float *B_lo = B_hi + S::B_FLOATS;
+                const uint32_t lbo = 128, sbo = KP * 32;
+#pragma unroll
+                for (int ks = 0; ks < KP / 8; ++ks) {
+                    const uint64_t ahi = smem_desc(smem_u32(A_hi) + ks * 256, lbo, sbo);
+                    const uint64_t alo = smem_desc(smem_u32(A_lo) + ks * 256, lbo, sbo);
+                    const uint64_t bhi = smem_desc(smem_u32(B_hi) + ks * 256, lbo, sbo);
+                    const uint64_t blo = smem_desc(smem_u32(B_lo) + ks * 256, lbo, sbo);
+                    mma_tf32(tmem, ahi, bhi, S::IDESC, (item_issued > 0 || ks > 0) ? 1u : 0u);
+                    mma_tf32(tmem, ahi, blo, S::IDESC, 1u);
+                    mma_tf32(tmem, alo, bhi, S::IDESC, 1u);
+                }
+                mma_commit(&bar_done[s]);
+            }
+            ++issued;
+            ++item_issued;
         }
+        // epilogue: TMEM -> registers -> bias/ReLU -> global (or split-K partials)
+        float acc[NP];
+        if (item_issued > 0) {
+            const int last = issued - 1;
+            mbar_wait(&bar_done[last % S::STAGES], (last / S::STAGES) & 1);
+            asm volatile("tcgen05.fence::after_thread_sync;");
+            const uint32_t lane_base = (uint32_t)(warp * 32) << 16;
+#pragma unroll
+            for (int c = 0; c < NP; c += 16) tmem_ld16(tmem + lane_base + c, acc + c);
+        } else {
+#pragma unroll
+            for (int c = 0; c < NP; ++c) acc[c] = 0.f;
+        }
+        if (row < m) {
+            if (splits > 1) {
+                float *p = partial + ((size_t)split * m + row) * NP;
+#pragma unroll
+                for (int c = 0; c < NP; c += 4)
+                    *reinterpret_cast<float4 *>(p + c) = make_float4(acc[c], acc[c + 1], acc[c + 2], acc[c + 3]);
+            } else {
+                float *o = out + row * (int64_t)ld_out;
+#pragma unroll
+                for (int c = 0; c < NP; ++c)
+                    if (c < cout) {
+                        float v = acc[c] + bias[c];
+                        o[c] = relu ? fmaxf(v, 0.f) : v;
+                    }
+            }
+        }
+        // all TMEM reads done before the next item's MMAs overwrite the accumulator
+        asm volatile("tcgen05.fence::before_thread_sync;");
+        __syncthreads();
+        asm volatile("tcgen05.fence::after_thread_sync;");
     }
-    asm volatile("tcgen05.fence::before_thread_sync;");
-    __syncthreads();
     if (warp == 0)
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem),
                      "r"(S::TMEM_COLS));
 }
 
 // deterministic split-K reduction: out = act(b + sum_s partial[s]) in split order
-__global__ void k_splitk_reduce(const float *__restrict__ partial, int splits, int64_t m, int np,
-                                const float *__restrict__ bias, int cout, int relu,
-                                float *__restrict__ out, int ld_out) {
-    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (i >= m * cout) return;
-    int64_t r = i / cout;
-    int c = (int)(i % cout);
-    float s = 0.f;
-    for (int k = 0; k < splits; ++k) s += partial[((size_t)k * m + r) * np + c];
-    float v = s + bias[c];
-    out[r * ld_out + c] = relu ? fmaxf(v, 0.f) : v;
+__global__ void k_splitk_reduce(const float *__restrict__ partial, const int64_t *__restrict__ d_m,
+                                int64_t m_fixed, int taps, int np, const float *__restrict__ bias,
+                                int cout, int relu, float *__restrict__ out, int ld_out) {
+    const int64_t m = d_m ? *d_m : m_fixed;
+    const int splits = choose_splits((m + kM - 1) / kM, taps, kSplitTarget);
+    if (splits == 1) return;
+    SFB_FOR(i, m * cout) {
+        const int64_t r = i / cout;
+        const int c = (int)(i % cout);
+        float s = 0.f;
+        for (int k = 0; k < splits; ++k) s += partial[((size_t)k * m + r) * np + c];
+        const float v = s + bias[c];
+        out[r * ld_out + c] = relu ? fmaxf(v, 0.f) : v;
+    }
 }
 
 // W[t][ci][co] -> per tap [hi | lo] tiles of [NP x KP] in the canonical layout
@@ -295,7 +323,8 @@ int pad_n(int c) { return c <= 16 ? 16 : (c <= 32 ? 32 : (c <= 64 ? 64 : (c <= 1
 
 template <int KP, int NP>
 void launch_tc(sfb_ctx *ctx, const NetLayer &L, const float *in, int ld_in, const int32_t *nbr,
-               int64_t m, int relu, float *out, int ld_out) {
+               int64_t nbr_ld, const int64_t *d_m, int64_t m_bound, int relu, float *out,
+               int ld_out) {
     using S = TcShape<KP, NP>;
     static bool attr = false;
     if (!attr) {
@@ -303,27 +332,19 @@ void launch_tc(sfb_ctx *ctx, const NetLayer &L, const float *in, int ld_in, cons
                                       S::SMEM));
         attr = true;
     }
-    const int64_t tiles = (m + kM - 1) / kM;
-    // split the taps across CTAs until ~2 CTAs per SM are in flight
-    int splits = 1;
-    const int cands[] = {1, 3, 9, 27};
-    for (int c : cands)
-        if (c <= L.taps && L.taps % c == 0) {
-            splits = c;
-            if (tiles * c >= 2 * ctx->num_sms) break;
-        }
-    const int tps = (L.taps + splits - 1) / splits;
-    float *partial = nullptr;
-    if (splits > 1) partial = ctx->arena.alloc<float>((size_t)splits * m * NP);
-    dim3 grid((unsigned)tiles, splits);
+    const int64_t tiles_bound = (m_bound + kM - 1) / kM;
+    const int64_t work_bound = tiles_bound * choose_splits(tiles_bound, L.taps, kSplitTarget);
+    const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(work_bound, kSplitTarget));
+    float *partial = ctx->arena.alloc<float>((size_t)std::min<int64_t>(kMaxPartialRows,
+                                                                       32 * m_bound) * NP);
     k_conv_tc<KP, NP><<<grid, kThreadsTC, S::SMEM, ctx->stream>>>(
-        in, ld_in, L.cin, nbr, m, L.taps, tps, L.w_tc, L.b, L.cout, relu, out, ld_out, partial);
+        in, ld_in, L.cin, nbr, nbr_ld, d_m, m_bound, L.taps, L.w_tc, L.b, L.cout, relu, out, ld_out,
+        partial);
     SFB_CHECK_LAUNCH();
-    if (splits > 1) {
-        k_splitk_reduce<<<grid_for(m * L.cout, 256), 256, 0, ctx->stream>>>(
-            partial, splits, m, NP, L.b, L.cout, relu, out, ld_out);
-        SFB_CHECK_LAUNCH();
-    }
+    k_splitk_reduce<<<dgrid(std::min<int64_t>(m_bound, kMaxPartialRows) * L.cout, 256), 256, 0,
+                      ctx->stream>>>(partial, d_m, m_bound, L.taps, NP, L.b, L.cout, relu, out,
+                                     ld_out);
+    SFB_CHECK_LAUNCH();
 }
 
 }  // namespace
@@ -348,11 +369,12 @@ void prepare_tc_weights(sfb_ctx *ctx, NetLayer &L) {
 }
 
 void conv_layer_tc(sfb_ctx *ctx, const NetLayer &L, const float *in, int ld_in, const int32_t *nbr,
-                   int64_t m, int relu, float *out, int ld_out) {
-#define SFB_TC_CASE(K, N)                                                 \
-    if (L.cin_pad == K && L.cout_pad == N) {                              \
-        launch_tc<K, N>(ctx, L, in, ld_in, nbr, m, relu, out, ld_out);    \
-        return;                                                           \
+                   int64_t nbr_ld, const int64_t *d_m, int64_t m_bound, int relu, float *out,
+                   int ld_out) {
+#define SFB_TC_CASE(K, N)                                                                 \
+    if (L.cin_pad == K && L.cout_pad == N) {                                              \
+        launch_tc<K, N>(ctx, L, in, ld_in, nbr, nbr_ld, d_m, m_bound, relu, out, ld_out); \
+        return;                                                                           \
     }
     SFB_TC_CASE(16, 16) SFB_TC_CASE(16, 32) SFB_TC_CASE(16, 64) SFB_TC_CASE(16, 128)
     SFB_TC_CASE(32, 16) SFB_TC_CASE(32, 32) SFB_TC_CASE(32, 64) SFB_TC_CASE(32, 128)

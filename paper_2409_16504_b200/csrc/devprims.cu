@@ -1,0 +1,229 @@
+// Device-count primitives: scans and a stable LSD radix sort whose element
+// count lives in DEVICE memory (written by an earlier kernel), with grids
+// sized from a host capacity. They let the whole frame run without a single
+// device->host size read after the bbox, which is what makes it capturable
+// as one CUDA graph (the P2ENet level sizes, kept splats, runs and tile
+// entries are all data-dependent).
+#include "common.cuh"
+
+namespace sfb {
+
+constexpr int kScanBlocks = 148;
+constexpr int kScanThreads = 1024;
+
+// ------------------------------------------------------------------ scan
+__device__ __forceinline__ int64_t chunk_of(int64_t n, int blocks) {
+    return (n + blocks - 1) / blocks;
+}
+
+__device__ __forceinline__ int32_t block_excl_scan(int32_t v, int32_t *s_warp, int32_t *total) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    int32_t x = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        int32_t y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
+    }
+    if (lane == 31) s_warp[warp] = x;
+    __syncthreads();
+    if (warp == 0) {
+        int32_t w = lane < (int)(blockDim.x >> 5) ? s_warp[lane] : 0;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            int32_t y = __shfl_up_sync(0xffffffffu, w, o);
+            if (lane >= o) w += y;
+        }
+        s_warp[lane] = w;
+    }
+    __syncthreads();
+    int32_t incl = x + (warp ? s_warp[warp - 1] : 0);
+    if (total) *total = s_warp[(blockDim.x >> 5) - 1];
+    __syncthreads();
+    return incl - v;
+}
+
+__global__ void __launch_bounds__(kScanThreads)
+k_scan_partials(const int32_t *__restrict__ in, const int64_t *__restrict__ d_n, int64_t n_fixed,
+                int32_t *__restrict__ part) {
+    __shared__ int32_t s_warp[32];
+    const int64_t n = d_n ? *d_n : n_fixed;
+    const int64_t ch = chunk_of(n, gridDim.x);
+    const int64_t b0 = blockIdx.x * ch, b1 = min(n, b0 + ch);
+    int32_t s = 0;
+    for (int64_t i = b0 + threadIdx.x; i < b1; i += blockDim.x) s += in[i];
+    int32_t tot;
+    block_excl_scan(s, s_warp, &tot);
+    if (threadIdx.x == 0) part[blockIdx.x] = tot;
+}
+
+__global__ void __launch_bounds__(kScanThreads)
+k_scan_apply(const int32_t *__restrict__ in, const int64_t *__restrict__ d_n, int64_t n_fixed,
+             const int32_t *__restrict__ part, int32_t *__restrict__ out,
+             int64_t *__restrict__ total_out, int inclusive) {
+    __shared__ int32_t s_warp[32];
+    __shared__ int32_t s_base;
+    const int64_t n = d_n ? *d_n : n_fixed;
+    const int64_t ch = chunk_of(n, gridDim.x);
+    const int64_t b0 = blockIdx.x * ch, b1 = min(n, b0 + ch);
+    if (threadIdx.x == 0) {
+        int32_t acc = 0;
+        for (int b = 0; b < (int)blockIdx.x; ++b) acc += part[b];
+        s_base = acc;
+        if (blockIdx.x == gridDim.x - 1 && total_out) *total_out = acc + part[blockIdx.x];
+    }
+    __syncthreads();
+    int32_t base = s_base;
+    for (int64_t t0 = b0; t0 < b1; t0 += blockDim.x) {
+        const int64_t i = t0 + threadIdx.x;
+        const int32_t v = i < b1 ? in[i] : 0;
+        int32_t tile_total;
+        const int32_t ex = block_excl_scan(v, s_warp, &tile_total);
+        if (i < b1) out[i] = base + ex + (inclusive ? v : 0);
+        base += tile_total;
+    }
+}
+
+// exclusive (or inclusive) scan of n int32 (n from device if d_n, else n_fixed);
+// in-place allowed; the grand total is written to *total_out when given.
+void dscan(sfb_ctx *ctx, const int32_t *in, int32_t *out, const int64_t *d_n, int64_t n_fixed,
+           int64_t *total_out, bool inclusive) {
+    int32_t *part = ctx->arena.alloc<int32_t>(kScanBlocks);
+    k_scan_partials<<<kScanBlocks, kScanThreads, 0, ctx->stream>>>(in, d_n, n_fixed, part);
+    k_scan_apply<<<kScanBlocks, kScanThreads, 0, ctx->stream>>>(in, d_n, n_fixed, part, out,
+                                                                total_out, inclusive ? 1 : 0);
+    SFB_CHECK_LAUNCH();
+}
+
+// ------------------------------------------------------------------ params
+__global__ void k_write_params(FrameParams p, FrameParams *dst) { *dst = p; }
+
+void write_params(sfb_ctx *ctx, const FrameParams &host, FrameParams *dev) {
+    k_write_params<<<1, 1, 0, ctx->stream>>>(host, dev);
+    SFB_CHECK_LAUNCH();
+}
+
+const void *write_params_func() { return reinterpret_cast<const void *>(&k_write_params); }
+
+Cam to_cam(const sfb_camera &c) {
+    Cam k;
+    for (int i = 0; i < 9; ++i) k.r[i] = c.rot[i];
+    for (int i = 0; i < 3; ++i) k.t[i] = c.trans[i];
+    k.fx = c.fx;
+    k.fy = c.fy;
+    k.cx = c.cx;
+    k.cy = c.cy;
+    k.w = c.width;
+    k.h = c.height;
+    return k;
+}
+
+// ------------------------------------------------------------------ radix sort
+constexpr int kRsBlocks = 148;
+constexpr int kRsThreads = 256;
+constexpr int kRsWarps = kRsThreads / 32;
+
+template <class K>
+__global__ void __launch_bounds__(kRsThreads)
+k_rs_upsweep(const K *__restrict__ keys, const int64_t *__restrict__ d_n, int64_t n_fixed, int shift,
+             int32_t *__restrict__ hist) {
+    __shared__ int32_t h[256];
+    h[threadIdx.x] = 0;
+    __syncthreads();
+    const int64_t n = d_n ? *d_n : n_fixed;
+    const int64_t ch = chunk_of(n, gridDim.x);
+    const int64_t b0 = blockIdx.x * ch, b1 = min(n, b0 + ch);
+    for (int64_t i = b0 + threadIdx.x; i < b1; i += blockDim.x)
+        atomicAdd(&h[(uint32_t)(keys[i] >> shift) & 255u], 1);
+    __syncthreads();
+    hist[threadIdx.x * gridDim.x + blockIdx.x] = h[threadIdx.x];
+}
+
+// exclusive scan of the digit-major histogram (256 x blocks), one CTA
+__global__ void __launch_bounds__(1024) k_rs_scan(int32_t *__restrict__ hist, int count) {
+    __shared__ int32_t s_warp[32];
+    int32_t base = 0;
+    for (int t0 = 0; t0 < count; t0 += blockDim.x) {
+        const int i = t0 + threadIdx.x;
+        const int32_t v = i < count ? hist[i] : 0;
+        int32_t tot;
+        const int32_t ex = block_excl_scan(v, s_warp, &tot);
+        if (i < count) hist[i] = base + ex;
+        base += tot;
+    }
+}
+
+// stable scatter: each block walks its chunk in order, 256 items at a time;
+// rank within a sub-tile = (warps before me with this digit) + (lower lanes
+// of my warp with this digit), found with __match_any_sync
+template <class K, bool HAS_VALS>
+__global__ void __launch_bounds__(kRsThreads)
+k_rs_downsweep(const K *__restrict__ kin, const uint32_t *__restrict__ vin, K *__restrict__ kout,
+               uint32_t *__restrict__ vout, const int64_t *__restrict__ d_n, int64_t n_fixed,
+               int shift, const int32_t *__restrict__ hist) {
+    __shared__ int32_t run[256];
+    __shared__ int32_t wcnt[kRsWarps][256];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    run[threadIdx.x] = hist[threadIdx.x * gridDim.x + blockIdx.x];
+    for (int w = 0; w < kRsWarps; ++w) wcnt[w][threadIdx.x] = 0;
+    __syncthreads();
+    const int64_t n = d_n ? *d_n : n_fixed;
+    const int64_t ch = chunk_of(n, gridDim.x);
+    const int64_t b0 = blockIdx.x * ch, b1 = min(n, b0 + ch);
+    const uint32_t lt = (1u << lane) - 1u;
+    for (int64_t t0 = b0; t0 < b1; t0 += kRsThreads) {
+        const int64_t i = t0 + threadIdx.x;
+        const bool ok = i < b1;
+        K key = ok ? kin[i] : K(0);
+        uint32_t val = (HAS_VALS && ok) ? vin[i] : 0u;
+        const uint32_t d = ok ? ((uint32_t)(key >> shift) & 255u) : 256u;
+        const uint32_t peers = __match_any_sync(0xffffffffu, d);
+        const int rank_w = __popc(peers & lt);
+        if (ok && rank_w == 0) wcnt[warp][d] = __popc(peers);
+        __syncthreads();
+        if (ok) {
+            int32_t pos = run[d] + rank_w;
+            for (int w = 0; w < warp; ++w) pos += wcnt[w][d];
+            kout[pos] = key;
+            if (HAS_VALS) vout[pos] = val;
+        }
+        __syncthreads();
+        int32_t add = 0;
+        for (int w = 0; w < kRsWarps; ++w) {
+            add += wcnt[w][threadIdx.x];
+            wcnt[w][threadIdx.x] = 0;
+        }
+        run[threadIdx.x] += add;
+        __syncthreads();
+    }
+}
+
+// Stable LSD sort of (key, val) over bits [0, bits). Result ends in (k0, v0)
+// if the pass count is even, else in (k1, v1); returns which (0/1).
+template <class K>
+int dsort_pairs(sfb_ctx *ctx, K *k0, uint32_t *v0, K *k1, uint32_t *v1, const int64_t *d_n,
+                int64_t n_fixed, int bits) {
+    const int passes = (bits + 7) / 8;
+    int32_t *hist = ctx->arena.alloc<int32_t>(256 * kRsBlocks);
+    for (int p = 0; p < passes; ++p) {
+        K *ki = (p & 1) ? k1 : k0, *ko = (p & 1) ? k0 : k1;
+        uint32_t *vi = (p & 1) ? v1 : v0, *vo = (p & 1) ? v0 : v1;
+        k_rs_upsweep<K><<<kRsBlocks, kRsThreads, 0, ctx->stream>>>(ki, d_n, n_fixed, 8 * p, hist);
+        k_rs_scan<<<1, 1024, 0, ctx->stream>>>(hist, 256 * kRsBlocks);
+        if (v0)
+            k_rs_downsweep<K, true><<<kRsBlocks, kRsThreads, 0, ctx->stream>>>(ki, vi, ko, vo, d_n,
+                                                                               n_fixed, 8 * p, hist);
+        else
+            k_rs_downsweep<K, false><<<kRsBlocks, kRsThreads, 0, ctx->stream>>>(
+                ki, nullptr, ko, nullptr, d_n, n_fixed, 8 * p, hist);
+        SFB_CHECK_LAUNCH();
+    }
+    return passes & 1;
+}
+
+template int dsort_pairs<uint32_t>(sfb_ctx *, uint32_t *, uint32_t *, uint32_t *, uint32_t *,
+                                   const int64_t *, int64_t, int);
+template int dsort_pairs<unsigned long long>(sfb_ctx *, unsigned long long *, uint32_t *,
+                                             unsigned long long *, uint32_t *, const int64_t *,
+                                             int64_t, int);
+
+}  // namespace sfb

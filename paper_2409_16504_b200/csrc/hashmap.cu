@@ -6,13 +6,12 @@
 // 233-238) and pool_2x2x2 (voxelgrid.py:171-185).
 //
 // B200 design: an open-addressing table of packed 64-bit keys -> canonical
-// row (one CAS insert per voxel, 1-2 probes per lookup, sized to 2x the
-// voxel count so it stays L2-resident), kernel maps written tap-major
-// (taps x rows, int32) so the gather-GEMM reads them coalesced, and pooling
-// as a stable radix sort of compact parent keys + ordered segment means
-// (children summed in increasing child row, as np.add.at does).
-#include <cub/cub.cuh>
-
+// row (one CAS insert per voxel, 1-2 probes per lookup, sized on the device
+// to 2x the voxel count so it stays L2-resident), kernel maps written
+// tap-major (taps x rows, int32) so the gather-GEMM reads them coalesced,
+// and pooling as a stable radix sort of compact parent keys + ordered
+// segment means (children summed in increasing child row, as np.add.at
+// does). Every size is a device count: no host round trip per level.
 #include "common.cuh"
 
 namespace sfb {
@@ -28,242 +27,275 @@ __device__ __forceinline__ uint32_t hash64(unsigned long long k) {
     return (uint32_t)k;
 }
 
-__global__ void k_hash_insert(const int32_t *__restrict__ coords, int64_t m,
-                              unsigned long long *__restrict__ keys, int32_t *__restrict__ vals,
-                              uint32_t mask) {
-    int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (r >= m) return;
-    unsigned long long key =
-        (unsigned long long)pack_key(coords[3 * r], coords[3 * r + 1], coords[3 * r + 2]);
-    uint32_t h = hash64(key) & mask;
-    while (true) {
-        unsigned long long prev = atomicCAS(&keys[h], kEmpty, key);
-        if (prev == kEmpty || prev == key) {
-            vals[h] = (int32_t)r;
-            return;
-        }
-        h = (h + 1) & mask;
-    }
-}
-
-__device__ __forceinline__ int32_t hash_find(const unsigned long long *__restrict__ keys,
-                                             const int32_t *__restrict__ vals, uint32_t mask,
-                                             int64_t x, int64_t y, int64_t z) {
-    if (!key_in_range(x, y, z)) return -1;
-    unsigned long long key = (unsigned long long)pack_key(x, y, z);
-    uint32_t h = hash64(key) & mask;
-    while (true) {
-        unsigned long long k = keys[h];
-        if (k == key) return vals[h];
-        if (k == kEmpty) return -1;
-        h = (h + 1) & mask;
-    }
-}
-
-HashTable hash_build(sfb_ctx *ctx, const int32_t *coords, int64_t m) {
-    HashTable h;
+__global__ void k_hash_clear(HashTable h, const int64_t *__restrict__ d_m, int64_t m_fixed) {
+    const int64_t m = d_m ? *d_m : m_fixed;
     uint64_t cap = 64;
     while (cap < (uint64_t)(2 * m)) cap <<= 1;
-    h.mask = (uint32_t)(cap - 1);
+    if (blockIdx.x == 0 && threadIdx.x == 0) *h.mask = (uint32_t)(cap - 1);
+    SFB_FOR(i, (int64_t)cap) h.keys[i] = kEmpty;
+}
+
+__global__ void k_hash_insert(const int32_t *__restrict__ coords, const int64_t *__restrict__ d_m,
+                              int64_t m_fixed, HashTable h) {
+    const int64_t m = d_m ? *d_m : m_fixed;
+    const uint32_t mask = *h.mask;
+    SFB_FOR(r, m) {
+        unsigned long long key =
+            (unsigned long long)pack_key(coords[3 * r], coords[3 * r + 1], coords[3 * r + 2]);
+        uint32_t slot = hash64(key) & mask;
+        while (true) {
+            unsigned long long prev = atomicCAS(&h.keys[slot], kEmpty, key);
+            if (prev == kEmpty || prev == key) {
+                h.vals[slot] = (int32_t)r;
+                break;
+            }
+            slot = (slot + 1) & mask;
+        }
+    }
+}
+
+__device__ __forceinline__ int32_t hash_find(const HashTable &h, uint32_t mask, int64_t x, int64_t y,
+                                             int64_t z) {
+    if (!key_in_range(x, y, z)) return -1;
+    unsigned long long key = (unsigned long long)pack_key(x, y, z);
+    uint32_t slot = hash64(key) & mask;
+    while (true) {
+        unsigned long long k = h.keys[slot];
+        if (k == key) return h.vals[slot];
+        if (k == kEmpty) return -1;
+        slot = (slot + 1) & mask;
+    }
+}
+
+HashTable hash_build(sfb_ctx *ctx, const int32_t *coords, const int64_t *d_m, int64_t m_bound) {
+    HashTable h;
+    uint64_t cap = 64;
+    while (cap < (uint64_t)(2 * m_bound)) cap <<= 1;
     h.keys = ctx->arena.alloc<unsigned long long>(cap);
     h.vals = ctx->arena.alloc<int32_t>(cap);
-    SFB_CUDA(cudaMemsetAsync(h.keys, 0xff, cap * sizeof(unsigned long long), ctx->stream));
-    if (m > 0) {
-        k_hash_insert<<<grid_for(m, 256), 256, 0, ctx->stream>>>(coords, m, h.keys, h.vals, h.mask);
-        SFB_CHECK_LAUNCH();
-    }
+    h.mask = ctx->arena.alloc<uint32_t>(1);
+    k_hash_clear<<<dgrid((int64_t)cap, 256), 256, 0, ctx->stream>>>(h, d_m, m_bound);
+    k_hash_insert<<<dgrid(m_bound, 256), 256, 0, ctx->stream>>>(coords, d_m, m_bound, h);
+    SFB_CHECK_LAUNCH();
     return h;
 }
 
-// map[t*m + r] = row of coords[r] + offset(t)*stride, -1 when empty/out of range
-__global__ void k_kernel_map(const int32_t *__restrict__ coords, int64_t m, int stride, int kernel,
-                             const unsigned long long *__restrict__ keys,
-                             const int32_t *__restrict__ vals, uint32_t mask,
+// map[t*m_cap + r] = row of coords[r] + offset(t)*stride, -1 when empty/out of range
+__global__ void k_kernel_map(const int32_t *__restrict__ coords, const int64_t *__restrict__ d_m,
+                             int64_t m_fixed, int64_t ld, int stride, int kernel, HashTable h,
                              int32_t *__restrict__ map) {
-    int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    int t = blockIdx.y;
-    if (r >= m) return;
-    int k2 = kernel * kernel, rad = kernel / 2;
-    int a = t / k2, b = (t / kernel) % kernel, c = t % kernel;  // (dz, dy, dx) lexicographic
-    int64_t x = coords[3 * r] + (int64_t)(c - rad) * stride;
-    int64_t y = coords[3 * r + 1] + (int64_t)(b - rad) * stride;
-    int64_t z = coords[3 * r + 2] + (int64_t)(a - rad) * stride;
-    map[(int64_t)t * m + r] = hash_find(keys, vals, mask, x, y, z);
+    const int64_t m = d_m ? *d_m : m_fixed;
+    const uint32_t mask = *h.mask;
+    const int taps = kernel * kernel * kernel, k2 = kernel * kernel, rad = kernel / 2;
+    SFB_FOR(idx, m * taps) {
+        const int64_t r = idx % m;
+        const int t = (int)(idx / m);
+        const int a = t / k2, b = (t / kernel) % kernel, c = t % kernel;  // (dz, dy, dx)
+        const int64_t x = coords[3 * r] + (int64_t)(c - rad) * stride;
+        const int64_t y = coords[3 * r + 1] + (int64_t)(b - rad) * stride;
+        const int64_t z = coords[3 * r + 2] + (int64_t)(a - rad) * stride;
+        map[(int64_t)t * ld + r] = hash_find(h, mask, x, y, z);
+    }
 }
 
-void kernel_map_build(sfb_ctx *ctx, const HashTable &h, const int32_t *coords, int64_t m,
-                      int stride, int kernel, int32_t *map_tap_major) {
-    if (m == 0) return;
-    int taps = kernel * kernel * kernel;
-    dim3 grid(grid_for(m, 128), taps);
-    k_kernel_map<<<grid, 128, 0, ctx->stream>>>(coords, m, stride, kernel, h.keys, h.vals, h.mask,
-                                                map_tap_major);
+void kernel_map_build(sfb_ctx *ctx, const HashTable &h, const int32_t *coords, const int64_t *d_m,
+                      int64_t m_bound, int stride, int kernel, int32_t *map_tap_major) {
+    const int taps = kernel * kernel * kernel;
+    k_kernel_map<<<dgrid(m_bound * taps, 256), 256, 0, ctx->stream>>>(
+        coords, d_m, m_bound, m_bound, stride, kernel, h, map_tap_major);
     SFB_CHECK_LAUNCH();
 }
 
-__global__ void k_transposed_lookup(const int32_t *__restrict__ targets, int64_t m, int ps,
-                                    const unsigned long long *__restrict__ keys,
-                                    const int32_t *__restrict__ vals, uint32_t mask,
-                                    int32_t *__restrict__ parent, int32_t *__restrict__ tap) {
-    int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (r >= m) return;
-    int64_t t[3], p[3];
+__global__ void k_transposed_lookup(const int32_t *__restrict__ targets,
+                                    const int64_t *__restrict__ d_m, int64_t m_fixed, int ps,
+                                    HashTable h, int32_t *__restrict__ parent,
+                                    int32_t *__restrict__ tap) {
+    const int64_t m = d_m ? *d_m : m_fixed;
+    const uint32_t mask = *h.mask;
+    SFB_FOR(r, m) {
+        int64_t t[3], p[3];
 #pragma unroll
-    for (int a = 0; a < 3; ++a) {
-        t[a] = targets[3 * r + a];
-        p[a] = floor_div(t[a], ps) * ps;
+        for (int a = 0; a < 3; ++a) {
+            t[a] = targets[3 * r + a];
+            p[a] = floor_div(t[a], ps) * ps;
+        }
+        const int half = ps / 2;
+        tap[r] = (int32_t)(((t[2] - p[2]) / half) * 4 + ((t[1] - p[1]) / half) * 2 + (t[0] - p[0]) / half);
+        parent[r] = hash_find(h, mask, p[0], p[1], p[2]);
     }
-    int half = ps / 2;
-    tap[r] = (int32_t)(((t[2] - p[2]) / half) * 4 + ((t[1] - p[1]) / half) * 2 + (t[0] - p[0]) / half);
-    parent[r] = hash_find(keys, vals, mask, p[0], p[1], p[2]);
 }
 
 void transposed_lookup(sfb_ctx *ctx, const HashTable &h, int parent_stride,
-                       const int32_t *targets, int64_t m, int32_t *parent_out, int32_t *tap_out) {
-    if (m == 0) return;
-    k_transposed_lookup<<<grid_for(m, 256), 256, 0, ctx->stream>>>(
-        targets, m, parent_stride, h.keys, h.vals, h.mask, parent_out, tap_out);
+                       const int32_t *targets, const int64_t *d_m, int64_t m_bound,
+                       int32_t *parent_out, int32_t *tap_out) {
+    k_transposed_lookup<<<dgrid(m_bound, 256), 256, 0, ctx->stream>>>(
+        targets, d_m, m_bound, parent_stride, h, parent_out, tap_out);
     SFB_CHECK_LAUNCH();
 }
 
 // ---------------------------------------------------------------- pooling
-struct ParentLayout {
-    int64_t lo[3];
-    int bits[3];
-    int total;
-    int64_t step;
-};
-
-__global__ void k_int_bbox(const int32_t *__restrict__ c, int64_t m, int *mm) {
-    int lo[3] = {INT_MAX, INT_MAX, INT_MAX}, hi[3] = {INT_MIN, INT_MIN, INT_MIN};
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m;
-         i += (int64_t)gridDim.x * blockDim.x)
-        for (int a = 0; a < 3; ++a) {
-            lo[a] = min(lo[a], c[3 * i + a]);
-            hi[a] = max(hi[a], c[3 * i + a]);
-        }
+// parent layout at step S from the level-0 key layout: the lattice of every
+// level lies inside [lo, lo + 2^bits - 1] per axis
+__device__ __forceinline__ void parent_layout(const FrameParams *P, int64_t S, int64_t *plo,
+                                              int *pbits) {
+#pragma unroll
     for (int a = 0; a < 3; ++a) {
-        atomicMin(&mm[a], lo[a]);
-        atomicMax(&mm[3 + a], hi[a]);
+        const int64_t lo = P->lo[a], hi = lo + ((int64_t)1 << P->bits[a]) - 1;
+        plo[a] = floor_div(lo, S) * S;
+        const int64_t span = (floor_div(hi, S) * S - plo[a]) / S;
+        int b = 0;
+        while (b < 63 && (span >> b) != 0) ++b;
+        pbits[a] = b;
     }
 }
-__global__ void k_int_bbox_init(int *mm) {
-    if (threadIdx.x < 3) mm[threadIdx.x] = INT_MAX;
-    else if (threadIdx.x < 6) mm[threadIdx.x] = INT_MIN;
-}
 
 template <class K>
-__global__ void k_parent_keys(const int32_t *__restrict__ coords, int64_t m, ParentLayout L,
-                              K *__restrict__ keys, uint32_t *__restrict__ vals) {
-    int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (j >= m) return;
-    uint64_t q[3];
+__global__ void k_parent_keys(const int32_t *__restrict__ coords, const int64_t *__restrict__ d_m,
+                              int64_t S, const FrameParams *__restrict__ P, K *__restrict__ keys,
+                              uint32_t *__restrict__ vals) {
+    int64_t plo[3];
+    int pb[3];
+    parent_layout(P, S, plo, pb);
+    const int64_t m = *d_m;
+    SFB_FOR(j, m) {
+        uint64_t q[3];
 #pragma unroll
-    for (int a = 0; a < 3; ++a)
-        q[a] = (uint64_t)((floor_div(coords[3 * j + a], L.step) * L.step - L.lo[a]) / L.step);
-    keys[j] = (K)((q[2] << (L.bits[0] + L.bits[1])) | (q[1] << L.bits[0]) | q[0]);
-    vals[j] = (uint32_t)j;
+        for (int a = 0; a < 3; ++a) q[a] = (uint64_t)((floor_div(coords[3 * j + a], S) * S - plo[a]) / S);
+        keys[j] = (K)((q[2] << (pb[0] + pb[1])) | (q[1] << pb[0]) | q[0]);
+        vals[j] = (uint32_t)j;
+    }
 }
 
 template <class K>
-__global__ void k_flag_heads(const K *__restrict__ k, int64_t n, int32_t *__restrict__ f) {
-    int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (j < n) f[j] = (j == 0 || k[j] != k[j - 1]) ? 1 : 0;
+__global__ void k_flag_heads(const K *__restrict__ k, const int64_t *__restrict__ d_n,
+                             int32_t *__restrict__ f) {
+    const int64_t n = *d_n;
+    SFB_FOR(j, n) f[j] = (j == 0 || k[j] != k[j - 1]) ? 1 : 0;
 }
 
 template <class K>
 __global__ void k_pool_segments(const K *__restrict__ keys, const uint32_t *__restrict__ vals,
-                                const int32_t *__restrict__ incl, int64_t m, ParentLayout L,
+                                const int32_t *__restrict__ incl, const int64_t *__restrict__ d_m,
+                                int64_t S, const FrameParams *__restrict__ P,
                                 int32_t *__restrict__ pcoords, int32_t *__restrict__ seg_start,
-                                int32_t *__restrict__ child_to_parent) {
-    int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (j >= m) return;
-    int32_t v = incl[j] - 1;
-    child_to_parent[vals[j]] = v;
-    if (j == m - 1) seg_start[v + 1] = (int32_t)m;
-    if (j == 0 || incl[j - 1] != incl[j]) {
-        uint64_t k = (uint64_t)keys[j];
-        int64_t qx = (int64_t)(k & ((1ull << L.bits[0]) - 1));
-        int64_t qy = (int64_t)((k >> L.bits[0]) & ((1ull << L.bits[1]) - 1));
-        int64_t qz = (int64_t)(k >> (L.bits[0] + L.bits[1]));
-        pcoords[3 * v + 0] = (int32_t)(qx * L.step + L.lo[0]);
-        pcoords[3 * v + 1] = (int32_t)(qy * L.step + L.lo[1]);
-        pcoords[3 * v + 2] = (int32_t)(qz * L.step + L.lo[2]);
-        seg_start[v] = (int32_t)j;
+                                int32_t *__restrict__ child_to_parent, int64_t *__restrict__ d_mp) {
+    int64_t plo[3];
+    int pb[3];
+    parent_layout(P, S, plo, pb);
+    const int64_t m = *d_m;
+    SFB_FOR(j, m) {
+        const int32_t v = incl[j] - 1;
+        child_to_parent[vals[j]] = v;
+        if (j == m - 1) {
+            seg_start[v + 1] = (int32_t)m;
+            *d_mp = v + 1;
+        }
+        if (j == 0 || incl[j - 1] != incl[j]) {
+            const uint64_t k = (uint64_t)keys[j];
+            const int64_t qx = (int64_t)(k & ((1ull << pb[0]) - 1));
+            const int64_t qy = (int64_t)((k >> pb[0]) & ((1ull << pb[1]) - 1));
+            const int64_t qz = (int64_t)(k >> (pb[0] + pb[1]));
+            pcoords[3 * v + 0] = (int32_t)(qx * S + plo[0]);
+            pcoords[3 * v + 1] = (int32_t)(qy * S + plo[1]);
+            pcoords[3 * v + 2] = (int32_t)(qz * S + plo[2]);
+            seg_start[v] = (int32_t)j;
+        }
     }
 }
 
 // thread per (parent, channel): ordered float32 mean of its children
 __global__ void k_pool_means(const float *__restrict__ feats, int ld_in, int c,
                              const uint32_t *__restrict__ child_rows,
-                             const int32_t *__restrict__ seg_start, int64_t mp,
+                             const int32_t *__restrict__ seg_start, const int64_t *__restrict__ d_mp,
                              float *__restrict__ out, int ld_out) {
-    int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (idx >= mp * c) return;
-    int64_t v = idx / c;
-    int ch = (int)(idx % c);
-    int32_t b = seg_start[v], e = seg_start[v + 1];
-    float acc = 0.f;
-    for (int32_t j = b; j < e; ++j) acc = __fadd_rn(acc, feats[(int64_t)child_rows[j] * ld_in + ch]);
-    out[v * ld_out + ch] = __fdiv_rn(acc, (float)(e - b));
+    const int64_t mp = *d_mp;
+    SFB_FOR(idx, mp * c) {
+        const int64_t v = idx / c;
+        const int ch = (int)(idx % c);
+        const int32_t b = seg_start[v], e = seg_start[v + 1];
+        float acc = 0.f;
+        for (int32_t j = b; j < e; ++j) acc = __fadd_rn(acc, feats[(int64_t)child_rows[j] * ld_in + ch]);
+        out[v * ld_out + ch] = __fdiv_rn(acc, (float)(e - b));
+    }
 }
 
 template <class K>
-static int64_t pool_typed(sfb_ctx *ctx, const int32_t *coords, int64_t m, const ParentLayout &L,
-                          const float *feats, int c, int ld_in, int32_t *parent_coords,
-                          float *parent_feats, int ld_out, int32_t *child_to_parent) {
+static void pool_typed(sfb_ctx *ctx, const int32_t *coords, const int64_t *d_m, int64_t m_bound,
+                       int stride, const FrameParams *P, int key_bits, const float *feats, int c,
+                       int ld_in, int32_t *parent_coords, float *parent_feats, int ld_out,
+                       int32_t *child_to_parent, int64_t *d_mp) {
     cudaStream_t st = ctx->stream;
-    K *keys = ctx->arena.alloc<K>(m), *keys2 = ctx->arena.alloc<K>(m);
-    uint32_t *vals = ctx->arena.alloc<uint32_t>(m), *vals2 = ctx->arena.alloc<uint32_t>(m);
-    int32_t *flag = ctx->arena.alloc<int32_t>(m), *incl = ctx->arena.alloc<int32_t>(m);
-    int32_t *seg = ctx->arena.alloc<int32_t>(m + 1);
-    unsigned g = grid_for(m, 256);
-    k_parent_keys<K><<<g, 256, 0, st>>>(coords, m, L, keys, vals);
-    size_t tb = 0, tb2 = 0;
-    int bits = L.total > 0 ? L.total : 1;
-    cub::DeviceRadixSort::SortPairs(nullptr, tb, keys, keys2, vals, vals2, (int)m, 0, bits, st);
-    cub::DeviceScan::InclusiveSum(nullptr, tb2, flag, incl, (int)m, st);
-    void *tmp = ctx->arena.alloc_bytes(tb > tb2 ? tb : tb2);
-    SFB_CUDA(cub::DeviceRadixSort::SortPairs(tmp, tb, keys, keys2, vals, vals2, (int)m, 0, bits, st));
-    k_flag_heads<K><<<g, 256, 0, st>>>(keys2, m, flag);
-    SFB_CUDA(cub::DeviceScan::InclusiveSum(tmp, tb2, flag, incl, (int)m, st));
-    k_pool_segments<K><<<g, 256, 0, st>>>(keys2, vals2, incl, m, L, parent_coords, seg,
-                                          child_to_parent);
+    const int64_t S = 2 * (int64_t)stride;
+    K *keys = ctx->arena.alloc<K>(m_bound), *keys2 = ctx->arena.alloc<K>(m_bound);
+    uint32_t *vals = ctx->arena.alloc<uint32_t>(m_bound), *vals2 = ctx->arena.alloc<uint32_t>(m_bound);
+    int32_t *flag = ctx->arena.alloc<int32_t>(m_bound);
+    int32_t *seg = ctx->arena.alloc<int32_t>(m_bound + 1);
+    const unsigned g = dgrid(m_bound, 256);
+    k_parent_keys<K><<<g, 256, 0, st>>>(coords, d_m, S, P, keys, vals);
     SFB_CHECK_LAUNCH();
-    ctx->read_back(incl + (m - 1), sizeof(int32_t));
-    int64_t mp = *reinterpret_cast<int32_t *>(ctx->pinned);
+    const int which = dsort_pairs<K>(ctx, keys, vals, keys2, vals2, d_m, m_bound, key_bits);
+    K *ks = which ? keys2 : keys;
+    uint32_t *vs = which ? vals2 : vals;
+    k_flag_heads<K><<<g, 256, 0, st>>>(ks, d_m, flag);
+    dscan(ctx, flag, flag, d_m, m_bound, nullptr, true);
+    k_pool_segments<K><<<g, 256, 0, st>>>(ks, vs, flag, d_m, S, P, parent_coords, seg,
+                                          child_to_parent, d_mp);
+    SFB_CHECK_LAUNCH();
     if (feats && c > 0) {
-        k_pool_means<<<grid_for(mp * c, 256), 256, 0, st>>>(feats, ld_in, c, vals2, seg, mp,
-                                                            parent_feats, ld_out);
+        k_pool_means<<<dgrid(m_bound * c, 256), 256, 0, st>>>(feats, ld_in, c, vs, seg, d_mp,
+                                                               parent_feats, ld_out);
         SFB_CHECK_LAUNCH();
     }
-    return mp;
 }
 
-int64_t pool_build(sfb_ctx *ctx, const int32_t *coords, int64_t m, int stride, const float *feats,
-                   int c, int ld_in, int32_t *parent_coords, float *parent_feats, int ld_out,
-                   int32_t *child_to_parent) {
+void pool_build(sfb_ctx *ctx, const int32_t *coords, const int64_t *d_m, int64_t m_bound,
+                int stride, const FrameParams &host, const FrameParams *P, const float *feats,
+                int c, int ld_in, int32_t *parent_coords, float *parent_feats, int ld_out,
+                int32_t *child_to_parent, int64_t *d_mp) {
+    const int bits = host.total > 0 ? host.total : 1;
+    if (host.total <= 32)
+        pool_typed<uint32_t>(ctx, coords, d_m, m_bound, stride, P, bits, feats, c, ld_in,
+                             parent_coords, parent_feats, ld_out, child_to_parent, d_mp);
+    else
+        pool_typed<unsigned long long>(ctx, coords, d_m, m_bound, stride, P, bits, feats, c, ld_in,
+                                       parent_coords, parent_feats, ld_out, child_to_parent, d_mp);
+}
+
+// Key layout of an arbitrary coordinate set (standalone pool API): one
+// reduction + read-back, then the same layout type the frame uses.
+__global__ void k_int_bbox_init(int *mm) {
+    if (threadIdx.x < 3) mm[threadIdx.x] = INT_MAX;
+    else if (threadIdx.x < 6) mm[threadIdx.x] = INT_MIN;
+}
+__global__ void k_int_bbox(const int32_t *__restrict__ c, int64_t m, int *mm) {
+    int lo[3] = {INT_MAX, INT_MAX, INT_MAX}, hi[3] = {INT_MIN, INT_MIN, INT_MIN};
+    SFB_FOR(i, m)
+    for (int a = 0; a < 3; ++a) {
+        lo[a] = min(lo[a], c[3 * i + a]);
+        hi[a] = max(hi[a], c[3 * i + a]);
+    }
+    for (int a = 0; a < 3; ++a) {
+        atomicMin(&mm[a], lo[a]);
+        atomicMax(&mm[3 + a], hi[a]);
+    }
+}
+
+void coords_layout(sfb_ctx *ctx, const int32_t *coords, int64_t m, FrameParams &P) {
     SFB_REQUIRE(m > 0, "cannot pool an empty grid");
     int *mm = ctx->arena.alloc<int>(6);
     k_int_bbox_init<<<1, 32, 0, ctx->stream>>>(mm);
-    k_int_bbox<<<grid_for(m, 256, 256), 256, 0, ctx->stream>>>(coords, m, mm);
+    k_int_bbox<<<dgrid(m, 256, 2), 256, 0, ctx->stream>>>(coords, m, mm);
     SFB_CHECK_LAUNCH();
     ctx->read_back(mm, 6 * sizeof(int));
     const int *h = reinterpret_cast<const int *>(ctx->pinned);
-    ParentLayout L{};
-    L.step = 2 * (int64_t)stride;
-    L.total = 0;
+    P = FrameParams{};
+    P.total = 0;
     for (int a = 0; a < 3; ++a) {
-        int64_t lo = floor_div(h[a], L.step) * L.step, hi = floor_div(h[3 + a], L.step) * L.step;
-        L.lo[a] = lo;
-        L.bits[a] = bits_for((uint64_t)((hi - lo) / L.step));
-        L.total += L.bits[a];
+        P.lo[a] = h[a];
+        P.bits[a] = bits_for((uint64_t)((int64_t)h[3 + a] - h[a]));
+        P.total += P.bits[a];
     }
-    if (L.total <= 32)
-        return pool_typed<uint32_t>(ctx, coords, m, L, feats, c, ld_in, parent_coords,
-                                    parent_feats, ld_out, child_to_parent);
-    return pool_typed<uint64_t>(ctx, coords, m, L, feats, c, ld_in, parent_coords, parent_feats,
-                                ld_out, child_to_parent);
+    P.total += 3;  // parent ranges may need one more bit per axis
 }
 
 }  // namespace sfb

@@ -20,7 +20,8 @@
 namespace sfb {
 
 void conv_layer_tc(sfb_ctx *ctx, const NetLayer &L, const float *in, int ld_in, const int32_t *nbr,
-                   int64_t m, int relu, float *out, int ld_out);
+                   int64_t nbr_ld, const int64_t *d_m, int64_t m_bound, int relu, float *out,
+                   int ld_out);
 bool conv_tc_supported(const NetLayer &L);
 void prepare_tc_weights(sfb_ctx *ctx, NetLayer &L);
 
@@ -152,61 +153,66 @@ constexpr int kThreads = 256;
 constexpr int kMaxOut = 16;  // kRows * cout / kThreads for cout <= 128
 
 __global__ void __launch_bounds__(kThreads)
-k_conv_simt(const float *__restrict__ in, int ld_in, const int32_t *__restrict__ nbr, int64_t m,
-            int taps, int cin, int cout, const float *__restrict__ w, const float *__restrict__ b,
-            int relu, float *__restrict__ out, int ld_out) {
+k_conv_simt(const float *__restrict__ in, int ld_in, const int32_t *__restrict__ nbr, int64_t nbr_ld,
+            const int64_t *__restrict__ d_m, int64_t m_fixed, int taps, int cin, int cout,
+            const float *__restrict__ w, const float *__restrict__ b, int relu,
+            float *__restrict__ out, int ld_out) {
     extern __shared__ float sm[];
     float *A = sm;                  // [kRows][cin]
     float *W = sm + kRows * cin;    // [cin][cout]
-    int64_t r0 = (int64_t)blockIdx.x * kRows;
-    int nout = kRows * cout;
-    float acc[kMaxOut];
+    const int64_t m = d_m ? *d_m : m_fixed;
+    const int nout = kRows * cout;
+    for (int64_t r0 = (int64_t)blockIdx.x * kRows; r0 < m; r0 += (int64_t)gridDim.x * kRows) {
+        float acc[kMaxOut];
 #pragma unroll
-    for (int k = 0; k < kMaxOut; ++k) acc[k] = 0.f;
-    for (int t = 0; t < taps; ++t) {
-        int any = 0;
-        for (int i = threadIdx.x; i < kRows * cin; i += kThreads) {
-            int r = i / cin, ci = i % cin;
-            int64_t row = r0 + r;
-            int32_t src = row < m ? nbr[(int64_t)t * m + row] : -1;
-            any |= src >= 0;
-            A[i] = src >= 0 ? in[(int64_t)src * ld_in + ci] : 0.f;
+        for (int k = 0; k < kMaxOut; ++k) acc[k] = 0.f;
+        for (int t = 0; t < taps; ++t) {
+            int any = 0;
+            for (int i = threadIdx.x; i < kRows * cin; i += kThreads) {
+                int r = i / cin, ci = i % cin;
+                int64_t row = r0 + r;
+                int32_t src = row < m ? nbr[(int64_t)t * nbr_ld + row] : -1;
+                any |= src >= 0;
+                A[i] = src >= 0 ? in[(int64_t)src * ld_in + ci] : 0.f;
+            }
+            if (!__syncthreads_or(any)) continue;
+            const float *wt = w + (size_t)t * cin * cout;
+            for (int i = threadIdx.x; i < cin * cout; i += kThreads) W[i] = wt[i];
+            __syncthreads();
+#pragma unroll
+            for (int k = 0; k < kMaxOut; ++k) {
+                int o = threadIdx.x + k * kThreads;
+                if (o < nout) {
+                    int r = o / cout, co = o % cout;
+                    float sacc = acc[k];
+                    for (int ci = 0; ci < cin; ++ci) sacc = fmaf(A[r * cin + ci], W[ci * cout + co], sacc);
+                    acc[k] = sacc;
+                }
+            }
+            __syncthreads();
         }
-        if (!__syncthreads_or(any)) continue;
-        const float *wt = w + (size_t)t * cin * cout;
-        for (int i = threadIdx.x; i < cin * cout; i += kThreads) W[i] = wt[i];
-        __syncthreads();
 #pragma unroll
         for (int k = 0; k < kMaxOut; ++k) {
             int o = threadIdx.x + k * kThreads;
             if (o < nout) {
                 int r = o / cout, co = o % cout;
-                float s = acc[k];
-                for (int ci = 0; ci < cin; ++ci) s = fmaf(A[r * cin + ci], W[ci * cout + co], s);
-                acc[k] = s;
+                int64_t row = r0 + r;
+                if (row < m) {
+                    float v = acc[k] + b[co];
+                    out[row * ld_out + co] = relu ? fmaxf(v, 0.f) : v;
+                }
             }
         }
         __syncthreads();
     }
-#pragma unroll
-    for (int k = 0; k < kMaxOut; ++k) {
-        int o = threadIdx.x + k * kThreads;
-        if (o < nout) {
-            int r = o / cout, co = o % cout;
-            int64_t row = r0 + r;
-            if (row < m) {
-                float v = acc[k] + b[co];
-                out[row * ld_out + co] = relu ? fmaxf(v, 0.f) : v;
-            }
-        }
-    }
 }
 
 void conv_layer(sfb_ctx *ctx, const NetLayer &L, const float *in, int ld_in, const int32_t *nbr,
-                int64_t m, int relu, float *out, int ld_out) {
-    if (m == 0) return;
+                int64_t nbr_ld, const int64_t *d_m, int64_t m_bound, int relu, float *out,
+                int ld_out) {
+    if (m_bound == 0) return;
     if (ctx->net_mode == SFB_NET_TC_TF32X3 && L.w_tc) {
-        conv_layer_tc(ctx, L, in, ld_in, nbr, m, relu, out, ld_out);
+        conv_layer_tc(ctx, L, in, ld_in, nbr, nbr_ld, d_m, m_bound, relu, out, ld_out);
         return;
     }
     SFB_REQUIRE(kRows * L.cout <= kMaxOut * kThreads, "conv: cout > 128 unsupported");
@@ -218,69 +224,73 @@ void conv_layer(sfb_ctx *ctx, const NetLayer &L, const float *in, int ld_in, con
                                       200 * 1024));
         attr = true;
     }
-    k_conv_simt<<<grid_for(m, kRows), kThreads, smem, ctx->stream>>>(
-        in, ld_in, nbr, m, L.taps, L.cin, L.cout, L.w, L.b, relu, out, ld_out);
+    k_conv_simt<<<dgrid(m_bound, kRows, 4), kThreads, smem, ctx->stream>>>(
+        in, ld_in, nbr, nbr_ld, d_m, m_bound, L.taps, L.cin, L.cout, L.w, L.b, relu, out, ld_out);
     SFB_CHECK_LAUNCH();
 }
 
 // transposed conv: out[r] = b + in[parent[r]] @ W[tap[r]]  (orphans: bias only)
 __global__ void k_tconv(const float *__restrict__ in, int ld_in, const int32_t *__restrict__ parent,
-                        const int32_t *__restrict__ tap, int64_t m, int cin, int cout,
-                        const float *__restrict__ w, const float *__restrict__ b, int relu,
-                        float *__restrict__ out, int ld_out) {
-    int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (idx >= m * cout) return;
-    int64_t r = idx / cout;
-    int co = (int)(idx % cout);
-    int32_t p = parent[r];
-    float s = 0.f;
-    if (p >= 0) {
-        const float *x = in + (int64_t)p * ld_in;
-        const float *wt = w + (size_t)tap[r] * cin * cout + co;
-        for (int ci = 0; ci < cin; ++ci) s = fmaf(x[ci], wt[(size_t)ci * cout], s);
+                        const int32_t *__restrict__ tap, const int64_t *__restrict__ d_m,
+                        int64_t m_fixed, int cin, int cout, const float *__restrict__ w,
+                        const float *__restrict__ b, int relu, float *__restrict__ out, int ld_out) {
+    const int64_t m = d_m ? *d_m : m_fixed;
+    SFB_FOR(idx, m * cout) {
+        const int64_t r = idx / cout;
+        const int co = (int)(idx % cout);
+        const int32_t p = parent[r];
+        float s = 0.f;
+        if (p >= 0) {
+            const float *x = in + (int64_t)p * ld_in;
+            const float *wt = w + (size_t)tap[r] * cin * cout + co;
+            for (int ci = 0; ci < cin; ++ci) s = fmaf(x[ci], wt[(size_t)ci * cout], s);
+        }
+        const float v = s + b[co];
+        out[r * ld_out + co] = relu ? fmaxf(v, 0.f) : v;
     }
-    float v = s + b[co];
-    out[r * ld_out + co] = relu ? fmaxf(v, 0.f) : v;
 }
 
 void tconv_layer(sfb_ctx *ctx, const NetLayer &L, const float *in, int ld_in,
-                 const int32_t *parent, const int32_t *tap, int64_t m, int relu, float *out,
-                 int ld_out) {
-    if (m == 0) return;
-    k_tconv<<<grid_for(m * L.cout, 256), 256, 0, ctx->stream>>>(in, ld_in, parent, tap, m, L.cin,
-                                                                 L.cout, L.w, L.b, relu, out, ld_out);
+                 const int32_t *parent, const int32_t *tap, const int64_t *d_m, int64_t m_bound,
+                 int relu, float *out, int ld_out) {
+    if (m_bound == 0) return;
+    k_tconv<<<dgrid(m_bound * L.cout, 256), 256, 0, ctx->stream>>>(
+        in, ld_in, parent, tap, d_m, m_bound, L.cin, L.cout, L.w, L.b, relu, out, ld_out);
     SFB_CHECK_LAUNCH();
 }
 
 // child tap from coordinates (child stride cs, parent stride 2cs)
-__global__ void k_child_tap(const int32_t *__restrict__ coords, int64_t m, int cs,
-                            int32_t *__restrict__ tap) {
-    int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (r >= m) return;
-    int64_t ps = 2 * (int64_t)cs;
-    int64_t d[3];
-    for (int a = 0; a < 3; ++a) {
-        int64_t c = coords[3 * r + a];
-        d[a] = (c - floor_div(c, ps) * ps) / cs;
+__global__ void k_child_tap(const int32_t *__restrict__ coords, const int64_t *__restrict__ d_m,
+                            int cs, int32_t *__restrict__ tap) {
+    const int64_t m = *d_m;
+    const int64_t ps = 2 * (int64_t)cs;
+    SFB_FOR(r, m) {
+        int64_t d[3];
+        for (int a = 0; a < 3; ++a) {
+            int64_t c = coords[3 * r + a];
+            d[a] = (c - floor_div(c, ps) * ps) / cs;
+        }
+        tap[r] = (int32_t)(d[2] * 4 + d[1] * 2 + d[0]);
     }
-    tap[r] = (int32_t)(d[2] * 4 + d[1] * 2 + d[0]);
 }
 
 // ------------------------------------------------------------ MLP head
 constexpr int kHeadRows = 32;
 
-__global__ void k_head_mlp(const float *__restrict__ f, int ld, int64_t m, int cin, int hid,
-                           const float *__restrict__ w1, const float *__restrict__ b1,
-                           const float *__restrict__ w2, const float *__restrict__ b2,
-                           float *__restrict__ raw) {
+__global__ void k_head_mlp(const float *__restrict__ f, int ld, const int64_t *__restrict__ d_m,
+                           int cin, int hid, const float *__restrict__ w1,
+                           const float *__restrict__ b1, const float *__restrict__ w2,
+                           const float *__restrict__ b2, float *__restrict__ raw) {
     extern __shared__ float sm[];
     float *F = sm;                         // [rows][cin]
     float *H = F + kHeadRows * cin;        // [rows][hid]
     float *W1 = H + kHeadRows * hid;       // [cin][hid]
     float *W2 = W1 + cin * hid;            // [hid][14]
-    int64_t r0 = (int64_t)blockIdx.x * kHeadRows;
+    const int64_t m = *d_m;
     for (int i = threadIdx.x; i < cin * hid; i += blockDim.x) W1[i] = w1[i];
     for (int i = threadIdx.x; i < hid * 14; i += blockDim.x) W2[i] = w2[i];
+    for (int64_t r0 = (int64_t)blockIdx.x * kHeadRows; r0 < m; r0 += (int64_t)gridDim.x * kHeadRows) {
+    __syncthreads();
     for (int i = threadIdx.x; i < kHeadRows * cin; i += blockDim.x) {
         int64_t row = r0 + i / cin;
         F[i] = row < m ? f[row * ld + i % cin] : 0.f;
@@ -300,6 +310,7 @@ __global__ void k_head_mlp(const float *__restrict__ f, int ld, int64_t m, int c
         float s = 0.f;
         for (int c = 0; c < hid; ++c) s = fmaf(H[r * hid + c], W2[c * 14 + k], s);
         raw[row * 14 + k] = s + b2[k];
+    }
     }
 }
 
@@ -368,11 +379,12 @@ void activate_run(sfb_ctx *ctx, const float *raw, int64_t m, double scale, doubl
 // Per-voxel Gaussian: centre = (coord + 0.5 + residual) * scale + delta
 // (voxelgrid.py:119-122 + estimators.py:223), then the activated fields.
 __global__ void k_voxel_splats(const float *__restrict__ raw, const int32_t *__restrict__ coords,
-                               const double *__restrict__ feats9, int64_t m, double scale,
-                               double *centers, double *sigma, double *quat, double *opac,
-                               double *normal) {
-    int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (v >= m) return;
+                               const double *__restrict__ feats9, const int64_t *__restrict__ d_m,
+                               const FrameParams *__restrict__ P, double *centers, double *sigma,
+                               double *quat, double *opac, double *normal) {
+    const int64_t m = *d_m;
+    const double scale = P->inv_s;
+    SFB_FOR(v, m) {
     double delta[3];
     activate_row(raw + 14 * v, scale, delta, sigma + 3 * v, quat + 4 * v, opac + v, normal + 3 * v);
 #pragma unroll
@@ -381,70 +393,77 @@ __global__ void k_voxel_splats(const float *__restrict__ raw, const int32_t *__r
                                scale);
         centers[3 * v + a] = __dadd_rn(rec, delta[a]);
     }
+    }
 }
 
 void head_to_voxel_splats(sfb_ctx *ctx, const float *raw, const int32_t *coords,
-                          const double *feats9, int64_t m0, double scale, double *centers,
-                          double *sigma, double *quat, double *opac, double *normal) {
-    k_voxel_splats<<<grid_for(m0, 128), 128, 0, ctx->stream>>>(raw, coords, feats9, m0, scale,
-                                                               centers, sigma, quat, opac, normal);
+                          const double *feats9, const int64_t *d_m, int64_t m_bound,
+                          const FrameParams *P, double *centers, double *sigma, double *quat,
+                          double *opac, double *normal) {
+    k_voxel_splats<<<dgrid(m_bound, 128), 128, 0, ctx->stream>>>(raw, coords, feats9, d_m, P,
+                                                                 centers, sigma, quat, opac, normal);
     SFB_CHECK_LAUNCH();
 }
 
 // ------------------------------------------------------------ UNet
-__global__ void k_feats_to_f32(const double *__restrict__ f, int64_t n, float *__restrict__ o) {
-    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (i < n) o[i] = (float)f[i];
+__global__ void k_feats_to_f32(const double *__restrict__ f, const int64_t *__restrict__ d_m, int c,
+                               float *__restrict__ o) {
+    const int64_t n = *d_m * c;
+    SFB_FOR(i, n) o[i] = (float)f[i];
 }
 
-void unet_run(sfb_ctx *ctx, const int32_t *coords0, const double *feats9, int64_t m0, float *raw) {
+// Whole UNet + head with every level size kept on the device: buffers are
+// sized by the host bound (the point count bounds every level), kernels loop
+// over the device counts, so the sequence has no host synchronisation.
+void unet_run(sfb_ctx *ctx, const int32_t *coords0, const double *feats9, int64_t mb,
+              const FrameParams &host, const FrameParams *P, DevCounts *C, float *raw) {
     Net &net = ctx->net;
     SFB_REQUIRE(net.loaded, "network weights are not loaded");
     const int L = net.levels;
+    SFB_REQUIRE(L + 1 <= 9, "at most 8 UNet levels");
     const auto &enc = net.enc;
     const auto &dec = net.dec;
-    SFB_REQUIRE(m0 > 0, "empty voxel grid");
     cudaStream_t st = ctx->stream;
-    std::vector<int64_t> M(L + 1);
     std::vector<const int32_t *> coords(L + 1);
     std::vector<int32_t *> nbr(L + 1), c2p(L);
     std::vector<float *> cat(L), pin(L + 1);
     std::vector<int> width(L);
-    M[0] = m0;
     coords[0] = coords0;
     for (int l = 0; l < L; ++l) width[l] = dec[L - 1 - l] + enc[l + 1];
-    pin[0] = ctx->arena.alloc<float>((size_t)m0 * enc[0]);
-    k_feats_to_f32<<<grid_for(m0 * enc[0], 256), 256, 0, st>>>(feats9, m0 * enc[0], pin[0]);
+    pin[0] = ctx->arena.alloc<float>((size_t)mb * enc[0]);
+    k_feats_to_f32<<<dgrid(mb * enc[0], 256), 256, 0, st>>>(feats9, &C->m[0], enc[0], pin[0]);
     SFB_CHECK_LAUNCH();
     int layer = 0;
     for (int l = 0; l <= L; ++l) {
-        int stride = 1 << l;
-        HashTable h = hash_build(ctx, coords[l], M[l]);
-        int kern = net.layers[layer].kernel, taps = kern * kern * kern;
-        nbr[l] = ctx->arena.alloc<int32_t>((size_t)taps * M[l]);
-        kernel_map_build(ctx, h, coords[l], M[l], stride, kern, nbr[l]);
+        const int stride = 1 << l;
+        const int64_t *dm = &C->m[l];
+        HashTable h = hash_build(ctx, coords[l], dm, mb);
+        const int kern = net.layers[layer].kernel, taps = kern * kern * kern;
+        nbr[l] = ctx->arena.alloc<int32_t>((size_t)taps * mb);
+        kernel_map_build(ctx, h, coords[l], dm, mb, stride, kern, nbr[l]);
         if (l == L) break;
-        cat[l] = ctx->arena.alloc<float>((size_t)M[l] * width[l]);
-        int up = dec[L - 1 - l];
-        conv_layer(ctx, net.layers[layer++], pin[l], enc[l], nbr[l], M[l], 1, cat[l] + up, width[l]);
-        // pool the skip features into the next level's input
-        int32_t *pc = ctx->arena.alloc<int32_t>((size_t)M[l] * 3);
-        pin[l + 1] = ctx->arena.alloc<float>((size_t)M[l] * enc[l + 1]);
-        c2p[l] = ctx->arena.alloc<int32_t>(M[l]);
-        M[l + 1] = pool_build(ctx, coords[l], M[l], stride, cat[l] + up, enc[l + 1], width[l], pc,
-                              pin[l + 1], enc[l + 1], c2p[l]);
+        cat[l] = ctx->arena.alloc<float>((size_t)mb * width[l]);
+        const int up = dec[L - 1 - l];
+        conv_layer(ctx, net.layers[layer++], pin[l], enc[l], nbr[l], mb, dm, mb, 1, cat[l] + up,
+                   width[l]);
+        int32_t *pc = ctx->arena.alloc<int32_t>((size_t)mb * 3);
+        pin[l + 1] = ctx->arena.alloc<float>((size_t)mb * enc[l + 1]);
+        c2p[l] = ctx->arena.alloc<int32_t>(mb);
+        pool_build(ctx, coords[l], dm, mb, stride, host, P, cat[l] + up, enc[l + 1], width[l], pc,
+                   pin[l + 1], enc[l + 1], c2p[l], &C->m[l + 1]);
         coords[l + 1] = pc;
     }
-    // bottleneck
-    float *bott = ctx->arena.alloc<float>((size_t)M[L] * enc[L + 1]);
-    conv_layer(ctx, net.layers[layer++], pin[L], enc[L], nbr[L], M[L], 1, bott, enc[L + 1]);
+    float *bott = ctx->arena.alloc<float>((size_t)mb * enc[L + 1]);
+    conv_layer(ctx, net.layers[layer++], pin[L], enc[L], nbr[L], mb, &C->m[L], mb, 1, bott,
+               enc[L + 1]);
     const float *coarse = bott;
     int ld_coarse = enc[L + 1];
     for (int l = L - 1; l >= 0; --l) {
-        int32_t *tap = ctx->arena.alloc<int32_t>(M[l]);
-        k_child_tap<<<grid_for(M[l], 256), 256, 0, st>>>(coords[l], M[l], 1 << l, tap);
+        int32_t *tap = ctx->arena.alloc<int32_t>(mb);
+        k_child_tap<<<dgrid(mb, 256), 256, 0, st>>>(coords[l], &C->m[l], 1 << l, tap);
         SFB_CHECK_LAUNCH();
-        tconv_layer(ctx, net.layers[layer++], coarse, ld_coarse, c2p[l], tap, M[l], 1, cat[l], width[l]);
+        tconv_layer(ctx, net.layers[layer++], coarse, ld_coarse, c2p[l], tap, &C->m[l], mb, 1,
+                    cat[l], width[l]);
         coarse = cat[l];
         ld_coarse = width[l];
     }
@@ -458,10 +477,9 @@ void unet_run(sfb_ctx *ctx, const int32_t *coords0, const double *feats9, int64_
         attr = true;
     }
     SFB_REQUIRE(smem <= 200 * 1024, "head MLP too wide");
-    k_head_mlp<<<grid_for(m0, kHeadRows), 128, smem, st>>>(cat[0], width[0], m0, h1.cin, h1.cout,
-                                                           h1.w, h1.b, h2.w, h2.b, raw);
+    k_head_mlp<<<dgrid(mb, kHeadRows, 4), 128, smem, st>>>(cat[0], width[0], &C->m[0], h1.cin,
+                                                           h1.cout, h1.w, h1.b, h2.w, h2.b, raw);
     SFB_CHECK_LAUNCH();
-    for (int l = 0; l <= L && l < 8; ++l) ctx->stats.voxels[l] = M[l];
 }
 
 }  // namespace sfb

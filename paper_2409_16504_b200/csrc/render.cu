@@ -36,44 +36,22 @@ constexpr int kSuper = 8;      // tiles per super-tile edge
 constexpr int kSuperMax = 16;  // super tiles per run at the middle level
 constexpr int kWin = 2048;     // rank window of the merge
 constexpr int kCT = 256;       // compositor threads per CTA
-constexpr int kPre = 4;        // staged points per run
-
-struct Cam {
-    double r[9], t[3], fx, fy, cx, cy;
-    int64_t w, h;
-};
-
-static Cam to_cam(const sfb_camera &c) {
-    Cam k;
-    for (int i = 0; i < 9; ++i) k.r[i] = c.rot[i];
-    for (int i = 0; i < 3; ++i) k.t[i] = c.trans[i];
-    k.fx = c.fx;
-    k.fy = c.fy;
-    k.cx = c.cx;
-    k.cy = c.cy;
-    k.w = c.width;
-    k.h = c.height;
-    return k;
-}
+constexpr int kPre = 16;       // staged points per run
+constexpr int kChunk = 64;     // runs per compositing chunk
 
 // ------------------------------------------------------------ 1. projection
-__global__ void k_project(const double *__restrict__ centers, const double *__restrict__ quats,
-                          const double *__restrict__ scales, int64_t n, Cam C, double z_near,
-                          double dil, double *__restrict__ sx, double *__restrict__ sy,
-                          double *__restrict__ depth, double *__restrict__ ca,
-                          double *__restrict__ cb, double *__restrict__ cc,
-                          double *__restrict__ rad3, uint8_t *__restrict__ keep) {
-    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (i >= n) return;
-    const double *p = centers + 3 * i;
+__device__ __forceinline__ void project_one(const double *__restrict__ p, const double *__restrict__ q,
+                                            const double *__restrict__ sc, const Cam &C, double z_near,
+                                            double dil, double *o_sx, double *o_sy, double *o_d,
+                                            double *o_a, double *o_b, double *o_c, double *o_r,
+                                            uint8_t *o_keep) {
     const double *R = C.r;
     double px = R[0] * p[0] + R[1] * p[1] + R[2] * p[2] + C.t[0];
     double py = R[3] * p[0] + R[4] * p[1] + R[5] * p[2] + C.t[1];
     double pz = R[6] * p[0] + R[7] * p[1] + R[8] * p[2] + C.t[2];
     uint8_t ok = 0;
-    double o_sx = 0, o_sy = 0, o_d = 0, o_a = 0, o_b = 0, o_c = 0, o_r = 0;
+    double vsx = 0, vsy = 0, vd = 0, va = 0, vb = 0, vc = 0, vr = 0;
     if (pz > z_near) {
-        const double *q = quats + 4 * i;
         double w = q[0], x = q[1], y = q[2], z = q[3];
         double qn = sqrt(w * w + x * x + y * y + z * z);
         w /= qn;
@@ -89,8 +67,7 @@ __global__ void k_project(const double *__restrict__ centers, const double *__re
 #pragma unroll
             for (int b = 0; b < 3; ++b)
                 u[3 * a + b] = r[3 * a] * R[3 * b] + r[3 * a + 1] * R[3 * b + 1] + r[3 * a + 2] * R[3 * b + 2];
-        const double *s = scales + 3 * i;
-        double d0 = s[0] * s[0], d1 = s[1] * s[1], d2 = s[2] * s[2];
+        double d0 = sc[0] * sc[0], d1 = sc[1] * sc[1], d2 = sc[2] * sc[2];
 #define SIG(j, k) (d0 * u[j] * u[k] + d1 * u[3 + j] * u[3 + k] + d2 * u[6 + j] * u[6 + k])
         double s00 = SIG(0, 0), s01 = SIG(0, 1), s02 = SIG(0, 2);
         double s11 = SIG(1, 1), s12 = SIG(1, 2), s22 = SIG(2, 2);
@@ -107,33 +84,47 @@ __global__ void k_project(const double *__restrict__ centers, const double *__re
         if (!(csx + rr < 0.0 || csx - rr > (double)C.w - 1.0 || csy + rr < 0.0 ||
               csy - rr > (double)C.h - 1.0)) {
             ok = 1;
-            o_sx = csx;
-            o_sy = csy;
-            o_d = pz;
-            o_a = a;
-            o_b = b;
-            o_c = c;
-            o_r = rr;
+            vsx = csx;
+            vsy = csy;
+            vd = pz;
+            va = a;
+            vb = b;
+            vc = c;
+            vr = rr;
         }
     }
-    sx[i] = o_sx;
-    sy[i] = o_sy;
-    depth[i] = o_d;
-    ca[i] = o_a;
-    cb[i] = o_b;
-    cc[i] = o_c;
-    rad3[i] = o_r;
-    keep[i] = ok;
+    *o_sx = vsx;
+    *o_sy = vsy;
+    *o_d = vd;
+    *o_a = va;
+    *o_b = vb;
+    *o_c = vc;
+    *o_r = vr;
+    *o_keep = ok;
+}
+
+__global__ void k_project(const double *__restrict__ centers, const double *__restrict__ quats,
+                          const double *__restrict__ scales, const int64_t *__restrict__ d_n,
+                          int64_t n_fixed, const FrameParams *__restrict__ FP, double z_near,
+                          double dil, double *__restrict__ sx, double *__restrict__ sy,
+                          double *__restrict__ depth, double *__restrict__ ca,
+                          double *__restrict__ cb, double *__restrict__ cc,
+                          double *__restrict__ rad3, uint8_t *__restrict__ keep) {
+    const int64_t n = d_n ? *d_n : n_fixed;
+    const Cam C = FP->cam;
+    SFB_FOR(i, n)
+    project_one(centers + 3 * i, quats + 4 * i, scales + 3 * i, C, z_near, dil, sx + i, sy + i,
+                depth + i, ca + i, cb + i, cc + i, rad3 + i, keep + i);
 }
 
 void project_run(sfb_ctx *ctx, const double *centers, const double *quats, const double *scales,
-                 int64_t n, const sfb_camera &cam, double z_near, double dilation, double *sx,
-                 double *sy, double *depth, double *ca, double *cb, double *cc, double *radius,
-                 uint8_t *keep) {
-    if (n == 0) return;
-    k_project<<<grid_for(n, 128), 128, 0, ctx->stream>>>(centers, quats, scales, n, to_cam(cam),
-                                                         z_near, dilation, sx, sy, depth, ca, cb,
-                                                         cc, radius, keep);
+                 const int64_t *d_n, int64_t n_bound, const FrameParams *FP, double z_near,
+                 double dilation, double *sx, double *sy, double *depth, double *ca, double *cb,
+                 double *cc, double *radius, uint8_t *keep) {
+    if (n_bound == 0) return;
+    k_project<<<dgrid(n_bound, 128), 128, 0, ctx->stream>>>(centers, quats, scales, d_n, n_bound, FP,
+                                                            z_near, dilation, sx, sy, depth, ca, cb,
+                                                            cc, radius, keep);
     SFB_CHECK_LAUNCH();
 }
 
@@ -143,9 +134,9 @@ struct Proj {
     uint8_t *keep;
 };
 
-static Proj project_inputs(sfb_ctx *ctx, const RenderInputs &in, const sfb_camera &cam) {
+static Proj project_inputs(sfb_ctx *ctx, const RenderInputs &in, const FrameParams *FP) {
     Proj P;
-    int64_t n = in.n_geom;
+    const int64_t n = in.n_geom;   // bound
     double *blk = ctx->arena.alloc<double>(7 * (size_t)(n > 0 ? n : 1));
     P.sx = blk;
     P.sy = blk + n;
@@ -155,59 +146,40 @@ static Proj project_inputs(sfb_ctx *ctx, const RenderInputs &in, const sfb_camer
     P.c = blk + 5 * n;
     P.r3 = blk + 6 * n;
     P.keep = ctx->arena.alloc<uint8_t>(n > 0 ? n : 1);
-    project_run(ctx, in.centers, in.quats, in.scales, n, cam, 0.01, 0.3, P.sx, P.sy, P.depth, P.a,
-                P.b, P.c, P.r3, P.keep);
+    project_run(ctx, in.centers, in.quats, in.scales, in.d_n_geom, n, FP, 0.01, 0.3, P.sx, P.sy,
+                P.depth, P.a, P.b, P.c, P.r3, P.keep);
     return P;
 }
 
-__global__ void k_point_keep(const uint8_t *__restrict__ keep, const int32_t *__restrict__ p2g,
-                             int64_t n, uint8_t *__restrict__ flag) {
-    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (i < n) flag[i] = keep[p2g ? p2g[i] : i];
+// key = depth bits of kept points (positive doubles order as uint64), ~0 for
+// culled ones so they sort last; warp-aggregated count of the kept points
+__global__ void k_depth_keys(int64_t n, const int32_t *__restrict__ p2g, const Proj P,
+                             unsigned long long *__restrict__ keys, uint32_t *__restrict__ vals,
+                             int64_t *__restrict__ d_kept) {
+    SFB_FOR(i, ((n + 31) & ~int64_t(31))) {
+        bool k = false;
+        unsigned long long key = ~0ull;
+        if (i < n) {
+            const int64_t g = p2g ? p2g[i] : i;
+            k = P.keep[g];
+            if (k) key = (unsigned long long)__double_as_longlong(P.depth[g]);
+            keys[i] = key;
+            vals[i] = (uint32_t)i;
+        }
+        const unsigned ball = __ballot_sync(0xffffffffu, k);
+        if ((threadIdx.x & 31) == 0 && ball) atomicAdd((unsigned long long *)d_kept, (unsigned long long)__popc(ball));
+    }
 }
 
-__global__ void k_depth_keys(const uint32_t *__restrict__ kept, const int32_t *__restrict__ num,
-                             const int32_t *__restrict__ p2g, const double *__restrict__ depth,
-                             unsigned long long *__restrict__ keys) {
-    int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (j >= *num) return;
-    uint32_t i = kept[j];
-    keys[j] = (unsigned long long)__double_as_longlong(depth[p2g ? p2g[i] : i]);
-}
-
-// returns K (host) and the rank -> point array `source`
-static int64_t depth_order(sfb_ctx *ctx, const RenderInputs &in, const Proj &P, uint32_t **source) {
-    cudaStream_t st = ctx->stream;
-    int64_t n = in.n_points;
-    if (n == 0) {
-        *source = nullptr;
-        return 0;
-    }
-    uint8_t *flag = ctx->arena.alloc<uint8_t>(n);
-    k_point_keep<<<grid_for(n, 256), 256, 0, st>>>(P.keep, in.point_to_geom, n, flag);
-    uint32_t *kept = ctx->arena.alloc<uint32_t>(n);
-    int32_t *num = ctx->arena.alloc<int32_t>(1);
-    cub::CountingInputIterator<uint32_t> iota(0);
-    size_t tb = 0;
-    cub::DeviceSelect::Flagged(nullptr, tb, iota, flag, kept, num, (int)n, st);
-    void *tmp = ctx->arena.alloc_bytes(tb);
-    SFB_CUDA(cub::DeviceSelect::Flagged(tmp, tb, iota, flag, kept, num, (int)n, st));
-    ctx->read_back(num, sizeof(int32_t));
-    int64_t K = *reinterpret_cast<int32_t *>(ctx->pinned);
-    if (K == 0) {
-        *source = nullptr;
-        return 0;
-    }
-    auto *keys = ctx->arena.alloc<unsigned long long>(K), *keys2 = ctx->arena.alloc<unsigned long long>(K);
-    uint32_t *src = ctx->arena.alloc<uint32_t>(K);
-    k_depth_keys<<<grid_for(K, 256), 256, 0, st>>>(kept, num, in.point_to_geom, P.depth, keys);
+// returns the rank -> point array (first *d_kept entries valid)
+static uint32_t *depth_order(sfb_ctx *ctx, const RenderInputs &in, const Proj &P, DevCounts *C) {
+    const int64_t n = in.n_points;
+    unsigned long long *k0 = ctx->arena.alloc<unsigned long long>(n), *k1 = ctx->arena.alloc<unsigned long long>(n);
+    uint32_t *v0 = ctx->arena.alloc<uint32_t>(n), *v1 = ctx->arena.alloc<uint32_t>(n);
+    k_depth_keys<<<dgrid(n, 256), 256, 0, ctx->stream>>>(n, in.point_to_geom, P, k0, v0, &C->kept);
     SFB_CHECK_LAUNCH();
-    tb = 0;
-    cub::DeviceRadixSort::SortPairs(nullptr, tb, keys, keys2, kept, src, (int)K, 0, 64, st);
-    tmp = ctx->arena.alloc_bytes(tb);
-    SFB_CUDA(cub::DeviceRadixSort::SortPairs(tmp, tb, keys, keys2, kept, src, (int)K, 0, 64, st));
-    *source = src;
-    return K;
+    const int which = dsort_pairs<unsigned long long>(ctx, k0, v0, k1, v1, nullptr, n, 64);
+    return which ? v1 : v0;
 }
 
 // ------------------------------------------------------------ 3. runs
@@ -242,84 +214,89 @@ __device__ __forceinline__ TileRect tile_rect(double sx, double sy, double r, do
     return t;
 }
 
-__global__ void k_run_heads(const uint32_t *__restrict__ src, int64_t K, const int32_t *__restrict__ p2g,
-                            Proj P, const double *__restrict__ opac, int32_t *__restrict__ head) {
-    int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (j >= K) return;
-    int h = 1;
-    if (j > 0) {
-        uint32_t i = src[j], k = src[j - 1];
-        if (p2g) {
-            h = p2g[i] != p2g[k];
-        } else {
-            h = !(P.sx[i] == P.sx[k] && P.sy[i] == P.sy[k] && P.depth[i] == P.depth[k] &&
-                  P.a[i] == P.a[k] && P.b[i] == P.b[k] && P.c[i] == P.c[k] && opac[i] == opac[k]);
+__global__ void k_run_heads(const uint32_t *__restrict__ src, const int64_t *__restrict__ d_k,
+                            const int32_t *__restrict__ p2g, Proj P, const double *__restrict__ opac,
+                            int32_t *__restrict__ head) {
+    const int64_t K = *d_k;
+    SFB_FOR(j, K) {
+        int h = 1;
+        if (j > 0) {
+            const uint32_t i = src[j], k = src[j - 1];
+            if (p2g) {
+                h = p2g[i] != p2g[k];
+            } else {
+                h = !(P.sx[i] == P.sx[k] && P.sy[i] == P.sy[k] && P.depth[i] == P.depth[k] &&
+                      P.a[i] == P.a[k] && P.b[i] == P.b[k] && P.c[i] == P.c[k] && opac[i] == opac[k]);
+            }
         }
+        head[j] = h;
     }
-    head[j] = h;
 }
 
 struct Runs {
-    int64_t R;
     double *mx, *my, *rad, *ia, *ib, *ic, *op;
     int32_t *start, *count;
     int4 *rect;
     uint8_t *level;  // 0 fine, 1 super, 2 global, 3 dead
     int32_t *nf, *ns, *ng;  // per-run entry counts
+    const int64_t *d_R;
 };
 
-__global__ void k_run_build(const uint32_t *__restrict__ src, int64_t K,
+__global__ void k_run_build(const uint32_t *__restrict__ src, DevCounts *__restrict__ C,
                             const int32_t *__restrict__ incl, const int32_t *__restrict__ p2g, Proj P,
                             const double *__restrict__ opac, double ft, int64_t ntx, int64_t nty,
-                            int64_t nsx, int64_t nsy, double alpha_max, Runs R) {
-    int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (j >= K) return;
-    int32_t r = incl[j] - 1;
-    const bool last = j == K - 1 || incl[j + 1] != incl[j];
-    if (last) R.count[r] = (int32_t)(j + 1);   // end of run r; start subtracted below
-    bool head = j == 0 || incl[j - 1] != incl[j];
-    if (!head) return;
-    R.start[r] = (int32_t)j;
-    uint32_t i = src[j];
-    int32_t g = p2g ? p2g[i] : (int32_t)i;
-    double a = P.a[g], b = P.b[g], c = P.c[g];
-    double op = opac[g];
-    double det = a * c - b * b;
-    R.mx[r] = P.sx[g];
-    R.my[r] = P.sy[g];
-    R.ia[r] = c / det;
-    R.ib[r] = -b / det;
-    R.ic[r] = a / det;
-    R.op[r] = op;
-    double rad = support_radius(a, b, c, op);
-    R.rad[r] = rad;
-    TileRect t = tile_rect(P.sx[g], P.sy[g], rad, ft, ntx, nty);
-    R.rect[r] = make_int4(t.x0, t.x1, t.y0, t.y1);
-    int lvl = 3;
-    int nf = 0, ns = 0, ng = 0;
-    bool live = !(op < kCutoff) && !(alpha_max < kCutoff) && t.x0 <= t.x1 && t.y0 <= t.y1;
-    if (live) {
-        int64_t cnt = (int64_t)(t.x1 - t.x0 + 1) * (t.y1 - t.y0 + 1);
-        if (cnt <= kFineMax) {
-            lvl = 0;
-            nf = (int)cnt;
-        } else {
-            int64_t scnt = (int64_t)(t.x1 / kSuper - t.x0 / kSuper + 1) * (t.y1 / kSuper - t.y0 / kSuper + 1);
-            if (scnt <= kSuperMax) {
-                lvl = 1;
-                ns = (int)scnt;
+                            double alpha_max, Runs R) {
+    const int64_t K = C->kept;
+    SFB_FOR(j, K) {
+        const int32_t r = incl[j] - 1;
+        const bool last = j == K - 1 || incl[j + 1] != incl[j];
+        if (last) R.count[r] = (int32_t)(j + 1);   // end of run r; start subtracted in k_emit
+        if (j == K - 1) {
+            C->runs = r + 1;
+            C->runs1 = r + 2;
+        }
+        const bool head = j == 0 || incl[j - 1] != incl[j];
+        if (!head) continue;
+        R.start[r] = (int32_t)j;
+        const uint32_t i = src[j];
+        const int64_t g = p2g ? p2g[i] : (int64_t)i;
+        const double a = P.a[g], b = P.b[g], c = P.c[g];
+        const double op = opac[g];
+        const double det = a * c - b * b;
+        R.mx[r] = P.sx[g];
+        R.my[r] = P.sy[g];
+        R.ia[r] = c / det;
+        R.ib[r] = -b / det;
+        R.ic[r] = a / det;
+        R.op[r] = op;
+        const double rad = support_radius(a, b, c, op);
+        R.rad[r] = rad;
+        const TileRect t = tile_rect(P.sx[g], P.sy[g], rad, ft, ntx, nty);
+        R.rect[r] = make_int4(t.x0, t.x1, t.y0, t.y1);
+        int lvl = 3, nf = 0, ns = 0, ng = 0;
+        const bool live = !(op < kCutoff) && !(alpha_max < kCutoff) && t.x0 <= t.x1 && t.y0 <= t.y1;
+        if (live) {
+            const int64_t cnt = (int64_t)(t.x1 - t.x0 + 1) * (t.y1 - t.y0 + 1);
+            if (cnt <= kFineMax) {
+                lvl = 0;
+                nf = (int)cnt;
             } else {
-                lvl = 2;
-                ng = 1;
+                const int64_t scnt =
+                    (int64_t)(t.x1 / kSuper - t.x0 / kSuper + 1) * (t.y1 / kSuper - t.y0 / kSuper + 1);
+                if (scnt <= kSuperMax) {
+                    lvl = 1;
+                    ns = (int)scnt;
+                } else {
+                    lvl = 2;
+                    ng = 1;
+                }
             }
         }
+        R.level[r] = (uint8_t)lvl;
+        R.nf[r] = nf;
+        R.ns[r] = ns;
+        R.ng[r] = ng;
     }
-    (void)nsx;
-    (void)nsy;
-    R.level[r] = (uint8_t)lvl;
-    R.nf[r] = nf;
-    R.ns[r] = ns;
-    R.ng[r] = ng;
 }
 
 __global__ void k_emit(Runs R, const int32_t *__restrict__ fpos, const int32_t *__restrict__ spos,
@@ -327,33 +304,35 @@ __global__ void k_emit(Runs R, const int32_t *__restrict__ fpos, const int32_t *
                        uint32_t *__restrict__ fkey, uint32_t *__restrict__ fval,
                        uint32_t *__restrict__ skey, uint32_t *__restrict__ sval,
                        uint32_t *__restrict__ glist) {
-    int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (r >= R.R) return;
-    R.count[r] -= R.start[r];   // k_run_build stored the run's end
-    int lvl = R.level[r];
-    int4 t = R.rect[r];
-    if (lvl == 0) {
-        int32_t p = fpos[r];
-        for (int y = t.z; y <= t.w; ++y)
-            for (int x = t.x; x <= t.y; ++x) {
-                fkey[p] = (uint32_t)(y * ntx + x);
-                fval[p++] = (uint32_t)r;
-            }
-    } else if (lvl == 1) {
-        int32_t p = spos[r];
-        for (int y = t.z / kSuper; y <= t.w / kSuper; ++y)
-            for (int x = t.x / kSuper; x <= t.y / kSuper; ++x) {
-                skey[p] = (uint32_t)(y * nsx + x);
-                sval[p++] = (uint32_t)r;
-            }
-    } else if (lvl == 2) {
-        glist[gpos[r]] = (uint32_t)r;
+    const int64_t nr = *R.d_R;
+    SFB_FOR(r, nr) {
+        R.count[r] -= R.start[r];   // k_run_build stored the run's end
+        const int lvl = R.level[r];
+        const int4 t = R.rect[r];
+        if (lvl == 0) {
+            int32_t p = fpos[r];
+            for (int y = t.z; y <= t.w; ++y)
+                for (int x = t.x; x <= t.y; ++x) {
+                    fkey[p] = (uint32_t)(y * ntx + x);
+                    fval[p++] = (uint32_t)r;
+                }
+        } else if (lvl == 1) {
+            int32_t p = spos[r];
+            for (int y = t.z / kSuper; y <= t.w / kSuper; ++y)
+                for (int x = t.x / kSuper; x <= t.y / kSuper; ++x) {
+                    skey[p] = (uint32_t)(y * nsx + x);
+                    sval[p++] = (uint32_t)r;
+                }
+        } else if (lvl == 2) {
+            glist[gpos[r]] = (uint32_t)r;
+        }
     }
 }
 
-__global__ void k_histogram(const uint32_t *__restrict__ keys, int64_t n, int32_t *__restrict__ cnt) {
-    int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (j < n) atomicAdd(&cnt[keys[j]], 1);
+__global__ void k_histogram(const uint32_t *__restrict__ keys, const int64_t *__restrict__ d_n,
+                            int32_t *__restrict__ cnt) {
+    const int64_t n = *d_n;
+    SFB_FOR(j, n) atomicAdd(&cnt[keys[j]], 1);
 }
 
 // ------------------------------------------------------------ 5. compositor
@@ -363,14 +342,14 @@ struct CompParams {
     int terminate;
     double alpha_max;
     int plane_mask;
-    double bg[3];
+    const FrameParams *fp;
     // lists
     const int32_t *f_off;
     const uint32_t *f_ids;
     const int32_t *s_off;
     const uint32_t *s_ids;
     const uint32_t *g_ids;
-    int64_t G;
+    const int64_t *d_G;
     Runs R;
     // points
     const uint32_t *src;
@@ -389,13 +368,15 @@ __global__ void __launch_bounds__(kCT) k_composite(CompParams P) {
     __shared__ int s_nlist;
     __shared__ uint32_t s_add[3];
     // the current chunk's run records (pixel box precomputed per run)
-    __shared__ double r_mx[kCT], r_my[kCT], r_rr[kCT], r_ia[kCT], r_ib[kCT], r_ic[kCT], r_op[kCT];
-    __shared__ int32_t r_x0[kCT], r_x1[kCT], r_y0[kCT], r_y1[kCT], r_start[kCT], r_count[kCT];
+    __shared__ double r_mx[kChunk], r_my[kChunk], r_rr[kChunk], r_ia[kChunk], r_ib[kChunk],
+        r_ic[kChunk], r_op[kChunk];
+    __shared__ int32_t r_x0[kChunk], r_x1[kChunk], r_y0[kChunk], r_y1[kChunk], r_start[kChunk],
+        r_count[kChunk];
     // attributes of each run's first kPre points, staged so the blend loop
     // does not chase src[] -> colours[] through global memory per pixel
     extern __shared__ double dyn_smem[];
-    double (*r_col)[3][kCT] = reinterpret_cast<double (*)[3][kCT]>(dyn_smem);
-    double (*r_nrm)[3][kCT] = reinterpret_cast<double (*)[3][kCT]>(dyn_smem + kPre * 3 * kCT);
+    double (*r_col)[3][kChunk] = reinterpret_cast<double (*)[3][kChunk]>(dyn_smem);
+    double (*r_nrm)[3][kChunk] = reinterpret_cast<double (*)[3][kChunk]>(dyn_smem + kPre * 3 * kChunk);
 
     const int64_t t = blockIdx.x;
     const int64_t tx = t % P.ntx, ty = t / P.ntx;
@@ -427,9 +408,18 @@ __global__ void __launch_bounds__(kCT) k_composite(CompParams P) {
         return mine;
     };
 
+    const uint32_t *__restrict__ src = P.src;
+    const int32_t *__restrict__ p2g = P.p2g;
+    const double *__restrict__ colors = P.colors, *__restrict__ normals = P.normals;
+    const double *__restrict__ gdepth = P.gdepth;
+    const double *__restrict__ Rmx = P.R.mx, *__restrict__ Rmy = P.R.my, *__restrict__ Rrad = P.R.rad;
+    const double *__restrict__ Ria = P.R.ia, *__restrict__ Rib = P.R.ib, *__restrict__ Ric = P.R.ic;
+    const double *__restrict__ Rop = P.R.op;
+    const int32_t *__restrict__ Rstart = P.R.start, *__restrict__ Rcount = P.R.count;
+    const double alpha_max = P.alpha_max;
     const uint32_t *ids[3] = {P.f_ids, P.s_ids, P.g_ids};
     int64_t cur[3] = {P.f_off[t], P.s_off[st], 0};
-    const int64_t end[3] = {P.f_off[t + 1], P.s_off[st + 1], P.G};
+    const int64_t end[3] = {P.f_off[t + 1], P.s_off[st + 1], *P.d_G};
     int ws = kCT;  // rank window grows 256 -> 2048: most tiles saturate in the first
     bool done = false;
     while (!done) {
@@ -504,47 +494,58 @@ __global__ void __launch_bounds__(kCT) k_composite(CompParams P) {
         }
         __syncthreads();
         const int nlist = s_nlist;
-        for (int base = 0; base < nlist && !done; base += kCT) {
-            const int nb = min(kCT, nlist - base);
+        for (int base = 0; base < nlist && !done; base += kChunk) {
+            const int nb = min(kChunk, nlist - base);
             if (threadIdx.x < nb) {
                 const uint32_t r = list[base + threadIdx.x];
                 const int j = threadIdx.x;
-                const double mx = P.R.mx[r], my = P.R.my[r];
-                const double rad = P.R.rad[r] + 1.0;
+                const double mx = Rmx[r], my = Rmy[r];
+                const double rad = Rrad[r] + 1.0;
                 r_mx[j] = mx;
                 r_my[j] = my;
                 r_rr[j] = rad * rad;
-                r_ia[j] = P.R.ia[r];
-                r_ib[j] = P.R.ib[r];
-                r_ic[j] = P.R.ic[r];
-                r_op[j] = P.R.op[r];
-                const int32_t st0 = P.R.start[r], cnt0 = P.R.count[r];
-                r_start[j] = st0;
-                r_count[j] = cnt0;
-                uint32_t pi[kPre];
-#pragma unroll
-                for (int q = 0; q < kPre; ++q) pi[q] = q < cnt0 ? P.src[st0 + q] : 0u;
-#pragma unroll
-                for (int q = 0; q < kPre; ++q) {
-                    if (q >= cnt0) break;
-                    if (want_rgb) {
-                        const double *cc = P.colors + 3 * (size_t)pi[q];
-                        r_col[q][0][j] = cc[0];
-                        r_col[q][1][j] = cc[1];
-                        r_col[q][2][j] = cc[2];
-                    }
-                    if (want_n) {
-                        const double *nn = P.normals + 3 * (P.p2g ? (int64_t)P.p2g[pi[q]] : (int64_t)pi[q]);
-                        r_nrm[q][0][j] = nn[0];
-                        r_nrm[q][1][j] = nn[1];
-                        r_nrm[q][2][j] = nn[2];
-                    }
-                }
+                r_ia[j] = Ria[r];
+                r_ib[j] = Rib[r];
+                r_ic[j] = Ric[r];
+                r_op[j] = Rop[r];
+                r_start[j] = Rstart[r];
+                r_count[j] = Rcount[r];
                 // pixel box of forward_kernel (_raster_kernels.py:178-181), clamped to the tile
                 r_x0[j] = (int32_t)fmin(fmax((double)x_lo, ceil(mx - rad)), (double)x_end);
                 r_x1[j] = (int32_t)fmax(fmin((double)(x_end - 1), floor(mx + rad)), (double)(x_lo - 1));
                 r_y0[j] = (int32_t)fmin(fmax((double)y_lo, ceil(my - rad)), (double)y_end);
                 r_y1[j] = (int32_t)fmax(fmin((double)(y_end - 1), floor(my + rad)), (double)(y_lo - 1));
+            }
+            __syncthreads();
+            {   // stage the first kPre points of every run: 4 threads per run
+                const int e = threadIdx.x >> 2, part = threadIdx.x & 3;
+                if (e < nb) {
+                    const int32_t st0 = r_start[e], cnt0 = r_count[e];
+                    uint32_t pi[kPre / 4];
+#pragma unroll
+                    for (int u = 0; u < kPre / 4; ++u) {
+                        const int q = part * (kPre / 4) + u;
+                        pi[u] = q < cnt0 ? src[st0 + q] : 0u;
+                    }
+#pragma unroll
+                    for (int u = 0; u < kPre / 4; ++u) {
+                        const int q = part * (kPre / 4) + u;
+                        if (q < cnt0) {
+                            if (want_rgb) {
+                                const double *cc = colors + 3 * (size_t)pi[u];
+                                r_col[q][0][e] = cc[0];
+                                r_col[q][1][e] = cc[1];
+                                r_col[q][2][e] = cc[2];
+                            }
+                            if (want_n) {
+                                const double *nn = normals + 3 * (p2g ? (int64_t)p2g[pi[u]] : (int64_t)pi[u]);
+                                r_nrm[q][0][e] = nn[0];
+                                r_nrm[q][1][e] = nn[1];
+                                r_nrm[q][2][e] = nn[2];
+                            }
+                        }
+                    }
+                }
             }
             __syncthreads();
             for (int e = 0; e < nb; ++e) {
@@ -562,7 +563,7 @@ __global__ void __launch_bounds__(kCT) k_composite(CompParams P) {
                     if (dx * dx + dy * dy > r_rr[e]) continue;
                     const double q = r_ia[e] * dx * dx + 2.0 * r_ib[e] * dx * dy + r_ic[e] * dy * dy;
                     double alpha = r_op[e] * exp(-0.5 * q);
-                    if (alpha > P.alpha_max) alpha = P.alpha_max;
+                    if (alpha > alpha_max) alpha = alpha_max;
                     if (alpha < kCutoff) continue;
                     const double om = 1.0 - alpha;
                     const int32_t b0 = r_start[e], b1 = b0 + r_count[e];
@@ -582,26 +583,26 @@ __global__ void __launch_bounds__(kCT) k_composite(CompParams P) {
                                 n2[k] = n2[k] + w * r_nrm[q][2][e];
                             }
                             if (want_d) {
-                                const uint32_t i = P.src[j];
-                                dd[k] = dd[k] + w * P.gdepth[P.p2g ? P.p2g[i] : (int64_t)i];
+                                const uint32_t i = src[j];
+                                dd[k] = dd[k] + w * gdepth[p2g ? p2g[i] : (int64_t)i];
                             }
                         } else {
-                            const uint32_t i = P.src[j];
+                            const uint32_t i = src[j];
                             if (want_rgb) {
-                                const double *cc = P.colors + 3 * (size_t)i;
+                                const double *cc = colors + 3 * (size_t)i;
                                 c0[k] = c0[k] + w * cc[0];
                                 c1[k] = c1[k] + w * cc[1];
                                 c2[k] = c2[k] + w * cc[2];
                             }
                             if (want_n || want_d) {
-                                const int64_t g = P.p2g ? P.p2g[i] : (int64_t)i;
+                                const int64_t g = p2g ? p2g[i] : (int64_t)i;
                                 if (want_n) {
-                                    const double *nn = P.normals + 3 * g;
+                                    const double *nn = normals + 3 * g;
                                     n0[k] = n0[k] + w * nn[0];
                                     n1[k] = n1[k] + w * nn[1];
                                     n2[k] = n2[k] + w * nn[2];
                                 }
-                                if (want_d) dd[k] = dd[k] + w * P.gdepth[g];
+                                if (want_d) dd[k] = dd[k] + w * gdepth[g];
                             }
                         }
                         T[k] = T[k] * om;
@@ -615,14 +616,15 @@ __global__ void __launch_bounds__(kCT) k_composite(CompParams P) {
         ws = min(ws * 2, kWin);
     }
     // planes (rasterizer.py:140-149; FrameBuffer clips T to [0,1])
+    const double bgc[3] = {P.fp->bg[0], P.fp->bg[1], P.fp->bg[2]};
 #pragma unroll
     for (int k = 0; k < NPIX; ++k) {
         if (!valid[k]) continue;
         const int64_t pix = (int64_t)pys[k] * P.W + pxs[k];
         if (P.rgb) {
-            P.rgb[3 * pix + 0] = (float)(c0[k] + T[k] * P.bg[0]);
-            P.rgb[3 * pix + 1] = (float)(c1[k] + T[k] * P.bg[1]);
-            P.rgb[3 * pix + 2] = (float)(c2[k] + T[k] * P.bg[2]);
+            P.rgb[3 * pix + 0] = (float)(c0[k] + T[k] * bgc[0]);
+            P.rgb[3 * pix + 1] = (float)(c1[k] + T[k] * bgc[1]);
+            P.rgb[3 * pix + 2] = (float)(c2[k] + T[k] * bgc[2]);
         }
         if (P.normal) {
             double nrm = sqrt(n0[k] * n0[k] + n1[k] * n1[k] + n2[k] * n2[k]);
@@ -637,154 +639,121 @@ __global__ void __launch_bounds__(kCT) k_composite(CompParams P) {
 }
 
 // ------------------------------------------------------------ driver
-void render_run(sfb_ctx *ctx, const RenderInputs &in, const sfb_camera &cam,
-                const sfb_render_options &opts, int plane_mask, const double *bg, float *rgb,
-                float *normal, float *depth, float *trans) {
-    SFB_REQUIRE(cam.width >= 1 && cam.height >= 1, "image must have positive dimensions");
+// No host synchronisation: every size (kept points, runs, pyramid entries)
+// stays on the device; buffers are sized from host bounds.
+void render_run(sfb_ctx *ctx, const RenderInputs &in, const FrameParams *FP, int64_t width,
+                int64_t height, const sfb_render_options &opts, int plane_mask, DevCounts *C,
+                float *rgb, float *normal, float *depth, float *trans) {
+    SFB_REQUIRE(width >= 1 && height >= 1, "image must have positive dimensions");
     SFB_REQUIRE(opts.tile_size >= 1 && opts.tile_size <= 32, "tile_size must be in [1, 32]");
     cudaStream_t st = ctx->stream;
     const int TS = opts.tile_size;
-    const int64_t ntx = (cam.width + TS - 1) / TS, nty = (cam.height + TS - 1) / TS;
+    const int64_t ntx = (width + TS - 1) / TS, nty = (height + TS - 1) / TS;
     const int64_t nsx = (ntx + kSuper - 1) / kSuper, nsy = (nty + kSuper - 1) / kSuper;
-    Proj P = project_inputs(ctx, in, cam);
+    const int64_t nt = ntx * nty, ns = nsx * nsy;
+    const int64_t n = in.n_points;
+    Proj P = project_inputs(ctx, in, FP);
     ctx->mark(ST_PROJECT);
-    uint32_t *src = nullptr;
-    int64_t K = depth_order(ctx, in, P, &src);
+    const int64_t nb = n > 0 ? n : 1;
+    uint32_t *src = n > 0 ? depth_order(ctx, in, P, C) : ctx->arena.alloc<uint32_t>(1);
     ctx->mark(ST_SORT);
-    ctx->stats.kept = K;
 
     Runs R{};
-    R.R = 0;
-    int32_t *f_off = ctx->arena.alloc<int32_t>(ntx * nty + 1);
-    int32_t *s_off = ctx->arena.alloc<int32_t>(nsx * nsy + 1);
-    uint32_t *fval2 = nullptr, *sval2 = nullptr, *glist = nullptr;
-    int64_t Ef = 0, Es = 0, G = 0;
-    SFB_CUDA(cudaMemsetAsync(f_off, 0, sizeof(int32_t) * (ntx * nty + 1), st));
-    SFB_CUDA(cudaMemsetAsync(s_off, 0, sizeof(int32_t) * (nsx * nsy + 1), st));
-    if (K > 0) {
-        int32_t *head = ctx->arena.alloc<int32_t>(K), *incl = ctx->arena.alloc<int32_t>(K);
-        k_run_heads<<<grid_for(K, 256), 256, 0, st>>>(src, K, in.point_to_geom, P, in.opac, head);
-        size_t tb = 0;
-        cub::DeviceScan::InclusiveSum(nullptr, tb, head, incl, (int)K, st);
-        void *tmp = ctx->arena.alloc_bytes(tb);
-        SFB_CUDA(cub::DeviceScan::InclusiveSum(tmp, tb, head, incl, (int)K, st));
-        ctx->read_back(incl + K - 1, sizeof(int32_t));
-        R.R = *reinterpret_cast<int32_t *>(ctx->pinned);
-        int64_t nr = R.R;
-        double *blk = ctx->arena.alloc<double>(7 * nr);
-        R.mx = blk;
-        R.my = blk + nr;
-        R.rad = blk + 2 * nr;
-        R.ia = blk + 3 * nr;
-        R.ib = blk + 4 * nr;
-        R.ic = blk + 5 * nr;
-        R.op = blk + 6 * nr;
-        R.start = ctx->arena.alloc<int32_t>(nr);
-        R.count = ctx->arena.alloc<int32_t>(nr);
-        R.rect = ctx->arena.alloc<int4>(nr);
-        R.level = ctx->arena.alloc<uint8_t>(nr);
-        int32_t *cnts = ctx->arena.alloc<int32_t>(3 * (nr + 1));
-        R.nf = cnts;
-        R.ns = cnts + (nr + 1);
-        R.ng = cnts + 2 * (nr + 1);
-        SFB_CUDA(cudaMemsetAsync(cnts, 0, sizeof(int32_t) * 3 * (nr + 1), st));
-        k_run_build<<<grid_for(K, 256), 256, 0, st>>>(src, K, incl, in.point_to_geom, P, in.opac,
-                                                      (double)TS, ntx, nty, nsx, nsy,
-                                                      opts.alpha_max, R);
+    R.d_R = &C->runs;
+    int32_t *head = ctx->arena.alloc<int32_t>(nb);
+    double *blk = ctx->arena.alloc<double>(7 * nb);
+    R.mx = blk;
+    R.my = blk + nb;
+    R.rad = blk + 2 * nb;
+    R.ia = blk + 3 * nb;
+    R.ib = blk + 4 * nb;
+    R.ic = blk + 5 * nb;
+    R.op = blk + 6 * nb;
+    R.start = ctx->arena.alloc<int32_t>(nb);
+    R.count = ctx->arena.alloc<int32_t>(nb);
+    R.rect = ctx->arena.alloc<int4>(nb);
+    R.level = ctx->arena.alloc<uint8_t>(nb);
+    int32_t *cnts = ctx->arena.alloc<int32_t>(3 * (nb + 1));
+    R.nf = cnts;
+    R.ns = cnts + (nb + 1);
+    R.ng = cnts + 2 * (nb + 1);
+    int32_t *pos = ctx->arena.alloc<int32_t>(3 * (nb + 1));
+    const int64_t ebound = kFineMax * nb;   // at most kFineMax entries per run and level
+    uint32_t *fkey = ctx->arena.alloc<uint32_t>(ebound), *fval = ctx->arena.alloc<uint32_t>(ebound);
+    uint32_t *fkey2 = ctx->arena.alloc<uint32_t>(ebound), *fval2 = ctx->arena.alloc<uint32_t>(ebound);
+    uint32_t *skey = ctx->arena.alloc<uint32_t>(ebound), *sval = ctx->arena.alloc<uint32_t>(ebound);
+    uint32_t *skey2 = ctx->arena.alloc<uint32_t>(ebound), *sval2 = ctx->arena.alloc<uint32_t>(ebound);
+    uint32_t *glist = ctx->arena.alloc<uint32_t>(nb);
+    int32_t *f_off = ctx->arena.alloc<int32_t>(nt + 1);
+    int32_t *s_off = ctx->arena.alloc<int32_t>(ns + 1);
+    SFB_CUDA(cudaMemsetAsync(f_off, 0, sizeof(int32_t) * (nt + 1), st));
+    SFB_CUDA(cudaMemsetAsync(s_off, 0, sizeof(int32_t) * (ns + 1), st));
+    SFB_CUDA(cudaMemsetAsync(cnts, 0, sizeof(int32_t) * 3 * (nb + 1), st));
+    const uint32_t *f_ids = fval, *s_ids = sval;
+    if (n > 0) {
+        const unsigned g = dgrid(n, 256);
+        k_run_heads<<<g, 256, 0, st>>>(src, &C->kept, in.point_to_geom, P, in.opac, head);
         SFB_CHECK_LAUNCH();
-        // exclusive positions of every level's entries (+1 slot carries the total)
-        int32_t *pos = ctx->arena.alloc<int32_t>(3 * (nr + 1));
-        tb = 0;
-        cub::DeviceScan::ExclusiveSum(nullptr, tb, R.nf, pos, (int)(nr + 1), st);
-        tmp = ctx->arena.alloc_bytes(tb);
-        for (int l = 0; l < 3; ++l)
-            SFB_CUDA(cub::DeviceScan::ExclusiveSum(tmp, tb, cnts + l * (nr + 1), pos + l * (nr + 1),
-                                                   (int)(nr + 1), st));
-        int32_t *tot = ctx->arena.alloc<int32_t>(3);
-        for (int l = 0; l < 3; ++l)
-            SFB_CUDA(cudaMemcpyAsync(tot + l, pos + l * (nr + 1) + nr, sizeof(int32_t),
-                                     cudaMemcpyDeviceToDevice, st));
-        ctx->read_back(tot, 3 * sizeof(int32_t));
-        const int32_t *h = reinterpret_cast<const int32_t *>(ctx->pinned);
-        Ef = h[0];
-        Es = h[1];
-        G = h[2];
-        uint32_t *fkey = ctx->arena.alloc<uint32_t>(Ef + 1), *fval = ctx->arena.alloc<uint32_t>(Ef + 1);
-        uint32_t *skey = ctx->arena.alloc<uint32_t>(Es + 1), *sval = ctx->arena.alloc<uint32_t>(Es + 1);
-        glist = ctx->arena.alloc<uint32_t>(G + 1);
-        k_emit<<<grid_for(nr, 128), 128, 0, st>>>(R, pos, pos + (nr + 1), pos + 2 * (nr + 1), ntx,
-                                                  nsx, fkey, fval, skey, sval, glist);
+        dscan(ctx, head, head, &C->kept, n, nullptr, true);
+        k_run_build<<<g, 256, 0, st>>>(src, C, head, in.point_to_geom, P, in.opac, (double)TS, ntx,
+                                       nty, opts.alpha_max, R);
+        SFB_CHECK_LAUNCH();
+        dscan(ctx, R.nf, pos, &C->runs1, nb + 1, &C->ef, false);
+        dscan(ctx, R.ns, pos + (nb + 1), &C->runs1, nb + 1, &C->es, false);
+        dscan(ctx, R.ng, pos + 2 * (nb + 1), &C->runs1, nb + 1, &C->g, false);
+        k_emit<<<g, 256, 0, st>>>(R, pos, pos + (nb + 1), pos + 2 * (nb + 1), ntx, nsx, fkey, fval,
+                                  skey, sval, glist);
         SFB_CHECK_LAUNCH();
         // stable sort by tile id keeps each tile's runs in rank order
-        uint32_t *fkey2 = ctx->arena.alloc<uint32_t>(Ef + 1), *skey2 = ctx->arena.alloc<uint32_t>(Es + 1);
-        fval2 = ctx->arena.alloc<uint32_t>(Ef + 1);
-        sval2 = ctx->arena.alloc<uint32_t>(Es + 1);
-        int fbits = bits_for((uint64_t)(ntx * nty)), sbits = bits_for((uint64_t)(nsx * nsy));
-        size_t tb1 = 0, tb2 = 0, tb3 = 0;
-        if (Ef) cub::DeviceRadixSort::SortPairs(nullptr, tb1, fkey, fkey2, fval, fval2, (int)Ef, 0, fbits, st);
-        if (Es) cub::DeviceRadixSort::SortPairs(nullptr, tb2, skey, skey2, sval, sval2, (int)Es, 0, sbits, st);
-        int64_t nt = ntx * nty, ns = nsx * nsy;
-        cub::DeviceScan::ExclusiveSum(nullptr, tb3, f_off, f_off, (int)(nt + 1), st);
-        size_t tbm = std::max(tb1, std::max(tb2, tb3));
-        size_t tb4 = 0;
-        cub::DeviceScan::ExclusiveSum(nullptr, tb4, s_off, s_off, (int)(ns + 1), st);
-        tbm = std::max(tbm, tb4);
-        tmp = ctx->arena.alloc_bytes(tbm);
-        if (Ef) {
-            SFB_CUDA(cub::DeviceRadixSort::SortPairs(tmp, tb1, fkey, fkey2, fval, fval2, (int)Ef, 0, fbits, st));
-            k_histogram<<<grid_for(Ef, 256), 256, 0, st>>>(fkey2, Ef, f_off);
-        }
-        if (Es) {
-            SFB_CUDA(cub::DeviceRadixSort::SortPairs(tmp, tb2, skey, skey2, sval, sval2, (int)Es, 0, sbits, st));
-            k_histogram<<<grid_for(Es, 256), 256, 0, st>>>(skey2, Es, s_off);
-        }
+        const int fbits = bits_for((uint64_t)nt), sbits = bits_for((uint64_t)ns);
+        f_ids = dsort_pairs<uint32_t>(ctx, fkey, fval, fkey2, fval2, &C->ef, ebound, fbits) ? fval2 : fval;
+        const uint32_t *fk = (f_ids == fval2) ? fkey2 : fkey;
+        s_ids = dsort_pairs<uint32_t>(ctx, skey, sval, skey2, sval2, &C->es, ebound, sbits) ? sval2 : sval;
+        const uint32_t *sk = (s_ids == sval2) ? skey2 : skey;
+        k_histogram<<<dgrid(ebound, 256), 256, 0, st>>>(fk, &C->ef, f_off);
+        k_histogram<<<dgrid(ebound, 256), 256, 0, st>>>(sk, &C->es, s_off);
         SFB_CHECK_LAUNCH();
-        SFB_CUDA(cub::DeviceScan::ExclusiveSum(tmp, tbm, f_off, f_off, (int)(nt + 1), st));
-        SFB_CUDA(cub::DeviceScan::ExclusiveSum(tmp, tbm, s_off, s_off, (int)(ns + 1), st));
     }
+    dscan(ctx, f_off, f_off, nullptr, nt + 1, nullptr, false);
+    dscan(ctx, s_off, s_off, nullptr, ns + 1, nullptr, false);
     ctx->mark(ST_BIN);
-    ctx->stats.runs = R.R;
-    ctx->stats.fine_entries = Ef;
-    ctx->stats.super_entries = Es;
-    ctx->stats.global_entries = G;
 
-    CompParams C{};
-    C.W = cam.width;
-    C.H = cam.height;
-    C.ntx = ntx;
-    C.nty = nty;
-    C.nsx = nsx;
-    C.tile = TS;
-    C.terminate = opts.early_termination;
-    C.alpha_max = opts.alpha_max;
-    C.plane_mask = plane_mask;
-    for (int a = 0; a < 3; ++a) C.bg[a] = bg ? bg[a] : 0.0;
-    C.f_off = f_off;
-    C.f_ids = fval2;
-    C.s_off = s_off;
-    C.s_ids = sval2;
-    C.g_ids = glist;
-    C.G = G;
-    C.R = R;
-    C.src = src;
-    C.p2g = in.point_to_geom;
-    C.colors = in.colors;
-    C.normals = in.normals;
-    C.gdepth = P.depth;
-    C.rgb = (plane_mask & SFB_PLANE_RGB) ? rgb : nullptr;
-    C.normal = (plane_mask & SFB_PLANE_NORMAL) ? normal : nullptr;
-    C.depth = (plane_mask & SFB_PLANE_DEPTH) ? depth : nullptr;
-    C.trans = trans;
-    int64_t ntiles = ntx * nty;
-    const size_t dyn = sizeof(double) * 2 * kPre * 3 * kCT;
+    CompParams CP{};
+    CP.W = width;
+    CP.H = height;
+    CP.ntx = ntx;
+    CP.nty = nty;
+    CP.nsx = nsx;
+    CP.tile = TS;
+    CP.terminate = opts.early_termination;
+    CP.alpha_max = opts.alpha_max;
+    CP.plane_mask = plane_mask;
+    CP.fp = FP;
+    CP.f_off = f_off;
+    CP.f_ids = f_ids;
+    CP.s_off = s_off;
+    CP.s_ids = s_ids;
+    CP.g_ids = glist;
+    CP.d_G = &C->g;
+    CP.R = R;
+    CP.src = src;
+    CP.p2g = in.point_to_geom;
+    CP.colors = in.colors;
+    CP.normals = in.normals;
+    CP.gdepth = P.depth;
+    CP.rgb = (plane_mask & SFB_PLANE_RGB) ? rgb : nullptr;
+    CP.normal = (plane_mask & SFB_PLANE_NORMAL) ? normal : nullptr;
+    CP.depth = (plane_mask & SFB_PLANE_DEPTH) ? depth : nullptr;
+    CP.trans = trans;
+    const size_t dyn = sizeof(double) * 2 * kPre * 3 * kChunk;
     static bool attr = false;
     if (!attr) {
         SFB_CUDA(cudaFuncSetAttribute(k_composite<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn));
         SFB_CUDA(cudaFuncSetAttribute(k_composite<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn));
         attr = true;
     }
-    if (TS * TS <= kCT) k_composite<1><<<(unsigned)ntiles, kCT, dyn, st>>>(C);
-    else k_composite<4><<<(unsigned)ntiles, kCT, dyn, st>>>(C);
+    if (TS * TS <= kCT) k_composite<1><<<(unsigned)nt, kCT, dyn, st>>>(CP);
+    else k_composite<4><<<(unsigned)nt, kCT, dyn, st>>>(CP);
     SFB_CHECK_LAUNCH();
     ctx->mark(ST_COMPOSITE);
 }
@@ -794,88 +763,85 @@ __global__ void k_rank_rects(const uint32_t *__restrict__ src, int64_t K, const 
                              Proj P, const double *__restrict__ opac, double ft, int64_t ntx,
                              int64_t nty, double *__restrict__ radius, int4 *__restrict__ rect,
                              int32_t *__restrict__ cnt, int64_t *__restrict__ source) {
-    int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (j >= K) return;
-    uint32_t i = src[j];
-    int32_t g = p2g ? p2g[i] : (int32_t)i;
-    double r = support_radius(P.a[g], P.b[g], P.c[g], opac[g]);
-    radius[j] = r;
-    source[j] = i;
-    TileRect t = tile_rect(P.sx[g], P.sy[g], r, ft, ntx, nty);
-    rect[j] = make_int4(t.x0, t.x1, t.y0, t.y1);
-    cnt[j] = (t.x0 <= t.x1 && t.y0 <= t.y1) ? (t.x1 - t.x0 + 1) * (t.y1 - t.y0 + 1) : 0;
+    SFB_FOR(j, K) {
+        const uint32_t i = src[j];
+        const int64_t g = p2g ? p2g[i] : (int64_t)i;
+        const double r = support_radius(P.a[g], P.b[g], P.c[g], opac[g]);
+        radius[j] = r;
+        source[j] = i;
+        const TileRect t = tile_rect(P.sx[g], P.sy[g], r, ft, ntx, nty);
+        rect[j] = make_int4(t.x0, t.x1, t.y0, t.y1);
+        cnt[j] = (t.x0 <= t.x1 && t.y0 <= t.y1) ? (t.x1 - t.x0 + 1) * (t.y1 - t.y0 + 1) : 0;
+    }
 }
 
-__global__ void k_rank_emit(const int4 *__restrict__ rect, const int64_t *__restrict__ pos, int64_t K,
+__global__ void k_rank_emit(const int4 *__restrict__ rect, const int32_t *__restrict__ pos, int64_t K,
                             int64_t ntx, uint32_t *__restrict__ key, uint32_t *__restrict__ val) {
-    int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (j >= K) return;
-    int4 t = rect[j];
-    int64_t p = pos[j];
-    for (int y = t.z; y <= t.w; ++y)
-        for (int x = t.x; x <= t.y; ++x) {
-            key[p] = (uint32_t)(y * ntx + x);
-            val[p++] = (uint32_t)j;
-        }
+    SFB_FOR(j, K) {
+        const int4 t = rect[j];
+        int64_t p = pos[j];
+        for (int y = t.z; y <= t.w; ++y)
+            for (int x = t.x; x <= t.y; ++x) {
+                key[p] = (uint32_t)(y * ntx + x);
+                val[p++] = (uint32_t)j;
+            }
+    }
 }
 
 __global__ void k_widen(const uint32_t *__restrict__ a, int64_t n, int64_t *__restrict__ b) {
-    int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (j < n) b[j] = a[j];
+    SFB_FOR(j, n) b[j] = a[j];
 }
 __global__ void k_widen32(const int32_t *__restrict__ a, int64_t n, int64_t *__restrict__ b) {
-    int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (j < n) b[j] = a[j];
+    SFB_FOR(j, n) b[j] = a[j];
 }
 
-void prepare_debug_run(sfb_ctx *ctx, const RenderInputs &in, const sfb_camera &cam, int tile,
-                       int64_t *source, double *radius, int64_t *offsets, int64_t *ids,
-                       int64_t cap, int64_t *k_host, int64_t *e_host) {
+// The reference CSR (for parity tests only): host-synchronising by design.
+void prepare_debug_run(sfb_ctx *ctx, const RenderInputs &in, const FrameParams *FP, int64_t width,
+                       int64_t height, int tile, DevCounts *C, int64_t *source, double *radius,
+                       int64_t *offsets, int64_t *ids, int64_t cap, int64_t *k_host,
+                       int64_t *e_host) {
     cudaStream_t st = ctx->stream;
-    const int64_t ntx = (cam.width + tile - 1) / tile, nty = (cam.height + tile - 1) / tile;
-    Proj P = project_inputs(ctx, in, cam);
-    uint32_t *src = nullptr;
-    int64_t K = depth_order(ctx, in, P, &src);
-    *k_host = K;
-    int64_t nt = ntx * nty;
+    const int64_t ntx = (width + tile - 1) / tile, nty = (height + tile - 1) / tile;
+    const int64_t nt = ntx * nty;
+    Proj P = project_inputs(ctx, in, FP);
     int32_t *toff = ctx->arena.alloc<int32_t>(nt + 1);
     SFB_CUDA(cudaMemsetAsync(toff, 0, sizeof(int32_t) * (nt + 1), st));
+    int64_t K = 0;
+    uint32_t *src = nullptr;
+    if (in.n_points > 0) {
+        src = depth_order(ctx, in, P, C);
+        ctx->read_back(&C->kept, sizeof(int64_t));
+        K = ctx->pinned[0];
+    }
+    *k_host = K;
     if (K == 0) {
         *e_host = 0;
-        k_widen32<<<grid_for(nt + 1, 256), 256, 0, st>>>(toff, nt + 1, offsets);
+        k_widen32<<<dgrid(nt + 1, 256), 256, 0, st>>>(toff, nt + 1, offsets);
+        SFB_CHECK_LAUNCH();
         return;
     }
     int4 *rect = ctx->arena.alloc<int4>(K);
     int32_t *cnt = ctx->arena.alloc<int32_t>(K + 1);
-    int64_t *pos = ctx->arena.alloc<int64_t>(K + 1);
+    int32_t *pos = ctx->arena.alloc<int32_t>(K + 1);
     SFB_CUDA(cudaMemsetAsync(cnt, 0, sizeof(int32_t) * (K + 1), st));
-    k_rank_rects<<<grid_for(K, 256), 256, 0, st>>>(src, K, in.point_to_geom, P, in.opac,
-                                                   (double)tile, ntx, nty, radius, rect, cnt, source);
-    size_t tb = 0;
-    cub::DeviceScan::ExclusiveSum(nullptr, tb, cnt, pos, (int)(K + 1), st);
-    void *tmp = ctx->arena.alloc_bytes(tb);
-    SFB_CUDA(cub::DeviceScan::ExclusiveSum(tmp, tb, cnt, pos, (int)(K + 1), st));
-    ctx->read_back(pos + K, sizeof(int64_t));
-    int64_t E = ctx->pinned[0];
+    k_rank_rects<<<dgrid(K, 256), 256, 0, st>>>(src, K, in.point_to_geom, P, in.opac, (double)tile,
+                                                ntx, nty, radius, rect, cnt, source);
+    dscan(ctx, cnt, pos, nullptr, K + 1, &C->scratch[0], false);
+    ctx->read_back(&C->scratch[0], sizeof(int64_t));
+    const int64_t E = ctx->pinned[0];
     *e_host = E;
     SFB_REQUIRE(E < (int64_t(1) << 31), "debug CSR larger than 2^31 entries");
     uint32_t *key = ctx->arena.alloc<uint32_t>(E + 1), *val = ctx->arena.alloc<uint32_t>(E + 1);
     uint32_t *key2 = ctx->arena.alloc<uint32_t>(E + 1), *val2 = ctx->arena.alloc<uint32_t>(E + 1);
-    k_rank_emit<<<grid_for(K, 256), 256, 0, st>>>(rect, pos, K, ntx, key, val);
-    tb = 0;
-    int bits = bits_for((uint64_t)nt);
-    if (E) cub::DeviceRadixSort::SortPairs(nullptr, tb, key, key2, val, val2, (int)E, 0, bits, st);
-    size_t tb2 = 0;
-    cub::DeviceScan::ExclusiveSum(nullptr, tb2, toff, toff, (int)(nt + 1), st);
-    size_t tbx = std::max(tb, tb2);
-    tmp = ctx->arena.alloc_bytes(tbx);
-    if (E) {
-        SFB_CUDA(cub::DeviceRadixSort::SortPairs(tmp, tb, key, key2, val, val2, (int)E, 0, bits, st));
-        k_histogram<<<grid_for(E, 256), 256, 0, st>>>(key2, E, toff);
-    }
-    SFB_CUDA(cub::DeviceScan::ExclusiveSum(tmp, tbx, toff, toff, (int)(nt + 1), st));
-    k_widen32<<<grid_for(nt + 1, 256), 256, 0, st>>>(toff, nt + 1, offsets);
-    if (E && E <= cap) k_widen<<<grid_for(E, 256), 256, 0, st>>>(val2, E, ids);
+    k_rank_emit<<<dgrid(K, 256), 256, 0, st>>>(rect, pos, K, ntx, key, val);
+    SFB_CHECK_LAUNCH();
+    const int bits = bits_for((uint64_t)nt);
+    const bool second = dsort_pairs<uint32_t>(ctx, key, val, key2, val2, nullptr, E, bits);
+    const uint32_t *ks = second ? key2 : key, *vs = second ? val2 : val;
+    k_histogram<<<dgrid(E, 256), 256, 0, st>>>(ks, &C->scratch[0], toff);
+    dscan(ctx, toff, toff, nullptr, nt + 1, nullptr, false);
+    k_widen32<<<dgrid(nt + 1, 256), 256, 0, st>>>(toff, nt + 1, offsets);
+    if (E <= cap && ids) k_widen<<<dgrid(E, 256), 256, 0, st>>>(vs, E, ids);
     SFB_CHECK_LAUNCH();
 }
 

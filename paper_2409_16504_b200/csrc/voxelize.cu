@@ -67,55 +67,54 @@ void bbox_run(sfb_ctx *ctx, const double *pos, int64_t n, double *lo_hi_host) {
     for (int a = 0; a < 6; ++a) lo_hi_host[a] = unord_bits((unsigned long long)ctx->pinned[a]);
 }
 
-struct KeyLayout {
-    int64_t lo[3];
-    int bits[3];
-    int total;
-};
-
 template <class K>
-__global__ void k_keygen(const double *__restrict__ pos, int64_t n, double s, KeyLayout L,
+__global__ void k_keygen(const double *__restrict__ pos, int64_t n, const FrameParams *__restrict__ P,
                          K *__restrict__ keys, uint32_t *__restrict__ vals) {
-    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (i >= n) return;
-    int64_t ix = (int64_t)floor(__dmul_rn(pos[3 * i + 0], s)) - L.lo[0];
-    int64_t iy = (int64_t)floor(__dmul_rn(pos[3 * i + 1], s)) - L.lo[1];
-    int64_t iz = (int64_t)floor(__dmul_rn(pos[3 * i + 2], s)) - L.lo[2];
-    keys[i] = (K)(((uint64_t)iz << (L.bits[0] + L.bits[1])) | ((uint64_t)iy << L.bits[0]) |
-                  (uint64_t)ix);
-    vals[i] = (uint32_t)i;
+    const double s = P->s;
+    const int bx = P->bits[0], bxy = P->bits[0] + P->bits[1];
+    const int64_t lx = P->lo[0], ly = P->lo[1], lz = P->lo[2];
+    SFB_FOR(i, n) {
+        int64_t ix = (int64_t)floor(__dmul_rn(pos[3 * i + 0], s)) - lx;
+        int64_t iy = (int64_t)floor(__dmul_rn(pos[3 * i + 1], s)) - ly;
+        int64_t iz = (int64_t)floor(__dmul_rn(pos[3 * i + 2], s)) - lz;
+        keys[i] = (K)(((uint64_t)iz << bxy) | ((uint64_t)iy << bx) | (uint64_t)ix);
+        vals[i] = (uint32_t)i;
+    }
 }
 
 template <class K>
 __global__ void k_heads(const K *__restrict__ keys, int64_t n, int32_t *__restrict__ flag) {
-    int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (j >= n) return;
-    flag[j] = (j == 0 || keys[j] != keys[j - 1]) ? 1 : 0;
+    SFB_FOR(j, n) flag[j] = (j == 0 || keys[j] != keys[j - 1]) ? 1 : 0;
 }
 
 template <class K>
 __global__ void k_segments(const K *__restrict__ keys, const uint32_t *__restrict__ vals,
-                           const int32_t *__restrict__ incl, int64_t n, KeyLayout L,
-                           int32_t *__restrict__ coords, int64_t *__restrict__ pkeys,
-                           int32_t *__restrict__ p2v, int32_t *__restrict__ order,
-                           int32_t *__restrict__ offsets) {
-    int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (j >= n) return;
-    int32_t v = incl[j] - 1;
-    uint32_t i = vals[j];
-    order[j] = (int32_t)i;
-    p2v[i] = v;
-    if (j == n - 1) offsets[v + 1] = (int32_t)n;
-    if (j == 0 || incl[j - 1] != incl[j]) {
-        uint64_t k = (uint64_t)keys[j];
-        int64_t x = (int64_t)(k & ((1ull << L.bits[0]) - 1)) + L.lo[0];
-        int64_t y = (int64_t)((k >> L.bits[0]) & ((1ull << L.bits[1]) - 1)) + L.lo[1];
-        int64_t z = (int64_t)(k >> (L.bits[0] + L.bits[1])) + L.lo[2];
-        coords[3 * v + 0] = (int32_t)x;
-        coords[3 * v + 1] = (int32_t)y;
-        coords[3 * v + 2] = (int32_t)z;
-        pkeys[v] = pack_key(x, y, z);
-        offsets[v] = (int32_t)j;
+                           const int32_t *__restrict__ incl, int64_t n,
+                           const FrameParams *__restrict__ P, int32_t *__restrict__ coords,
+                           int64_t *__restrict__ pkeys, int32_t *__restrict__ p2v,
+                           int32_t *__restrict__ order, int32_t *__restrict__ offsets,
+                           DevCounts *__restrict__ C) {
+    const int bx = P->bits[0], by = P->bits[1];
+    SFB_FOR(j, n) {
+        int32_t v = incl[j] - 1;
+        uint32_t i = vals[j];
+        order[j] = (int32_t)i;
+        p2v[i] = v;
+        if (j == n - 1) {
+            offsets[v + 1] = (int32_t)n;
+            C->m[0] = v + 1;
+        }
+        if (j == 0 || incl[j - 1] != incl[j]) {
+            uint64_t k = (uint64_t)keys[j];
+            int64_t x = (int64_t)(k & ((1ull << bx) - 1)) + P->lo[0];
+            int64_t y = (int64_t)((k >> bx) & ((1ull << by) - 1)) + P->lo[1];
+            int64_t z = (int64_t)(k >> (bx + by)) + P->lo[2];
+            coords[3 * v + 0] = (int32_t)x;
+            coords[3 * v + 1] = (int32_t)y;
+            coords[3 * v + 2] = (int32_t)z;
+            pkeys[v] = pack_key(x, y, z);
+            offsets[v] = (int32_t)j;
+        }
     }
 }
 
@@ -124,11 +123,13 @@ __global__ void k_segments(const K *__restrict__ keys, const uint32_t *__restric
 // that order — bit-identical to np.add.at, with the loads in parallel.
 __global__ void k_voxel_feats(const double *__restrict__ pos, const double *__restrict__ col,
                               const int32_t *__restrict__ order, const int32_t *__restrict__ offsets,
-                              const int32_t *__restrict__ coords, int64_t m, double s,
-                              double *__restrict__ feats) {
-    const int64_t v = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+                              const int32_t *__restrict__ coords, const DevCounts *__restrict__ C,
+                              const FrameParams *__restrict__ P, double *__restrict__ feats) {
     const int lane = threadIdx.x & 31;
-    if (v >= m) return;
+    const int64_t m = C->m[0];
+    const double s = P->s;
+    for (int64_t v = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; v < m;
+         v += ((int64_t)gridDim.x * blockDim.x) >> 5) {
     const int32_t b = offsets[v], e = offsets[v + 1];
     double acc[6] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
     for (int32_t j0 = b; j0 < e; j0 += 32) {
@@ -147,7 +148,7 @@ __global__ void k_voxel_feats(const double *__restrict__ pos, const double *__re
 #pragma unroll
             for (int a = 0; a < 6; ++a) acc[a] = __dadd_rn(acc[a], __shfl_sync(0xffffffffu, val[a], q));
     }
-    if (lane != 0) return;
+    if (lane != 0) continue;
     double cnt = (double)(e - b);
     double cen[3] = {__ddiv_rn(acc[0], cnt), __ddiv_rn(acc[1], cnt), __ddiv_rn(acc[2], cnt)};
     double *f = feats + 9 * v;
@@ -159,55 +160,58 @@ __global__ void k_voxel_feats(const double *__restrict__ pos, const double *__re
         f[6 + a] = res;
         f[3 + a] = __ddiv_rn(acc[3 + a], cnt);
     }
+    }
 }
 
 template <class K>
-static void voxelize_typed(sfb_ctx *ctx, const double *pos, const double *col, int64_t n, double s,
-                           const KeyLayout &L, VoxelOut &out) {
+static void voxelize_typed(sfb_ctx *ctx, const double *pos, const double *col, int64_t n,
+                           const FrameParams *P, int key_bits, VoxelOut &out, DevCounts *C) {
     cudaStream_t st = ctx->stream;
     K *keys = ctx->arena.alloc<K>(n), *keys2 = ctx->arena.alloc<K>(n);
     uint32_t *vals = ctx->arena.alloc<uint32_t>(n), *vals2 = ctx->arena.alloc<uint32_t>(n);
-    int32_t *flag = ctx->arena.alloc<int32_t>(n), *incl = ctx->arena.alloc<int32_t>(n);
-    unsigned g = grid_for(n, 256);
-    k_keygen<K><<<g, 256, 0, st>>>(pos, n, s, L, keys, vals);
+    int32_t *flag = ctx->arena.alloc<int32_t>(n);
+    const unsigned g = dgrid(n, 256);
+    k_keygen<K><<<g, 256, 0, st>>>(pos, n, P, keys, vals);
     SFB_CHECK_LAUNCH();
-    size_t tb = 0, tb2 = 0;
-    cub::DeviceRadixSort::SortPairs(nullptr, tb, keys, keys2, vals, vals2, (int)n, 0, L.total, st);
-    cub::DeviceScan::InclusiveSum(nullptr, tb2, flag, incl, (int)n, st);
-    void *tmp = ctx->arena.alloc_bytes(tb > tb2 ? tb : tb2);
-    SFB_CUDA(cub::DeviceRadixSort::SortPairs(tmp, tb, keys, keys2, vals, vals2, (int)n, 0,
-                                             L.total > 0 ? L.total : 1, st));
-    k_heads<K><<<g, 256, 0, st>>>(keys2, n, flag);
-    SFB_CUDA(cub::DeviceScan::InclusiveSum(tmp, tb2, flag, incl, (int)n, st));
-    k_segments<K><<<g, 256, 0, st>>>(keys2, vals2, incl, n, L, out.coords, out.keys, out.p2v,
-                                     out.order, out.offsets);
+    const int which = dsort_pairs<K>(ctx, keys, vals, keys2, vals2, nullptr, n, key_bits);
+    K *ks = which ? keys2 : keys;
+    uint32_t *vs = which ? vals2 : vals;
+    k_heads<K><<<g, 256, 0, st>>>(ks, n, flag);
+    dscan(ctx, flag, flag, nullptr, n, nullptr, true);
+    k_segments<K><<<g, 256, 0, st>>>(ks, vs, flag, n, P, out.coords, out.keys, out.p2v, out.order,
+                                     out.offsets, C);
     SFB_CHECK_LAUNCH();
-    ctx->read_back(incl + (n - 1), sizeof(int32_t));
-    out.m = *reinterpret_cast<int32_t *>(ctx->pinned);
-    k_voxel_feats<<<grid_for(32 * out.m, 256), 256, 0, st>>>(pos, col, out.order, out.offsets,
-                                                             out.coords, out.m, s, out.feats);
+    k_voxel_feats<<<dgrid(32 * n, 256), 256, 0, st>>>(pos, col, out.order, out.offsets, out.coords,
+                                                      C, P, out.feats);
     SFB_CHECK_LAUNCH();
 }
 
-void voxelize_run(sfb_ctx *ctx, const double *pos, const double *col, int64_t n, double s,
-                  const double *lo_hi, VoxelOut &out) {
-    SFB_REQUIRE(n >= 2, "voxelization needs at least 2 points");
-    SFB_REQUIRE(n < (int64_t(1) << 31), "at most 2^31-1 points per cloud");
+// Host half of voxelize_adaptive's key setup: s and the per-axis ranges are
+// known from the bbox, so the compact key needs only the bits the cloud spans.
+void voxel_layout(const double *lo_hi, double s, FrameParams &P) {
     SFB_REQUIRE(s > 0.0 && s == s, "voxel scale must be positive");
-    KeyLayout L{};
-    L.total = 0;
+    P.s = s;
+    P.inv_s = 1.0 / s;
+    P.total = 0;
     for (int a = 0; a < 3; ++a) {
         // floor(lo*s) .. floor(hi*s) bounds floor(p*s) for every point (monotone rounding)
         int64_t lo = (int64_t)std::floor(lo_hi[a] * s);
         int64_t hi = (int64_t)std::floor(lo_hi[3 + a] * s);
         SFB_REQUIRE(lo > -(int64_t(1) << 20) && hi < (int64_t(1) << 20),
                     "voxel coordinates must satisfy |c| < 1048576");
-        L.lo[a] = lo;
-        L.bits[a] = bits_for((uint64_t)(hi - lo));
-        L.total += L.bits[a];
+        P.lo[a] = lo;
+        P.bits[a] = bits_for((uint64_t)(hi - lo));
+        P.total += P.bits[a];
     }
-    if (L.total <= 32) voxelize_typed<uint32_t>(ctx, pos, col, n, s, L, out);
-    else voxelize_typed<uint64_t>(ctx, pos, col, n, s, L, out);
+}
+
+void voxelize_run(sfb_ctx *ctx, const double *pos, const double *col, int64_t n,
+                  const FrameParams &host, const FrameParams *P, VoxelOut &out, DevCounts *C) {
+    SFB_REQUIRE(n >= 2, "voxelization needs at least 2 points");
+    SFB_REQUIRE(n < (int64_t(1) << 31), "at most 2^31-1 points per cloud");
+    const int bits = host.total > 0 ? host.total : 1;
+    if (host.total <= 32) voxelize_typed<uint32_t>(ctx, pos, col, n, P, bits, out, C);
+    else voxelize_typed<unsigned long long>(ctx, pos, col, n, P, bits, out, C);
 }
 
 }  // namespace sfb
