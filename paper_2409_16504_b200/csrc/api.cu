@@ -507,6 +507,15 @@ int sfb_frame(sfb_ctx *ctx, const double *positions, const double *colors, int64
             enqueue_frame(ctx, positions, colors, n, host, P, cam, opts, plane_mask, rgb, normal,
                           depth, trans);
             G->seen = 1;
+            // size hints for the capture (grids only; kernels loop over device counts)
+            DevCounts c{};
+            SFB_CUDA(cudaMemcpyAsync(&c, ctx->last_counts, sizeof(c), cudaMemcpyDeviceToHost,
+                                     ctx->stream));
+            SFB_CUDA(cudaStreamSynchronize(ctx->stream));
+            for (int l = 0; l < 9; ++l) ctx->hint_m[l] = c.m[l];
+            ctx->hint_kept = c.kept;
+            ctx->hint_runs = c.runs;
+            ctx->hint_e = c.es + c.ef;
             return;
         }
         if (!G->exec) {

@@ -129,6 +129,14 @@ struct sfb_ctx {
     std::vector<sfb_frame_graph *> graphs;
     int64_t graph_nodes = 0;
     sfb::DevCounts *last_counts = nullptr;   // device counts of the last call
+    // launch-size hints (host copies of the counts of the last eager frame):
+    // every kernel loops over its device count, so hints only size grids
+    int64_t hint_m[9] = {}, hint_kept = 0, hint_runs = 0, hint_e = 0;
+    int64_t grid_bound(int64_t bound, int64_t hint) const {
+        if (hint <= 0) return bound;
+        int64_t g = hint + hint / 4 + 1024;
+        return g < bound ? g : bound;
+    }
     int num_sms = 148;
     std::string last_error;
     sfb_stats stats{};
@@ -257,9 +265,11 @@ struct HashTable {
     uint32_t *mask = nullptr;  // device: capacity - 1, sized from the device count
 };
 // counts: device pointer d_m (or nullptr -> m_bound is the exact count)
-HashTable hash_build(sfb_ctx *ctx, const int32_t *coords, const int64_t *d_m, int64_t m_bound);
+HashTable hash_build(sfb_ctx *ctx, const int32_t *coords, const int64_t *d_m, int64_t m_bound,
+                     int64_t m_grid = -1);
 void kernel_map_build(sfb_ctx *ctx, const HashTable &h, const int32_t *coords, const int64_t *d_m,
-                      int64_t m_bound, int stride, int kernel, int32_t *map_tap_major);
+                      int64_t m_bound, int stride, int kernel, int32_t *map_tap_major,
+                      int64_t m_grid = -1);
 void transposed_lookup(sfb_ctx *ctx, const HashTable &h, int parent_stride,
                        const int32_t *targets, const int64_t *d_m, int64_t m_bound,
                        int32_t *parent_out, int32_t *tap_out);
@@ -269,6 +279,11 @@ void pool_build(sfb_ctx *ctx, const int32_t *coords, const int64_t *d_m, int64_t
                 int c, int ld_in, int32_t *parent_coords, float *parent_feats, int ld_out,
                 int32_t *child_to_parent, int64_t *d_mp);
 void coords_layout(sfb_ctx *ctx, const int32_t *coords, int64_t m, FrameParams &P);
+// sort-free pooling for the fused UNet: parents in first-child order
+void pool_fast(sfb_ctx *ctx, const int32_t *coords, const int64_t *d_m, int64_t m_bound,
+               int64_t m_grid, int stride, const float *feats, int c, int ld_in,
+               int32_t *parent_coords, float *parent_feats, int ld_out, int32_t *child_to_parent,
+               int64_t *d_mp);
 
 // voxelize.cu
 struct VoxelOut {
@@ -292,10 +307,10 @@ void activate_run(sfb_ctx *ctx, const float *raw, int64_t m, double scale, doubl
                   double *sigma, double *quat, double *opac, double *normal);
 void conv_layer(sfb_ctx *ctx, const NetLayer &L, const float *in, int ld_in, const int32_t *nbr,
                 int64_t nbr_ld, const int64_t *d_m, int64_t m_bound, int relu, float *out,
-                int ld_out);
+                int ld_out, int64_t m_grid = -1);
 void tconv_layer(sfb_ctx *ctx, const NetLayer &L, const float *in, int ld_in,
                  const int32_t *parent, const int32_t *tap, const int64_t *d_m, int64_t m_bound,
-                 int relu, float *out, int ld_out);
+                 int relu, float *out, int ld_out, int64_t m_grid = -1);
 void layer_set(sfb_ctx *ctx, int kind, int kernel, int cin, int cout, const float *w_host,
                const float *b_host);
 // per-voxel Gaussians for the fused frame: centres, sigma, quat, opacity, normal

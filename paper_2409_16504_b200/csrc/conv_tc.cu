@@ -324,7 +324,7 @@ int pad_n(int c) { return c <= 16 ? 16 : (c <= 32 ? 32 : (c <= 64 ? 64 : (c <= 1
 template <int KP, int NP>
 void launch_tc(sfb_ctx *ctx, const NetLayer &L, const float *in, int ld_in, const int32_t *nbr,
                int64_t nbr_ld, const int64_t *d_m, int64_t m_bound, int relu, float *out,
-               int ld_out) {
+               int ld_out, int64_t m_grid) {
     using S = TcShape<KP, NP>;
     static bool attr = false;
     if (!attr) {
@@ -332,7 +332,7 @@ void launch_tc(sfb_ctx *ctx, const NetLayer &L, const float *in, int ld_in, cons
                                       S::SMEM));
         attr = true;
     }
-    const int64_t tiles_bound = (m_bound + kM - 1) / kM;
+    const int64_t tiles_bound = (m_grid + kM - 1) / kM;
     const int64_t work_bound = tiles_bound * choose_splits(tiles_bound, L.taps, kSplitTarget);
     const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(work_bound, kSplitTarget));
     float *partial = ctx->arena.alloc<float>((size_t)std::min<int64_t>(kMaxPartialRows,
@@ -341,7 +341,7 @@ void launch_tc(sfb_ctx *ctx, const NetLayer &L, const float *in, int ld_in, cons
         in, ld_in, L.cin, nbr, nbr_ld, d_m, m_bound, L.taps, L.w_tc, L.b, L.cout, relu, out, ld_out,
         partial);
     SFB_CHECK_LAUNCH();
-    k_splitk_reduce<<<dgrid(std::min<int64_t>(m_bound, kMaxPartialRows) * L.cout, 256), 256, 0,
+    k_splitk_reduce<<<dgrid(std::min<int64_t>(m_grid, kMaxPartialRows) * L.cout, 256), 256, 0,
                       ctx->stream>>>(partial, d_m, m_bound, L.taps, NP, L.b, L.cout, relu, out,
                                      ld_out);
     SFB_CHECK_LAUNCH();
@@ -370,10 +370,10 @@ void prepare_tc_weights(sfb_ctx *ctx, NetLayer &L) {
 
 void conv_layer_tc(sfb_ctx *ctx, const NetLayer &L, const float *in, int ld_in, const int32_t *nbr,
                    int64_t nbr_ld, const int64_t *d_m, int64_t m_bound, int relu, float *out,
-                   int ld_out) {
+                   int ld_out, int64_t m_grid) {
 #define SFB_TC_CASE(K, N)                                                                 \
     if (L.cin_pad == K && L.cout_pad == N) {                                              \
-        launch_tc<K, N>(ctx, L, in, ld_in, nbr, nbr_ld, d_m, m_bound, relu, out, ld_out); \
+        launch_tc<K, N>(ctx, L, in, ld_in, nbr, nbr_ld, d_m, m_bound, relu, out, ld_out, m_grid); \
         return;                                                                           \
     }
     SFB_TC_CASE(16, 16) SFB_TC_CASE(16, 32) SFB_TC_CASE(16, 64) SFB_TC_CASE(16, 128)

@@ -65,13 +65,16 @@ k_scan_apply(const int32_t *__restrict__ in, const int64_t *__restrict__ d_n, in
     const int64_t n = d_n ? *d_n : n_fixed;
     const int64_t ch = chunk_of(n, gridDim.x);
     const int64_t b0 = blockIdx.x * ch, b1 = min(n, b0 + ch);
-    if (threadIdx.x == 0) {
-        int32_t acc = 0;
-        for (int b = 0; b < (int)blockIdx.x; ++b) acc += part[b];
-        s_base = acc;
-        if (blockIdx.x == gridDim.x - 1 && total_out) *total_out = acc + part[blockIdx.x];
+    {   // base = sum of the partials of earlier blocks (parallel, <= 1024 blocks)
+        const int32_t v = (int)threadIdx.x < (int)blockIdx.x ? part[threadIdx.x] : 0;
+        int32_t tot;
+        block_excl_scan(v, s_warp, &tot);
+        if (threadIdx.x == 0) {
+            s_base = tot;
+            if (blockIdx.x == gridDim.x - 1 && total_out) *total_out = tot + part[blockIdx.x];
+        }
+        __syncthreads();
     }
-    __syncthreads();
     int32_t base = s_base;
     for (int64_t t0 = b0; t0 < b1; t0 += blockDim.x) {
         const int64_t i = t0 + threadIdx.x;
@@ -122,34 +125,57 @@ constexpr int kRsBlocks = 148;
 constexpr int kRsThreads = 256;
 constexpr int kRsWarps = kRsThreads / 32;
 
+// blocks that take part in a pass: ~kRsItems items each, at most gridDim.x
+constexpr int kRsItems = 2048;
+__device__ __forceinline__ int rs_blocks(int64_t n) {
+    int64_t b = (n + kRsItems - 1) / kRsItems;
+    return (int)max((int64_t)1, min(b, (int64_t)gridDim.x));
+}
+
 template <class K>
 __global__ void __launch_bounds__(kRsThreads)
 k_rs_upsweep(const K *__restrict__ keys, const int64_t *__restrict__ d_n, int64_t n_fixed, int shift,
              int32_t *__restrict__ hist) {
     __shared__ int32_t h[256];
+    const int64_t n = d_n ? *d_n : n_fixed;
+    const int nb = rs_blocks(n);
+    if ((int)blockIdx.x >= nb) return;
     h[threadIdx.x] = 0;
     __syncthreads();
-    const int64_t n = d_n ? *d_n : n_fixed;
-    const int64_t ch = chunk_of(n, gridDim.x);
+    const int64_t ch = chunk_of(n, nb);
     const int64_t b0 = blockIdx.x * ch, b1 = min(n, b0 + ch);
     for (int64_t i = b0 + threadIdx.x; i < b1; i += blockDim.x)
         atomicAdd(&h[(uint32_t)(keys[i] >> shift) & 255u], 1);
     __syncthreads();
-    hist[threadIdx.x * gridDim.x + blockIdx.x] = h[threadIdx.x];
+    hist[threadIdx.x * nb + blockIdx.x] = h[threadIdx.x];
 }
 
-// exclusive scan of the digit-major histogram (256 x blocks), one CTA
-__global__ void __launch_bounds__(1024) k_rs_scan(int32_t *__restrict__ hist, int count) {
+// exclusive scan of the digit-major histogram (256 x active blocks), one CTA:
+// coalesced load into shared memory, per-thread serial segment, one block scan
+constexpr int kRsScanMax = 256 * 148;
+__global__ void __launch_bounds__(1024)
+k_rs_scan(int32_t *__restrict__ hist, const int64_t *__restrict__ d_n, int64_t n_fixed) {
+    extern __shared__ int32_t sh[];
     __shared__ int32_t s_warp[32];
-    int32_t base = 0;
-    for (int t0 = 0; t0 < count; t0 += blockDim.x) {
-        const int i = t0 + threadIdx.x;
-        const int32_t v = i < count ? hist[i] : 0;
-        int32_t tot;
-        const int32_t ex = block_excl_scan(v, s_warp, &tot);
-        if (i < count) hist[i] = base + ex;
-        base += tot;
+    const int64_t n = d_n ? *d_n : n_fixed;
+    int64_t b = (n + kRsItems - 1) / kRsItems;
+    const int nb = (int)max((int64_t)1, min(b, (int64_t)148));
+    const int count = 256 * nb;
+    for (int i = threadIdx.x; i < count; i += blockDim.x) sh[i] = hist[i];
+    __syncthreads();
+    const int per = (count + blockDim.x - 1) / blockDim.x;
+    const int b0 = threadIdx.x * per, b1 = min(count, b0 + per);
+    int32_t sum = 0;
+    for (int i = b0; i < b1; ++i) sum += sh[i];
+    int32_t tot;
+    int32_t run = block_excl_scan(sum, s_warp, &tot);
+    for (int i = b0; i < b1; ++i) {
+        const int32_t v = sh[i];
+        sh[i] = run;
+        run += v;
     }
+    __syncthreads();
+    for (int i = threadIdx.x; i < count; i += blockDim.x) hist[i] = sh[i];
 }
 
 // stable scatter: each block walks its chunk in order, 256 items at a time;
@@ -163,11 +189,13 @@ k_rs_downsweep(const K *__restrict__ kin, const uint32_t *__restrict__ vin, K *_
     __shared__ int32_t run[256];
     __shared__ int32_t wcnt[kRsWarps][256];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    run[threadIdx.x] = hist[threadIdx.x * gridDim.x + blockIdx.x];
+    const int64_t n = d_n ? *d_n : n_fixed;
+    const int nb = rs_blocks(n);
+    if ((int)blockIdx.x >= nb) return;
+    run[threadIdx.x] = hist[threadIdx.x * nb + blockIdx.x];
     for (int w = 0; w < kRsWarps; ++w) wcnt[w][threadIdx.x] = 0;
     __syncthreads();
-    const int64_t n = d_n ? *d_n : n_fixed;
-    const int64_t ch = chunk_of(n, gridDim.x);
+    const int64_t ch = chunk_of(n, nb);
     const int64_t b0 = blockIdx.x * ch, b1 = min(n, b0 + ch);
     const uint32_t lt = (1u << lane) - 1u;
     for (int64_t t0 = b0; t0 < b1; t0 += kRsThreads) {
@@ -204,11 +232,17 @@ int dsort_pairs(sfb_ctx *ctx, K *k0, uint32_t *v0, K *k1, uint32_t *v1, const in
                 int64_t n_fixed, int bits) {
     const int passes = (bits + 7) / 8;
     int32_t *hist = ctx->arena.alloc<int32_t>(256 * kRsBlocks);
+    static bool attr = false;
+    if (!attr) {
+        SFB_CUDA(cudaFuncSetAttribute(k_rs_scan, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      kRsScanMax * (int)sizeof(int32_t)));
+        attr = true;
+    }
     for (int p = 0; p < passes; ++p) {
         K *ki = (p & 1) ? k1 : k0, *ko = (p & 1) ? k0 : k1;
         uint32_t *vi = (p & 1) ? v1 : v0, *vo = (p & 1) ? v0 : v1;
         k_rs_upsweep<K><<<kRsBlocks, kRsThreads, 0, ctx->stream>>>(ki, d_n, n_fixed, 8 * p, hist);
-        k_rs_scan<<<1, 1024, 0, ctx->stream>>>(hist, 256 * kRsBlocks);
+        k_rs_scan<<<1, 1024, kRsScanMax * sizeof(int32_t), ctx->stream>>>(hist, d_n, n_fixed);
         if (v0)
             k_rs_downsweep<K, true><<<kRsBlocks, kRsThreads, 0, ctx->stream>>>(ki, vi, ko, vo, d_n,
                                                                                n_fixed, 8 * p, hist);

@@ -67,15 +67,18 @@ __device__ __forceinline__ int32_t hash_find(const HashTable &h, uint32_t mask, 
     }
 }
 
-HashTable hash_build(sfb_ctx *ctx, const int32_t *coords, const int64_t *d_m, int64_t m_bound) {
+HashTable hash_build(sfb_ctx *ctx, const int32_t *coords, const int64_t *d_m, int64_t m_bound,
+                     int64_t m_grid) {
+    if (m_grid < 0) m_grid = m_bound;
     HashTable h;
-    uint64_t cap = 64;
+    uint64_t cap = 64, capg = 64;
     while (cap < (uint64_t)(2 * m_bound)) cap <<= 1;
+    while (capg < (uint64_t)(2 * m_grid)) capg <<= 1;
     h.keys = ctx->arena.alloc<unsigned long long>(cap);
     h.vals = ctx->arena.alloc<int32_t>(cap);
     h.mask = ctx->arena.alloc<uint32_t>(1);
-    k_hash_clear<<<dgrid((int64_t)cap, 256), 256, 0, ctx->stream>>>(h, d_m, m_bound);
-    k_hash_insert<<<dgrid(m_bound, 256), 256, 0, ctx->stream>>>(coords, d_m, m_bound, h);
+    k_hash_clear<<<dgrid((int64_t)capg, 256), 256, 0, ctx->stream>>>(h, d_m, m_bound);
+    k_hash_insert<<<dgrid(m_grid, 256), 256, 0, ctx->stream>>>(coords, d_m, m_bound, h);
     SFB_CHECK_LAUNCH();
     return h;
 }
@@ -99,9 +102,11 @@ __global__ void k_kernel_map(const int32_t *__restrict__ coords, const int64_t *
 }
 
 void kernel_map_build(sfb_ctx *ctx, const HashTable &h, const int32_t *coords, const int64_t *d_m,
-                      int64_t m_bound, int stride, int kernel, int32_t *map_tap_major) {
+                      int64_t m_bound, int stride, int kernel, int32_t *map_tap_major,
+                      int64_t m_grid) {
+    if (m_grid < 0) m_grid = m_bound;
     const int taps = kernel * kernel * kernel;
-    k_kernel_map<<<dgrid(m_bound * taps, 256), 256, 0, ctx->stream>>>(
+    k_kernel_map<<<dgrid(m_grid * taps, 256), 256, 0, ctx->stream>>>(
         coords, d_m, m_bound, m_bound, stride, kernel, h, map_tap_major);
     SFB_CHECK_LAUNCH();
 }
@@ -259,6 +264,126 @@ void pool_build(sfb_ctx *ctx, const int32_t *coords, const int64_t *d_m, int64_t
     else
         pool_typed<unsigned long long>(ctx, coords, d_m, m_bound, stride, P, bits, feats, c, ld_in,
                                        parent_coords, parent_feats, ld_out, child_to_parent, d_mp);
+}
+
+// ---------------------------------------------------------------- fast pooling
+// Pooling inside the fused UNet does not need canonical parent order: every
+// conv output row depends only on its own neighbourhood, so parents are
+// numbered in order of their first child (deterministic, no sort). Each
+// parent still averages its children in increasing child row, like
+// np.add.at (the <= 8 children are sorted in-register before summing).
+__global__ void k_pool_clear(unsigned long long *__restrict__ keys, int32_t *__restrict__ minrow,
+                             int32_t *__restrict__ nkids, uint32_t *__restrict__ mask,
+                             const int64_t *__restrict__ d_m) {
+    const int64_t m = *d_m;
+    uint64_t cap = 64;
+    while (cap < (uint64_t)(2 * m)) cap <<= 1;
+    if (blockIdx.x == 0 && threadIdx.x == 0) *mask = (uint32_t)(cap - 1);
+    SFB_FOR(i, (int64_t)cap) {
+        keys[i] = kEmpty;
+        minrow[i] = INT_MAX;
+    }
+    SFB_FOR(i, m) nkids[i] = 0;
+}
+
+__global__ void k_pool_insert(const int32_t *__restrict__ coords, const int64_t *__restrict__ d_m,
+                              int64_t S, unsigned long long *__restrict__ keys,
+                              int32_t *__restrict__ minrow, const uint32_t *__restrict__ d_mask,
+                              int32_t *__restrict__ slot_of) {
+    const int64_t m = *d_m;
+    const uint32_t mask = *d_mask;
+    SFB_FOR(j, m) {
+        const int64_t px = floor_div(coords[3 * j], S) * S, py = floor_div(coords[3 * j + 1], S) * S,
+                      pz = floor_div(coords[3 * j + 2], S) * S;
+        const unsigned long long key = (unsigned long long)pack_key(px, py, pz);
+        uint32_t slot = hash64(key) & mask;
+        while (true) {
+            const unsigned long long prev = atomicCAS(&keys[slot], kEmpty, key);
+            if (prev == kEmpty || prev == key) break;
+            slot = (slot + 1) & mask;
+        }
+        atomicMin(&minrow[slot], (int32_t)j);
+        slot_of[j] = (int32_t)slot;
+    }
+}
+
+__global__ void k_pool_first(const int32_t *__restrict__ slot_of, const int32_t *__restrict__ minrow,
+                             const int64_t *__restrict__ d_m, int32_t *__restrict__ flag) {
+    const int64_t m = *d_m;
+    SFB_FOR(j, m) flag[j] = minrow[slot_of[j]] == (int32_t)j;
+}
+
+__global__ void k_pool_assign(const int32_t *__restrict__ coords, const int32_t *__restrict__ slot_of,
+                              const int32_t *__restrict__ minrow, const int32_t *__restrict__ pid_of_first,
+                              const int64_t *__restrict__ d_m, int64_t S, int32_t *__restrict__ pcoords,
+                              int32_t *__restrict__ c2p, int32_t *__restrict__ nkids,
+                              int32_t *__restrict__ kids) {
+    const int64_t m = *d_m;
+    SFB_FOR(j, m) {
+        const int32_t first = minrow[slot_of[j]];
+        const int32_t pid = pid_of_first[first];
+        c2p[j] = pid;
+        if (first == (int32_t)j)
+            for (int a = 0; a < 3; ++a) pcoords[3 * pid + a] = (int32_t)(floor_div(coords[3 * j + a], S) * S);
+        const int32_t k = atomicAdd(&nkids[pid], 1);
+        if (k < 8) kids[8 * (int64_t)pid + k] = (int32_t)j;
+    }
+}
+
+__global__ void k_pool_means_fast(const float *__restrict__ feats, int ld_in, int c,
+                                  const int32_t *__restrict__ nkids, const int32_t *__restrict__ kids,
+                                  const int64_t *__restrict__ d_mp, float *__restrict__ out,
+                                  int ld_out) {
+    const int64_t mp = *d_mp;
+    SFB_FOR(idx, mp * c) {
+        const int64_t v = idx / c;
+        const int ch = (int)(idx % c);
+        const int cnt = min(nkids[v], 8);
+        int32_t kk[8];
+        for (int q = 0; q < cnt; ++q) kk[q] = kids[8 * v + q];
+        for (int q = 1; q < cnt; ++q) {   // ascending child rows
+            const int32_t x = kk[q];
+            int r = q - 1;
+            while (r >= 0 && kk[r] > x) {
+                kk[r + 1] = kk[r];
+                --r;
+            }
+            kk[r + 1] = x;
+        }
+        float acc = 0.f;
+        for (int q = 0; q < cnt; ++q) acc = __fadd_rn(acc, feats[(int64_t)kk[q] * ld_in + ch]);
+        out[v * ld_out + ch] = __fdiv_rn(acc, (float)cnt);
+    }
+}
+
+void pool_fast(sfb_ctx *ctx, const int32_t *coords, const int64_t *d_m, int64_t m_bound,
+               int64_t m_grid, int stride, const float *feats, int c, int ld_in,
+               int32_t *parent_coords, float *parent_feats, int ld_out, int32_t *child_to_parent,
+               int64_t *d_mp) {
+    cudaStream_t st = ctx->stream;
+    const int64_t S = 2 * (int64_t)stride;
+    uint64_t cap = 64;
+    while (cap < (uint64_t)(2 * m_bound)) cap <<= 1;
+    uint64_t cap_grid = 64;
+    while (cap_grid < (uint64_t)(2 * m_grid)) cap_grid <<= 1;
+    auto *keys = ctx->arena.alloc<unsigned long long>(cap);
+    int32_t *minrow = ctx->arena.alloc<int32_t>(cap);
+    uint32_t *mask = ctx->arena.alloc<uint32_t>(1);
+    int32_t *slot_of = ctx->arena.alloc<int32_t>(m_bound);
+    int32_t *flag = ctx->arena.alloc<int32_t>(m_bound);
+    int32_t *nkids = ctx->arena.alloc<int32_t>(m_bound);
+    int32_t *kids = ctx->arena.alloc<int32_t>(8 * m_bound);
+    const unsigned g = dgrid(m_grid, 256);
+    k_pool_clear<<<dgrid((int64_t)cap_grid, 256), 256, 0, st>>>(keys, minrow, nkids, mask, d_m);
+    k_pool_insert<<<g, 256, 0, st>>>(coords, d_m, S, keys, minrow, mask, slot_of);
+    k_pool_first<<<g, 256, 0, st>>>(slot_of, minrow, d_m, flag);
+    SFB_CHECK_LAUNCH();
+    dscan(ctx, flag, flag, d_m, m_bound, d_mp, false);
+    k_pool_assign<<<g, 256, 0, st>>>(coords, slot_of, minrow, flag, d_m, S, parent_coords,
+                                     child_to_parent, nkids, kids);
+    k_pool_means_fast<<<dgrid(m_grid * c, 256), 256, 0, st>>>(feats, ld_in, c, nkids, kids, d_mp,
+                                                              parent_feats, ld_out);
+    SFB_CHECK_LAUNCH();
 }
 
 // Key layout of an arbitrary coordinate set (standalone pool API): one

@@ -21,7 +21,7 @@ namespace sfb {
 
 void conv_layer_tc(sfb_ctx *ctx, const NetLayer &L, const float *in, int ld_in, const int32_t *nbr,
                    int64_t nbr_ld, const int64_t *d_m, int64_t m_bound, int relu, float *out,
-                   int ld_out);
+                   int ld_out, int64_t m_grid);
 bool conv_tc_supported(const NetLayer &L);
 void prepare_tc_weights(sfb_ctx *ctx, NetLayer &L);
 
@@ -209,10 +209,11 @@ k_conv_simt(const float *__restrict__ in, int ld_in, const int32_t *__restrict__
 
 void conv_layer(sfb_ctx *ctx, const NetLayer &L, const float *in, int ld_in, const int32_t *nbr,
                 int64_t nbr_ld, const int64_t *d_m, int64_t m_bound, int relu, float *out,
-                int ld_out) {
+                int ld_out, int64_t m_grid) {
     if (m_bound == 0) return;
+    if (m_grid < 0) m_grid = m_bound;
     if (ctx->net_mode == SFB_NET_TC_TF32X3 && L.w_tc) {
-        conv_layer_tc(ctx, L, in, ld_in, nbr, nbr_ld, d_m, m_bound, relu, out, ld_out);
+        conv_layer_tc(ctx, L, in, ld_in, nbr, nbr_ld, d_m, m_bound, relu, out, ld_out, m_grid);
         return;
     }
     SFB_REQUIRE(kRows * L.cout <= kMaxOut * kThreads, "conv: cout > 128 unsupported");
@@ -224,7 +225,7 @@ void conv_layer(sfb_ctx *ctx, const NetLayer &L, const float *in, int ld_in, con
                                       200 * 1024));
         attr = true;
     }
-    k_conv_simt<<<dgrid(m_bound, kRows, 4), kThreads, smem, ctx->stream>>>(
+    k_conv_simt<<<dgrid(m_grid, kRows, 4), kThreads, smem, ctx->stream>>>(
         in, ld_in, nbr, nbr_ld, d_m, m_bound, L.taps, L.cin, L.cout, L.w, L.b, relu, out, ld_out);
     SFB_CHECK_LAUNCH();
 }
@@ -252,9 +253,10 @@ __global__ void k_tconv(const float *__restrict__ in, int ld_in, const int32_t *
 
 void tconv_layer(sfb_ctx *ctx, const NetLayer &L, const float *in, int ld_in,
                  const int32_t *parent, const int32_t *tap, const int64_t *d_m, int64_t m_bound,
-                 int relu, float *out, int ld_out) {
+                 int relu, float *out, int ld_out, int64_t m_grid) {
     if (m_bound == 0) return;
-    k_tconv<<<dgrid(m_bound * L.cout, 256), 256, 0, ctx->stream>>>(
+    if (m_grid < 0) m_grid = m_bound;
+    k_tconv<<<dgrid(m_grid * L.cout, 256), 256, 0, ctx->stream>>>(
         in, ld_in, parent, tap, d_m, m_bound, L.cin, L.cout, L.w, L.b, relu, out, ld_out);
     SFB_CHECK_LAUNCH();
 }
@@ -430,40 +432,43 @@ void unet_run(sfb_ctx *ctx, const int32_t *coords0, const double *feats9, int64_
     std::vector<int> width(L);
     coords[0] = coords0;
     for (int l = 0; l < L; ++l) width[l] = dec[L - 1 - l] + enc[l + 1];
+    std::vector<int64_t> mg(L + 1);
+    for (int l = 0; l <= L; ++l) mg[l] = ctx->grid_bound(mb, ctx->hint_m[l]);
     pin[0] = ctx->arena.alloc<float>((size_t)mb * enc[0]);
-    k_feats_to_f32<<<dgrid(mb * enc[0], 256), 256, 0, st>>>(feats9, &C->m[0], enc[0], pin[0]);
+    k_feats_to_f32<<<dgrid(mg[0] * enc[0], 256), 256, 0, st>>>(feats9, &C->m[0], enc[0], pin[0]);
     SFB_CHECK_LAUNCH();
     int layer = 0;
     for (int l = 0; l <= L; ++l) {
         const int stride = 1 << l;
         const int64_t *dm = &C->m[l];
-        HashTable h = hash_build(ctx, coords[l], dm, mb);
+        HashTable h = hash_build(ctx, coords[l], dm, mb, mg[l]);
         const int kern = net.layers[layer].kernel, taps = kern * kern * kern;
         nbr[l] = ctx->arena.alloc<int32_t>((size_t)taps * mb);
-        kernel_map_build(ctx, h, coords[l], dm, mb, stride, kern, nbr[l]);
+        kernel_map_build(ctx, h, coords[l], dm, mb, stride, kern, nbr[l], mg[l]);
         if (l == L) break;
         cat[l] = ctx->arena.alloc<float>((size_t)mb * width[l]);
         const int up = dec[L - 1 - l];
         conv_layer(ctx, net.layers[layer++], pin[l], enc[l], nbr[l], mb, dm, mb, 1, cat[l] + up,
-                   width[l]);
+                   width[l], mg[l]);
         int32_t *pc = ctx->arena.alloc<int32_t>((size_t)mb * 3);
         pin[l + 1] = ctx->arena.alloc<float>((size_t)mb * enc[l + 1]);
         c2p[l] = ctx->arena.alloc<int32_t>(mb);
-        pool_build(ctx, coords[l], dm, mb, stride, host, P, cat[l] + up, enc[l + 1], width[l], pc,
-                   pin[l + 1], enc[l + 1], c2p[l], &C->m[l + 1]);
+        // sort-free pooling: coarse rows in first-child order (results per voxel unchanged)
+        pool_fast(ctx, coords[l], dm, mb, mg[l], stride, cat[l] + up, enc[l + 1], width[l], pc,
+                  pin[l + 1], enc[l + 1], c2p[l], &C->m[l + 1]);
         coords[l + 1] = pc;
     }
     float *bott = ctx->arena.alloc<float>((size_t)mb * enc[L + 1]);
     conv_layer(ctx, net.layers[layer++], pin[L], enc[L], nbr[L], mb, &C->m[L], mb, 1, bott,
-               enc[L + 1]);
+               enc[L + 1], mg[L]);
     const float *coarse = bott;
     int ld_coarse = enc[L + 1];
     for (int l = L - 1; l >= 0; --l) {
         int32_t *tap = ctx->arena.alloc<int32_t>(mb);
-        k_child_tap<<<dgrid(mb, 256), 256, 0, st>>>(coords[l], &C->m[l], 1 << l, tap);
+        k_child_tap<<<dgrid(mg[l], 256), 256, 0, st>>>(coords[l], &C->m[l], 1 << l, tap);
         SFB_CHECK_LAUNCH();
         tconv_layer(ctx, net.layers[layer++], coarse, ld_coarse, c2p[l], tap, &C->m[l], mb, 1,
-                    cat[l], width[l]);
+                    cat[l], width[l], mg[l]);
         coarse = cat[l];
         ld_coarse = width[l];
     }
@@ -477,7 +482,7 @@ void unet_run(sfb_ctx *ctx, const int32_t *coords0, const double *feats9, int64_
         attr = true;
     }
     SFB_REQUIRE(smem <= 200 * 1024, "head MLP too wide");
-    k_head_mlp<<<dgrid(mb, kHeadRows, 4), 128, smem, st>>>(cat[0], width[0], &C->m[0], h1.cin,
+    k_head_mlp<<<dgrid(mg[0], kHeadRows, 4), 128, smem, st>>>(cat[0], width[0], &C->m[0], h1.cin,
                                                            h1.cout, h1.w, h1.b, h2.w, h2.b, raw);
     SFB_CHECK_LAUNCH();
 }

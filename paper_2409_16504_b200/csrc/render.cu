@@ -178,8 +178,11 @@ static uint32_t *depth_order(sfb_ctx *ctx, const RenderInputs &in, const Proj &P
     uint32_t *v0 = ctx->arena.alloc<uint32_t>(n), *v1 = ctx->arena.alloc<uint32_t>(n);
     k_depth_keys<<<dgrid(n, 256), 256, 0, ctx->stream>>>(n, in.point_to_geom, P, k0, v0, &C->kept);
     SFB_CHECK_LAUNCH();
-    const int which = dsort_pairs<unsigned long long>(ctx, k0, v0, k1, v1, nullptr, n, 64);
-    return which ? v1 : v0;
+    size_t tb = 0;
+    cub::DeviceRadixSort::SortPairs(nullptr, tb, k0, k1, v0, v1, (int)n, 0, 64, ctx->stream);
+    void *tmp = ctx->arena.alloc_bytes(tb);
+    SFB_CUDA(cub::DeviceRadixSort::SortPairs(tmp, tb, k0, k1, v0, v1, (int)n, 0, 64, ctx->stream));
+    return v1;
 }
 
 // ------------------------------------------------------------ 3. runs
@@ -701,8 +704,8 @@ void render_run(sfb_ctx *ctx, const RenderInputs &in, const FrameParams *FP, int
         dscan(ctx, R.nf, pos, &C->runs1, nb + 1, &C->ef, false);
         dscan(ctx, R.ns, pos + (nb + 1), &C->runs1, nb + 1, &C->es, false);
         dscan(ctx, R.ng, pos + 2 * (nb + 1), &C->runs1, nb + 1, &C->g, false);
-        k_emit<<<g, 256, 0, st>>>(R, pos, pos + (nb + 1), pos + 2 * (nb + 1), ntx, nsx, fkey, fval,
-                                  skey, sval, glist);
+        k_emit<<<dgrid(ctx->grid_bound(n, ctx->hint_runs), 256), 256, 0, st>>>(
+            R, pos, pos + (nb + 1), pos + 2 * (nb + 1), ntx, nsx, fkey, fval, skey, sval, glist);
         SFB_CHECK_LAUNCH();
         // stable sort by tile id keeps each tile's runs in rank order
         const int fbits = bits_for((uint64_t)nt), sbits = bits_for((uint64_t)ns);

@@ -173,9 +173,13 @@ static void voxelize_typed(sfb_ctx *ctx, const double *pos, const double *col, i
     const unsigned g = dgrid(n, 256);
     k_keygen<K><<<g, 256, 0, st>>>(pos, n, P, keys, vals);
     SFB_CHECK_LAUNCH();
-    const int which = dsort_pairs<K>(ctx, keys, vals, keys2, vals2, nullptr, n, key_bits);
-    K *ks = which ? keys2 : keys;
-    uint32_t *vs = which ? vals2 : vals;
+    // host-known n: CUB onesweep (captured into the frame graph like any launch)
+    size_t tb = 0;
+    cub::DeviceRadixSort::SortPairs(nullptr, tb, keys, keys2, vals, vals2, (int)n, 0, key_bits, st);
+    void *tmp = ctx->arena.alloc_bytes(tb);
+    SFB_CUDA(cub::DeviceRadixSort::SortPairs(tmp, tb, keys, keys2, vals, vals2, (int)n, 0, key_bits, st));
+    K *ks = keys2;
+    uint32_t *vs = vals2;
     k_heads<K><<<g, 256, 0, st>>>(ks, n, flag);
     dscan(ctx, flag, flag, nullptr, n, nullptr, true);
     k_segments<K><<<g, 256, 0, st>>>(ks, vs, flag, n, P, out.coords, out.keys, out.p2v, out.order,

@@ -80,3 +80,29 @@ def test_device_resident_inputs(setup):
     a = render_frame(dev, w, Camera.of(view))
     b = render_frame(pc, w, Camera.of(view))
     assert torch.equal(a.rgb, b.rgb) and torch.equal(a.normal, b.normal)
+
+
+def test_graph_replay_matches_eager(setup):
+    """sfb_frame: eager first call, graph capture on the second, replays after;
+    every replay (with a new camera each time) must equal the eager render."""
+    from paper_2409_16504_b200 import _lib, scenes as S
+    pc, cloud, view, w = setup
+    views = S.ring_views(cloud, 4, 128)
+    cams = [Camera.of(v) for v in views]
+    h, wd = 128, 128
+    out = (torch.empty((h, wd, 3), dtype=torch.float32, device="cuda"),
+           torch.empty((h, wd, 3), dtype=torch.float32, device="cuda"), None,
+           torch.empty((h, wd), dtype=torch.float32, device="cuda"))
+    dev = PointCloud(torch.from_numpy(cloud.positions).cuda(), torch.from_numpy(cloud.colors).cuda())
+    ctx = _lib.context()
+    ctx.lib.sfb_set_graphs(ctx.handle, 0)
+    eager = []
+    for cam in cams:
+        fb = render_frame(dev, w, cam, ("rgb", "normal"))
+        eager.append((fb.rgb.clone(), fb.normal.clone(), fb.transmittance.clone()))
+    ctx.lib.sfb_set_graphs(ctx.handle, 1)
+    for rep in range(2):
+        for cam, (r, n, t) in zip(cams, eager):
+            render_frame(dev, w, cam, ("rgb", "normal"), out=out)
+            torch.cuda.synchronize()
+            assert torch.equal(out[0], r) and torch.equal(out[1], n) and torch.equal(out[3], t)
