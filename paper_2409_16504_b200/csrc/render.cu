@@ -36,7 +36,7 @@ constexpr int kSuper = 8;      // tiles per super-tile edge
 constexpr int kSuperMax = 16;  // super tiles per run at the middle level
 constexpr int kWin = 2048;     // rank window of the merge
 constexpr int kCT = 256;       // compositor threads per CTA
-constexpr int kPre = 16;       // staged points per run
+constexpr int kPre = 8;        // staged points per run
 constexpr int kChunk = 64;     // runs per compositing chunk
 
 // ------------------------------------------------------------ 1. projection
@@ -363,7 +363,7 @@ struct CompParams {
 };
 
 template <int NPIX>
-__global__ void __launch_bounds__(kCT) k_composite(CompParams P) {
+__global__ void __launch_bounds__(kCT, 4) k_composite(CompParams P) {
     constexpr int KMAX = kWin / kCT;
     constexpr uint32_t NONE = 0xffffffffu;
     __shared__ uint32_t bitmap[kWin / 32];
@@ -423,7 +423,7 @@ __global__ void __launch_bounds__(kCT) k_composite(CompParams P) {
     const uint32_t *ids[3] = {P.f_ids, P.s_ids, P.g_ids};
     int64_t cur[3] = {P.f_off[t], P.s_off[st], 0};
     const int64_t end[3] = {P.f_off[t + 1], P.s_off[st + 1], *P.d_G};
-    int ws = kCT;  // rank window grows 256 -> 2048: most tiles saturate in the first
+    int ws = 128;  // rank window grows 128 -> 2048: most tiles saturate in the first
     bool done = false;
     while (!done) {
         uint32_t head[3];
@@ -434,38 +434,33 @@ __global__ void __launch_bounds__(kCT) k_composite(CompParams P) {
         const uint32_t w1 = w0 + (uint32_t)ws;
         for (int i = threadIdx.x; i < kWin / 32; i += kCT) bitmap[i] = 0;
         if (threadIdx.x < 3) s_add[threadIdx.x] = 0;
-        // independent loads first (memory-level parallelism), then the tests
-        uint32_t id[3][KMAX];
-#pragma unroll
-        for (int s = 0; s < 3; ++s)
-#pragma unroll
-            for (int k = 0; k < KMAX; ++k) {
-                int64_t idx = cur[s] + k * kCT + threadIdx.x;
-                id[s][k] = (k * kCT < ws && idx < end[s]) ? ids[s][idx] : NONE;
-            }
-        int4 rc[2][KMAX];
-#pragma unroll
-        for (int s = 1; s < 3; ++s)
-#pragma unroll
-            for (int k = 0; k < KMAX; ++k)
-                if (id[s][k] < w1) rc[s - 1][k] = P.R.rect[id[s][k]];
         __syncthreads();
+        // one 256-rank slice of the window at a time: 3 id loads + 2 rect
+        // loads in flight per thread, few registers (occupancy)
+        for (int k = 0; k * kCT < ws; ++k) {
+            uint32_t id[3];
 #pragma unroll
-        for (int s = 0; s < 3; ++s) {
-            uint32_t cnt = 0;
+            for (int s = 0; s < 3; ++s) {
+                const int64_t idx = cur[s] + k * kCT + threadIdx.x;
+                id[s] = idx < end[s] ? ids[s][idx] : NONE;
+            }
+            int4 rc[2];
 #pragma unroll
-            for (int k = 0; k < KMAX; ++k) {
-                uint32_t r = id[s][k];
-                if (r >= w1) continue;
-                ++cnt;
-                bool cover = true;
-                if (s) {
-                    int4 q = rc[s - 1][k];
+            for (int s = 1; s < 3; ++s)
+                if (id[s] < w1) rc[s - 1] = P.R.rect[id[s]];
+#pragma unroll
+            for (int s = 0; s < 3; ++s) {
+                const uint32_t r = id[s];
+                const bool in = r < w1;
+                bool cover = in;
+                if (s && in) {
+                    const int4 q = rc[s - 1];
                     cover = tx >= q.x && tx <= q.y && ty >= q.z && ty <= q.w;
                 }
                 if (cover) atomicOr(&bitmap[(r - w0) >> 5], 1u << ((r - w0) & 31));
+                const unsigned ball = __ballot_sync(0xffffffffu, in);
+                if ((threadIdx.x & 31) == 0 && ball) atomicAdd(&s_add[s], (uint32_t)__popc(ball));
             }
-            if (cnt) atomicAdd(&s_add[s], cnt);
         }
         __syncthreads();
 #pragma unroll
@@ -555,6 +550,10 @@ __global__ void __launch_bounds__(kCT) k_composite(CompParams P) {
                 if (term && e && (e & 31) == 0 && __syncthreads_and(saturated())) {
                     done = true;
                     break;
+                }
+                if (term && __all_sync(0xffffffffu, saturated())) {
+                    e |= 31;   // my warp is finished: skip to the next block checkpoint
+                    continue;
                 }
 #pragma unroll
                 for (int k = 0; k < NPIX; ++k) {
