@@ -151,18 +151,57 @@ static Proj project_inputs(sfb_ctx *ctx, const RenderInputs &in, const FramePara
     return P;
 }
 
-// key = depth bits of kept points (positive doubles order as uint64), ~0 for
-// culled ones so they sort last; warp-aggregated count of the kept points
+// Depth order = stable sort of (float64 depth, point index) over kept points
+// (rasterizer.py:105). Sorting 64-bit depth keys costs 8 radix passes, so the
+// sort runs on a 32-bit MONOTONE quantisation q(d) = floor((d - zmin) * s)
+// (4 passes); points with equal q keep index order (stable), and a fix-up
+// pass re-sorts each equal-q group by the exact (depth bits, index) key.
+// Equal-q groups are almost always one voxel's points (identical depth,
+// already in index order: O(k) check) or exact ties.
+__device__ __forceinline__ unsigned long long dbits(double d) {
+    return (unsigned long long)__double_as_longlong(d);
+}
+
+__global__ void k_depth_range(const Proj P, const int64_t *__restrict__ d_ng, int64_t ng_fixed,
+                              unsigned long long *__restrict__ mm) {
+    const int64_t ng = d_ng ? *d_ng : ng_fixed;
+    unsigned long long lo = ~0ull, hi = 0ull;
+    SFB_FOR(g, ng)
+    if (P.keep[g]) {
+        const unsigned long long b = dbits(P.depth[g]);   // depth > z_near > 0
+        lo = b < lo ? b : lo;
+        hi = b > hi ? b : hi;
+    }
+    for (int o = 16; o; o >>= 1) {
+        const unsigned long long l2 = __shfl_xor_sync(0xffffffffu, lo, o);
+        const unsigned long long h2 = __shfl_xor_sync(0xffffffffu, hi, o);
+        lo = l2 < lo ? l2 : lo;
+        hi = h2 > hi ? h2 : hi;
+    }
+    if ((threadIdx.x & 31) == 0) {
+        atomicMin(&mm[0], lo);
+        atomicMax(&mm[1], hi);
+    }
+}
+
+__global__ void k_init_range(unsigned long long *mm) {
+    mm[0] = ~0ull;
+    mm[1] = 0ull;
+}
+
 __global__ void k_depth_keys(int64_t n, const int32_t *__restrict__ p2g, const Proj P,
-                             unsigned long long *__restrict__ keys, uint32_t *__restrict__ vals,
-                             int64_t *__restrict__ d_kept) {
+                             const unsigned long long *__restrict__ mm, uint32_t *__restrict__ keys,
+                             uint32_t *__restrict__ vals, int64_t *__restrict__ d_kept) {
+    const double zmin = __longlong_as_double((long long)mm[0]);
+    const double zmax = __longlong_as_double((long long)mm[1]);
+    const double scale = zmax > zmin ? 4294967294.0 / (zmax - zmin) : 0.0;
     SFB_FOR(i, ((n + 31) & ~int64_t(31))) {
         bool k = false;
-        unsigned long long key = ~0ull;
         if (i < n) {
             const int64_t g = p2g ? p2g[i] : i;
             k = P.keep[g];
-            if (k) key = (unsigned long long)__double_as_longlong(P.depth[g]);
+            uint32_t key = 0xffffffffu;
+            if (k) key = (uint32_t)fmin(floor((P.depth[g] - zmin) * scale), 4294967294.0);
             keys[i] = key;
             vals[i] = (uint32_t)i;
         }
@@ -171,17 +210,125 @@ __global__ void k_depth_keys(int64_t n, const int32_t *__restrict__ p2g, const P
     }
 }
 
+// exact (depth bits, index) order inside every group of equal quantised keys:
+// (1) full depth bits per rank, (2) flag ranks that are out of order w.r.t.
+// their predecessor in the same group and mark that group's head (rare),
+// (3) heads of marked groups insertion-sort their group
+__global__ void k_depth_full(const uint32_t *__restrict__ src, const int32_t *__restrict__ p2g,
+                             const Proj P, const int64_t *__restrict__ d_kept,
+                             unsigned long long *__restrict__ full) {
+    const int64_t K = *d_kept;
+    SFB_FOR(j, K) {
+        const uint32_t i = src[j];
+        full[j] = dbits(P.depth[p2g ? p2g[i] : (int64_t)i]);
+    }
+}
+
+__global__ void k_depth_mark(const uint32_t *__restrict__ keys,
+                             const unsigned long long *__restrict__ full,
+                             const int64_t *__restrict__ d_kept, uint8_t *__restrict__ need,
+                             uint32_t *__restrict__ heads, int64_t *__restrict__ n_heads) {
+    const int64_t K = *d_kept;
+    SFB_FOR(j, K) {
+        if (j == 0 || keys[j] != keys[j - 1] || full[j] >= full[j - 1]) continue;
+        // first element of the group: keys are sorted, so binary search
+        int64_t lo = 0, hi = j;
+        const uint32_t kj = keys[j];
+        while (lo < hi) {
+            const int64_t mid = (lo + hi) >> 1;
+            if (keys[mid] < kj) lo = mid + 1;
+            else hi = mid;
+        }
+        if (atomicCAS((unsigned int *)(need + 4 * lo), 0u, 1u) == 0u) {
+            const unsigned long long slot = atomicAdd((unsigned long long *)n_heads, 1ull);
+            heads[slot] = (uint32_t)lo;
+        }
+    }
+}
+
+// one CTA per out-of-order group: rank sort of (depth bits, index) in smem
+constexpr int kFixMax = 2048;
+__global__ void __launch_bounds__(256)
+k_depth_fixup(const uint32_t *__restrict__ keys, uint32_t *__restrict__ src,
+              unsigned long long *__restrict__ full, const int64_t *__restrict__ d_kept,
+              const uint32_t *__restrict__ heads, const int64_t *__restrict__ n_heads) {
+    __shared__ unsigned long long s_full[kFixMax];
+    __shared__ uint32_t s_src[kFixMax];
+    __shared__ int64_t s_end;
+    const int64_t K = *d_kept, H = *n_heads;
+    for (int64_t gi = blockIdx.x; gi < H; gi += gridDim.x) {
+        const int64_t h = heads[gi];
+        if (threadIdx.x == 0) {
+            int64_t lo = h, hi = K;   // first index with key > keys[h]
+            const uint32_t kh = keys[h];
+            while (lo < hi) {
+                const int64_t mid = (lo + hi) >> 1;
+                if (keys[mid] <= kh) lo = mid + 1;
+                else hi = mid;
+            }
+            s_end = lo;
+        }
+        __syncthreads();
+        const int64_t e = s_end, cnt = e - h;
+        if (cnt <= kFixMax) {
+            for (int64_t i = threadIdx.x; i < cnt; i += blockDim.x) {
+                s_full[i] = full[h + i];
+                s_src[i] = src[h + i];
+            }
+            __syncthreads();
+            for (int64_t i = threadIdx.x; i < cnt; i += blockDim.x) {
+                const unsigned long long d = s_full[i];
+                const uint32_t x = s_src[i];
+                int64_t r = 0;
+                for (int64_t k = 0; k < cnt; ++k) {
+                    const unsigned long long dk = s_full[k];
+                    r += (dk < d) || (dk == d && s_src[k] < x);
+                }
+                src[h + r] = x;
+                full[h + r] = d;
+            }
+        } else if (threadIdx.x == 0) {   // pathological huge group: serial insertion sort
+            for (int64_t a = h + 1; a < e; ++a) {
+                const uint32_t ia = src[a];
+                const unsigned long long da = full[a];
+                int64_t b = a - 1;
+                while (b >= h && (full[b] > da || (full[b] == da && src[b] > ia))) {
+                    src[b + 1] = src[b];
+                    full[b + 1] = full[b];
+                    --b;
+                }
+                src[b + 1] = ia;
+                full[b + 1] = da;
+            }
+        }
+        __syncthreads();
+    }
+}
+
 // returns the rank -> point array (first *d_kept entries valid)
 static uint32_t *depth_order(sfb_ctx *ctx, const RenderInputs &in, const Proj &P, DevCounts *C) {
     const int64_t n = in.n_points;
-    unsigned long long *k0 = ctx->arena.alloc<unsigned long long>(n), *k1 = ctx->arena.alloc<unsigned long long>(n);
+    uint32_t *k0 = ctx->arena.alloc<uint32_t>(n), *k1 = ctx->arena.alloc<uint32_t>(n);
     uint32_t *v0 = ctx->arena.alloc<uint32_t>(n), *v1 = ctx->arena.alloc<uint32_t>(n);
-    k_depth_keys<<<dgrid(n, 256), 256, 0, ctx->stream>>>(n, in.point_to_geom, P, k0, v0, &C->kept);
+    auto *mm = ctx->arena.alloc<unsigned long long>(2);
+    k_init_range<<<1, 1, 0, ctx->stream>>>(mm);
+    k_depth_range<<<dgrid(ctx->grid_bound(in.n_geom, in.d_n_geom ? ctx->hint_m[0] : 0), 256), 256, 0,
+                    ctx->stream>>>(P, in.d_n_geom, in.n_geom, mm);
+    k_depth_keys<<<dgrid(n, 256), 256, 0, ctx->stream>>>(n, in.point_to_geom, P, mm, k0, v0, &C->kept);
     SFB_CHECK_LAUNCH();
     size_t tb = 0;
-    cub::DeviceRadixSort::SortPairs(nullptr, tb, k0, k1, v0, v1, (int)n, 0, 64, ctx->stream);
+    cub::DeviceRadixSort::SortPairs(nullptr, tb, k0, k1, v0, v1, (int)n, 0, 32, ctx->stream);
     void *tmp = ctx->arena.alloc_bytes(tb);
-    SFB_CUDA(cub::DeviceRadixSort::SortPairs(tmp, tb, k0, k1, v0, v1, (int)n, 0, 64, ctx->stream));
+    SFB_CUDA(cub::DeviceRadixSort::SortPairs(tmp, tb, k0, k1, v0, v1, (int)n, 0, 32, ctx->stream));
+    auto *full = ctx->arena.alloc<unsigned long long>(n);
+    uint8_t *need = ctx->arena.alloc<uint8_t>(4 * n);
+    uint32_t *heads = ctx->arena.alloc<uint32_t>(n);
+    SFB_CUDA(cudaMemsetAsync(need, 0, 4 * n, ctx->stream));
+    const unsigned g = dgrid(n, 256);
+    k_depth_full<<<g, 256, 0, ctx->stream>>>(v1, in.point_to_geom, P, &C->kept, full);
+    k_depth_mark<<<g, 256, 0, ctx->stream>>>(k1, full, &C->kept, need, heads, &C->scratch[2]);
+    k_depth_fixup<<<2 * 148, 256, 0, ctx->stream>>>(k1, v1, full, &C->kept, heads, &C->scratch[2]);
+    SFB_CHECK_LAUNCH();
     return v1;
 }
 
