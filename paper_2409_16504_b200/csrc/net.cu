@@ -316,6 +316,48 @@ __global__ void k_head_mlp(const float *__restrict__ f, int ld, const int64_t *_
     }
 }
 
+// thread-per-row head for the default widths: the row's features live in
+// registers, weights are broadcast from shared memory (every lane reads the
+// same W element in the same step), hidden units are consumed as produced
+template <int CIN, int HID>
+__global__ void __launch_bounds__(128)
+k_head_row(const float *__restrict__ f, int ld, const int64_t *__restrict__ d_m,
+           const float *__restrict__ w1, const float *__restrict__ b1, const float *__restrict__ w2,
+           const float *__restrict__ b2, float *__restrict__ raw) {
+    __shared__ float W1[CIN * HID], B1[HID], W2[HID * 14], B2[14];
+    for (int i = threadIdx.x; i < CIN * HID; i += blockDim.x) W1[i] = w1[i];
+    for (int i = threadIdx.x; i < HID * 14; i += blockDim.x) W2[i] = w2[i];
+    for (int i = threadIdx.x; i < HID; i += blockDim.x) B1[i] = b1[i];
+    if (threadIdx.x < 14) B2[threadIdx.x] = b2[threadIdx.x];
+    __syncthreads();
+    const int64_t m = *d_m;
+    SFB_FOR(row, m) {
+        float x[CIN];
+#pragma unroll
+        for (int c = 0; c < CIN; c += 4) {
+            const float4 v = *reinterpret_cast<const float4 *>(f + row * ld + c);
+            x[c] = v.x;
+            x[c + 1] = v.y;
+            x[c + 2] = v.z;
+            x[c + 3] = v.w;
+        }
+        float o[14];
+#pragma unroll
+        for (int k = 0; k < 14; ++k) o[k] = 0.f;
+#pragma unroll 4
+        for (int j = 0; j < HID; ++j) {
+            float h = 0.f;
+#pragma unroll
+            for (int c = 0; c < CIN; ++c) h = fmaf(x[c], W1[c * HID + j], h);
+            h = fmaxf(h + B1[j], 0.f);
+#pragma unroll
+            for (int k = 0; k < 14; ++k) o[k] = fmaf(h, W2[j * 14 + k], o[k]);
+        }
+#pragma unroll
+        for (int k = 0; k < 14; ++k) raw[row * 14 + k] = o[k] + B2[k];
+    }
+}
+
 // ------------------------------------------------------------ activations
 __device__ __forceinline__ double logaddexp0(double x) {
     // numpy npy_logaddexp(0, x): larger + log1p(exp(-|difference|))
@@ -482,6 +524,12 @@ void unet_run(sfb_ctx *ctx, const int32_t *coords0, const double *feats9, int64_
         attr = true;
     }
     SFB_REQUIRE(smem <= 200 * 1024, "head MLP too wide");
+    if (h1.cin == 32 && h1.cout == 64 && width[0] % 4 == 0) {
+        k_head_row<32, 64><<<dgrid(mg[0], 128, 4), 128, 0, st>>>(cat[0], width[0], &C->m[0], h1.w,
+                                                                 h1.b, h2.w, h2.b, raw);
+        SFB_CHECK_LAUNCH();
+        return;
+    }
     k_head_mlp<<<dgrid(mg[0], kHeadRows, 4), 128, smem, st>>>(cat[0], width[0], &C->m[0], h1.cin,
                                                            h1.cout, h1.w, h1.b, h2.w, h2.b, raw);
     SFB_CHECK_LAUNCH();
