@@ -157,13 +157,16 @@ class Context:
                     voxels=list(s.voxels))
 
 
-def context(device=None) -> Context:
+def context(device=None, lane: int = 0) -> Context:
+    """Library context of (device, lane). Each lane owns its own scratch arena
+    and frame graphs, so frames issued on different CUDA streams through
+    different lanes run concurrently on one GPU."""
     import torch
     dev = torch.cuda.current_device() if device is None else int(device)
     with _lock:
-        ctx = _contexts.get(dev)
+        ctx = _contexts.get((dev, lane))
         if ctx is None:
-            ctx = _contexts[dev] = Context(dev)
+            ctx = _contexts[(dev, lane)] = Context(dev)
     return ctx
 
 

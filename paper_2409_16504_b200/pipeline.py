@@ -22,12 +22,15 @@ from .voxelgrid import device_bbox, lattice_scale, stage_cloud
 
 def render_frame(cloud: PointCloud, weights: NetworkWeights, cam: Camera,
                  planes=("rgb", "normal"), background=(0.0, 0.0, 0.0),
-                 options: RenderOptions = None, out=None) -> FrameBuffer:
-    ctx = ensure_loaded(weights)
+                 options: RenderOptions = None, out=None, lane: int = 0) -> FrameBuffer:
+    """Cloud -> P2ENet -> planes. ``lane`` selects an independent library
+    context (own arena and CUDA graphs): issue frames from different lanes on
+    different torch streams and they overlap on the GPU."""
+    ctx = ensure_loaded(weights, lane)
     options = options or RenderOptions()
     pos, col = stage_cloud(cloud)
     n = int(pos.shape[0])
-    lo_hi = device_bbox(pos)
+    lo_hi = device_bbox(pos, lane)
     s = lattice_scale(n, lo_hi)
     bg = np.ascontiguousarray(np.asarray(background, dtype=np.float64).reshape(3))
     rgb, nrm, dep, trans = out if out is not None else _alloc_planes(cam, planes, pos.device)
@@ -44,6 +47,6 @@ def render_frame(cloud: PointCloud, weights: NetworkWeights, cam: Camera,
     return FrameBuffer(int(cam.width), int(cam.height), rgb, trans, bg, nrm, dep)
 
 
-def stats() -> dict:
+def stats(lane: int = 0) -> dict:
     """Sizes of the last call (kept splats, runs, pyramid entries, voxels per level)."""
-    return _lib.context().stats()
+    return _lib.context(lane=lane).stats()

@@ -32,9 +32,9 @@ def set_mode(mode: str) -> None:
         raise ValueError(f"cannot select network mode {mode!r}")
 
 
-def ensure_loaded(weights: NetworkWeights) -> _lib.Context:
+def ensure_loaded(weights: NetworkWeights, lane: int = 0) -> _lib.Context:
     """Upload a network once per context (re-upload when a different object is passed)."""
-    ctx = _lib.context()
+    ctx = _lib.context(lane=lane)
     if ctx.net_token is not weights:
         blob = weights_to_bytes(weights)
         buf = np.frombuffer(blob, dtype=np.uint8)

@@ -104,14 +104,14 @@ class VoxelizedCloud:
         return (g.coords.to(torch.float64) + 0.5 + g.feats[:, 6:9]) * g.scale_to_world
 
 
-def device_bbox(positions: torch.Tensor) -> np.ndarray:
+def device_bbox(positions: torch.Tensor, lane: int = 0) -> np.ndarray:
     """(lo xyz, hi xyz) of device positions via one reduction + 48-byte read-back."""
     n = int(positions.shape[0])
     if n == 0:
         raise EmptyCloudError("empty cloud has no bbox")
     out = np.zeros(6, dtype=np.float64)
-    _lib.context().call("sfb_bbox", _lib.ptr(positions), n,
-                        out.ctypes.data_as(_lib.P))
+    _lib.context(lane=lane).call("sfb_bbox", _lib.ptr(positions), n,
+                                 out.ctypes.data_as(_lib.P))
     return out
 
 
