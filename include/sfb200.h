@@ -84,6 +84,10 @@ int sfb_set_timing(sfb_ctx *ctx, int on);
 /* CUDA-graph replay of sfb_frame (default on): the first call of a shape runs
  * eagerly, the second captures, later calls update parameters and replay. */
 int sfb_set_graphs(sfb_ctx *ctx, int on);
+/* Diagnostics: when set (device buffer of 4 int64 per tile, zeroed by the
+ * caller) the compositor accumulates windows, list entries and alpha
+ * evaluations per tile. NULL disables. */
+int sfb_set_debug_counters(sfb_ctx *ctx, int64_t *dev_counters);
 int sfb_stage_times(sfb_ctx *ctx, int32_t *stage_ids, float *ms, int32_t cap, int32_t *n_out);
 
 /* ---- voxelization (voxelgrid.py:125-168, voxelize_adaptive) ------------- */

@@ -56,6 +56,7 @@ SIGNATURES = {
     "sfb_version": [],
     "sfb_set_timing": [P, ctypes.c_int],
     "sfb_set_graphs": [P, ctypes.c_int],
+    "sfb_set_debug_counters": [P, P],
     "sfb_stage_times": [P, P, P, I32, ctypes.POINTER(I32)],
     "sfb_bbox": [P, P, I64, P],
     "sfb_voxelize": [P, P, P, I64, D, P, P, P, P, P, P, P, ctypes.POINTER(I64)],

@@ -226,6 +226,12 @@ int sfb_set_timing(sfb_ctx *ctx, int on) {
     return SFB_OK;
 }
 
+int sfb_set_debug_counters(sfb_ctx *ctx, int64_t *dev_counters) {
+    if (!ctx) return SFB_ERR_ARG;
+    ctx->debug_counters = dev_counters;
+    return SFB_OK;
+}
+
 int sfb_set_graphs(sfb_ctx *ctx, int on) {
     if (!ctx) return SFB_ERR_ARG;
     ctx->use_graphs = on != 0;

@@ -128,6 +128,7 @@ struct sfb_ctx {
     cudaEvent_t fork_event = nullptr;
     std::vector<sfb_frame_graph *> graphs;
     int64_t graph_nodes = 0;
+    int64_t *debug_counters = nullptr;   // compositor per-tile counters (diagnostics)
     sfb::DevCounts *last_counts = nullptr;   // device counts of the last call
     // launch-size hints (host copies of the counts of the last eager frame):
     // every kernel loops over its device count, so hints only size grids

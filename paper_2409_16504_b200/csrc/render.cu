@@ -385,6 +385,9 @@ __global__ void k_run_heads(const uint32_t *__restrict__ src, const int64_t *__r
 
 struct Runs {
     double *mx, *my, *rad, *ia, *ib, *ic, *op;
+    double *pcol, *pnrm;  // attributes of each run's first kPre points [r][q][3]
+    double *dep;          // the run's camera depth (constant over the run)
+    uint8_t *uni;         // 1 when every point of the run has the same normal
     int32_t *start, *count;
     int4 *rect;
     uint8_t *level;  // 0 fine, 1 super, 2 global, 3 dead
@@ -479,6 +482,41 @@ __global__ void k_emit(Runs R, const int32_t *__restrict__ fpos, const int32_t *
     }
 }
 
+// once per frame: the first kPre points' colour / normal of every run, laid
+// out contiguously so each tile stages a run with straight loads; plus the
+// run's depth and whether its normal is uniform
+__global__ void k_stage_runs(Runs R, const uint32_t *__restrict__ src, const int32_t *__restrict__ p2g,
+                             const double *__restrict__ colors, const double *__restrict__ normals,
+                             const double *__restrict__ gdepth, int want_rgb, int want_n) {
+    const int64_t nr = *R.d_R;
+    SFB_FOR(idx, nr * kPre) {
+        const int64_t r = idx / kPre;
+        const int q = (int)(idx % kPre);
+        if (q == 0) {
+            const uint32_t i0 = src[R.start[r]];
+            const int64_t g0 = p2g ? p2g[i0] : (int64_t)i0;
+            R.dep[r] = gdepth[g0];
+            uint8_t u = 1;
+            if (!p2g && want_n)   // generic splats: compare every point's normal
+                for (int32_t j = R.start[r] + 1; j < R.start[r] + R.count[r] && u; ++j) {
+                    const uint32_t i = src[j];
+                    u = normals[3 * (size_t)i] == normals[3 * (size_t)i0] &&
+                        normals[3 * (size_t)i + 1] == normals[3 * (size_t)i0 + 1] &&
+                        normals[3 * (size_t)i + 2] == normals[3 * (size_t)i0 + 2];
+                }
+            R.uni[r] = u;
+        }
+        if (q >= R.count[r]) continue;
+        const uint32_t i = src[R.start[r] + q];
+        if (want_rgb)
+            for (int c = 0; c < 3; ++c) R.pcol[idx * 3 + c] = colors[3 * (size_t)i + c];
+        if (want_n) {
+            const int64_t g = p2g ? p2g[i] : (int64_t)i;
+            for (int c = 0; c < 3; ++c) R.pnrm[idx * 3 + c] = normals[3 * g + c];
+        }
+    }
+}
+
 __global__ void k_histogram(const uint32_t *__restrict__ keys, const int64_t *__restrict__ d_n,
                             int32_t *__restrict__ cnt) {
     const int64_t n = *d_n;
@@ -507,6 +545,7 @@ struct CompParams {
     const double *colors, *normals, *gdepth;
     // outputs
     float *rgb, *normal, *depth, *trans;
+    int64_t *dbg;   // optional per-tile counters: windows, list entries, alpha evals, point blends
 };
 
 template <int NPIX>
@@ -522,6 +561,8 @@ __global__ void __launch_bounds__(kCT, 4) k_composite(CompParams P) {
         r_ic[kChunk], r_op[kChunk];
     __shared__ int32_t r_x0[kChunk], r_x1[kChunk], r_y0[kChunk], r_y1[kChunk], r_start[kChunk],
         r_count[kChunk];
+    __shared__ double r_dep[kChunk];
+    __shared__ uint8_t r_uni[kChunk];
     // attributes of each run's first kPre points, staged so the blend loop
     // does not chase src[] -> colours[] through global memory per pixel
     extern __shared__ double dyn_smem[];
@@ -566,6 +607,9 @@ __global__ void __launch_bounds__(kCT, 4) k_composite(CompParams P) {
     const double *__restrict__ Ria = P.R.ia, *__restrict__ Rib = P.R.ib, *__restrict__ Ric = P.R.ic;
     const double *__restrict__ Rop = P.R.op;
     const int32_t *__restrict__ Rstart = P.R.start, *__restrict__ Rcount = P.R.count;
+    const double *__restrict__ pcol = P.R.pcol, *__restrict__ pnrm = P.R.pnrm;
+    const double *__restrict__ Rdep = P.R.dep;
+    const uint8_t *__restrict__ Runi = P.R.uni;
     const double alpha_max = P.alpha_max;
     const uint32_t *ids[3] = {P.f_ids, P.s_ids, P.g_ids};
     int64_t cur[3] = {P.f_off[t], P.s_off[st], 0};
@@ -639,8 +683,11 @@ __global__ void __launch_bounds__(kCT, 4) k_composite(CompParams P) {
         }
         __syncthreads();
         const int nlist = s_nlist;
-        for (int base = 0; base < nlist && !done; base += kChunk) {
-            const int nb = min(kChunk, nlist - base);
+        // chunks grow 8 -> 64 runs: most tiles saturate within the first few
+        // runs, so the first chunk stages (and pays latency for) only 8 records
+        int chunk = 8;
+        for (int base = 0; base < nlist && !done; base += chunk, chunk = min(2 * chunk, kChunk)) {
+            const int nb = min(chunk, nlist - base);
             if (threadIdx.x < nb) {
                 const uint32_t r = list[base + threadIdx.x];
                 const int j = threadIdx.x;
@@ -655,6 +702,8 @@ __global__ void __launch_bounds__(kCT, 4) k_composite(CompParams P) {
                 r_op[j] = Rop[r];
                 r_start[j] = Rstart[r];
                 r_count[j] = Rcount[r];
+                r_dep[j] = Rdep[r];
+                r_uni[j] = Runi[r];
                 // pixel box of forward_kernel (_raster_kernels.py:178-181), clamped to the tile
                 r_x0[j] = (int32_t)fmin(fmax((double)x_lo, ceil(mx - rad)), (double)x_end);
                 r_x1[j] = (int32_t)fmax(fmin((double)(x_end - 1), floor(mx + rad)), (double)(x_lo - 1));
@@ -662,31 +711,25 @@ __global__ void __launch_bounds__(kCT, 4) k_composite(CompParams P) {
                 r_y1[j] = (int32_t)fmax(fmin((double)(y_end - 1), floor(my + rad)), (double)(y_lo - 1));
             }
             __syncthreads();
-            {   // stage the first kPre points of every run: 4 threads per run
+            {   // stage the first kPre points of every run (pre-gathered per frame)
                 const int e = threadIdx.x >> 2, part = threadIdx.x & 3;
                 if (e < nb) {
-                    const int32_t st0 = r_start[e], cnt0 = r_count[e];
-                    uint32_t pi[kPre / 4];
-#pragma unroll
-                    for (int u = 0; u < kPre / 4; ++u) {
-                        const int q = part * (kPre / 4) + u;
-                        pi[u] = q < cnt0 ? src[st0 + q] : 0u;
-                    }
+                    const int64_t r = list[base + e];
+                    const int32_t cnt0 = r_count[e];
 #pragma unroll
                     for (int u = 0; u < kPre / 4; ++u) {
                         const int q = part * (kPre / 4) + u;
                         if (q < cnt0) {
+                            const int64_t o = (r * kPre + q) * 3;
                             if (want_rgb) {
-                                const double *cc = colors + 3 * (size_t)pi[u];
-                                r_col[q][0][e] = cc[0];
-                                r_col[q][1][e] = cc[1];
-                                r_col[q][2][e] = cc[2];
+                                r_col[q][0][e] = pcol[o];
+                                r_col[q][1][e] = pcol[o + 1];
+                                r_col[q][2][e] = pcol[o + 2];
                             }
                             if (want_n) {
-                                const double *nn = normals + 3 * (p2g ? (int64_t)p2g[pi[u]] : (int64_t)pi[u]);
-                                r_nrm[q][0][e] = nn[0];
-                                r_nrm[q][1][e] = nn[1];
-                                r_nrm[q][2][e] = nn[2];
+                                r_nrm[q][0][e] = pnrm[o];
+                                r_nrm[q][1][e] = pnrm[o + 1];
+                                r_nrm[q][2][e] = pnrm[o + 2];
                             }
                         }
                     }
@@ -716,7 +759,14 @@ __global__ void __launch_bounds__(kCT, 4) k_composite(CompParams P) {
                     if (alpha < kCutoff) continue;
                     const double om = 1.0 - alpha;
                     const int32_t b0 = r_start[e], b1 = b0 + r_count[e];
-                    for (int32_t j = b0; j < b1; ++j) {
+                    if (P.dbg) atomicAdd((unsigned long long *)&P.dbg[4 * t + 2], 1ull);
+                    // a run's points share alpha; colours are per point. Normal and
+                    // depth are constant over the run when r_uni[e] is set, so they
+                    // take the run's total weight once instead of once per point
+                    const bool uni = r_uni[e];
+                    double wsum = 0.0;
+                    int32_t j = b0;
+                    for (; j < b1; ++j) {
                         if (term && T[k] < kCutoff) break;
                         const int q = j - b0;
                         const double w = T[k] * alpha;
@@ -726,14 +776,10 @@ __global__ void __launch_bounds__(kCT, 4) k_composite(CompParams P) {
                                 c1[k] = c1[k] + w * r_col[q][1][e];
                                 c2[k] = c2[k] + w * r_col[q][2][e];
                             }
-                            if (want_n) {
+                            if (want_n && !uni) {
                                 n0[k] = n0[k] + w * r_nrm[q][0][e];
                                 n1[k] = n1[k] + w * r_nrm[q][1][e];
                                 n2[k] = n2[k] + w * r_nrm[q][2][e];
-                            }
-                            if (want_d) {
-                                const uint32_t i = src[j];
-                                dd[k] = dd[k] + w * gdepth[p2g ? p2g[i] : (int64_t)i];
                             }
                         } else {
                             const uint32_t i = src[j];
@@ -743,19 +789,23 @@ __global__ void __launch_bounds__(kCT, 4) k_composite(CompParams P) {
                                 c1[k] = c1[k] + w * cc[1];
                                 c2[k] = c2[k] + w * cc[2];
                             }
-                            if (want_n || want_d) {
-                                const int64_t g = p2g ? p2g[i] : (int64_t)i;
-                                if (want_n) {
-                                    const double *nn = normals + 3 * g;
-                                    n0[k] = n0[k] + w * nn[0];
-                                    n1[k] = n1[k] + w * nn[1];
-                                    n2[k] = n2[k] + w * nn[2];
-                                }
-                                if (want_d) dd[k] = dd[k] + w * gdepth[g];
+                            if (want_n && !uni) {
+                                const double *nn = normals + 3 * (p2g ? (int64_t)p2g[i] : (int64_t)i);
+                                n0[k] = n0[k] + w * nn[0];
+                                n1[k] = n1[k] + w * nn[1];
+                                n2[k] = n2[k] + w * nn[2];
                             }
                         }
+                        wsum = wsum + w;
                         T[k] = T[k] * om;
                     }
+                    if (P.dbg) atomicAdd((unsigned long long *)&P.dbg[4 * t + 3], (unsigned long long)(j - b0));
+                    if (want_n && uni) {
+                        n0[k] = n0[k] + wsum * r_nrm[0][0][e];
+                        n1[k] = n1[k] + wsum * r_nrm[0][1][e];
+                        n2[k] = n2[k] + wsum * r_nrm[0][2][e];
+                    }
+                    if (want_d) dd[k] = dd[k] + wsum * r_dep[e];
                 }
             }
             if (done) break;
@@ -763,6 +813,10 @@ __global__ void __launch_bounds__(kCT, 4) k_composite(CompParams P) {
             else __syncthreads();
         }
         ws = min(ws * 2, kWin);
+        if (P.dbg && threadIdx.x == 0) {
+            atomicAdd((unsigned long long *)&P.dbg[4 * t + 0], 1ull);
+            atomicAdd((unsigned long long *)&P.dbg[4 * t + 1], (unsigned long long)nlist);
+        }
     }
     // planes (rasterizer.py:140-149; FrameBuffer clips T to [0,1])
     const double bgc[3] = {P.fp->bg[0], P.fp->bg[1], P.fp->bg[2]};
@@ -820,6 +874,10 @@ void render_run(sfb_ctx *ctx, const RenderInputs &in, const FrameParams *FP, int
     R.op = blk + 6 * nb;
     R.start = ctx->arena.alloc<int32_t>(nb);
     R.count = ctx->arena.alloc<int32_t>(nb);
+    R.pcol = ctx->arena.alloc<double>((size_t)nb * kPre * 3);
+    R.pnrm = ctx->arena.alloc<double>((size_t)nb * kPre * 3);
+    R.dep = ctx->arena.alloc<double>(nb);
+    R.uni = ctx->arena.alloc<uint8_t>(nb);
     R.rect = ctx->arena.alloc<int4>(nb);
     R.level = ctx->arena.alloc<uint8_t>(nb);
     int32_t *cnts = ctx->arena.alloc<int32_t>(3 * (nb + 1));
@@ -852,6 +910,10 @@ void render_run(sfb_ctx *ctx, const RenderInputs &in, const FrameParams *FP, int
         dscan(ctx, R.ng, pos + 2 * (nb + 1), &C->runs1, nb + 1, &C->g, false);
         k_emit<<<dgrid(ctx->grid_bound(n, ctx->hint_runs), 256), 256, 0, st>>>(
             R, pos, pos + (nb + 1), pos + 2 * (nb + 1), ntx, nsx, fkey, fval, skey, sval, glist);
+        SFB_CHECK_LAUNCH();
+        k_stage_runs<<<dgrid(ctx->grid_bound(n, ctx->hint_runs) * kPre, 256), 256, 0, st>>>(
+            R, src, in.point_to_geom, in.colors, in.normals, P.depth,
+            (plane_mask & SFB_PLANE_RGB) ? 1 : 0, (plane_mask & SFB_PLANE_NORMAL) ? 1 : 0);
         SFB_CHECK_LAUNCH();
         // stable sort by tile id keeps each tile's runs in rank order
         const int fbits = bits_for((uint64_t)nt), sbits = bits_for((uint64_t)ns);
@@ -894,6 +956,7 @@ void render_run(sfb_ctx *ctx, const RenderInputs &in, const FrameParams *FP, int
     CP.normal = (plane_mask & SFB_PLANE_NORMAL) ? normal : nullptr;
     CP.depth = (plane_mask & SFB_PLANE_DEPTH) ? depth : nullptr;
     CP.trans = trans;
+    CP.dbg = ctx->debug_counters;
     const size_t dyn = sizeof(double) * 2 * kPre * 3 * kChunk;
     static bool attr = false;
     if (!attr) {
