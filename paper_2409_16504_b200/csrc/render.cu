@@ -517,6 +517,16 @@ __global__ void k_stage_runs(Runs R, const uint32_t *__restrict__ src, const int
     }
 }
 
+// colours in rank order: the compositor then reads a run's points contiguously
+__global__ void k_gather_colors(const uint32_t *__restrict__ src, const double *__restrict__ colors,
+                                const int64_t *__restrict__ d_k, double *__restrict__ scol) {
+    const int64_t K = *d_k;
+    SFB_FOR(idx, 3 * K) {
+        const int64_t j = idx / 3;
+        scol[idx] = colors[3 * (size_t)src[j] + (idx - 3 * j)];
+    }
+}
+
 __global__ void k_histogram(const uint32_t *__restrict__ keys, const int64_t *__restrict__ d_n,
                             int32_t *__restrict__ cnt) {
     const int64_t n = *d_n;
@@ -546,6 +556,7 @@ struct CompParams {
     // outputs
     float *rgb, *normal, *depth, *trans;
     int64_t *dbg;   // optional per-tile counters: windows, list entries, alpha evals, point blends
+    const double *scol;   // colours in rank order (K,3)
 };
 
 template <int NPIX>
@@ -608,6 +619,7 @@ __global__ void __launch_bounds__(kCT, 4) k_composite(CompParams P) {
     const double *__restrict__ Rop = P.R.op;
     const int32_t *__restrict__ Rstart = P.R.start, *__restrict__ Rcount = P.R.count;
     const double *__restrict__ pcol = P.R.pcol, *__restrict__ pnrm = P.R.pnrm;
+    const double *__restrict__ scol = P.scol;
     const double *__restrict__ Rdep = P.R.dep;
     const uint8_t *__restrict__ Runi = P.R.uni;
     const double alpha_max = P.alpha_max;
@@ -782,14 +794,14 @@ __global__ void __launch_bounds__(kCT, 4) k_composite(CompParams P) {
                                 n2[k] = n2[k] + w * r_nrm[q][2][e];
                             }
                         } else {
-                            const uint32_t i = src[j];
-                            if (want_rgb) {
-                                const double *cc = colors + 3 * (size_t)i;
+                            if (want_rgb) {   // colours pre-gathered in rank order
+                                const double *cc = scol + 3 * (size_t)j;
                                 c0[k] = c0[k] + w * cc[0];
                                 c1[k] = c1[k] + w * cc[1];
                                 c2[k] = c2[k] + w * cc[2];
                             }
                             if (want_n && !uni) {
+                                const uint32_t i = src[j];
                                 const double *nn = normals + 3 * (p2g ? (int64_t)p2g[i] : (int64_t)i);
                                 n0[k] = n0[k] + w * nn[0];
                                 n1[k] = n1[k] + w * nn[1];
@@ -878,6 +890,7 @@ void render_run(sfb_ctx *ctx, const RenderInputs &in, const FrameParams *FP, int
     R.pnrm = ctx->arena.alloc<double>((size_t)nb * kPre * 3);
     R.dep = ctx->arena.alloc<double>(nb);
     R.uni = ctx->arena.alloc<uint8_t>(nb);
+    double *scol = ctx->arena.alloc<double>(3 * (size_t)nb);
     R.rect = ctx->arena.alloc<int4>(nb);
     R.level = ctx->arena.alloc<uint8_t>(nb);
     int32_t *cnts = ctx->arena.alloc<int32_t>(3 * (nb + 1));
@@ -911,6 +924,10 @@ void render_run(sfb_ctx *ctx, const RenderInputs &in, const FrameParams *FP, int
         k_emit<<<dgrid(ctx->grid_bound(n, ctx->hint_runs), 256), 256, 0, st>>>(
             R, pos, pos + (nb + 1), pos + 2 * (nb + 1), ntx, nsx, fkey, fval, skey, sval, glist);
         SFB_CHECK_LAUNCH();
+        if (plane_mask & SFB_PLANE_RGB) {
+            k_gather_colors<<<dgrid(3 * n, 256), 256, 0, st>>>(src, in.colors, &C->kept, scol);
+            SFB_CHECK_LAUNCH();
+        }
         k_stage_runs<<<dgrid(ctx->grid_bound(n, ctx->hint_runs) * kPre, 256), 256, 0, st>>>(
             R, src, in.point_to_geom, in.colors, in.normals, P.depth,
             (plane_mask & SFB_PLANE_RGB) ? 1 : 0, (plane_mask & SFB_PLANE_NORMAL) ? 1 : 0);
@@ -957,6 +974,7 @@ void render_run(sfb_ctx *ctx, const RenderInputs &in, const FrameParams *FP, int
     CP.depth = (plane_mask & SFB_PLANE_DEPTH) ? depth : nullptr;
     CP.trans = trans;
     CP.dbg = ctx->debug_counters;
+    CP.scol = scol;
     const size_t dyn = sizeof(double) * 2 * kPre * 3 * kChunk;
     static bool attr = false;
     if (!attr) {
