@@ -46,7 +46,7 @@ UNIT = "frames/s"
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=100)
+    ap.add_argument("--steps", type=int, default=2000)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
     ap.add_argument("--config", choices=("c2", "c1"), default="c2")
@@ -160,13 +160,20 @@ class ClockSampler:
                                       stdout=self.f, stderr=subprocess.DEVNULL)
         except OSError:
             self.p = None
+        self.skip = 0
+
+    def mark(self):
+        """Samples before this call (nvidia-smi start-up, idle clocks) are dropped."""
+        self.f.flush()
+        self.skip = len(Path(self.f.name).read_text().splitlines())
 
     def stop(self):
         if self.p is None:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
         self.p.terminate()
         self.p.wait()
-        rows = [r.split(",") for r in Path(self.f.name).read_text().splitlines() if r.strip()]
+        rows = [r.split(",") for r in Path(self.f.name).read_text().splitlines()[self.skip:]
+                if r.strip()]
         os.unlink(self.f.name)
         sm = [float(r[0]) for r in rows if r[0].strip().replace(".", "").isdigit()]
         mx = [float(r[1]) for r in rows if r[1].strip().replace(".", "").isdigit()]
@@ -285,6 +292,8 @@ def run_ours(args):
     # ---- timed region: throughput, frames overlapped over the lanes
     barrier()
     clocks = ClockSampler(local)
+    time.sleep(0.5)   # nvidia-smi needs a moment before its first sample
+    clocks.mark()
     ms, host_s = run_batch(args.steps, dev_clouds)
     barrier()
     clk = clocks.stop()
@@ -346,10 +355,15 @@ def run_ours(args):
     n = len(cloud)
     px = W * H
     m0 = st["voxels"][0]
-    algo = {   # algorithmic bytes per launch of each stage
+    # the unit is one frame; algorithmic bytes per frame
+    # B_frame = 48*N (read the fp64 cloud) + 28*W*H (write rgb + normal + T,
+    # f32); the fused path never writes per-point Gaussians, so §8(d)'s 68*N
+    # term is dropped. One k_composite launch processes one frame.
+    b_frame = 48 * n + 28 * px
+    kb = {   # bytes each stage must move, for the per-stage GB/s
         "voxelize": 48 * n + 16 * n + (9 * 8 + 12) * m0,
         "sort": st["kept"] * (4 + 4) * 2,
-        "composite": 28 * px + 24 * n + 80 * st["runs"],
+        "composite": 28 * px + 128 * st["runs"],
         "project": 14 * 8 * m0 + 8 * 8 * m0,
     }
     # The dominant single kernel of the frame is k_composite (the composite
@@ -358,13 +372,17 @@ def run_ours(args):
     kern = "composite"
     roof = None
     if kern in stage_ms:
-        dom_b = algo[kern]
-        ach = dom_b / (stage_ms[kern] / 1e3) / 1e9
+        ach = b_frame / (stage_ms[kern] / 1e3) / 1e9
         roof = {"kernel": "k_composite", "bound": "hbm", "achieved": ach, "peak": hbm,
                 "unit": "GB/s", "frac": ach / hbm, "traffic": traffic("k_composite"),
-                "peak_kind": hbm_kind, "algorithmic_bytes": dom_b, "ms": stage_ms[kern],
-                "stages": {k: {"ms": stage_ms[k], "GB/s": algo[k] / (stage_ms[k] / 1e3) / 1e9}
-                           for k in algo if k in stage_ms}}
+                "peak_kind": hbm_kind, "algorithmic_bytes": b_frame,
+                "algorithmic_bytes_formula": "48*N + 28*W*H per frame (SURVEY.md 8(d), fused path)",
+                "ms": stage_ms[kern],
+                "frame": {"ms": ms_max / args.steps,
+                          "GB/s": b_frame / (ms_max / args.steps / 1e3) / 1e9},
+                "stages": {k: {"ms": stage_ms[k], "bytes": kb[k],
+                               "GB/s": kb[k] / (stage_ms[k] / 1e3) / 1e9}
+                           for k in kb if k in stage_ms}}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
