@@ -36,7 +36,6 @@ constexpr int kSuper = 8;      // tiles per super-tile edge
 constexpr int kSuperMax = 16;  // super tiles per run at the middle level
 constexpr int kWin = 2048;     // rank window of the merge
 constexpr int kCT = 256;       // compositor threads per CTA
-constexpr int kPre = 8;        // staged points per run
 constexpr int kChunk = 64;     // runs per compositing chunk
 
 // ------------------------------------------------------------ 1. projection
@@ -385,7 +384,7 @@ __global__ void k_run_heads(const uint32_t *__restrict__ src, const int64_t *__r
 
 struct Runs {
     double *mx, *my, *rad, *ia, *ib, *ic, *op;
-    double *pcol, *pnrm;  // attributes of each run's first kPre points [r][q][3]
+    double *rn;           // normal of the run's first point [r][3]
     double *dep;          // the run's camera depth (constant over the run)
     uint8_t *uni;         // 1 when every point of the run has the same normal
     int32_t *start, *count;
@@ -482,48 +481,44 @@ __global__ void k_emit(Runs R, const int32_t *__restrict__ fpos, const int32_t *
     }
 }
 
-// once per frame: the first kPre points' colour / normal of every run, laid
-// out contiguously so each tile stages a run with straight loads; plus the
-// run's depth and whether its normal is uniform
+// once per frame, per run: its depth, its first point's normal and whether
+// the normal is uniform over the run (always, for per-voxel geometry)
 __global__ void k_stage_runs(Runs R, const uint32_t *__restrict__ src, const int32_t *__restrict__ p2g,
-                             const double *__restrict__ colors, const double *__restrict__ normals,
-                             const double *__restrict__ gdepth, int want_rgb, int want_n) {
+                             const double *__restrict__ normals, const double *__restrict__ gdepth,
+                             int want_n) {
     const int64_t nr = *R.d_R;
-    SFB_FOR(idx, nr * kPre) {
-        const int64_t r = idx / kPre;
-        const int q = (int)(idx % kPre);
-        if (q == 0) {
-            const uint32_t i0 = src[R.start[r]];
-            const int64_t g0 = p2g ? p2g[i0] : (int64_t)i0;
-            R.dep[r] = gdepth[g0];
-            uint8_t u = 1;
-            if (!p2g && want_n)   // generic splats: compare every point's normal
+    SFB_FOR(r, nr) {
+        const uint32_t i0 = src[R.start[r]];
+        const int64_t g0 = p2g ? p2g[i0] : (int64_t)i0;
+        R.dep[r] = gdepth[g0];
+        uint8_t u = 1;
+        if (want_n) {
+            for (int c = 0; c < 3; ++c) R.rn[3 * r + c] = normals[3 * g0 + c];
+            if (!p2g)   // generic splats: compare every point's normal
                 for (int32_t j = R.start[r] + 1; j < R.start[r] + R.count[r] && u; ++j) {
                     const uint32_t i = src[j];
                     u = normals[3 * (size_t)i] == normals[3 * (size_t)i0] &&
                         normals[3 * (size_t)i + 1] == normals[3 * (size_t)i0 + 1] &&
                         normals[3 * (size_t)i + 2] == normals[3 * (size_t)i0 + 2];
                 }
-            R.uni[r] = u;
         }
-        if (q >= R.count[r]) continue;
-        const uint32_t i = src[R.start[r] + q];
-        if (want_rgb)
-            for (int c = 0; c < 3; ++c) R.pcol[idx * 3 + c] = colors[3 * (size_t)i + c];
-        if (want_n) {
-            const int64_t g = p2g ? p2g[i] : (int64_t)i;
-            for (int c = 0; c < 3; ++c) R.pnrm[idx * 3 + c] = normals[3 * g + c];
-        }
+        R.uni[r] = u;
     }
 }
 
-// colours in rank order: the compositor then reads a run's points contiguously
-__global__ void k_gather_colors(const uint32_t *__restrict__ src, const double *__restrict__ colors,
-                                const int64_t *__restrict__ d_k, double *__restrict__ scol) {
+// per-point attributes in rank order as float4 (one 16-byte load per point in
+// the compositor); normals only for per-point geometry (runs may mix them)
+__global__ void k_gather_attrs(const uint32_t *__restrict__ src, const int32_t *__restrict__ p2g,
+                               const double *__restrict__ colors, const double *__restrict__ normals,
+                               const int64_t *__restrict__ d_k, float4 *__restrict__ scol,
+                               float4 *__restrict__ snrm) {
     const int64_t K = *d_k;
-    SFB_FOR(idx, 3 * K) {
-        const int64_t j = idx / 3;
-        scol[idx] = colors[3 * (size_t)src[j] + (idx - 3 * j)];
+    SFB_FOR(j, K) {
+        const size_t i = src[j];
+        if (scol)
+            scol[j] = make_float4((float)colors[3 * i], (float)colors[3 * i + 1], (float)colors[3 * i + 2], 0.f);
+        if (snrm && !p2g)
+            snrm[j] = make_float4((float)normals[3 * i], (float)normals[3 * i + 1], (float)normals[3 * i + 2], 0.f);
     }
 }
 
@@ -549,19 +544,66 @@ struct CompParams {
     const uint32_t *g_ids;
     const int64_t *d_G;
     Runs R;
-    // points
-    const uint32_t *src;
-    const int32_t *p2g;
-    const double *colors, *normals, *gdepth;
+    // per-point attributes in rank order (float4: x, y, z, pad)
+    const float4 *scol;   // colours (rgb plane)
+    const float4 *snrm;   // normals of per-point geometry (runs with mixed normals)
     // outputs
     float *rgb, *normal, *depth, *trans;
     int64_t *dbg;   // optional per-tile counters: windows, list entries, alpha evals, point blends
-    const double *scol;   // colours in rank order (K,3)
 };
 
+// b^e for e >= 0 by repeated squaring (float64)
+__device__ __forceinline__ double ipow(double b, int e) {
+    double r = 1.0;
+    while (e) {
+        if (e & 1) r = r * b;
+        b = b * b;
+        e >>= 1;
+    }
+    return r;
+}
+
+// sum_{j<m} om^j v_j by Horner from the last point (float32; v in rank order)
+__device__ __forceinline__ float3 horner3(const float4 *__restrict__ v, int m, float om) {
+    float x = 0.f, y = 0.f, z = 0.f;
+    int j = m - 1;
+    for (; j >= 3; j -= 4) {
+        const float4 a = __ldg(v + j), b = __ldg(v + j - 1), c = __ldg(v + j - 2), d = __ldg(v + j - 3);
+        x = fmaf(x, om, a.x);
+        y = fmaf(y, om, a.y);
+        z = fmaf(z, om, a.z);
+        x = fmaf(x, om, b.x);
+        y = fmaf(y, om, b.y);
+        z = fmaf(z, om, b.z);
+        x = fmaf(x, om, c.x);
+        y = fmaf(y, om, c.y);
+        z = fmaf(z, om, c.z);
+        x = fmaf(x, om, d.x);
+        y = fmaf(y, om, d.y);
+        z = fmaf(z, om, d.z);
+    }
+    for (; j >= 0; --j) {
+        const float4 a = __ldg(v + j);
+        x = fmaf(x, om, a.x);
+        y = fmaf(y, om, a.y);
+        z = fmaf(z, om, a.z);
+    }
+    return make_float3(x, y, z);
+}
+
+// One CTA per tile. The rank-ordered fine / super / global lists are merged
+// in rank windows (bitmap + ordered compaction), candidate runs are staged
+// in chunks, and every pixel blends each covering run in closed form: a
+// run's points share alpha, so before point j of the run T = T0 (1-a)^j and
+//   sum_j T_j a c_j = T0 a sum_{j<m} (1-a)^j c_j       (Horner, float32)
+//   sum_j T_j a     = T0 - T_m                         (normal / depth of
+//                                                       uniform runs)
+// where m = points blended before T < 1/255 (forward_kernel's per-point
+// check, _raster_kernels.py:185-187). m = run length unless T crosses the
+// cutoff inside the run; then T is iterated point by point exactly as the
+// reference does. Alpha, T and the thresholds stay float64.
 template <int NPIX>
 __global__ void __launch_bounds__(kCT, 4) k_composite(CompParams P) {
-    constexpr int KMAX = kWin / kCT;
     constexpr uint32_t NONE = 0xffffffffu;
     __shared__ uint32_t bitmap[kWin / 32];
     __shared__ uint32_t list[kWin];
@@ -569,16 +611,10 @@ __global__ void __launch_bounds__(kCT, 4) k_composite(CompParams P) {
     __shared__ uint32_t s_add[3];
     // the current chunk's run records (pixel box precomputed per run)
     __shared__ double r_mx[kChunk], r_my[kChunk], r_rr[kChunk], r_ia[kChunk], r_ib[kChunk],
-        r_ic[kChunk], r_op[kChunk];
+        r_ic[kChunk], r_op[kChunk], r_dep[kChunk], r_rn[3][kChunk];
     __shared__ int32_t r_x0[kChunk], r_x1[kChunk], r_y0[kChunk], r_y1[kChunk], r_start[kChunk],
         r_count[kChunk];
-    __shared__ double r_dep[kChunk];
     __shared__ uint8_t r_uni[kChunk];
-    // attributes of each run's first kPre points, staged so the blend loop
-    // does not chase src[] -> colours[] through global memory per pixel
-    extern __shared__ double dyn_smem[];
-    double (*r_col)[3][kChunk] = reinterpret_cast<double (*)[3][kChunk]>(dyn_smem);
-    double (*r_nrm)[3][kChunk] = reinterpret_cast<double (*)[3][kChunk]>(dyn_smem + kPre * 3 * kChunk);
 
     const int64_t t = blockIdx.x;
     const int64_t tx = t % P.ntx, ty = t / P.ntx;
@@ -610,18 +646,12 @@ __global__ void __launch_bounds__(kCT, 4) k_composite(CompParams P) {
         return mine;
     };
 
-    const uint32_t *__restrict__ src = P.src;
-    const int32_t *__restrict__ p2g = P.p2g;
-    const double *__restrict__ colors = P.colors, *__restrict__ normals = P.normals;
-    const double *__restrict__ gdepth = P.gdepth;
     const double *__restrict__ Rmx = P.R.mx, *__restrict__ Rmy = P.R.my, *__restrict__ Rrad = P.R.rad;
     const double *__restrict__ Ria = P.R.ia, *__restrict__ Rib = P.R.ib, *__restrict__ Ric = P.R.ic;
-    const double *__restrict__ Rop = P.R.op;
+    const double *__restrict__ Rop = P.R.op, *__restrict__ Rdep = P.R.dep, *__restrict__ Rrn = P.R.rn;
     const int32_t *__restrict__ Rstart = P.R.start, *__restrict__ Rcount = P.R.count;
-    const double *__restrict__ pcol = P.R.pcol, *__restrict__ pnrm = P.R.pnrm;
-    const double *__restrict__ scol = P.scol;
-    const double *__restrict__ Rdep = P.R.dep;
     const uint8_t *__restrict__ Runi = P.R.uni;
+    const float4 *__restrict__ scol = P.scol, *__restrict__ snrm = P.snrm;
     const double alpha_max = P.alpha_max;
     const uint32_t *ids[3] = {P.f_ids, P.s_ids, P.g_ids};
     int64_t cur[3] = {P.f_off[t], P.s_off[st], 0};
@@ -716,36 +746,16 @@ __global__ void __launch_bounds__(kCT, 4) k_composite(CompParams P) {
                 r_count[j] = Rcount[r];
                 r_dep[j] = Rdep[r];
                 r_uni[j] = Runi[r];
+                if (want_n) {
+                    r_rn[0][j] = Rrn[3 * (size_t)r];
+                    r_rn[1][j] = Rrn[3 * (size_t)r + 1];
+                    r_rn[2][j] = Rrn[3 * (size_t)r + 2];
+                }
                 // pixel box of forward_kernel (_raster_kernels.py:178-181), clamped to the tile
                 r_x0[j] = (int32_t)fmin(fmax((double)x_lo, ceil(mx - rad)), (double)x_end);
                 r_x1[j] = (int32_t)fmax(fmin((double)(x_end - 1), floor(mx + rad)), (double)(x_lo - 1));
                 r_y0[j] = (int32_t)fmin(fmax((double)y_lo, ceil(my - rad)), (double)y_end);
                 r_y1[j] = (int32_t)fmax(fmin((double)(y_end - 1), floor(my + rad)), (double)(y_lo - 1));
-            }
-            __syncthreads();
-            {   // stage the first kPre points of every run (pre-gathered per frame)
-                const int e = threadIdx.x >> 2, part = threadIdx.x & 3;
-                if (e < nb) {
-                    const int64_t r = list[base + e];
-                    const int32_t cnt0 = r_count[e];
-#pragma unroll
-                    for (int u = 0; u < kPre / 4; ++u) {
-                        const int q = part * (kPre / 4) + u;
-                        if (q < cnt0) {
-                            const int64_t o = (r * kPre + q) * 3;
-                            if (want_rgb) {
-                                r_col[q][0][e] = pcol[o];
-                                r_col[q][1][e] = pcol[o + 1];
-                                r_col[q][2][e] = pcol[o + 2];
-                            }
-                            if (want_n) {
-                                r_nrm[q][0][e] = pnrm[o];
-                                r_nrm[q][1][e] = pnrm[o + 1];
-                                r_nrm[q][2][e] = pnrm[o + 2];
-                            }
-                        }
-                    }
-                }
             }
             __syncthreads();
             for (int e = 0; e < nb; ++e) {
@@ -770,54 +780,54 @@ __global__ void __launch_bounds__(kCT, 4) k_composite(CompParams P) {
                     if (alpha > alpha_max) alpha = alpha_max;
                     if (alpha < kCutoff) continue;
                     const double om = 1.0 - alpha;
-                    const int32_t b0 = r_start[e], b1 = b0 + r_count[e];
-                    if (P.dbg) atomicAdd((unsigned long long *)&P.dbg[4 * t + 2], 1ull);
-                    // a run's points share alpha; colours are per point. Normal and
-                    // depth are constant over the run when r_uni[e] is set, so they
-                    // take the run's total weight once instead of once per point
-                    const bool uni = r_uni[e];
-                    double wsum = 0.0;
-                    int32_t j = b0;
-                    for (; j < b1; ++j) {
-                        if (term && T[k] < kCutoff) break;
-                        const int q = j - b0;
-                        const double w = T[k] * alpha;
-                        if (q < kPre) {
-                            if (want_rgb) {
-                                c0[k] = c0[k] + w * r_col[q][0][e];
-                                c1[k] = c1[k] + w * r_col[q][1][e];
-                                c2[k] = c2[k] + w * r_col[q][2][e];
+                    const int32_t b0 = r_start[e], cnt = r_count[e];
+                    const double T0 = T[k];
+                    int m = cnt;
+                    double Tend;
+                    if (term) {
+                        const double Tl = T0 * ipow(om, cnt - 1);   // T before the last point
+                        if (Tl >= kCutoff * (1.0 + 1e-12)) {
+                            Tend = Tl * om;
+                        } else {   // the run crosses the cutoff: exact per-point iteration
+                            double Tt = T0;
+                            int j = 0;
+                            while (j < cnt && !(Tt < kCutoff)) {
+                                Tt = Tt * om;
+                                ++j;
                             }
-                            if (want_n && !uni) {
-                                n0[k] = n0[k] + w * r_nrm[q][0][e];
-                                n1[k] = n1[k] + w * r_nrm[q][1][e];
-                                n2[k] = n2[k] + w * r_nrm[q][2][e];
-                            }
-                        } else {
-                            if (want_rgb) {   // colours pre-gathered in rank order
-                                const double *cc = scol + 3 * (size_t)j;
-                                c0[k] = c0[k] + w * cc[0];
-                                c1[k] = c1[k] + w * cc[1];
-                                c2[k] = c2[k] + w * cc[2];
-                            }
-                            if (want_n && !uni) {
-                                const uint32_t i = src[j];
-                                const double *nn = normals + 3 * (p2g ? (int64_t)p2g[i] : (int64_t)i);
-                                n0[k] = n0[k] + w * nn[0];
-                                n1[k] = n1[k] + w * nn[1];
-                                n2[k] = n2[k] + w * nn[2];
-                            }
+                            m = j;
+                            Tend = Tt;
                         }
-                        wsum = wsum + w;
-                        T[k] = T[k] * om;
+                    } else {
+                        Tend = T0 * ipow(om, cnt);
                     }
-                    if (P.dbg) atomicAdd((unsigned long long *)&P.dbg[4 * t + 3], (unsigned long long)(j - b0));
-                    if (want_n && uni) {
-                        n0[k] = n0[k] + wsum * r_nrm[0][0][e];
-                        n1[k] = n1[k] + wsum * r_nrm[0][1][e];
-                        n2[k] = n2[k] + wsum * r_nrm[0][2][e];
+                    if (P.dbg) {
+                        atomicAdd((unsigned long long *)&P.dbg[4 * t + 2], 1ull);
+                        atomicAdd((unsigned long long *)&P.dbg[4 * t + 3], (unsigned long long)m);
                     }
-                    if (want_d) dd[k] = dd[k] + wsum * r_dep[e];
+                    const double wa = T0 * alpha;    // weight of the run's first point
+                    const double wsum = T0 - Tend;   // total weight of its m points
+                    const float omf = (float)om;
+                    if (want_rgb) {
+                        const float3 S = horner3(scol + b0, m, omf);
+                        c0[k] = __fma_rn(wa, (double)S.x, c0[k]);
+                        c1[k] = __fma_rn(wa, (double)S.y, c1[k]);
+                        c2[k] = __fma_rn(wa, (double)S.z, c2[k]);
+                    }
+                    if (want_n) {
+                        if (r_uni[e]) {
+                            n0[k] = __fma_rn(wsum, r_rn[0][e], n0[k]);
+                            n1[k] = __fma_rn(wsum, r_rn[1][e], n1[k]);
+                            n2[k] = __fma_rn(wsum, r_rn[2][e], n2[k]);
+                        } else {
+                            const float3 S = horner3(snrm + b0, m, omf);
+                            n0[k] = __fma_rn(wa, (double)S.x, n0[k]);
+                            n1[k] = __fma_rn(wa, (double)S.y, n1[k]);
+                            n2[k] = __fma_rn(wa, (double)S.z, n2[k]);
+                        }
+                    }
+                    if (want_d) dd[k] = __fma_rn(wsum, r_dep[e], dd[k]);
+                    T[k] = Tend;
                 }
             }
             if (done) break;
@@ -886,11 +896,12 @@ void render_run(sfb_ctx *ctx, const RenderInputs &in, const FrameParams *FP, int
     R.op = blk + 6 * nb;
     R.start = ctx->arena.alloc<int32_t>(nb);
     R.count = ctx->arena.alloc<int32_t>(nb);
-    R.pcol = ctx->arena.alloc<double>((size_t)nb * kPre * 3);
-    R.pnrm = ctx->arena.alloc<double>((size_t)nb * kPre * 3);
+    R.rn = ctx->arena.alloc<double>(3 * (size_t)nb);
     R.dep = ctx->arena.alloc<double>(nb);
     R.uni = ctx->arena.alloc<uint8_t>(nb);
-    double *scol = ctx->arena.alloc<double>(3 * (size_t)nb);
+    const bool want_rgb = plane_mask & SFB_PLANE_RGB, want_n = plane_mask & SFB_PLANE_NORMAL;
+    float4 *scol = want_rgb ? ctx->arena.alloc<float4>(nb) : nullptr;
+    float4 *snrm = (want_n && !in.point_to_geom) ? ctx->arena.alloc<float4>(nb) : nullptr;
     R.rect = ctx->arena.alloc<int4>(nb);
     R.level = ctx->arena.alloc<uint8_t>(nb);
     int32_t *cnts = ctx->arena.alloc<int32_t>(3 * (nb + 1));
@@ -924,13 +935,13 @@ void render_run(sfb_ctx *ctx, const RenderInputs &in, const FrameParams *FP, int
         k_emit<<<dgrid(ctx->grid_bound(n, ctx->hint_runs), 256), 256, 0, st>>>(
             R, pos, pos + (nb + 1), pos + 2 * (nb + 1), ntx, nsx, fkey, fval, skey, sval, glist);
         SFB_CHECK_LAUNCH();
-        if (plane_mask & SFB_PLANE_RGB) {
-            k_gather_colors<<<dgrid(3 * n, 256), 256, 0, st>>>(src, in.colors, &C->kept, scol);
+        if (scol || snrm) {
+            k_gather_attrs<<<dgrid(n, 256), 256, 0, st>>>(src, in.point_to_geom, in.colors,
+                                                          in.normals, &C->kept, scol, snrm);
             SFB_CHECK_LAUNCH();
         }
-        k_stage_runs<<<dgrid(ctx->grid_bound(n, ctx->hint_runs) * kPre, 256), 256, 0, st>>>(
-            R, src, in.point_to_geom, in.colors, in.normals, P.depth,
-            (plane_mask & SFB_PLANE_RGB) ? 1 : 0, (plane_mask & SFB_PLANE_NORMAL) ? 1 : 0);
+        k_stage_runs<<<dgrid(ctx->grid_bound(n, ctx->hint_runs), 256), 256, 0, st>>>(
+            R, src, in.point_to_geom, in.normals, P.depth, want_n ? 1 : 0);
         SFB_CHECK_LAUNCH();
         // stable sort by tile id keeps each tile's runs in rank order
         const int fbits = bits_for((uint64_t)nt), sbits = bits_for((uint64_t)ns);
@@ -964,26 +975,15 @@ void render_run(sfb_ctx *ctx, const RenderInputs &in, const FrameParams *FP, int
     CP.g_ids = glist;
     CP.d_G = &C->g;
     CP.R = R;
-    CP.src = src;
-    CP.p2g = in.point_to_geom;
-    CP.colors = in.colors;
-    CP.normals = in.normals;
-    CP.gdepth = P.depth;
+    CP.scol = scol;
+    CP.snrm = snrm;
     CP.rgb = (plane_mask & SFB_PLANE_RGB) ? rgb : nullptr;
     CP.normal = (plane_mask & SFB_PLANE_NORMAL) ? normal : nullptr;
     CP.depth = (plane_mask & SFB_PLANE_DEPTH) ? depth : nullptr;
     CP.trans = trans;
     CP.dbg = ctx->debug_counters;
-    CP.scol = scol;
-    const size_t dyn = sizeof(double) * 2 * kPre * 3 * kChunk;
-    static bool attr = false;
-    if (!attr) {
-        SFB_CUDA(cudaFuncSetAttribute(k_composite<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn));
-        SFB_CUDA(cudaFuncSetAttribute(k_composite<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn));
-        attr = true;
-    }
-    if (TS * TS <= kCT) k_composite<1><<<(unsigned)nt, kCT, dyn, st>>>(CP);
-    else k_composite<4><<<(unsigned)nt, kCT, dyn, st>>>(CP);
+    if (TS * TS <= kCT) k_composite<1><<<(unsigned)nt, kCT, 0, st>>>(CP);
+    else k_composite<4><<<(unsigned)nt, kCT, 0, st>>>(CP);
     SFB_CHECK_LAUNCH();
     ctx->mark(ST_COMPOSITE);
 }

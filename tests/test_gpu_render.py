@@ -194,3 +194,34 @@ def test_determinism_bitwise(c1):
     b = render_planes(sp, cam, ("rgb", "normal"))
     assert torch.equal(a.rgb, b.rgb) and torch.equal(a.normal, b.normal)
     assert torch.equal(a.transmittance, b.transmittance)
+
+
+@pytest.mark.parametrize("terminate", [True, False])
+def test_identical_geometry_runs_vs_oracle(terminate):
+    """Runs of identical splats (one alpha per pixel, colours and normals per
+    point): long runs that blend completely, runs that cross the T cutoff
+    inside the run, and no-termination mode, against the oracle."""
+    rng = np.random.default_rng(5)
+    parts = {k: [] for k in KEYS}
+    for _ in range(60):
+        k = int(rng.integers(1, 150))
+        q = rng.normal(size=4)
+        q /= np.linalg.norm(q)
+        nr = rng.normal(size=(k, 3))
+        nr /= np.linalg.norm(nr, axis=1, keepdims=True)
+        parts["centers"].append(np.tile(rng.normal(size=3) * [0.6, 0.45, 0.3] + [0, 0, 3.0], (k, 1)))
+        parts["scales"].append(np.tile(rng.uniform(0.05, 0.5, 3), (k, 1)))
+        parts["quaternions"].append(np.tile(q, (k, 1)))
+        parts["opacities"].append(np.full(k, rng.choice([rng.uniform(0.004, 0.05),
+                                                          rng.uniform(0.05, 0.99)])))
+        parts["colors"].append(rng.random((k, 3)))
+        parts["normals"].append(nr)
+    d = {k: np.concatenate(v) for k, v in parts.items()}
+    perm = rng.permutation(d["opacities"].shape[0])
+    d = {k: v[perm] for k, v in d.items()}
+    cam = Cam(np.eye(3), np.zeros(3), 60.0, 60.0, 32.0, 24.0, 64, 48)
+    opts = RenderOptions(early_termination=terminate)
+    for mode in ("rgb", "normal", "depth"):
+        fb = render(gpu_splats(d), Camera.of(cam), mode, options=opts)
+        ref = OR.render(d, cam, mode, terminate=terminate)
+        planes_close(fb, ref, (mode,))
