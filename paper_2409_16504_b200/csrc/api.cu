@@ -153,6 +153,8 @@ void enqueue_frame(sfb_ctx *ctx, const double *pos, const double *col, int64_t n
     in.n_geom = n;
     in.d_n_geom = &C->m[0];
     in.point_to_geom = V.vox.p2v;
+    in.geom_offsets = V.vox.offsets;
+    in.geom_order = V.vox.order;
     in.colors = col;
     in.normals = V.n;
     in.n_points = n;

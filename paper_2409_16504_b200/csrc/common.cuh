@@ -328,6 +328,9 @@ struct RenderInputs {
     int64_t n_geom;                 // host bound on geometry rows
     const int64_t *d_n_geom;        // device count of geometry rows (nullptr: n_geom exact)
     const int32_t *point_to_geom;   // nullptr: identity (geometry per point)
+    // CSR of the points of each geometry row in increasing index order
+    // (voxelgrid.py:165-168 source_order/offsets); enables the voxel-level order
+    const int32_t *geom_offsets, *geom_order;
     const double *colors, *normals;
     int64_t n_points;               // exact, host
 };

@@ -125,11 +125,11 @@ constexpr int kRsBlocks = 148;
 constexpr int kRsThreads = 256;
 constexpr int kRsWarps = kRsThreads / 32;
 
-// blocks that take part in a pass: ~kRsItems items each, at most gridDim.x
-constexpr int kRsItems = 2048;
+// blocks that take part in a pass: at least one 256-item sub-tile each, at
+// most kRsBlocks (small sorts spread thin: one sub-tile per block)
 __device__ __forceinline__ int rs_blocks(int64_t n) {
-    int64_t b = (n + kRsItems - 1) / kRsItems;
-    return (int)max((int64_t)1, min(b, (int64_t)gridDim.x));
+    int64_t b = (n + kRsThreads - 1) / kRsThreads;
+    return (int)max((int64_t)1, min(b, (int64_t)kRsBlocks));
 }
 
 template <class K>
@@ -158,8 +158,7 @@ k_rs_scan(int32_t *__restrict__ hist, const int64_t *__restrict__ d_n, int64_t n
     extern __shared__ int32_t sh[];
     __shared__ int32_t s_warp[32];
     const int64_t n = d_n ? *d_n : n_fixed;
-    int64_t b = (n + kRsItems - 1) / kRsItems;
-    const int nb = (int)max((int64_t)1, min(b, (int64_t)148));
+    const int nb = rs_blocks(n);
     const int count = 256 * nb;
     for (int i = threadIdx.x; i < count; i += blockDim.x) sh[i] = hist[i];
     __syncthreads();

@@ -394,6 +394,49 @@ struct Runs {
     const int64_t *d_R;
 };
 
+// geometry of run r from geometry row g: conic, support radius, tile rect
+// and pyramid level (rasterizer.py:112-127)
+__device__ __forceinline__ void run_geometry(Runs &R, int64_t r, int64_t g, const Proj &P,
+                                             const double *__restrict__ opac, double ft, int64_t ntx,
+                                             int64_t nty, double alpha_max) {
+    const double a = P.a[g], b = P.b[g], c = P.c[g];
+    const double op = opac[g];
+    const double det = a * c - b * b;
+    R.mx[r] = P.sx[g];
+    R.my[r] = P.sy[g];
+    R.ia[r] = c / det;
+    R.ib[r] = -b / det;
+    R.ic[r] = a / det;
+    R.op[r] = op;
+    const double rad = support_radius(a, b, c, op);
+    R.rad[r] = rad;
+    const TileRect t = tile_rect(P.sx[g], P.sy[g], rad, ft, ntx, nty);
+    R.rect[r] = make_int4(t.x0, t.x1, t.y0, t.y1);
+    int lvl = 3, nf = 0, ns = 0, ng = 0;
+    const bool live = !(op < kCutoff) && !(alpha_max < kCutoff) && t.x0 <= t.x1 && t.y0 <= t.y1;
+    if (live) {
+        const int64_t cnt = (int64_t)(t.x1 - t.x0 + 1) * (t.y1 - t.y0 + 1);
+        if (cnt <= kFineMax) {
+            lvl = 0;
+            nf = (int)cnt;
+        } else {
+            const int64_t scnt =
+                (int64_t)(t.x1 / kSuper - t.x0 / kSuper + 1) * (t.y1 / kSuper - t.y0 / kSuper + 1);
+            if (scnt <= kSuperMax) {
+                lvl = 1;
+                ns = (int)scnt;
+            } else {
+                lvl = 2;
+                ng = 1;
+            }
+        }
+    }
+    R.level[r] = (uint8_t)lvl;
+    R.nf[r] = nf;
+    R.ns[r] = ns;
+    R.ng[r] = ng;
+}
+
 __global__ void k_run_build(const uint32_t *__restrict__ src, DevCounts *__restrict__ C,
                             const int32_t *__restrict__ incl, const int32_t *__restrict__ p2g, Proj P,
                             const double *__restrict__ opac, double ft, int64_t ntx, int64_t nty,
@@ -411,43 +454,169 @@ __global__ void k_run_build(const uint32_t *__restrict__ src, DevCounts *__restr
         if (!head) continue;
         R.start[r] = (int32_t)j;
         const uint32_t i = src[j];
-        const int64_t g = p2g ? p2g[i] : (int64_t)i;
-        const double a = P.a[g], b = P.b[g], c = P.c[g];
-        const double op = opac[g];
-        const double det = a * c - b * b;
-        R.mx[r] = P.sx[g];
-        R.my[r] = P.sy[g];
-        R.ia[r] = c / det;
-        R.ib[r] = -b / det;
-        R.ic[r] = a / det;
-        R.op[r] = op;
-        const double rad = support_radius(a, b, c, op);
-        R.rad[r] = rad;
-        const TileRect t = tile_rect(P.sx[g], P.sy[g], rad, ft, ntx, nty);
-        R.rect[r] = make_int4(t.x0, t.x1, t.y0, t.y1);
-        int lvl = 3, nf = 0, ns = 0, ng = 0;
-        const bool live = !(op < kCutoff) && !(alpha_max < kCutoff) && t.x0 <= t.x1 && t.y0 <= t.y1;
-        if (live) {
-            const int64_t cnt = (int64_t)(t.x1 - t.x0 + 1) * (t.y1 - t.y0 + 1);
-            if (cnt <= kFineMax) {
-                lvl = 0;
-                nf = (int)cnt;
-            } else {
-                const int64_t scnt =
-                    (int64_t)(t.x1 / kSuper - t.x0 / kSuper + 1) * (t.y1 / kSuper - t.y0 / kSuper + 1);
-                if (scnt <= kSuperMax) {
-                    lvl = 1;
-                    ns = (int)scnt;
+        run_geometry(R, r, p2g ? p2g[i] : (int64_t)i, P, opac, ft, ntx, nty, alpha_max);
+    }
+}
+
+// ------------------------------------------------------------ 2b. voxel-level order
+// Fused frame: every point of a voxel shares the voxel's geometry, hence its
+// depth, so the stable (depth, point index) order of the points is the depth
+// order of the VOXELS with each voxel's points in index order (its CSR list),
+// except inside groups of voxels whose depths are exactly equal, where the
+// points of the group interleave by index (rasterizer.py:105). Sorting the
+// M0 voxels instead of the N points replaces an 800k-key sort by a ~30k one,
+// and runs come out per voxel (one run per voxel outside tie groups).
+__global__ void k_vdepth_keys(const int64_t *__restrict__ d_ng, const Proj P,
+                              const unsigned long long *__restrict__ mm, uint32_t *__restrict__ keys,
+                              uint32_t *__restrict__ vals, int32_t *__restrict__ vpos,
+                              int64_t *__restrict__ d_kept_geom) {
+    const int64_t ng = *d_ng;
+    const double zmin = __longlong_as_double((long long)mm[0]);
+    const double zmax = __longlong_as_double((long long)mm[1]);
+    const double scale = zmax > zmin ? 4294967294.0 / (zmax - zmin) : 0.0;
+    SFB_FOR(g, ((ng + 31) & ~int64_t(31))) {
+        bool k = false;
+        if (g < ng) {
+            k = P.keep[g];
+            keys[g] = k ? (uint32_t)fmin(floor((P.depth[g] - zmin) * scale), 4294967294.0) : 0xffffffffu;
+            vals[g] = (uint32_t)g;
+            vpos[g] = -1;
+        }
+        const unsigned ball = __ballot_sync(0xffffffffu, k);
+        if ((threadIdx.x & 31) == 0 && ball) atomicAdd((unsigned long long *)d_kept_geom, (unsigned long long)__popc(ball));
+    }
+}
+
+// per sorted kept voxel: its point count and its sorted position
+__global__ void k_vcounts(const uint32_t *__restrict__ vs, const int64_t *__restrict__ d_kg,
+                          const int32_t *__restrict__ goff, int32_t *__restrict__ cnt,
+                          int32_t *__restrict__ vpos) {
+    const int64_t KG = *d_kg;
+    SFB_FOR(i, KG) {
+        const uint32_t v = vs[i];
+        cnt[i] = goff[v + 1] - goff[v];
+        vpos[v] = (int32_t)i;
+    }
+}
+
+// [gs, ge) = the group of sorted voxels with depth bits equal to full[i]
+__device__ __forceinline__ bool tie_group(const unsigned long long *__restrict__ full, int64_t i,
+                                          int64_t KG, int64_t &gs, int64_t &ge) {
+    const unsigned long long d = full[i];
+    gs = i;
+    while (gs > 0 && full[gs - 1] == d) --gs;
+    ge = i + 1;
+    while (ge < KG && full[ge] == d) ++ge;
+    return ge - gs > 1;
+}
+
+// number of points of a sorted index list below p
+__device__ __forceinline__ int32_t count_below(const int32_t *__restrict__ lst, int32_t n, int32_t p) {
+    int32_t lo = 0, hi = n;
+    while (lo < hi) {
+        const int32_t mid = (lo + hi) >> 1;
+        if (lst[mid] < p) lo = mid + 1;
+        else hi = mid;
+    }
+    return lo;
+}
+
+// CSR slot -> rank: src[rank] = point, colours gathered in rank order.
+// thead[rank] = 1 where a tie group's merged order switches voxel (its first
+// rank included): the predecessor of p in the group is the largest group
+// point index below p, found with the same per-voxel binary searches.
+__global__ void k_vranks(const int32_t *__restrict__ order, const int32_t *__restrict__ p2g, int64_t n,
+                         const int32_t *__restrict__ goff, const int32_t *__restrict__ vpos,
+                         const int32_t *__restrict__ off, const unsigned long long *__restrict__ full,
+                         const uint32_t *__restrict__ vs, const int64_t *__restrict__ d_kg,
+                         const double *__restrict__ colors, float4 *__restrict__ scol,
+                         uint32_t *__restrict__ src, int32_t *__restrict__ thead) {
+    const int64_t KG = *d_kg;
+    SFB_FOR(s, n) {
+        const int32_t p = order[s];
+        const int32_t v = p2g[p];
+        const int32_t i = vpos[v];
+        if (i < 0) continue;
+        const int32_t w = (int32_t)s - goff[v];
+        int64_t rank = off[i] + w;
+        int64_t gs, ge;
+        int32_t h = 0;
+        if (tie_group(full, i, KG, gs, ge)) {
+            rank = off[gs];
+            int32_t own = w > 0 ? order[s - 1] : -1, other = -1;   // predecessors of p
+            for (int64_t u = gs; u < ge; ++u) {
+                const uint32_t vu = vs[u];
+                if (vu == (uint32_t)v) {
+                    rank += w;
                 } else {
-                    lvl = 2;
-                    ng = 1;
+                    const int32_t *lst = order + goff[vu];
+                    const int32_t cb = count_below(lst, goff[vu + 1] - goff[vu], p);
+                    rank += cb;
+                    if (cb > 0) other = max(other, lst[cb - 1]);
                 }
             }
+            h = other > own || (own < 0 && other < 0);
         }
-        R.level[r] = (uint8_t)lvl;
-        R.nf[r] = nf;
-        R.ns[r] = ns;
-        R.ng[r] = ng;
+        src[rank] = (uint32_t)p;
+        thead[rank] = h;
+        if (scol)
+            scol[rank] = make_float4((float)colors[3 * (size_t)p], (float)colors[3 * (size_t)p + 1],
+                                     (float)colors[3 * (size_t)p + 2], 0.f);
+    }
+}
+
+// Runs per sorted voxel: 1 outside tie groups; the first voxel of a tie
+// group holds the group's block count (inclusive scan of thead over ranks).
+__global__ void k_vblocks(const unsigned long long *__restrict__ full, const int64_t *__restrict__ d_kg,
+                          const int32_t *__restrict__ off, const int32_t *__restrict__ cnt,
+                          const int32_t *__restrict__ hincl, int32_t *__restrict__ nblk) {
+    const int64_t KG = *d_kg;
+    SFB_FOR(i, KG) {
+        int64_t gs, ge;
+        int32_t b = 1;
+        if (tie_group(full, i, KG, gs, ge)) {
+            b = 0;
+            if (gs == i) {
+                const int64_t j0 = off[gs], j1 = off[ge - 1] + cnt[ge - 1];
+                b = hincl[j1 - 1] - (j0 > 0 ? hincl[j0 - 1] : 0);
+            }
+        }
+        nblk[i] = b;
+    }
+}
+
+// Run records. x < KG: one run per non-tie sorted voxel; x < K: a tie-group
+// head rank starts run ro[group] + (heads of the group before it), ending at
+// the next head or the group end.
+__global__ void k_vbuild(const uint32_t *__restrict__ vs, const unsigned long long *__restrict__ full,
+                         DevCounts *__restrict__ C, const int64_t *__restrict__ d_kg,
+                         const int32_t *__restrict__ off, const int32_t *__restrict__ cnt,
+                         const int32_t *__restrict__ ro, const int32_t *__restrict__ vpos,
+                         const int32_t *__restrict__ thead, const int32_t *__restrict__ hincl,
+                         const uint32_t *__restrict__ src, const int32_t *__restrict__ p2g, Proj P,
+                         const double *__restrict__ opac, double ft, int64_t ntx, int64_t nty,
+                         double alpha_max, Runs R) {
+    const int64_t KG = *d_kg, K = C->kept;
+    if (blockIdx.x == 0 && threadIdx.x == 0) C->runs1 = C->runs + 1;
+    SFB_FOR(x, max(KG, K)) {
+        int64_t gs, ge;
+        if (x < KG && !tie_group(full, x, KG, gs, ge)) {
+            const int64_t r = ro[x];
+            R.start[r] = off[x];
+            R.count[r] = off[x] + cnt[x];   // run end; k_emit subtracts the start
+            run_geometry(R, r, vs[x], P, opac, ft, ntx, nty, alpha_max);
+        }
+        if (x < K && thead[x]) {
+            const int32_t g = p2g[src[x]];
+            tie_group(full, vpos[g], KG, gs, ge);
+            const int64_t j0 = off[gs], j1 = off[ge - 1] + cnt[ge - 1];
+            const int64_t r = ro[gs] + (hincl[x] - (j0 > 0 ? hincl[j0 - 1] : 0)) - 1;
+            int64_t e = x + 1;
+            while (e < j1 && !thead[e]) ++e;
+            R.start[r] = (int32_t)x;
+            R.count[r] = (int32_t)e;
+            run_geometry(R, r, g, P, opac, ft, ntx, nty, alpha_max);
+        }
     }
 }
 
@@ -864,6 +1033,49 @@ __global__ void __launch_bounds__(kCT, 4) k_composite(CompParams P) {
 }
 
 // ------------------------------------------------------------ driver
+// voxel-level depth order (see k_vdepth_keys): fills src (rank -> point) and
+// the rank-ordered colours; returns the sorted kept voxels, their exact depth
+// bits, rank offsets and point counts, and the device count of kept voxels
+static void voxel_order(sfb_ctx *ctx, const RenderInputs &in, const Proj &P, DevCounts *C,
+                        uint32_t *src, float4 *scol, uint32_t *&vs, unsigned long long *&full,
+                        int32_t *&off, int32_t *&cnt, int64_t *&d_kg, int32_t *&vpos,
+                        int32_t *thead) {
+    cudaStream_t st = ctx->stream;
+    const int64_t nbg = in.n_geom > 0 ? in.n_geom : 1;
+    const unsigned gv = dgrid(ctx->grid_bound(nbg, ctx->hint_m[0]), 256);
+    uint32_t *k0 = ctx->arena.alloc<uint32_t>(nbg), *k1 = ctx->arena.alloc<uint32_t>(nbg);
+    uint32_t *v0 = ctx->arena.alloc<uint32_t>(nbg), *v1 = ctx->arena.alloc<uint32_t>(nbg);
+    vpos = ctx->arena.alloc<int32_t>(nbg);
+    auto *mm = ctx->arena.alloc<unsigned long long>(2);
+    d_kg = &C->scratch[3];
+    k_init_range<<<1, 1, 0, st>>>(mm);
+    k_depth_range<<<gv, 256, 0, st>>>(P, in.d_n_geom, in.n_geom, mm);
+    k_vdepth_keys<<<gv, 256, 0, st>>>(in.d_n_geom, P, mm, k0, v0, vpos, d_kg);
+    SFB_CHECK_LAUNCH();
+    // stable by voxel id within equal quantised keys; culled voxels (key ~0) last
+    const bool second = dsort_pairs<uint32_t>(ctx, k0, v0, k1, v1, in.d_n_geom, nbg, 32);
+    uint32_t *ks = second ? k1 : k0;
+    vs = second ? v1 : v0;
+    // exact (depth bits, voxel id) order inside equal-quantised-key groups
+    full = ctx->arena.alloc<unsigned long long>(nbg);
+    uint8_t *need = ctx->arena.alloc<uint8_t>(4 * nbg);
+    uint32_t *heads = ctx->arena.alloc<uint32_t>(nbg);
+    SFB_CUDA(cudaMemsetAsync(need, 0, 4 * nbg, st));
+    k_depth_full<<<gv, 256, 0, st>>>(vs, nullptr, P, d_kg, full);
+    k_depth_mark<<<gv, 256, 0, st>>>(ks, full, d_kg, need, heads, &C->scratch[2]);
+    k_depth_fixup<<<2 * 148, 256, 0, st>>>(ks, vs, full, d_kg, heads, &C->scratch[2]);
+    SFB_CHECK_LAUNCH();
+    cnt = ctx->arena.alloc<int32_t>(nbg);
+    off = ctx->arena.alloc<int32_t>(nbg);
+    k_vcounts<<<gv, 256, 0, st>>>(vs, d_kg, in.geom_offsets, cnt, vpos);
+    SFB_CHECK_LAUNCH();
+    dscan(ctx, cnt, off, d_kg, nbg, &C->kept, false);
+    k_vranks<<<dgrid(in.n_points, 256), 256, 0, st>>>(in.geom_order, in.point_to_geom, in.n_points,
+                                                      in.geom_offsets, vpos, off, full, vs, d_kg,
+                                                      in.colors, scol, src, thead);
+    SFB_CHECK_LAUNCH();
+}
+
 // No host synchronisation: every size (kept points, runs, pyramid entries)
 // stays on the device; buffers are sized from host bounds.
 void render_run(sfb_ctx *ctx, const RenderInputs &in, const FrameParams *FP, int64_t width,
@@ -880,7 +1092,24 @@ void render_run(sfb_ctx *ctx, const RenderInputs &in, const FrameParams *FP, int
     Proj P = project_inputs(ctx, in, FP);
     ctx->mark(ST_PROJECT);
     const int64_t nb = n > 0 ? n : 1;
-    uint32_t *src = n > 0 ? depth_order(ctx, in, P, C) : ctx->arena.alloc<uint32_t>(1);
+    const bool want_rgb = plane_mask & SFB_PLANE_RGB, want_n = plane_mask & SFB_PLANE_NORMAL;
+    float4 *scol = want_rgb ? ctx->arena.alloc<float4>(nb) : nullptr;
+    float4 *snrm = (want_n && !in.point_to_geom) ? ctx->arena.alloc<float4>(nb) : nullptr;
+    // voxel-level order (fused frame): sorted kept voxels, their point offsets
+    const bool by_voxel = in.point_to_geom && in.geom_offsets && in.geom_order && n > 0;
+    uint32_t *vs = nullptr;
+    unsigned long long *vfull = nullptr;
+    int32_t *voff = nullptr, *vcnt = nullptr;
+    int64_t *d_kg = nullptr;
+    int32_t *vpos = nullptr, *thead = nullptr;
+    uint32_t *src;
+    if (by_voxel) {
+        src = ctx->arena.alloc<uint32_t>(nb);
+        thead = ctx->arena.alloc<int32_t>(nb);
+        voxel_order(ctx, in, P, C, src, scol, vs, vfull, voff, vcnt, d_kg, vpos, thead);
+    } else {
+        src = n > 0 ? depth_order(ctx, in, P, C) : ctx->arena.alloc<uint32_t>(1);
+    }
     ctx->mark(ST_SORT);
 
     Runs R{};
@@ -899,9 +1128,6 @@ void render_run(sfb_ctx *ctx, const RenderInputs &in, const FrameParams *FP, int
     R.rn = ctx->arena.alloc<double>(3 * (size_t)nb);
     R.dep = ctx->arena.alloc<double>(nb);
     R.uni = ctx->arena.alloc<uint8_t>(nb);
-    const bool want_rgb = plane_mask & SFB_PLANE_RGB, want_n = plane_mask & SFB_PLANE_NORMAL;
-    float4 *scol = want_rgb ? ctx->arena.alloc<float4>(nb) : nullptr;
-    float4 *snrm = (want_n && !in.point_to_geom) ? ctx->arena.alloc<float4>(nb) : nullptr;
     R.rect = ctx->arena.alloc<int4>(nb);
     R.level = ctx->arena.alloc<uint8_t>(nb);
     int32_t *cnts = ctx->arena.alloc<int32_t>(3 * (nb + 1));
@@ -922,20 +1148,34 @@ void render_run(sfb_ctx *ctx, const RenderInputs &in, const FrameParams *FP, int
     SFB_CUDA(cudaMemsetAsync(cnts, 0, sizeof(int32_t) * 3 * (nb + 1), st));
     const uint32_t *f_ids = fval, *s_ids = sval;
     if (n > 0) {
-        const unsigned g = dgrid(n, 256);
-        k_run_heads<<<g, 256, 0, st>>>(src, &C->kept, in.point_to_geom, P, in.opac, head);
-        SFB_CHECK_LAUNCH();
-        dscan(ctx, head, head, &C->kept, n, nullptr, true);
-        k_run_build<<<g, 256, 0, st>>>(src, C, head, in.point_to_geom, P, in.opac, (double)TS, ntx,
-                                       nty, opts.alpha_max, R);
-        SFB_CHECK_LAUNCH();
+        if (by_voxel) {
+            const unsigned gv = dgrid(ctx->grid_bound(in.n_geom, ctx->hint_m[0]), 256);
+            int32_t *hincl = head;   // inclusive count of tie-group run heads per rank
+            dscan(ctx, thead, hincl, &C->kept, n, nullptr, true);
+            int32_t *nblk = ctx->arena.alloc<int32_t>(in.n_geom + 1);   // then run offsets
+            k_vblocks<<<gv, 256, 0, st>>>(vfull, d_kg, voff, vcnt, hincl, nblk);
+            SFB_CHECK_LAUNCH();
+            dscan(ctx, nblk, nblk, d_kg, in.n_geom, &C->runs, false);
+            k_vbuild<<<dgrid(n, 256), 256, 0, st>>>(vs, vfull, C, d_kg, voff, vcnt, nblk, vpos, thead,
+                                                   hincl, src, in.point_to_geom, P, in.opac,
+                                                   (double)TS, ntx, nty, opts.alpha_max, R);
+            SFB_CHECK_LAUNCH();
+        } else {
+            const unsigned g = dgrid(n, 256);
+            k_run_heads<<<g, 256, 0, st>>>(src, &C->kept, in.point_to_geom, P, in.opac, head);
+            SFB_CHECK_LAUNCH();
+            dscan(ctx, head, head, &C->kept, n, nullptr, true);
+            k_run_build<<<g, 256, 0, st>>>(src, C, head, in.point_to_geom, P, in.opac, (double)TS, ntx,
+                                           nty, opts.alpha_max, R);
+            SFB_CHECK_LAUNCH();
+        }
         dscan(ctx, R.nf, pos, &C->runs1, nb + 1, &C->ef, false);
         dscan(ctx, R.ns, pos + (nb + 1), &C->runs1, nb + 1, &C->es, false);
         dscan(ctx, R.ng, pos + 2 * (nb + 1), &C->runs1, nb + 1, &C->g, false);
         k_emit<<<dgrid(ctx->grid_bound(n, ctx->hint_runs), 256), 256, 0, st>>>(
             R, pos, pos + (nb + 1), pos + 2 * (nb + 1), ntx, nsx, fkey, fval, skey, sval, glist);
         SFB_CHECK_LAUNCH();
-        if (scol || snrm) {
+        if ((scol && !by_voxel) || snrm) {
             k_gather_attrs<<<dgrid(n, 256), 256, 0, st>>>(src, in.point_to_geom, in.colors,
                                                           in.normals, &C->kept, scol, snrm);
             SFB_CHECK_LAUNCH();

@@ -12,6 +12,7 @@ from paper_2409_16504_b200.gaussians import Camera
 from paper_2409_16504_b200.pcio import PointCloud
 from paper_2409_16504_b200.pipeline import render_frame, stats
 from paper_2409_16504_b200.rasterizer import render_planes
+from conftest import Cam
 
 pytestmark = pytest.mark.gpu
 TOL = 2e-3
@@ -106,3 +107,44 @@ def test_graph_replay_matches_eager(setup):
             render_frame(dev, w, cam, ("rgb", "normal"), out=out)
             torch.cuda.synchronize()
             assert torch.equal(out[0], r) and torch.equal(out[1], n) and torch.equal(out[3], t)
+
+
+def tie_cloud():
+    """Voxels in exact depth ties: s = 1 exactly (N = bbox volume), two points per
+    voxel at dyadic offsets (exact centroids, zero residuals), a network whose
+    weights are zero (every voxel gets the same head), an axis-aligned camera:
+    each z layer of 256 voxels is ONE tie group whose 512 points interleave by
+    (shuffled) index in the reference order (rasterizer.py:105)."""
+    rng = np.random.default_rng(11)
+    i, j, k, u = np.meshgrid(np.arange(16), np.arange(16), np.arange(4), [0.25, 0.75], indexing="ij")
+    pts = np.stack([i + u, j + 0.5, k + 0.5], -1).reshape(-1, 3)
+    pts = np.concatenate([pts, [[0.0, 0.0, 0.0], [32.03125, 16.0, 4.0]]])
+    pts = pts[rng.permutation(pts.shape[0])]
+    cols = rng.random(pts.shape)
+    plan = netplan.NetworkPlan()
+    layers = [(s, np.zeros(s.weight_shape, np.float32), np.zeros(s.out_channels, np.float32))
+              for s in plan.layer_specs()]
+    head = np.array([0.3, -0.2, 0.1, -0.5, -0.7, -0.3, 0.9, 0.2, -0.1, 0.3, 0.0, 0.2, -0.4, 0.8],
+                    np.float32)
+    layers[-1] = (layers[-1][0], layers[-1][1], head)
+    cam = Cam(np.eye(3), [-8.0, -8.0, 25.0], 60.0, 60.0, 32.0, 32.0, 64, 64)
+    return pts, cols, netplan.NetworkWeights(plan, layers), cam
+
+
+def test_exact_depth_tie_groups():
+    pts, cols, w, cam = tie_cloud()
+    est = ON.estimate(pts, cols, w.as_oracle_layers(), 3)
+    assert est["vox"]["scale_to_world"] == 1.0
+    depth = est["centers"][:, 2]
+    assert len(np.unique(depth)) <= 6   # the layers tie exactly
+    pc = PointCloud(pts, cols)
+    gcam = Camera.of(cam)
+    fused = render_frame(pc, w, gcam, ("rgb", "normal", "depth"))
+    two = render_planes(estimate_neural(pc, w), gcam, ("rgb", "normal", "depth"))
+    for k in ("rgb", "normal", "depth", "transmittance"):
+        assert torch.equal(getattr(fused, k), getattr(two, k)), k
+    got = fused.numpy()
+    for mode in ("rgb", "normal", "depth"):
+        ref = OR.render(est, cam, mode)
+        assert np.abs(got[mode] - ref[mode]).max() <= TOL, mode
+        assert np.abs(got["transmittance"] - ref["transmittance"]).max() <= TOL
