@@ -4,6 +4,8 @@
 // device->host size read after the bbox, which is what makes it capturable
 // as one CUDA graph (the P2ENet level sizes, kept splats, runs and tile
 // entries are all data-dependent).
+#include <algorithm>
+
 #include "common.cuh"
 
 namespace sfb {
@@ -86,14 +88,108 @@ k_scan_apply(const int32_t *__restrict__ in, const int64_t *__restrict__ d_n, in
     }
 }
 
+// Single-pass scan with decoupled look-back: tiles of kLbItems*1024 values
+// are taken in ticket order (so every tile a tile waits on is already
+// running); a tile publishes its aggregate, warp 0 accumulates predecessor
+// aggregates 32 at a time until it meets an inclusive prefix, then publishes
+// its own inclusive prefix. One launch per scan instead of two.
+constexpr int kLbItems = 4;
+constexpr int kLbTile = kLbItems * kScanThreads;
+constexpr unsigned long long kLbAgg = 1ull << 32, kLbInc = 2ull << 32;
+
+__device__ __forceinline__ unsigned long long lb_load(const unsigned long long *p) {
+    unsigned long long v;
+    asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+
+__global__ void __launch_bounds__(kScanThreads)
+k_scan_lb(const int32_t *__restrict__ in, int32_t *__restrict__ out, const int64_t *__restrict__ d_n,
+          int64_t n_fixed, int64_t *__restrict__ total_out, int inclusive,
+          unsigned long long *__restrict__ status, unsigned int *__restrict__ ticket) {
+    __shared__ int32_t s_val[kLbTile];
+    __shared__ int32_t s_warp[32];
+    __shared__ int s_tile;
+    __shared__ int32_t s_excl;
+    const int64_t n = d_n ? *d_n : n_fixed;
+    const int64_t ntiles = (n + kLbTile - 1) / kLbTile;
+    const int lane = threadIdx.x & 31;
+    for (;;) {
+        if (threadIdx.x == 0) s_tile = (int)atomicAdd(ticket, 1u);
+        __syncthreads();
+        const int64_t tile = s_tile;
+        if (tile >= ntiles) break;
+        const int64_t base = tile * kLbTile;
+#pragma unroll
+        for (int k = 0; k < kLbItems; ++k) {
+            const int64_t i = base + k * kScanThreads + threadIdx.x;
+            s_val[k * kScanThreads + threadIdx.x] = i < n ? in[i] : 0;
+        }
+        __syncthreads();
+        int32_t v[kLbItems], sum = 0;
+#pragma unroll
+        for (int k = 0; k < kLbItems; ++k) {
+            v[k] = s_val[threadIdx.x * kLbItems + k];
+            sum += v[k];
+        }
+        int32_t agg;
+        const int32_t ex = block_excl_scan(sum, s_warp, &agg);
+        if (threadIdx.x < 32) {
+            int32_t prefix = 0;
+            if (tile == 0) {
+                if (lane == 0) atomicExch(&status[0], kLbInc | (uint32_t)agg);
+            } else {
+                if (lane == 0) atomicExch(&status[tile], kLbAgg | (uint32_t)agg);
+                int64_t pred = tile - 1;
+                for (;;) {   // window of 32 predecessors, nearest in lane 0
+                    const int64_t q = pred - lane;
+                    unsigned long long st = q >= 0 ? lb_load(&status[q]) : kLbInc;
+                    while (__any_sync(0xffffffffu, (st >> 32) == 0)) {
+                        if ((st >> 32) == 0) st = lb_load(&status[q]);
+                    }
+                    const unsigned inc = __ballot_sync(0xffffffffu, (st >> 32) == 2);
+                    const int stop = inc ? __ffs(inc) - 1 : 31;   // lanes 0..stop count
+                    int32_t val = lane <= stop ? (int32_t)(uint32_t)st : 0;
+                    for (int o = 16; o; o >>= 1) val += __shfl_xor_sync(0xffffffffu, val, o);
+                    prefix += val;
+                    if (inc) break;
+                    pred -= 32;
+                }
+                if (lane == 0) atomicExch(&status[tile], kLbInc | (uint32_t)(prefix + agg));
+            }
+            if (lane == 0) s_excl = prefix;
+        }
+        __syncthreads();
+        int32_t run = s_excl + ex;
+#pragma unroll
+        for (int k = 0; k < kLbItems; ++k) {
+            s_val[threadIdx.x * kLbItems + k] = run + (inclusive ? v[k] : 0);
+            run += v[k];
+        }
+        __syncthreads();
+#pragma unroll
+        for (int k = 0; k < kLbItems; ++k) {
+            const int64_t i = base + k * kScanThreads + threadIdx.x;
+            if (i < n) out[i] = s_val[k * kScanThreads + threadIdx.x];
+        }
+        if (tile == ntiles - 1 && threadIdx.x == 0 && total_out) *total_out = s_excl + agg;
+        __syncthreads();
+    }
+    if (ntiles == 0 && blockIdx.x == 0 && threadIdx.x == 0 && total_out) *total_out = 0;
+}
+
 // exclusive (or inclusive) scan of n int32 (n from device if d_n, else n_fixed);
 // in-place allowed; the grand total is written to *total_out when given.
 void dscan(sfb_ctx *ctx, const int32_t *in, int32_t *out, const int64_t *d_n, int64_t n_fixed,
            int64_t *total_out, bool inclusive) {
-    int32_t *part = ctx->arena.alloc<int32_t>(kScanBlocks);
-    k_scan_partials<<<kScanBlocks, kScanThreads, 0, ctx->stream>>>(in, d_n, n_fixed, part);
-    k_scan_apply<<<kScanBlocks, kScanThreads, 0, ctx->stream>>>(in, d_n, n_fixed, part, out,
-                                                                total_out, inclusive ? 1 : 0);
+    const int64_t tiles = (n_fixed + kLbTile - 1) / kLbTile;
+    const size_t bytes = sizeof(unsigned long long) * (size_t)(tiles + 1);
+    auto *status = static_cast<unsigned long long *>(ctx->arena.alloc_bytes(bytes));
+    SFB_CUDA(cudaMemsetAsync(status, 0, bytes, ctx->stream));
+    auto *ticket = reinterpret_cast<unsigned int *>(status + tiles);
+    const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(tiles, 2 * 148));
+    k_scan_lb<<<grid, kScanThreads, 0, ctx->stream>>>(in, out, d_n, n_fixed, total_out,
+                                                      inclusive ? 1 : 0, status, ticket);
     SFB_CHECK_LAUNCH();
 }
 
@@ -147,37 +243,13 @@ k_rs_upsweep(const K *__restrict__ keys, const int64_t *__restrict__ d_n, int64_
     for (int64_t i = b0 + threadIdx.x; i < b1; i += blockDim.x)
         atomicAdd(&h[(uint32_t)(keys[i] >> shift) & 255u], 1);
     __syncthreads();
-    hist[threadIdx.x * nb + blockIdx.x] = h[threadIdx.x];
+    hist[blockIdx.x * 256 + threadIdx.x] = h[threadIdx.x];
 }
 
-// exclusive scan of the digit-major histogram (256 x active blocks), one CTA:
-// coalesced load into shared memory, per-thread serial segment, one block scan
-constexpr int kRsScanMax = 256 * 148;
-__global__ void __launch_bounds__(1024)
-k_rs_scan(int32_t *__restrict__ hist, const int64_t *__restrict__ d_n, int64_t n_fixed) {
-    extern __shared__ int32_t sh[];
-    __shared__ int32_t s_warp[32];
-    const int64_t n = d_n ? *d_n : n_fixed;
-    const int nb = rs_blocks(n);
-    const int count = 256 * nb;
-    for (int i = threadIdx.x; i < count; i += blockDim.x) sh[i] = hist[i];
-    __syncthreads();
-    const int per = (count + blockDim.x - 1) / blockDim.x;
-    const int b0 = threadIdx.x * per, b1 = min(count, b0 + per);
-    int32_t sum = 0;
-    for (int i = b0; i < b1; ++i) sum += sh[i];
-    int32_t tot;
-    int32_t run = block_excl_scan(sum, s_warp, &tot);
-    for (int i = b0; i < b1; ++i) {
-        const int32_t v = sh[i];
-        sh[i] = run;
-        run += v;
-    }
-    __syncthreads();
-    for (int i = threadIdx.x; i < count; i += blockDim.x) hist[i] = sh[i];
-}
-
-// stable scatter: each block walks its chunk in order, 256 items at a time;
+// stable scatter: each block first forms its digit offsets from the
+// block-major histogram (digit base = exclusive scan over digits of the
+// totals, plus the counts of earlier blocks), then walks its chunk in order,
+// 256 items at a time;
 // rank within a sub-tile = (warps before me with this digit) + (lower lanes
 // of my warp with this digit), found with __match_any_sync
 template <class K, bool HAS_VALS>
@@ -191,7 +263,18 @@ k_rs_downsweep(const K *__restrict__ kin, const uint32_t *__restrict__ vin, K *_
     const int64_t n = d_n ? *d_n : n_fixed;
     const int nb = rs_blocks(n);
     if ((int)blockIdx.x >= nb) return;
-    run[threadIdx.x] = hist[threadIdx.x * nb + blockIdx.x];
+    {
+        int32_t tot = 0, pre = 0;
+#pragma unroll 8
+        for (int b = 0; b < nb; ++b) {
+            const int32_t c = hist[b * 256 + threadIdx.x];
+            tot += c;
+            pre += b < (int)blockIdx.x ? c : 0;
+        }
+        __shared__ int32_t s_warp[32];
+        const int32_t base = block_excl_scan(tot, s_warp, nullptr);
+        run[threadIdx.x] = base + pre;
+    }
     for (int w = 0; w < kRsWarps; ++w) wcnt[w][threadIdx.x] = 0;
     __syncthreads();
     const int64_t ch = chunk_of(n, nb);
@@ -231,17 +314,10 @@ int dsort_pairs(sfb_ctx *ctx, K *k0, uint32_t *v0, K *k1, uint32_t *v1, const in
                 int64_t n_fixed, int bits) {
     const int passes = (bits + 7) / 8;
     int32_t *hist = ctx->arena.alloc<int32_t>(256 * kRsBlocks);
-    static bool attr = false;
-    if (!attr) {
-        SFB_CUDA(cudaFuncSetAttribute(k_rs_scan, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      kRsScanMax * (int)sizeof(int32_t)));
-        attr = true;
-    }
     for (int p = 0; p < passes; ++p) {
         K *ki = (p & 1) ? k1 : k0, *ko = (p & 1) ? k0 : k1;
         uint32_t *vi = (p & 1) ? v1 : v0, *vo = (p & 1) ? v0 : v1;
         k_rs_upsweep<K><<<kRsBlocks, kRsThreads, 0, ctx->stream>>>(ki, d_n, n_fixed, 8 * p, hist);
-        k_rs_scan<<<1, 1024, kRsScanMax * sizeof(int32_t), ctx->stream>>>(hist, d_n, n_fixed);
         if (v0)
             k_rs_downsweep<K, true><<<kRsBlocks, kRsThreads, 0, ctx->stream>>>(ki, vi, ko, vo, d_n,
                                                                                n_fixed, 8 * p, hist);

@@ -100,6 +100,7 @@ __global__ void k_segments(const K *__restrict__ keys, const uint32_t *__restric
         uint32_t i = vals[j];
         order[j] = (int32_t)i;
         p2v[i] = v;
+
         if (j == n - 1) {
             offsets[v + 1] = (int32_t)n;
             C->m[0] = v + 1;
@@ -118,48 +119,41 @@ __global__ void k_segments(const K *__restrict__ keys, const uint32_t *__restric
     }
 }
 
-// One warp per voxel: lanes fetch 32 of the voxel's points at a time (in
-// ascending point index, the CSR order), lane 0 then adds them strictly in
-// that order — bit-identical to np.add.at, with the loads in parallel.
+// Six lanes per voxel, one per summed channel (scaled x, y, z, colour r, g,
+// b; five voxels per warp): each lane walks the voxel's points in ascending
+// point index (the CSR order) and adds its channel strictly in that order —
+// bit-identical to np.add.at — with the point gathers of ~6 M voxels-lanes
+// in flight instead of one serial walk per voxel.
 __global__ void k_voxel_feats(const double *__restrict__ pos, const double *__restrict__ col,
                               const int32_t *__restrict__ order, const int32_t *__restrict__ offsets,
                               const int32_t *__restrict__ coords, const DevCounts *__restrict__ C,
                               const FrameParams *__restrict__ P, double *__restrict__ feats) {
-    const int lane = threadIdx.x & 31;
     const int64_t m = C->m[0];
     const double s = P->s;
-    for (int64_t v = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; v < m;
-         v += ((int64_t)gridDim.x * blockDim.x) >> 5) {
-    const int32_t b = offsets[v], e = offsets[v + 1];
-    double acc[6] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
-    for (int32_t j0 = b; j0 < e; j0 += 32) {
-        const int32_t j = j0 + lane;
-        double val[6] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
-        if (j < e) {
-            const int64_t i = order[j];
-#pragma unroll
-            for (int a = 0; a < 3; ++a) {
-                val[a] = __dmul_rn(pos[3 * i + a], s);
-                val[3 + a] = col[3 * i + a];
-            }
+    const int lane = threadIdx.x & 31;
+    if (lane >= 30) return;
+    const int slot = lane / 6, ch = lane % 6;
+    const double *__restrict__ src = ch < 3 ? pos + ch : col + (ch - 3);
+    const int64_t w0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t v = 5 * w0 + slot; v < m; v += 5 * nw) {
+        const int32_t b = offsets[v], e = offsets[v + 1];
+        double acc = 0.0;
+#pragma unroll 8
+        for (int32_t j = b; j < e; ++j) {
+            const double x = src[3 * (size_t)order[j]];
+            acc = __dadd_rn(acc, ch < 3 ? __dmul_rn(x, s) : x);
         }
-        const int cnt = min(32, e - j0);
-        for (int q = 0; q < cnt; ++q)
-#pragma unroll
-            for (int a = 0; a < 6; ++a) acc[a] = __dadd_rn(acc[a], __shfl_sync(0xffffffffu, val[a], q));
-    }
-    if (lane != 0) continue;
-    double cnt = (double)(e - b);
-    double cen[3] = {__ddiv_rn(acc[0], cnt), __ddiv_rn(acc[1], cnt), __ddiv_rn(acc[2], cnt)};
-    double *f = feats + 9 * v;
-#pragma unroll
-    for (int a = 0; a < 3; ++a) {
-        double res = __dsub_rn(cen[a], __dadd_rn((double)coords[3 * v + a], 0.5));
-        res = fmin(fmax(res, -0.5), 0.5);
-        f[a] = __ddiv_rn(cen[a], s);
-        f[6 + a] = res;
-        f[3 + a] = __ddiv_rn(acc[3 + a], cnt);
-    }
+        const double cnt = (double)(e - b);
+        const double mean = __ddiv_rn(acc, cnt);
+        double *f = feats + 9 * v;
+        if (ch < 3) {
+            double res = __dsub_rn(mean, __dadd_rn((double)coords[3 * v + ch], 0.5));
+            f[ch] = __ddiv_rn(mean, s);
+            f[6 + ch] = fmin(fmax(res, -0.5), 0.5);
+        } else {
+            f[ch] = mean;
+        }
     }
 }
 
@@ -185,8 +179,9 @@ static void voxelize_typed(sfb_ctx *ctx, const double *pos, const double *col, i
     k_segments<K><<<g, 256, 0, st>>>(ks, vs, flag, n, P, out.coords, out.keys, out.p2v, out.order,
                                      out.offsets, C);
     SFB_CHECK_LAUNCH();
-    k_voxel_feats<<<dgrid(32 * n, 256), 256, 0, st>>>(pos, col, out.order, out.offsets, out.coords,
-                                                      C, P, out.feats);
+    const int64_t vwarps = (ctx->grid_bound(n, ctx->hint_m[0]) + 4) / 5;
+    k_voxel_feats<<<dgrid(32 * vwarps, 256), 256, 0, st>>>(pos, col, out.order, out.offsets,
+                                                          out.coords, C, P, out.feats);
     SFB_CHECK_LAUNCH();
 }
 
