@@ -205,11 +205,7 @@ def run_ours(args):
             dist.barrier()
         torch.cuda.synchronize()
 
-    def max_over_ranks(x):
-        t = torch.tensor([x], dtype=torch.float64, device="cuda")
-        if world > 1:
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        return float(t.item())
+    from paper_2409_16504_b200.shard import max_over_ranks, unit_of
 
     cloud, views = workload(args.config)
     cams = [Camera.of(v) for v in views]
@@ -233,8 +229,8 @@ def run_ours(args):
     outs = [[planes_buf() for _ in range(copies)] for _ in range(lanes)]
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")   # 256 MB > 126 MB L2
 
-    def view_of(i):
-        return cams[(rank + i * world) % len(cams)]
+    def view_of(i):   # views round-robin over ranks
+        return cams[unit_of(i, rank, world, len(cams))]
 
     def issue(i, cloud_list, host_out=None):
         lane = i % lanes

@@ -38,9 +38,9 @@ def lib():
         _lib = ctypes.CDLL(str(LIB))
         P, I, D = ctypes.c_void_p, ctypes.c_int64, ctypes.c_double
         _lib.oracle_project.argtypes = [P, P, P, I, P, P, D, D, D, D, I, I, D, D] + [P] * 8
-        _lib.oracle_bin_count.argtypes = [P, P, P, I, I, I, I, I, I, P]
+        _lib.oracle_bin_count.argtypes = [P, P, P, I, I, I, I, I, I, I, I, P]
         _lib.oracle_bin_count.restype = I
-        _lib.oracle_bin_fill.argtypes = [P, P, P, I, I, I, I, I, I, P, P]
+        _lib.oracle_bin_fill.argtypes = [P, P, P, I, I, I, I, I, I, I, I, P, P]
         _lib.oracle_forward.argtypes = [I, I, I, I, I, I, I, P, P, P, P, P, P, P, P, P, P,
                                         D, ctypes.c_int, P, P]
     return _lib
@@ -70,7 +70,7 @@ def project(centers, quats, scales, cam) -> dict:
     return out
 
 
-def prepare(splats: dict, cam, mode: str, tile: int = 16, ty_window=None) -> dict:
+def prepare(splats: dict, cam, mode: str, tile: int = 16, ty_window=None, tx_window=None) -> dict:
     """Depth sort, inverse covariance, alpha-support radius, CSR tile lists
     (rasterizer.py:99-130)."""
     pr = project(splats["centers"], splats["quaternions"], splats["scales"], cam)
@@ -89,13 +89,14 @@ def prepare(splats: dict, cam, mode: str, tile: int = 16, ty_window=None) -> dic
     ntx = -(-int(cam.width) // tile)
     nty = -(-int(cam.height) // tile)
     lo, hi = (0, nty) if ty_window is None else ty_window
+    xlo, xhi = (0, ntx) if tx_window is None else tx_window
     offsets = np.zeros(ntx * nty + 1, dtype=np.int64)
     sx, sy, radius = _c(sx), _c(sy), _c(radius)
     e = lib().oracle_bin_count(_p(sx), _p(sy), _p(radius), sx.size, tile, ntx, nty, lo, hi,
-                               _p(offsets))
+                               xlo, xhi, _p(offsets))
     ids = np.empty(e, dtype=np.int64)
     lib().oracle_bin_fill(_p(sx), _p(sy), _p(radius), sx.size, tile, ntx, nty, lo, hi,
-                          _p(offsets), _p(ids))
+                          xlo, xhi, _p(offsets), _p(ids))
     if mode == "rgb":
         attr = np.asarray(splats["colors"], dtype=np.float64)[source]
     elif mode == "normal":
@@ -122,10 +123,12 @@ def compose(out, trans, mode, background):
 
 
 def render(splats: dict, cam, mode="rgb", background=(0.0, 0.0, 0.0), tile=16,
-           alpha_max=ALPHA_MAX, terminate=True, ty_window=None, prep=None) -> dict:
-    """Tiled render (rasterizer.py:152-166); returns planes plus the prepared CSR."""
+           alpha_max=ALPHA_MAX, terminate=True, ty_window=None, prep=None, tx_window=None) -> dict:
+    """Tiled render (rasterizer.py:152-166); returns planes plus the prepared CSR.
+    ty_window / tx_window restrict the binned tiles to a crop (tests and the
+    bounded CPU sample): pixels outside it are left unrendered."""
     if prep is None:
-        prep = prepare(splats, cam, mode, tile, ty_window)
+        prep = prepare(splats, cam, mode, tile, ty_window, tx_window)
     w, h = int(cam.width), int(cam.height)
     out = np.zeros((h, w, 3))
     trans = np.ones((h, w))

@@ -84,7 +84,7 @@ static void tile_range(double sx, double sy, double r, double ft, int64_t ntx, i
 /* Pass 1: counts per tile (offsets must hold ntx*nty+1 entries); returns E. */
 int64_t oracle_bin_count(const double *sx, const double *sy, const double *radius, int64_t n,
                          int64_t tile, int64_t ntx, int64_t nty, int64_t ty_lo, int64_t ty_hi,
-                         int64_t *offsets) {
+                         int64_t tx_lo, int64_t tx_hi, int64_t *offsets) {
     memset(offsets, 0, sizeof(int64_t) * (ntx * nty + 1));
     double ft = (double)tile;
     for (int64_t i = 0; i < n; ++i) {
@@ -92,6 +92,8 @@ int64_t oracle_bin_count(const double *sx, const double *sy, const double *radiu
         tile_range(sx[i], sy[i], radius[i], ft, ntx, nty, &x0, &x1, &y0, &y1);
         y0 = imax(y0, ty_lo);
         y1 = imin(y1, ty_hi - 1);
+        x0 = imax(x0, tx_lo);   /* crop window (tests): tiles outside stay empty */
+        x1 = imin(x1, tx_hi - 1);
         for (int64_t ty = y0; ty <= y1; ++ty)
             for (int64_t tx = x0; tx <= x1; ++tx) offsets[ty * ntx + tx + 1] += 1;
     }
@@ -102,7 +104,7 @@ int64_t oracle_bin_count(const double *sx, const double *sy, const double *radiu
 /* Pass 2: scatter splat ranks in iteration (= depth) order. */
 void oracle_bin_fill(const double *sx, const double *sy, const double *radius, int64_t n,
                      int64_t tile, int64_t ntx, int64_t nty, int64_t ty_lo, int64_t ty_hi,
-                     const int64_t *offsets, int64_t *ids) {
+                     int64_t tx_lo, int64_t tx_hi, const int64_t *offsets, int64_t *ids) {
     int64_t *cursor = (int64_t *)malloc(sizeof(int64_t) * (ntx * nty));
     memcpy(cursor, offsets, sizeof(int64_t) * (ntx * nty));
     double ft = (double)tile;
@@ -111,6 +113,8 @@ void oracle_bin_fill(const double *sx, const double *sy, const double *radius, i
         tile_range(sx[i], sy[i], radius[i], ft, ntx, nty, &x0, &x1, &y0, &y1);
         y0 = imax(y0, ty_lo);
         y1 = imin(y1, ty_hi - 1);
+        x0 = imax(x0, tx_lo);   /* crop window (tests): tiles outside stay empty */
+        x1 = imin(x1, tx_hi - 1);
         for (int64_t ty = y0; ty <= y1; ++ty)
             for (int64_t tx = x0; tx <= x1; ++tx) ids[cursor[ty * ntx + tx]++] = i;
     }
