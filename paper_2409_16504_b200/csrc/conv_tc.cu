@@ -8,8 +8,9 @@
 //  * CTA = 128 output rows (UMMA M=128, cta_group::1) x all Cout (UMMA N),
 //    accumulator in TMEM (fp32, N columns), one elected thread issues
 //    tcgen05.mma.kind::tf32 for the whole CTA.
-//  * fp32 accuracy with tf32 tensor cores ("3xTF32"): every operand x is split
-//    into hi = tf32(x) and lo = tf32(x - hi); D += Ahi*Bhi + Ahi*Blo + Alo*Bhi.
+//  * fp32 accuracy with tf32 tensor cores: every operand x is split into
+//    hi = rn_tf32(x) and lo = rn_tf32(x - hi); D += Alo*Blo + Alo*Bhi +
+//    Ahi*Blo + Ahi*Bhi (all four products, small terms first).
 //    This keeps the conv at ~1e-6 relative error (bf16 inputs would break the
 //    1e-3 Gaussian-parameter tolerance).
 //  * per tap: the weight tile W[t] (pre-split, pre-laid-out in the UMMA
@@ -37,8 +38,13 @@ __host__ __device__ inline int core_off(int row, int k, int KP) {
     return (row >> 3) * (KP * 8) + (k >> 2) * 32 + (row & 7) * 4 + (k & 3);
 }
 
-__device__ __forceinline__ float tf32_trunc(float x) {
-    return __uint_as_float(__float_as_uint(x) & 0xffffe000u);
+// round-to-nearest (ties away) to tf32: the hi part of the split carries
+// |x - hi| <= 2^-11 |x|, and lo = x - hi is exact in fp32 before its own
+// rounding, so hi + lo keeps ~22 bits (truncation would keep ~20)
+__device__ __forceinline__ float tf32_round(float x) {
+    uint32_t r;
+    asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
+    return __uint_as_float(r);
 }
 
 __device__ __forceinline__ uint32_t smem_u32(const void *p) {
@@ -120,7 +126,9 @@ struct TcShape {
     static constexpr int STAGE_FLOATS = 2 * A_FLOATS + 2 * B_FLOATS;
     static constexpr int STAGES = (STAGE_FLOATS * 4 * 2 <= 200 * 1024) ? 2 : 1;
     static constexpr int SMEM = STAGES * STAGE_FLOATS * 4 + 1024 + 64;
-    static constexpr uint32_t TMEM_COLS = NP <= 32 ? 32 : (NP <= 64 ? 64 : (NP <= 128 ? 128 : 256));
+    // two accumulators (tap t in buffer t % 2): the epilogue of tap t-1 reads
+    // one while the MMAs of tap t write the other
+    static constexpr uint32_t TMEM_COLS = 2 * NP <= 32 ? 32 : (2 * NP <= 64 ? 64 : (2 * NP <= 128 ? 128 : 256));
     static constexpr uint32_t IDESC = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(NP >> 3) << 17) |
                                       ((uint32_t)(kM >> 4) << 24);
 };
@@ -179,12 +187,33 @@ k_conv_tc(const float *__restrict__ in, int ld_in, int cin, const int32_t *__res
     asm volatile("tcgen05.fence::after_thread_sync;");
     const uint32_t tmem = *tmem_slot;
 
+    // Per-tap accumulation: each tap's MMAs start a fresh TMEM accumulator
+    // and the threads add it into fp32 registers with IEEE adds. (Summing all
+    // taps inside the tensor core loses ~20x more to its accumulator rounding
+    // than FFMA does; per tap the K is only Cin.)
+    const uint32_t lane_base = (uint32_t)(warp * 32) << 16;
     int issued = 0;  // MMA batches issued by this CTA so far (drives stage/phase)
+    float acc[NP];
+    auto drain = [&](int i) {   // add the accumulator of batch i into acc
+        mbar_wait(&bar_done[i % S::STAGES], (i / S::STAGES) & 1);
+        asm volatile("tcgen05.fence::after_thread_sync;");
+        const uint32_t buf = tmem + lane_base + (uint32_t)((i & 1) * NP);
+#pragma unroll
+        for (int c = 0; c < NP; c += 16) {
+            float v[16];
+            tmem_ld16(buf + c, v);
+#pragma unroll
+            for (int q = 0; q < 16; ++q) acc[c + q] = __fadd_rn(acc[c + q], v[q]);
+        }
+        asm volatile("tcgen05.fence::before_thread_sync;");
+    };
     for (int64_t wi = blockIdx.x; wi < work; wi += gridDim.x) {
         const int64_t row0 = (wi / splits) * kM;
         const int split = (int)(wi % splits);
         const int t0 = split * tps, t1 = min(taps, t0 + tps);
         const int64_t row = row0 + tid;
+#pragma unroll
+        for (int c = 0; c < NP; ++c) acc[c] = 0.f;
         int item_issued = 0;
         for (int t = t0; t < t1; ++t) {
             const int s = issued % S::STAGES;
@@ -211,53 +240,45 @@ k_conv_tc(const float *__restrict__ in, int ld_in, int cin, const int32_t *__res
                     v[q] = (x && k < cin) ? __ldg(x + k) : 0.f;
                 }
                 float4 hi, lo;
-                hi.x = tf32_trunc(v[0]);
-                hi.y = tf32_trunc(v[1]);
-                hi.z = tf32_trunc(v[2]);
-                hi.w = tf32_trunc(v[3]);
-                lo.x = tf32_trunc(v[0] - hi.x);
-                lo.y = tf32_trunc(v[1] - hi.y);
-                lo.z = tf32_trunc(v[2] - hi.z);
-                lo.w = tf32_trunc(v[3] - hi.w);
+                hi.x = tf32_round(v[0]);
+                hi.y = tf32_round(v[1]);
+                hi.z = tf32_round(v[2]);
+                hi.w = tf32_round(v[3]);
+                lo.x = tf32_round(v[0] - hi.x);
+                lo.y = tf32_round(v[1] - hi.y);
+                lo.z = tf32_round(v[2] - hi.z);
+                lo.w = tf32_round(v[3] - hi.w);
                 const int off = core_off(tid, 4 * c, KP);
                 *reinterpret_cast<float4 *>(A_hi + off) = hi;
                 *reinterpret_cast<float4 *>(A_lo + off) = lo;
             }
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-            __syncthreads();
+            __syncthreads();   // also orders the last drain's TMEM reads before these MMAs
             if (tid == 0) {
                 mbar_wait(&bar_full[s], use & 1);
                 asm volatile("tcgen05.fence::after_thread_sync;");
                 const float *B_lo = B_hi + S::B_FLOATS;
                 const uint32_t lbo = 128, sbo = KP * 32;
+                const uint32_t dst = tmem + (uint32_t)((issued & 1) * NP);
 #pragma unroll
                 for (int ks = 0; ks < KP / 8; ++ks) {
                     const uint64_t ahi = smem_desc(smem_u32(A_hi) + ks * 256, lbo, sbo);
                     const uint64_t alo = smem_desc(smem_u32(A_lo) + ks * 256, lbo, sbo);
                     const uint64_t bhi = smem_desc(smem_u32(B_hi) + ks * 256, lbo, sbo);
                     const uint64_t blo = smem_desc(smem_u32(B_lo) + ks * 256, lbo, sbo);
-                    mma_tf32(tmem, ahi, bhi, S::IDESC, (item_issued > 0 || ks > 0) ? 1u : 0u);
-                    mma_tf32(tmem, ahi, blo, S::IDESC, 1u);
-                    mma_tf32(tmem, alo, bhi, S::IDESC, 1u);
+                    // small terms first: lo*lo, lo*hi, hi*lo, then hi*hi
+                    mma_tf32(dst, alo, blo, S::IDESC, ks > 0 ? 1u : 0u);
+                    mma_tf32(dst, alo, bhi, S::IDESC, 1u);
+                    mma_tf32(dst, ahi, blo, S::IDESC, 1u);
+                    mma_tf32(dst, ahi, bhi, S::IDESC, 1u);
                 }
                 mma_commit(&bar_done[s]);
             }
+            if (item_issued > 0) drain(issued - 1);   // previous tap, overlapping this one's MMAs
             ++issued;
             ++item_issued;
         }
-        // epilogue: TMEM -> registers -> bias/ReLU -> global (or split-K partials)
-        float acc[NP];
-        if (item_issued > 0) {
-            const int last = issued - 1;
-            mbar_wait(&bar_done[last % S::STAGES], (last / S::STAGES) & 1);
-            asm volatile("tcgen05.fence::after_thread_sync;");
-            const uint32_t lane_base = (uint32_t)(warp * 32) << 16;
-#pragma unroll
-            for (int c = 0; c < NP; c += 16) tmem_ld16(tmem + lane_base + c, acc + c);
-        } else {
-#pragma unroll
-            for (int c = 0; c < NP; ++c) acc[c] = 0.f;
-        }
+        if (item_issued > 0) drain(issued - 1);
         if (row < m) {
             if (splits > 1) {
                 float *p = partial + ((size_t)split * m + row) * NP;
@@ -274,8 +295,7 @@ k_conv_tc(const float *__restrict__ in, int ld_in, int cin, const int32_t *__res
                     }
             }
         }
-        // all TMEM reads done before the next item's MMAs overwrite the accumulator
-        asm volatile("tcgen05.fence::before_thread_sync;");
+        // all TMEM reads done before the next item's MMAs overwrite the accumulators
         __syncthreads();
         asm volatile("tcgen05.fence::after_thread_sync;");
     }
@@ -311,7 +331,7 @@ __global__ void k_prep_weights(const float *__restrict__ w, int taps, int cin, i
     int rem = (int)(i % per);
     int n = rem / KP, k = rem % KP;
     float x = (n < cout && k < cin) ? w[((size_t)t * cin + k) * cout + n] : 0.f;
-    float hi = tf32_trunc(x), lo = tf32_trunc(x - hi);
+    float hi = tf32_round(x), lo = tf32_round(x - hi);
     float *base = wtc + (size_t)t * 2 * per;
     int off = core_off(n, k, KP);
     base[off] = hi;
