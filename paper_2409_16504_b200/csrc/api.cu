@@ -196,10 +196,16 @@ int sfb_ctx_create(int device, sfb_ctx **out) {
         cudaDeviceGetAttribute(&ctx->num_sms, cudaDevAttrMultiProcessorCount, device) != cudaSuccess ||
         cudaMallocHost(&ctx->pinned, 4096) != cudaSuccess ||
         cudaStreamCreateWithFlags(&ctx->capture_stream, cudaStreamNonBlocking) != cudaSuccess ||
-        cudaEventCreateWithFlags(&ctx->fork_event, cudaEventDisableTiming) != cudaSuccess) {
+        cudaEventCreateWithFlags(&ctx->fork_event, cudaEventDisableTiming) != cudaSuccess ||
+        cudaStreamCreateWithFlags(&ctx->side_stream, cudaStreamNonBlocking) != cudaSuccess) {
         delete ctx;
         return SFB_ERR_CUDA;
     }
+    for (auto &e : ctx->side_ev)
+        if (cudaEventCreateWithFlags(&e, cudaEventDisableTiming) != cudaSuccess) {
+            delete ctx;
+            return SFB_ERR_CUDA;
+        }
     *out = ctx;
     return SFB_OK;
 }

@@ -126,6 +126,11 @@ struct sfb_ctx {
     bool use_graphs = true;
     cudaStream_t capture_stream = nullptr;
     cudaEvent_t fork_event = nullptr;
+    // side branch of the frame (coordinate structure of the UNet levels runs
+    // concurrently with the convolutions): its stream and fork/join events
+    cudaStream_t side_stream = nullptr;
+    static constexpr int kSideEvents = 10;
+    cudaEvent_t side_ev[kSideEvents] = {};
     std::vector<sfb_frame_graph *> graphs;
     int64_t graph_nodes = 0;
     int64_t *debug_counters = nullptr;   // compositor per-tile counters (diagnostics)
@@ -163,6 +168,9 @@ struct sfb_ctx {
         for (auto &e : ev)
             if (e) cudaEventDestroy(e);
         if (capture_stream) cudaStreamDestroy(capture_stream);
+        if (side_stream) cudaStreamDestroy(side_stream);
+        for (auto &e : side_ev)
+            if (e) cudaEventDestroy(e);
         if (fork_event) cudaEventDestroy(fork_event);
     }
     // read `count` int64 values back from device (one sync)
@@ -280,6 +288,17 @@ void pool_build(sfb_ctx *ctx, const int32_t *coords, const int64_t *d_m, int64_t
                 int c, int ld_in, int32_t *parent_coords, float *parent_feats, int ld_out,
                 int32_t *child_to_parent, int64_t *d_mp);
 void coords_layout(sfb_ctx *ctx, const int32_t *coords, int64_t m, FrameParams &P);
+// fused UNet pooling, split: coordinate structure (side stream) + means
+struct PoolStructure {
+    HashTable table;        // parent key -> parent row (the coarse level's hash)
+    int32_t *c2p, *tap;     // per child: parent row, tap under the parent
+    int32_t *nkids, *kids;  // per parent: child count, up to 8 child rows
+};
+PoolStructure pool_structure(sfb_ctx *ctx, const int32_t *coords, const int64_t *d_m,
+                             int64_t m_bound, int64_t m_grid, int stride, int32_t *parent_coords,
+                             int64_t *d_mp);
+void pool_means(sfb_ctx *ctx, const PoolStructure &P, const int64_t *d_mp, int64_t mp_grid,
+                const float *feats, int c, int ld_in, float *parent_feats, int ld_out);
 // sort-free pooling for the fused UNet: parents in first-child order
 void pool_fast(sfb_ctx *ctx, const int32_t *coords, const int64_t *d_m, int64_t m_bound,
                int64_t m_grid, int stride, const float *feats, int c, int ld_in,

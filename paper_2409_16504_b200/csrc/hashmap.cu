@@ -313,18 +313,30 @@ __global__ void k_pool_first(const int32_t *__restrict__ slot_of, const int32_t 
     SFB_FOR(j, m) flag[j] = minrow[slot_of[j]] == (int32_t)j;
 }
 
+// child -> parent row, parent coords, children lists; optionally the child's
+// tap under its parent (dz*4+dy*2+dx, sparsenet.py:236) and the parent row in
+// the table's value slots (the table then IS the parent level's voxel hash)
 __global__ void k_pool_assign(const int32_t *__restrict__ coords, const int32_t *__restrict__ slot_of,
                               const int32_t *__restrict__ minrow, const int32_t *__restrict__ pid_of_first,
                               const int64_t *__restrict__ d_m, int64_t S, int32_t *__restrict__ pcoords,
                               int32_t *__restrict__ c2p, int32_t *__restrict__ nkids,
-                              int32_t *__restrict__ kids) {
+                              int32_t *__restrict__ kids, int32_t *__restrict__ tap,
+                              int32_t *__restrict__ vals) {
     const int64_t m = *d_m;
+    const int64_t cs = S / 2;
     SFB_FOR(j, m) {
-        const int32_t first = minrow[slot_of[j]];
+        const int32_t slot = slot_of[j];
+        const int32_t first = minrow[slot];
         const int32_t pid = pid_of_first[first];
         c2p[j] = pid;
-        if (first == (int32_t)j)
-            for (int a = 0; a < 3; ++a) pcoords[3 * pid + a] = (int32_t)(floor_div(coords[3 * j + a], S) * S);
+        int64_t d[3];
+        for (int a = 0; a < 3; ++a) {
+            const int64_t c = coords[3 * j + a], pc = floor_div(c, S) * S;
+            d[a] = (c - pc) / cs;
+            if (first == (int32_t)j) pcoords[3 * pid + a] = (int32_t)pc;
+        }
+        if (tap) tap[j] = (int32_t)(d[2] * 4 + d[1] * 2 + d[0]);
+        if (vals && first == (int32_t)j) vals[slot] = pid;
         const int32_t k = atomicAdd(&nkids[pid], 1);
         if (k < 8) kids[8 * (int64_t)pid + k] = (int32_t)j;
     }
@@ -380,9 +392,53 @@ void pool_fast(sfb_ctx *ctx, const int32_t *coords, const int64_t *d_m, int64_t 
     SFB_CHECK_LAUNCH();
     dscan(ctx, flag, flag, d_m, m_bound, d_mp, false);
     k_pool_assign<<<g, 256, 0, st>>>(coords, slot_of, minrow, flag, d_m, S, parent_coords,
-                                     child_to_parent, nkids, kids);
+                                     child_to_parent, nkids, kids, nullptr, nullptr);
     k_pool_means_fast<<<dgrid(m_grid * c, 256), 256, 0, st>>>(feats, ld_in, c, nkids, kids, d_mp,
                                                               parent_feats, ld_out);
+    SFB_CHECK_LAUNCH();
+}
+
+// The fused UNet splits pooling in two: the coordinate structure (parents,
+// children lists, child taps, the parent level's hash table) depends only on
+// coordinates and runs on a side stream ahead of the convolutions; the means
+// need the level's conv output and stay on the critical path.
+PoolStructure pool_structure(sfb_ctx *ctx, const int32_t *coords, const int64_t *d_m,
+                             int64_t m_bound, int64_t m_grid, int stride, int32_t *parent_coords,
+                             int64_t *d_mp) {
+    cudaStream_t st = ctx->stream;
+    PoolStructure P;
+    const int64_t S = 2 * (int64_t)stride;
+    uint64_t cap = 64;
+    while (cap < (uint64_t)(2 * m_bound)) cap <<= 1;
+    uint64_t cap_grid = 64;
+    while (cap_grid < (uint64_t)(2 * m_grid)) cap_grid <<= 1;
+    P.table.keys = ctx->arena.alloc<unsigned long long>(cap);
+    P.table.vals = ctx->arena.alloc<int32_t>(cap);
+    P.table.mask = ctx->arena.alloc<uint32_t>(1);
+    int32_t *minrow = ctx->arena.alloc<int32_t>(cap);
+    int32_t *slot_of = ctx->arena.alloc<int32_t>(m_bound);
+    int32_t *flag = ctx->arena.alloc<int32_t>(m_bound);
+    P.nkids = ctx->arena.alloc<int32_t>(m_bound);
+    P.kids = ctx->arena.alloc<int32_t>(8 * m_bound);
+    P.c2p = ctx->arena.alloc<int32_t>(m_bound);
+    P.tap = ctx->arena.alloc<int32_t>(m_bound);
+    const unsigned g = dgrid(m_grid, 256);
+    k_pool_clear<<<dgrid((int64_t)cap_grid, 256), 256, 0, st>>>(P.table.keys, minrow, P.nkids,
+                                                                P.table.mask, d_m);
+    k_pool_insert<<<g, 256, 0, st>>>(coords, d_m, S, P.table.keys, minrow, P.table.mask, slot_of);
+    k_pool_first<<<g, 256, 0, st>>>(slot_of, minrow, d_m, flag);
+    SFB_CHECK_LAUNCH();
+    dscan(ctx, flag, flag, d_m, m_bound, d_mp, false);
+    k_pool_assign<<<g, 256, 0, st>>>(coords, slot_of, minrow, flag, d_m, S, parent_coords, P.c2p,
+                                     P.nkids, P.kids, P.tap, P.table.vals);
+    SFB_CHECK_LAUNCH();
+    return P;
+}
+
+void pool_means(sfb_ctx *ctx, const PoolStructure &P, const int64_t *d_mp, int64_t mp_grid,
+                const float *feats, int c, int ld_in, float *parent_feats, int ld_out) {
+    k_pool_means_fast<<<dgrid(mp_grid * c, 256), 256, 0, ctx->stream>>>(
+        feats, ld_in, c, P.nkids, P.kids, d_mp, parent_feats, ld_out);
     SFB_CHECK_LAUNCH();
 }
 

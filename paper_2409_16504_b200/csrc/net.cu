@@ -465,40 +465,64 @@ void unet_run(sfb_ctx *ctx, const int32_t *coords0, const double *feats9, int64_
     SFB_REQUIRE(net.loaded, "network weights are not loaded");
     const int L = net.levels;
     SFB_REQUIRE(L + 1 <= 9, "at most 8 UNet levels");
+    SFB_REQUIRE(L <= sfb_ctx::kSideEvents - 1, "too many UNet levels for the side branch");
     const auto &enc = net.enc;
     const auto &dec = net.dec;
     cudaStream_t st = ctx->stream;
     std::vector<const int32_t *> coords(L + 1);
-    std::vector<int32_t *> nbr(L + 1), c2p(L);
+    std::vector<int32_t *> nbr(L + 1);
+    std::vector<PoolStructure> ps(L);
     std::vector<float *> cat(L), pin(L + 1);
     std::vector<int> width(L);
     coords[0] = coords0;
     for (int l = 0; l < L; ++l) width[l] = dec[L - 1 - l] + enc[l + 1];
     std::vector<int64_t> mg(L + 1);
     for (int l = 0; l <= L; ++l) mg[l] = ctx->grid_bound(mb, ctx->hint_m[l]);
+    std::vector<int> kern(L + 1);
+    {
+        int layer = 0;
+        for (int l = 0; l <= L; ++l) kern[l] = net.layers[layer++].kernel;
+    }
+    // level 0: hash + kernel map on the critical path
+    HashTable h0 = hash_build(ctx, coords[0], &C->m[0], mb, mg[0]);
+    nbr[0] = ctx->arena.alloc<int32_t>((size_t)kern[0] * kern[0] * kern[0] * mb);
+    kernel_map_build(ctx, h0, coords[0], &C->m[0], mb, 1, kern[0], nbr[0], mg[0]);
+    // side branch: the coordinate structure of every coarser level (parents,
+    // children, taps, hash = the pooling table, kernel map) depends only on
+    // coordinates, so it runs concurrently with the convolutions; event l
+    // marks "level l+1 structure and kernel map ready"
+    SFB_CUDA(cudaEventRecord(ctx->side_ev[L], st));
+    SFB_CUDA(cudaStreamWaitEvent(ctx->side_stream, ctx->side_ev[L], 0));
+    ctx->stream = ctx->side_stream;
+    try {
+        for (int l = 0; l < L; ++l) {
+            int32_t *pc = ctx->arena.alloc<int32_t>((size_t)mb * 3);
+            ps[l] = pool_structure(ctx, coords[l], &C->m[l], mb, mg[l], 1 << l, pc, &C->m[l + 1]);
+            coords[l + 1] = pc;
+            const int k = kern[l + 1];
+            nbr[l + 1] = ctx->arena.alloc<int32_t>((size_t)k * k * k * mb);
+            kernel_map_build(ctx, ps[l].table, pc, &C->m[l + 1], mb, 2 << l, k, nbr[l + 1],
+                             mg[l + 1]);
+            SFB_CUDA(cudaEventRecord(ctx->side_ev[l], ctx->stream));
+        }
+    } catch (...) {
+        ctx->stream = st;
+        throw;
+    }
+    ctx->stream = st;
     pin[0] = ctx->arena.alloc<float>((size_t)mb * enc[0]);
     k_feats_to_f32<<<dgrid(mg[0] * enc[0], 256), 256, 0, st>>>(feats9, &C->m[0], enc[0], pin[0]);
     SFB_CHECK_LAUNCH();
     int layer = 0;
-    for (int l = 0; l <= L; ++l) {
-        const int stride = 1 << l;
-        const int64_t *dm = &C->m[l];
-        HashTable h = hash_build(ctx, coords[l], dm, mb, mg[l]);
-        const int kern = net.layers[layer].kernel, taps = kern * kern * kern;
-        nbr[l] = ctx->arena.alloc<int32_t>((size_t)taps * mb);
-        kernel_map_build(ctx, h, coords[l], dm, mb, stride, kern, nbr[l], mg[l]);
-        if (l == L) break;
+    for (int l = 0; l < L; ++l) {
         cat[l] = ctx->arena.alloc<float>((size_t)mb * width[l]);
         const int up = dec[L - 1 - l];
-        conv_layer(ctx, net.layers[layer++], pin[l], enc[l], nbr[l], mb, dm, mb, 1, cat[l] + up,
-                   width[l], mg[l]);
-        int32_t *pc = ctx->arena.alloc<int32_t>((size_t)mb * 3);
+        conv_layer(ctx, net.layers[layer++], pin[l], enc[l], nbr[l], mb, &C->m[l], mb, 1,
+                   cat[l] + up, width[l], mg[l]);
         pin[l + 1] = ctx->arena.alloc<float>((size_t)mb * enc[l + 1]);
-        c2p[l] = ctx->arena.alloc<int32_t>(mb);
-        // sort-free pooling: coarse rows in first-child order (results per voxel unchanged)
-        pool_fast(ctx, coords[l], dm, mb, mg[l], stride, cat[l] + up, enc[l + 1], width[l], pc,
-                  pin[l + 1], enc[l + 1], c2p[l], &C->m[l + 1]);
-        coords[l + 1] = pc;
+        SFB_CUDA(cudaStreamWaitEvent(st, ctx->side_ev[l], 0));   // level l+1 structure ready
+        pool_means(ctx, ps[l], &C->m[l + 1], mg[l + 1], cat[l] + up, enc[l + 1], width[l],
+                   pin[l + 1], enc[l + 1]);
     }
     float *bott = ctx->arena.alloc<float>((size_t)mb * enc[L + 1]);
     conv_layer(ctx, net.layers[layer++], pin[L], enc[L], nbr[L], mb, &C->m[L], mb, 1, bott,
@@ -506,11 +530,8 @@ void unet_run(sfb_ctx *ctx, const int32_t *coords0, const double *feats9, int64_
     const float *coarse = bott;
     int ld_coarse = enc[L + 1];
     for (int l = L - 1; l >= 0; --l) {
-        int32_t *tap = ctx->arena.alloc<int32_t>(mb);
-        k_child_tap<<<dgrid(mg[l], 256), 256, 0, st>>>(coords[l], &C->m[l], 1 << l, tap);
-        SFB_CHECK_LAUNCH();
-        tconv_layer(ctx, net.layers[layer++], coarse, ld_coarse, c2p[l], tap, &C->m[l], mb, 1,
-                    cat[l], width[l], mg[l]);
+        tconv_layer(ctx, net.layers[layer++], coarse, ld_coarse, ps[l].c2p, ps[l].tap, &C->m[l], mb,
+                    1, cat[l], width[l], mg[l]);
         coarse = cat[l];
         ld_coarse = width[l];
     }
