@@ -292,6 +292,7 @@ void coords_layout(sfb_ctx *ctx, const int32_t *coords, int64_t m, FrameParams &
 struct PoolStructure {
     HashTable table;        // parent key -> parent row (the coarse level's hash)
     int32_t *c2p, *tap;     // per child: parent row, tap under the parent
+    int32_t *tmap;          // (8, m) tap-major map of the transposed conv
     int32_t *nkids, *kids;  // per parent: child count, up to 8 child rows
 };
 PoolStructure pool_structure(sfb_ctx *ctx, const int32_t *coords, const int64_t *d_m,
@@ -330,7 +331,8 @@ void conv_layer(sfb_ctx *ctx, const NetLayer &L, const float *in, int ld_in, con
                 int ld_out, int64_t m_grid = -1);
 void tconv_layer(sfb_ctx *ctx, const NetLayer &L, const float *in, int ld_in,
                  const int32_t *parent, const int32_t *tap, const int64_t *d_m, int64_t m_bound,
-                 int relu, float *out, int ld_out, int64_t m_grid = -1);
+                 int relu, float *out, int ld_out, int64_t m_grid = -1,
+                 const int32_t *tmap = nullptr);
 void layer_set(sfb_ctx *ctx, int kind, int kernel, int cin, int cout, const float *w_host,
                const float *b_host);
 // per-voxel Gaussians for the fused frame: centres, sigma, quat, opacity, normal

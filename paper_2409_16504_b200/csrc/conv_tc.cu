@@ -64,15 +64,22 @@ __device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
 }
 
+// wait for the phase of `parity` to complete; a wait that never completes
+// (a pipeline bug) traps after ~2^28 polls instead of hanging the GPU
 __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
-    uint32_t addr = smem_u32(bar);
-    asm volatile(
-        "{\n\t.reg .pred P;\n"
-        "WAIT_%=:\n\t"
-        "mbarrier.try_wait.parity.shared::cta.b64 P, [%0], %1;\n\t"
-        "@!P bra WAIT_%=;\n}" ::"r"(addr),
-        "r"(parity)
-        : "memory");
+    const uint32_t addr = smem_u32(bar);
+    for (uint32_t n = 0;; ++n) {
+        uint32_t done;
+        asm volatile(
+            "{\n\t.reg .pred P;\n\t"
+            "mbarrier.try_wait.parity.shared::cta.b64 P, [%1], %2;\n\t"
+            "selp.u32 %0, 1, 0, P;\n\t}"
+            : "=r"(done)
+            : "r"(addr), "r"(parity)
+            : "memory");
+        if (done) return;
+        if (n > (1u << 28)) __trap();
+    }
 }
 
 __device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, uint32_t bytes) {
@@ -158,7 +165,7 @@ k_conv_tc(const float *__restrict__ in, int ld_in, int cin, const int32_t *__res
     float *stage_base = reinterpret_cast<float *>(
         (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     uint64_t *bar_full = reinterpret_cast<uint64_t *>(stage_base + S::STAGES * S::STAGE_FLOATS);
-    uint64_t *bar_done = bar_full + 2;
+    uint64_t *bar_done = bar_full + 2;   // indexed by batch parity (i & 1), phase i >> 1
     uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(bar_done + 2);
 
     const int tid = threadIdx.x, warp = tid >> 5;
@@ -195,7 +202,7 @@ k_conv_tc(const float *__restrict__ in, int ld_in, int cin, const int32_t *__res
     int issued = 0;  // MMA batches issued by this CTA so far (drives stage/phase)
     float acc[NP];
     auto drain = [&](int i) {   // add the accumulator of batch i into acc
-        mbar_wait(&bar_done[i % S::STAGES], (i / S::STAGES) & 1);
+        mbar_wait(&bar_done[i & 1], (i >> 1) & 1);
         asm volatile("tcgen05.fence::after_thread_sync;");
         const uint32_t buf = tmem + lane_base + (uint32_t)((i & 1) * NP);
 #pragma unroll
@@ -223,7 +230,14 @@ k_conv_tc(const float *__restrict__ in, int ld_in, int cin, const int32_t *__res
             float *B_hi = A_lo + S::A_FLOATS;
             const int32_t src = row < m ? nbr[(int64_t)t * nbr_ld + row] : -1;
             if (!__syncthreads_or(src >= 0)) continue;   // empty tap for the whole tile
-            if (use > 0) mbar_wait(&bar_done[s], (use - 1) & 1);   // stage free again
+            // stage free again: the batch that last used it (i - STAGES) has
+            // completed. Batch barriers alternate by batch parity, so no wait
+            // below can alias a later phase: the next commit to the barrier
+            // of batch j is batch j+2, issued only after j is drained.
+            if (issued >= S::STAGES) {
+                const int j = issued - S::STAGES;
+                mbar_wait(&bar_done[j & 1], (j >> 1) & 1);
+            }
             if (tid == 0) {
                 const uint32_t bytes = (uint32_t)(2 * S::B_FLOATS * 4);
                 mbar_expect_tx(&bar_full[s], bytes);
@@ -272,7 +286,7 @@ k_conv_tc(const float *__restrict__ in, int ld_in, int cin, const int32_t *__res
                     mma_tf32(dst, ahi, blo, S::IDESC, 1u);
                     mma_tf32(dst, ahi, bhi, S::IDESC, 1u);
                 }
-                mma_commit(&bar_done[s]);
+                mma_commit(&bar_done[issued & 1]);
             }
             if (item_issued > 0) drain(issued - 1);   // previous tap, overlapping this one's MMAs
             ++issued;
@@ -370,7 +384,7 @@ void launch_tc(sfb_ctx *ctx, const NetLayer &L, const float *in, int ld_in, cons
 }  // namespace
 
 bool conv_tc_supported(const NetLayer &L) {
-    if (L.kind != 0) return false;
+    if (L.kind != 0 && L.kind != 1) return false;   // conv, or transposed conv as an 8-tap map
     int kp = pad_k(L.cin), np = pad_n(L.cout);
     if (L.cin > 128 || L.cout > 128) return false;
     size_t stage = (size_t)(2 * kM * kp + 2 * np * kp) * 4;

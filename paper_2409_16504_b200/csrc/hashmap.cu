@@ -321,7 +321,7 @@ __global__ void k_pool_assign(const int32_t *__restrict__ coords, const int32_t 
                               const int64_t *__restrict__ d_m, int64_t S, int32_t *__restrict__ pcoords,
                               int32_t *__restrict__ c2p, int32_t *__restrict__ nkids,
                               int32_t *__restrict__ kids, int32_t *__restrict__ tap,
-                              int32_t *__restrict__ vals) {
+                              int32_t *__restrict__ vals, int32_t *__restrict__ tmap, int64_t ld) {
     const int64_t m = *d_m;
     const int64_t cs = S / 2;
     SFB_FOR(j, m) {
@@ -335,7 +335,11 @@ __global__ void k_pool_assign(const int32_t *__restrict__ coords, const int32_t 
             d[a] = (c - pc) / cs;
             if (first == (int32_t)j) pcoords[3 * pid + a] = (int32_t)pc;
         }
-        if (tap) tap[j] = (int32_t)(d[2] * 4 + d[1] * 2 + d[0]);
+        const int32_t tj = (int32_t)(d[2] * 4 + d[1] * 2 + d[0]);
+        if (tap) tap[j] = tj;
+        if (tmap)
+#pragma unroll
+            for (int k = 0; k < 8; ++k) tmap[k * ld + j] = (k == tj) ? pid : -1;
         if (vals && first == (int32_t)j) vals[slot] = pid;
         const int32_t k = atomicAdd(&nkids[pid], 1);
         if (k < 8) kids[8 * (int64_t)pid + k] = (int32_t)j;
@@ -392,7 +396,7 @@ void pool_fast(sfb_ctx *ctx, const int32_t *coords, const int64_t *d_m, int64_t 
     SFB_CHECK_LAUNCH();
     dscan(ctx, flag, flag, d_m, m_bound, d_mp, false);
     k_pool_assign<<<g, 256, 0, st>>>(coords, slot_of, minrow, flag, d_m, S, parent_coords,
-                                     child_to_parent, nkids, kids, nullptr, nullptr);
+                                     child_to_parent, nkids, kids, nullptr, nullptr, nullptr, 0);
     k_pool_means_fast<<<dgrid(m_grid * c, 256), 256, 0, st>>>(feats, ld_in, c, nkids, kids, d_mp,
                                                               parent_feats, ld_out);
     SFB_CHECK_LAUNCH();
@@ -422,6 +426,7 @@ PoolStructure pool_structure(sfb_ctx *ctx, const int32_t *coords, const int64_t 
     P.kids = ctx->arena.alloc<int32_t>(8 * m_bound);
     P.c2p = ctx->arena.alloc<int32_t>(m_bound);
     P.tap = ctx->arena.alloc<int32_t>(m_bound);
+    P.tmap = ctx->arena.alloc<int32_t>(8 * m_bound);
     const unsigned g = dgrid(m_grid, 256);
     k_pool_clear<<<dgrid((int64_t)cap_grid, 256), 256, 0, st>>>(P.table.keys, minrow, P.nkids,
                                                                 P.table.mask, d_m);
@@ -430,7 +435,7 @@ PoolStructure pool_structure(sfb_ctx *ctx, const int32_t *coords, const int64_t 
     SFB_CHECK_LAUNCH();
     dscan(ctx, flag, flag, d_m, m_bound, d_mp, false);
     k_pool_assign<<<g, 256, 0, st>>>(coords, slot_of, minrow, flag, d_m, S, parent_coords, P.c2p,
-                                     P.nkids, P.kids, P.tap, P.table.vals);
+                                     P.nkids, P.kids, P.tap, P.table.vals, P.tmap, m_bound);
     SFB_CHECK_LAUNCH();
     return P;
 }

@@ -100,7 +100,7 @@ void net_load(sfb_ctx *ctx, const void *blob, size_t nbytes) {
         }
         SFB_REQUIRE(c.pos == c.n, "weights: trailing bytes after last layer");
         for (auto &L : fresh.layers)
-            if (L.kind == 0 && conv_tc_supported(L)) {
+            if (conv_tc_supported(L)) {
                 prepare_tc_weights(ctx, L);
                 fresh.allocations.push_back(L.w_tc);
             }
@@ -140,7 +140,7 @@ void layer_set(sfb_ctx *ctx, int kind, int kernel, int cin, int cout, const floa
     SFB_CUDA(cudaMalloc(&L.b, 4 * (size_t)cout));
     SFB_CUDA(cudaMemcpyAsync(L.w, w_host, 4 * nw, cudaMemcpyHostToDevice, ctx->stream));
     SFB_CUDA(cudaMemcpyAsync(L.b, b_host, 4 * (size_t)cout, cudaMemcpyHostToDevice, ctx->stream));
-    if (kind == 0 && conv_tc_supported(L)) prepare_tc_weights(ctx, L);
+    if (conv_tc_supported(L)) prepare_tc_weights(ctx, L);
     SFB_CUDA(cudaStreamSynchronize(ctx->stream));
 }
 
@@ -251,11 +251,35 @@ __global__ void k_tconv(const float *__restrict__ in, int ld_in, const int32_t *
     }
 }
 
+// 8-tap "kernel map" of a transposed conv: row r gathers its parent under
+// tap[r] only, so sum_t in[map[t][r]] @ W[t] = in[parent[r]] @ W[tap[r]]
+// (orphans: no tap, bias only) — the tcgen05 gather-GEMM then runs it as-is
+__global__ void k_tmap(const int32_t *__restrict__ parent, const int32_t *__restrict__ tap,
+                       const int64_t *__restrict__ d_m, int64_t m_fixed, int64_t ld,
+                       int32_t *__restrict__ tmap) {
+    const int64_t m = d_m ? *d_m : m_fixed;
+    SFB_FOR(r, m) {
+        const int32_t p = parent[r], t = tap[r];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) tmap[k * ld + r] = (k == t) ? p : -1;
+    }
+}
+
 void tconv_layer(sfb_ctx *ctx, const NetLayer &L, const float *in, int ld_in,
                  const int32_t *parent, const int32_t *tap, const int64_t *d_m, int64_t m_bound,
-                 int relu, float *out, int ld_out, int64_t m_grid) {
+                 int relu, float *out, int ld_out, int64_t m_grid, const int32_t *tmap) {
     if (m_bound == 0) return;
     if (m_grid < 0) m_grid = m_bound;
+    if (ctx->net_mode == SFB_NET_TC_TF32X3 && L.w_tc) {
+        if (!tmap) {
+            int32_t *t = ctx->arena.alloc<int32_t>(8 * (size_t)m_bound);
+            k_tmap<<<dgrid(m_grid, 256), 256, 0, ctx->stream>>>(parent, tap, d_m, m_bound, m_bound, t);
+            SFB_CHECK_LAUNCH();
+            tmap = t;
+        }
+        conv_layer_tc(ctx, L, in, ld_in, tmap, m_bound, d_m, m_bound, relu, out, ld_out, m_grid);
+        return;
+    }
     k_tconv<<<dgrid(m_grid * L.cout, 256), 256, 0, ctx->stream>>>(
         in, ld_in, parent, tap, d_m, m_bound, L.cin, L.cout, L.w, L.b, relu, out, ld_out);
     SFB_CHECK_LAUNCH();
@@ -531,7 +555,7 @@ void unet_run(sfb_ctx *ctx, const int32_t *coords0, const double *feats9, int64_
     int ld_coarse = enc[L + 1];
     for (int l = L - 1; l >= 0; --l) {
         tconv_layer(ctx, net.layers[layer++], coarse, ld_coarse, ps[l].c2p, ps[l].tap, &C->m[l], mb,
-                    1, cat[l], width[l], mg[l]);
+                    1, cat[l], width[l], mg[l], ps[l].tmap);
         coarse = cat[l];
         ld_coarse = width[l];
     }
