@@ -38,13 +38,12 @@ __host__ __device__ inline int core_off(int row, int k, int KP) {
     return (row >> 3) * (KP * 8) + (k >> 2) * 32 + (row & 7) * 4 + (k & 3);
 }
 
-// round-to-nearest (ties away) to tf32: the hi part of the split carries
-// |x - hi| <= 2^-11 |x|, and lo = x - hi is exact in fp32 before its own
-// rounding, so hi + lo keeps ~22 bits (truncation would keep ~20)
+// round-to-nearest (ties away) to tf32, as cvt.rna.tf32.f32 but in two
+// integer ops (add half an ulp of tf32, clear the 13 dropped bits): the hi
+// part of the split carries |x - hi| <= 2^-11 |x|, and lo = x - hi is exact
+// in fp32 before its own rounding, so hi + lo keeps ~22 bits
 __device__ __forceinline__ float tf32_round(float x) {
-    uint32_t r;
-    asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
-    return __uint_as_float(r);
+    return __uint_as_float((__float_as_uint(x) + 0x1000u) & 0xffffe000u);
 }
 
 __device__ __forceinline__ uint32_t smem_u32(const void *p) {
@@ -141,11 +140,12 @@ struct TcShape {
 };
 
 // split-K factor for a level: the smallest divisor c (<= 32) of the tap count
-// with tiles*c >= target work items (else the largest such divisor)
+// with at most 32 taps per split and tiles*c >= target work items (else the
+// largest such divisor); 0 when no divisor keeps a split within 32 taps
 __host__ __device__ inline int choose_splits(int64_t tiles, int taps, int target) {
-    int best = 1;
+    int best = 0;
     for (int c = 1; c <= taps && c <= 32; ++c) {
-        if (taps % c) continue;
+        if (taps % c || taps / c > 32) continue;
         best = c;
         if (tiles * c >= target) break;
     }
@@ -175,6 +175,7 @@ k_conv_tc(const float *__restrict__ in, int ld_in, int cin, const int32_t *__res
     const int tps = (taps + splits - 1) / splits;
     const int64_t work = tiles * splits;
     if ((int64_t)blockIdx.x >= work) return;   // uniform per CTA, before any collective
+    if (tps > 32) __trap();                    // the host side guarantees <= 27 taps
 
     if (tid == 0) {
         for (int s = 0; s < 2; ++s) {
@@ -214,6 +215,8 @@ k_conv_tc(const float *__restrict__ in, int ld_in, int cin, const int32_t *__res
         }
         asm volatile("tcgen05.fence::before_thread_sync;");
     };
+    __shared__ int32_t s_src[32][kM];   // kernel-map rows of this item's taps
+    __shared__ uint32_t s_mask[kThreadsTC / 32];
     for (int64_t wi = blockIdx.x; wi < work; wi += gridDim.x) {
         const int64_t row0 = (wi / splits) * kM;
         const int split = (int)(wi % splits);
@@ -221,15 +224,47 @@ k_conv_tc(const float *__restrict__ in, int ld_in, int cin, const int32_t *__res
         const int64_t row = row0 + tid;
 #pragma unroll
         for (int c = 0; c < NP; ++c) acc[c] = 0.f;
-        int item_issued = 0;
+        // prefetch the kernel map of every tap of the item (independent
+        // coalesced loads) and OR the per-tap occupancy over the tile
+        uint32_t mymask = 0;
         for (int t = t0; t < t1; ++t) {
+            const int32_t src = row < m ? nbr[(int64_t)t * nbr_ld + row] : -1;
+            s_src[t - t0][tid] = src;
+            mymask |= (src >= 0 ? 1u : 0u) << (t - t0);
+        }
+        mymask = __reduce_or_sync(0xffffffffu, mymask);
+        if ((tid & 31) == 0) s_mask[warp] = mymask;
+        __syncthreads();
+        uint32_t mask = 0;
+#pragma unroll
+        for (int w = 0; w < kThreadsTC / 32; ++w) mask |= s_mask[w];
+        // register-prefetched gather: the rows of the next non-empty tap are
+        // in flight while the current tap is split, staged and multiplied
+        float v[KP];
+        auto fetch = [&](int t) {
+            const int32_t src = s_src[t - t0][tid];
+            const float *x = src >= 0 ? in + (int64_t)src * ld_in : nullptr;
+#pragma unroll
+            for (int k = 0; k < KP; ++k) v[k] = (x && k < cin) ? __ldg(x + k) : 0.f;
+        };
+        if (mask) fetch(t0 + __ffs(mask) - 1);
+        // weights: with two stages, tap k+1's tile is fetched (TMA) as soon as
+        // batch k-1 has drained, so its latency hides behind tap k
+        auto load_w = [&](int t, int slot) {
+            const uint32_t bytes = (uint32_t)(2 * S::B_FLOATS * 4);
+            float *B = stage_base + slot * S::STAGE_FLOATS + 2 * S::A_FLOATS;
+            mbar_expect_tx(&bar_full[slot], bytes);
+            tma_bulk_g2s(B, wtc + (size_t)t * 2 * S::B_FLOATS, bytes, &bar_full[slot]);
+        };
+        int item_issued = 0;
+        while (mask) {
+            const int t = t0 + __ffs(mask) - 1;
+            mask &= mask - 1;
             const int s = issued % S::STAGES;
             const int use = issued / S::STAGES;
             float *A_hi = stage_base + s * S::STAGE_FLOATS;
             float *A_lo = A_hi + S::A_FLOATS;
             float *B_hi = A_lo + S::A_FLOATS;
-            const int32_t src = row < m ? nbr[(int64_t)t * nbr_ld + row] : -1;
-            if (!__syncthreads_or(src >= 0)) continue;   // empty tap for the whole tile
             // stage free again: the batch that last used it (i - STAGES) has
             // completed. Batch barriers alternate by batch parity, so no wait
             // below can alias a later phase: the next commit to the barrier
@@ -238,34 +273,24 @@ k_conv_tc(const float *__restrict__ in, int ld_in, int cin, const int32_t *__res
                 const int j = issued - S::STAGES;
                 mbar_wait(&bar_done[j & 1], (j >> 1) & 1);
             }
-            if (tid == 0) {
-                const uint32_t bytes = (uint32_t)(2 * S::B_FLOATS * 4);
-                mbar_expect_tx(&bar_full[s], bytes);
-                tma_bulk_g2s(B_hi, wtc + (size_t)t * 2 * S::B_FLOATS, bytes, &bar_full[s]);
-            }
-            // gather my row of this tap, split into tf32 hi/lo, canonical layout
-            const float *x = src >= 0 ? in + (int64_t)src * ld_in : nullptr;
+            if (tid == 0 && (S::STAGES == 1 || item_issued == 0)) load_w(t, s);
+            // split my row of this tap into tf32 hi/lo, canonical layout
 #pragma unroll
             for (int c = 0; c < KP / 4; ++c) {
-                float v[4];
-#pragma unroll
-                for (int q = 0; q < 4; ++q) {
-                    int k = 4 * c + q;
-                    v[q] = (x && k < cin) ? __ldg(x + k) : 0.f;
-                }
                 float4 hi, lo;
-                hi.x = tf32_round(v[0]);
-                hi.y = tf32_round(v[1]);
-                hi.z = tf32_round(v[2]);
-                hi.w = tf32_round(v[3]);
-                lo.x = tf32_round(v[0] - hi.x);
-                lo.y = tf32_round(v[1] - hi.y);
-                lo.z = tf32_round(v[2] - hi.z);
-                lo.w = tf32_round(v[3] - hi.w);
+                hi.x = tf32_round(v[4 * c]);
+                hi.y = tf32_round(v[4 * c + 1]);
+                hi.z = tf32_round(v[4 * c + 2]);
+                hi.w = tf32_round(v[4 * c + 3]);
+                lo.x = tf32_round(v[4 * c] - hi.x);
+                lo.y = tf32_round(v[4 * c + 1] - hi.y);
+                lo.z = tf32_round(v[4 * c + 2] - hi.z);
+                lo.w = tf32_round(v[4 * c + 3] - hi.w);
                 const int off = core_off(tid, 4 * c, KP);
                 *reinterpret_cast<float4 *>(A_hi + off) = hi;
                 *reinterpret_cast<float4 *>(A_lo + off) = lo;
             }
+            if (mask) fetch(t0 + __ffs(mask) - 1);   // next tap's rows, in flight from here
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
             __syncthreads();   // also orders the last drain's TMEM reads before these MMAs
             if (tid == 0) {
@@ -289,6 +314,8 @@ k_conv_tc(const float *__restrict__ in, int ld_in, int cin, const int32_t *__res
                 mma_commit(&bar_done[issued & 1]);
             }
             if (item_issued > 0) drain(issued - 1);   // previous tap, overlapping this one's MMAs
+            if (S::STAGES == 2 && tid == 0 && mask)   // slot of batch issued-1 is free now
+                load_w(t0 + __ffs(mask) - 1, (issued + 1) & 1);
             ++issued;
             ++item_issued;
         }
@@ -385,6 +412,7 @@ void launch_tc(sfb_ctx *ctx, const NetLayer &L, const float *in, int ld_in, cons
 
 bool conv_tc_supported(const NetLayer &L) {
     if (L.kind != 0 && L.kind != 1) return false;   // conv, or transposed conv as an 8-tap map
+    if (choose_splits(1, L.taps, kSplitTarget) == 0) return false;   // > 32 taps per split
     int kp = pad_k(L.cin), np = pad_n(L.cout);
     if (L.cin > 128 || L.cout > 128) return false;
     size_t stage = (size_t)(2 * kM * kp + 2 * np * kp) * 4;

@@ -6,7 +6,12 @@ sass_csv, dis, fn = sys.argv[1:4]
 top = int(sys.argv[4]) if len(sys.argv) > 4 else 40
 rows = list(csv.reader(open(sass_csv)))
 hdr = rows[1]
-data = [r for r in rows[2:] if len(r) == len(hdr)]
+data = []
+for r in rows[2:]:   # first kernel of the page only
+    if r and r[0] == "Kernel Name":
+        break
+    if len(r) == len(hdr):
+        data.append(r)
 iA, iS, iW, iE = (hdr.index(k) for k in ("Address", "Source", "Warp Stall Sampling (All Samples)",
                                          "Instructions Executed"))
 base = int(data[0][iA], 16)
