@@ -509,7 +509,7 @@ int sfb_frame(sfb_ctx *ctx, const double *positions, const double *colors, int64
             G->net_mode = ctx->net_mode;
             G->net_epoch = ctx->net_epoch;
             std::copy(ptrs, ptrs + 6, G->ptrs);
-            if (ctx->graphs.size() >= 8) {
+            if (ctx->graphs.size() >= 32) {
                 delete ctx->graphs.front();
                 ctx->graphs.erase(ctx->graphs.begin());
             }

@@ -784,6 +784,7 @@ __global__ void __launch_bounds__(kCT, 4) k_composite(CompParams P) {
     __shared__ int32_t r_x0[kChunk], r_x1[kChunk], r_y0[kChunk], r_y1[kChunk], r_start[kChunk],
         r_count[kChunk];
     __shared__ uint8_t r_uni[kChunk];
+    __shared__ uint8_t r_full[kChunk];   // run's pixel box and circle cover the whole tile
 
     const int64_t t = blockIdx.x;
     const int64_t tx = t % P.ntx, ty = t / P.ntx;
@@ -925,6 +926,12 @@ __global__ void __launch_bounds__(kCT, 4) k_composite(CompParams P) {
                 r_x1[j] = (int32_t)fmax(fmin((double)(x_end - 1), floor(mx + rad)), (double)(x_lo - 1));
                 r_y0[j] = (int32_t)fmin(fmax((double)y_lo, ceil(my - rad)), (double)y_end);
                 r_y1[j] = (int32_t)fmax(fmin((double)(y_end - 1), floor(my + rad)), (double)(y_lo - 1));
+                // whole tile inside the box and the circle (farthest corner
+                // within the radius): the per-pixel tests are then all true
+                const double fx = fmax(fabs((double)x_lo - mx), fabs((double)(x_end - 1) - mx));
+                const double fy = fmax(fabs((double)y_lo - my), fabs((double)(y_end - 1) - my));
+                r_full[j] = r_x0[j] == x_lo && r_x1[j] == x_end - 1 && r_y0[j] == y_lo &&
+                            r_y1[j] == y_end - 1 && fx * fx + fy * fy <= rad * rad;
             }
             __syncthreads();
             for (int e = 0; e < nb; ++e) {
@@ -940,10 +947,12 @@ __global__ void __launch_bounds__(kCT, 4) k_composite(CompParams P) {
                 for (int k = 0; k < NPIX; ++k) {
                     if (!valid[k]) continue;
                     if (term && T[k] < kCutoff) continue;
-                    if (pxs[k] < r_x0[e] || pxs[k] > r_x1[e] || pys[k] < r_y0[e] || pys[k] > r_y1[e])
-                        continue;
                     const double dx = (double)pxs[k] - r_mx[e], dy = (double)pys[k] - r_my[e];
-                    if (dx * dx + dy * dy > r_rr[e]) continue;
+                    if (!r_full[e]) {
+                        if (pxs[k] < r_x0[e] || pxs[k] > r_x1[e] || pys[k] < r_y0[e] || pys[k] > r_y1[e])
+                            continue;
+                        if (dx * dx + dy * dy > r_rr[e]) continue;
+                    }
                     const double q = r_ia[e] * dx * dx + 2.0 * r_ib[e] * dx * dy + r_ic[e] * dy * dy;
                     double alpha = r_op[e] * exp(-0.5 * q);
                     if (alpha > alpha_max) alpha = alpha_max;

@@ -19,6 +19,51 @@ from .rasterizer import _PLANE_BIT, FrameBuffer, RenderOptions, _alloc_planes
 from .sparsenet import ensure_loaded
 from .voxelgrid import device_bbox, lattice_scale, stage_cloud
 
+# Host clouds are uploaded on a dedicated stream (one per device) into
+# persistent per-lane staging buffers (two per lane, alternating), with their
+# own library context (own scratch arena) for the bbox: the copy of frame i
+# waits only for earlier uploads and for the frame that last used its staging
+# buffer — not for everything queued on the lane — and the one host round
+# trip per frame (the 48-byte bbox read-back that gives the bit-exact lattice
+# scale) waits only for the positions copy. Fixed staging addresses also keep
+# the lane's CUDA-graph cache hot (the frame graph is keyed by pointers).
+_UPLOAD_LANE = 1 << 16
+_upload_streams = {}
+_staging = {}   # (device, lane) -> {"k": next buffer, "bufs": [[pos, col, done_event], ...]}
+
+
+def _upload(cloud: PointCloud, lane: int):
+    dev = torch.cuda.current_device()
+    up = _upload_streams.get(dev)
+    if up is None:
+        up = _upload_streams[dev] = torch.cuda.Stream(device=dev)
+    st = _staging.setdefault((dev, lane), {"k": 0, "bufs": [[None, None, None], [None, None, None]]})
+    slot = st["bufs"][st["k"]]
+    st["k"] ^= 1
+    n = int(cloud.positions.shape[0])
+    if slot[0] is None or slot[0].shape[0] < n:
+        slot[0] = torch.empty((n, 3), dtype=torch.float64, device=dev)
+        slot[1] = torch.empty((n, 3), dtype=torch.float64, device=dev)
+    pos, col = slot[0][:n], slot[1][:n]
+    cur = torch.cuda.current_stream(dev)
+    up.wait_stream(cur)   # inputs the caller just wrote on its stream
+    if slot[2] is not None:
+        up.wait_event(slot[2])   # the frame that last read this staging buffer
+
+    def host(a):
+        if isinstance(a, torch.Tensor):
+            return a
+        return torch.from_numpy(np.ascontiguousarray(a))
+    with torch.cuda.stream(up):
+        hp = host(cloud.positions)
+        pos.copy_(hp, non_blocking=hp.is_pinned())
+        lo_hi = device_bbox(pos, _UPLOAD_LANE + lane)
+        hc = host(cloud.colors)
+        col.copy_(hc, non_blocking=hc.is_pinned())
+        ev = up.record_event()
+    cur.wait_event(ev)
+    return pos, col, lo_hi, slot
+
 
 def render_frame(cloud: PointCloud, weights: NetworkWeights, cam: Camera,
                  planes=("rgb", "normal"), background=(0.0, 0.0, 0.0),
@@ -28,9 +73,13 @@ def render_frame(cloud: PointCloud, weights: NetworkWeights, cam: Camera,
     different torch streams and they overlap on the GPU."""
     ctx = ensure_loaded(weights, lane)
     options = options or RenderOptions()
-    pos, col = stage_cloud(cloud)
+    slot = None
+    if cloud.on_device:
+        pos, col = stage_cloud(cloud)
+        lo_hi = device_bbox(pos, lane)
+    else:
+        pos, col, lo_hi, slot = _upload(cloud, lane)
     n = int(pos.shape[0])
-    lo_hi = device_bbox(pos, lane)
     s = lattice_scale(n, lo_hi)
     bg = np.ascontiguousarray(np.asarray(background, dtype=np.float64).reshape(3))
     rgb, nrm, dep, trans = out if out is not None else _alloc_planes(cam, planes, pos.device)
@@ -41,6 +90,8 @@ def render_frame(cloud: PointCloud, weights: NetworkWeights, cam: Camera,
     ctx.call("sfb_frame", _lib.ptr(pos), _lib.ptr(col), n, s, lo_hi.ctypes.data_as(_lib.P),
              _lib.ctypes.byref(c), _lib.ctypes.byref(o), mask, bg.ctypes.data_as(_lib.P),
              _lib.ptr(rgb), _lib.ptr(nrm), _lib.ptr(dep), _lib.ptr(trans))
+    if slot is not None:   # the staging buffer is free once this frame is done
+        slot[2] = torch.cuda.current_stream().record_event()
     if rgb is None:
         rgb = torch.zeros((int(cam.height), int(cam.width), 3), dtype=torch.float32,
                           device=pos.device)

@@ -5,14 +5,14 @@ tag=${1:-r01}
 mkdir -p gpurun_out
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm --format=csv > gpurun_out/smi.txt 2>&1
 nproc > gpurun_out/nproc.txt
-timeout 900 python -m pytest tests -m gpu -x -q > gpurun_out/gpu_tests_$tag.log 2>&1
+timeout 900 python -m pytest tests -m gpu -x -q --timeout 240 > gpurun_out/gpu_tests_$tag.log 2>&1
 echo "pytest rc=$?" >> gpurun_out/gpu_tests_$tag.log
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke_$tag.log 2>&1
 echo "smoke rc=$?" >> gpurun_out/smoke_$tag.log
 timeout 900 python bench.py > gpurun_out/bench_$tag.json 2> gpurun_out/bench_$tag.err
 echo "bench rc=$?" >> gpurun_out/bench_$tag.err
 timeout 600 python bench.py --impl reference --steps 1 --warmup 0 > gpurun_out/bench_ref_$tag.json 2> gpurun_out/bench_ref_$tag.err
-timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv \
+timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --cache-control none -c 400 --csv \
   --log-file gpurun_out/launches_$tag.csv python bench.py --steps 2 --warmup 1 --lanes 1 \
   --no-e2e --no-cpu --no-profile > gpurun_out/ncu_$tag.log 2>&1
 echo "ncu launches rc=$?" >> gpurun_out/ncu_$tag.log
