@@ -179,6 +179,24 @@ int sfb_prepare_debug(sfb_ctx *ctx, const sfb_splats *splats, const sfb_camera *
                       int32_t tile_size, int64_t *source, double *radius, int64_t *offsets,
                       int64_t *ids, int64_t ids_capacity, int64_t *k_host, int64_t *e_host);
 
+/* ---- render_pose epilogue (service.py:116-136, rasterizer.py:209-226) ------ */
+/* RGBA8 output of service.render_pose: mode rgb -> to_rgba(rgb, T); normal ->
+ * to_rgba(normal*0.5+0.5, T); relit -> to_rgba(relight(normal, rgb, light,
+ * ambient, diffuse), T), the relit rgb and normal planes from ONE compositing
+ * pass. Quantisation as to_rgba: clip(rint(v*255), 0, 255), alpha from
+ * coverage 1-T; computed from the float64 accumulators. */
+enum { SFB_MODE_RGB = 0, SFB_MODE_NORMAL = 1, SFB_MODE_RELIT = 2 };
+typedef struct {
+    int32_t mode;       /* SFB_MODE_* (service.py MODE_CODES) */
+    double light[3];    /* unit light direction (relit) */
+    double ambient, diffuse;
+} sfb_shading;
+
+/* render_pose on a Splats batch: rgba (H,W,4) uint8, device. */
+int sfb_render_rgba(sfb_ctx *ctx, const sfb_splats *splats, const sfb_camera *cam,
+                    const sfb_render_options *opts, const sfb_shading *shading,
+                    const double *background3, uint8_t *rgba);
+
 /* ---- fused frame: cloud -> P2ENet -> splat, no per-point splats ---------- */
 /* The bench hot path: voxelize, UNet, head, then render the per-voxel
  * Gaussians broadcast to their points (colours per point) straight to planes. */
@@ -186,6 +204,13 @@ int sfb_frame(sfb_ctx *ctx, const double *positions, const double *colors, int64
               const double *lo_hi_host, const sfb_camera *cam, const sfb_render_options *opts,
               int32_t plane_mask, const double *background3, float *rgb, float *normal,
               float *depth, float *trans);
+
+/* The fused frame straight to RGBA8 (render_pose of the estimated splats):
+ * the streaming path of service.py, 4 bytes per pixel instead of 28. */
+int sfb_frame_rgba(sfb_ctx *ctx, const double *positions, const double *colors, int64_t n,
+                   double s, const double *lo_hi_host, const sfb_camera *cam,
+                   const sfb_render_options *opts, const sfb_shading *shading,
+                   const double *background3, uint8_t *rgba);
 
 #ifdef __cplusplus
 }

@@ -41,6 +41,10 @@ class Splats_t(ctypes.Structure):
                 ("colors", P), ("normals", P), ("n", I64)]
 
 
+class Shading_t(ctypes.Structure):
+    _fields_ = [("mode", I32), ("light", D * 3), ("ambient", D), ("diffuse", D)]
+
+
 class Stats_t(ctypes.Structure):
     _fields_ = [("kept", I64), ("runs", I64), ("fine_entries", I64), ("super_entries", I64),
                 ("global_entries", I64), ("voxels", I64 * 8)]
@@ -78,6 +82,10 @@ SIGNATURES = {
                           I64, ctypes.POINTER(I64), ctypes.POINTER(I64)],
     "sfb_frame": [P, P, P, I64, D, P, ctypes.POINTER(Camera_t), ctypes.POINTER(RenderOptions_t),
                   I32, P, P, P, P, P],
+    "sfb_render_rgba": [P, ctypes.POINTER(Splats_t), ctypes.POINTER(Camera_t),
+                        ctypes.POINTER(RenderOptions_t), ctypes.POINTER(Shading_t), P, P],
+    "sfb_frame_rgba": [P, P, P, I64, D, P, ctypes.POINTER(Camera_t),
+                       ctypes.POINTER(RenderOptions_t), ctypes.POINTER(Shading_t), P, P],
 }
 
 _lib = None

@@ -9,6 +9,7 @@
 // calls update the parameter kernel node (lattice scale, key layout, camera,
 // background) and launch the graph.
 #include <algorithm>
+#include <cmath>
 
 #include "common.cuh"
 
@@ -141,7 +142,7 @@ RenderInputs splat_inputs(const sfb_splats *s) {
 void enqueue_frame(sfb_ctx *ctx, const double *pos, const double *col, int64_t n,
                    const FrameParams &host, FrameParams *P, const sfb_camera *cam,
                    const sfb_render_options *opts, int mask, float *rgb, float *normal,
-                   float *depth, float *trans) {
+                   float *depth, float *trans, uint8_t *rgba) {
     write_params(ctx, host, P);
     DevCounts *C = new_counts(ctx);
     VoxelSplats V = neural_voxels(ctx, pos, col, n, host, P, C);
@@ -158,7 +159,26 @@ void enqueue_frame(sfb_ctx *ctx, const double *pos, const double *col, int64_t n
     in.colors = col;
     in.normals = V.n;
     in.n_points = n;
-    render_run(ctx, in, P, cam->width, cam->height, *opts, mask, C, rgb, normal, depth, trans);
+    render_run(ctx, in, P, cam->width, cam->height, *opts, mask, C, rgb, normal, depth, trans, rgba);
+}
+
+// render_pose shading into the frame parameters; returns the plane mask the
+// compositor must accumulate for the mode
+int apply_shading(FrameParams &P, const sfb_shading *sh) {
+    SFB_REQUIRE(sh, "null shading");
+    SFB_REQUIRE(sh->mode == SFB_MODE_RGB || sh->mode == SFB_MODE_NORMAL || sh->mode == SFB_MODE_RELIT,
+                "unknown render_pose mode");
+    P.shade_mode = sh->mode;
+    for (int a = 0; a < 3; ++a) P.light[a] = sh->light[a];
+    P.ambient = sh->ambient;
+    P.diffuse = sh->diffuse;
+    if (sh->mode == SFB_MODE_RELIT) {
+        const double l2 = sh->light[0] * sh->light[0] + sh->light[1] * sh->light[1] +
+                          sh->light[2] * sh->light[2];
+        SFB_REQUIRE(std::fabs(std::sqrt(l2) - 1.0) <= 1e-6, "light_dir must be unit length");
+    }
+    return sh->mode == SFB_MODE_RGB ? SFB_PLANE_RGB
+           : sh->mode == SFB_MODE_NORMAL ? SFB_PLANE_NORMAL : (SFB_PLANE_RGB | SFB_PLANE_NORMAL);
 }
 
 }  // namespace
@@ -168,7 +188,7 @@ struct sfb_frame_graph {
     int64_t n;
     int32_t width, height, tile, terminate, mask, key_bits;
     double alpha_max;
-    const void *ptrs[6];
+    const void *ptrs[7];
     int net_mode;
     uint64_t net_epoch;
     int seen = 0;                     // eager runs with this key
@@ -448,6 +468,20 @@ int sfb_render(sfb_ctx *ctx, const sfb_splats *splats, const sfb_camera *cam,
     });
 }
 
+int sfb_render_rgba(sfb_ctx *ctx, const sfb_splats *splats, const sfb_camera *cam,
+                    const sfb_render_options *opts, const sfb_shading *shading, const double *bg,
+                    uint8_t *rgba) {
+    return guard(ctx, [&] {
+        SFB_REQUIRE(splats && cam && opts && rgba, "null argument");
+        FrameParams host = camera_params(cam, bg);
+        const int mask = apply_shading(host, shading);
+        FrameParams *P = params(ctx, host);
+        DevCounts *C = new_counts(ctx);
+        render_run(ctx, splat_inputs(splats), P, cam->width, cam->height, *opts, mask, C, nullptr,
+                   nullptr, nullptr, nullptr, rgba);
+    });
+}
+
 int sfb_project(sfb_ctx *ctx, const sfb_splats *s, const sfb_camera *cam, double z_near,
                 double dilation, double *sx, double *sy, double *depth, double *ca, double *cb,
                 double *cc, double *radius, uint8_t *keep) {
@@ -470,31 +504,33 @@ int sfb_prepare_debug(sfb_ctx *ctx, const sfb_splats *s, const sfb_camera *cam, 
     });
 }
 
-int sfb_frame(sfb_ctx *ctx, const double *positions, const double *colors, int64_t n, double s,
-              const double *lo_hi_host, const sfb_camera *cam, const sfb_render_options *opts,
-              int32_t plane_mask, const double *bg, float *rgb, float *normal, float *depth,
-              float *trans) {
+static int frame_impl(sfb_ctx *ctx, const double *positions, const double *colors, int64_t n,
+                      double s, const double *lo_hi_host, const sfb_camera *cam,
+                      const sfb_render_options *opts, int32_t plane_mask, const double *bg,
+                      float *rgb, float *normal, float *depth, float *trans, uint8_t *rgba,
+                      const sfb_shading *shading) {
     return guard(ctx, [&] {
         SFB_REQUIRE(cam && opts, "null argument");
         SFB_REQUIRE(n >= 2, "voxelization needs at least 2 points");
         FrameParams host = camera_params(cam, bg);
+        if (rgba) plane_mask = apply_shading(host, shading);
         voxel_layout(lo_hi_host, s, host);
         const int key_bits = host.total <= 32 ? ((host.total + 7) / 8) * 8 : 64;
         if (!ctx->use_graphs || ctx->timing) {
             FrameParams *P = ctx->arena.alloc<FrameParams>(1);
             enqueue_frame(ctx, positions, colors, n, host, P, cam, opts, plane_mask, rgb, normal,
-                          depth, trans);
+                          depth, trans, rgba);
             return;
         }
         // ---- graph path: find / build the graph of this shape
         sfb_frame_graph *G = nullptr;
-        const void *ptrs[6] = {positions, colors, rgb, normal, depth, trans};
+        const void *ptrs[7] = {positions, colors, rgb, normal, depth, trans, rgba};
         for (auto *g : ctx->graphs)
             if (g->n == n && g->width == cam->width && g->height == cam->height &&
                 g->tile == opts->tile_size && g->terminate == opts->early_termination &&
                 g->alpha_max == opts->alpha_max && g->mask == plane_mask && g->key_bits == key_bits &&
                 g->net_mode == ctx->net_mode && g->net_epoch == ctx->net_epoch &&
-                std::equal(ptrs, ptrs + 6, g->ptrs))
+                std::equal(ptrs, ptrs + 7, g->ptrs))
                 G = g;
         if (!G) {
             G = new sfb_frame_graph();
@@ -508,7 +544,7 @@ int sfb_frame(sfb_ctx *ctx, const double *positions, const double *colors, int64
             G->key_bits = key_bits;
             G->net_mode = ctx->net_mode;
             G->net_epoch = ctx->net_epoch;
-            std::copy(ptrs, ptrs + 6, G->ptrs);
+            std::copy(ptrs, ptrs + 7, G->ptrs);
             if (ctx->graphs.size() >= 32) {
                 delete ctx->graphs.front();
                 ctx->graphs.erase(ctx->graphs.begin());
@@ -519,7 +555,7 @@ int sfb_frame(sfb_ctx *ctx, const double *positions, const double *colors, int64
             // first call of this shape: eager run (grows the arena, sets kernel attributes)
             FrameParams *P = ctx->arena.alloc<FrameParams>(1);
             enqueue_frame(ctx, positions, colors, n, host, P, cam, opts, plane_mask, rgb, normal,
-                          depth, trans);
+                          depth, trans, rgba);
             G->seen = 1;
             // size hints for the capture (grids only; kernels loop over device counts)
             DevCounts c{};
@@ -542,7 +578,7 @@ int sfb_frame(sfb_ctx *ctx, const double *positions, const double *colors, int64
             SFB_CUDA(cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeThreadLocal));
             try {
                 enqueue_frame(ctx, positions, colors, n, host, P, cam, opts, plane_mask, rgb,
-                              normal, depth, trans);
+                              normal, depth, trans, rgba);
             } catch (...) {
                 cudaGraph_t junk = nullptr;
                 cudaStreamEndCapture(ctx->stream, &junk);
@@ -584,6 +620,23 @@ int sfb_frame(sfb_ctx *ctx, const double *positions, const double *colors, int64
         SFB_CUDA(cudaGraphExecKernelNodeSetParams(G->exec, G->param_node, &kp));
         SFB_CUDA(cudaGraphLaunch(G->exec, ctx->stream));
     });
+}
+
+int sfb_frame(sfb_ctx *ctx, const double *positions, const double *colors, int64_t n, double s,
+              const double *lo_hi_host, const sfb_camera *cam, const sfb_render_options *opts,
+              int32_t plane_mask, const double *bg, float *rgb, float *normal, float *depth,
+              float *trans) {
+    return frame_impl(ctx, positions, colors, n, s, lo_hi_host, cam, opts, plane_mask, bg, rgb,
+                      normal, depth, trans, nullptr, nullptr);
+}
+
+int sfb_frame_rgba(sfb_ctx *ctx, const double *positions, const double *colors, int64_t n,
+                   double s, const double *lo_hi_host, const sfb_camera *cam,
+                   const sfb_render_options *opts, const sfb_shading *shading, const double *bg,
+                   uint8_t *rgba) {
+    if (!rgba) return SFB_ERR_ARG;
+    return frame_impl(ctx, positions, colors, n, s, lo_hi_host, cam, opts, 0, bg, nullptr, nullptr,
+                      nullptr, nullptr, rgba, shading);
 }
 
 }  // extern "C"

@@ -255,6 +255,9 @@ struct FrameParams {
     int32_t total;
     Cam cam;
     double bg[3];
+    // render_pose epilogue (RGBA8 output): mode, light, ambient, diffuse
+    int32_t shade_mode;
+    double light[3], ambient, diffuse;
 };
 
 // devprims.cu
@@ -357,7 +360,7 @@ struct RenderInputs {
 };
 void render_run(sfb_ctx *ctx, const RenderInputs &in, const FrameParams *FP, int64_t width,
                 int64_t height, const sfb_render_options &opts, int plane_mask, DevCounts *C,
-                float *rgb, float *normal, float *depth, float *trans);
+                float *rgb, float *normal, float *depth, float *trans, uint8_t *rgba = nullptr);
 void project_run(sfb_ctx *ctx, const double *centers, const double *quats, const double *scales,
                  const int64_t *d_n, int64_t n_bound, const FrameParams *FP, double z_near,
                  double dilation, double *sx, double *sy, double *depth, double *ca, double *cb,

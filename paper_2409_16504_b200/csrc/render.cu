@@ -718,6 +718,7 @@ struct CompParams {
     const float4 *snrm;   // normals of per-point geometry (runs with mixed normals)
     // outputs
     float *rgb, *normal, *depth, *trans;
+    uint8_t *rgba;   // render_pose RGBA8 (FrameParams shading), or null
     int64_t *dbg;   // optional per-tile counters: windows, list entries, alpha evals, point blends
 };
 
@@ -1024,6 +1025,41 @@ __global__ void __launch_bounds__(kCT, 4) k_composite(CompParams P) {
     for (int k = 0; k < NPIX; ++k) {
         if (!valid[k]) continue;
         const int64_t pix = (int64_t)pys[k] * P.W + pxs[k];
+        if (P.rgba) {   // service.py:116-136 render_pose + to_rgba (+ relight)
+            const FrameParams &F = *P.fp;
+            const double tc = fmin(fmax(T[k], 0.0), 1.0);
+            double v[3];
+            if (F.shade_mode == SFB_MODE_RGB || F.shade_mode == SFB_MODE_RELIT) {
+                v[0] = c0[k] + T[k] * bgc[0];
+                v[1] = c1[k] + T[k] * bgc[1];
+                v[2] = c2[k] + T[k] * bgc[2];
+            }
+            if (F.shade_mode != SFB_MODE_RGB) {
+                const double nrm = sqrt(n0[k] * n0[k] + n1[k] * n1[k] + n2[k] * n2[k]);
+                const bool z = !(nrm > 0.0);
+                const double u0 = z ? 0.0 : n0[k] / nrm, u1 = z ? 0.0 : n1[k] / nrm,
+                             u2 = z ? 0.0 : n2[k] / nrm;
+                if (F.shade_mode == SFB_MODE_NORMAL) {
+                    v[0] = u0 * 0.5 + 0.5;
+                    v[1] = u1 * 0.5 + 0.5;
+                    v[2] = u2 * 0.5 + 0.5;
+                } else if (!(tc > 0.999)) {   // relight (rasterizer.py:209-226)
+                    const double lam = fmax(u0 * F.light[0] + u1 * F.light[1] + u2 * F.light[2], 0.0);
+                    const double g = F.ambient + F.diffuse * lam;
+#pragma unroll
+                    for (int a = 0; a < 3; ++a) v[a] = fmin(fmax(v[a] * g, 0.0), 1.0);
+                } else {
+#pragma unroll
+                    for (int a = 0; a < 3; ++a) v[a] = fmin(fmax(v[a], 0.0), 1.0);
+                }
+            }
+            uchar4 q;
+            q.x = (unsigned char)fmin(fmax(rint(v[0] * 255.0), 0.0), 255.0);
+            q.y = (unsigned char)fmin(fmax(rint(v[1] * 255.0), 0.0), 255.0);
+            q.z = (unsigned char)fmin(fmax(rint(v[2] * 255.0), 0.0), 255.0);
+            q.w = (unsigned char)fmin(fmax(rint((1.0 - tc) * 255.0), 0.0), 255.0);
+            reinterpret_cast<uchar4 *>(P.rgba)[pix] = q;
+        }
         if (P.rgb) {
             P.rgb[3 * pix + 0] = (float)(c0[k] + T[k] * bgc[0]);
             P.rgb[3 * pix + 1] = (float)(c1[k] + T[k] * bgc[1]);
@@ -1089,7 +1125,7 @@ static void voxel_order(sfb_ctx *ctx, const RenderInputs &in, const Proj &P, Dev
 // stays on the device; buffers are sized from host bounds.
 void render_run(sfb_ctx *ctx, const RenderInputs &in, const FrameParams *FP, int64_t width,
                 int64_t height, const sfb_render_options &opts, int plane_mask, DevCounts *C,
-                float *rgb, float *normal, float *depth, float *trans) {
+                float *rgb, float *normal, float *depth, float *trans, uint8_t *rgba) {
     SFB_REQUIRE(width >= 1 && height >= 1, "image must have positive dimensions");
     SFB_REQUIRE(opts.tile_size >= 1 && opts.tile_size <= 32, "tile_size must be in [1, 32]");
     cudaStream_t st = ctx->stream;
@@ -1230,6 +1266,7 @@ void render_run(sfb_ctx *ctx, const RenderInputs &in, const FrameParams *FP, int
     CP.normal = (plane_mask & SFB_PLANE_NORMAL) ? normal : nullptr;
     CP.depth = (plane_mask & SFB_PLANE_DEPTH) ? depth : nullptr;
     CP.trans = trans;
+    CP.rgba = rgba;
     CP.dbg = ctx->debug_counters;
     if (TS * TS <= kCT) k_composite<1><<<(unsigned)nt, kCT, 0, st>>>(CP);
     else k_composite<4><<<(unsigned)nt, kCT, 0, st>>>(CP);

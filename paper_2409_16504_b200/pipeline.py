@@ -65,6 +65,20 @@ def _upload(cloud: PointCloud, lane: int):
     return pos, col, lo_hi, slot
 
 
+def prepare_cloud(cloud: PointCloud, lane: int = 0):
+    """Device positions/colours, point count, lattice scale and bbox of a cloud
+    (host clouds go through the upload stream); ``slot`` is the staging buffer
+    whose done-event the caller records after its frame (None for device clouds)."""
+    slot = None
+    if cloud.on_device:
+        pos, col = stage_cloud(cloud)
+        lo_hi = device_bbox(pos, lane)
+    else:
+        pos, col, lo_hi, slot = _upload(cloud, lane)
+    n = int(pos.shape[0])
+    return pos, col, n, lattice_scale(n, lo_hi), lo_hi, slot
+
+
 def render_frame(cloud: PointCloud, weights: NetworkWeights, cam: Camera,
                  planes=("rgb", "normal"), background=(0.0, 0.0, 0.0),
                  options: RenderOptions = None, out=None, lane: int = 0) -> FrameBuffer:
@@ -73,14 +87,7 @@ def render_frame(cloud: PointCloud, weights: NetworkWeights, cam: Camera,
     different torch streams and they overlap on the GPU."""
     ctx = ensure_loaded(weights, lane)
     options = options or RenderOptions()
-    slot = None
-    if cloud.on_device:
-        pos, col = stage_cloud(cloud)
-        lo_hi = device_bbox(pos, lane)
-    else:
-        pos, col, lo_hi, slot = _upload(cloud, lane)
-    n = int(pos.shape[0])
-    s = lattice_scale(n, lo_hi)
+    pos, col, n, s, lo_hi, slot = prepare_cloud(cloud, lane)
     bg = np.ascontiguousarray(np.asarray(background, dtype=np.float64).reshape(3))
     rgb, nrm, dep, trans = out if out is not None else _alloc_planes(cam, planes, pos.device)
     mask = 0
