@@ -192,6 +192,7 @@ def run_ours(args):
     from paper_2409_16504_b200.gaussians import Camera
     from paper_2409_16504_b200.pcio import PointCloud
     from paper_2409_16504_b200.pipeline import render_frame, stats
+    from paper_2409_16504_b200.service import CameraPose, render_pose_frame
 
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -209,6 +210,7 @@ def run_ours(args):
 
     cloud, views = workload(args.config)
     cams = [Camera.of(v) for v in views]
+    poses = [CameraPose(c, "relit") for c in cams]   # render_pose requests (headlight)
     weights = netplan.init_random(netplan.NetworkPlan(), 0)
     W, H = cams[0].width, cams[0].height
     planes = ("rgb", "normal")
@@ -232,10 +234,17 @@ def run_ours(args):
     def view_of(i):   # views round-robin over ranks
         return cams[unit_of(i, rank, world, len(cams))]
 
+    rgba_out = None   # render_pose leg: one RGBA8 device frame per (lane, input copy)
+
     def issue(i, cloud_list, host_out=None):
         lane = i % lanes
         k = i % copies
         with torch.cuda.stream(streams[lane]):
+            if rgba_out is not None:   # service.render_pose streaming path (relit, RGBA8)
+                fr = render_pose_frame(cloud_list[k], weights, poses[unit_of(i, rank, world, len(cams))],
+                                       out=rgba_out[lane][k], lane=lane)
+                host_out[lane][0].copy_(fr, non_blocking=True)
+                return fr
             fb = render_frame(cloud_list[k], weights, view_of(i), planes, out=outs[lane][k],
                               lane=lane)
             if host_out is not None:
@@ -330,6 +339,21 @@ def run_ours(args):
         e2e = {"value": world * args.steps / (ms2 / 1e3), "unit": UNIT,
                "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
                "ms_per_step": ms2 / args.steps}
+        # the streaming caller (service.render_pose, mode relit): same host
+        # clouds in, one RGBA8 frame out per step (4 bytes/px instead of 28)
+        rgba_out = [[torch.empty((H, W, 4), dtype=torch.uint8, device="cuda")
+                     for _ in range(copies)] for _ in range(lanes)]
+        host_rgba = [[torch.empty((H, W, 4), dtype=torch.uint8).pin_memory()] for _ in range(lanes)]
+        for _ in range(6):
+            run_batch(lanes * copies, host_clouds, host_rgba)
+        barrier()
+        ms3, _ = run_batch(args.steps, host_clouds, host_rgba)
+        barrier()
+        ms3 = max_over_ranks(ms3)
+        e2e["render_pose_relit_rgba8"] = {
+            "value": world * args.steps / (ms3 / 1e3), "unit": UNIT, "h2d_bytes_per_step": int(h2d),
+            "d2h_bytes_per_step": int(host_rgba[0][0].nbytes), "ms_per_step": ms3 / args.steps}
+        rgba_out = None
 
     # ---- kernel launches of one frame (CUPTI via torch.profiler, outside the timed region)
     launches = None

@@ -63,6 +63,28 @@ class PoseMessage:
                       self.fx, self.fy, self.width / 2.0, self.height / 2.0, self.width, self.height)
 
 
+@dataclass(frozen=True, eq=False)
+class CameraPose:
+    """A render_pose request whose camera is given as a Camera (e.g. a ring
+    view built with look_at) rather than a quaternion + focal lengths."""
+
+    cam: Camera
+    mode: str = "rgb"
+    light_dir: tuple = None
+    sequence: int = 0
+
+    @property
+    def width(self) -> int:
+        return int(self.cam.width)
+
+    @property
+    def height(self) -> int:
+        return int(self.cam.height)
+
+    def camera(self) -> Camera:
+        return self.cam
+
+
 def _shading(mode: str, light_dir, ambient: float, diffuse: float) -> _lib.Shading_t:
     if mode not in MODE_CODES:
         raise ValueError(f"unknown mode {mode!r}; expected one of {tuple(MODE_CODES)}")

@@ -21,16 +21,10 @@ pytestmark = pytest.mark.gpu
 KEYS = ("centers", "scales", "quaternions", "opacities", "colors", "normals")
 
 
-class FixedPose:
+def FixedPose(cam, mode, light=None):
     """A pose whose camera is given directly (the KAT records the matrix)."""
-
-    def __init__(self, cam, mode, light=None):
-        self._cam, self.mode, self.light_dir = cam, mode, light
-        self.width, self.height = cam.width, cam.height
-
-    def camera(self):
-        from paper_2409_16504_b200.gaussians import Camera
-        return Camera.of(self._cam)
+    from paper_2409_16504_b200.gaussians import Camera
+    return service.CameraPose(Camera.of(cam), mode, light)
 
 
 def lsb_close(got, want, frac=1e-3):
