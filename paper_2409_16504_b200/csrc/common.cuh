@@ -291,8 +291,18 @@ void pool_build(sfb_ctx *ctx, const int32_t *coords, const int64_t *d_m, int64_t
                 int c, int ld_in, int32_t *parent_coords, float *parent_feats, int ld_out,
                 int32_t *child_to_parent, int64_t *d_mp);
 void coords_layout(sfb_ctx *ctx, const int32_t *coords, int64_t m, FrameParams &P);
+// children of a level grouped by their tap under the parent, each bucket
+// padded to whole 128-row tiles (the tap-bucketed transposed conv)
+struct TapBuckets {
+    int32_t *perm;       // padded row -> child row (-1 pad)
+    int32_t *src;        // padded row -> parent row (-1 pad)
+    int32_t *off;        // 9 padded bucket offsets (device)
+    int64_t *d_rows;     // padded row count (device)
+    int64_t rows_bound, rows_grid;
+};
 // fused UNet pooling, split: coordinate structure (side stream) + means
 struct PoolStructure {
+    TapBuckets buckets;
     HashTable table;        // parent key -> parent row (the coarse level's hash)
     int32_t *c2p, *tap;     // per child: parent row, tap under the parent
     int32_t *tmap;          // (8, m) tap-major map of the transposed conv
@@ -335,7 +345,7 @@ void conv_layer(sfb_ctx *ctx, const NetLayer &L, const float *in, int ld_in, con
 void tconv_layer(sfb_ctx *ctx, const NetLayer &L, const float *in, int ld_in,
                  const int32_t *parent, const int32_t *tap, const int64_t *d_m, int64_t m_bound,
                  int relu, float *out, int ld_out, int64_t m_grid = -1,
-                 const int32_t *tmap = nullptr);
+                 const int32_t *tmap = nullptr, const struct TapBuckets *tb = nullptr);
 void layer_set(sfb_ctx *ctx, int kind, int kernel, int cin, int cout, const float *w_host,
                const float *b_host);
 // per-voxel Gaussians for the fused frame: centres, sigma, quat, opacity, normal

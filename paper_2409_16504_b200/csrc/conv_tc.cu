@@ -159,7 +159,12 @@ __global__ void __launch_bounds__(kThreadsTC)
 k_conv_tc(const float *__restrict__ in, int ld_in, int cin, const int32_t *__restrict__ nbr,
           int64_t nbr_ld, const int64_t *__restrict__ d_m, int64_t m_fixed, int taps,
           const float *__restrict__ wtc, const float *__restrict__ bias, int cout, int relu,
-          float *__restrict__ out, int ld_out, float *__restrict__ partial) {
+          float *__restrict__ out, int ld_out, float *__restrict__ partial,
+          const int32_t *__restrict__ row_map, const int32_t *__restrict__ tap_off) {
+    // tap-bucketed mode (transposed conv, tap_off != null): rows arrive grouped
+    // by tap, each bucket padded to whole 128-row tiles (tap_off = 9 padded
+    // offsets), nbr[row] is the row's parent (-1 pad), row_map[row] its output
+    // row; every tile is ONE tap (K = Cin), so no split-K is needed
     using S = TcShape<KP, NP>;
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     float *stage_base = reinterpret_cast<float *>(
@@ -171,7 +176,7 @@ k_conv_tc(const float *__restrict__ in, int ld_in, int cin, const int32_t *__res
     const int tid = threadIdx.x, warp = tid >> 5;
     const int64_t m = d_m ? *d_m : m_fixed;
     const int64_t tiles = (m + kM - 1) / kM;
-    const int splits = choose_splits(tiles, taps, kSplitTarget);
+    const int splits = tap_off ? 1 : choose_splits(tiles, taps, kSplitTarget);
     const int tps = (taps + splits - 1) / splits;
     const int64_t work = tiles * splits;
     if ((int64_t)blockIdx.x >= work) return;   // uniform per CTA, before any collective
@@ -220,7 +225,13 @@ k_conv_tc(const float *__restrict__ in, int ld_in, int cin, const int32_t *__res
     for (int64_t wi = blockIdx.x; wi < work; wi += gridDim.x) {
         const int64_t row0 = (wi / splits) * kM;
         const int split = (int)(wi % splits);
-        const int t0 = split * tps, t1 = min(taps, t0 + tps);
+        int t0 = split * tps, t1 = min(taps, t0 + tps);
+        if (tap_off) {   // the bucket of this tile
+            int tb = 0;
+            while (tb < 7 && row0 >= tap_off[tb + 1]) ++tb;
+            t0 = tb;
+            t1 = tb + 1;
+        }
         const int64_t row = row0 + tid;
 #pragma unroll
         for (int c = 0; c < NP; ++c) acc[c] = 0.f;
@@ -228,7 +239,7 @@ k_conv_tc(const float *__restrict__ in, int ld_in, int cin, const int32_t *__res
         // coalesced loads) and OR the per-tap occupancy over the tile
         uint32_t mymask = 0;
         for (int t = t0; t < t1; ++t) {
-            const int32_t src = row < m ? nbr[(int64_t)t * nbr_ld + row] : -1;
+            const int32_t src = row < m ? nbr[(tap_off ? 0 : (int64_t)t * nbr_ld) + row] : -1;
             s_src[t - t0][tid] = src;
             mymask |= (src >= 0 ? 1u : 0u) << (t - t0);
         }
@@ -327,13 +338,16 @@ k_conv_tc(const float *__restrict__ in, int ld_in, int cin, const int32_t *__res
                 for (int c = 0; c < NP; c += 4)
                     *reinterpret_cast<float4 *>(p + c) = make_float4(acc[c], acc[c + 1], acc[c + 2], acc[c + 3]);
             } else {
-                float *o = out + row * (int64_t)ld_out;
+                const int64_t orow = row_map ? (int64_t)row_map[row] : row;
+                if (orow >= 0) {
+                    float *o = out + orow * (int64_t)ld_out;
 #pragma unroll
-                for (int c = 0; c < NP; ++c)
-                    if (c < cout) {
-                        float v = acc[c] + bias[c];
-                        o[c] = relu ? fmaxf(v, 0.f) : v;
-                    }
+                    for (int c = 0; c < NP; ++c)
+                        if (c < cout) {
+                            float v = acc[c] + bias[c];
+                            o[c] = relu ? fmaxf(v, 0.f) : v;
+                        }
+                }
             }
         }
         // all TMEM reads done before the next item's MMAs overwrite the accumulators
@@ -385,7 +399,7 @@ int pad_n(int c) { return c <= 16 ? 16 : (c <= 32 ? 32 : (c <= 64 ? 64 : (c <= 1
 template <int KP, int NP>
 void launch_tc(sfb_ctx *ctx, const NetLayer &L, const float *in, int ld_in, const int32_t *nbr,
                int64_t nbr_ld, const int64_t *d_m, int64_t m_bound, int relu, float *out,
-               int ld_out, int64_t m_grid) {
+               int ld_out, int64_t m_grid, const int32_t *row_map, const int32_t *tap_off) {
     using S = TcShape<KP, NP>;
     static bool attr = false;
     if (!attr) {
@@ -394,14 +408,16 @@ void launch_tc(sfb_ctx *ctx, const NetLayer &L, const float *in, int ld_in, cons
         attr = true;
     }
     const int64_t tiles_bound = (m_grid + kM - 1) / kM;
-    const int64_t work_bound = tiles_bound * choose_splits(tiles_bound, L.taps, kSplitTarget);
+    const int64_t work_bound = tap_off ? tiles_bound
+                                       : tiles_bound * choose_splits(tiles_bound, L.taps, kSplitTarget);
     const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(work_bound, kSplitTarget));
     float *partial = ctx->arena.alloc<float>((size_t)std::min<int64_t>(kMaxPartialRows,
                                                                        32 * m_bound) * NP);
     k_conv_tc<KP, NP><<<grid, kThreadsTC, S::SMEM, ctx->stream>>>(
         in, ld_in, L.cin, nbr, nbr_ld, d_m, m_bound, L.taps, L.w_tc, L.b, L.cout, relu, out, ld_out,
-        partial);
+        partial, row_map, tap_off);
     SFB_CHECK_LAUNCH();
+    if (tap_off) return;   // one tap per tile: no split-K partials
     k_splitk_reduce<<<dgrid(std::min<int64_t>(m_grid, kMaxPartialRows) * L.cout, 256), 256, 0,
                       ctx->stream>>>(partial, d_m, m_bound, L.taps, NP, L.b, L.cout, relu, out,
                                      ld_out);
@@ -432,10 +448,11 @@ void prepare_tc_weights(sfb_ctx *ctx, NetLayer &L) {
 
 void conv_layer_tc(sfb_ctx *ctx, const NetLayer &L, const float *in, int ld_in, const int32_t *nbr,
                    int64_t nbr_ld, const int64_t *d_m, int64_t m_bound, int relu, float *out,
-                   int ld_out, int64_t m_grid) {
+                   int ld_out, int64_t m_grid, const int32_t *row_map, const int32_t *tap_off) {
 #define SFB_TC_CASE(K, N)                                                                 \
     if (L.cin_pad == K && L.cout_pad == N) {                                              \
-        launch_tc<K, N>(ctx, L, in, ld_in, nbr, nbr_ld, d_m, m_bound, relu, out, ld_out, m_grid); \
+        launch_tc<K, N>(ctx, L, in, ld_in, nbr, nbr_ld, d_m, m_bound, relu, out, ld_out, m_grid, \
+                        row_map, tap_off);                                               \
         return;                                                                           \
     }
     SFB_TC_CASE(16, 16) SFB_TC_CASE(16, 32) SFB_TC_CASE(16, 64) SFB_TC_CASE(16, 128)

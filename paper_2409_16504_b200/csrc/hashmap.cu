@@ -321,7 +321,8 @@ __global__ void k_pool_assign(const int32_t *__restrict__ coords, const int32_t 
                               const int64_t *__restrict__ d_m, int64_t S, int32_t *__restrict__ pcoords,
                               int32_t *__restrict__ c2p, int32_t *__restrict__ nkids,
                               int32_t *__restrict__ kids, int32_t *__restrict__ tap,
-                              int32_t *__restrict__ vals, int32_t *__restrict__ tmap, int64_t ld) {
+                              int32_t *__restrict__ vals, int32_t *__restrict__ tmap, int64_t ld,
+                              int32_t *__restrict__ tap_cnt) {
     const int64_t m = *d_m;
     const int64_t cs = S / 2;
     SFB_FOR(j, m) {
@@ -337,6 +338,7 @@ __global__ void k_pool_assign(const int32_t *__restrict__ coords, const int32_t 
         }
         const int32_t tj = (int32_t)(d[2] * 4 + d[1] * 2 + d[0]);
         if (tap) tap[j] = tj;
+        if (tap_cnt) atomicAdd(&tap_cnt[tj], 1);
         if (tmap)
 #pragma unroll
             for (int k = 0; k < 8; ++k) tmap[k * ld + j] = (k == tj) ? pid : -1;
@@ -396,10 +398,37 @@ void pool_fast(sfb_ctx *ctx, const int32_t *coords, const int64_t *d_m, int64_t 
     SFB_CHECK_LAUNCH();
     dscan(ctx, flag, flag, d_m, m_bound, d_mp, false);
     k_pool_assign<<<g, 256, 0, st>>>(coords, slot_of, minrow, flag, d_m, S, parent_coords,
-                                     child_to_parent, nkids, kids, nullptr, nullptr, nullptr, 0);
+                                     child_to_parent, nkids, kids, nullptr, nullptr, nullptr, 0,
+                                     nullptr);
     k_pool_means_fast<<<dgrid(m_grid * c, 256), 256, 0, st>>>(feats, ld_in, c, nkids, kids, d_mp,
                                                               parent_feats, ld_out);
     SFB_CHECK_LAUNCH();
+}
+
+// children grouped by tap for the transposed conv (bucket order within a tap
+// is arbitrary — each output row depends only on its own parent and tap)
+// per-tap counts come from k_pool_assign; every thread forms the padded
+// bucket offsets from the 8 counts, block 0 publishes them
+__global__ void k_tap_scatter(const int32_t *__restrict__ tap, const int32_t *__restrict__ c2p,
+                              const int64_t *__restrict__ d_m, const int32_t *__restrict__ cnt,
+                              int32_t *__restrict__ cur, int32_t *__restrict__ off,
+                              int64_t *__restrict__ d_rows, int32_t *__restrict__ perm,
+                              int32_t *__restrict__ src) {
+    const int64_t m = *d_m;
+    int32_t o[9];
+    o[0] = 0;
+#pragma unroll
+    for (int t = 0; t < 8; ++t) o[t + 1] = o[t] + (cnt[t] + 127) / 128 * 128;
+    if (blockIdx.x == 0 && threadIdx.x < 9) {
+        off[threadIdx.x] = o[threadIdx.x];
+        if (threadIdx.x == 8) *d_rows = o[8];
+    }
+    SFB_FOR(j, m) {
+        const int32_t t = tap[j];
+        const int32_t pos = o[t] + atomicAdd(&cur[t], 1);
+        perm[pos] = (int32_t)j;
+        src[pos] = c2p[j];
+    }
 }
 
 // The fused UNet splits pooling in two: the coordinate structure (parents,
@@ -426,7 +455,7 @@ PoolStructure pool_structure(sfb_ctx *ctx, const int32_t *coords, const int64_t 
     P.kids = ctx->arena.alloc<int32_t>(8 * m_bound);
     P.c2p = ctx->arena.alloc<int32_t>(m_bound);
     P.tap = ctx->arena.alloc<int32_t>(m_bound);
-    P.tmap = ctx->arena.alloc<int32_t>(8 * m_bound);
+    P.tmap = nullptr;   // the fused UNet uses the tap buckets instead
     const unsigned g = dgrid(m_grid, 256);
     k_pool_clear<<<dgrid((int64_t)cap_grid, 256), 256, 0, st>>>(P.table.keys, minrow, P.nkids,
                                                                 P.table.mask, d_m);
@@ -434,8 +463,22 @@ PoolStructure pool_structure(sfb_ctx *ctx, const int32_t *coords, const int64_t 
     k_pool_first<<<g, 256, 0, st>>>(slot_of, minrow, d_m, flag);
     SFB_CHECK_LAUNCH();
     dscan(ctx, flag, flag, d_m, m_bound, d_mp, false);
+    // tap buckets for the transposed conv of this level (counts by k_pool_assign)
+    TapBuckets &B = P.buckets;
+    int32_t *cnt = ctx->arena.alloc<int32_t>(32);   // counts, cursors, offsets
+    SFB_CUDA(cudaMemsetAsync(cnt, 0, 16 * sizeof(int32_t), st));
     k_pool_assign<<<g, 256, 0, st>>>(coords, slot_of, minrow, flag, d_m, S, parent_coords, P.c2p,
-                                     P.nkids, P.kids, P.tap, P.table.vals, P.tmap, m_bound);
+                                     P.nkids, P.kids, P.tap, P.table.vals, P.tmap, m_bound, cnt);
+    SFB_CHECK_LAUNCH();
+    B.rows_bound = m_bound + 8 * 128;
+    B.rows_grid = m_grid + 8 * 128;
+    B.perm = ctx->arena.alloc<int32_t>(B.rows_bound);
+    B.src = ctx->arena.alloc<int32_t>(B.rows_bound);
+    B.off = cnt + 16;
+    B.d_rows = ctx->arena.alloc<int64_t>(1);
+    SFB_CUDA(cudaMemsetAsync(B.perm, 0xff, sizeof(int32_t) * B.rows_bound, st));
+    SFB_CUDA(cudaMemsetAsync(B.src, 0xff, sizeof(int32_t) * B.rows_bound, st));
+    k_tap_scatter<<<g, 256, 0, st>>>(P.tap, P.c2p, d_m, cnt, cnt + 8, B.off, B.d_rows, B.perm, B.src);
     SFB_CHECK_LAUNCH();
     return P;
 }

@@ -21,7 +21,8 @@ namespace sfb {
 
 void conv_layer_tc(sfb_ctx *ctx, const NetLayer &L, const float *in, int ld_in, const int32_t *nbr,
                    int64_t nbr_ld, const int64_t *d_m, int64_t m_bound, int relu, float *out,
-                   int ld_out, int64_t m_grid);
+                   int ld_out, int64_t m_grid, const int32_t *row_map = nullptr,
+                   const int32_t *tap_off = nullptr);
 bool conv_tc_supported(const NetLayer &L);
 void prepare_tc_weights(sfb_ctx *ctx, NetLayer &L);
 
@@ -267,10 +268,18 @@ __global__ void k_tmap(const int32_t *__restrict__ parent, const int32_t *__rest
 
 void tconv_layer(sfb_ctx *ctx, const NetLayer &L, const float *in, int ld_in,
                  const int32_t *parent, const int32_t *tap, const int64_t *d_m, int64_t m_bound,
-                 int relu, float *out, int ld_out, int64_t m_grid, const int32_t *tmap) {
+                 int relu, float *out, int ld_out, int64_t m_grid, const int32_t *tmap,
+                 const TapBuckets *tb) {
     if (m_bound == 0) return;
     if (m_grid < 0) m_grid = m_bound;
     if (ctx->net_mode == SFB_NET_TC_TF32X3 && L.w_tc) {
+        // rows bucketed by tap (one tap per 128-row tile) when the level has
+        // enough tiles to fill the GPU; small levels split the 8 taps instead
+        if (tb && m_grid >= 64 * 128) {
+            conv_layer_tc(ctx, L, in, ld_in, tb->src, 0, tb->d_rows, tb->rows_bound, relu, out,
+                          ld_out, tb->rows_grid, tb->perm, tb->off);
+            return;
+        }
         if (!tmap) {
             int32_t *t = ctx->arena.alloc<int32_t>(8 * (size_t)m_bound);
             k_tmap<<<dgrid(m_grid, 256), 256, 0, ctx->stream>>>(parent, tap, d_m, m_bound, m_bound, t);
@@ -555,7 +564,7 @@ void unet_run(sfb_ctx *ctx, const int32_t *coords0, const double *feats9, int64_
     int ld_coarse = enc[L + 1];
     for (int l = L - 1; l >= 0; --l) {
         tconv_layer(ctx, net.layers[layer++], coarse, ld_coarse, ps[l].c2p, ps[l].tap, &C->m[l], mb,
-                    1, cat[l], width[l], mg[l], ps[l].tmap);
+                    1, cat[l], width[l], mg[l], ps[l].tmap, &ps[l].buckets);
         coarse = cat[l];
         ld_coarse = width[l];
     }
