@@ -25,6 +25,7 @@
 //      when every pixel of the tile has T < 1/255 — identical to the
 //      reference, whose per-pixel skip makes all later splats no-ops.
 #include <cub/cub.cuh>
+#include <cstddef>
 
 #include "common.cuh"
 
@@ -382,11 +383,23 @@ __global__ void k_run_heads(const uint32_t *__restrict__ src, const int64_t *__r
     }
 }
 
+// What the compositor stages per candidate run, packed so a run costs a few
+// 16-byte loads: geometry (conic, centre, opacity, support radius, depth)
+// and the attribute side (first normal, point range, uniform-normal flag).
+struct __align__(16) RunRec {
+    double mx, my, ia, ib, ic, op, rad, dep;
+};
+struct __align__(16) RunAux {
+    double rn[3];          // normal of the run's first point
+    int32_t start, count;  // the run's points in rank order
+    int32_t uni, pad;      // 1 when every point of the run has the same normal
+};
+static_assert(sizeof(RunAux) == 48 && offsetof(RunAux, start) == 24 && offsetof(RunAux, uni) == 32,
+              "the compositor stages RunAux as three double2 loads");
+
 struct Runs {
-    double *mx, *my, *rad, *ia, *ib, *ic, *op;
-    double *rn;           // normal of the run's first point [r][3]
-    double *dep;          // the run's camera depth (constant over the run)
-    uint8_t *uni;         // 1 when every point of the run has the same normal
+    RunRec *rec;
+    RunAux *aux;
     int32_t *start, *count;
     int4 *rect;
     uint8_t *level;  // 0 fine, 1 super, 2 global, 3 dead
@@ -402,14 +415,15 @@ __device__ __forceinline__ void run_geometry(Runs &R, int64_t r, int64_t g, cons
     const double a = P.a[g], b = P.b[g], c = P.c[g];
     const double op = opac[g];
     const double det = a * c - b * b;
-    R.mx[r] = P.sx[g];
-    R.my[r] = P.sy[g];
-    R.ia[r] = c / det;
-    R.ib[r] = -b / det;
-    R.ic[r] = a / det;
-    R.op[r] = op;
     const double rad = support_radius(a, b, c, op);
-    R.rad[r] = rad;
+    RunRec &q = R.rec[r];
+    q.mx = P.sx[g];
+    q.my = P.sy[g];
+    q.ia = c / det;
+    q.ib = -b / det;
+    q.ic = a / det;
+    q.op = op;
+    q.rad = rad;
     const TileRect t = tile_rect(P.sx[g], P.sy[g], rad, ft, ntx, nty);
     R.rect[r] = make_int4(t.x0, t.x1, t.y0, t.y1);
     int lvl = 3, nf = 0, ns = 0, ng = 0;
@@ -624,7 +638,7 @@ __global__ void k_emit(Runs R, const int32_t *__restrict__ fpos, const int32_t *
                        const int32_t *__restrict__ gpos, int64_t ntx, int64_t nsx,
                        uint32_t *__restrict__ fkey, uint32_t *__restrict__ fval,
                        uint32_t *__restrict__ skey, uint32_t *__restrict__ sval,
-                       uint32_t *__restrict__ glist) {
+                       uint32_t *__restrict__ glist, int4 *__restrict__ grect) {
     const int64_t nr = *R.d_R;
     SFB_FOR(r, nr) {
         R.count[r] -= R.start[r];   // k_run_build stored the run's end
@@ -646,6 +660,7 @@ __global__ void k_emit(Runs R, const int32_t *__restrict__ fpos, const int32_t *
                 }
         } else if (lvl == 2) {
             glist[gpos[r]] = (uint32_t)r;
+            grect[gpos[r]] = t;
         }
     }
 }
@@ -659,10 +674,14 @@ __global__ void k_stage_runs(Runs R, const uint32_t *__restrict__ src, const int
     SFB_FOR(r, nr) {
         const uint32_t i0 = src[R.start[r]];
         const int64_t g0 = p2g ? p2g[i0] : (int64_t)i0;
-        R.dep[r] = gdepth[g0];
+        R.rec[r].dep = gdepth[g0];
+        RunAux &x = R.aux[r];
+        x.start = R.start[r];
+        x.count = R.count[r];
+        x.pad = 0;
         uint8_t u = 1;
         if (want_n) {
-            for (int c = 0; c < 3; ++c) R.rn[3 * r + c] = normals[3 * g0 + c];
+            for (int c = 0; c < 3; ++c) x.rn[c] = normals[3 * g0 + c];
             if (!p2g)   // generic splats: compare every point's normal
                 for (int32_t j = R.start[r] + 1; j < R.start[r] + R.count[r] && u; ++j) {
                     const uint32_t i = src[j];
@@ -671,7 +690,7 @@ __global__ void k_stage_runs(Runs R, const uint32_t *__restrict__ src, const int
                         normals[3 * (size_t)i + 2] == normals[3 * (size_t)i0 + 2];
                 }
         }
-        R.uni[r] = u;
+        x.uni = u;
     }
 }
 
@@ -689,6 +708,14 @@ __global__ void k_gather_attrs(const uint32_t *__restrict__ src, const int32_t *
         if (snrm && !p2g)
             snrm[j] = make_float4((float)normals[3 * i], (float)normals[3 * i + 1], (float)normals[3 * i + 2], 0.f);
     }
+}
+
+// tile rects of a sorted list's entries, in list order (the compositor then
+// loads an entry's id and rect side by side instead of rect[id])
+__global__ void k_list_rects(const uint32_t *__restrict__ ids, const int64_t *__restrict__ d_n,
+                             const int4 *__restrict__ rect, int4 *__restrict__ out) {
+    const int64_t n = *d_n;
+    SFB_FOR(i, n) out[i] = rect[ids[i]];
 }
 
 __global__ void k_histogram(const uint32_t *__restrict__ keys, const int64_t *__restrict__ d_n,
@@ -711,6 +738,7 @@ struct CompParams {
     const int32_t *s_off;
     const uint32_t *s_ids;
     const uint32_t *g_ids;
+    const int4 *s_rect, *g_rect;   // tile rects of the super / global entries, in list order
     const int64_t *d_G;
     Runs R;
     // per-point attributes in rank order (float4: x, y, z, pad)
@@ -721,6 +749,35 @@ struct CompParams {
     uint8_t *rgba;   // render_pose RGBA8 (FrameParams shading), or null
     int64_t *dbg;   // optional per-tile counters: windows, list entries, alpha evals, point blends
 };
+
+// exp(x) for x <= 0 in float64 (the compositor's alpha = o * exp(-q/2)):
+// x = k ln2 + r, |r| <= ln2/2, with ln2 split hi/lo (Cody-Waite), exp(r) by
+// a degree-12 Taylor polynomial in FMA Horner form (truncation < 2^-60), then
+// scaled by 2^k through the exponent bits. Within ~1 ulp like the libm exp
+// (the reference's numba kernel uses LLVM's), at ~25 instructions instead of
+// the ~50 of the general-purpose CUDA exp with its special-case paths.
+__device__ __forceinline__ double exp_nonpos(double x) {
+    if (x < -708.0) return 0.0;   // below the smallest normal: alpha < 1/255 anyway
+    if (x > 0.0) return exp(x);   // q < 0 only through rounding of a degenerate conic
+    const double kd = rint(x * 1.4426950408889634);
+    const double r = __fma_rn(-kd, 6.93147180369123816490e-01, x);
+    const double rr = __fma_rn(-kd, 1.90821492927058770002e-10, r);
+    double p = 2.08767569878680989792e-09;            // 1/12!
+    p = __fma_rn(p, rr, 2.50521083854417187751e-08);  // 1/11!
+    p = __fma_rn(p, rr, 2.75573192239858906526e-07);  // 1/10!
+    p = __fma_rn(p, rr, 2.75573192239858906526e-06);  // 1/9!
+    p = __fma_rn(p, rr, 2.48015873015873015873e-05);  // 1/8!
+    p = __fma_rn(p, rr, 1.98412698412698412698e-04);  // 1/7!
+    p = __fma_rn(p, rr, 1.38888888888888888889e-03);  // 1/6!
+    p = __fma_rn(p, rr, 8.33333333333333333333e-03);  // 1/5!
+    p = __fma_rn(p, rr, 4.16666666666666666667e-02);  // 1/4!
+    p = __fma_rn(p, rr, 1.66666666666666666667e-01);  // 1/3!
+    p = __fma_rn(p, rr, 0.5);
+    p = __fma_rn(p, rr, 1.0);
+    p = __fma_rn(p, rr, 1.0);
+    const int k = (int)kd;   // in [-1022, 0]: 2^k is a normal double
+    return p * __longlong_as_double((long long)(k + 1023) << 52);
+}
 
 // b^e for e >= 0 by repeated squaring (float64)
 __device__ __forceinline__ double ipow(double b, int e) {
@@ -733,32 +790,52 @@ __device__ __forceinline__ double ipow(double b, int e) {
     return r;
 }
 
-// sum_{j<m} om^j v_j by Horner from the last point (float32; v in rank order)
+// sum_{j<m} om^j v_j (float32; v in rank order). Two interleaved Horner
+// chains in om^2 (even and odd points), S = E + om * O, so two independent
+// FMA chains and four 16-byte loads are in flight per step.
 __device__ __forceinline__ float3 horner3(const float4 *__restrict__ v, int m, float om) {
-    float x = 0.f, y = 0.f, z = 0.f;
+    const float om2 = om * om;
+    float ex = 0.f, ey = 0.f, ez = 0.f, ox = 0.f, oy = 0.f, oz = 0.f;
     int j = m - 1;
-    for (; j >= 3; j -= 4) {
-        const float4 a = __ldg(v + j), b = __ldg(v + j - 1), c = __ldg(v + j - 2), d = __ldg(v + j - 3);
-        x = fmaf(x, om, a.x);
-        y = fmaf(y, om, a.y);
-        z = fmaf(z, om, a.z);
-        x = fmaf(x, om, b.x);
-        y = fmaf(y, om, b.y);
-        z = fmaf(z, om, b.z);
-        x = fmaf(x, om, c.x);
-        y = fmaf(y, om, c.y);
-        z = fmaf(z, om, c.z);
-        x = fmaf(x, om, d.x);
-        y = fmaf(y, om, d.y);
-        z = fmaf(z, om, d.z);
-    }
-    for (; j >= 0; --j) {
+    if (!(m & 1) && j >= 0) {   // make the last point an even one
         const float4 a = __ldg(v + j);
-        x = fmaf(x, om, a.x);
-        y = fmaf(y, om, a.y);
-        z = fmaf(z, om, a.z);
+        ox = a.x;
+        oy = a.y;
+        oz = a.z;
+        --j;
     }
-    return make_float3(x, y, z);
+    // j is even here: pairs (j-1 odd, j even) ... down to (-, 0)
+    for (; j >= 4; j -= 4) {
+        const float4 a = __ldg(v + j), b = __ldg(v + j - 1), c = __ldg(v + j - 2), d = __ldg(v + j - 3);
+        ex = fmaf(ex, om2, a.x);
+        ey = fmaf(ey, om2, a.y);
+        ez = fmaf(ez, om2, a.z);
+        ox = fmaf(ox, om2, b.x);
+        oy = fmaf(oy, om2, b.y);
+        oz = fmaf(oz, om2, b.z);
+        ex = fmaf(ex, om2, c.x);
+        ey = fmaf(ey, om2, c.y);
+        ez = fmaf(ez, om2, c.z);
+        ox = fmaf(ox, om2, d.x);
+        oy = fmaf(oy, om2, d.y);
+        oz = fmaf(oz, om2, d.z);
+    }
+    for (; j >= 2; j -= 2) {
+        const float4 a = __ldg(v + j), b = __ldg(v + j - 1);
+        ex = fmaf(ex, om2, a.x);
+        ey = fmaf(ey, om2, a.y);
+        ez = fmaf(ez, om2, a.z);
+        ox = fmaf(ox, om2, b.x);
+        oy = fmaf(oy, om2, b.y);
+        oz = fmaf(oz, om2, b.z);
+    }
+    if (j == 0) {
+        const float4 a = __ldg(v);
+        ex = fmaf(ex, om2, a.x);
+        ey = fmaf(ey, om2, a.y);
+        ez = fmaf(ez, om2, a.z);
+    }
+    return make_float3(fmaf(om, ox, ex), fmaf(om, oy, ey), fmaf(om, oz, ez));
 }
 
 // One CTA per tile. The rank-ordered fine / super / global lists are merged
@@ -817,11 +894,8 @@ __global__ void __launch_bounds__(kCT, 4) k_composite(CompParams P) {
         return mine;
     };
 
-    const double *__restrict__ Rmx = P.R.mx, *__restrict__ Rmy = P.R.my, *__restrict__ Rrad = P.R.rad;
-    const double *__restrict__ Ria = P.R.ia, *__restrict__ Rib = P.R.ib, *__restrict__ Ric = P.R.ic;
-    const double *__restrict__ Rop = P.R.op, *__restrict__ Rdep = P.R.dep, *__restrict__ Rrn = P.R.rn;
-    const int32_t *__restrict__ Rstart = P.R.start, *__restrict__ Rcount = P.R.count;
-    const uint8_t *__restrict__ Runi = P.R.uni;
+    const double2 *__restrict__ Rrec = reinterpret_cast<const double2 *>(P.R.rec);
+    const double2 *__restrict__ Raux = reinterpret_cast<const double2 *>(P.R.aux);
     const float4 *__restrict__ scol = P.scol, *__restrict__ snrm = P.snrm;
     const double alpha_max = P.alpha_max;
     const uint32_t *ids[3] = {P.f_ids, P.s_ids, P.g_ids};
@@ -851,7 +925,10 @@ __global__ void __launch_bounds__(kCT, 4) k_composite(CompParams P) {
             int4 rc[2];
 #pragma unroll
             for (int s = 1; s < 3; ++s)
-                if (id[s] < w1) rc[s - 1] = P.R.rect[id[s]];
+                if (id[s] < w1) {   // rects stored in list order: no dependent load
+                    const int64_t idx = cur[s] + k * kCT + threadIdx.x;
+                    rc[s - 1] = (s == 1 ? P.s_rect : P.g_rect)[idx];
+                }
 #pragma unroll
             for (int s = 0; s < 3; ++s) {
                 const uint32_t r = id[s];
@@ -904,23 +981,28 @@ __global__ void __launch_bounds__(kCT, 4) k_composite(CompParams P) {
             if (threadIdx.x < nb) {
                 const uint32_t r = list[base + threadIdx.x];
                 const int j = threadIdx.x;
-                const double mx = Rmx[r], my = Rmy[r];
-                const double rad = Rrad[r] + 1.0;
+                const double2 q0 = Rrec[4 * (size_t)r], q1 = Rrec[4 * (size_t)r + 1],
+                              q2 = Rrec[4 * (size_t)r + 2], q3 = Rrec[4 * (size_t)r + 3];
+                const double2 a0 = Raux[3 * (size_t)r], a1 = Raux[3 * (size_t)r + 1],
+                              a2 = Raux[3 * (size_t)r + 2];
+                const double mx = q0.x, my = q0.y;
+                const double rad = q3.x + 1.0;
                 r_mx[j] = mx;
                 r_my[j] = my;
                 r_rr[j] = rad * rad;
-                r_ia[j] = Ria[r];
-                r_ib[j] = Rib[r];
-                r_ic[j] = Ric[r];
-                r_op[j] = Rop[r];
-                r_start[j] = Rstart[r];
-                r_count[j] = Rcount[r];
-                r_dep[j] = Rdep[r];
-                r_uni[j] = Runi[r];
+                r_ia[j] = q1.x;
+                r_ib[j] = q1.y;
+                r_ic[j] = q2.x;
+                r_op[j] = q2.y;
+                r_dep[j] = q3.y;
+                // RunAux as double2: {rn0, rn1}, {rn2, (start, count)}, {(uni, pad), -}
+                r_start[j] = __double2loint(a1.y);
+                r_count[j] = __double2hiint(a1.y);
+                r_uni[j] = (uint8_t)__double2loint(a2.x);
                 if (want_n) {
-                    r_rn[0][j] = Rrn[3 * (size_t)r];
-                    r_rn[1][j] = Rrn[3 * (size_t)r + 1];
-                    r_rn[2][j] = Rrn[3 * (size_t)r + 2];
+                    r_rn[0][j] = a0.x;
+                    r_rn[1][j] = a0.y;
+                    r_rn[2][j] = a1.x;
                 }
                 // pixel box of forward_kernel (_raster_kernels.py:178-181), clamped to the tile
                 r_x0[j] = (int32_t)fmin(fmax((double)x_lo, ceil(mx - rad)), (double)x_end);
@@ -955,7 +1037,7 @@ __global__ void __launch_bounds__(kCT, 4) k_composite(CompParams P) {
                         if (dx * dx + dy * dy > r_rr[e]) continue;
                     }
                     const double q = r_ia[e] * dx * dx + 2.0 * r_ib[e] * dx * dy + r_ic[e] * dy * dy;
-                    double alpha = r_op[e] * exp(-0.5 * q);
+                    double alpha = r_op[e] * exp_nonpos(-0.5 * q);
                     if (alpha > alpha_max) alpha = alpha_max;
                     if (alpha < kCutoff) continue;
                     const double om = 1.0 - alpha;
@@ -1160,19 +1242,11 @@ void render_run(sfb_ctx *ctx, const RenderInputs &in, const FrameParams *FP, int
     Runs R{};
     R.d_R = &C->runs;
     int32_t *head = ctx->arena.alloc<int32_t>(nb);
-    double *blk = ctx->arena.alloc<double>(7 * nb);
-    R.mx = blk;
-    R.my = blk + nb;
-    R.rad = blk + 2 * nb;
-    R.ia = blk + 3 * nb;
-    R.ib = blk + 4 * nb;
-    R.ic = blk + 5 * nb;
-    R.op = blk + 6 * nb;
+    R.rec = ctx->arena.alloc<RunRec>(nb);
+    R.aux = ctx->arena.alloc<RunAux>(nb);
     R.start = ctx->arena.alloc<int32_t>(nb);
     R.count = ctx->arena.alloc<int32_t>(nb);
-    R.rn = ctx->arena.alloc<double>(3 * (size_t)nb);
-    R.dep = ctx->arena.alloc<double>(nb);
-    R.uni = ctx->arena.alloc<uint8_t>(nb);
+
     R.rect = ctx->arena.alloc<int4>(nb);
     R.level = ctx->arena.alloc<uint8_t>(nb);
     int32_t *cnts = ctx->arena.alloc<int32_t>(3 * (nb + 1));
@@ -1186,6 +1260,8 @@ void render_run(sfb_ctx *ctx, const RenderInputs &in, const FrameParams *FP, int
     uint32_t *skey = ctx->arena.alloc<uint32_t>(ebound), *sval = ctx->arena.alloc<uint32_t>(ebound);
     uint32_t *skey2 = ctx->arena.alloc<uint32_t>(ebound), *sval2 = ctx->arena.alloc<uint32_t>(ebound);
     uint32_t *glist = ctx->arena.alloc<uint32_t>(nb);
+    int4 *grect = ctx->arena.alloc<int4>(nb);
+    int4 *srect = ctx->arena.alloc<int4>(ebound);
     int32_t *f_off = ctx->arena.alloc<int32_t>(nt + 1);
     int32_t *s_off = ctx->arena.alloc<int32_t>(ns + 1);
     SFB_CUDA(cudaMemsetAsync(f_off, 0, sizeof(int32_t) * (nt + 1), st));
@@ -1218,7 +1294,7 @@ void render_run(sfb_ctx *ctx, const RenderInputs &in, const FrameParams *FP, int
         dscan(ctx, R.ns, pos + (nb + 1), &C->runs1, nb + 1, &C->es, false);
         dscan(ctx, R.ng, pos + 2 * (nb + 1), &C->runs1, nb + 1, &C->g, false);
         k_emit<<<dgrid(ctx->grid_bound(n, ctx->hint_runs), 256), 256, 0, st>>>(
-            R, pos, pos + (nb + 1), pos + 2 * (nb + 1), ntx, nsx, fkey, fval, skey, sval, glist);
+            R, pos, pos + (nb + 1), pos + 2 * (nb + 1), ntx, nsx, fkey, fval, skey, sval, glist, grect);
         SFB_CHECK_LAUNCH();
         if ((scol && !by_voxel) || snrm) {
             k_gather_attrs<<<dgrid(n, 256), 256, 0, st>>>(src, in.point_to_geom, in.colors,
@@ -1234,6 +1310,7 @@ void render_run(sfb_ctx *ctx, const RenderInputs &in, const FrameParams *FP, int
         const uint32_t *fk = (f_ids == fval2) ? fkey2 : fkey;
         s_ids = dsort_pairs<uint32_t>(ctx, skey, sval, skey2, sval2, &C->es, ebound, sbits) ? sval2 : sval;
         const uint32_t *sk = (s_ids == sval2) ? skey2 : skey;
+        k_list_rects<<<dgrid(ebound, 256), 256, 0, st>>>(s_ids, &C->es, R.rect, srect);
         k_histogram<<<dgrid(ebound, 256), 256, 0, st>>>(fk, &C->ef, f_off);
         k_histogram<<<dgrid(ebound, 256), 256, 0, st>>>(sk, &C->es, s_off);
         SFB_CHECK_LAUNCH();
@@ -1258,6 +1335,8 @@ void render_run(sfb_ctx *ctx, const RenderInputs &in, const FrameParams *FP, int
     CP.s_off = s_off;
     CP.s_ids = s_ids;
     CP.g_ids = glist;
+    CP.s_rect = srect;
+    CP.g_rect = grect;
     CP.d_G = &C->g;
     CP.R = R;
     CP.scol = scol;
