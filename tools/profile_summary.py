@@ -25,7 +25,7 @@ if lp.exists():
     r = subprocess.run([sys.executable, str(ROOT / "tools" / "launches.py"), str(lp), "200"],
                        capture_output=True, text=True, check=True)
     (out / f"{tag}_launches.txt").write_text(
-        f"# ncu --metrics gpu__time_duration.sum --clock-control none (cold cache, serialised)\n"
+        f"# ncu --metrics gpu__time_duration.sum --clock-control none --cache-control none (L2 warm as in the frame, launches serialised)\n"
         f"# one full config-2 frame (the launches between two k_composite), us per kernel name\n"
         + r.stdout)
     print(r.stdout)
