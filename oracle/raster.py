@@ -43,6 +43,8 @@ def lib():
         _lib.oracle_bin_fill.argtypes = [P, P, P, I, I, I, I, I, I, I, I, P, P]
         _lib.oracle_forward.argtypes = [I, I, I, I, I, I, I, P, P, P, P, P, P, P, P, P, P,
                                         D, ctypes.c_int, P, P]
+        _lib.oracle_backward.argtypes = [I, I, I, I, I, P, P, P, P, P, P, P, P, P, D,
+                                         ctypes.c_int, ctypes.c_int, P, P, P, P, P, P]
     return _lib
 
 
@@ -186,3 +188,124 @@ def relight(normal, rgb, transmittance, light, ambient, diffuse) -> np.ndarray:
     lam = np.maximum(normal @ np.asarray(light, dtype=np.float64), 0.0)
     shaded = rgb * (ambient + diffuse * lam)[:, :, None]
     return np.clip(np.where((transmittance > 0.999)[:, :, None], rgb, shaded), 0.0, 1.0)
+
+
+def _quat_to_rotmat(q):
+    """gaussians.py:160-177, batched."""
+    q = np.asarray(q, dtype=np.float64)
+    norm = np.linalg.norm(q, axis=-1, keepdims=True)
+    w, x, y, z = np.moveaxis(q / norm, -1, 0)
+    r = np.empty(q.shape[:-1] + (3, 3), dtype=np.float64)
+    r[..., 0, 0] = 1 - 2 * (y * y + z * z)
+    r[..., 0, 1] = 2 * (x * y - w * z)
+    r[..., 0, 2] = 2 * (x * z + w * y)
+    r[..., 1, 0] = 2 * (x * y + w * z)
+    r[..., 1, 1] = 1 - 2 * (x * x + z * z)
+    r[..., 1, 2] = 2 * (y * z - w * x)
+    r[..., 2, 0] = 2 * (x * z - w * y)
+    r[..., 2, 1] = 2 * (y * z + w * x)
+    r[..., 2, 2] = 1 - 2 * (x * x + y * y)
+    return r
+
+
+def render_backward(splats: dict, cam, upstream, mode="rgb", background=(0.0, 0.0, 0.0),
+                    tile=16, alpha_max=ALPHA_MAX, terminate=True) -> dict:
+    """Analytic gradients of render() (rasterizer.py:229-354): per-entry slots from
+    backward_kernel, the ordered entry->splat reduction (np.add.at), then the chain
+    rule through the inverse covariance, EWA Jacobian, rotation and normalisation."""
+    modes = ("rgb", "normal", "depth")
+    background = np.asarray(background, dtype=np.float64).reshape(3)
+    h, w = int(cam.height), int(cam.width)
+    if mode == "depth":
+        upstream = np.asarray(upstream, dtype=np.float64)
+        if upstream.shape == (h, w):
+            lifted = np.zeros((h, w, 3))
+            lifted[:, :, 0] = upstream
+            upstream = lifted
+    upstream = np.ascontiguousarray(upstream, dtype=np.float64)
+    prep = prepare(splats, cam, mode, tile)
+    k = len(prep["source"])
+    entries = prep["ids"].shape[0]
+    g_mu = np.zeros((entries, 2))
+    g_q = np.zeros((entries, 3))
+    g_opac = np.zeros(entries)
+    g_attr = np.zeros((entries, 3))
+    inv = prep["inv"]
+    lib().oracle_backward(w, h, tile, prep["ntx"], prep["nty"], _p(prep["offsets"]),
+                          _p(prep["ids"]), _p(prep["sx"]), _p(prep["sy"]), _p(_c(inv[:, 0])),
+                          _p(_c(inv[:, 1])), _p(_c(inv[:, 2])), _p(prep["opac"]), _p(prep["attr"]),
+                          float(alpha_max), int(bool(terminate)), modes.index(mode),
+                          _p(background), _p(upstream), _p(g_mu), _p(g_q), _p(g_opac), _p(g_attr))
+    d_mu = np.zeros((k, 2))
+    d_qf = np.zeros((k, 3))
+    d_op = np.zeros(k)
+    d_at = np.zeros((k, 3))
+    np.add.at(d_mu, prep["ids"], g_mu)
+    np.add.at(d_qf, prep["ids"], g_q)
+    np.add.at(d_op, prep["ids"], g_opac)
+    np.add.at(d_at, prep["ids"], g_attr)
+    n = np.asarray(splats["opacities"]).shape[0]
+    out = dict(d_centers=np.zeros((n, 3)), d_scales=np.zeros((n, 3)),
+               d_quaternions=np.zeros((n, 4)), d_opacities=np.zeros(n),
+               d_colors=np.zeros((n, 3)), d_normals=np.zeros((n, 3)))
+    if k == 0:
+        return out
+    src = prep["source"]
+    inv_m = np.empty((k, 2, 2))
+    inv_m[:, 0, 0] = inv[:, 0]
+    inv_m[:, 0, 1] = inv_m[:, 1, 0] = inv[:, 1]
+    inv_m[:, 1, 1] = inv[:, 2]
+    g_inv = np.empty((k, 2, 2))
+    g_inv[:, 0, 0] = d_qf[:, 0]
+    g_inv[:, 0, 1] = g_inv[:, 1, 0] = 0.5 * d_qf[:, 1]
+    g_inv[:, 1, 1] = d_qf[:, 2]
+    g_cov = -np.einsum("kij,kjl,klm->kim", inv_m, g_inv, inv_m)
+    rot_c = np.asarray(cam.rotation, dtype=np.float64)
+    centers = np.asarray(splats["centers"], dtype=np.float64)
+    p_cam = centers[src] @ rot_c.T + np.asarray(cam.translation, dtype=np.float64)
+    x, y, z = p_cam[:, 0], p_cam[:, 1], p_cam[:, 2]
+    fx, fy = float(cam.fx), float(cam.fy)
+    jac = np.zeros((k, 2, 3))
+    jac[:, 0, 0] = fx / z
+    jac[:, 0, 2] = -fx * x / (z * z)
+    jac[:, 1, 1] = fy / z
+    jac[:, 1, 2] = -fy * y / (z * z)
+    a2 = jac @ rot_c
+    g_s3 = np.einsum("kji,kjl,klm->kim", a2, g_cov, a2)
+    quats = np.asarray(splats["quaternions"], dtype=np.float64)[src]
+    scales = np.asarray(splats["scales"], dtype=np.float64)[src]
+    rot = _quat_to_rotmat(quats)
+    sigma3 = np.einsum("kji,kj,kjl->kil", rot, scales * scales, rot)
+    m_cam = np.einsum("ij,kjl,ml->kim", rot_c, sigma3, rot_c)
+    g_jac = 2.0 * np.einsum("kij,kjl,klm->kim", g_cov, jac, m_cam)
+    d_pcam = np.zeros((k, 3))
+    d_pcam[:, 0] = g_jac[:, 0, 2] * (-fx / (z * z))
+    d_pcam[:, 1] = g_jac[:, 1, 2] * (-fy / (z * z))
+    d_pcam[:, 2] = (g_jac[:, 0, 0] * (-fx / (z * z)) + g_jac[:, 0, 2] * (2.0 * fx * x / z ** 3)
+                    + g_jac[:, 1, 1] * (-fy / (z * z)) + g_jac[:, 1, 2] * (2.0 * fy * y / z ** 3))
+    d_pcam[:, 0] += d_mu[:, 0] * fx / z
+    d_pcam[:, 1] += d_mu[:, 1] * fy / z
+    d_pcam[:, 2] += d_mu[:, 0] * (-fx * x / (z * z)) + d_mu[:, 1] * (-fy * y / (z * z))
+    if mode == "depth":
+        d_pcam[:, 2] += d_at[:, 0]
+    out["d_centers"][src] = d_pcam @ rot_c
+    g_d = np.einsum("kij,kjl,kml->kim", rot, g_s3, rot)
+    out["d_scales"][src] = 2.0 * scales * np.stack([g_d[:, 0, 0], g_d[:, 1, 1], g_d[:, 2, 2]], axis=1)
+    g_r = 2.0 * (scales * scales)[:, :, None] * (rot @ g_s3)
+    qn = np.linalg.norm(quats, axis=1, keepdims=True)
+    w_, qx, qy, qz = (quats / qn).T
+    zero = np.zeros(k)
+    drdq = np.empty((k, 4, 3, 3))
+    drdq[:, 0] = 2.0 * np.stack([zero, -qz, qy, qz, zero, -qx, -qy, qx, zero], axis=1).reshape(k, 3, 3)
+    drdq[:, 1] = 2.0 * np.stack([zero, qy, qz, qy, -2 * qx, -w_, qz, w_, -2 * qx], axis=1).reshape(k, 3, 3)
+    drdq[:, 2] = 2.0 * np.stack([-2 * qy, qx, w_, qx, zero, qz, -w_, qz, -2 * qy], axis=1).reshape(k, 3, 3)
+    drdq[:, 3] = 2.0 * np.stack([-2 * qz, -w_, qx, w_, -2 * qz, qy, qx, qy, zero], axis=1).reshape(k, 3, 3)
+    d_qhat = np.einsum("kij,kqij->kq", g_r, drdq)
+    qhat = quats / qn
+    out["d_quaternions"][src] = (d_qhat - qhat * np.sum(qhat * d_qhat, axis=1, keepdims=True)) / qn
+    out["d_opacities"][src] = d_op
+    if mode == "rgb":
+        out["d_colors"][src] = d_at
+    elif mode == "normal":
+        out["d_normals"][src] = d_at
+    return out

@@ -164,3 +164,93 @@ void oracle_forward(int64_t width, int64_t height, int64_t tile, int64_t ntx, in
         }
     }
 }
+
+/* backward_kernel (_raster_kernels.py:204-310): per-pixel forward replay of
+ * the tile list (no box/circle test, break after the blend that takes T below
+ * the cutoff), then a reverse sweep reconstructing T_k and the suffix sums;
+ * gradients accumulate into per-CSR-entry slots. mode 0 rgb (background
+ * composited), 1 normal (upstream through the renormalisation), 2 depth. */
+void oracle_backward(int64_t width, int64_t height, int64_t tile, int64_t ntx, int64_t nty,
+                     const int64_t *offsets, const int64_t *ids, const double *sx,
+                     const double *sy, const double *inv_a, const double *inv_b,
+                     const double *inv_c, const double *opac, const double *attr,
+                     double alpha_max, int terminate, int mode, const double *background,
+                     const double *upstream, double *g_mu, double *g_q, double *g_opac,
+                     double *g_attr) {
+#pragma omp parallel for schedule(dynamic, 1)
+    for (int64_t t = 0; t < ntx * nty; ++t) {
+        int64_t tx = t % ntx, ty = t / ntx;
+        int64_t x_end = imin((tx + 1) * tile, width), y_end = imin((ty + 1) * tile, height);
+        int64_t start = offsets[t], end = offsets[t + 1];
+        for (int64_t py = ty * tile; py < y_end; ++py)
+            for (int64_t px = tx * tile; px < x_end; ++px) {
+                double tr = 1.0, n0 = 0.0, n1 = 0.0, n2 = 0.0;
+                int64_t e_last = start - 1;
+                for (int64_t e = start; e < end; ++e) {
+                    int64_t s = ids[e];
+                    double dx = (double)px - sx[s], dy = (double)py - sy[s];
+                    double q = inv_a[s] * dx * dx + 2.0 * inv_b[s] * dx * dy + inv_c[s] * dy * dy;
+                    double alpha = opac[s] * exp(-0.5 * q);
+                    if (alpha > alpha_max) alpha = alpha_max;
+                    if (alpha < ALPHA_CUTOFF) continue;
+                    double w = tr * alpha;
+                    n0 += w * attr[3 * s];
+                    n1 += w * attr[3 * s + 1];
+                    n2 += w * attr[3 * s + 2];
+                    tr *= 1.0 - alpha;
+                    e_last = e;
+                    if (terminate && tr < TRANS_CUTOFF) break;
+                }
+                double t_fin = tr;
+                const double *up = upstream + 3 * (py * width + px);
+                double u0 = up[0], u1 = up[1], u2 = up[2];
+                if (mode == 1) {
+                    double nn = sqrt(n0 * n0 + n1 * n1 + n2 * n2);
+                    if (nn > 1e-12) {
+                        double dot = (n0 * u0 + n1 * u1 + n2 * u2) / (nn * nn * nn);
+                        u0 = u0 / nn - n0 * dot;
+                        u1 = u1 / nn - n1 * dot;
+                        u2 = u2 / nn - n2 * dot;
+                    }
+                }
+                double d_tfin = 0.0;
+                if (mode == 0) d_tfin = u0 * background[0] + u1 * background[1] + u2 * background[2];
+                if (u0 == 0.0 && u1 == 0.0 && u2 == 0.0) continue;
+                double s0 = 0.0, s1 = 0.0, s2 = 0.0, t_next = t_fin;
+                for (int64_t e = e_last; e > start - 1; --e) {
+                    int64_t s = ids[e];
+                    double dx = (double)px - sx[s], dy = (double)py - sy[s];
+                    double q = inv_a[s] * dx * dx + 2.0 * inv_b[s] * dx * dy + inv_c[s] * dy * dy;
+                    double g = exp(-0.5 * q);
+                    double raw = opac[s] * g;
+                    int clamped = raw > alpha_max;
+                    double alpha = clamped ? alpha_max : raw;
+                    if (alpha < ALPHA_CUTOFF) continue;
+                    double one_m = 1.0 - alpha;
+                    double t_k = t_next / one_m;
+                    double w = t_k * alpha;
+                    const double *a = attr + 3 * s;
+                    g_attr[3 * e] += u0 * w;
+                    g_attr[3 * e + 1] += u1 * w;
+                    g_attr[3 * e + 2] += u2 * w;
+                    double d_alpha = (u0 * (t_k * a[0] - s0 / one_m) + u1 * (t_k * a[1] - s1 / one_m) +
+                                      u2 * (t_k * a[2] - s2 / one_m) - d_tfin * t_fin / one_m);
+                    if (!clamped) {
+                        g_opac[e] += d_alpha * g;
+                        double d_q = -0.5 * opac[s] * g * d_alpha;
+                        g_q[3 * e] += d_q * dx * dx;
+                        g_q[3 * e + 1] += d_q * 2.0 * dx * dy;
+                        g_q[3 * e + 2] += d_q * dy * dy;
+                        double ddx = d_q * 2.0 * (inv_a[s] * dx + inv_b[s] * dy);
+                        double ddy = d_q * 2.0 * (inv_b[s] * dx + inv_c[s] * dy);
+                        g_mu[2 * e] -= ddx;
+                        g_mu[2 * e + 1] -= ddy;
+                    }
+                    s0 += w * a[0];
+                    s1 += w * a[1];
+                    s2 += w * a[2];
+                    t_next = t_k;
+                }
+            }
+    }
+}
