@@ -179,6 +179,19 @@ int sfb_prepare_debug(sfb_ctx *ctx, const sfb_splats *splats, const sfb_camera *
                       int32_t tile_size, int64_t *source, double *radius, int64_t *offsets,
                       int64_t *ids, int64_t ids_capacity, int64_t *k_host, int64_t *e_host);
 
+/* ---- render_backward (rasterizer.py:229-354, _raster_kernels.py:204-310) -- */
+/* Analytic gradients of render(splats, cam, mode) w.r.t. every splat
+ * parameter. upstream: dL/d(plane), (H,W,3) float64 device (depth: channel 0
+ * used). Outputs (n,3)/(n,4)/(n,) float64 device, zeros for culled splats;
+ * d_colors is written for mode rgb, d_normals for mode normal (either may be
+ * NULL otherwise). mode: 0 rgb (background composited), 1 normal, 2 depth.
+ * tile_size <= 16. */
+int sfb_render_backward(sfb_ctx *ctx, const sfb_splats *splats, const sfb_camera *cam,
+                        const sfb_render_options *opts, int32_t mode, const double *background3,
+                        const double *upstream, double *d_centers, double *d_scales,
+                        double *d_quaternions, double *d_opacities, double *d_colors,
+                        double *d_normals);
+
 /* ---- render_pose epilogue (service.py:116-136, rasterizer.py:209-226) ------ */
 /* RGBA8 output of service.render_pose: mode rgb -> to_rgba(rgb, T); normal ->
  * to_rgba(normal*0.5+0.5, T); relit -> to_rgba(relight(normal, rgb, light,

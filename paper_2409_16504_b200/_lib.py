@@ -82,6 +82,8 @@ SIGNATURES = {
                           I64, ctypes.POINTER(I64), ctypes.POINTER(I64)],
     "sfb_frame": [P, P, P, I64, D, P, ctypes.POINTER(Camera_t), ctypes.POINTER(RenderOptions_t),
                   I32, P, P, P, P, P],
+    "sfb_render_backward": [P, ctypes.POINTER(Splats_t), ctypes.POINTER(Camera_t),
+                            ctypes.POINTER(RenderOptions_t), I32, P, P, P, P, P, P, P, P],
     "sfb_render_rgba": [P, ctypes.POINTER(Splats_t), ctypes.POINTER(Camera_t),
                         ctypes.POINTER(RenderOptions_t), ctypes.POINTER(Shading_t), P, P],
     "sfb_frame_rgba": [P, P, P, I64, D, P, ctypes.POINTER(Camera_t),

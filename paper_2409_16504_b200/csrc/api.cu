@@ -468,6 +468,22 @@ int sfb_render(sfb_ctx *ctx, const sfb_splats *splats, const sfb_camera *cam,
     });
 }
 
+int sfb_render_backward(sfb_ctx *ctx, const sfb_splats *splats, const sfb_camera *cam,
+                        const sfb_render_options *opts, int32_t mode, const double *bg,
+                        const double *upstream, double *d_centers, double *d_scales,
+                        double *d_quaternions, double *d_opacities, double *d_colors,
+                        double *d_normals) {
+    return guard(ctx, [&] {
+        SFB_REQUIRE(splats && cam && opts && upstream, "null argument");
+        SFB_REQUIRE(d_centers && d_scales && d_quaternions && d_opacities, "null gradient buffer");
+        FrameParams *P = params(ctx, camera_params(cam, bg));
+        DevCounts *C = new_counts(ctx);
+        render_backward_run(ctx, splat_inputs(splats), P, cam->width, cam->height, *opts, mode, C,
+                            upstream, d_centers, d_scales, d_quaternions, d_opacities, d_colors,
+                            d_normals);
+    });
+}
+
 int sfb_render_rgba(sfb_ctx *ctx, const sfb_splats *splats, const sfb_camera *cam,
                     const sfb_render_options *opts, const sfb_shading *shading, const double *bg,
                     uint8_t *rgba) {

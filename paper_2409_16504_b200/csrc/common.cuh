@@ -375,6 +375,10 @@ void project_run(sfb_ctx *ctx, const double *centers, const double *quats, const
                  const int64_t *d_n, int64_t n_bound, const FrameParams *FP, double z_near,
                  double dilation, double *sx, double *sy, double *depth, double *ca, double *cb,
                  double *cc, double *radius, uint8_t *keep);
+void render_backward_run(sfb_ctx *ctx, const RenderInputs &in, const FrameParams *FP, int64_t width,
+                         int64_t height, const sfb_render_options &opts, int mode, DevCounts *C,
+                         const double *upstream, double *d_centers, double *d_scales,
+                         double *d_quats, double *d_opac, double *d_colors, double *d_normals);
 void prepare_debug_run(sfb_ctx *ctx, const RenderInputs &in, const FrameParams *FP, int64_t width,
                        int64_t height, int tile, DevCounts *C, int64_t *source, double *radius,
                        int64_t *offsets, int64_t *ids, int64_t cap, int64_t *k_host,

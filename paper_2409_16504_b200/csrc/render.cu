@@ -26,6 +26,7 @@
 //      reference, whose per-pixel skip makes all later splats no-ops.
 #include <cub/cub.cuh>
 #include <cstddef>
+#include <utility>
 
 #include "common.cuh"
 
@@ -1390,53 +1391,414 @@ __global__ void k_widen32(const int32_t *__restrict__ a, int64_t n, int64_t *__r
     SFB_FOR(j, n) b[j] = a[j];
 }
 
-// The reference CSR (for parity tests only): host-synchronising by design.
+// The reference CSR of _prepare + bin_tiles (rasterizer.py:99-130,
+// _raster_kernels.py:108-143): rank -> splat, per-rank support radius, per-tile
+// offsets and rank lists. Host-synchronising by design (it sizes buffers from
+// K and E); used by the parity seam and by render_backward.
+struct Csr {
+    Proj P;
+    uint32_t *src = nullptr;        // rank -> splat (first K)
+    int64_t K = 0, E = 0;
+    double *radius = nullptr;       // per rank
+    int32_t *toff = nullptr;        // (nt+1) tile offsets
+    const uint32_t *ids = nullptr;  // (E) ranks, tile-major, ascending within a tile
+    int64_t ntx = 0, nty = 0;
+};
+
+static Csr build_csr(sfb_ctx *ctx, const RenderInputs &in, const FrameParams *FP, int64_t width,
+                     int64_t height, int tile, DevCounts *C, int64_t *source) {
+    cudaStream_t st = ctx->stream;
+    Csr R;
+    R.ntx = (width + tile - 1) / tile;
+    R.nty = (height + tile - 1) / tile;
+    const int64_t nt = R.ntx * R.nty;
+    R.P = project_inputs(ctx, in, FP);
+    R.toff = ctx->arena.alloc<int32_t>(nt + 1);
+    SFB_CUDA(cudaMemsetAsync(R.toff, 0, sizeof(int32_t) * (nt + 1), st));
+    if (in.n_points > 0) {
+        R.src = depth_order(ctx, in, R.P, C);
+        ctx->read_back(&C->kept, sizeof(int64_t));
+        R.K = ctx->pinned[0];
+    }
+    if (R.K == 0) return R;
+    const int64_t K = R.K;
+    int4 *rect = ctx->arena.alloc<int4>(K);
+    int32_t *cnt = ctx->arena.alloc<int32_t>(K + 1);
+    int32_t *pos = ctx->arena.alloc<int32_t>(K + 1);
+    R.radius = ctx->arena.alloc<double>(K);
+    int64_t *src64 = source ? source : ctx->arena.alloc<int64_t>(K);
+    SFB_CUDA(cudaMemsetAsync(cnt, 0, sizeof(int32_t) * (K + 1), st));
+    k_rank_rects<<<dgrid(K, 256), 256, 0, st>>>(R.src, K, in.point_to_geom, R.P, in.opac, (double)tile,
+                                                R.ntx, R.nty, R.radius, rect, cnt, src64);
+    dscan(ctx, cnt, pos, nullptr, K + 1, &C->scratch[0], false);
+    ctx->read_back(&C->scratch[0], sizeof(int64_t));
+    R.E = ctx->pinned[0];
+    SFB_REQUIRE(R.E < (int64_t(1) << 31), "CSR larger than 2^31 entries");
+    const int64_t E = R.E;
+    uint32_t *key = ctx->arena.alloc<uint32_t>(E + 1), *val = ctx->arena.alloc<uint32_t>(E + 1);
+    uint32_t *key2 = ctx->arena.alloc<uint32_t>(E + 1), *val2 = ctx->arena.alloc<uint32_t>(E + 1);
+    k_rank_emit<<<dgrid(K, 256), 256, 0, st>>>(rect, pos, K, R.ntx, key, val);
+    SFB_CHECK_LAUNCH();
+    const int bits = bits_for((uint64_t)nt);
+    const bool second = dsort_pairs<uint32_t>(ctx, key, val, key2, val2, nullptr, E, bits);
+    const uint32_t *ks = second ? key2 : key;
+    R.ids = second ? val2 : val;
+    k_histogram<<<dgrid(E, 256), 256, 0, st>>>(ks, &C->scratch[0], R.toff);
+    dscan(ctx, R.toff, R.toff, nullptr, nt + 1, nullptr, false);
+    SFB_CHECK_LAUNCH();
+    return R;
+}
+
 void prepare_debug_run(sfb_ctx *ctx, const RenderInputs &in, const FrameParams *FP, int64_t width,
                        int64_t height, int tile, DevCounts *C, int64_t *source, double *radius,
                        int64_t *offsets, int64_t *ids, int64_t cap, int64_t *k_host,
                        int64_t *e_host) {
     cudaStream_t st = ctx->stream;
-    const int64_t ntx = (width + tile - 1) / tile, nty = (height + tile - 1) / tile;
-    const int64_t nt = ntx * nty;
-    Proj P = project_inputs(ctx, in, FP);
-    int32_t *toff = ctx->arena.alloc<int32_t>(nt + 1);
-    SFB_CUDA(cudaMemsetAsync(toff, 0, sizeof(int32_t) * (nt + 1), st));
-    int64_t K = 0;
-    uint32_t *src = nullptr;
-    if (in.n_points > 0) {
-        src = depth_order(ctx, in, P, C);
-        ctx->read_back(&C->kept, sizeof(int64_t));
-        K = ctx->pinned[0];
+    Csr R = build_csr(ctx, in, FP, width, height, tile, C, source);
+    const int64_t nt = R.ntx * R.nty;
+    *k_host = R.K;
+    *e_host = R.E;
+    k_widen32<<<dgrid(nt + 1, 256), 256, 0, st>>>(R.toff, nt + 1, offsets);
+    if (R.K > 0) {
+        SFB_CUDA(cudaMemcpyAsync(radius, R.radius, sizeof(double) * R.K, cudaMemcpyDeviceToDevice, st));
+        if (R.E <= cap && ids) k_widen<<<dgrid(R.E, 256), 256, 0, st>>>(R.ids, R.E, ids);
     }
-    *k_host = K;
-    if (K == 0) {
-        *e_host = 0;
-        k_widen32<<<dgrid(nt + 1, 256), 256, 0, st>>>(toff, nt + 1, offsets);
-        SFB_CHECK_LAUNCH();
-        return;
+    SFB_CHECK_LAUNCH();
+}
+
+// ------------------------------------------------------------ render_backward
+// Analytic gradients of render() (rasterizer.py:229-354). Per-rank inputs of
+// the reference's backward_kernel (_raster_kernels.py:204-310) in rank order.
+struct BwdRank {
+    double *sx, *sy, *ia, *ib, *ic, *op, *attr;   // attr (K,3)
+};
+
+__global__ void k_bwd_rank_inputs(const Proj P, const uint32_t *__restrict__ src, int64_t K,
+                                  const double *__restrict__ opac, const double *__restrict__ colors,
+                                  const double *__restrict__ normals, int mode, BwdRank B) {
+    SFB_FOR(j, K) {
+        const int64_t i = src[j];
+        const double a = P.a[i], b = P.b[i], c = P.c[i];
+        const double det = a * c - b * b;
+        B.sx[j] = P.sx[i];
+        B.sy[j] = P.sy[i];
+        B.ia[j] = c / det;
+        B.ib[j] = -b / det;
+        B.ic[j] = a / det;
+        B.op[j] = opac[i];
+        for (int k = 0; k < 3; ++k)
+            B.attr[3 * j + k] = mode == 0 ? colors[3 * i + k]
+                                : mode == 1 ? normals[3 * i + k] : (k == 0 ? P.depth[i] : 0.0);
     }
-    int4 *rect = ctx->arena.alloc<int4>(K);
-    int32_t *cnt = ctx->arena.alloc<int32_t>(K + 1);
-    int32_t *pos = ctx->arena.alloc<int32_t>(K + 1);
-    SFB_CUDA(cudaMemsetAsync(cnt, 0, sizeof(int32_t) * (K + 1), st));
-    k_rank_rects<<<dgrid(K, 256), 256, 0, st>>>(src, K, in.point_to_geom, P, in.opac, (double)tile,
-                                                ntx, nty, radius, rect, cnt, source);
-    dscan(ctx, cnt, pos, nullptr, K + 1, &C->scratch[0], false);
-    ctx->read_back(&C->scratch[0], sizeof(int64_t));
-    const int64_t E = ctx->pinned[0];
-    *e_host = E;
-    SFB_REQUIRE(E < (int64_t(1) << 31), "debug CSR larger than 2^31 entries");
+}
+
+// block-wide sum of NV doubles in a fixed order (warp trees, then warps in
+// order): deterministic run to run
+template <int NV>
+__device__ __forceinline__ void block_sum(double (&v)[NV], double (*s_part)[NV], double *out) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+    for (int k = 0; k < NV; ++k)
+        for (int o = 16; o; o >>= 1) v[k] += __shfl_down_sync(0xffffffffu, v[k], o);
+    if (lane == 0)
+#pragma unroll
+        for (int k = 0; k < NV; ++k) s_part[warp][k] = v[k];
+    __syncthreads();
+    if (threadIdx.x < NV) {
+        double t = 0.0;
+        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += s_part[w][threadIdx.x];
+        out[threadIdx.x] = t;
+    }
+    __syncthreads();
+}
+
+// One CTA per tile, one thread per pixel (tile <= 16): forward replay of the
+// tile list, then the reverse sweep walked in lockstep over the entries; the
+// 9 per-entry partials (g_attr 3, g_opac, g_q 3, g_mu 2) are block-summed.
+__global__ void __launch_bounds__(256)
+k_backward(int64_t W, int64_t H, int tile, int64_t ntx, const int32_t *__restrict__ toff,
+           const uint32_t *__restrict__ ids, BwdRank B, double alpha_max, int terminate, int mode,
+           const FrameParams *__restrict__ FP, const double *__restrict__ upstream,
+           double *__restrict__ g_ent /* (E, 9) */) {
+    __shared__ double s_part[8][9];
+    __shared__ double s_out[9];
+    __shared__ int s_elast;
+    const int64_t t = blockIdx.x;
+    const int64_t tx = t % ntx, ty = t / ntx;
+    const int64_t px = tx * tile + threadIdx.x % tile, py = ty * tile + threadIdx.x / tile;
+    const bool valid = (int)threadIdx.x < tile * tile && px < W && py < H;
+    const int64_t start = toff[t], end = toff[t + 1];
+    double tr = 1.0, n0 = 0.0, n1 = 0.0, n2 = 0.0;
+    int64_t e_last = start - 1;
+    if (valid)
+        for (int64_t e = start; e < end; ++e) {
+            const uint32_t s = ids[e];
+            const double dx = (double)px - B.sx[s], dy = (double)py - B.sy[s];
+            const double q = B.ia[s] * dx * dx + 2.0 * B.ib[s] * dx * dy + B.ic[s] * dy * dy;
+            double alpha = B.op[s] * exp(-0.5 * q);
+            if (alpha > alpha_max) alpha = alpha_max;
+            if (alpha < kCutoff) continue;
+            const double w = tr * alpha;
+            n0 += w * B.attr[3 * s];
+            n1 += w * B.attr[3 * s + 1];
+            n2 += w * B.attr[3 * s + 2];
+            tr *= 1.0 - alpha;
+            e_last = e;
+            if (terminate && tr < kCutoff) break;
+        }
+    const double t_fin = tr;
+    double u0 = 0.0, u1 = 0.0, u2 = 0.0, d_tfin = 0.0;
+    if (valid) {
+        const double *up = upstream + 3 * (py * W + px);
+        u0 = up[0];
+        u1 = up[1];
+        u2 = up[2];
+        if (mode == 1) {
+            const double nn = sqrt(n0 * n0 + n1 * n1 + n2 * n2);
+            if (nn > 1e-12) {
+                const double dot = (n0 * u0 + n1 * u1 + n2 * u2) / (nn * nn * nn);
+                u0 = u0 / nn - n0 * dot;
+                u1 = u1 / nn - n1 * dot;
+                u2 = u2 / nn - n2 * dot;
+            }
+        }
+        if (mode == 0) d_tfin = u0 * FP->bg[0] + u1 * FP->bg[1] + u2 * FP->bg[2];
+    }
+    const bool live = valid && !(u0 == 0.0 && u1 == 0.0 && u2 == 0.0);
+    if (!live) e_last = start - 1;
+    // lockstep reverse sweep from the largest e_last of the tile
+    if (threadIdx.x == 0) s_elast = (int)(start - 1);
+    __syncthreads();
+    if (e_last >= start) atomicMax(&s_elast, (int)e_last);
+    __syncthreads();
+    const int64_t e_top = s_elast;
+    double s0 = 0.0, s1 = 0.0, s2 = 0.0, t_next = t_fin;
+    for (int64_t e = e_top; e >= start; --e) {
+        double v[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
+        bool any = false;
+        if (e <= e_last) {
+            const uint32_t s = ids[e];
+            const double dx = (double)px - B.sx[s], dy = (double)py - B.sy[s];
+            const double ia = B.ia[s], ib = B.ib[s], ic = B.ic[s], op = B.op[s];
+            const double q = ia * dx * dx + 2.0 * ib * dx * dy + ic * dy * dy;
+            const double g = exp(-0.5 * q);
+            const double raw = op * g;
+            const bool clamped = raw > alpha_max;
+            const double alpha = clamped ? alpha_max : raw;
+            if (!(alpha < kCutoff)) {
+                any = true;
+                const double one_m = 1.0 - alpha;
+                const double t_k = t_next / one_m;
+                const double w = t_k * alpha;
+                const double a0 = B.attr[3 * s], a1 = B.attr[3 * s + 1], a2 = B.attr[3 * s + 2];
+                v[0] = u0 * w;
+                v[1] = u1 * w;
+                v[2] = u2 * w;
+                const double d_alpha = (u0 * (t_k * a0 - s0 / one_m) + u1 * (t_k * a1 - s1 / one_m) +
+                                        u2 * (t_k * a2 - s2 / one_m) - d_tfin * t_fin / one_m);
+                if (!clamped) {
+                    v[3] = d_alpha * g;
+                    const double d_q = -0.5 * op * g * d_alpha;
+                    v[4] = d_q * dx * dx;
+                    v[5] = d_q * 2.0 * dx * dy;
+                    v[6] = d_q * dy * dy;
+                    v[7] = -(d_q * 2.0 * (ia * dx + ib * dy));
+                    v[8] = -(d_q * 2.0 * (ib * dx + ic * dy));
+                }
+                s0 += w * a0;
+                s1 += w * a1;
+                s2 += w * a2;
+                t_next = t_k;
+            }
+        }
+        if (!__syncthreads_or(any)) continue;
+        block_sum<9>(v, s_part, s_out);
+        if (threadIdx.x < 9) g_ent[9 * e + threadIdx.x] = s_out[threadIdx.x];
+    }
+}
+
+// per rank: sum of its entries' slots in CSR order (np.add.at walks ids in order)
+__global__ void k_bwd_reduce(const uint32_t *__restrict__ ent_sorted, const int32_t *__restrict__ roff,
+                             int64_t K, const double *__restrict__ g_ent, double *__restrict__ g_rank) {
+    SFB_FOR(j, K) {
+        double acc[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
+        for (int32_t q = roff[j]; q < roff[j + 1]; ++q) {
+            const double *g = g_ent + 9 * (size_t)ent_sorted[q];
+#pragma unroll
+            for (int k = 0; k < 9; ++k) acc[k] += g[k];
+        }
+#pragma unroll
+        for (int k = 0; k < 9; ++k) g_rank[9 * j + k] = acc[k];
+    }
+}
+
+// chain rule per rank (rasterizer.py:286-354): inverse-covariance partials ->
+// screen covariance -> EWA Jacobian / camera point -> world covariance ->
+// scales and the normalised quaternion; written at the splat's input index
+__global__ void k_bwd_chain(const uint32_t *__restrict__ src, int64_t K, const double *__restrict__ g_rank,
+                            const BwdRank B, const double *__restrict__ centers,
+                            const double *__restrict__ scales, const double *__restrict__ quats,
+                            const FrameParams *__restrict__ FP, int mode, double *__restrict__ d_centers,
+                            double *__restrict__ d_scales, double *__restrict__ d_quats,
+                            double *__restrict__ d_opac, double *__restrict__ d_colors,
+                            double *__restrict__ d_normals) {
+    const Cam C = FP->cam;
+    SFB_FOR(j, K) {
+        const int64_t i = src[j];
+        const double *g = g_rank + 9 * j;   // attr 0-2, opac 3, q 4-6, mu 7-8
+        const double ia = B.ia[j], ib = B.ib[j], ic = B.ic[j];
+        const double im[2][2] = {{ia, ib}, {ib, ic}};
+        const double gi[2][2] = {{g[4], 0.5 * g[5]}, {0.5 * g[5], g[6]}};
+        double tmp[2][2], gcov[2][2];
+        for (int r = 0; r < 2; ++r)
+            for (int c = 0; c < 2; ++c) tmp[r][c] = im[r][0] * gi[0][c] + im[r][1] * gi[1][c];
+        for (int r = 0; r < 2; ++r)
+            for (int c = 0; c < 2; ++c) gcov[r][c] = -(tmp[r][0] * im[0][c] + tmp[r][1] * im[1][c]);
+        const double *R = C.r;
+        const double *ce = centers + 3 * i;
+        double pc[3];
+        for (int r = 0; r < 3; ++r) pc[r] = ce[0] * R[3 * r] + ce[1] * R[3 * r + 1] + ce[2] * R[3 * r + 2] + C.t[r];
+        const double x = pc[0], y = pc[1], z = pc[2];
+        double jac[2][3] = {{C.fx / z, 0.0, -C.fx * x / (z * z)}, {0.0, C.fy / z, -C.fy * y / (z * z)}};
+        double a2m[2][3];
+        for (int r = 0; r < 2; ++r)
+            for (int c = 0; c < 3; ++c)
+                a2m[r][c] = jac[r][0] * R[c] + jac[r][1] * R[3 + c] + jac[r][2] * R[6 + c];
+        double gs3[3][3];
+        for (int a = 0; a < 3; ++a)
+            for (int m = 0; m < 3; ++m) {
+                double acc = 0.0;
+                for (int jj = 0; jj < 2; ++jj)
+                    for (int l = 0; l < 2; ++l) acc += a2m[jj][a] * gcov[jj][l] * a2m[l][m];
+                gs3[a][m] = acc;
+            }
+        // rotation of the (normalised) quaternion, sigma3 = rot^T diag(s^2) rot
+        const double *qq = quats + 4 * i;
+        const double qn = sqrt(qq[0] * qq[0] + qq[1] * qq[1] + qq[2] * qq[2] + qq[3] * qq[3]);
+        const double w = qq[0] / qn, qx = qq[1] / qn, qy = qq[2] / qn, qz = qq[3] / qn;
+        const double rot[3][3] = {{1 - 2 * (qy * qy + qz * qz), 2 * (qx * qy - w * qz), 2 * (qx * qz + w * qy)},
+                                  {2 * (qx * qy + w * qz), 1 - 2 * (qx * qx + qz * qz), 2 * (qy * qz - w * qx)},
+                                  {2 * (qx * qz - w * qy), 2 * (qy * qz + w * qx), 1 - 2 * (qx * qx + qy * qy)}};
+        const double *sc = scales + 3 * i;
+        const double s2[3] = {sc[0] * sc[0], sc[1] * sc[1], sc[2] * sc[2]};
+        double sig[3][3];
+        for (int a = 0; a < 3; ++a)
+            for (int l = 0; l < 3; ++l)
+                sig[a][l] = rot[0][a] * s2[0] * rot[0][l] + rot[1][a] * s2[1] * rot[1][l] + rot[2][a] * s2[2] * rot[2][l];
+        double mcam[3][3];
+        for (int a = 0; a < 3; ++a)
+            for (int m = 0; m < 3; ++m) {
+                double acc = 0.0;
+                for (int jj = 0; jj < 3; ++jj)
+                    for (int l = 0; l < 3; ++l) acc += R[3 * a + jj] * sig[jj][l] * R[3 * m + l];
+                mcam[a][m] = acc;
+            }
+        double gjac[2][3];
+        for (int a = 0; a < 2; ++a)
+            for (int m = 0; m < 3; ++m) {
+                double acc = 0.0;
+                for (int jj = 0; jj < 2; ++jj)
+                    for (int l = 0; l < 3; ++l) acc += gcov[a][jj] * jac[jj][l] * mcam[l][m];
+                gjac[a][m] = 2.0 * acc;
+            }
+        double dp[3];
+        dp[0] = gjac[0][2] * (-C.fx / (z * z));
+        dp[1] = gjac[1][2] * (-C.fy / (z * z));
+        dp[2] = gjac[0][0] * (-C.fx / (z * z)) + gjac[0][2] * (2.0 * C.fx * x / (z * z * z)) +
+                gjac[1][1] * (-C.fy / (z * z)) + gjac[1][2] * (2.0 * C.fy * y / (z * z * z));
+        dp[0] += g[7] * C.fx / z;
+        dp[1] += g[8] * C.fy / z;
+        dp[2] += g[7] * (-C.fx * x / (z * z)) + g[8] * (-C.fy * y / (z * z));
+        if (mode == 2) dp[2] += g[0];
+        for (int c = 0; c < 3; ++c) d_centers[3 * i + c] = dp[0] * R[c] + dp[1] * R[3 + c] + dp[2] * R[6 + c];
+        // g_d = rot gs3 rot^T ; d_scales = 2 s diag(g_d)
+        for (int a = 0; a < 3; ++a) {
+            double acc = 0.0;
+            for (int jj = 0; jj < 3; ++jj)
+                for (int l = 0; l < 3; ++l) acc += rot[a][jj] * gs3[jj][l] * rot[a][l];
+            d_scales[3 * i + a] = 2.0 * sc[a] * acc;
+        }
+        // g_r = 2 s^2 (rot gs3); d_qhat = <g_r, dR/dq>
+        double gr[3][3];
+        for (int a = 0; a < 3; ++a)
+            for (int c = 0; c < 3; ++c)
+                gr[a][c] = 2.0 * s2[a] * (rot[a][0] * gs3[0][c] + rot[a][1] * gs3[1][c] + rot[a][2] * gs3[2][c]);
+        const double dr[4][9] = {{0, -qz, qy, qz, 0, -qx, -qy, qx, 0},
+                                 {0, qy, qz, qy, -2 * qx, -w, qz, w, -2 * qx},
+                                 {-2 * qy, qx, w, qx, 0, qz, -w, qz, -2 * qy},
+                                 {-2 * qz, -w, qx, w, -2 * qz, qy, qx, qy, 0}};
+        double dq[4];
+        for (int k = 0; k < 4; ++k) {
+            double acc = 0.0;
+            for (int e = 0; e < 9; ++e) acc += gr[e / 3][e % 3] * 2.0 * dr[k][e];
+            dq[k] = acc;
+        }
+        const double qh[4] = {w, qx, qy, qz};
+        const double dot = qh[0] * dq[0] + qh[1] * dq[1] + qh[2] * dq[2] + qh[3] * dq[3];
+        for (int k = 0; k < 4; ++k) d_quats[4 * i + k] = (dq[k] - qh[k] * dot) / qn;
+        d_opac[i] = g[3];
+        if (mode == 0 && d_colors)
+            for (int c = 0; c < 3; ++c) d_colors[3 * i + c] = g[c];
+        if (mode == 1 && d_normals)
+            for (int c = 0; c < 3; ++c) d_normals[3 * i + c] = g[c];
+    }
+}
+
+__global__ void k_upcast_ranks(const uint32_t *__restrict__ ids, int64_t E, uint32_t *__restrict__ key,
+                               uint32_t *__restrict__ val) {
+    SFB_FOR(e, E) {
+        key[e] = ids[e];
+        val[e] = (uint32_t)e;
+    }
+}
+
+void render_backward_run(sfb_ctx *ctx, const RenderInputs &in, const FrameParams *FP, int64_t width,
+                         int64_t height, const sfb_render_options &opts, int mode, DevCounts *C,
+                         const double *upstream, double *d_centers, double *d_scales,
+                         double *d_quats, double *d_opac, double *d_colors, double *d_normals) {
+    SFB_REQUIRE(mode >= 0 && mode <= 2, "mode must be rgb, normal or depth");
+    SFB_REQUIRE(opts.tile_size >= 1 && opts.tile_size <= 16, "render_backward supports tile_size <= 16");
+    cudaStream_t st = ctx->stream;
+    const int64_t n = in.n_points;
+    for (auto pr : {std::make_pair(d_centers, 3), std::make_pair(d_scales, 3), std::make_pair(d_quats, 4),
+                    std::make_pair(d_opac, 1), std::make_pair(d_colors, 3), std::make_pair(d_normals, 3)})
+        if (pr.first) SFB_CUDA(cudaMemsetAsync(pr.first, 0, sizeof(double) * pr.second * (size_t)n, st));
+    if (n == 0) return;
+    Csr R = build_csr(ctx, in, FP, width, height, opts.tile_size, C, nullptr);
+    if (R.K == 0) return;
+    const int64_t K = R.K, E = R.E;
+    BwdRank B;
+    double *blk = ctx->arena.alloc<double>(9 * (size_t)K);
+    B.sx = blk;
+    B.sy = blk + K;
+    B.ia = blk + 2 * K;
+    B.ib = blk + 3 * K;
+    B.ic = blk + 4 * K;
+    B.op = blk + 5 * K;
+    B.attr = blk + 6 * K;
+    k_bwd_rank_inputs<<<dgrid(K, 256), 256, 0, st>>>(R.P, R.src, K, in.opac, in.colors, in.normals, mode, B);
+    double *g_ent = ctx->arena.alloc<double>(9 * (size_t)(E > 0 ? E : 1));
+    SFB_CUDA(cudaMemsetAsync(g_ent, 0, sizeof(double) * 9 * (size_t)(E > 0 ? E : 1), st));
+    k_backward<<<(unsigned)(R.ntx * R.nty), 256, 0, st>>>(width, height, opts.tile_size, R.ntx, R.toff,
+                                                         R.ids, B, opts.alpha_max, opts.early_termination,
+                                                         mode, FP, upstream, g_ent);
+    SFB_CHECK_LAUNCH();
+    // entries -> ranks in CSR order: stable sort of (rank, entry)
     uint32_t *key = ctx->arena.alloc<uint32_t>(E + 1), *val = ctx->arena.alloc<uint32_t>(E + 1);
     uint32_t *key2 = ctx->arena.alloc<uint32_t>(E + 1), *val2 = ctx->arena.alloc<uint32_t>(E + 1);
-    k_rank_emit<<<dgrid(K, 256), 256, 0, st>>>(rect, pos, K, ntx, key, val);
-    SFB_CHECK_LAUNCH();
-    const int bits = bits_for((uint64_t)nt);
-    const bool second = dsort_pairs<uint32_t>(ctx, key, val, key2, val2, nullptr, E, bits);
+    k_upcast_ranks<<<dgrid(E, 256), 256, 0, st>>>(R.ids, E, key, val);
+    const bool second = dsort_pairs<uint32_t>(ctx, key, val, key2, val2, nullptr, E,
+                                              bits_for((uint64_t)K));
     const uint32_t *ks = second ? key2 : key, *vs = second ? val2 : val;
-    k_histogram<<<dgrid(E, 256), 256, 0, st>>>(ks, &C->scratch[0], toff);
-    dscan(ctx, toff, toff, nullptr, nt + 1, nullptr, false);
-    k_widen32<<<dgrid(nt + 1, 256), 256, 0, st>>>(toff, nt + 1, offsets);
-    if (E <= cap && ids) k_widen<<<dgrid(E, 256), 256, 0, st>>>(vs, E, ids);
+    int32_t *roff = ctx->arena.alloc<int32_t>(K + 1);
+    SFB_CUDA(cudaMemsetAsync(roff, 0, sizeof(int32_t) * (K + 1), st));
+    k_histogram<<<dgrid(E, 256), 256, 0, st>>>(ks, &C->scratch[0], roff);   // scratch[0] = E
+    dscan(ctx, roff, roff, nullptr, K + 1, nullptr, false);
+    double *g_rank = ctx->arena.alloc<double>(9 * (size_t)K);
+    k_bwd_reduce<<<dgrid(K, 256), 256, 0, st>>>(vs, roff, K, g_ent, g_rank);
+    k_bwd_chain<<<dgrid(K, 128), 128, 0, st>>>(R.src, K, g_rank, B, in.centers, in.scales, in.quats, FP,
+                                              mode, d_centers, d_scales, d_quats, d_opac, d_colors,
+                                              d_normals);
     SFB_CHECK_LAUNCH();
 }
 

@@ -152,3 +152,48 @@ def relight(normal_fb: FrameBuffer, rgb_fb: FrameBuffer, light_dir, ambient: flo
     shaded = rgb * (ambient + diffuse * lam)[:, :, None]
     passthrough = (rgb_fb.transmittance > 0.999)[:, :, None]
     return torch.clamp(torch.where(passthrough, rgb, shaded), 0.0, 1.0)
+
+
+@dataclass(eq=False)
+class RenderGradients:
+    """Loss partials per input splat (rasterizer.py:59-68); culled splats hold zeros."""
+
+    d_centers: torch.Tensor
+    d_scales: torch.Tensor
+    d_quaternions: torch.Tensor
+    d_opacities: torch.Tensor
+    d_colors: torch.Tensor
+    d_normals: torch.Tensor
+
+
+def render_backward(splats: Splats, cam: Camera, upstream, mode: str = "rgb",
+                    background=(0.0, 0.0, 0.0), options: RenderOptions = None) -> RenderGradients:
+    """Analytic gradients of render() w.r.t. every splat parameter
+    (rasterizer.py:229-354). ``upstream`` is dL/d(plane): (H, W, 3) for rgb and
+    normal, (H, W) for depth (numpy or CUDA tensor)."""
+    _check(cam, mode)
+    options = options or RenderOptions()
+    if int(options.tile_size) > 16:
+        raise ValueError("render_backward supports tile_size <= 16")
+    dev = splats.centers.device
+    h, w = int(cam.height), int(cam.width)
+    up = upstream if isinstance(upstream, torch.Tensor) else torch.from_numpy(np.asarray(upstream))
+    up = up.to(device=dev, dtype=torch.float64)
+    if mode == "depth" and tuple(up.shape) == (h, w):
+        lifted = torch.zeros((h, w, 3), dtype=torch.float64, device=dev)
+        lifted[:, :, 0] = up
+        up = lifted
+    if tuple(up.shape) != (h, w, 3):
+        raise ValueError("upstream shape must match the rendered plane")
+    up = up.contiguous()
+    n = len(splats)
+    z = lambda *shape: torch.zeros(shape, dtype=torch.float64, device=dev)
+    g = RenderGradients(z(n, 3), z(n, 3), z(n, 4), z(n), z(n, 3), z(n, 3))
+    bg = np.ascontiguousarray(np.asarray(background, dtype=np.float64).reshape(3))
+    s, c, o = splats.struct(), cam.struct(), options.struct()
+    _lib.context().call("sfb_render_backward", _lib.ctypes.byref(s), _lib.ctypes.byref(c),
+                        _lib.ctypes.byref(o), _MODES.index(mode), bg.ctypes.data_as(_lib.P),
+                        _lib.ptr(up), _lib.ptr(g.d_centers), _lib.ptr(g.d_scales),
+                        _lib.ptr(g.d_quaternions), _lib.ptr(g.d_opacities), _lib.ptr(g.d_colors),
+                        _lib.ptr(g.d_normals))
+    return g
