@@ -179,6 +179,19 @@ int sfb_prepare_debug(sfb_ctx *ctx, const sfb_splats *splats, const sfb_camera *
                       int32_t tile_size, int64_t *source, double *radius, int64_t *offsets,
                       int64_t *ids, int64_t ids_capacity, int64_t *k_host, int64_t *e_host);
 
+/* ---- file formats decoded on the device (pcio.py:210-257, gaussians.py:277-311) */
+/* Binary little-endian PLY vertex rows (the file body as read, device bytes)
+ * -> PointCloud arrays: positions (n,3) float64, colors (n,3) = uchar/255,
+ * normals (n,3) renormalised ((0,0,1) below 1e-12) or NULL. offsets_host: byte
+ * offsets of x y z red green blue nx ny nz within a row (-1 = absent). */
+int sfb_ply_decode(sfb_ctx *ctx, const uint8_t *body, int64_t n, int32_t stride,
+                   const int32_t *offsets_host, double *positions, double *colors,
+                   double *normals);
+/* SPL1 cache rows ((n,17) little-endian float32, device) <-> float64 Splats. */
+int sfb_spl1_decode(sfb_ctx *ctx, const float *rows, int64_t n, double *centers, double *scales,
+                    double *quaternions, double *opacities, double *colors, double *normals);
+int sfb_spl1_encode(sfb_ctx *ctx, const sfb_splats *splats, float *rows);
+
 /* ---- render_backward (rasterizer.py:229-354, _raster_kernels.py:204-310) -- */
 /* Analytic gradients of render(splats, cam, mode) w.r.t. every splat
  * parameter. upstream: dL/d(plane), (H,W,3) float64 device (depth: channel 0

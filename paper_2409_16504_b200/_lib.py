@@ -82,6 +82,9 @@ SIGNATURES = {
                           I64, ctypes.POINTER(I64), ctypes.POINTER(I64)],
     "sfb_frame": [P, P, P, I64, D, P, ctypes.POINTER(Camera_t), ctypes.POINTER(RenderOptions_t),
                   I32, P, P, P, P, P],
+    "sfb_ply_decode": [P, P, I64, I32, P, P, P, P],
+    "sfb_spl1_decode": [P, P, I64, P, P, P, P, P, P],
+    "sfb_spl1_encode": [P, ctypes.POINTER(Splats_t), P],
     "sfb_render_backward": [P, ctypes.POINTER(Splats_t), ctypes.POINTER(Camera_t),
                             ctypes.POINTER(RenderOptions_t), I32, P, P, P, P, P, P, P, P],
     "sfb_render_rgba": [P, ctypes.POINTER(Splats_t), ctypes.POINTER(Camera_t),

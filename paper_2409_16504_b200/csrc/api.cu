@@ -468,6 +468,29 @@ int sfb_render(sfb_ctx *ctx, const sfb_splats *splats, const sfb_camera *cam,
     });
 }
 
+int sfb_ply_decode(sfb_ctx *ctx, const uint8_t *body, int64_t n, int32_t stride,
+                   const int32_t *offsets, double *positions, double *colors, double *normals) {
+    return guard(ctx, [&] {
+        SFB_REQUIRE(offsets && positions && colors && (body || n == 0), "null argument");
+        ply_decode_run(ctx, body, n, stride, offsets, positions, colors, normals);
+    });
+}
+
+int sfb_spl1_decode(sfb_ctx *ctx, const float *rows, int64_t n, double *c, double *s, double *q,
+                    double *o, double *col, double *nrm) {
+    return guard(ctx, [&] {
+        SFB_REQUIRE(n == 0 || (rows && c && s && q && o && col && nrm), "null argument");
+        spl1_decode_run(ctx, rows, n, c, s, q, o, col, nrm);
+    });
+}
+
+int sfb_spl1_encode(sfb_ctx *ctx, const sfb_splats *splats, float *rows) {
+    return guard(ctx, [&] {
+        SFB_REQUIRE(splats && (rows || splats->n == 0), "null argument");
+        spl1_encode_run(ctx, *splats, rows);
+    });
+}
+
 int sfb_render_backward(sfb_ctx *ctx, const sfb_splats *splats, const sfb_camera *cam,
                         const sfb_render_options *opts, int32_t mode, const double *bg,
                         const double *upstream, double *d_centers, double *d_scales,

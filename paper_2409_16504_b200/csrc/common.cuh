@@ -354,6 +354,13 @@ void head_to_voxel_splats(sfb_ctx *ctx, const float *raw, const int32_t *coords,
                           const FrameParams *P, double *centers, double *sigma, double *quat,
                           double *opac, double *normal);
 
+// formats.cu
+void ply_decode_run(sfb_ctx *ctx, const uint8_t *body, int64_t n, int32_t stride,
+                    const int32_t *offsets, double *pos, double *col, double *nrm);
+void spl1_decode_run(sfb_ctx *ctx, const float *rows, int64_t n, double *c, double *s, double *q,
+                     double *o, double *col, double *nrm);
+void spl1_encode_run(sfb_ctx *ctx, const sfb_splats &sp, float *rows);
+
 // render.cu
 struct RenderInputs {
     // geometry, either per splat (n rows) or per voxel (geometry rows) with a
