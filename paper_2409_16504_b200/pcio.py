@@ -233,3 +233,54 @@ def save_ply(cloud: PointCloud, path, binary: bool = True) -> None:
                 fh.write(("\n".join(body) + "\n").encode("ascii"))
     except OSError as exc:
         raise OSError(f"cannot write PLY to {path}: {exc}") from exc
+
+
+class PlyBody:
+    """A binary little-endian PLY vertex body kept as the file's own bytes
+    (pinned host memory): what a streaming client ships per frame. The fused
+    pipeline copies these bytes to the device (15 B per vertex without
+    normals, vs 48 B of float64 PointCloud arrays) and decodes them there."""
+
+    ORDER = ("x", "y", "z", "red", "green", "blue", "nx", "ny", "nz")
+
+    def __init__(self, raw: torch.Tensor, count: int, props):
+        self.raw, self.count, self.props = raw, int(count), list(props)
+        offs, stride = {}, 0
+        for p in self.props:
+            offs[p] = stride
+            stride += 4 if p in _FLOATS else 1
+        self.stride = stride
+        self.offsets = [offs.get(p, -1) for p in self.ORDER]
+        self.has_normals = "nx" in offs
+
+    def __len__(self) -> int:
+        return self.count
+
+    @classmethod
+    def from_file(cls, path) -> "PlyBody":
+        import os
+        path = os.fspath(path)
+        with open(path, "rb") as fh:
+            binary, count, props = _header(fh, path)
+            if not binary:
+                raise PlyUnsupportedError(f"{path}: PlyBody needs a binary body")
+            stride = sum(4 if p in _FLOATS else 1 for p in props)
+            raw = fh.read(count * stride)
+        if len(raw) < count * stride:
+            raise PlyParseError(f"{path}: body truncated, expected {count * stride} bytes")
+        return cls(torch.frombuffer(bytearray(raw), dtype=torch.uint8).pin_memory(), count, props)
+
+    @classmethod
+    def from_cloud(cls, cloud: PointCloud) -> "PlyBody":
+        """The body save_ply(cloud, binary=True) would write, in pinned memory."""
+        host = lambda a: a.detach().cpu().numpy() if isinstance(a, torch.Tensor) else np.asarray(a)
+        pos = host(cloud.positions).astype(np.float32)
+        rgb = np.clip(np.rint(host(cloud.colors) * 255.0), 0, 255).astype(np.uint8)
+        props = ["x", "y", "z", "red", "green", "blue"]
+        rec = np.empty(pos.shape[0], dtype=np.dtype([(p, "<f4" if p in _FLOATS else "u1") for p in props]))
+        for a, p in enumerate(("x", "y", "z")):
+            rec[p] = pos[:, a]
+        for a, p in enumerate(("red", "green", "blue")):
+            rec[p] = rgb[:, a]
+        raw = torch.from_numpy(np.frombuffer(rec.tobytes(), dtype=np.uint8).copy()).pin_memory()
+        return cls(raw, pos.shape[0], props)

@@ -14,7 +14,7 @@ import torch
 from . import _lib
 from .gaussians import Camera
 from .netplan import NetworkWeights
-from .pcio import PointCloud
+from .pcio import PlyBody, PointCloud
 from .rasterizer import _PLANE_BIT, FrameBuffer, RenderOptions, _alloc_planes
 from .sparsenet import ensure_loaded
 from .voxelgrid import device_bbox, lattice_scale, stage_cloud
@@ -32,18 +32,22 @@ _upload_streams = {}
 _staging = {}   # (device, lane) -> {"k": next buffer, "bufs": [[pos, col, done_event], ...]}
 
 
-def _upload(cloud: PointCloud, lane: int):
+def _upload(cloud, lane: int):
     dev = torch.cuda.current_device()
     up = _upload_streams.get(dev)
     if up is None:
         up = _upload_streams[dev] = torch.cuda.Stream(device=dev)
-    st = _staging.setdefault((dev, lane), {"k": 0, "bufs": [[None, None, None], [None, None, None]]})
+    st = _staging.setdefault((dev, lane), {"k": 0, "bufs": [[None, None, None, None],
+                                                            [None, None, None, None]]})
     slot = st["bufs"][st["k"]]
     st["k"] ^= 1
-    n = int(cloud.positions.shape[0])
+    ply = isinstance(cloud, PlyBody)
+    n = len(cloud) if ply else int(cloud.positions.shape[0])
     if slot[0] is None or slot[0].shape[0] < n:
         slot[0] = torch.empty((n, 3), dtype=torch.float64, device=dev)
         slot[1] = torch.empty((n, 3), dtype=torch.float64, device=dev)
+    if ply and (slot[3] is None or slot[3].numel() < cloud.raw.numel()):
+        slot[3] = torch.empty(cloud.raw.numel(), dtype=torch.uint8, device=dev)
     pos, col = slot[0][:n], slot[1][:n]
     cur = torch.cuda.current_stream(dev)
     up.wait_stream(cur)   # inputs the caller just wrote on its stream
@@ -55,11 +59,20 @@ def _upload(cloud: PointCloud, lane: int):
             return a
         return torch.from_numpy(np.ascontiguousarray(a))
     with torch.cuda.stream(up):
-        hp = host(cloud.positions)
-        pos.copy_(hp, non_blocking=hp.is_pinned())
-        lo_hi = device_bbox(pos, _UPLOAD_LANE + lane)
-        hc = host(cloud.colors)
-        col.copy_(hc, non_blocking=hc.is_pinned())
+        if ply:   # the file's bytes cross PCIe; widened to float64 on the device
+            body = slot[3][:cloud.raw.numel()]
+            body.copy_(cloud.raw, non_blocking=cloud.raw.is_pinned())
+            layout = (_lib.I32 * 9)(*cloud.offsets)
+            _lib.context(lane=_UPLOAD_LANE + lane).call(
+                "sfb_ply_decode", _lib.ptr(body), n, cloud.stride, layout, _lib.ptr(pos),
+                _lib.ptr(col), _lib.P(0))
+            lo_hi = device_bbox(pos, _UPLOAD_LANE + lane)
+        else:
+            hp = host(cloud.positions)
+            pos.copy_(hp, non_blocking=hp.is_pinned())
+            lo_hi = device_bbox(pos, _UPLOAD_LANE + lane)
+            hc = host(cloud.colors)
+            col.copy_(hc, non_blocking=hc.is_pinned())
         ev = up.record_event()
     cur.wait_event(ev)
     return pos, col, lo_hi, slot
@@ -70,7 +83,7 @@ def prepare_cloud(cloud: PointCloud, lane: int = 0):
     (host clouds go through the upload stream); ``slot`` is the staging buffer
     whose done-event the caller records after its frame (None for device clouds)."""
     slot = None
-    if cloud.on_device:
+    if not isinstance(cloud, PlyBody) and cloud.on_device:
         pos, col = stage_cloud(cloud)
         lo_hi = device_bbox(pos, lane)
     else:

@@ -113,3 +113,16 @@ def test_encode_decode_round_trip_device(c1):
     fields, back = service.decode_frame(blob)
     assert fields["sequence"] == 7 and fields["mode"] == "rgb"
     assert np.array_equal(back, rgba.cpu().numpy())
+
+
+def test_ply_body_frame_equals_cloud_frame(c1):
+    """render_pose_frame fed the binary PLY body (decoded on the device) equals
+    the float64 cloud's frame: integer positions and uint8/255 colours survive
+    the PLY round trip exactly."""
+    from paper_2409_16504_b200.pcio import PlyBody
+    cloud, view, w, est = c1
+    pc = PointCloud(cloud.positions, cloud.colors)
+    pose = FixedPose(view, "relit", (0.0, 0.0, -1.0))
+    a = service.render_pose_frame(PlyBody.from_cloud(pc), w, pose).clone()
+    b = service.render_pose_frame(pc, w, pose)
+    assert torch.equal(a, b)
