@@ -55,6 +55,8 @@ def parse():
     ap.add_argument("--no-profile", action="store_true", help="skip the CUPTI launch count")
     ap.add_argument("--cpu-rows", type=int, default=2, help="tile rows in the CPU sample")
     ap.add_argument("--lanes", type=int, default=4, help="frames in flight per GPU (streams)")
+    ap.add_argument("--net-mode", choices=("tc_tf32x3", "tc_bf16", "simt_f32"), default="tc_tf32x3",
+                    help="P2ENet arithmetic (tc_tf32x3: fp32-accurate parity mode)")
     return ap.parse_args()
 
 
@@ -213,6 +215,8 @@ def run_ours(args):
     cams = [Camera.of(v) for v in views]
     poses = [CameraPose(c, "relit") for c in cams]   # render_pose requests (headlight)
     weights = netplan.init_random(netplan.NetworkPlan(), 0)
+    from paper_2409_16504_b200 import sparsenet
+    sparsenet.set_mode(args.net_mode)
     W, H = cams[0].width, cams[0].height
     planes = ("rgb", "normal")
     lanes = max(1, args.lanes)
@@ -442,7 +446,10 @@ def run_ours(args):
                        "l2": (f"timed region: {copies} distinct 38 MB input copies rotated "
                               f"({copies * 38} MB > 126 MB L2), frames overlapped on {lanes} "
                               "streams; latency: 256 MB L2 flush between frames"),
-                       "net_arithmetic": "tcgen05 3xTF32 (fp32-accurate) conv, fp64 geometry/compositing"},
+                       "net_arithmetic": {"tc_tf32x3": "tcgen05 tf32 hi/lo split (fp32-accurate)",
+                                          "tc_bf16": "tcgen05 bf16 operands, fp32 accumulation",
+                                          "simt_f32": "fp32 FFMA"}[args.net_mode]
+                                         + " convs; fp64 geometry / compositing"},
             "latency_ms_per_frame": lat_ms,
             "e2e": e2e, "gpu_launches": launches, "roofline": roof, "cpu_baseline": cpu,
             "clocks": clk, "stages_ms_eager": stage_ms, "stats": st,

@@ -34,8 +34,11 @@ enum {
 /* Render planes (bit mask for sfb_render). */
 enum { SFB_PLANE_RGB = 1, SFB_PLANE_NORMAL = 2, SFB_PLANE_DEPTH = 4 };
 
-/* P2ENet arithmetic: fp32 SIMT gather-GEMM, or tcgen05 (3xTF32, fp32-accurate). */
-enum { SFB_NET_SIMT_F32 = 0, SFB_NET_TC_TF32X3 = 1 };
+/* P2ENet arithmetic: fp32 SIMT gather-GEMM; tcgen05 tf32 hi/lo split
+ * (fp32-accurate, the default and the parity mode); tcgen05 single bf16
+ * operands with fp32 accumulation (the north star's fast mode; does not meet
+ * the 1e-3 Gaussian-parameter bound). */
+enum { SFB_NET_SIMT_F32 = 0, SFB_NET_TC_TF32X3 = 1, SFB_NET_TC_BF16 = 2 };
 
 typedef struct sfb_ctx sfb_ctx;
 

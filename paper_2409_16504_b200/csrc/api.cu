@@ -370,7 +370,8 @@ int sfb_net_load(sfb_ctx *ctx, const void *blob, size_t nbytes) {
 }
 
 int sfb_net_set_mode(sfb_ctx *ctx, int mode) {
-    if (!ctx || (mode != SFB_NET_SIMT_F32 && mode != SFB_NET_TC_TF32X3)) return SFB_ERR_ARG;
+    if (!ctx || (mode != SFB_NET_SIMT_F32 && mode != SFB_NET_TC_TF32X3 && mode != SFB_NET_TC_BF16))
+        return SFB_ERR_ARG;
     ctx->net_mode = mode;
     return SFB_OK;
 }

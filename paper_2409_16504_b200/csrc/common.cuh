@@ -92,6 +92,7 @@ struct NetLayer {
     float *b = nullptr;  // device, [cout]
     // tcgen05 operands (split tf32 hi/lo, K-major per tap, padded)
     float *w_tc = nullptr;
+    uint16_t *w_bf16 = nullptr;   // single bf16 operands, same canonical layout (fast mode)
     int cin_pad = 0, cout_pad = 0;
 };
 
@@ -162,7 +163,7 @@ struct sfb_ctx {
     }
     ~sfb_ctx() {
         net.release();
-        for (void *p : {(void *)adhoc.w, (void *)adhoc.b, (void *)adhoc.w_tc})
+        for (void *p : {(void *)adhoc.w, (void *)adhoc.b, (void *)adhoc.w_tc, (void *)adhoc.w_bf16})
             if (p) cudaFree(p);
         if (pinned) cudaFreeHost(pinned);
         for (auto &e : ev)

@@ -23,6 +23,8 @@
 //    27 taps are split across CTAs (split-K) to fill the 148 SMs; partial
 //    tiles go to a workspace and a deterministic reduce kernel sums them in
 //    split order, adds the bias and applies ReLU (bitwise run-to-run stable).
+#include <cuda_bf16.h>
+
 #include "common.cuh"
 
 namespace sfb {
@@ -105,6 +107,15 @@ __device__ __forceinline__ void mma_tf32(uint32_t tmem_d, uint64_t a, uint64_t b
         "l"(a), "l"(b), "r"(idesc), "r"(accumulate));
 }
 
+__device__ __forceinline__ void mma_bf16(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t idesc,
+                                         uint32_t accumulate) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+        "l"(a), "l"(b), "r"(idesc), "r"(accumulate));
+}
+
 __device__ __forceinline__ void mma_commit(uint64_t *bar) {
     asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
                      smem_u32(bar))
@@ -125,18 +136,28 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, float *v) {
     for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
 }
 
-template <int KP, int NP>
+// canonical K-major SWIZZLE_NONE offset (bf16 elements): 8-row groups of
+// KP*8 elements, 8-wide k chunks of 64 elements (16-byte core rows)
+__host__ __device__ inline int core_off_bf16(int row, int k, int KP) {
+    return (row >> 3) * (KP * 8) + (k >> 3) * 64 + (row & 7) * 8 + (k & 7);
+}
+
+// BF = false: tf32 operands split hi + lo (fp32-accurate, 4 MMAs per k-step);
+// BF = true: single bf16 operands (the north star's fast mode, 1 MMA)
+template <int KP, int NP, bool BF = false>
 struct TcShape {
-    static constexpr int A_FLOATS = kM * KP;               // one of hi/lo
-    static constexpr int B_FLOATS = NP * KP;
-    static constexpr int STAGE_FLOATS = 2 * A_FLOATS + 2 * B_FLOATS;
+    static constexpr int TERMS = BF ? 1 : 2;
+    static constexpr int A_FLOATS = BF ? kM * KP / 2 : kM * KP;   // one term, in 4-byte words
+    static constexpr int B_FLOATS = BF ? NP * KP / 2 : NP * KP;
+    static constexpr int STAGE_FLOATS = TERMS * A_FLOATS + TERMS * B_FLOATS;
     static constexpr int STAGES = (STAGE_FLOATS * 4 * 2 <= 200 * 1024) ? 2 : 1;
     static constexpr int SMEM = STAGES * STAGE_FLOATS * 4 + 1024 + 64;
     // two accumulators (tap t in buffer t % 2): the epilogue of tap t-1 reads
     // one while the MMAs of tap t write the other
     static constexpr uint32_t TMEM_COLS = 2 * NP <= 32 ? 32 : (2 * NP <= 64 ? 64 : (2 * NP <= 128 ? 128 : 256));
-    static constexpr uint32_t IDESC = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(NP >> 3) << 17) |
-                                      ((uint32_t)(kM >> 4) << 24);
+    // c_format F32; a/b_format TF32 (2) or BF16 (1); N >> 3; M >> 4
+    static constexpr uint32_t IDESC = (1u << 4) | ((BF ? 1u : 2u) << 7) | ((BF ? 1u : 2u) << 10) |
+                                      ((uint32_t)(NP >> 3) << 17) | ((uint32_t)(kM >> 4) << 24);
 };
 
 // split-K factor for a level: the smallest divisor c (<= 32) of the tap count
@@ -154,7 +175,7 @@ __host__ __device__ inline int choose_splits(int64_t tiles, int taps, int target
 constexpr int kSplitTarget = 2 * 148;
 constexpr int64_t kMaxPartialRows = 1480 * 128;
 
-template <int KP, int NP>
+template <int KP, int NP, bool BF>
 __global__ void __launch_bounds__(kThreadsTC)
 k_conv_tc(const float *__restrict__ in, int ld_in, int cin, const int32_t *__restrict__ nbr,
           int64_t nbr_ld, const int64_t *__restrict__ d_m, int64_t m_fixed, int taps,
@@ -165,7 +186,7 @@ k_conv_tc(const float *__restrict__ in, int ld_in, int cin, const int32_t *__res
     // by tap, each bucket padded to whole 128-row tiles (tap_off = 9 padded
     // offsets), nbr[row] is the row's parent (-1 pad), row_map[row] its output
     // row; every tile is ONE tap (K = Cin), so no split-K is needed
-    using S = TcShape<KP, NP>;
+    using S = TcShape<KP, NP, BF>;
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     float *stage_base = reinterpret_cast<float *>(
         (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -262,10 +283,10 @@ k_conv_tc(const float *__restrict__ in, int ld_in, int cin, const int32_t *__res
         // weights: with two stages, tap k+1's tile is fetched (TMA) as soon as
         // batch k-1 has drained, so its latency hides behind tap k
         auto load_w = [&](int t, int slot) {
-            const uint32_t bytes = (uint32_t)(2 * S::B_FLOATS * 4);
-            float *B = stage_base + slot * S::STAGE_FLOATS + 2 * S::A_FLOATS;
+            const uint32_t bytes = (uint32_t)(S::TERMS * S::B_FLOATS * 4);
+            float *B = stage_base + slot * S::STAGE_FLOATS + S::TERMS * S::A_FLOATS;
             mbar_expect_tx(&bar_full[slot], bytes);
-            tma_bulk_g2s(B, wtc + (size_t)t * 2 * S::B_FLOATS, bytes, &bar_full[slot]);
+            tma_bulk_g2s(B, wtc + (size_t)t * S::TERMS * S::B_FLOATS, bytes, &bar_full[slot]);
         };
         int item_issued = 0;
         while (mask) {
@@ -274,8 +295,8 @@ k_conv_tc(const float *__restrict__ in, int ld_in, int cin, const int32_t *__res
             const int s = issued % S::STAGES;
             const int use = issued / S::STAGES;
             float *A_hi = stage_base + s * S::STAGE_FLOATS;
-            float *A_lo = A_hi + S::A_FLOATS;
-            float *B_hi = A_lo + S::A_FLOATS;
+            float *A_lo = A_hi + S::A_FLOATS;                  // tf32 only
+            float *B_hi = A_hi + S::TERMS * S::A_FLOATS;
             // stage free again: the batch that last used it (i - STAGES) has
             // completed. Batch barriers alternate by batch parity, so no wait
             // below can alias a later phase: the next commit to the barrier
@@ -285,7 +306,21 @@ k_conv_tc(const float *__restrict__ in, int ld_in, int cin, const int32_t *__res
                 mbar_wait(&bar_done[j & 1], (j >> 1) & 1);
             }
             if (tid == 0 && (S::STAGES == 1 || item_issued == 0)) load_w(t, s);
-            // split my row of this tap into tf32 hi/lo, canonical layout
+            // my row of this tap in the canonical layout: bf16, or tf32 hi/lo
+            if constexpr (BF) {
+                uint16_t *A16 = reinterpret_cast<uint16_t *>(A_hi);
+#pragma unroll
+                for (int c = 0; c < KP / 8; ++c) {
+                    uint32_t w[4];
+#pragma unroll
+                    for (int h = 0; h < 4; ++h) {
+                        const __nv_bfloat162 b2 = __floats2bfloat162_rn(v[8 * c + 2 * h], v[8 * c + 2 * h + 1]);
+                        w[h] = *reinterpret_cast<const uint32_t *>(&b2);
+                    }
+                    *reinterpret_cast<uint4 *>(A16 + core_off_bf16(tid, 8 * c, KP)) =
+                        make_uint4(w[0], w[1], w[2], w[3]);
+                }
+            } else
 #pragma unroll
             for (int c = 0; c < KP / 4; ++c) {
                 float4 hi, lo;
@@ -308,8 +343,15 @@ k_conv_tc(const float *__restrict__ in, int ld_in, int cin, const int32_t *__res
                 mbar_wait(&bar_full[s], use & 1);
                 asm volatile("tcgen05.fence::after_thread_sync;");
                 const float *B_lo = B_hi + S::B_FLOATS;
-                const uint32_t lbo = 128, sbo = KP * 32;
+                const uint32_t lbo = 128, sbo = BF ? KP * 16 : KP * 32;
                 const uint32_t dst = tmem + (uint32_t)((issued & 1) * NP);
+                if constexpr (BF) {
+#pragma unroll
+                    for (int ks = 0; ks < KP / 16; ++ks)
+                        mma_bf16(dst, smem_desc(smem_u32(A_hi) + ks * 256, lbo, sbo),
+                                 smem_desc(smem_u32(B_hi) + ks * 256, lbo, sbo), S::IDESC,
+                                 ks > 0 ? 1u : 0u);
+                } else
 #pragma unroll
                 for (int ks = 0; ks < KP / 8; ++ks) {
                     const uint64_t ahi = smem_desc(smem_u32(A_hi) + ks * 256, lbo, sbo);
@@ -393,17 +435,30 @@ __global__ void k_prep_weights(const float *__restrict__ w, int taps, int cin, i
     base[per + off] = lo;
 }
 
+__global__ void k_prep_weights_bf16(const float *__restrict__ w, int taps, int cin, int cout, int KP,
+                                    int NP, uint16_t *__restrict__ wbf) {
+    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    int64_t per = (int64_t)NP * KP;
+    if (i >= taps * per) return;
+    int t = (int)(i / per);
+    int rem = (int)(i % per);
+    int n = rem / KP, k = rem % KP;
+    float x = (n < cout && k < cin) ? w[((size_t)t * cin + k) * cout + n] : 0.f;
+    const __nv_bfloat16 b = __float2bfloat16_rn(x);
+    wbf[(size_t)t * per + core_off_bf16(n, k, KP)] = *reinterpret_cast<const uint16_t *>(&b);
+}
+
 int pad_k(int c) { return c <= 16 ? 16 : (c <= 32 ? 32 : (c <= 64 ? 64 : 128)); }
 int pad_n(int c) { return c <= 16 ? 16 : (c <= 32 ? 32 : (c <= 64 ? 64 : (c <= 128 ? 128 : 256))); }
 
-template <int KP, int NP>
+template <int KP, int NP, bool BF>
 void launch_tc(sfb_ctx *ctx, const NetLayer &L, const float *in, int ld_in, const int32_t *nbr,
                int64_t nbr_ld, const int64_t *d_m, int64_t m_bound, int relu, float *out,
                int ld_out, int64_t m_grid, const int32_t *row_map, const int32_t *tap_off) {
-    using S = TcShape<KP, NP>;
+    using S = TcShape<KP, NP, BF>;
     static bool attr = false;
     if (!attr) {
-        SFB_CUDA(cudaFuncSetAttribute(k_conv_tc<KP, NP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        SFB_CUDA(cudaFuncSetAttribute(k_conv_tc<KP, NP, BF>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       S::SMEM));
         attr = true;
     }
@@ -413,8 +468,9 @@ void launch_tc(sfb_ctx *ctx, const NetLayer &L, const float *in, int ld_in, cons
     const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(work_bound, kSplitTarget));
     float *partial = ctx->arena.alloc<float>((size_t)std::min<int64_t>(kMaxPartialRows,
                                                                        32 * m_bound) * NP);
-    k_conv_tc<KP, NP><<<grid, kThreadsTC, S::SMEM, ctx->stream>>>(
-        in, ld_in, L.cin, nbr, nbr_ld, d_m, m_bound, L.taps, L.w_tc, L.b, L.cout, relu, out, ld_out,
+    const float *wts = BF ? reinterpret_cast<const float *>(L.w_bf16) : L.w_tc;
+    k_conv_tc<KP, NP, BF><<<grid, kThreadsTC, S::SMEM, ctx->stream>>>(
+        in, ld_in, L.cin, nbr, nbr_ld, d_m, m_bound, L.taps, wts, L.b, L.cout, relu, out, ld_out,
         partial, row_map, tap_off);
     SFB_CHECK_LAUNCH();
     if (tap_off) return;   // one tap per tile: no split-K partials
@@ -443,16 +499,24 @@ void prepare_tc_weights(sfb_ctx *ctx, NetLayer &L) {
     int64_t total = (int64_t)L.taps * L.cin_pad * L.cout_pad;
     k_prep_weights<<<grid_for(total, 256), 256, 0, ctx->stream>>>(L.w, L.taps, L.cin, L.cout,
                                                                   L.cin_pad, L.cout_pad, L.w_tc);
+    SFB_CUDA(cudaMalloc(&L.w_bf16, (size_t)total * sizeof(uint16_t)));
+    k_prep_weights_bf16<<<grid_for(total, 256), 256, 0, ctx->stream>>>(L.w, L.taps, L.cin, L.cout,
+                                                                       L.cin_pad, L.cout_pad, L.w_bf16);
     SFB_CHECK_LAUNCH();
 }
 
 void conv_layer_tc(sfb_ctx *ctx, const NetLayer &L, const float *in, int ld_in, const int32_t *nbr,
                    int64_t nbr_ld, const int64_t *d_m, int64_t m_bound, int relu, float *out,
                    int ld_out, int64_t m_grid, const int32_t *row_map, const int32_t *tap_off) {
+    const bool bf = ctx->net_mode == SFB_NET_TC_BF16;
 #define SFB_TC_CASE(K, N)                                                                 \
     if (L.cin_pad == K && L.cout_pad == N) {                                              \
-        launch_tc<K, N>(ctx, L, in, ld_in, nbr, nbr_ld, d_m, m_bound, relu, out, ld_out, m_grid, \
-                        row_map, tap_off);                                               \
+        if (bf)                                                                           \
+            launch_tc<K, N, true>(ctx, L, in, ld_in, nbr, nbr_ld, d_m, m_bound, relu, out, ld_out, \
+                                  m_grid, row_map, tap_off);                              \
+        else                                                                              \
+            launch_tc<K, N, false>(ctx, L, in, ld_in, nbr, nbr_ld, d_m, m_bound, relu, out, ld_out, \
+                                   m_grid, row_map, tap_off);                             \
         return;                                                                           \
     }
     SFB_TC_CASE(16, 16) SFB_TC_CASE(16, 32) SFB_TC_CASE(16, 64) SFB_TC_CASE(16, 128)

@@ -104,6 +104,7 @@ void net_load(sfb_ctx *ctx, const void *blob, size_t nbytes) {
             if (conv_tc_supported(L)) {
                 prepare_tc_weights(ctx, L);
                 fresh.allocations.push_back(L.w_tc);
+                fresh.allocations.push_back(L.w_bf16);
             }
         SFB_CUDA(cudaStreamSynchronize(ctx->stream));
     } catch (...) {
@@ -128,7 +129,7 @@ void layer_set(sfb_ctx *ctx, int kind, int kernel, int cin, int cout, const floa
     if (kind == 0) SFB_REQUIRE(kernel >= 1 && (kernel & 1), "conv kernels must be odd");
     if (kind == 1) SFB_REQUIRE(kernel == 2, "transposed_conv kernel is fixed at 2");
     NetLayer &L = ctx->adhoc;
-    for (void *p : {(void *)L.w, (void *)L.b, (void *)L.w_tc})
+    for (void *p : {(void *)L.w, (void *)L.b, (void *)L.w_tc, (void *)L.w_bf16})
         if (p) cudaFree(p);
     L = NetLayer{};
     L.kind = kind;
@@ -213,7 +214,7 @@ void conv_layer(sfb_ctx *ctx, const NetLayer &L, const float *in, int ld_in, con
                 int ld_out, int64_t m_grid) {
     if (m_bound == 0) return;
     if (m_grid < 0) m_grid = m_bound;
-    if (ctx->net_mode == SFB_NET_TC_TF32X3 && L.w_tc) {
+    if (ctx->net_mode != SFB_NET_SIMT_F32 && L.w_tc) {
         conv_layer_tc(ctx, L, in, ld_in, nbr, nbr_ld, d_m, m_bound, relu, out, ld_out, m_grid);
         return;
     }
@@ -272,7 +273,7 @@ void tconv_layer(sfb_ctx *ctx, const NetLayer &L, const float *in, int ld_in,
                  const TapBuckets *tb) {
     if (m_bound == 0) return;
     if (m_grid < 0) m_grid = m_bound;
-    if (ctx->net_mode == SFB_NET_TC_TF32X3 && L.w_tc) {
+    if (ctx->net_mode != SFB_NET_SIMT_F32 && L.w_tc) {
         // rows bucketed by tap (one tap per 128-row tile) when the level has
         // enough tiles to fill the GPU; small levels split the 8 taps instead
         if (tb && m_grid >= 64 * 128) {

@@ -20,21 +20,35 @@ from .netplan import (HEAD_CHANNELS, ConvLayerSpec, NetworkPlan, NetworkWeights,
                       load_weights, save_weights, weights_from_bytes, weights_to_bytes)
 from .voxelgrid import SparseVoxelGrid, VoxelizedCloud
 
-MODES = {"simt_f32": _lib.NET_SIMT_F32, "tc_tf32x3": _lib.NET_TC_TF32X3}
+MODES = {"simt_f32": _lib.NET_SIMT_F32, "tc_tf32x3": _lib.NET_TC_TF32X3,
+         "tc_bf16": _lib.NET_TC_BF16}
+_mode = "tc_tf32x3"
 
 
 def set_mode(mode: str) -> None:
-    """Select the conv arithmetic: 'tc_tf32x3' (tcgen05, the default) or 'simt_f32' (FFMA)."""
+    """Select the conv arithmetic for every lane: 'tc_tf32x3' (tcgen05, tf32
+    hi/lo split, fp32-accurate: the default), 'tc_bf16' (tcgen05, single bf16
+    operands, fp32 accumulation: fast, outside the 1e-3 parameter bound) or
+    'simt_f32' (FFMA)."""
+    global _mode
     if mode not in MODES:
         raise ValueError(f"unknown network mode {mode!r}; expected one of {tuple(MODES)}")
-    ctx = _lib.context()
-    if ctx.lib.sfb_net_set_mode(ctx.handle, MODES[mode]) != _lib.SFB_OK:
-        raise ValueError(f"cannot select network mode {mode!r}")
+    _mode = mode
+    for ctx in _lib.all_contexts():
+        _apply_mode(ctx)
+
+
+def _apply_mode(ctx) -> None:
+    if getattr(ctx, "net_mode", None) != _mode:
+        if ctx.lib.sfb_net_set_mode(ctx.handle, MODES[_mode]) != _lib.SFB_OK:
+            raise ValueError(f"cannot select network mode {_mode!r}")
+        ctx.net_mode = _mode
 
 
 def ensure_loaded(weights: NetworkWeights, lane: int = 0) -> _lib.Context:
     """Upload a network once per context (re-upload when a different object is passed)."""
     ctx = _lib.context(lane=lane)
+    _apply_mode(ctx)
     if ctx.net_token is not weights:
         blob = weights_to_bytes(weights)
         buf = np.frombuffer(blob, dtype=np.uint8)
@@ -55,6 +69,7 @@ def _check_layer(grid, spec, kind, weights, bias):
     if b.shape != (spec.out_channels,):
         raise ValueError(f"bias must be ({spec.out_channels},), got {b.shape}")
     ctx = _lib.context()
+    _apply_mode(ctx)
     ctx.call("sfb_layer_set", 0 if kind == "conv" else 1, spec.kernel, spec.in_channels,
              spec.out_channels, w.ctypes.data_as(_lib.P), b.ctypes.data_as(_lib.P))
     return ctx

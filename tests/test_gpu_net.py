@@ -167,3 +167,31 @@ def test_activate_head_closed_forms():
     out = sparsenet.activate_head(raw, voxel_scale=2.0)
     assert np_(out.quat).tolist() == [1.0, 0.0, 0.0, 0.0]
     np.testing.assert_allclose(np_(out.sigma), 2e-12, rtol=1e-12)
+
+
+@pytest.mark.parametrize("kernel,stride,cin,cout", [(3, 1, 9, 16), (3, 2, 16, 32), (3, 8, 64, 128)])
+def test_bf16_mode_conv_bounded_error(kernel, stride, cin, cout):
+    """The fast mode (single bf16 operands, fp32 accumulation): within the
+    bf16 error model of the dense oracle — |d| <= 2^-7 * sum_k |x_k w_k| —
+    and clearly not fp32-accurate (that is what the tf32 split is for)."""
+    rng = np.random.default_rng(kernel + 7 * stride + cin)
+    side = 10
+    lattice = np.stack(np.meshgrid(*[np.arange(side)] * 3, indexing="ij"), -1).reshape(-1, 3)
+    pick = rng.choice(lattice.shape[0], size=300, replace=False)
+    coords = (lattice[pick] * stride).astype(np.int32)
+    feats = rng.normal(size=(300, cin)).astype(np.float32)
+    spec = netplan.ConvLayerSpec("conv", cin, cout, kernel=kernel)
+    w = rng.uniform(-0.3, 0.3, size=spec.weight_shape).astype(np.float32)
+    b = rng.normal(size=cout).astype(np.float32)
+    grid = SparseVoxelGrid.from_host(coords, feats, stride=stride)
+    sparsenet.set_mode("tc_bf16")
+    try:
+        out = sparsenet.sparse_conv(grid, spec, w, b, relu=False)
+    finally:
+        sparsenet.set_mode("tc_tf32x3")
+    c = np_(grid.coords).astype(np.int32)
+    ref = dense_conv(c, np_(grid.feats), stride, w, b)
+    mag = dense_conv(c, np.abs(np_(grid.feats)), stride, np.abs(w), np.zeros_like(b))
+    err = np.abs(np_(out.feats) - ref)
+    assert (err <= 2.0 ** -7 * mag + 1e-6).all(), err.max()
+    assert err.max() > 1e-4   # really bf16

@@ -12,7 +12,7 @@ which = sys.argv[1] if len(sys.argv) > 1 else "c5"
 cloud, _ = {"c1": scenes.config1, "c2": scenes.config2, "c3": scenes.config3, "c5": scenes.config5}[which]()
 w = netplan.init_random(netplan.NetworkPlan(), 0)
 est = ON.estimate(cloud.positions, cloud.colors, w.as_oracle_layers(), 3)
-for mode in ("tc_tf32x3", "simt_f32"):
+for mode in (sys.argv[2].split(",") if len(sys.argv) > 2 else ("tc_tf32x3", "simt_f32")):
     sparsenet.set_mode(mode)
     sp = estimate_neural(PointCloud(cloud.positions, cloud.colors), w)
     scale = est["vox"]["scale_to_world"]
