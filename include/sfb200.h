@@ -182,6 +182,24 @@ int sfb_prepare_debug(sfb_ctx *ctx, const sfb_splats *splats, const sfb_camera *
                       int32_t tile_size, int64_t *source, double *radius, int64_t *offsets,
                       int64_t *ids, int64_t ids_capacity, int64_t *k_host, int64_t *e_host);
 
+/* ---- analytic estimators (estimators.py:41-211, _neighbors.py:33-128) ---- */
+/* Exact k nearest neighbours of every point among the others: (n,k) squared
+ * distances ascending and int64 indices, ties broken by index — bit-identical
+ * to the reference's uniform-grid search. k <= 64, n > k. */
+int sfb_knn(sfb_ctx *ctx, const double *positions, int64_t n, int32_t k, double *d2_out,
+            int64_t *idx_out);
+/* sqrt of the first column of a (n,k) kNN distance array (per-point nearest
+ * distance; the caller averages it into d-bar). */
+int sfb_nn_distance(sfb_ctx *ctx, const double *d2, int64_t n, int32_t k, double *dist_out);
+/* estimate_local_pca per point from the kNN indices: covariance of the k
+ * neighbours, symeig3x3 frame with the reference's sign rules, scales =
+ * max(sigma_mult*sqrt(lambda), 0.1*dbar), quaternion of the frame, normal =
+ * smallest-eigenvalue direction flipped away from centroid_host. */
+int sfb_local_pca(sfb_ctx *ctx, const double *positions, int64_t n, int32_t k,
+                  const int64_t *knn_idx, double sigma_mult, double dbar,
+                  const double *centroid_host, double *scales, double *quaternions,
+                  double *normals);
+
 /* ---- file formats decoded on the device (pcio.py:210-257, gaussians.py:277-311) */
 /* Binary little-endian PLY vertex rows (the file body as read, device bytes)
  * -> PointCloud arrays: positions (n,3) float64, colors (n,3) = uchar/255,

@@ -82,6 +82,9 @@ SIGNATURES = {
                           I64, ctypes.POINTER(I64), ctypes.POINTER(I64)],
     "sfb_frame": [P, P, P, I64, D, P, ctypes.POINTER(Camera_t), ctypes.POINTER(RenderOptions_t),
                   I32, P, P, P, P, P],
+    "sfb_knn": [P, P, I64, I32, P, P],
+    "sfb_nn_distance": [P, P, I64, I32, P],
+    "sfb_local_pca": [P, P, I64, I32, P, D, D, P, P, P, P],
     "sfb_ply_decode": [P, P, I64, I32, P, P, P, P],
     "sfb_spl1_decode": [P, P, I64, P, P, P, P, P, P],
     "sfb_spl1_encode": [P, ctypes.POINTER(Splats_t), P],

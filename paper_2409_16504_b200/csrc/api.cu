@@ -469,6 +469,32 @@ int sfb_render(sfb_ctx *ctx, const sfb_splats *splats, const sfb_camera *cam,
     });
 }
 
+int sfb_knn(sfb_ctx *ctx, const double *positions, int64_t n, int32_t k, double *d2, int64_t *idx) {
+    return guard(ctx, [&] {
+        SFB_REQUIRE(positions && d2 && idx, "null argument");
+        knn_run(ctx, positions, n, k, d2, idx);
+    });
+}
+
+int sfb_nn_distance(sfb_ctx *ctx, const double *d2, int64_t n, int32_t k, double *dist) {
+    return guard(ctx, [&] {
+        SFB_REQUIRE(d2 && dist && k >= 1, "null argument");
+        if (n > 0) nn_dist_run(ctx, d2, n, k, dist);
+    });
+}
+
+int sfb_local_pca(sfb_ctx *ctx, const double *positions, int64_t n, int32_t k, const int64_t *idx,
+                  double sigma_mult, double dbar, const double *centroid, double *scales,
+                  double *quats, double *normals) {
+    return guard(ctx, [&] {
+        SFB_REQUIRE(positions && idx && centroid && scales && quats && normals, "null argument");
+        double *mc = ctx->arena.alloc<double>(3);
+        SFB_CUDA(cudaMemcpyAsync(mc, centroid, 3 * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
+        if (n > 0) local_pca_run(ctx, positions, n, k, sigma_mult, idx, dbar, mc, scales, quats, normals);
+        SFB_CUDA(cudaStreamSynchronize(ctx->stream));   // centroid_host is the caller's stack
+    });
+}
+
 int sfb_ply_decode(sfb_ctx *ctx, const uint8_t *body, int64_t n, int32_t stride,
                    const int32_t *offsets, double *positions, double *colors, double *normals) {
     return guard(ctx, [&] {

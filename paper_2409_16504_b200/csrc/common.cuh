@@ -355,6 +355,13 @@ void head_to_voxel_splats(sfb_ctx *ctx, const float *raw, const int32_t *coords,
                           const FrameParams *P, double *centers, double *sigma, double *quat,
                           double *opac, double *normal);
 
+// knn.cu
+void knn_run(sfb_ctx *ctx, const double *pos, int64_t n, int k, double *out_d2, int64_t *out_idx);
+void local_pca_run(sfb_ctx *ctx, const double *pos, int64_t n, int k, double sigma_mult,
+                   const int64_t *idx, double dbar, const double *mean_c, double *scales,
+                   double *quats, double *normals);
+void nn_dist_run(sfb_ctx *ctx, const double *d2, int64_t n, int k, double *dist);
+
 // formats.cu
 void ply_decode_run(sfb_ctx *ctx, const uint8_t *body, int64_t n, int32_t stride,
                     const int32_t *offsets, double *pos, double *col, double *nrm);

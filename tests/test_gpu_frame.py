@@ -71,8 +71,7 @@ def test_run_estimator_default_weights(setup):
     a = run_estimator(pc, EstimatorConfig(kind="neural"))
     b = estimate_neural(pc, w)
     assert torch.equal(a.centers, b.centers)
-    with pytest.raises(NotImplementedError):
-        run_estimator(pc, EstimatorConfig(kind="local_pca"))
+    assert len(run_estimator(pc, EstimatorConfig(kind="local_pca"))) == len(pc)
 
 
 def test_device_resident_inputs(setup):
