@@ -193,7 +193,7 @@ def run_ours(args):
     from paper_2409_16504_b200 import _lib, netplan
     from paper_2409_16504_b200.gaussians import Camera
     from paper_2409_16504_b200.pcio import PointCloud
-    from paper_2409_16504_b200.pipeline import render_frame, stats
+    from paper_2409_16504_b200.pipeline import render_frame, stage, stats
     from paper_2409_16504_b200.pcio import PlyBody
     from paper_2409_16504_b200.service import CameraPose, render_pose_frame
 
@@ -240,23 +240,30 @@ def run_ours(args):
         return cams[unit_of(i, rank, world, len(cams))]
 
     rgba_out = None   # render_pose leg: one RGBA8 device frame per (lane, input copy)
+    down = torch.cuda.Stream()   # device->host read-backs of the e2e legs
+    down_done = {}
 
-    def issue(i, cloud_list, host_out=None):
+    def issue(i, cloud_list, host_out=None, src=None):
         lane = i % lanes
         k = i % copies
+        src = cloud_list[k] if src is None else src
         with torch.cuda.stream(streams[lane]):
             if rgba_out is not None:   # service.render_pose streaming path (relit, RGBA8)
-                fr = render_pose_frame(cloud_list[k], weights, poses[unit_of(i, rank, world, len(cams))],
+                fr = render_pose_frame(src, weights, poses[unit_of(i, rank, world, len(cams))],
                                        out=rgba_out[lane][k], lane=lane)
                 host_out[lane][0].copy_(fr, non_blocking=True)
                 return fr
-            fb = render_frame(cloud_list[k], weights, view_of(i), planes, out=outs[lane][k],
-                              lane=lane)
-            if host_out is not None:
-                ho = host_out[lane]
-                ho[0].copy_(fb.rgb, non_blocking=True)
-                ho[1].copy_(fb.normal, non_blocking=True)
-                ho[2].copy_(fb.transmittance, non_blocking=True)
+            if (lane, k) in down_done:   # the previous read-back of these planes
+                streams[lane].wait_event(down_done.pop((lane, k)))
+            fb = render_frame(src, weights, view_of(i), planes, out=outs[lane][k], lane=lane)
+            if host_out is not None:   # read-backs queue on one download stream
+                down.wait_stream(streams[lane])
+                with torch.cuda.stream(down):
+                    ho = host_out[lane]
+                    ho[0].copy_(fb.rgb, non_blocking=True)
+                    ho[1].copy_(fb.normal, non_blocking=True)
+                    ho[2].copy_(fb.transmittance, non_blocking=True)
+                    down_done[(lane, k)] = down.record_event()
         return fb
 
     def run_batch(n_frames, cloud_list, host_out=None):
@@ -268,10 +275,17 @@ def run_ours(args):
         for st in streams:
             st.wait_stream(cur)
         h0 = time.perf_counter()
+        host_in = not (isinstance(cloud_list[0], PointCloud) and cloud_list[0].on_device)
+        # host inputs: frame i+1's upload is enqueued (pipeline.stage) before
+        # frame i waits for its bbox, so the copy engine never idles
+        nxt = stage(cloud_list[0], 0) if host_in else None
         for i in range(n_frames):
-            issue(i, cloud_list, host_out)
+            cur_src = nxt
+            if host_in and i + 1 < n_frames:
+                nxt = stage(cloud_list[(i + 1) % copies], (i + 1) % lanes)
+            issue(i, cloud_list, host_out, cur_src)
         host = time.perf_counter() - h0
-        for st in streams:
+        for st in streams + [down]:
             cur.wait_stream(st)
         end.record(cur)
         end.synchronize()

@@ -98,6 +98,11 @@ int sfb_stage_times(sfb_ctx *ctx, int32_t *stage_ids, float *ms, int32_t cap, in
  * caller forms s = (n / prod(hi-lo)) ** (1/3) in host float64 exactly as
  * voxelgrid.py:133-141 does, so the lattice scale is bit-identical. */
 int sfb_bbox(sfb_ctx *ctx, const double *positions, int64_t n, double *lo_hi_host);
+/* Enqueue-only bbox: the six order-preserving 64-bit words (lo xyz, hi xyz;
+ * u ^ (sign ? ~0 : 1<<63) of the float64 bits) are copied into caller PINNED
+ * memory when the stream gets there; the caller synchronises (event) and
+ * decodes. Lets an upload pipeline keep the copy engine busy. */
+int sfb_bbox_async(sfb_ctx *ctx, const double *positions, int64_t n, uint64_t *ordered_pinned);
 
 /* Density-1 voxelization at scale s. Outputs (capacity n / n+1):
  * coords (M,3) int32 in canonical packed-key order, feats (M,9) float64

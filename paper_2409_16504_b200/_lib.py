@@ -13,7 +13,7 @@ import threading
 from pathlib import Path
 
 PKG = Path(__file__).resolve().parent
-LIB_PATH = PKG / "_build" / "libsfb200.so"
+LIB_PATH = Path(os.environ.get("SFB_LIB_PATH", PKG / "_build" / "libsfb200.so"))   # env: A/B builds
 
 SFB_OK, SFB_ERR_ARG, SFB_ERR_OOM, SFB_ERR_CUDA, SFB_ERR_STATE = 0, 1, 2, 3, 4
 PLANE_RGB, PLANE_NORMAL, PLANE_DEPTH = 1, 2, 4
@@ -63,6 +63,7 @@ SIGNATURES = {
     "sfb_set_debug_counters": [P, P],
     "sfb_stage_times": [P, P, P, I32, ctypes.POINTER(I32)],
     "sfb_bbox": [P, P, I64, P],
+    "sfb_bbox_async": [P, P, I64, P],
     "sfb_voxelize": [P, P, P, I64, D, P, P, P, P, P, P, P, ctypes.POINTER(I64)],
     "sfb_kernel_map": [P, P, I64, I32, I32, P],
     "sfb_transposed_map": [P, P, I64, I32, P, I64, P, P],

@@ -302,6 +302,13 @@ int sfb_bbox(sfb_ctx *ctx, const double *positions, int64_t n, double *lo_hi_hos
     return guard(ctx, [&] { bbox_run(ctx, positions, n, lo_hi_host); });
 }
 
+int sfb_bbox_async(sfb_ctx *ctx, const double *positions, int64_t n, uint64_t *ordered) {
+    return guard(ctx, [&] {
+        SFB_REQUIRE(positions && ordered, "null argument");
+        bbox_async_run(ctx, positions, n, ordered);
+    });
+}
+
 int sfb_voxelize(sfb_ctx *ctx, const double *positions, const double *colors, int64_t n, double s,
                  const double *lo_hi_host, int32_t *coords, double *feats, int64_t *keys,
                  int32_t *p2v, int32_t *order, int32_t *offsets, int64_t *m_host) {

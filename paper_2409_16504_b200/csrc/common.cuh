@@ -328,6 +328,7 @@ struct VoxelOut {
     int32_t *p2v, *order, *offsets;
 };
 void bbox_run(sfb_ctx *ctx, const double *pos, int64_t n, double *lo_hi_host);
+void bbox_async_run(sfb_ctx *ctx, const double *pos, int64_t n, uint64_t *ordered_host);
 void voxel_layout(const double *lo_hi, double s, FrameParams &P);
 // voxel count lands in C->m[0] (device)
 void voxelize_run(sfb_ctx *ctx, const double *pos, const double *col, int64_t n,

@@ -38,6 +38,9 @@ constexpr int kSuper = 8;      // tiles per super-tile edge
 constexpr int kSuperMax = 16;  // super tiles per run at the middle level
 constexpr int kWin = 2048;     // rank window of the merge
 constexpr int kCT = 256;       // compositor threads per CTA
+#ifndef SFB_COMP_MINB
+#define SFB_COMP_MINB 4
+#endif
 constexpr int kChunk = 64;     // runs per compositing chunk
 
 // ------------------------------------------------------------ 1. projection
@@ -851,7 +854,7 @@ __device__ __forceinline__ float3 horner3(const float4 *__restrict__ v, int m, f
 // cutoff inside the run; then T is iterated point by point exactly as the
 // reference does. Alpha, T and the thresholds stay float64.
 template <int NPIX>
-__global__ void __launch_bounds__(kCT, 4) k_composite(CompParams P) {
+__global__ void __launch_bounds__(kCT, SFB_COMP_MINB) k_composite(CompParams P) {
     constexpr uint32_t NONE = 0xffffffffu;
     __shared__ uint32_t bitmap[kWin / 32];
     __shared__ uint32_t list[kWin];

@@ -67,6 +67,19 @@ void bbox_run(sfb_ctx *ctx, const double *pos, int64_t n, double *lo_hi_host) {
     for (int a = 0; a < 6; ++a) lo_hi_host[a] = unord_bits((unsigned long long)ctx->pinned[a]);
 }
 
+// enqueue-only variant: the 6 order-preserving words land in caller pinned
+// memory when the stream reaches them (no host synchronisation)
+void bbox_async_run(sfb_ctx *ctx, const double *pos, int64_t n, uint64_t *ordered_host) {
+    SFB_REQUIRE(n > 0, "empty cloud has no bbox");
+    auto *mm = ctx->arena.alloc<unsigned long long>(6);
+    k_bbox_init<<<1, 32, 0, ctx->stream>>>(mm);
+    k_bbox<<<grid_for(3 * n, kBBoxThreads, ctx->num_sms * 4), kBBoxThreads, 0, ctx->stream>>>(
+        pos, n, mm);
+    SFB_CHECK_LAUNCH();
+    SFB_CUDA(cudaMemcpyAsync(ordered_host, mm, 6 * sizeof(unsigned long long), cudaMemcpyDeviceToHost,
+                             ctx->stream));
+}
+
 template <class K>
 __global__ void k_keygen(const double *__restrict__ pos, int64_t n, const FrameParams *__restrict__ P,
                          K *__restrict__ keys, uint32_t *__restrict__ vals) {

@@ -14,45 +14,73 @@ import torch
 from . import _lib
 from .gaussians import Camera
 from .netplan import NetworkWeights
-from .pcio import PlyBody, PointCloud
+from .pcio import EmptyCloudError, PlyBody, PointCloud
 from .rasterizer import _PLANE_BIT, FrameBuffer, RenderOptions, _alloc_planes
 from .sparsenet import ensure_loaded
 from .voxelgrid import device_bbox, lattice_scale, stage_cloud
 
 # Host clouds are uploaded on a dedicated stream (one per device) into
 # persistent per-lane staging buffers (two per lane, alternating), with their
-# own library context (own scratch arena) for the bbox: the copy of frame i
-# waits only for earlier uploads and for the frame that last used its staging
-# buffer — not for everything queued on the lane — and the one host round
-# trip per frame (the 48-byte bbox read-back that gives the bit-exact lattice
-# scale) waits only for the positions copy. Fixed staging addresses also keep
-# the lane's CUDA-graph cache hot (the frame graph is keyed by pointers).
+# own library context (own scratch arena) for the bbox. ``stage`` only
+# ENQUEUES the copies, the bbox reduction and the 48-byte read-back of the
+# bbox into pinned memory; ``prepare_cloud`` later waits for that read-back
+# alone. Staging frame i+1 before rendering frame i therefore keeps the copy
+# engine busy while the host waits for frame i's bbox (the one host round
+# trip per frame, which gives the bit-exact lattice scale). Fixed staging
+# addresses also keep the lane's CUDA-graph cache hot (graphs are keyed by
+# pointers).
 _UPLOAD_LANE = 1 << 16
 _upload_streams = {}
-_staging = {}   # (device, lane) -> {"k": next buffer, "bufs": [[pos, col, done_event], ...]}
+_staging = {}   # (device, lane) -> {"k": next, "bufs": [[pos, col, done_ev, ply_bytes, bbox_words], ...]}
 
 
-def _upload(cloud, lane: int):
+class StagedCloud:
+    """A host cloud whose upload is in flight (see ``stage``)."""
+
+    def __init__(self, pos, col, n, slot, bbox_ev, done_ev, words):
+        self.pos, self.col, self.n, self.slot = pos, col, n, slot
+        self.bbox_ev, self.done_ev, self.words = bbox_ev, done_ev, words
+
+    def __len__(self) -> int:
+        return self.n
+
+
+def _decode_words(words: np.ndarray) -> np.ndarray:
+    """Order-preserving bbox words -> float64 (inverse of the device encoding)."""
+    u = words.astype(np.uint64)
+    neg = (u >> np.uint64(63)) == 0
+    bits = np.where(neg, ~u, u & np.uint64(0x7FFFFFFFFFFFFFFF))
+    return bits.view(np.float64).copy()
+
+
+def stage(cloud, lane: int = 0) -> StagedCloud:
+    """Enqueue the upload of a host cloud (PointCloud or PlyBody) for ``lane``:
+    positions H2D (or the PLY bytes + device decode), bbox + its read-back,
+    colours H2D — no host synchronisation."""
     dev = torch.cuda.current_device()
     up = _upload_streams.get(dev)
     if up is None:
         up = _upload_streams[dev] = torch.cuda.Stream(device=dev)
-    st = _staging.setdefault((dev, lane), {"k": 0, "bufs": [[None, None, None, None],
-                                                            [None, None, None, None]]})
+    st = _staging.setdefault((dev, lane), {"k": 0, "bufs": [[None] * 5, [None] * 5]})
     slot = st["bufs"][st["k"]]
     st["k"] ^= 1
     ply = isinstance(cloud, PlyBody)
     n = len(cloud) if ply else int(cloud.positions.shape[0])
+    if n == 0:
+        raise EmptyCloudError("empty cloud has no bbox")
     if slot[0] is None or slot[0].shape[0] < n:
         slot[0] = torch.empty((n, 3), dtype=torch.float64, device=dev)
         slot[1] = torch.empty((n, 3), dtype=torch.float64, device=dev)
     if ply and (slot[3] is None or slot[3].numel() < cloud.raw.numel()):
         slot[3] = torch.empty(cloud.raw.numel(), dtype=torch.uint8, device=dev)
+    if slot[4] is None:
+        slot[4] = torch.empty(6, dtype=torch.int64).pin_memory()
     pos, col = slot[0][:n], slot[1][:n]
     cur = torch.cuda.current_stream(dev)
     up.wait_stream(cur)   # inputs the caller just wrote on its stream
     if slot[2] is not None:
         up.wait_event(slot[2])   # the frame that last read this staging buffer
+    uctx = _lib.context(lane=_UPLOAD_LANE + lane)
 
     def host(a):
         if isinstance(a, torch.Tensor):
@@ -63,33 +91,36 @@ def _upload(cloud, lane: int):
             body = slot[3][:cloud.raw.numel()]
             body.copy_(cloud.raw, non_blocking=cloud.raw.is_pinned())
             layout = (_lib.I32 * 9)(*cloud.offsets)
-            _lib.context(lane=_UPLOAD_LANE + lane).call(
-                "sfb_ply_decode", _lib.ptr(body), n, cloud.stride, layout, _lib.ptr(pos),
-                _lib.ptr(col), _lib.P(0))
-            lo_hi = device_bbox(pos, _UPLOAD_LANE + lane)
+            uctx.call("sfb_ply_decode", _lib.ptr(body), n, cloud.stride, layout, _lib.ptr(pos),
+                      _lib.ptr(col), _lib.P(0))
+            uctx.call("sfb_bbox_async", _lib.ptr(pos), n, _lib.ptr(slot[4]))
+            bbox_ev = up.record_event()
         else:
             hp = host(cloud.positions)
             pos.copy_(hp, non_blocking=hp.is_pinned())
-            lo_hi = device_bbox(pos, _UPLOAD_LANE + lane)
+            uctx.call("sfb_bbox_async", _lib.ptr(pos), n, _lib.ptr(slot[4]))
+            bbox_ev = up.record_event()
             hc = host(cloud.colors)
             col.copy_(hc, non_blocking=hc.is_pinned())
-        ev = up.record_event()
-    cur.wait_event(ev)
-    return pos, col, lo_hi, slot
+        done_ev = up.record_event()
+    return StagedCloud(pos, col, n, slot, bbox_ev, done_ev, slot[4])
 
 
-def prepare_cloud(cloud: PointCloud, lane: int = 0):
+def prepare_cloud(cloud, lane: int = 0):
     """Device positions/colours, point count, lattice scale and bbox of a cloud
-    (host clouds go through the upload stream); ``slot`` is the staging buffer
-    whose done-event the caller records after its frame (None for device clouds)."""
-    slot = None
-    if not isinstance(cloud, PlyBody) and cloud.on_device:
+    (host clouds go through the upload stream; a ``StagedCloud`` from
+    ``stage`` is used as is); ``slot`` is the staging buffer whose done-event
+    the caller records after its frame (None for device clouds)."""
+    if not isinstance(cloud, (PlyBody, StagedCloud)) and cloud.on_device:
         pos, col = stage_cloud(cloud)
         lo_hi = device_bbox(pos, lane)
-    else:
-        pos, col, lo_hi, slot = _upload(cloud, lane)
-    n = int(pos.shape[0])
-    return pos, col, n, lattice_scale(n, lo_hi), lo_hi, slot
+        n = int(pos.shape[0])
+        return pos, col, n, lattice_scale(n, lo_hi), lo_hi, None
+    sc = cloud if isinstance(cloud, StagedCloud) else stage(cloud, lane)
+    sc.bbox_ev.synchronize()   # the 48-byte read-back only
+    lo_hi = _decode_words(sc.words.numpy().view(np.uint64))
+    torch.cuda.current_stream().wait_event(sc.done_ev)
+    return sc.pos, sc.col, sc.n, lattice_scale(sc.n, lo_hi), lo_hi, sc.slot
 
 
 def render_frame(cloud: PointCloud, weights: NetworkWeights, cam: Camera,
