@@ -54,7 +54,7 @@ def parse():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-profile", action="store_true", help="skip the CUPTI launch count")
     ap.add_argument("--cpu-rows", type=int, default=2, help="tile rows in the CPU sample")
-    ap.add_argument("--lanes", type=int, default=4, help="frames in flight per GPU (streams)")
+    ap.add_argument("--lanes", type=int, default=8, help="frames in flight per GPU (streams)")
     ap.add_argument("--net-mode", choices=("tc_tf32x3", "tc_bf16", "simt_f32"), default="tc_tf32x3",
                     help="P2ENet arithmetic (tc_tf32x3: fp32-accurate parity mode)")
     return ap.parse_args()

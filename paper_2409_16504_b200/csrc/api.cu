@@ -649,10 +649,28 @@ static int frame_impl(sfb_ctx *ctx, const double *positions, const double *color
             FrameParams *P = ctx->arena.alloc<FrameParams>(1);
             G->dev_params = P;
             SFB_CUDA(cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeThreadLocal));
+            ctx->arena.no_grow = true;
             try {
                 enqueue_frame(ctx, positions, colors, n, host, P, cam, opts, plane_mask, rgb,
                               normal, depth, trans, rgba);
+                ctx->arena.no_grow = false;
+            } catch (const ArenaGrowth &) {
+                // the eager run used less scratch (size hints changed a path):
+                // drop the capture, run this frame eagerly (growing the arena),
+                // capture on the next call
+                ctx->arena.no_grow = false;
+                cudaGraph_t junk = nullptr;
+                cudaStreamEndCapture(ctx->stream, &junk);
+                if (junk) cudaGraphDestroy(junk);
+                cudaGetLastError();
+                ctx->stream = user;
+                ctx->arena.reset();
+                FrameParams *P2 = ctx->arena.alloc<FrameParams>(1);
+                enqueue_frame(ctx, positions, colors, n, host, P2, cam, opts, plane_mask, rgb, normal,
+                              depth, trans, rgba);
+                return;
             } catch (...) {
+                ctx->arena.no_grow = false;
                 cudaGraph_t junk = nullptr;
                 cudaStreamEndCapture(ctx->stream, &junk);
                 if (junk) cudaGraphDestroy(junk);

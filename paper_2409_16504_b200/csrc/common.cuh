@@ -34,6 +34,12 @@ struct Error : std::runtime_error {
         if (!(cond)) throw ::sfb::Error(SFB_ERR_ARG, (msg));      \
     } while (0)
 
+// thrown when a frame being captured into a CUDA graph needs more scratch than
+// the eager run that preceded it (cudaMalloc is illegal during capture)
+struct ArenaGrowth : std::runtime_error {
+    ArenaGrowth() : std::runtime_error("scratch arena must grow during graph capture") {}
+};
+
 // Grow-only device scratch: a list of chunks; a top-level call resets the
 // cursor, allocations bump through existing chunks and only allocate a new
 // chunk when none has room (so steady-state frames never call cudaMalloc).
@@ -62,6 +68,7 @@ class Arena {
             ++cur_;
             off_ = 0;
         }
+        if (no_grow) throw ArenaGrowth();   // capturing: the caller retries eagerly
         size_t sz = bytes < (size_t(64) << 20) ? (size_t(64) << 20) : bytes;
         void *p = nullptr;
         SFB_CUDA(cudaMalloc(&p, sz));
@@ -75,6 +82,8 @@ class Arena {
         for (auto &c : chunks_) s += c.size;
         return s;
     }
+
+    bool no_grow = false;   // set while a frame is captured into a graph
 
   private:
     struct Chunk {

@@ -274,6 +274,9 @@ void tconv_layer(sfb_ctx *ctx, const NetLayer &L, const float *in, int ld_in,
     if (m_bound == 0) return;
     if (m_grid < 0) m_grid = m_bound;
     if (ctx->net_mode != SFB_NET_SIMT_F32 && L.w_tc) {
+        // the 8-tap map's scratch is taken on both paths so the arena layout
+        // does not depend on which one the size hints select
+        int32_t *tbuf = tmap ? nullptr : ctx->arena.alloc<int32_t>(8 * (size_t)m_bound);
         // rows bucketed by tap (one tap per 128-row tile) when the level has
         // enough tiles to fill the GPU; small levels split the 8 taps instead
         if (tb && m_grid >= 64 * 128) {
@@ -282,10 +285,9 @@ void tconv_layer(sfb_ctx *ctx, const NetLayer &L, const float *in, int ld_in,
             return;
         }
         if (!tmap) {
-            int32_t *t = ctx->arena.alloc<int32_t>(8 * (size_t)m_bound);
-            k_tmap<<<dgrid(m_grid, 256), 256, 0, ctx->stream>>>(parent, tap, d_m, m_bound, m_bound, t);
+            k_tmap<<<dgrid(m_grid, 256), 256, 0, ctx->stream>>>(parent, tap, d_m, m_bound, m_bound, tbuf);
             SFB_CHECK_LAUNCH();
-            tmap = t;
+            tmap = tbuf;
         }
         conv_layer_tc(ctx, L, in, ld_in, tmap, m_bound, d_m, m_bound, relu, out, ld_out, m_grid);
         return;
