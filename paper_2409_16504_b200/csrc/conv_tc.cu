@@ -147,9 +147,13 @@ __host__ __device__ inline int core_off_bf16(int row, int k, int KP) {
 template <int KP, int NP, bool BF = false>
 struct TcShape {
     static constexpr int TERMS = BF ? 1 : 2;
-    static constexpr int A_FLOATS = BF ? kM * KP / 2 : kM * KP;   // one term, in 4-byte words
+    // taps per MMA batch: narrow inputs (Cin <= 16) take two taps per round of
+    // gather / barrier / drain, halving the per-tap latency cost
+    static constexpr int TAPB = KP == 16 ? 2 : 1;
+    static constexpr int A_FLOATS = BF ? kM * KP / 2 : kM * KP;   // one term of one tap, 4-byte words
     static constexpr int B_FLOATS = BF ? NP * KP / 2 : NP * KP;
-    static constexpr int STAGE_FLOATS = TERMS * A_FLOATS + TERMS * B_FLOATS;
+    static constexpr int A_TAP = TERMS * A_FLOATS, B_TAP = TERMS * B_FLOATS;   // per tap
+    static constexpr int STAGE_FLOATS = TAPB * (A_TAP + B_TAP);
     static constexpr int STAGES = (STAGE_FLOATS * 4 * 2 <= 200 * 1024) ? 2 : 1;
     static constexpr int SMEM = STAGES * STAGE_FLOATS * 4 + 1024 + 64;
     // two accumulators (tap t in buffer t % 2): the epilogue of tap t-1 reads
@@ -270,33 +274,49 @@ k_conv_tc(const float *__restrict__ in, int ld_in, int cin, const int32_t *__res
         uint32_t mask = 0;
 #pragma unroll
         for (int w = 0; w < kThreadsTC / 32; ++w) mask |= s_mask[w];
-        // register-prefetched gather: the rows of the next non-empty tap are
-        // in flight while the current tap is split, staged and multiplied
-        float v[KP];
-        auto fetch = [&](int t) {
-            const int32_t src = s_src[t - t0][tid];
-            const float *x = src >= 0 ? in + (int64_t)src * ld_in : nullptr;
-#pragma unroll
-            for (int k = 0; k < KP; ++k) v[k] = (x && k < cin) ? __ldg(x + k) : 0.f;
+        // register-prefetched gather: the rows of the next batch (up to TAPB
+        // non-empty taps) are in flight while the current one is split,
+        // staged and multiplied
+        constexpr int TB = S::TAPB;
+        float v[TB][KP];
+        int nxt_t[TB], nxt_n = 0;
+        auto take = [&]() {   // pop the next batch of taps off the mask
+            nxt_n = 0;
+            while (mask && nxt_n < TB) {
+                nxt_t[nxt_n++] = t0 + __ffs(mask) - 1;
+                mask &= mask - 1;
+            }
         };
-        if (mask) fetch(t0 + __ffs(mask) - 1);
-        // weights: with two stages, tap k+1's tile is fetched (TMA) as soon as
-        // batch k-1 has drained, so its latency hides behind tap k
-        auto load_w = [&](int t, int slot) {
-            const uint32_t bytes = (uint32_t)(S::TERMS * S::B_FLOATS * 4);
-            float *B = stage_base + slot * S::STAGE_FLOATS + S::TERMS * S::A_FLOATS;
+        auto fetch = [&]() {
+#pragma unroll
+            for (int q = 0; q < TB; ++q) {
+                const int32_t src = q < nxt_n ? s_src[nxt_t[q] - t0][tid] : -1;
+                const float *x = src >= 0 ? in + (int64_t)src * ld_in : nullptr;
+#pragma unroll
+                for (int k = 0; k < KP; ++k) v[q][k] = (x && k < cin) ? __ldg(x + k) : 0.f;
+            }
+        };
+        take();
+        if (nxt_n) fetch();
+        // weights: with two stages, batch k+1's tiles are fetched (TMA) as soon
+        // as batch k-1 has drained, so their latency hides behind batch k
+        auto load_w = [&](const int *tt, int nt, int slot) {
+            const uint32_t bytes = (uint32_t)(nt * S::B_TAP * 4);
+            float *B = stage_base + slot * S::STAGE_FLOATS + TB * S::A_TAP;
             mbar_expect_tx(&bar_full[slot], bytes);
-            tma_bulk_g2s(B, wtc + (size_t)t * S::TERMS * S::B_FLOATS, bytes, &bar_full[slot]);
+            for (int q = 0; q < nt; ++q)
+                tma_bulk_g2s(B + q * S::B_TAP, wtc + (size_t)tt[q] * S::B_TAP, S::B_TAP * 4, &bar_full[slot]);
         };
         int item_issued = 0;
-        while (mask) {
-            const int t = t0 + __ffs(mask) - 1;
-            mask &= mask - 1;
+        while (nxt_n) {
+            int cur_t[TB];
+            const int cur_n = nxt_n;
+#pragma unroll
+            for (int q = 0; q < TB; ++q) cur_t[q] = nxt_t[q];
             const int s = issued % S::STAGES;
             const int use = issued / S::STAGES;
-            float *A_hi = stage_base + s * S::STAGE_FLOATS;
-            float *A_lo = A_hi + S::A_FLOATS;                  // tf32 only
-            float *B_hi = A_hi + S::TERMS * S::A_FLOATS;
+            float *A_base = stage_base + s * S::STAGE_FLOATS;
+            float *B_base = A_base + TB * S::A_TAP;
             // stage free again: the batch that last used it (i - STAGES) has
             // completed. Batch barriers alternate by batch parity, so no wait
             // below can alias a later phase: the next commit to the barrier
@@ -305,70 +325,83 @@ k_conv_tc(const float *__restrict__ in, int ld_in, int cin, const int32_t *__res
                 const int j = issued - S::STAGES;
                 mbar_wait(&bar_done[j & 1], (j >> 1) & 1);
             }
-            if (tid == 0 && (S::STAGES == 1 || item_issued == 0)) load_w(t, s);
-            // my row of this tap in the canonical layout: bf16, or tf32 hi/lo
-            if constexpr (BF) {
-                uint16_t *A16 = reinterpret_cast<uint16_t *>(A_hi);
+            if (tid == 0 && (S::STAGES == 1 || item_issued == 0)) load_w(cur_t, cur_n, s);
+            // my row of each tap of the batch in the canonical layout: bf16, or tf32 hi/lo
 #pragma unroll
-                for (int c = 0; c < KP / 8; ++c) {
-                    uint32_t w[4];
+            for (int q = 0; q < TB; ++q) {
+                if (q >= cur_n) break;
+                float *A_hi = A_base + q * S::A_TAP;
+                float *A_lo = A_hi + S::A_FLOATS;   // tf32 only
+                if constexpr (BF) {
+                    uint16_t *A16 = reinterpret_cast<uint16_t *>(A_hi);
 #pragma unroll
-                    for (int h = 0; h < 4; ++h) {
-                        const __nv_bfloat162 b2 = __floats2bfloat162_rn(v[8 * c + 2 * h], v[8 * c + 2 * h + 1]);
-                        w[h] = *reinterpret_cast<const uint32_t *>(&b2);
+                    for (int c = 0; c < KP / 8; ++c) {
+                        uint32_t w[4];
+#pragma unroll
+                        for (int h = 0; h < 4; ++h) {
+                            const __nv_bfloat162 b2 =
+                                __floats2bfloat162_rn(v[q][8 * c + 2 * h], v[q][8 * c + 2 * h + 1]);
+                            w[h] = *reinterpret_cast<const uint32_t *>(&b2);
+                        }
+                        *reinterpret_cast<uint4 *>(A16 + core_off_bf16(tid, 8 * c, KP)) =
+                            make_uint4(w[0], w[1], w[2], w[3]);
                     }
-                    *reinterpret_cast<uint4 *>(A16 + core_off_bf16(tid, 8 * c, KP)) =
-                        make_uint4(w[0], w[1], w[2], w[3]);
-                }
-            } else
+                } else {
 #pragma unroll
-            for (int c = 0; c < KP / 4; ++c) {
-                float4 hi, lo;
-                hi.x = tf32_round(v[4 * c]);
-                hi.y = tf32_round(v[4 * c + 1]);
-                hi.z = tf32_round(v[4 * c + 2]);
-                hi.w = tf32_round(v[4 * c + 3]);
-                lo.x = tf32_round(v[4 * c] - hi.x);
-                lo.y = tf32_round(v[4 * c + 1] - hi.y);
-                lo.z = tf32_round(v[4 * c + 2] - hi.z);
-                lo.w = tf32_round(v[4 * c + 3] - hi.w);
-                const int off = core_off(tid, 4 * c, KP);
-                *reinterpret_cast<float4 *>(A_hi + off) = hi;
-                *reinterpret_cast<float4 *>(A_lo + off) = lo;
+                    for (int c = 0; c < KP / 4; ++c) {
+                        float4 hi, lo;
+                        hi.x = tf32_round(v[q][4 * c]);
+                        hi.y = tf32_round(v[q][4 * c + 1]);
+                        hi.z = tf32_round(v[q][4 * c + 2]);
+                        hi.w = tf32_round(v[q][4 * c + 3]);
+                        lo.x = tf32_round(v[q][4 * c] - hi.x);
+                        lo.y = tf32_round(v[q][4 * c + 1] - hi.y);
+                        lo.z = tf32_round(v[q][4 * c + 2] - hi.z);
+                        lo.w = tf32_round(v[q][4 * c + 3] - hi.w);
+                        const int off = core_off(tid, 4 * c, KP);
+                        *reinterpret_cast<float4 *>(A_hi + off) = hi;
+                        *reinterpret_cast<float4 *>(A_lo + off) = lo;
+                    }
+                }
             }
-            if (mask) fetch(t0 + __ffs(mask) - 1);   // next tap's rows, in flight from here
+            take();
+            if (nxt_n) fetch();   // next batch's rows, in flight from here
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
             __syncthreads();   // also orders the last drain's TMEM reads before these MMAs
             if (tid == 0) {
                 mbar_wait(&bar_full[s], use & 1);
                 asm volatile("tcgen05.fence::after_thread_sync;");
-                const float *B_lo = B_hi + S::B_FLOATS;
                 const uint32_t lbo = 128, sbo = BF ? KP * 16 : KP * 32;
                 const uint32_t dst = tmem + (uint32_t)((issued & 1) * NP);
-                if constexpr (BF) {
+                for (int q = 0; q < cur_n; ++q) {
+                    const float *A_hi = A_base + q * S::A_TAP, *A_lo = A_hi + S::A_FLOATS;
+                    const float *B_hi = B_base + q * S::B_TAP, *B_lo = B_hi + S::B_FLOATS;
+                    if constexpr (BF) {
 #pragma unroll
-                    for (int ks = 0; ks < KP / 16; ++ks)
-                        mma_bf16(dst, smem_desc(smem_u32(A_hi) + ks * 256, lbo, sbo),
-                                 smem_desc(smem_u32(B_hi) + ks * 256, lbo, sbo), S::IDESC,
-                                 ks > 0 ? 1u : 0u);
-                } else
+                        for (int ks = 0; ks < KP / 16; ++ks)
+                            mma_bf16(dst, smem_desc(smem_u32(A_hi) + ks * 256, lbo, sbo),
+                                     smem_desc(smem_u32(B_hi) + ks * 256, lbo, sbo), S::IDESC,
+                                     (q > 0 || ks > 0) ? 1u : 0u);
+                    } else {
 #pragma unroll
-                for (int ks = 0; ks < KP / 8; ++ks) {
-                    const uint64_t ahi = smem_desc(smem_u32(A_hi) + ks * 256, lbo, sbo);
-                    const uint64_t alo = smem_desc(smem_u32(A_lo) + ks * 256, lbo, sbo);
-                    const uint64_t bhi = smem_desc(smem_u32(B_hi) + ks * 256, lbo, sbo);
-                    const uint64_t blo = smem_desc(smem_u32(B_lo) + ks * 256, lbo, sbo);
-                    // small terms first: lo*lo, lo*hi, hi*lo, then hi*hi
-                    mma_tf32(dst, alo, blo, S::IDESC, ks > 0 ? 1u : 0u);
-                    mma_tf32(dst, alo, bhi, S::IDESC, 1u);
-                    mma_tf32(dst, ahi, blo, S::IDESC, 1u);
-                    mma_tf32(dst, ahi, bhi, S::IDESC, 1u);
+                        for (int ks = 0; ks < KP / 8; ++ks) {
+                            const uint64_t ahi = smem_desc(smem_u32(A_hi) + ks * 256, lbo, sbo);
+                            const uint64_t alo = smem_desc(smem_u32(A_lo) + ks * 256, lbo, sbo);
+                            const uint64_t bhi = smem_desc(smem_u32(B_hi) + ks * 256, lbo, sbo);
+                            const uint64_t blo = smem_desc(smem_u32(B_lo) + ks * 256, lbo, sbo);
+                            // small terms first: lo*lo, lo*hi, hi*lo, then hi*hi
+                            mma_tf32(dst, alo, blo, S::IDESC, (q > 0 || ks > 0) ? 1u : 0u);
+                            mma_tf32(dst, alo, bhi, S::IDESC, 1u);
+                            mma_tf32(dst, ahi, blo, S::IDESC, 1u);
+                            mma_tf32(dst, ahi, bhi, S::IDESC, 1u);
+                        }
+                    }
                 }
                 mma_commit(&bar_done[issued & 1]);
             }
-            if (item_issued > 0) drain(issued - 1);   // previous tap, overlapping this one's MMAs
-            if (S::STAGES == 2 && tid == 0 && mask)   // slot of batch issued-1 is free now
-                load_w(t0 + __ffs(mask) - 1, (issued + 1) & 1);
+            if (item_issued > 0) drain(issued - 1);   // previous batch, overlapping this one's MMAs
+            if (S::STAGES == 2 && tid == 0 && nxt_n)   // slot of batch issued-1 is free now
+                load_w(nxt_t, nxt_n, (issued + 1) & 1);
             ++issued;
             ++item_issued;
         }
@@ -487,7 +520,8 @@ bool conv_tc_supported(const NetLayer &L) {
     if (choose_splits(1, L.taps, kSplitTarget) == 0) return false;   // > 32 taps per split
     int kp = pad_k(L.cin), np = pad_n(L.cout);
     if (L.cin > 128 || L.cout > 128) return false;
-    size_t stage = (size_t)(2 * kM * kp + 2 * np * kp) * 4;
+    const int tapb = kp == 16 ? 2 : 1;
+    size_t stage = (size_t)tapb * (2 * kM * kp + 2 * np * kp) * 4;
     return stage + 2048 <= 200 * 1024;
 }
 
