@@ -273,6 +273,9 @@ struct FrameParams {
 // devprims.cu
 void dscan(sfb_ctx *ctx, const int32_t *in, int32_t *out, const int64_t *d_n, int64_t n_fixed,
            int64_t *total_out, bool inclusive);
+void dscan3(sfb_ctx *ctx, const int32_t *in0, const int32_t *in1, const int32_t *in2, int32_t *out0,
+            int32_t *out1, int32_t *out2, const int64_t *d_n, int64_t n_fixed, int64_t *tot0,
+            int64_t *tot1, int64_t *tot2);
 template <class K>
 int dsort_pairs(sfb_ctx *ctx, K *k0, uint32_t *v0, K *k1, uint32_t *v1, const int64_t *d_n,
                 int64_t n_fixed, int bits);

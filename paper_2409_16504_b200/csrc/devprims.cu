@@ -178,6 +178,120 @@ k_scan_lb(const int32_t *__restrict__ in, int32_t *__restrict__ out, const int64
     if (ntiles == 0 && blockIdx.x == 0 && threadIdx.x == 0 && total_out) *total_out = 0;
 }
 
+// Three exclusive scans of one length in ONE launch (per-run fine / super /
+// global entry counts): the same look-back with a status word per column.
+constexpr int kScan3Items = 2;   // 3 x 2048 int32 staged per tile (24 KB)
+struct Scan3 {
+    const int32_t *in[3];
+    int32_t *out[3];
+    int64_t *tot[3];
+};
+
+__global__ void __launch_bounds__(kScanThreads)
+k_scan3_lb(Scan3 S, const int64_t *__restrict__ d_n, int64_t n_fixed,
+           unsigned long long *__restrict__ status /* [3][tiles] */, int64_t tiles_cap,
+           unsigned int *__restrict__ ticket) {
+    constexpr int IT = kScan3Items;
+    constexpr int TILE = IT * kScanThreads;
+    __shared__ int32_t s_val[3][TILE];
+    __shared__ int32_t s_warp[32];
+    __shared__ int s_tile;
+    __shared__ int32_t s_excl[3];
+    const int64_t n = d_n ? *d_n : n_fixed;
+    const int64_t ntiles = (n + TILE - 1) / TILE;
+    const int lane = threadIdx.x & 31;
+    for (;;) {
+        if (threadIdx.x == 0) s_tile = (int)atomicAdd(ticket, 1u);
+        __syncthreads();
+        const int64_t tile = s_tile;
+        if (tile >= ntiles) break;
+        const int64_t base = tile * TILE;
+#pragma unroll
+        for (int c = 0; c < 3; ++c)
+#pragma unroll
+            for (int k = 0; k < IT; ++k) {
+                const int64_t i = base + k * kScanThreads + threadIdx.x;
+                s_val[c][k * kScanThreads + threadIdx.x] = i < n ? S.in[c][i] : 0;
+            }
+        __syncthreads();
+        int32_t v[3][IT], ex[3], agg[3];
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+            int32_t sum = 0;
+#pragma unroll
+            for (int k = 0; k < IT; ++k) {
+                v[c][k] = s_val[c][threadIdx.x * IT + k];
+                sum += v[c][k];
+            }
+            ex[c] = block_excl_scan(sum, s_warp, &agg[c]);
+        }
+        if (threadIdx.x < 32) {
+            for (int c = 0; c < 3; ++c) {
+                unsigned long long *stc = status + c * tiles_cap;
+                int32_t prefix = 0;
+                if (tile == 0) {
+                    if (lane == 0) atomicExch(&stc[0], kLbInc | (uint32_t)agg[c]);
+                } else {
+                    if (lane == 0) atomicExch(&stc[tile], kLbAgg | (uint32_t)agg[c]);
+                    int64_t pred = tile - 1;
+                    for (;;) {
+                        const int64_t q = pred - lane;
+                        unsigned long long st = q >= 0 ? lb_load(&stc[q]) : kLbInc;
+                        while (__any_sync(0xffffffffu, (st >> 32) == 0)) {
+                            if ((st >> 32) == 0) st = lb_load(&stc[q]);
+                        }
+                        const unsigned inc = __ballot_sync(0xffffffffu, (st >> 32) == 2);
+                        const int stop = inc ? __ffs(inc) - 1 : 31;
+                        int32_t val = lane <= stop ? (int32_t)(uint32_t)st : 0;
+                        for (int o = 16; o; o >>= 1) val += __shfl_xor_sync(0xffffffffu, val, o);
+                        prefix += val;
+                        if (inc) break;
+                        pred -= 32;
+                    }
+                    if (lane == 0) atomicExch(&stc[tile], kLbInc | (uint32_t)(prefix + agg[c]));
+                }
+                if (lane == 0) s_excl[c] = prefix;
+            }
+        }
+        __syncthreads();
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+            int32_t run = s_excl[c] + ex[c];
+#pragma unroll
+            for (int k = 0; k < IT; ++k) {
+                s_val[c][threadIdx.x * IT + k] = run;
+                run += v[c][k];
+            }
+        }
+        __syncthreads();
+#pragma unroll
+        for (int c = 0; c < 3; ++c)
+#pragma unroll
+            for (int k = 0; k < IT; ++k) {
+                const int64_t i = base + k * kScanThreads + threadIdx.x;
+                if (i < n) S.out[c][i] = s_val[c][k * kScanThreads + threadIdx.x];
+            }
+        if (tile == ntiles - 1 && threadIdx.x < 3 && S.tot[threadIdx.x])
+            *S.tot[threadIdx.x] = s_excl[threadIdx.x] + agg[threadIdx.x];
+        __syncthreads();
+    }
+    if (ntiles == 0 && blockIdx.x == 0 && threadIdx.x < 3 && S.tot[threadIdx.x]) *S.tot[threadIdx.x] = 0;
+}
+
+void dscan3(sfb_ctx *ctx, const int32_t *in0, const int32_t *in1, const int32_t *in2, int32_t *out0,
+            int32_t *out1, int32_t *out2, const int64_t *d_n, int64_t n_fixed, int64_t *tot0,
+            int64_t *tot1, int64_t *tot2) {
+    const int64_t tiles = (n_fixed + kScan3Items * kScanThreads - 1) / (kScan3Items * kScanThreads) + 1;
+    const size_t bytes = sizeof(unsigned long long) * (size_t)(3 * tiles + 1);
+    auto *status = static_cast<unsigned long long *>(ctx->arena.alloc_bytes(bytes));
+    SFB_CUDA(cudaMemsetAsync(status, 0, bytes, ctx->stream));
+    Scan3 S{{in0, in1, in2}, {out0, out1, out2}, {tot0, tot1, tot2}};
+    const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(tiles, 2 * 148));
+    k_scan3_lb<<<grid, kScanThreads, 0, ctx->stream>>>(S, d_n, n_fixed, status, tiles,
+                                                       reinterpret_cast<unsigned int *>(status + 3 * tiles));
+    SFB_CHECK_LAUNCH();
+}
+
 // exclusive (or inclusive) scan of n int32 (n from device if d_n, else n_fixed);
 // in-place allowed; the grand total is written to *total_out when given.
 void dscan(sfb_ctx *ctx, const int32_t *in, int32_t *out, const int64_t *d_n, int64_t n_fixed,

@@ -722,6 +722,28 @@ __global__ void k_list_rects(const uint32_t *__restrict__ ids, const int64_t *__
     SFB_FOR(i, n) out[i] = rect[ids[i]];
 }
 
+__global__ void k_tile_index(const uint32_t *__restrict__ fk, const int64_t *__restrict__ d_ef,
+                             const uint32_t *__restrict__ sk, const int64_t *__restrict__ d_es,
+                             const uint32_t *__restrict__ s_ids, const int4 *__restrict__ rect, int64_t nt,
+                             int64_t ns, int32_t *__restrict__ f_off, int32_t *__restrict__ s_off,
+                             int4 *__restrict__ srect) {
+    const int64_t ef = *d_ef, es = *d_es;
+    auto lower = [](const uint32_t *k, int64_t n, uint32_t v) {
+        int64_t lo = 0, hi = n;
+        while (lo < hi) {
+            const int64_t mid = (lo + hi) >> 1;
+            if (k[mid] < v) lo = mid + 1;
+            else hi = mid;
+        }
+        return (int32_t)lo;
+    };
+    SFB_FOR(x, max(es, nt + ns + 2)) {
+        if (x < es) srect[x] = rect[s_ids[x]];
+        if (x <= nt) f_off[x] = lower(fk, ef, (uint32_t)x);
+        else if (x <= nt + ns + 1) s_off[x - nt - 1] = lower(sk, es, (uint32_t)(x - nt - 1));
+    }
+}
+
 __global__ void k_histogram(const uint32_t *__restrict__ keys, const int64_t *__restrict__ d_n,
                             int32_t *__restrict__ cnt) {
     const int64_t n = *d_n;
@@ -1268,8 +1290,7 @@ void render_run(sfb_ctx *ctx, const RenderInputs &in, const FrameParams *FP, int
     int4 *srect = ctx->arena.alloc<int4>(ebound);
     int32_t *f_off = ctx->arena.alloc<int32_t>(nt + 1);
     int32_t *s_off = ctx->arena.alloc<int32_t>(ns + 1);
-    SFB_CUDA(cudaMemsetAsync(f_off, 0, sizeof(int32_t) * (nt + 1), st));
-    SFB_CUDA(cudaMemsetAsync(s_off, 0, sizeof(int32_t) * (ns + 1), st));
+    const uint32_t *fk_sorted = fkey, *sk_sorted = skey;
     SFB_CUDA(cudaMemsetAsync(cnts, 0, sizeof(int32_t) * 3 * (nb + 1), st));
     const uint32_t *f_ids = fval, *s_ids = sval;
     if (n > 0) {
@@ -1294,9 +1315,8 @@ void render_run(sfb_ctx *ctx, const RenderInputs &in, const FrameParams *FP, int
                                            nty, opts.alpha_max, R);
             SFB_CHECK_LAUNCH();
         }
-        dscan(ctx, R.nf, pos, &C->runs1, nb + 1, &C->ef, false);
-        dscan(ctx, R.ns, pos + (nb + 1), &C->runs1, nb + 1, &C->es, false);
-        dscan(ctx, R.ng, pos + 2 * (nb + 1), &C->runs1, nb + 1, &C->g, false);
+        dscan3(ctx, R.nf, R.ns, R.ng, pos, pos + (nb + 1), pos + 2 * (nb + 1), &C->runs1, nb + 1,
+               &C->ef, &C->es, &C->g);
         k_emit<<<dgrid(ctx->grid_bound(n, ctx->hint_runs), 256), 256, 0, st>>>(
             R, pos, pos + (nb + 1), pos + 2 * (nb + 1), ntx, nsx, fkey, fval, skey, sval, glist, grect);
         SFB_CHECK_LAUNCH();
@@ -1313,14 +1333,14 @@ void render_run(sfb_ctx *ctx, const RenderInputs &in, const FrameParams *FP, int
         f_ids = dsort_pairs<uint32_t>(ctx, fkey, fval, fkey2, fval2, &C->ef, ebound, fbits) ? fval2 : fval;
         const uint32_t *fk = (f_ids == fval2) ? fkey2 : fkey;
         s_ids = dsort_pairs<uint32_t>(ctx, skey, sval, skey2, sval2, &C->es, ebound, sbits) ? sval2 : sval;
-        const uint32_t *sk = (s_ids == sval2) ? skey2 : skey;
-        k_list_rects<<<dgrid(ebound, 256), 256, 0, st>>>(s_ids, &C->es, R.rect, srect);
-        k_histogram<<<dgrid(ebound, 256), 256, 0, st>>>(fk, &C->ef, f_off);
-        k_histogram<<<dgrid(ebound, 256), 256, 0, st>>>(sk, &C->es, s_off);
-        SFB_CHECK_LAUNCH();
+        sk_sorted = (s_ids == sval2) ? skey2 : skey;
+        fk_sorted = fk;
     }
-    dscan(ctx, f_off, f_off, nullptr, nt + 1, nullptr, false);
-    dscan(ctx, s_off, s_off, nullptr, ns + 1, nullptr, false);
+    // tile offsets by binary search in the sorted keys (no histogram / scan),
+    // and the super-list rects in list order, in one launch
+    k_tile_index<<<dgrid(std::max<int64_t>(ebound, nt + ns + 2), 256), 256, 0, st>>>(
+        fk_sorted, &C->ef, sk_sorted, &C->es, s_ids, R.rect, nt, ns, f_off, s_off, srect);
+    SFB_CHECK_LAUNCH();
     ctx->mark(ST_BIN);
 
     CompParams CP{};
