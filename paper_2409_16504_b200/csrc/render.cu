@@ -491,12 +491,14 @@ __global__ void k_vdepth_keys(const int64_t *__restrict__ d_ng, const Proj P,
     const int64_t ng = *d_ng;
     const double zmin = __longlong_as_double((long long)mm[0]);
     const double zmax = __longlong_as_double((long long)mm[1]);
-    const double scale = zmax > zmin ? 4294967294.0 / (zmax - zmin) : 0.0;
+    // 24-bit monotone quantisation (3 radix passes over ~30k voxels; exact
+    // order restored inside equal-key groups by the fix-up), culled last
+    const double scale = zmax > zmin ? 16777214.0 / (zmax - zmin) : 0.0;
     SFB_FOR(g, ((ng + 31) & ~int64_t(31))) {
         bool k = false;
         if (g < ng) {
             k = P.keep[g];
-            keys[g] = k ? (uint32_t)fmin(floor((P.depth[g] - zmin) * scale), 4294967294.0) : 0xffffffffu;
+            keys[g] = k ? (uint32_t)fmin(floor((P.depth[g] - zmin) * scale), 16777214.0) : 0xffffffu;
             vals[g] = (uint32_t)g;
             vpos[g] = -1;
         }
@@ -543,43 +545,47 @@ __device__ __forceinline__ int32_t count_below(const int32_t *__restrict__ lst, 
 // thead[rank] = 1 where a tie group's merged order switches voxel (its first
 // rank included): the predecessor of p in the group is the largest group
 // point index below p, found with the same per-voxel binary searches.
-__global__ void k_vranks(const int32_t *__restrict__ order, const int32_t *__restrict__ p2g, int64_t n,
-                         const int32_t *__restrict__ goff, const int32_t *__restrict__ vpos,
+__global__ void k_vranks(const int32_t *__restrict__ order, const int32_t *__restrict__ goff,
                          const int32_t *__restrict__ off, const unsigned long long *__restrict__ full,
                          const uint32_t *__restrict__ vs, const int64_t *__restrict__ d_kg,
                          const double *__restrict__ colors, float4 *__restrict__ scol,
                          uint32_t *__restrict__ src, int32_t *__restrict__ thead) {
+    // one warp per sorted kept voxel, lanes over its points (CSR slots):
+    // the voxel's offsets are loaded once, the point reads / rank writes
+    // are coalesced, only the colour gather is random
     const int64_t KG = *d_kg;
-    SFB_FOR(s, n) {
-        const int32_t p = order[s];
-        const int32_t v = p2g[p];
-        const int32_t i = vpos[v];
-        if (i < 0) continue;
-        const int32_t w = (int32_t)s - goff[v];
-        int64_t rank = off[i] + w;
+    const int lane = threadIdx.x & 31;
+    const int64_t w0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t i = w0; i < KG; i += nw) {
+        const uint32_t v = vs[i];
+        const int32_t s0 = goff[v], s1 = goff[v + 1];
         int64_t gs, ge;
-        int32_t h = 0;
-        if (tie_group(full, i, KG, gs, ge)) {
-            rank = off[gs];
-            int32_t own = w > 0 ? order[s - 1] : -1, other = -1;   // predecessors of p
-            for (int64_t u = gs; u < ge; ++u) {
-                const uint32_t vu = vs[u];
-                if (vu == (uint32_t)v) {
-                    rank += w;
-                } else {
+        const bool tie = tie_group(full, i, KG, gs, ge);
+        const int64_t base = tie ? (int64_t)off[gs] : (int64_t)off[i];
+        for (int32_t s = s0 + lane; s < s1; s += 32) {
+            const int32_t p = order[s];
+            const int32_t w = s - s0;
+            int64_t rank = base + w;
+            int32_t h = 0;
+            if (tie) {
+                int32_t own = w > 0 ? order[s - 1] : -1, other = -1;   // predecessors of p
+                for (int64_t u = gs; u < ge; ++u) {
+                    const uint32_t vu = vs[u];
+                    if (vu == v) continue;
                     const int32_t *lst = order + goff[vu];
                     const int32_t cb = count_below(lst, goff[vu + 1] - goff[vu], p);
                     rank += cb;
                     if (cb > 0) other = max(other, lst[cb - 1]);
                 }
+                h = other > own || (own < 0 && other < 0);
             }
-            h = other > own || (own < 0 && other < 0);
+            src[rank] = (uint32_t)p;
+            thead[rank] = h;
+            if (scol)
+                scol[rank] = make_float4((float)colors[3 * (size_t)p], (float)colors[3 * (size_t)p + 1],
+                                         (float)colors[3 * (size_t)p + 2], 0.f);
         }
-        src[rank] = (uint32_t)p;
-        thead[rank] = h;
-        if (scol)
-            scol[rank] = make_float4((float)colors[3 * (size_t)p], (float)colors[3 * (size_t)p + 1],
-                                     (float)colors[3 * (size_t)p + 2], 0.f);
     }
 }
 
@@ -1206,7 +1212,7 @@ static void voxel_order(sfb_ctx *ctx, const RenderInputs &in, const Proj &P, Dev
     k_vdepth_keys<<<gv, 256, 0, st>>>(in.d_n_geom, P, mm, k0, v0, vpos, d_kg);
     SFB_CHECK_LAUNCH();
     // stable by voxel id within equal quantised keys; culled voxels (key ~0) last
-    const bool second = dsort_pairs<uint32_t>(ctx, k0, v0, k1, v1, in.d_n_geom, nbg, 32);
+    const bool second = dsort_pairs<uint32_t>(ctx, k0, v0, k1, v1, in.d_n_geom, nbg, 24);
     uint32_t *ks = second ? k1 : k0;
     vs = second ? v1 : v0;
     // exact (depth bits, voxel id) order inside equal-quantised-key groups
@@ -1223,9 +1229,8 @@ static void voxel_order(sfb_ctx *ctx, const RenderInputs &in, const Proj &P, Dev
     k_vcounts<<<gv, 256, 0, st>>>(vs, d_kg, in.geom_offsets, cnt, vpos);
     SFB_CHECK_LAUNCH();
     dscan(ctx, cnt, off, d_kg, nbg, &C->kept, false);
-    k_vranks<<<dgrid(in.n_points, 256), 256, 0, st>>>(in.geom_order, in.point_to_geom, in.n_points,
-                                                      in.geom_offsets, vpos, off, full, vs, d_kg,
-                                                      in.colors, scol, src, thead);
+    k_vranks<<<dgrid(32 * ctx->grid_bound(nbg, ctx->hint_m[0]), 256), 256, 0, st>>>(
+        in.geom_order, in.geom_offsets, off, full, vs, d_kg, in.colors, scol, src, thead);
     SFB_CHECK_LAUNCH();
 }
 
