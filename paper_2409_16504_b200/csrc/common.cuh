@@ -355,11 +355,12 @@ void activate_run(sfb_ctx *ctx, const float *raw, int64_t m, double scale, doubl
                   double *sigma, double *quat, double *opac, double *normal);
 void conv_layer(sfb_ctx *ctx, const NetLayer &L, const float *in, int ld_in, const int32_t *nbr,
                 int64_t nbr_ld, const int64_t *d_m, int64_t m_bound, int relu, float *out,
-                int ld_out, int64_t m_grid = -1);
+                int ld_out, int64_t m_grid = -1, int csplit = -1);
 void tconv_layer(sfb_ctx *ctx, const NetLayer &L, const float *in, int ld_in,
                  const int32_t *parent, const int32_t *tap, const int64_t *d_m, int64_t m_bound,
                  int relu, float *out, int ld_out, int64_t m_grid = -1,
-                 const int32_t *tmap = nullptr, const struct TapBuckets *tb = nullptr);
+                 const int32_t *tmap = nullptr, const struct TapBuckets *tb = nullptr,
+                 int csplit = -1);
 void layer_set(sfb_ctx *ctx, int kind, int kernel, int cin, int cout, const float *w_host,
                const float *b_host);
 // per-voxel Gaussians for the fused frame: centres, sigma, quat, opacity, normal

@@ -23,11 +23,14 @@
 //    27 taps are split across CTAs (split-K) to fill the 148 SMs; partial
 //    tiles go to a workspace and a deterministic reduce kernel sums them in
 //    split order, adds the bias and applies ReLU (bitwise run-to-run stable).
+#include <cooperative_groups.h>
 #include <cuda_bf16.h>
 
 #include "common.cuh"
 
 namespace sfb {
+
+namespace cg = cooperative_groups;
 
 namespace {
 
@@ -155,7 +158,9 @@ struct TcShape {
     static constexpr int A_TAP = TERMS * A_FLOATS, B_TAP = TERMS * B_FLOATS;   // per tap
     static constexpr int STAGE_FLOATS = TAPB * (A_TAP + B_TAP);
     static constexpr int STAGES = (STAGE_FLOATS * 4 * 2 <= 200 * 1024) ? 2 : 1;
-    static constexpr int SMEM = STAGES * STAGE_FLOATS * 4 + 1024 + 64;
+    // the stage buffers double as the cluster split-K reduction tile [kM][NP]
+    static constexpr int BUF_FLOATS = STAGES * STAGE_FLOATS > kM * NP ? STAGES * STAGE_FLOATS : kM * NP;
+    static constexpr int SMEM = BUF_FLOATS * 4 + 1024 + 64;
     // two accumulators (tap t in buffer t % 2): the epilogue of tap t-1 reads
     // one while the MMAs of tap t write the other
     static constexpr uint32_t TMEM_COLS = 2 * NP <= 32 ? 32 : (2 * NP <= 64 ? 64 : (2 * NP <= 128 ? 128 : 256));
@@ -185,7 +190,12 @@ k_conv_tc(const float *__restrict__ in, int ld_in, int cin, const int32_t *__res
           int64_t nbr_ld, const int64_t *__restrict__ d_m, int64_t m_fixed, int taps,
           const float *__restrict__ wtc, const float *__restrict__ bias, int cout, int relu,
           float *__restrict__ out, int ld_out, float *__restrict__ partial,
-          const int32_t *__restrict__ row_map, const int32_t *__restrict__ tap_off) {
+          const int32_t *__restrict__ row_map, const int32_t *__restrict__ tap_off,
+          int cluster_splits) {
+    // cluster mode (cluster_splits > 1): the splits of a tile are the CTAs of
+    // one thread-block cluster; partial tiles meet in distributed shared
+    // memory and each CTA reduces a slice of the tile's rows in split order —
+    // no partial workspace in HBM, no reduce launch
     // tap-bucketed mode (transposed conv, tap_off != null): rows arrive grouped
     // by tap, each bucket padded to whole 128-row tiles (tap_off = 9 padded
     // offsets), nbr[row] is the row's parent (-1 pad), row_map[row] its output
@@ -194,14 +204,15 @@ k_conv_tc(const float *__restrict__ in, int ld_in, int cin, const int32_t *__res
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     float *stage_base = reinterpret_cast<float *>(
         (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-    uint64_t *bar_full = reinterpret_cast<uint64_t *>(stage_base + S::STAGES * S::STAGE_FLOATS);
+    uint64_t *bar_full = reinterpret_cast<uint64_t *>(stage_base + S::BUF_FLOATS);
     uint64_t *bar_done = bar_full + 2;   // indexed by batch parity (i & 1), phase i >> 1
     uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(bar_done + 2);
 
     const int tid = threadIdx.x, warp = tid >> 5;
     const int64_t m = d_m ? *d_m : m_fixed;
     const int64_t tiles = (m + kM - 1) / kM;
-    const int splits = tap_off ? 1 : choose_splits(tiles, taps, kSplitTarget);
+    const int splits = tap_off ? 1 : (cluster_splits > 0 ? cluster_splits
+                                                         : choose_splits(tiles, taps, kSplitTarget));
     const int tps = (taps + splits - 1) / splits;
     const int64_t work = tiles * splits;
     if ((int64_t)blockIdx.x >= work) return;   // uniform per CTA, before any collective
@@ -406,7 +417,31 @@ k_conv_tc(const float *__restrict__ in, int ld_in, int cin, const int32_t *__res
             ++item_issued;
         }
         if (item_issued > 0) drain(issued - 1);
-        if (row < m) {
+        if (cluster_splits > 1) {
+            // my partial tile into my shared memory (the stage buffers are idle
+            // now), cluster barrier, then rows [r0, r1) of the tile summed over
+            // the cluster's CTAs in split (= rank) order
+            float *red = stage_base;   // [kM][NP]
+#pragma unroll
+            for (int c = 0; c < NP; c += 4)
+                *reinterpret_cast<float4 *>(red + tid * NP + c) =
+                    make_float4(acc[c], acc[c + 1], acc[c + 2], acc[c + 3]);
+            cg::cluster_group cl = cg::this_cluster();
+            cl.sync();
+            const int rank = (int)cl.block_rank();
+            const int per = (kM + splits - 1) / splits;
+            const int r0 = rank * per, r1 = min(kM, r0 + per);
+            for (int e = tid; e < (r1 - r0) * NP; e += kThreadsTC) {
+                const int rr = r0 + e / NP, c = e % NP;
+                const int64_t grow = row0 + rr;
+                if (c >= cout || grow >= m) continue;
+                float sum = 0.f;
+                for (int k = 0; k < splits; ++k) sum += cl.map_shared_rank(red, k)[rr * NP + c];
+                const float v = sum + bias[c];
+                out[grow * (int64_t)ld_out + c] = relu ? fmaxf(v, 0.f) : v;
+            }
+            cl.sync();   // peers keep their shared memory until every slice is read
+        } else if (row < m) {
             if (splits > 1) {
                 float *p = partial + ((size_t)split * m + row) * NP;
 #pragma unroll
@@ -487,7 +522,8 @@ int pad_n(int c) { return c <= 16 ? 16 : (c <= 32 ? 32 : (c <= 64 ? 64 : (c <= 1
 template <int KP, int NP, bool BF>
 void launch_tc(sfb_ctx *ctx, const NetLayer &L, const float *in, int ld_in, const int32_t *nbr,
                int64_t nbr_ld, const int64_t *d_m, int64_t m_bound, int relu, float *out,
-               int ld_out, int64_t m_grid, const int32_t *row_map, const int32_t *tap_off) {
+               int ld_out, int64_t m_grid, const int32_t *row_map, const int32_t *tap_off,
+               int csplit_req) {
     using S = TcShape<KP, NP, BF>;
     static bool attr = false;
     if (!attr) {
@@ -496,17 +532,45 @@ void launch_tc(sfb_ctx *ctx, const NetLayer &L, const float *in, int ld_in, cons
         attr = true;
     }
     const int64_t tiles_bound = (m_grid + kM - 1) / kM;
-    const int64_t work_bound = tap_off ? tiles_bound
-                                       : tiles_bound * choose_splits(tiles_bound, L.taps, kSplitTarget);
+    // Split-K. csplit_req > 1: the splits of a tile form a thread-block
+    // cluster (size fixed by the caller from the layer's place in the
+    // network, never from size hints, so the summation order — hence the
+    // result — does not depend on launch-time bounds); 1: no split; < 0:
+    // splits chosen on the device from the actual row count, partials
+    // reduced by k_splitk_reduce.
+    const int csplit = tap_off ? 1 : (csplit_req > 8 ? 8 : csplit_req);
+    if (csplit > 1) {
+        const int64_t m_tiles = (m_bound + kM - 1) / kM;   // grid covers the device count's bound
+        cudaLaunchConfig_t cfg{};
+        cfg.gridDim = dim3((unsigned)(std::max<int64_t>(1, std::min(tiles_bound, m_tiles)) * csplit));
+        cfg.blockDim = dim3(kThreadsTC);
+        cfg.dynamicSmemBytes = S::SMEM;
+        cfg.stream = ctx->stream;
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeClusterDimension;
+        at[0].val.clusterDim.x = (unsigned)csplit;
+        at[0].val.clusterDim.y = 1;
+        at[0].val.clusterDim.z = 1;
+        cfg.attrs = at;
+        cfg.numAttrs = 1;
+        const float *wts = BF ? reinterpret_cast<const float *>(L.w_bf16) : L.w_tc;
+        SFB_CUDA(cudaLaunchKernelEx(&cfg, k_conv_tc<KP, NP, BF>, in, ld_in, L.cin, nbr, nbr_ld, d_m,
+                                    m_bound, L.taps, wts, L.b, L.cout, relu, out, ld_out,
+                                    static_cast<float *>(nullptr), row_map, tap_off, csplit));
+        return;
+    }
+    const int64_t work_bound = (tap_off || csplit == 1)
+                                   ? tiles_bound
+                                   : tiles_bound * choose_splits(tiles_bound, L.taps, kSplitTarget);
     const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(work_bound, kSplitTarget));
     float *partial = ctx->arena.alloc<float>((size_t)std::min<int64_t>(kMaxPartialRows,
                                                                        32 * m_bound) * NP);
     const float *wts = BF ? reinterpret_cast<const float *>(L.w_bf16) : L.w_tc;
     k_conv_tc<KP, NP, BF><<<grid, kThreadsTC, S::SMEM, ctx->stream>>>(
         in, ld_in, L.cin, nbr, nbr_ld, d_m, m_bound, L.taps, wts, L.b, L.cout, relu, out, ld_out,
-        partial, row_map, tap_off);
+        partial, row_map, tap_off, csplit == 1 ? 1 : 0);
     SFB_CHECK_LAUNCH();
-    if (tap_off) return;   // one tap per tile: no split-K partials
+    if (tap_off || csplit == 1) return;   // no split-K partials
     k_splitk_reduce<<<dgrid(std::min<int64_t>(m_grid, kMaxPartialRows) * L.cout, 256), 256, 0,
                       ctx->stream>>>(partial, d_m, m_bound, L.taps, NP, L.b, L.cout, relu, out,
                                      ld_out);
@@ -541,16 +605,17 @@ void prepare_tc_weights(sfb_ctx *ctx, NetLayer &L) {
 
 void conv_layer_tc(sfb_ctx *ctx, const NetLayer &L, const float *in, int ld_in, const int32_t *nbr,
                    int64_t nbr_ld, const int64_t *d_m, int64_t m_bound, int relu, float *out,
-                   int ld_out, int64_t m_grid, const int32_t *row_map, const int32_t *tap_off) {
+                   int ld_out, int64_t m_grid, const int32_t *row_map, const int32_t *tap_off,
+                   int csplit) {
     const bool bf = ctx->net_mode == SFB_NET_TC_BF16;
 #define SFB_TC_CASE(K, N)                                                                 \
     if (L.cin_pad == K && L.cout_pad == N) {                                              \
         if (bf)                                                                           \
             launch_tc<K, N, true>(ctx, L, in, ld_in, nbr, nbr_ld, d_m, m_bound, relu, out, ld_out, \
-                                  m_grid, row_map, tap_off);                              \
+                                  m_grid, row_map, tap_off, csplit);                      \
         else                                                                              \
             launch_tc<K, N, false>(ctx, L, in, ld_in, nbr, nbr_ld, d_m, m_bound, relu, out, ld_out, \
-                                   m_grid, row_map, tap_off);                             \
+                                   m_grid, row_map, tap_off, csplit);                     \
         return;                                                                           \
     }
     SFB_TC_CASE(16, 16) SFB_TC_CASE(16, 32) SFB_TC_CASE(16, 64) SFB_TC_CASE(16, 128)

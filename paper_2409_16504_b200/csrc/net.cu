@@ -22,7 +22,7 @@ namespace sfb {
 void conv_layer_tc(sfb_ctx *ctx, const NetLayer &L, const float *in, int ld_in, const int32_t *nbr,
                    int64_t nbr_ld, const int64_t *d_m, int64_t m_bound, int relu, float *out,
                    int ld_out, int64_t m_grid, const int32_t *row_map = nullptr,
-                   const int32_t *tap_off = nullptr);
+                   const int32_t *tap_off = nullptr, int csplit = -1);
 bool conv_tc_supported(const NetLayer &L);
 void prepare_tc_weights(sfb_ctx *ctx, NetLayer &L);
 
@@ -211,11 +211,12 @@ k_conv_simt(const float *__restrict__ in, int ld_in, const int32_t *__restrict__
 
 void conv_layer(sfb_ctx *ctx, const NetLayer &L, const float *in, int ld_in, const int32_t *nbr,
                 int64_t nbr_ld, const int64_t *d_m, int64_t m_bound, int relu, float *out,
-                int ld_out, int64_t m_grid) {
+                int ld_out, int64_t m_grid, int csplit) {
     if (m_bound == 0) return;
     if (m_grid < 0) m_grid = m_bound;
     if (ctx->net_mode != SFB_NET_SIMT_F32 && L.w_tc) {
-        conv_layer_tc(ctx, L, in, ld_in, nbr, nbr_ld, d_m, m_bound, relu, out, ld_out, m_grid);
+        conv_layer_tc(ctx, L, in, ld_in, nbr, nbr_ld, d_m, m_bound, relu, out, ld_out, m_grid,
+                      nullptr, nullptr, csplit);
         return;
     }
     SFB_REQUIRE(kRows * L.cout <= kMaxOut * kThreads, "conv: cout > 128 unsupported");
@@ -270,7 +271,7 @@ __global__ void k_tmap(const int32_t *__restrict__ parent, const int32_t *__rest
 void tconv_layer(sfb_ctx *ctx, const NetLayer &L, const float *in, int ld_in,
                  const int32_t *parent, const int32_t *tap, const int64_t *d_m, int64_t m_bound,
                  int relu, float *out, int ld_out, int64_t m_grid, const int32_t *tmap,
-                 const TapBuckets *tb) {
+                 const TapBuckets *tb, int csplit) {
     if (m_bound == 0) return;
     if (m_grid < 0) m_grid = m_bound;
     if (ctx->net_mode != SFB_NET_SIMT_F32 && L.w_tc) {
@@ -289,7 +290,8 @@ void tconv_layer(sfb_ctx *ctx, const NetLayer &L, const float *in, int ld_in,
             SFB_CHECK_LAUNCH();
             tmap = tbuf;
         }
-        conv_layer_tc(ctx, L, in, ld_in, tmap, m_bound, d_m, m_bound, relu, out, ld_out, m_grid);
+        conv_layer_tc(ctx, L, in, ld_in, tmap, m_bound, d_m, m_bound, relu, out, ld_out, m_grid,
+                      nullptr, nullptr, csplit);
         return;
     }
     k_tconv<<<dgrid(m_grid * L.cout, 256), 256, 0, ctx->stream>>>(
@@ -495,6 +497,12 @@ __global__ void k_feats_to_f32(const double *__restrict__ f, const int64_t *__re
 // Whole UNet + head with every level size kept on the device: buffers are
 // sized by the host bound (the point count bounds every level), kernels loop
 // over the device counts, so the sequence has no host synchronisation.
+// split-K of the encoder / bottleneck convs by level (fixed per level, never
+// from size hints, so results are independent of launch-time bounds): level 0
+// has ~M0/128 tiles, every level ~4x fewer; -1 = split on the device from the
+// actual row count (the bottleneck's few tiles want all 27 taps spread)
+constexpr int kLevelSplit[4] = {2, 4, 8, -1};
+
 void unet_run(sfb_ctx *ctx, const int32_t *coords0, const double *feats9, int64_t mb,
               const FrameParams &host, const FrameParams *P, DevCounts *C, float *raw) {
     Net &net = ctx->net;
@@ -554,7 +562,7 @@ void unet_run(sfb_ctx *ctx, const int32_t *coords0, const double *feats9, int64_
         cat[l] = ctx->arena.alloc<float>((size_t)mb * width[l]);
         const int up = dec[L - 1 - l];
         conv_layer(ctx, net.layers[layer++], pin[l], enc[l], nbr[l], mb, &C->m[l], mb, 1,
-                   cat[l] + up, width[l], mg[l]);
+                   cat[l] + up, width[l], mg[l], kLevelSplit[std::min(l, 3)]);
         pin[l + 1] = ctx->arena.alloc<float>((size_t)mb * enc[l + 1]);
         SFB_CUDA(cudaStreamWaitEvent(st, ctx->side_ev[l], 0));   // level l+1 structure ready
         pool_means(ctx, ps[l], &C->m[l + 1], mg[l + 1], cat[l] + up, enc[l + 1], width[l],
@@ -562,12 +570,12 @@ void unet_run(sfb_ctx *ctx, const int32_t *coords0, const double *feats9, int64_
     }
     float *bott = ctx->arena.alloc<float>((size_t)mb * enc[L + 1]);
     conv_layer(ctx, net.layers[layer++], pin[L], enc[L], nbr[L], mb, &C->m[L], mb, 1, bott,
-               enc[L + 1], mg[L]);
+               enc[L + 1], mg[L], kLevelSplit[std::min(L, 3)]);
     const float *coarse = bott;
     int ld_coarse = enc[L + 1];
     for (int l = L - 1; l >= 0; --l) {
         tconv_layer(ctx, net.layers[layer++], coarse, ld_coarse, ps[l].c2p, ps[l].tap, &C->m[l], mb,
-                    1, cat[l], width[l], mg[l], ps[l].tmap, &ps[l].buckets);
+                    1, cat[l], width[l], mg[l], ps[l].tmap, &ps[l].buckets, 8);
         coarse = cat[l];
         ld_coarse = width[l];
     }
