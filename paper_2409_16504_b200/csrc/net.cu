@@ -213,6 +213,9 @@ void conv_layer(sfb_ctx *ctx, const NetLayer &L, const float *in, int ld_in, con
                 int64_t nbr_ld, const int64_t *d_m, int64_t m_bound, int relu, float *out,
                 int ld_out, int64_t m_grid, int csplit) {
     if (m_bound == 0) return;
+#ifdef SFB_WHATIF_NO_CONV   // A/B builds only (tools/ab_*): measure the convs' share
+    return;
+#endif
     if (m_grid < 0) m_grid = m_bound;
     if (ctx->net_mode != SFB_NET_SIMT_F32 && L.w_tc) {
         conv_layer_tc(ctx, L, in, ld_in, nbr, nbr_ld, d_m, m_bound, relu, out, ld_out, m_grid,

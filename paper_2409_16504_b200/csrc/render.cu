@@ -1376,6 +1376,9 @@ void render_run(sfb_ctx *ctx, const RenderInputs &in, const FrameParams *FP, int
     CP.trans = trans;
     CP.rgba = rgba;
     CP.dbg = ctx->debug_counters;
+#ifdef SFB_WHATIF_NO_COMPOSITE   // A/B builds only (tools/ab_*): measure the stage's share
+    if (false)
+#endif
     if (TS * TS <= kCT) k_composite<1><<<(unsigned)nt, kCT, 0, st>>>(CP);
     else k_composite<4><<<(unsigned)nt, kCT, 0, st>>>(CP);
     SFB_CHECK_LAUNCH();

@@ -147,3 +147,20 @@ def test_exact_depth_tie_groups():
         ref = OR.render(est, cam, mode)
         assert np.abs(got[mode] - ref[mode]).max() <= TOL, mode
         assert np.abs(got["transmittance"] - ref["transmittance"]).max() <= TOL
+
+
+def test_lanes_and_graphs_bitwise_identical(setup):
+    """The same frame through different lanes (own contexts, arenas and graphs)
+    and through eager / captured / replayed calls is bitwise identical."""
+    pc, cloud, view, w = setup
+    cam = Camera.of(view)
+    dev = PointCloud(torch.from_numpy(cloud.positions).cuda(), torch.from_numpy(cloud.colors).cuda())
+    ref = None
+    for lane in (0, 1, 2):
+        for _ in range(3):   # eager, capture, replay
+            fb = render_frame(dev, w, cam, ("rgb", "normal"), lane=lane)
+            torch.cuda.synchronize()
+            got = (fb.rgb.clone(), fb.normal.clone(), fb.transmittance.clone())
+            if ref is None:
+                ref = got
+            assert all(torch.equal(a, b) for a, b in zip(got, ref)), lane
