@@ -164,3 +164,23 @@ def test_lanes_and_graphs_bitwise_identical(setup):
             if ref is None:
                 ref = got
             assert all(torch.equal(a, b) for a, b in zip(got, ref)), lane
+
+
+def test_fused_frame_edge_cases(setup):
+    """Everything culled (camera looking away), tiny clouds, alternating cloud
+    sizes on one lane (separate graphs per shape) — all against the two-step path."""
+    pc, cloud, view, w = setup
+    bg = (0.1, 0.2, 0.3)
+    away = Camera(np.diag([-1.0, 1.0, -1.0]) @ Camera.of(view).rotation, Camera.of(view).translation,
+                  view.fx, view.fy, view.cx, view.cy, 64, 48)
+    away.translation = -away.rotation @ Camera.of(view).eye()
+    fb = render_frame(pc, w, away, ("rgb", "normal"), background=bg).numpy()
+    assert (fb["transmittance"] == 1.0).all()
+    assert np.allclose(fb["rgb"], np.array(bg), atol=1e-7) and (fb["normal"] == 0).all()
+    rng = np.random.default_rng(8)
+    cam = Camera(np.eye(3), [0.0, 0.0, 5.0], 40.0, 40.0, 16.0, 16.0, 32, 32)
+    for n in (2, 3, 17, 2, 17):
+        tiny = PointCloud(rng.normal(size=(n, 3)), rng.random((n, 3)))
+        a = render_frame(tiny, w, cam, ("rgb", "normal"))
+        b = render_planes(estimate_neural(tiny, w), cam, ("rgb", "normal"))
+        assert torch.equal(a.rgb, b.rgb) and torch.equal(a.transmittance, b.transmittance), n
