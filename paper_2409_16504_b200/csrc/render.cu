@@ -881,7 +881,9 @@ __device__ __forceinline__ float3 horner3(const float4 *__restrict__ v, int m, f
 // check, _raster_kernels.py:185-187). m = run length unless T crosses the
 // cutoff inside the run; then T is iterated point by point exactly as the
 // reference does. Alpha, T and the thresholds stay float64.
-template <int NPIX>
+// MASK: the planes accumulated (SFB_PLANE_*), a compile-time constant so
+// unused accumulators and branches disappear from the hot loop
+template <int NPIX, int MASK>
 __global__ void __launch_bounds__(kCT, SFB_COMP_MINB) k_composite(CompParams P) {
     constexpr uint32_t NONE = 0xffffffffu;
     __shared__ uint32_t bitmap[kWin / 32];
@@ -902,8 +904,8 @@ __global__ void __launch_bounds__(kCT, SFB_COMP_MINB) k_composite(CompParams P) 
     const int TS = P.tile;
     const int64_t x_lo = tx * TS, y_lo = ty * TS;
     const int64_t x_end = min(x_lo + TS, P.W), y_end = min(y_lo + TS, P.H);
-    const bool want_rgb = P.plane_mask & SFB_PLANE_RGB, want_n = P.plane_mask & SFB_PLANE_NORMAL;
-    const bool want_d = P.plane_mask & SFB_PLANE_DEPTH;
+    constexpr bool want_rgb = MASK & SFB_PLANE_RGB, want_n = MASK & SFB_PLANE_NORMAL;
+    constexpr bool want_d = MASK & SFB_PLANE_DEPTH;
     const bool term = P.terminate;
 
     int32_t pxs[NPIX], pys[NPIX];
@@ -1379,8 +1381,15 @@ void render_run(sfb_ctx *ctx, const RenderInputs &in, const FrameParams *FP, int
 #ifdef SFB_WHATIF_NO_COMPOSITE   // A/B builds only (tools/ab_*): measure the stage's share
     if (false)
 #endif
-    if (TS * TS <= kCT) k_composite<1><<<(unsigned)nt, kCT, 0, st>>>(CP);
-    else k_composite<4><<<(unsigned)nt, kCT, 0, st>>>(CP);
+    const int cm = plane_mask & 7;
+#define SFB_COMP_CASE(M)                                                          \
+    if (cm == M) {                                                                \
+        if (TS * TS <= kCT) k_composite<1, M><<<(unsigned)nt, kCT, 0, st>>>(CP);  \
+        else k_composite<4, M><<<(unsigned)nt, kCT, 0, st>>>(CP);                 \
+    }
+    SFB_COMP_CASE(0) SFB_COMP_CASE(1) SFB_COMP_CASE(2) SFB_COMP_CASE(3)
+    SFB_COMP_CASE(4) SFB_COMP_CASE(5) SFB_COMP_CASE(6) SFB_COMP_CASE(7)
+#undef SFB_COMP_CASE
     SFB_CHECK_LAUNCH();
     ctx->mark(ST_COMPOSITE);
 }
