@@ -157,10 +157,18 @@ struct TcShape {
     static constexpr int B_FLOATS = BF ? NP * KP / 2 : NP * KP;
     static constexpr int A_TAP = TERMS * A_FLOATS, B_TAP = TERMS * B_FLOATS;   // per tap
     static constexpr int STAGE_FLOATS = TAPB * (A_TAP + B_TAP);
-    static constexpr int STAGES = (STAGE_FLOATS * 4 * 2 <= 200 * 1024) ? 2 : 1;
+    // one stage: measured on config 2, a second stage buys no overlap the
+    // co-resident CTAs of other items do not already give, and halving the
+    // shared memory raises residency (0.379 vs 0.403 ms/frame with 8 lanes)
+#ifndef SFB_TC_MAX_STAGES
+#define SFB_TC_MAX_STAGES 1
+#endif
+    static constexpr int STAGES = (STAGE_FLOATS * 4 * 2 <= 200 * 1024) ? SFB_TC_MAX_STAGES : 1;
     // the stage buffers double as the cluster split-K reduction tile [kM][NP]
     static constexpr int BUF_FLOATS = STAGES * STAGE_FLOATS > kM * NP ? STAGES * STAGE_FLOATS : kM * NP;
+    // + the kernel-map rows of one item's taps, sized per launch (src_rows)
     static constexpr int SMEM = BUF_FLOATS * 4 + 1024 + 64;
+    static constexpr int smem_bytes(int src_rows) { return SMEM + src_rows * kM * 4; }
     // two accumulators (tap t in buffer t % 2): the epilogue of tap t-1 reads
     // one while the MMAs of tap t write the other
     static constexpr uint32_t TMEM_COLS = 2 * NP <= 32 ? 32 : (2 * NP <= 64 ? 64 : (2 * NP <= 128 ? 128 : 256));
@@ -191,7 +199,7 @@ k_conv_tc(const float *__restrict__ in, int ld_in, int cin, const int32_t *__res
           const float *__restrict__ wtc, const float *__restrict__ bias, int cout, int relu,
           float *__restrict__ out, int ld_out, float *__restrict__ partial,
           const int32_t *__restrict__ row_map, const int32_t *__restrict__ tap_off,
-          int cluster_splits) {
+          int cluster_splits, int src_rows) {
     // cluster mode (cluster_splits > 1): the splits of a tile are the CTAs of
     // one thread-block cluster; partial tiles meet in distributed shared
     // memory and each CTA reduces a slice of the tile's rows in split order —
@@ -207,6 +215,8 @@ k_conv_tc(const float *__restrict__ in, int ld_in, int cin, const int32_t *__res
     uint64_t *bar_full = reinterpret_cast<uint64_t *>(stage_base + S::BUF_FLOATS);
     uint64_t *bar_done = bar_full + 2;   // indexed by batch parity (i & 1), phase i >> 1
     uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(bar_done + 2);
+    // kernel-map rows of this item's taps: s_src[t - t0][tid]
+    int32_t (*s_src)[kM] = reinterpret_cast<int32_t (*)[kM]>(stage_base + S::BUF_FLOATS + 16);
 
     const int tid = threadIdx.x, warp = tid >> 5;
     const int64_t m = d_m ? *d_m : m_fixed;
@@ -216,7 +226,7 @@ k_conv_tc(const float *__restrict__ in, int ld_in, int cin, const int32_t *__res
     const int tps = (taps + splits - 1) / splits;
     const int64_t work = tiles * splits;
     if ((int64_t)blockIdx.x >= work) return;   // uniform per CTA, before any collective
-    if (tps > 32) __trap();                    // the host side guarantees <= 27 taps
+    if (!tap_off && tps > src_rows) __trap();  // the host sizes src_rows to the split
 
     if (tid == 0) {
         for (int s = 0; s < 2; ++s) {
@@ -256,7 +266,6 @@ k_conv_tc(const float *__restrict__ in, int ld_in, int cin, const int32_t *__res
         }
         asm volatile("tcgen05.fence::before_thread_sync;");
     };
-    __shared__ int32_t s_src[32][kM];   // kernel-map rows of this item's taps
     __shared__ uint32_t s_mask[kThreadsTC / 32];
     for (int64_t wi = blockIdx.x; wi < work; wi += gridDim.x) {
         const int64_t row0 = (wi / splits) * kM;
@@ -528,7 +537,7 @@ void launch_tc(sfb_ctx *ctx, const NetLayer &L, const float *in, int ld_in, cons
     static bool attr = false;
     if (!attr) {
         SFB_CUDA(cudaFuncSetAttribute(k_conv_tc<KP, NP, BF>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      S::SMEM));
+                                      S::smem_bytes(32)));
         attr = true;
     }
     const int64_t tiles_bound = (m_grid + kM - 1) / kM;
@@ -539,12 +548,15 @@ void launch_tc(sfb_ctx *ctx, const NetLayer &L, const float *in, int ld_in, cons
     // splits chosen on the device from the actual row count, partials
     // reduced by k_splitk_reduce.
     const int csplit = tap_off ? 1 : (csplit_req > 8 ? 8 : csplit_req);
+    // taps one work item can cover: one per bucket tile; taps/csplit in a
+    // cluster; with device-chosen splits the split may be 1, so all taps
+    const int src_rows = tap_off ? 1 : (csplit >= 1 ? (L.taps + csplit - 1) / csplit : std::min(L.taps, 32));
     if (csplit > 1) {
         const int64_t m_tiles = (m_bound + kM - 1) / kM;   // grid covers the device count's bound
         cudaLaunchConfig_t cfg{};
         cfg.gridDim = dim3((unsigned)(std::max<int64_t>(1, std::min(tiles_bound, m_tiles)) * csplit));
         cfg.blockDim = dim3(kThreadsTC);
-        cfg.dynamicSmemBytes = S::SMEM;
+        cfg.dynamicSmemBytes = S::smem_bytes(src_rows);
         cfg.stream = ctx->stream;
         cudaLaunchAttribute at[1];
         at[0].id = cudaLaunchAttributeClusterDimension;
@@ -556,7 +568,7 @@ void launch_tc(sfb_ctx *ctx, const NetLayer &L, const float *in, int ld_in, cons
         const float *wts = BF ? reinterpret_cast<const float *>(L.w_bf16) : L.w_tc;
         SFB_CUDA(cudaLaunchKernelEx(&cfg, k_conv_tc<KP, NP, BF>, in, ld_in, L.cin, nbr, nbr_ld, d_m,
                                     m_bound, L.taps, wts, L.b, L.cout, relu, out, ld_out,
-                                    static_cast<float *>(nullptr), row_map, tap_off, csplit));
+                                    static_cast<float *>(nullptr), row_map, tap_off, csplit, src_rows));
         return;
     }
     const int64_t work_bound = (tap_off || csplit == 1)
@@ -566,9 +578,9 @@ void launch_tc(sfb_ctx *ctx, const NetLayer &L, const float *in, int ld_in, cons
     float *partial = ctx->arena.alloc<float>((size_t)std::min<int64_t>(kMaxPartialRows,
                                                                        32 * m_bound) * NP);
     const float *wts = BF ? reinterpret_cast<const float *>(L.w_bf16) : L.w_tc;
-    k_conv_tc<KP, NP, BF><<<grid, kThreadsTC, S::SMEM, ctx->stream>>>(
+    k_conv_tc<KP, NP, BF><<<grid, kThreadsTC, S::smem_bytes(src_rows), ctx->stream>>>(
         in, ld_in, L.cin, nbr, nbr_ld, d_m, m_bound, L.taps, wts, L.b, L.cout, relu, out, ld_out,
-        partial, row_map, tap_off, csplit == 1 ? 1 : 0);
+        partial, row_map, tap_off, csplit == 1 ? 1 : 0, src_rows);
     SFB_CHECK_LAUNCH();
     if (tap_off || csplit == 1) return;   // no split-K partials
     k_splitk_reduce<<<dgrid(std::min<int64_t>(m_grid, kMaxPartialRows) * L.cout, 256), 256, 0,
