@@ -164,8 +164,14 @@ struct TcShape {
 #define SFB_TC_MAX_STAGES 1
 #endif
     static constexpr int STAGES = (STAGE_FLOATS * 4 * 2 <= 200 * 1024) ? SFB_TC_MAX_STAGES : 1;
+    // single stage with small weight tiles: the weights alone get a second
+    // buffer, so batch k+1's tiles (TMA) are in flight while batch k is staged
+    // and multiplied
+    static constexpr bool BDB = STAGES == 1 && TAPB * B_TAP * 4 <= 32 * 1024;
+    static constexpr int B_EXTRA = BDB ? TAPB * B_TAP : 0;
     // the stage buffers double as the cluster split-K reduction tile [kM][NP]
-    static constexpr int BUF_FLOATS = STAGES * STAGE_FLOATS > kM * NP ? STAGES * STAGE_FLOATS : kM * NP;
+    static constexpr int BUF_FLOATS = STAGES * STAGE_FLOATS + B_EXTRA > kM * NP ? STAGES * STAGE_FLOATS + B_EXTRA
+                                                                                 : kM * NP;
     // + the kernel-map rows of one item's taps, sized per launch (src_rows)
     static constexpr int SMEM = BUF_FLOATS * 4 + 1024 + 64;
     static constexpr int smem_bytes(int src_rows) { return SMEM + src_rows * kM * 4; }
@@ -320,9 +326,13 @@ k_conv_tc(const float *__restrict__ in, int ld_in, int cin, const int32_t *__res
         if (nxt_n) fetch();
         // weights: with two stages, batch k+1's tiles are fetched (TMA) as soon
         // as batch k-1 has drained, so their latency hides behind batch k
+        auto b_slot = [&](int slot) {   // weight buffer of a slot
+            return S::BDB ? (slot ? stage_base + S::STAGE_FLOATS : stage_base + TB * S::A_TAP)
+                          : stage_base + slot * S::STAGE_FLOATS + TB * S::A_TAP;
+        };
         auto load_w = [&](const int *tt, int nt, int slot) {
             const uint32_t bytes = (uint32_t)(nt * S::B_TAP * 4);
-            float *B = stage_base + slot * S::STAGE_FLOATS + TB * S::A_TAP;
+            float *B = b_slot(slot);
             mbar_expect_tx(&bar_full[slot], bytes);
             for (int q = 0; q < nt; ++q)
                 tma_bulk_g2s(B + q * S::B_TAP, wtc + (size_t)tt[q] * S::B_TAP, S::B_TAP * 4, &bar_full[slot]);
@@ -334,9 +344,11 @@ k_conv_tc(const float *__restrict__ in, int ld_in, int cin, const int32_t *__res
 #pragma unroll
             for (int q = 0; q < TB; ++q) cur_t[q] = nxt_t[q];
             const int s = issued % S::STAGES;
-            const int use = issued / S::STAGES;
+            // weight slot and its barrier phase: per stage, or per batch parity (BDB)
+            const int ws = S::BDB ? (issued & 1) : s;
+            const int use = S::BDB ? (issued >> 1) : issued / S::STAGES;
             float *A_base = stage_base + s * S::STAGE_FLOATS;
-            float *B_base = A_base + TB * S::A_TAP;
+            float *B_base = b_slot(ws);
             // stage free again: the batch that last used it (i - STAGES) has
             // completed. Batch barriers alternate by batch parity, so no wait
             // below can alias a later phase: the next commit to the barrier
@@ -345,7 +357,7 @@ k_conv_tc(const float *__restrict__ in, int ld_in, int cin, const int32_t *__res
                 const int j = issued - S::STAGES;
                 mbar_wait(&bar_done[j & 1], (j >> 1) & 1);
             }
-            if (tid == 0 && (S::STAGES == 1 || item_issued == 0)) load_w(cur_t, cur_n, s);
+            if (tid == 0 && ((S::STAGES == 1 && !S::BDB) || item_issued == 0)) load_w(cur_t, cur_n, ws);
             // my row of each tap of the batch in the canonical layout: bf16, or tf32 hi/lo
 #pragma unroll
             for (int q = 0; q < TB; ++q) {
@@ -386,10 +398,13 @@ k_conv_tc(const float *__restrict__ in, int ld_in, int cin, const int32_t *__res
             }
             take();
             if (nxt_n) fetch();   // next batch's rows, in flight from here
+            // next batch's weights: its slot was last read by batch issued-1,
+            // complete since the wait above
+            if (S::BDB && tid == 0 && nxt_n) load_w(nxt_t, nxt_n, (issued + 1) & 1);
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
             __syncthreads();   // also orders the last drain's TMEM reads before these MMAs
             if (tid == 0) {
-                mbar_wait(&bar_full[s], use & 1);
+                mbar_wait(&bar_full[ws], use & 1);
                 asm volatile("tcgen05.fence::after_thread_sync;");
                 const uint32_t lbo = 128, sbo = BF ? KP * 16 : KP * 32;
                 const uint32_t dst = tmem + (uint32_t)((issued & 1) * NP);
