@@ -205,7 +205,7 @@ k_conv_tc(const float *__restrict__ in, int ld_in, int cin, const int32_t *__res
           const float *__restrict__ wtc, const float *__restrict__ bias, int cout, int relu,
           float *__restrict__ out, int ld_out, float *__restrict__ partial,
           const int32_t *__restrict__ row_map, const int32_t *__restrict__ tap_off,
-          int cluster_splits, int src_rows) {
+          int cluster_splits, int src_rows, int vec4) {
     // cluster mode (cluster_splits > 1): the splits of a tile are the CTAs of
     // one thread-block cluster; partial tiles meet in distributed shared
     // memory and each CTA reduces a slice of the tile's rows in split order —
@@ -318,8 +318,20 @@ k_conv_tc(const float *__restrict__ in, int ld_in, int cin, const int32_t *__res
             for (int q = 0; q < TB; ++q) {
                 const int32_t src = q < nxt_n ? s_src[nxt_t[q] - t0][tid] : -1;
                 const float *x = src >= 0 ? in + (int64_t)src * ld_in : nullptr;
+                if (vec4) {   // 16-byte rows (cin, ld_in multiples of 4, aligned base)
 #pragma unroll
-                for (int k = 0; k < KP; ++k) v[q][k] = (x && k < cin) ? __ldg(x + k) : 0.f;
+                    for (int k = 0; k < KP; k += 4) {
+                        const float4 f = (x && k < cin) ? __ldg(reinterpret_cast<const float4 *>(x + k))
+                                                        : make_float4(0.f, 0.f, 0.f, 0.f);
+                        v[q][k] = f.x;
+                        v[q][k + 1] = f.y;
+                        v[q][k + 2] = f.z;
+                        v[q][k + 3] = f.w;
+                    }
+                } else {
+#pragma unroll
+                    for (int k = 0; k < KP; ++k) v[q][k] = (x && k < cin) ? __ldg(x + k) : 0.f;
+                }
             }
         };
         take();
@@ -566,6 +578,7 @@ void launch_tc(sfb_ctx *ctx, const NetLayer &L, const float *in, int ld_in, cons
     // taps one work item can cover: one per bucket tile; taps/csplit in a
     // cluster; with device-chosen splits the split may be 1, so all taps
     const int src_rows = tap_off ? 1 : (csplit >= 1 ? (L.taps + csplit - 1) / csplit : std::min(L.taps, 32));
+    const int vec4 = (L.cin % 4 == 0 && ld_in % 4 == 0 && (reinterpret_cast<uintptr_t>(in) & 15) == 0) ? 1 : 0;
     if (csplit > 1) {
         const int64_t m_tiles = (m_bound + kM - 1) / kM;   // grid covers the device count's bound
         cudaLaunchConfig_t cfg{};
@@ -583,7 +596,7 @@ void launch_tc(sfb_ctx *ctx, const NetLayer &L, const float *in, int ld_in, cons
         const float *wts = BF ? reinterpret_cast<const float *>(L.w_bf16) : L.w_tc;
         SFB_CUDA(cudaLaunchKernelEx(&cfg, k_conv_tc<KP, NP, BF>, in, ld_in, L.cin, nbr, nbr_ld, d_m,
                                     m_bound, L.taps, wts, L.b, L.cout, relu, out, ld_out,
-                                    static_cast<float *>(nullptr), row_map, tap_off, csplit, src_rows));
+                                    static_cast<float *>(nullptr), row_map, tap_off, csplit, src_rows, vec4));
         return;
     }
     const int64_t work_bound = (tap_off || csplit == 1)
@@ -595,7 +608,7 @@ void launch_tc(sfb_ctx *ctx, const NetLayer &L, const float *in, int ld_in, cons
     const float *wts = BF ? reinterpret_cast<const float *>(L.w_bf16) : L.w_tc;
     k_conv_tc<KP, NP, BF><<<grid, kThreadsTC, S::smem_bytes(src_rows), ctx->stream>>>(
         in, ld_in, L.cin, nbr, nbr_ld, d_m, m_bound, L.taps, wts, L.b, L.cout, relu, out, ld_out,
-        partial, row_map, tap_off, csplit == 1 ? 1 : 0, src_rows);
+        partial, row_map, tap_off, csplit == 1 ? 1 : 0, src_rows, vec4);
     SFB_CHECK_LAUNCH();
     if (tap_off || csplit == 1) return;   // no split-K partials
     k_splitk_reduce<<<dgrid(std::min<int64_t>(m_grid, kMaxPartialRows) * L.cout, 256), 256, 0,

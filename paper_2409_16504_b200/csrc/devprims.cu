@@ -12,6 +12,9 @@ namespace sfb {
 
 constexpr int kScanBlocks = 148;
 constexpr int kScanThreads = 1024;
+#ifndef SFB_SCAN_GRID
+#define SFB_SCAN_GRID (2 * 148)
+#endif
 
 // ------------------------------------------------------------------ scan
 __device__ __forceinline__ int64_t chunk_of(int64_t n, int blocks) {
@@ -286,7 +289,7 @@ void dscan3(sfb_ctx *ctx, const int32_t *in0, const int32_t *in1, const int32_t 
     auto *status = static_cast<unsigned long long *>(ctx->arena.alloc_bytes(bytes));
     SFB_CUDA(cudaMemsetAsync(status, 0, bytes, ctx->stream));
     Scan3 S{{in0, in1, in2}, {out0, out1, out2}, {tot0, tot1, tot2}};
-    const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(tiles, 2 * 148));
+    const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(tiles, SFB_SCAN_GRID));
     k_scan3_lb<<<grid, kScanThreads, 0, ctx->stream>>>(S, d_n, n_fixed, status, tiles,
                                                        reinterpret_cast<unsigned int *>(status + 3 * tiles));
     SFB_CHECK_LAUNCH();
@@ -301,7 +304,7 @@ void dscan(sfb_ctx *ctx, const int32_t *in, int32_t *out, const int64_t *d_n, in
     auto *status = static_cast<unsigned long long *>(ctx->arena.alloc_bytes(bytes));
     SFB_CUDA(cudaMemsetAsync(status, 0, bytes, ctx->stream));
     auto *ticket = reinterpret_cast<unsigned int *>(status + tiles);
-    const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(tiles, 2 * 148));
+    const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(tiles, SFB_SCAN_GRID));
     k_scan_lb<<<grid, kScanThreads, 0, ctx->stream>>>(in, out, d_n, n_fixed, total_out,
                                                       inclusive ? 1 : 0, status, ticket);
     SFB_CHECK_LAUNCH();
@@ -337,8 +340,11 @@ constexpr int kRsWarps = kRsThreads / 32;
 
 // blocks that take part in a pass: at least one 256-item sub-tile each, at
 // most kRsBlocks (small sorts spread thin: one sub-tile per block)
+#ifndef SFB_RS_MIN_ITEMS
+#define SFB_RS_MIN_ITEMS 256
+#endif
 __device__ __forceinline__ int rs_blocks(int64_t n) {
-    int64_t b = (n + kRsThreads - 1) / kRsThreads;
+    int64_t b = (n + SFB_RS_MIN_ITEMS - 1) / SFB_RS_MIN_ITEMS;
     return (int)max((int64_t)1, min(b, (int64_t)kRsBlocks));
 }
 

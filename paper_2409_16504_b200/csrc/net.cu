@@ -506,6 +506,25 @@ __global__ void k_feats_to_f32(const double *__restrict__ f, const int64_t *__re
 // actual row count (the bottleneck's few tiles want all 27 taps spread)
 constexpr int kLevelSplit[4] = {2, 4, 8, -1};
 
+// What-if builds only (tools/abn.sh): run a part twice to measure its marginal
+// cost in the concurrent-lane throughput (results unchanged: each part is a
+// pure function of buffers it does not write)
+#ifdef SFB_WHATIF_DUP_CONV
+#define SFB_DUP_CONV(x) x; x
+#else
+#define SFB_DUP_CONV(x) x
+#endif
+#ifdef SFB_WHATIF_DUP_STRUCT
+#define SFB_DUP_STRUCT(x) x; x
+#else
+#define SFB_DUP_STRUCT(x) x
+#endif
+#ifdef SFB_WHATIF_DUP_POOL
+#define SFB_DUP_POOL(x) x; x
+#else
+#define SFB_DUP_POOL(x) x
+#endif
+
 void unet_run(sfb_ctx *ctx, const int32_t *coords0, const double *feats9, int64_t mb,
               const FrameParams &host, const FrameParams *P, DevCounts *C, float *raw) {
     Net &net = ctx->net;
@@ -531,9 +550,10 @@ void unet_run(sfb_ctx *ctx, const int32_t *coords0, const double *feats9, int64_
         for (int l = 0; l <= L; ++l) kern[l] = net.layers[layer++].kernel;
     }
     // level 0: hash + kernel map on the critical path
-    HashTable h0 = hash_build(ctx, coords[0], &C->m[0], mb, mg[0]);
+    HashTable h0;
     nbr[0] = ctx->arena.alloc<int32_t>((size_t)kern[0] * kern[0] * kern[0] * mb);
-    kernel_map_build(ctx, h0, coords[0], &C->m[0], mb, 1, kern[0], nbr[0], mg[0]);
+    SFB_DUP_STRUCT(h0 = hash_build(ctx, coords[0], &C->m[0], mb, mg[0]);
+                   kernel_map_build(ctx, h0, coords[0], &C->m[0], mb, 1, kern[0], nbr[0], mg[0]));
     // side branch: the coordinate structure of every coarser level (parents,
     // children, taps, hash = the pooling table, kernel map) depends only on
     // coordinates, so it runs concurrently with the convolutions; event l
@@ -544,12 +564,13 @@ void unet_run(sfb_ctx *ctx, const int32_t *coords0, const double *feats9, int64_
     try {
         for (int l = 0; l < L; ++l) {
             int32_t *pc = ctx->arena.alloc<int32_t>((size_t)mb * 3);
-            ps[l] = pool_structure(ctx, coords[l], &C->m[l], mb, mg[l], 1 << l, pc, &C->m[l + 1]);
-            coords[l + 1] = pc;
             const int k = kern[l + 1];
             nbr[l + 1] = ctx->arena.alloc<int32_t>((size_t)k * k * k * mb);
-            kernel_map_build(ctx, ps[l].table, pc, &C->m[l + 1], mb, 2 << l, k, nbr[l + 1],
-                             mg[l + 1]);
+            SFB_DUP_STRUCT(ps[l] = pool_structure(ctx, coords[l], &C->m[l], mb, mg[l], 1 << l, pc,
+                                                  &C->m[l + 1]);
+                           kernel_map_build(ctx, ps[l].table, pc, &C->m[l + 1], mb, 2 << l, k,
+                                            nbr[l + 1], mg[l + 1]));
+            coords[l + 1] = pc;
             SFB_CUDA(cudaEventRecord(ctx->side_ev[l], ctx->stream));
         }
     } catch (...) {
@@ -564,21 +585,24 @@ void unet_run(sfb_ctx *ctx, const int32_t *coords0, const double *feats9, int64_
     for (int l = 0; l < L; ++l) {
         cat[l] = ctx->arena.alloc<float>((size_t)mb * width[l]);
         const int up = dec[L - 1 - l];
-        conv_layer(ctx, net.layers[layer++], pin[l], enc[l], nbr[l], mb, &C->m[l], mb, 1,
-                   cat[l] + up, width[l], mg[l], kLevelSplit[std::min(l, 3)]);
+        SFB_DUP_CONV(conv_layer(ctx, net.layers[layer], pin[l], enc[l], nbr[l], mb, &C->m[l], mb, 1,
+                                cat[l] + up, width[l], mg[l], kLevelSplit[std::min(l, 3)]));
+        ++layer;
         pin[l + 1] = ctx->arena.alloc<float>((size_t)mb * enc[l + 1]);
         SFB_CUDA(cudaStreamWaitEvent(st, ctx->side_ev[l], 0));   // level l+1 structure ready
-        pool_means(ctx, ps[l], &C->m[l + 1], mg[l + 1], cat[l] + up, enc[l + 1], width[l],
-                   pin[l + 1], enc[l + 1]);
+        SFB_DUP_POOL(pool_means(ctx, ps[l], &C->m[l + 1], mg[l + 1], cat[l] + up, enc[l + 1], width[l],
+                                pin[l + 1], enc[l + 1]));
     }
     float *bott = ctx->arena.alloc<float>((size_t)mb * enc[L + 1]);
-    conv_layer(ctx, net.layers[layer++], pin[L], enc[L], nbr[L], mb, &C->m[L], mb, 1, bott,
-               enc[L + 1], mg[L], kLevelSplit[std::min(L, 3)]);
+    SFB_DUP_CONV(conv_layer(ctx, net.layers[layer], pin[L], enc[L], nbr[L], mb, &C->m[L], mb, 1, bott,
+                            enc[L + 1], mg[L], kLevelSplit[std::min(L, 3)]));
+    ++layer;
     const float *coarse = bott;
     int ld_coarse = enc[L + 1];
     for (int l = L - 1; l >= 0; --l) {
-        tconv_layer(ctx, net.layers[layer++], coarse, ld_coarse, ps[l].c2p, ps[l].tap, &C->m[l], mb,
-                    1, cat[l], width[l], mg[l], ps[l].tmap, &ps[l].buckets, 8);
+        SFB_DUP_CONV(tconv_layer(ctx, net.layers[layer], coarse, ld_coarse, ps[l].c2p, ps[l].tap, &C->m[l],
+                                 mb, 1, cat[l], width[l], mg[l], ps[l].tmap, &ps[l].buckets, 8));
+        ++layer;
         coarse = cat[l];
         ld_coarse = width[l];
     }

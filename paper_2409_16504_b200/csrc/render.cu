@@ -1378,10 +1378,11 @@ void render_run(sfb_ctx *ctx, const RenderInputs &in, const FrameParams *FP, int
     CP.trans = trans;
     CP.rgba = rgba;
     CP.dbg = ctx->debug_counters;
-#ifdef SFB_WHATIF_NO_COMPOSITE   // A/B builds only (tools/ab_*): measure the stage's share
-    if (false)
-#endif
     const int cm = plane_mask & 7;
+#ifndef SFB_WHATIF_COMP_REPS   // what-if builds only (tools/abn.sh): the stage's marginal cost
+#define SFB_WHATIF_COMP_REPS 1
+#endif
+    for (int rep = 0; rep < SFB_WHATIF_COMP_REPS; ++rep) {
 #define SFB_COMP_CASE(M)                                                          \
     if (cm == M) {                                                                \
         if (TS * TS <= kCT) k_composite<1, M><<<(unsigned)nt, kCT, 0, st>>>(CP);  \
@@ -1389,6 +1390,7 @@ void render_run(sfb_ctx *ctx, const RenderInputs &in, const FrameParams *FP, int
     }
     SFB_COMP_CASE(0) SFB_COMP_CASE(1) SFB_COMP_CASE(2) SFB_COMP_CASE(3)
     SFB_COMP_CASE(4) SFB_COMP_CASE(5) SFB_COMP_CASE(6) SFB_COMP_CASE(7)
+    }
 #undef SFB_COMP_CASE
     SFB_CHECK_LAUNCH();
     ctx->mark(ST_COMPOSITE);
