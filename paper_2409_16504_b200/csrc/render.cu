@@ -890,6 +890,7 @@ __global__ void __launch_bounds__(kCT, SFB_COMP_MINB) k_composite(CompParams P) 
     __shared__ uint32_t list[kWin];
     __shared__ int s_nlist;
     __shared__ uint32_t s_add[3];
+    __shared__ uint32_t s_head;
     // the current chunk's run records (pixel box precomputed per run)
     __shared__ double r_mx[kChunk], r_my[kChunk], r_rr[kChunk], r_ia[kChunk], r_ib[kChunk],
         r_ic[kChunk], r_op[kChunk], r_dep[kChunk], r_rn[3][kChunk];
@@ -938,31 +939,40 @@ __global__ void __launch_bounds__(kCT, SFB_COMP_MINB) k_composite(CompParams P) 
     int ws = 128;  // rank window grows 128 -> 2048: most tiles saturate in the first
     bool done = false;
     while (!done) {
-        uint32_t head[3];
+        // the window's first 256-rank slice (ids and, in list order, rects)
+        // is loaded before the window is known: thread 0's ids are the list
+        // heads, so the window start costs no extra dependent round trip
+        uint32_t id[3];
+        int4 rc[2];
 #pragma unroll
-        for (int s = 0; s < 3; ++s) head[s] = cur[s] < end[s] ? ids[s][cur[s]] : NONE;
-        const uint32_t w0 = min(head[0], min(head[1], head[2]));
-        if (w0 == NONE) break;
-        const uint32_t w1 = w0 + (uint32_t)ws;
+        for (int s = 0; s < 3; ++s) {
+            const int64_t idx = cur[s] + threadIdx.x;
+            id[s] = idx < end[s] ? ids[s][idx] : NONE;
+            if (s && idx < end[s]) rc[s - 1] = (s == 1 ? P.s_rect : P.g_rect)[idx];
+        }
+        if (threadIdx.x == 0) s_head = min(id[0], min(id[1], id[2]));
         for (int i = threadIdx.x; i < kWin / 32; i += kCT) bitmap[i] = 0;
         if (threadIdx.x < 3) s_add[threadIdx.x] = 0;
         __syncthreads();
+        const uint32_t w0 = s_head;
+        if (w0 == NONE) break;
+        const uint32_t w1 = w0 + (uint32_t)ws;
         // one 256-rank slice of the window at a time: 3 id loads + 2 rect
         // loads in flight per thread, few registers (occupancy)
         for (int k = 0; k * kCT < ws; ++k) {
-            uint32_t id[3];
+            if (k) {
 #pragma unroll
-            for (int s = 0; s < 3; ++s) {
-                const int64_t idx = cur[s] + k * kCT + threadIdx.x;
-                id[s] = idx < end[s] ? ids[s][idx] : NONE;
-            }
-            int4 rc[2];
-#pragma unroll
-            for (int s = 1; s < 3; ++s)
-                if (id[s] < w1) {   // rects stored in list order: no dependent load
+                for (int s = 0; s < 3; ++s) {
                     const int64_t idx = cur[s] + k * kCT + threadIdx.x;
-                    rc[s - 1] = (s == 1 ? P.s_rect : P.g_rect)[idx];
+                    id[s] = idx < end[s] ? ids[s][idx] : NONE;
                 }
+#pragma unroll
+                for (int s = 1; s < 3; ++s)
+                    if (id[s] < w1) {   // rects stored in list order: no dependent load
+                        const int64_t idx = cur[s] + k * kCT + threadIdx.x;
+                        rc[s - 1] = (s == 1 ? P.s_rect : P.g_rect)[idx];
+                    }
+            }
 #pragma unroll
             for (int s = 0; s < 3; ++s) {
                 const uint32_t r = id[s];
