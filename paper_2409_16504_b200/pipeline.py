@@ -30,7 +30,13 @@ from .voxelgrid import device_bbox, lattice_scale, stage_cloud
 # addresses also keep the lane's CUDA-graph cache hot (graphs are keyed by
 # pointers).
 _UPLOAD_LANE = 1 << 16
+_BBOX_LANE = 1 << 17
 _upload_streams = {}
+# The bbox reduction and its 48-byte read-back run on a stream of their own:
+# on the upload stream the read-back (a device->host copy, queued on the same
+# copy engine as earlier frames' plane read-backs) would hold back the next
+# frame's host->device copies behind it in stream order.
+_bbox_streams = {}
 _staging = {}   # (device, lane) -> {"k": next, "bufs": [[pos, col, done_ev, ply_bytes, bbox_words], ...]}
 
 
@@ -61,6 +67,8 @@ def stage(cloud, lane: int = 0) -> StagedCloud:
     up = _upload_streams.get(dev)
     if up is None:
         up = _upload_streams[dev] = torch.cuda.Stream(device=dev)
+        _bbox_streams[dev] = torch.cuda.Stream(device=dev)
+    bb = _bbox_streams[dev]
     st = _staging.setdefault((dev, lane), {"k": 0, "bufs": [[None] * 5, [None] * 5]})
     slot = st["bufs"][st["k"]]
     st["k"] ^= 1
@@ -81,6 +89,7 @@ def stage(cloud, lane: int = 0) -> StagedCloud:
     if slot[2] is not None:
         up.wait_event(slot[2])   # the frame that last read this staging buffer
     uctx = _lib.context(lane=_UPLOAD_LANE + lane)
+    bctx = _lib.context(lane=_BBOX_LANE + lane)
 
     def host(a):
         if isinstance(a, torch.Tensor):
@@ -93,16 +102,18 @@ def stage(cloud, lane: int = 0) -> StagedCloud:
             layout = (_lib.I32 * 9)(*cloud.offsets)
             uctx.call("sfb_ply_decode", _lib.ptr(body), n, cloud.stride, layout, _lib.ptr(pos),
                       _lib.ptr(col), _lib.P(0))
-            uctx.call("sfb_bbox_async", _lib.ptr(pos), n, _lib.ptr(slot[4]))
-            bbox_ev = up.record_event()
+            pos_ev = up.record_event()
         else:
             hp = host(cloud.positions)
             pos.copy_(hp, non_blocking=hp.is_pinned())
-            uctx.call("sfb_bbox_async", _lib.ptr(pos), n, _lib.ptr(slot[4]))
-            bbox_ev = up.record_event()
+            pos_ev = up.record_event()
             hc = host(cloud.colors)
             col.copy_(hc, non_blocking=hc.is_pinned())
         done_ev = up.record_event()
+    bb.wait_event(pos_ev)
+    with torch.cuda.stream(bb):
+        bctx.call("sfb_bbox_async", _lib.ptr(pos), n, _lib.ptr(slot[4]))
+        bbox_ev = bb.record_event()
     return StagedCloud(pos, col, n, slot, bbox_ev, done_ev, slot[4])
 
 
