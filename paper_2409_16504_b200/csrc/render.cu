@@ -900,7 +900,8 @@ __global__ void __launch_bounds__(kCT, SFB_COMP_MINB) k_composite(CompParams P) 
     __shared__ uint8_t r_full[kChunk];   // run's pixel box and circle cover the whole tile
 
     const int64_t t = blockIdx.x;
-    const int64_t tx = t % P.ntx, ty = t / P.ntx;
+    const uint32_t ntx32 = (uint32_t)P.ntx;   // 32-bit division: the grid is < 2^31 tiles
+    const int64_t tx = blockIdx.x % ntx32, ty = blockIdx.x / ntx32;
     const int64_t st = (ty / kSuper) * P.nsx + tx / kSuper;
     const int TS = P.tile;
     const int64_t x_lo = tx * TS, y_lo = ty * TS;
@@ -914,9 +915,9 @@ __global__ void __launch_bounds__(kCT, SFB_COMP_MINB) k_composite(CompParams P) 
     double T[NPIX], c0[NPIX], c1[NPIX], c2[NPIX], n0[NPIX], n1[NPIX], n2[NPIX], dd[NPIX];
 #pragma unroll
     for (int k = 0; k < NPIX; ++k) {
-        int p = threadIdx.x + k * kCT;
-        pxs[k] = (int32_t)(x_lo + p % TS);
-        pys[k] = (int32_t)(y_lo + p / TS);
+        const uint32_t p = threadIdx.x + k * kCT;
+        pxs[k] = (int32_t)(x_lo + p % (uint32_t)TS);
+        pys[k] = (int32_t)(y_lo + p / (uint32_t)TS);
         valid[k] = p < TS * TS && pxs[k] < x_end && pys[k] < y_end;
         T[k] = 1.0;
         c0[k] = c1[k] = c2[k] = n0[k] = n1[k] = n2[k] = dd[k] = 0.0;
@@ -1163,8 +1164,9 @@ __global__ void __launch_bounds__(kCT, SFB_COMP_MINB) k_composite(CompParams P) 
             if (F.shade_mode != SFB_MODE_RGB) {
                 const double nrm = sqrt(n0[k] * n0[k] + n1[k] * n1[k] + n2[k] * n2[k]);
                 const bool z = !(nrm > 0.0);
-                const double u0 = z ? 0.0 : n0[k] / nrm, u1 = z ? 0.0 : n1[k] / nrm,
-                             u2 = z ? 0.0 : n2[k] / nrm;
+                const double inv = 1.0 / nrm;   // one division (the planes are float32)
+                const double u0 = z ? 0.0 : n0[k] * inv, u1 = z ? 0.0 : n1[k] * inv,
+                             u2 = z ? 0.0 : n2[k] * inv;
                 if (F.shade_mode == SFB_MODE_NORMAL) {
                     v[0] = u0 * 0.5 + 0.5;
                     v[1] = u1 * 0.5 + 0.5;
@@ -1192,11 +1194,12 @@ __global__ void __launch_bounds__(kCT, SFB_COMP_MINB) k_composite(CompParams P) 
             P.rgb[3 * pix + 2] = (float)(c2[k] + T[k] * bgc[2]);
         }
         if (P.normal) {
-            double nrm = sqrt(n0[k] * n0[k] + n1[k] * n1[k] + n2[k] * n2[k]);
-            bool z = !(nrm > 0.0);
-            P.normal[3 * pix + 0] = z ? 0.f : (float)(n0[k] / nrm);
-            P.normal[3 * pix + 1] = z ? 0.f : (float)(n1[k] / nrm);
-            P.normal[3 * pix + 2] = z ? 0.f : (float)(n2[k] / nrm);
+            const double nrm = sqrt(n0[k] * n0[k] + n1[k] * n1[k] + n2[k] * n2[k]);
+            const bool z = !(nrm > 0.0);
+            const double inv = 1.0 / nrm;   // one division (the planes are float32)
+            P.normal[3 * pix + 0] = z ? 0.f : (float)(n0[k] * inv);
+            P.normal[3 * pix + 1] = z ? 0.f : (float)(n1[k] * inv);
+            P.normal[3 * pix + 2] = z ? 0.f : (float)(n2[k] * inv);
         }
         if (P.depth) P.depth[pix] = (float)dd[k];
         if (P.trans) P.trans[pix] = (float)fmin(fmax(T[k], 0.0), 1.0);
