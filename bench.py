@@ -116,6 +116,16 @@ def cpu_frame_sample(cloud, view, weights, rows):
                 bin_blend_sample_s=bin_blend, rows=win[1] - win[0], nty=nty)
 
 
+def workload_config(name, cloud, views):
+    """The `config` keys both arms report for the same workload."""
+    n = int(len(cloud.positions))
+    W, H = int(views[0].width), int(views[0].height)
+    scene = "scenes.config1" if name == "c1" else "5-ellipsoid union, scenes.config2"
+    return {"workload": f"{name}: {n} pts ({scene}), P2ENet "
+                        f"init_random(seed 0) -> {W}x{H} rgb+normal+T, {len(views)} ring views",
+            "points": n, "width": W, "height": H}
+
+
 def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
@@ -150,7 +160,7 @@ def run_reference(args):
         "ms_per_step": 1e3 * tot / len(secs), "steps_sampled": len(secs),
         "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": f"{args.config}: ellipsoid union ~800k pts -> 1024x1024 rgb+normal"},
+        "config": workload_config(args.config, cloud, views),
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port",
                          "sample": sample},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -460,10 +470,8 @@ def run_ours(args):
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": f"{args.config}: 5-ellipsoid union, {n} pts (scenes.config2), "
-                                   f"P2ENet init_random(seed 0) -> {W}x{H} rgb+normal+T, "
-                                   "8 ring views", "points": n, "voxels": m0,
-                       "width": W, "height": H, "parallelism": f"frames x{world} (no collective)",
+            "config": {**workload_config(args.config, cloud, cams), "voxels": m0,
+                       "parallelism": f"frames x{world} (no collective)",
                        "lanes_per_gpu": lanes,
                        "l2": (f"timed region: {copies} distinct 38 MB input copies rotated "
                               f"({copies * 38} MB > 126 MB L2), frames overlapped on {lanes} "

@@ -20,3 +20,7 @@ timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_co
   --launch-skip 12 -c 1 -f -o gpurun_out/prof_comp_$tag python bench.py --steps 2 --warmup 1 \
   --lanes 1 --no-e2e --no-cpu --no-profile > gpurun_out/ncu_full_$tag.log 2>&1
 echo "ncu full rc=$?" >> gpurun_out/ncu_full_$tag.log
+timeout 900 ncu --metrics gpu__time_duration.sum,sm__cycles_active.sum,sm__warps_active.avg.pct_of_peak_sustained_active,launch__grid_size,launch__block_size,launch__occupancy_limit_shared_mem,launch__occupancy_limit_registers \
+  --clock-control none --cache-control none -c 400 --csv --log-file gpurun_out/smlaunch_$tag.csv \
+  python bench.py --steps 2 --warmup 1 --lanes 1 --no-e2e --no-cpu --no-profile > gpurun_out/ncu_sm_$tag.log 2>&1
+echo "ncu sm rc=$?" >> gpurun_out/ncu_sm_$tag.log

@@ -30,6 +30,16 @@ if lp.exists():
         + r.stdout)
     print(r.stdout)
 
+# ---- SM-active cycles per kernel (what each kernel costs the concurrent lanes)
+sp = go / f"smlaunch_{tag}.csv"
+if sp.exists():
+    r = subprocess.run([sys.executable, str(ROOT / "tools" / "smcost.py"), str(sp)],
+                       capture_output=True, text=True, check=True)
+    (out / f"{tag}_smcost.txt").write_text(
+        "# ncu sm__cycles_active.sum per kernel of one config-2 frame (launches serialised, L2 warm)\n"
+        + r.stdout)
+    print(r.stdout)
+
 # ---- full capture of the compositor
 rep = go / f"prof_comp_{tag}.ncu-rep"
 if rep.exists():

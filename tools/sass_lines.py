@@ -42,5 +42,7 @@ for r in data:
     tot[0] += s
     tot[1] += e
 print(f"total stall samples {tot[0]:.0f}, warp instructions {tot[1]:.3g}")
-for ln, (s, e) in sorted(agg.items(), key=lambda x: -x[1][0])[:top]:
+import os
+key = 1 if os.environ.get("BY") == "instr" else 0
+for ln, (s, e) in sorted(agg.items(), key=lambda x: -x[1][key])[:top]:
     print(f"line {ln}: stall {100*s/tot[0]:5.1f}%  instr {100*e/tot[1]:5.1f}%")
