@@ -501,10 +501,26 @@ __global__ void k_feats_to_f32(const double *__restrict__ f, const int64_t *__re
 // sized by the host bound (the point count bounds every level), kernels loop
 // over the device counts, so the sequence has no host synchronisation.
 // split-K of the encoder / bottleneck convs by level (fixed per level, never
-// from size hints, so results are independent of launch-time bounds): level 0
-// has ~M0/128 tiles, every level ~4x fewer; -1 = split on the device from the
-// actual row count (the bottleneck's few tiles want all 27 taps spread)
-constexpr int kLevelSplit[4] = {2, 4, 8, -1};
+// from size hints, so results are independent of launch-time bounds): the
+// splits of a tile form a thread-block cluster (DSMEM reduction); 1 = no
+// split, -1 = split on the device from the actual row count. Level 0 has
+// ~M0/128 tiles, every level ~4x fewer. Chosen by A/B on config 2 with 8
+// frames in flight: {1, 1, 4, 8} gives 0.337 ms/frame vs 0.364 for {2, 4, 8,
+// device} at the same single-frame latency — with concurrent frames the extra
+// CTAs and the partial-sum reduction cost more than the parallelism they buy.
+#ifndef SFB_L0_SPLIT
+#define SFB_L0_SPLIT 1
+#endif
+#ifndef SFB_L1_SPLIT
+#define SFB_L1_SPLIT 1
+#endif
+#ifndef SFB_L2_SPLIT
+#define SFB_L2_SPLIT 4
+#endif
+#ifndef SFB_L3_SPLIT
+#define SFB_L3_SPLIT 8
+#endif
+constexpr int kLevelSplit[4] = {SFB_L0_SPLIT, SFB_L1_SPLIT, SFB_L2_SPLIT, SFB_L3_SPLIT};
 
 // What-if builds only (tools/abn.sh): run a part twice to measure its marginal
 // cost in the concurrent-lane throughput (results unchanged: each part is a
