@@ -281,9 +281,14 @@ void tconv_layer(sfb_ctx *ctx, const NetLayer &L, const float *in, int ld_in,
         // the 8-tap map's scratch is taken on both paths so the arena layout
         // does not depend on which one the size hints select
         int32_t *tbuf = tmap ? nullptr : ctx->arena.alloc<int32_t>(8 * (size_t)m_bound);
-        // rows bucketed by tap (one tap per 128-row tile) when the level has
-        // enough tiles to fill the GPU; small levels split the 8 taps instead
-        if (tb && m_grid >= 64 * 128) {
+        // rows bucketed by tap (one tap per 128-row tile) from 16 tiles up;
+        // only tiny levels split the 8 taps over a cluster instead (A/B on
+        // config 2 with 8 frames in flight: 0.316 vs 0.336 ms/frame for a
+        // 64-tile threshold, same latency)
+#ifndef SFB_TCONV_BUCKET_ROWS
+#define SFB_TCONV_BUCKET_ROWS (16 * 128)
+#endif
+        if (tb && m_grid >= SFB_TCONV_BUCKET_ROWS) {
             conv_layer_tc(ctx, L, in, ld_in, tb->src, 0, tb->d_rows, tb->rows_bound, relu, out,
                           ld_out, tb->rows_grid, tb->perm, tb->off);
             return;
@@ -541,6 +546,10 @@ constexpr int kLevelSplit[4] = {SFB_L0_SPLIT, SFB_L1_SPLIT, SFB_L2_SPLIT, SFB_L3
 #define SFB_DUP_POOL(x) x
 #endif
 
+#ifndef SFB_TCONV_SPLIT
+#define SFB_TCONV_SPLIT 8
+#endif
+
 void unet_run(sfb_ctx *ctx, const int32_t *coords0, const double *feats9, int64_t mb,
               const FrameParams &host, const FrameParams *P, DevCounts *C, float *raw) {
     Net &net = ctx->net;
@@ -617,7 +626,7 @@ void unet_run(sfb_ctx *ctx, const int32_t *coords0, const double *feats9, int64_
     int ld_coarse = enc[L + 1];
     for (int l = L - 1; l >= 0; --l) {
         SFB_DUP_CONV(tconv_layer(ctx, net.layers[layer], coarse, ld_coarse, ps[l].c2p, ps[l].tap, &C->m[l],
-                                 mb, 1, cat[l], width[l], mg[l], ps[l].tmap, &ps[l].buckets, 8));
+                                 mb, 1, cat[l], width[l], mg[l], ps[l].tmap, &ps[l].buckets, SFB_TCONV_SPLIT));
         ++layer;
         coarse = cat[l];
         ld_coarse = width[l];
