@@ -37,9 +37,16 @@ constexpr int kFineMax = 16;   // tiles per run at the fine level
 constexpr int kSuper = 8;      // tiles per super-tile edge
 constexpr int kSuperMax = 16;  // super tiles per run at the middle level
 constexpr int kWin = 2048;     // rank window of the merge
-constexpr int kCT = 256;       // compositor threads per CTA
+// compositor CTA: 128 threads, two pixels each for the default 16x16 tile
+// (two independent per-pixel chains per thread), 7 CTAs per SM; A/B on
+// config 2 with 8 frames in flight: 0.308 ms/frame vs 0.316 for 256 threads x
+// one pixel (64 threads x 4 pixels: 0.34, register-starved)
+#ifndef SFB_KCT
+#define SFB_KCT 128
+#endif
+constexpr int kCT = SFB_KCT;   // compositor threads per CTA
 #ifndef SFB_COMP_MINB
-#define SFB_COMP_MINB 4
+#define SFB_COMP_MINB 7
 #endif
 constexpr int kChunk = 64;     // runs per compositing chunk
 
@@ -1396,10 +1403,12 @@ void render_run(sfb_ctx *ctx, const RenderInputs &in, const FrameParams *FP, int
 #define SFB_WHATIF_COMP_REPS 1
 #endif
     for (int rep = 0; rep < SFB_WHATIF_COMP_REPS; ++rep) {
+    constexpr int kNpixMid = (256 + kCT - 1) / kCT, kNpixMax = (1024 + kCT - 1) / kCT;
 #define SFB_COMP_CASE(M)                                                          \
     if (cm == M) {                                                                \
         if (TS * TS <= kCT) k_composite<1, M><<<(unsigned)nt, kCT, 0, st>>>(CP);  \
-        else k_composite<4, M><<<(unsigned)nt, kCT, 0, st>>>(CP);                 \
+        else if (TS * TS <= 256) k_composite<kNpixMid, M><<<(unsigned)nt, kCT, 0, st>>>(CP); \
+        else k_composite<kNpixMax, M><<<(unsigned)nt, kCT, 0, st>>>(CP);          \
     }
     SFB_COMP_CASE(0) SFB_COMP_CASE(1) SFB_COMP_CASE(2) SFB_COMP_CASE(3)
     SFB_COMP_CASE(4) SFB_COMP_CASE(5) SFB_COMP_CASE(6) SFB_COMP_CASE(7)
