@@ -109,6 +109,9 @@ VoxelSplats neural_voxels(sfb_ctx *ctx, const double *pos, const double *col, in
     o.order = ctx->arena.alloc<int32_t>(n);
     o.offsets = ctx->arena.alloc<int32_t>(n + 1);
     voxelize_run(ctx, pos, col, n, host, P, o, C);
+#ifdef SFB_WHATIF_DUP_VOX   // what-if builds only (tools/abn.sh): the stage's marginal cost
+    voxelize_run(ctx, pos, col, n, host, P, o, C);
+#endif
     ctx->mark(ST_VOXELIZE);
     float *raw = ctx->arena.alloc<float>(14 * n);
     unet_run(ctx, o.coords, o.feats, n, host, P, C, raw);

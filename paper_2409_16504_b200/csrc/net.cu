@@ -644,6 +644,10 @@ void unet_run(sfb_ctx *ctx, const int32_t *coords0, const double *feats9, int64_
     if (h1.cin == 32 && h1.cout == 64 && width[0] % 4 == 0) {
         k_head_row<32, 64><<<dgrid(mg[0], 128, 4), 128, 0, st>>>(cat[0], width[0], &C->m[0], h1.w,
                                                                  h1.b, h2.w, h2.b, raw);
+#ifdef SFB_WHATIF_DUP_HEAD   // what-if builds only (tools/abn.sh)
+        k_head_row<32, 64><<<dgrid(mg[0], 128, 4), 128, 0, st>>>(cat[0], width[0], &C->m[0], h1.w,
+                                                                 h1.b, h2.w, h2.b, raw);
+#endif
         SFB_CHECK_LAUNCH();
         return;
     }

@@ -1270,6 +1270,9 @@ void render_run(sfb_ctx *ctx, const RenderInputs &in, const FrameParams *FP, int
     const int64_t nt = ntx * nty, ns = nsx * nsy;
     const int64_t n = in.n_points;
     Proj P = project_inputs(ctx, in, FP);
+#ifdef SFB_WHATIF_DUP_PROJ
+    P = project_inputs(ctx, in, FP);
+#endif
     ctx->mark(ST_PROJECT);
     const int64_t nb = n > 0 ? n : 1;
     const bool want_rgb = plane_mask & SFB_PLANE_RGB, want_n = plane_mask & SFB_PLANE_NORMAL;
@@ -1357,6 +1360,10 @@ void render_run(sfb_ctx *ctx, const RenderInputs &in, const FrameParams *FP, int
         SFB_CHECK_LAUNCH();
         // stable sort by tile id keeps each tile's runs in rank order
         const int fbits = bits_for((uint64_t)nt), sbits = bits_for((uint64_t)ns);
+#ifdef SFB_WHATIF_DUP_BIN   // what-if builds only: sorting the sorted lists again is idempotent
+        dsort_pairs<uint32_t>(ctx, fkey, fval, fkey2, fval2, &C->ef, ebound, fbits);
+        dsort_pairs<uint32_t>(ctx, skey, sval, skey2, sval2, &C->es, ebound, sbits);
+#endif
         f_ids = dsort_pairs<uint32_t>(ctx, fkey, fval, fkey2, fval2, &C->ef, ebound, fbits) ? fval2 : fval;
         const uint32_t *fk = (f_ids == fval2) ? fkey2 : fkey;
         s_ids = dsort_pairs<uint32_t>(ctx, skey, sval, skey2, sval2, &C->es, ebound, sbits) ? sval2 : sval;

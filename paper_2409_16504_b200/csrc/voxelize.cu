@@ -180,6 +180,7 @@ static void voxelize_typed(sfb_ctx *ctx, const double *pos, const double *col, i
     const unsigned g = dgrid(n, 256);
     k_keygen<K><<<g, 256, 0, st>>>(pos, n, P, keys, vals);
     SFB_CHECK_LAUNCH();
+#ifndef SFB_VOX_OWN_SORT
     // host-known n: CUB onesweep (captured into the frame graph like any launch)
     size_t tb = 0;
     cub::DeviceRadixSort::SortPairs(nullptr, tb, keys, keys2, vals, vals2, (int)n, 0, key_bits, st);
@@ -187,6 +188,15 @@ static void voxelize_typed(sfb_ctx *ctx, const double *pos, const double *col, i
     SFB_CUDA(cub::DeviceRadixSort::SortPairs(tmp, tb, keys, keys2, vals, vals2, (int)n, 0, key_bits, st));
     K *ks = keys2;
     uint32_t *vs = vals2;
+#else
+    // the library's own stable LSD sort (devprims.cu): small per-CTA shared
+    // memory, so its CTAs share SMs with other lanes' kernels; measured on
+    // config 2: 0.305 vs 0.309 ms/frame throughput but 0.815 vs 0.80 ms
+    // latency (148 CTAs walk ~21 sub-tiles each), so CUB stays the default
+    const bool second = dsort_pairs<K>(ctx, keys, vals, keys2, vals2, nullptr, n, key_bits);
+    K *ks = second ? keys2 : keys;
+    uint32_t *vs = second ? vals2 : vals;
+#endif
     k_heads<K><<<g, 256, 0, st>>>(ks, n, flag);
     dscan(ctx, flag, flag, nullptr, n, nullptr, true);
     k_segments<K><<<g, 256, 0, st>>>(ks, vs, flag, n, P, out.coords, out.keys, out.p2v, out.order,
