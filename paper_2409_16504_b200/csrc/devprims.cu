@@ -7,6 +7,7 @@
 #include <algorithm>
 
 #include "common.cuh"
+#include "scan.cuh"
 
 namespace sfb {
 
@@ -19,32 +20,6 @@ constexpr int kScanThreads = 1024;
 // ------------------------------------------------------------------ scan
 __device__ __forceinline__ int64_t chunk_of(int64_t n, int blocks) {
     return (n + blocks - 1) / blocks;
-}
-
-__device__ __forceinline__ int32_t block_excl_scan(int32_t v, int32_t *s_warp, int32_t *total) {
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    int32_t x = v;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-        int32_t y = __shfl_up_sync(0xffffffffu, x, o);
-        if (lane >= o) x += y;
-    }
-    if (lane == 31) s_warp[warp] = x;
-    __syncthreads();
-    if (warp == 0) {
-        int32_t w = lane < (int)(blockDim.x >> 5) ? s_warp[lane] : 0;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            int32_t y = __shfl_up_sync(0xffffffffu, w, o);
-            if (lane >= o) w += y;
-        }
-        s_warp[lane] = w;
-    }
-    __syncthreads();
-    int32_t incl = x + (warp ? s_warp[warp - 1] : 0);
-    if (total) *total = s_warp[(blockDim.x >> 5) - 1];
-    __syncthreads();
-    return incl - v;
 }
 
 __global__ void __launch_bounds__(kScanThreads)
@@ -98,14 +73,6 @@ k_scan_apply(const int32_t *__restrict__ in, const int64_t *__restrict__ d_n, in
 // its own inclusive prefix. One launch per scan instead of two.
 constexpr int kLbItems = 4;
 constexpr int kLbTile = kLbItems * kScanThreads;
-constexpr unsigned long long kLbAgg = 1ull << 32, kLbInc = 2ull << 32;
-
-__device__ __forceinline__ unsigned long long lb_load(const unsigned long long *p) {
-    unsigned long long v;
-    asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
-    return v;
-}
-
 __global__ void __launch_bounds__(kScanThreads)
 k_scan_lb(const int32_t *__restrict__ in, int32_t *__restrict__ out, const int64_t *__restrict__ d_n,
           int64_t n_fixed, int64_t *__restrict__ total_out, int inclusive,

@@ -9,6 +9,7 @@
 #include <cub/cub.cuh>
 
 #include "common.cuh"
+#include "scan.cuh"
 
 namespace sfb {
 
@@ -188,6 +189,94 @@ __global__ void k_segments(const K *__restrict__ keys, const uint32_t *__restric
     }
 }
 
+// Segmentation of the sorted point keys in one pass (np.unique's sorted keys,
+// inverse and CSR of voxelgrid.py:146, 165-168): head flags from adjacent
+// keys, their inclusive scan by decoupled look-back (tiles in ticket order),
+// then per element the point -> voxel map, the CSR order and, at each head,
+// the voxel's coordinates, packed key and first offset. Replaces a flag
+// kernel, a scan and a segment kernel (and the flag array's round trips).
+constexpr int kSegThreads = 1024, kSegItems = 4, kSegTile = kSegThreads * kSegItems;
+
+template <class K>
+__global__ void __launch_bounds__(kSegThreads)
+k_vox_segments(const K *__restrict__ keys, const uint32_t *__restrict__ vals, int64_t n,
+               const FrameParams *__restrict__ P, int32_t *__restrict__ coords,
+               int64_t *__restrict__ pkeys, int32_t *__restrict__ p2v, int32_t *__restrict__ order,
+               int32_t *__restrict__ offsets, DevCounts *__restrict__ C,
+               unsigned long long *__restrict__ status, unsigned int *__restrict__ ticket) {
+    __shared__ int32_t s_val[kSegTile];
+    __shared__ int32_t s_warp[32];
+    __shared__ int s_tile;
+    __shared__ int32_t s_excl;
+    const int bx = P->bits[0], by = P->bits[1];
+    const int64_t ntiles = (n + kSegTile - 1) / kSegTile;
+    for (;;) {
+        if (threadIdx.x == 0) s_tile = (int)atomicAdd(ticket, 1u);
+        __syncthreads();
+        const int64_t tile = s_tile;
+        if (tile >= ntiles) break;
+        const int64_t base = tile * kSegTile;
+        K key[kSegItems];
+        int32_t f[kSegItems];
+#pragma unroll
+        for (int k = 0; k < kSegItems; ++k) {   // coalesced: element base + k*1024 + tid
+            const int64_t i = base + k * kSegThreads + threadIdx.x;
+            f[k] = 0;
+            if (i < n) {
+                key[k] = keys[i];
+                f[k] = (i == 0 || key[k] != keys[i - 1]) ? 1 : 0;
+            }
+            s_val[k * kSegThreads + threadIdx.x] = f[k];
+        }
+        __syncthreads();
+        int32_t v[kSegItems], sum = 0;   // blocked: elements tid*4 .. tid*4+3 of the tile
+#pragma unroll
+        for (int k = 0; k < kSegItems; ++k) {
+            v[k] = s_val[threadIdx.x * kSegItems + k];
+            sum += v[k];
+        }
+        int32_t agg;
+        const int32_t ex = block_excl_scan(sum, s_warp, &agg);
+        if (threadIdx.x < 32) {
+            const int32_t prefix = lb_prefix(status, tile, agg);
+            if (threadIdx.x == 0) s_excl = prefix;
+        }
+        __syncthreads();
+        int32_t run = s_excl + ex;
+#pragma unroll
+        for (int k = 0; k < kSegItems; ++k) {
+            run += v[k];
+            s_val[threadIdx.x * kSegItems + k] = run;   // inclusive head count
+        }
+        __syncthreads();
+#pragma unroll
+        for (int k = 0; k < kSegItems; ++k) {
+            const int64_t j = base + k * kSegThreads + threadIdx.x;
+            if (j >= n) continue;
+            const int32_t vox = s_val[k * kSegThreads + threadIdx.x] - 1;
+            const uint32_t i = vals[j];
+            order[j] = (int32_t)i;
+            p2v[i] = vox;
+            if (j == n - 1) {
+                offsets[vox + 1] = (int32_t)n;
+                C->m[0] = vox + 1;
+            }
+            if (f[k]) {
+                const uint64_t kk = (uint64_t)key[k];
+                const int64_t x = (int64_t)(kk & ((1ull << bx) - 1)) + P->lo[0];
+                const int64_t y = (int64_t)((kk >> bx) & ((1ull << by) - 1)) + P->lo[1];
+                const int64_t z = (int64_t)(kk >> (bx + by)) + P->lo[2];
+                coords[3 * vox + 0] = (int32_t)x;
+                coords[3 * vox + 1] = (int32_t)y;
+                coords[3 * vox + 2] = (int32_t)z;
+                pkeys[vox] = pack_key(x, y, z);
+                offsets[vox] = (int32_t)j;
+            }
+        }
+        __syncthreads();
+    }
+}
+
 // Six lanes per voxel, one per summed channel (scaled x, y, z, colour r, g,
 // b; five voxels per warp): each lane walks the voxel's points in ascending
 // point index (the CSR order) and adds its channel strictly in that order —
@@ -253,10 +342,23 @@ static void voxelize_typed(sfb_ctx *ctx, const double *pos, const double *col, i
     K *ks = second ? keys2 : keys;
     uint32_t *vs = second ? vals2 : vals;
 #endif
+#ifdef SFB_VOX_UNFUSED_SEGMENTS   // the three-launch form (A/B builds)
     k_heads<K><<<g, 256, 0, st>>>(ks, n, flag);
     dscan(ctx, flag, flag, nullptr, n, nullptr, true);
     k_segments<K><<<g, 256, 0, st>>>(ks, vs, flag, n, P, out.coords, out.keys, out.p2v, out.order,
                                      out.offsets, C);
+#else
+    {
+        const int64_t tiles = (n + kSegTile - 1) / kSegTile;
+        const size_t bytes = sizeof(unsigned long long) * (size_t)(tiles + 1);
+        auto *status = static_cast<unsigned long long *>(ctx->arena.alloc_bytes(bytes));
+        SFB_CUDA(cudaMemsetAsync(status, 0, bytes, st));
+        const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(tiles, 2 * 148));
+        k_vox_segments<K><<<grid, kSegThreads, 0, st>>>(ks, vs, n, P, out.coords, out.keys, out.p2v,
+                                                        out.order, out.offsets, C, status,
+                                                        reinterpret_cast<unsigned int *>(status + tiles));
+    }
+#endif
     SFB_CHECK_LAUNCH();
     const int64_t vwarps = (ctx->grid_bound(n, ctx->hint_m[0]) + 4) / 5;
     k_voxel_feats<<<dgrid(32 * vwarps, 256), 256, 0, st>>>(pos, col, out.order, out.offsets,
