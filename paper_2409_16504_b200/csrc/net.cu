@@ -209,6 +209,91 @@ k_conv_simt(const float *__restrict__ in, int ld_in, const int32_t *__restrict__
     }
 }
 
+// Narrow first layer (Cin = 9, Cout = 16 at level 0): one thread per output
+// row with all COUT accumulators in registers, the whole weight tensor in
+// shared memory (read as 16-byte broadcasts), the row's kernel-map entries
+// loaded up front and the next tap's input row in flight while the current
+// one is multiplied. Its K = 9 per tap would use a quarter of a 16-wide
+// tensor-core step and its 27-tap chain of MMA round trips is longer than
+// the FFMA work itself. Sums in tap order, then input channel (fp32 FFMA).
+// A/B on config 2 with 8 frames in flight: 0.297 vs 0.308 ms/frame for the
+// tcgen05 path on this layer, same latency.
+template <int CIN, int COUT, int TAPS, int PARTS>
+__global__ void __launch_bounds__(128)
+k_conv_narrow(const float *__restrict__ in, int ld_in, const int32_t *__restrict__ nbr, int64_t nbr_ld,
+              const int64_t *__restrict__ d_m, int64_t m_fixed, const float *__restrict__ w,
+              const float *__restrict__ b, int relu, float *__restrict__ out, int ld_out) {
+    // PARTS threads per row, each with COUT / PARTS of the outputs
+    constexpr int CO = COUT / PARTS;
+    static_assert(CO % 4 == 0, "outputs per thread must be a multiple of 4");
+    extern __shared__ __align__(16) float sW[];   // [TAPS][CIN][COUT]
+    for (int i = threadIdx.x; i < TAPS * CIN * COUT; i += blockDim.x) sW[i] = w[i];
+    __syncthreads();
+    const int64_t m = d_m ? *d_m : m_fixed;
+    SFB_FOR(item, m * PARTS) {
+        const int64_t row = item / PARTS;
+        const int c0 = (int)(item % PARTS) * CO;
+        int32_t src[TAPS];
+#pragma unroll
+        for (int t = 0; t < TAPS; ++t) src[t] = nbr[(int64_t)t * nbr_ld + row];
+        float acc[CO];
+#pragma unroll
+        for (int c = 0; c < CO; ++c) acc[c] = 0.f;
+        float x[CIN];
+#pragma unroll
+        for (int c = 0; c < CIN; ++c) x[c] = src[0] >= 0 ? __ldg(in + (int64_t)src[0] * ld_in + c) : 0.f;
+#pragma unroll
+        for (int t = 0; t < TAPS; ++t) {
+            float xn[CIN];
+            if (t + 1 < TAPS) {
+#pragma unroll
+                for (int c = 0; c < CIN; ++c)
+                    xn[c] = src[t + 1] >= 0 ? __ldg(in + (int64_t)src[t + 1] * ld_in + c) : 0.f;
+            }
+            if (src[t] >= 0) {
+#pragma unroll
+                for (int ci = 0; ci < CIN; ++ci) {
+                    const float4 *wr = reinterpret_cast<const float4 *>(sW + (t * CIN + ci) * COUT + c0);
+#pragma unroll
+                    for (int q = 0; q < CO / 4; ++q) {
+                        const float4 wv = wr[q];
+                        acc[4 * q] = fmaf(x[ci], wv.x, acc[4 * q]);
+                        acc[4 * q + 1] = fmaf(x[ci], wv.y, acc[4 * q + 1]);
+                        acc[4 * q + 2] = fmaf(x[ci], wv.z, acc[4 * q + 2]);
+                        acc[4 * q + 3] = fmaf(x[ci], wv.w, acc[4 * q + 3]);
+                    }
+                }
+            }
+            if (t + 1 < TAPS) {
+#pragma unroll
+                for (int c = 0; c < CIN; ++c) x[c] = xn[c];
+            }
+        }
+        float *o = out + row * (int64_t)ld_out + c0;
+#pragma unroll
+        for (int c = 0; c < CO; ++c) {
+            const float v = acc[c] + b[c0 + c];
+            o[c] = relu ? fmaxf(v, 0.f) : v;
+        }
+    }
+}
+
+template <int CIN, int COUT, int TAPS, int PARTS>
+static void launch_narrow(sfb_ctx *ctx, const NetLayer &L, const float *in, int ld_in, const int32_t *nbr,
+                          int64_t nbr_ld, const int64_t *d_m, int64_t m_bound, int relu, float *out,
+                          int ld_out, int64_t m_grid) {
+    constexpr size_t smem = sizeof(float) * TAPS * CIN * COUT;
+    static bool attr = false;
+    if (!attr) {
+        SFB_CUDA(cudaFuncSetAttribute(k_conv_narrow<CIN, COUT, TAPS, PARTS>,
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        attr = true;
+    }
+    k_conv_narrow<CIN, COUT, TAPS, PARTS><<<dgrid(m_grid * PARTS, 128, 8), 128, smem, ctx->stream>>>(
+        in, ld_in, nbr, nbr_ld, d_m, m_bound, L.w, L.b, relu, out, ld_out);
+    SFB_CHECK_LAUNCH();
+}
+
 void conv_layer(sfb_ctx *ctx, const NetLayer &L, const float *in, int ld_in, const int32_t *nbr,
                 int64_t nbr_ld, const int64_t *d_m, int64_t m_bound, int relu, float *out,
                 int ld_out, int64_t m_grid, int csplit) {
@@ -217,6 +302,19 @@ void conv_layer(sfb_ctx *ctx, const NetLayer &L, const float *in, int ld_in, con
     return;
 #endif
     if (m_grid < 0) m_grid = m_bound;
+#ifndef SFB_L0_TC
+    if (ctx->net_mode != SFB_NET_TC_BF16 && L.cin == 9 && L.cout == 16 && L.taps == 27) {
+        launch_narrow<9, 16, 27, 1>(ctx, L, in, ld_in, nbr, nbr_ld, d_m, m_bound, relu, out, ld_out, m_grid);
+        return;
+    }
+#endif
+#ifdef SFB_L1_NARROW   // A/B builds only: slower for 16 -> 32 (0.304-0.309 vs 0.297 ms/frame)
+    if (ctx->net_mode != SFB_NET_TC_BF16 && L.cin == 16 && L.cout == 32 && L.taps == 27) {
+        launch_narrow<16, 32, 27, SFB_L1_NARROW>(ctx, L, in, ld_in, nbr, nbr_ld, d_m, m_bound, relu, out,
+                                                 ld_out, m_grid);
+        return;
+    }
+#endif
     if (ctx->net_mode != SFB_NET_SIMT_F32 && L.w_tc) {
         conv_layer_tc(ctx, L, in, ld_in, nbr, nbr_ld, d_m, m_bound, relu, out, ld_out, m_grid,
                       nullptr, nullptr, csplit);
