@@ -24,7 +24,6 @@
 //      RGB + normal (+ depth) + T in float64 registers in ONE pass, and stops
 //      when every pixel of the tile has T < 1/255 — identical to the
 //      reference, whose per-pixel skip makes all later splats no-ops.
-#include <cub/cub.cuh>
 #include <cstddef>
 #include <utility>
 
@@ -327,20 +326,19 @@ static uint32_t *depth_order(sfb_ctx *ctx, const RenderInputs &in, const Proj &P
                     ctx->stream>>>(P, in.d_n_geom, in.n_geom, mm);
     k_depth_keys<<<dgrid(n, 256), 256, 0, ctx->stream>>>(n, in.point_to_geom, P, mm, k0, v0, &C->kept);
     SFB_CHECK_LAUNCH();
-    size_t tb = 0;
-    cub::DeviceRadixSort::SortPairs(nullptr, tb, k0, k1, v0, v1, (int)n, 0, 32, ctx->stream);
-    void *tmp = ctx->arena.alloc_bytes(tb);
-    SFB_CUDA(cub::DeviceRadixSort::SortPairs(tmp, tb, k0, k1, v0, v1, (int)n, 0, 32, ctx->stream));
+    // stable by point index within equal keys (devprims.cu radix sort)
+    const bool second = dsort_pairs<uint32_t>(ctx, k0, v0, k1, v1, nullptr, n, 32);
+    uint32_t *ks = second ? k1 : k0, *vs = second ? v1 : v0;
     auto *full = ctx->arena.alloc<unsigned long long>(n);
     uint8_t *need = ctx->arena.alloc<uint8_t>(4 * n);
     uint32_t *heads = ctx->arena.alloc<uint32_t>(n);
     SFB_CUDA(cudaMemsetAsync(need, 0, 4 * n, ctx->stream));
     const unsigned g = dgrid(n, 256);
-    k_depth_full<<<g, 256, 0, ctx->stream>>>(v1, in.point_to_geom, P, &C->kept, full);
-    k_depth_mark<<<g, 256, 0, ctx->stream>>>(k1, full, &C->kept, need, heads, &C->scratch[2]);
-    k_depth_fixup<<<2 * 148, 256, 0, ctx->stream>>>(k1, v1, full, &C->kept, heads, &C->scratch[2]);
+    k_depth_full<<<g, 256, 0, ctx->stream>>>(vs, in.point_to_geom, P, &C->kept, full);
+    k_depth_mark<<<g, 256, 0, ctx->stream>>>(ks, full, &C->kept, need, heads, &C->scratch[2]);
+    k_depth_fixup<<<2 * 148, 256, 0, ctx->stream>>>(ks, vs, full, &C->kept, heads, &C->scratch[2]);
     SFB_CHECK_LAUNCH();
-    return v1;
+    return vs;
 }
 
 // ------------------------------------------------------------ 3. runs

@@ -6,7 +6,9 @@
 //   float64 sums (bit-identical to np.add.at, which walks points in increasing
 //   index) -> 9 feature channels.
 // HBM-bound integer/byte work; no tensor cores.
+#ifdef SFB_VOX_CUB_SORT   // A/B builds only
 #include <cub/cub.cuh>
+#endif
 
 #include "common.cuh"
 #include "scan.cuh"
@@ -325,22 +327,22 @@ static void voxelize_typed(sfb_ctx *ctx, const double *pos, const double *col, i
     const unsigned g = dgrid(n, 256);
     k_keygen<K><<<g, 256, 0, st>>>(pos, n, P, keys, vals);
     SFB_CHECK_LAUNCH();
-#ifndef SFB_VOX_OWN_SORT
-    // host-known n: CUB onesweep (captured into the frame graph like any launch)
+#ifndef SFB_VOX_CUB_SORT
+    // the library's own stable LSD sort (devprims.cu: 8-bit digits, 1024-item
+    // sub-tiles ranked with __match_any_sync, small shared memory so its CTAs
+    // share SMs with the other lanes' kernels); A/B on config 2 against CUB's
+    // onesweep: 0.291 vs 0.298 ms/frame throughput, 0.787 vs 0.790 ms latency
+    const bool second = dsort_pairs<K>(ctx, keys, vals, keys2, vals2, nullptr, n, key_bits);
+    K *ks = second ? keys2 : keys;
+    uint32_t *vs = second ? vals2 : vals;
+#else
+    // CUB onesweep (A/B builds only)
     size_t tb = 0;
     cub::DeviceRadixSort::SortPairs(nullptr, tb, keys, keys2, vals, vals2, (int)n, 0, key_bits, st);
     void *tmp = ctx->arena.alloc_bytes(tb);
     SFB_CUDA(cub::DeviceRadixSort::SortPairs(tmp, tb, keys, keys2, vals, vals2, (int)n, 0, key_bits, st));
     K *ks = keys2;
     uint32_t *vs = vals2;
-#else
-    // the library's own stable LSD sort (devprims.cu): small per-CTA shared
-    // memory, so its CTAs share SMs with other lanes' kernels; measured on
-    // config 2: 0.305 vs 0.309 ms/frame throughput but 0.815 vs 0.80 ms
-    // latency (148 CTAs walk ~21 sub-tiles each), so CUB stays the default
-    const bool second = dsort_pairs<K>(ctx, keys, vals, keys2, vals2, nullptr, n, key_bits);
-    K *ks = second ? keys2 : keys;
-    uint32_t *vs = second ? vals2 : vals;
 #endif
 #ifdef SFB_VOX_UNFUSED_SEGMENTS   // the three-launch form (A/B builds)
     k_heads<K><<<g, 256, 0, st>>>(ks, n, flag);
