@@ -258,7 +258,9 @@ def run_ours(args):
         return cams[unit_of(i, rank, world, len(cams))]
 
     rgba_out = None   # render_pose leg: one RGBA8 device frame per (lane, input copy)
-    down = torch.cuda.Stream()   # device->host read-backs of the e2e legs
+    # device->host read-backs of the e2e legs: one stream per lane, so a frame's
+    # read-back starts when that frame is done, not behind slower earlier ones
+    downs = [torch.cuda.Stream() for _ in range(lanes)]
     down_done = {}
 
     def issue(i, cloud_list, host_out=None, src=None):
@@ -274,7 +276,8 @@ def run_ours(args):
             if (lane, k) in down_done:   # the previous read-back of these planes
                 streams[lane].wait_event(down_done.pop((lane, k)))
             fb = render_frame(src, weights, view_of(i), planes, out=outs[lane][k], lane=lane)
-            if host_out is not None:   # read-backs queue on one download stream
+            if host_out is not None:   # read-back on the lane's download stream
+                down = downs[lane]
                 down.wait_stream(streams[lane])
                 with torch.cuda.stream(down):
                     ho = host_out[lane]
@@ -294,16 +297,19 @@ def run_ours(args):
             st.wait_stream(cur)
         h0 = time.perf_counter()
         host_in = not (isinstance(cloud_list[0], PointCloud) and cloud_list[0].on_device)
-        # host inputs: frame i+1's upload is enqueued (pipeline.stage) before
-        # frame i waits for its bbox, so the copy engine never idles
-        nxt = stage(cloud_list[0], 0) if host_in else None
+        # host inputs: the uploads of frames i+1 and i+2 are enqueued
+        # (pipeline.stage) before frame i waits for its bbox, so the copy
+        # engine has ~2 frames of work queued and host hiccups do not idle it
+        ahead = 2
+        staged = [stage(cloud_list[j % copies], j % lanes) for j in range(min(ahead, n_frames))] \
+            if host_in else []
         for i in range(n_frames):
-            cur_src = nxt
-            if host_in and i + 1 < n_frames:
-                nxt = stage(cloud_list[(i + 1) % copies], (i + 1) % lanes)
+            cur_src = staged.pop(0) if host_in else None
+            if host_in and i + ahead < n_frames:
+                staged.append(stage(cloud_list[(i + ahead) % copies], (i + ahead) % lanes))
             issue(i, cloud_list, host_out, cur_src)
         host = time.perf_counter() - h0
-        for st in streams + [down]:
+        for st in streams + downs:
             cur.wait_stream(st)
         end.record(cur)
         end.synchronize()

@@ -13,7 +13,8 @@ from paper_2409_16504_b200.gaussians import Camera
 from paper_2409_16504_b200.pcio import PointCloud
 from paper_2409_16504_b200.pipeline import render_frame, stage
 
-lanes, copies, steps = 8, 9, 200
+lanes, copies = 8, 9
+steps = int(sys.argv[1]) if len(sys.argv) > 1 else 200
 cloud, views = scenes.config2()
 w = netplan.init_random(netplan.NetworkPlan(), 0)
 cams = [Camera.of(v) for v in views]
