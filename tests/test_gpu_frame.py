@@ -184,3 +184,38 @@ def test_fused_frame_edge_cases(setup):
         a = render_frame(tiny, w, cam, ("rgb", "normal"))
         b = render_planes(estimate_neural(tiny, w), cam, ("rgb", "normal"))
         assert torch.equal(a.rgb, b.rgb) and torch.equal(a.transmittance, b.transmittance), n
+
+
+def test_staged_pipeline_matches_device(setup):
+    """bench.py's e2e pattern: pinned host clouds staged two frames ahead
+    (pipeline.stage: uploads + bbox read-back on their own streams), frames
+    issued round-robin over lanes, planes read back on per-lane download
+    streams — every frame bitwise equal to the device-resident render."""
+    from paper_2409_16504_b200.pipeline import stage
+    from paper_2409_16504_b200 import scenes as S
+    pc, cloud, view, w = setup
+    cams = [Camera.of(v) for v in S.ring_views(cloud, 3, 96)]
+    host = PointCloud(torch.from_numpy(cloud.positions).pin_memory(),
+                      torch.from_numpy(cloud.colors).pin_memory(), validate=False)
+    dev = PointCloud(torch.from_numpy(cloud.positions).cuda(), torch.from_numpy(cloud.colors).cuda())
+    lanes, n = 3, 9
+    streams = [torch.cuda.Stream() for _ in range(lanes)]
+    downs = [torch.cuda.Stream() for _ in range(lanes)]
+    got = []
+    staged = [stage(host, j % lanes) for j in range(2)]
+    for i in range(n):
+        src = staged.pop(0)
+        if i + 2 < n:
+            staged.append(stage(host, (i + 2) % lanes))
+        lane = i % lanes
+        with torch.cuda.stream(streams[lane]):
+            fb = render_frame(src, w, cams[i % len(cams)], lane=lane)
+            downs[lane].wait_stream(streams[lane])
+            with torch.cuda.stream(downs[lane]):
+                got.append((fb.rgb.to("cpu", non_blocking=True), fb.normal.to("cpu", non_blocking=True),
+                            fb.transmittance.to("cpu", non_blocking=True)))
+    torch.cuda.synchronize()
+    for i, planes in enumerate(got):
+        ref = render_frame(dev, w, cams[i % len(cams)])
+        for a, b in zip(planes, (ref.rgb, ref.normal, ref.transmittance)):
+            assert torch.equal(a, b.cpu()), i
