@@ -940,8 +940,9 @@ __global__ void __launch_bounds__(kCT, SFB_COMP_MINB) k_composite(CompParams P) 
     const float4 *__restrict__ scol = P.scol, *__restrict__ snrm = P.snrm;
     const double alpha_max = P.alpha_max;
     const uint32_t *ids[3] = {P.f_ids, P.s_ids, P.g_ids};
-    int64_t cur[3] = {P.f_off[t], P.s_off[st], 0};
-    const int64_t end[3] = {P.f_off[t + 1], P.s_off[st + 1], *P.d_G};
+    // list positions as 32-bit (the entry lists are int32-indexed)
+    int32_t cur[3] = {P.f_off[t], P.s_off[st], 0};
+    const int32_t end[3] = {P.f_off[t + 1], P.s_off[st + 1], (int32_t)*P.d_G};
     int ws = 128;  // rank window grows 128 -> 2048: most tiles saturate in the first
     bool done = false;
     while (!done) {
@@ -952,7 +953,7 @@ __global__ void __launch_bounds__(kCT, SFB_COMP_MINB) k_composite(CompParams P) 
         int4 rc[2];
 #pragma unroll
         for (int s = 0; s < 3; ++s) {
-            const int64_t idx = cur[s] + threadIdx.x;
+            const int32_t idx = cur[s] + (int32_t)threadIdx.x;
             id[s] = idx < end[s] ? ids[s][idx] : NONE;
             if (s && idx < end[s]) rc[s - 1] = (s == 1 ? P.s_rect : P.g_rect)[idx];
         }
@@ -969,13 +970,13 @@ __global__ void __launch_bounds__(kCT, SFB_COMP_MINB) k_composite(CompParams P) 
             if (k) {
 #pragma unroll
                 for (int s = 0; s < 3; ++s) {
-                    const int64_t idx = cur[s] + k * kCT + threadIdx.x;
+                    const int32_t idx = cur[s] + k * kCT + (int32_t)threadIdx.x;
                     id[s] = idx < end[s] ? ids[s][idx] : NONE;
                 }
 #pragma unroll
                 for (int s = 1; s < 3; ++s)
                     if (id[s] < w1) {   // rects stored in list order: no dependent load
-                        const int64_t idx = cur[s] + k * kCT + threadIdx.x;
+                        const int32_t idx = cur[s] + k * kCT + (int32_t)threadIdx.x;
                         rc[s - 1] = (s == 1 ? P.s_rect : P.g_rect)[idx];
                     }
             }
@@ -995,7 +996,7 @@ __global__ void __launch_bounds__(kCT, SFB_COMP_MINB) k_composite(CompParams P) 
         }
         __syncthreads();
 #pragma unroll
-        for (int s = 0; s < 3; ++s) cur[s] += s_add[s];
+        for (int s = 0; s < 3; ++s) cur[s] += (int32_t)s_add[s];
         // ordered compaction of the bitmap by warp 0 (2 words per lane)
         if (threadIdx.x < 32) {
             const int lane = threadIdx.x;
