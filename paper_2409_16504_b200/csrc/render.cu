@@ -906,11 +906,12 @@ __global__ void __launch_bounds__(kCT, SFB_COMP_MINB) k_composite(CompParams P) 
 
     const int64_t t = blockIdx.x;
     const uint32_t ntx32 = (uint32_t)P.ntx;   // 32-bit division: the grid is < 2^31 tiles
-    const int64_t tx = blockIdx.x % ntx32, ty = blockIdx.x / ntx32;
-    const int64_t st = (ty / kSuper) * P.nsx + tx / kSuper;
+    const int32_t tx = (int32_t)(blockIdx.x % ntx32), ty = (int32_t)(blockIdx.x / ntx32);
+    const int32_t st = (ty / kSuper) * (int32_t)P.nsx + tx / kSuper;
     const int TS = P.tile;
-    const int64_t x_lo = tx * TS, y_lo = ty * TS;
-    const int64_t x_end = min(x_lo + TS, P.W), y_end = min(y_lo + TS, P.H);
+    // pixel coordinates fit 32 bits (images are < 2^31 pixels wide and high)
+    const int32_t x_lo = tx * TS, y_lo = ty * TS;
+    const int32_t x_end = (int32_t)min((int64_t)x_lo + TS, P.W), y_end = (int32_t)min((int64_t)y_lo + TS, P.H);
     constexpr bool want_rgb = MASK & SFB_PLANE_RGB, want_n = MASK & SFB_PLANE_NORMAL;
     constexpr bool want_d = MASK & SFB_PLANE_DEPTH;
     const bool term = P.terminate;
