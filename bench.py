@@ -300,7 +300,8 @@ def run_ours(args):
         # host inputs: the uploads of frames i+1 and i+2 are enqueued
         # (pipeline.stage) before frame i waits for its bbox, so the copy
         # engine has ~2 frames of work queued and host hiccups do not idle it
-        ahead = 2
+        # (frames i and i+ahead must not share a lane: a lane has two staging buffers)
+        ahead = 2 if lanes >= 3 else 1
         staged = [stage(cloud_list[j % copies], j % lanes) for j in range(min(ahead, n_frames))] \
             if host_in else []
         for i in range(n_frames):
