@@ -69,8 +69,11 @@ def stage(cloud, lane: int = 0) -> StagedCloud:
         up = _upload_streams[dev] = torch.cuda.Stream(device=dev)
         _bbox_streams[dev] = torch.cuda.Stream(device=dev)
     bb = _bbox_streams[dev]
-    st = _staging.setdefault((dev, lane), {"k": 0, "bufs": [[None] * 5, [None] * 5]})
+    st = _staging.setdefault((dev, lane), {"k": 0, "bufs": [[None] * 6, [None] * 6]})
     slot = st["bufs"][st["k"]]
+    if slot[5]:   # staged but not yet rendered: its data would be overwritten
+        raise RuntimeError(f"both staging buffers of lane {lane} hold unrendered clouds: render "
+                           "a staged cloud of this lane (or stage on another lane) first")
     st["k"] ^= 1
     ply = isinstance(cloud, PlyBody)
     n = len(cloud) if ply else int(cloud.positions.shape[0])
@@ -114,6 +117,7 @@ def stage(cloud, lane: int = 0) -> StagedCloud:
     with torch.cuda.stream(bb):
         bctx.call("sfb_bbox_async", _lib.ptr(pos), n, _lib.ptr(slot[4]))
         bbox_ev = bb.record_event()
+    slot[5] = True   # pending until a frame consumes it (prepare_cloud)
     return StagedCloud(pos, col, n, slot, bbox_ev, done_ev, slot[4])
 
 
@@ -128,6 +132,7 @@ def prepare_cloud(cloud, lane: int = 0):
         n = int(pos.shape[0])
         return pos, col, n, lattice_scale(n, lo_hi), lo_hi, None
     sc = cloud if isinstance(cloud, StagedCloud) else stage(cloud, lane)
+    sc.slot[5] = False   # consumed: the caller records the frame's done event next
     sc.bbox_ev.synchronize()   # the 48-byte read-back only
     lo_hi = _decode_words(sc.words.numpy().view(np.uint64))
     torch.cuda.current_stream().wait_event(sc.done_ev)

@@ -219,3 +219,22 @@ def test_staged_pipeline_matches_device(setup):
         ref = render_frame(dev, w, cams[i % len(cams)])
         for a, b in zip(planes, (ref.rgb, ref.normal, ref.transmittance)):
             assert torch.equal(a, b.cpu()), i
+
+
+def test_staging_refuses_to_overwrite_unrendered(setup):
+    """A lane has two staging buffers: a third stage() before either staged
+    cloud is rendered raises instead of overwriting data a frame will read."""
+    from paper_2409_16504_b200.pipeline import stage
+    pc, cloud, view, w = setup
+    host = PointCloud(torch.from_numpy(cloud.positions).pin_memory(),
+                      torch.from_numpy(cloud.colors).pin_memory(), validate=False)
+    a, b = stage(host, 5), stage(host, 5)
+    with pytest.raises(RuntimeError, match="staging buffers"):
+        stage(host, 5)
+    cam = Camera.of(view)
+    ra = render_frame(a, w, cam, lane=5).rgb.clone()
+    rb = render_frame(b, w, cam, lane=5).rgb.clone()
+    c = stage(host, 5)   # a buffer is free again
+    rc = render_frame(c, w, cam, lane=5).rgb
+    torch.cuda.synchronize()
+    assert torch.equal(ra, rb) and torch.equal(ra, rc)
