@@ -1,5 +1,5 @@
-"""BASELINE.json configs 3, 4 and 5 as GPU parity cases (config 2 is the bench
-workload, config 1 the golden-pinned case): the fused cloud -> P2ENet ->
+"""BASELINE.json configs 2 (the bench workload), 3, 4 and 5 as GPU parity cases
+(config 1 is the golden-pinned case): the fused cloud -> P2ENet ->
 planes frame against the CPU oracle on tile crops the oracle bins in seconds,
 per-point Gaussian parameters against the oracle, and size-independent
 properties at full size (T in [0, 1], unit normals, run-to-run bitwise
@@ -65,6 +65,29 @@ def check_properties(fb):
     assert bool(torch.isfinite(fb.rgb).all()) and bool(torch.isfinite(fb.normal).all())
     n = fb.normal.double().norm(dim=2)
     assert bool(((n == 0) | ((n - 1).abs() < 1e-5)).all())
+
+
+def test_config2_bench_workload(weights):
+    """The bench workload itself (800,871 points, 1024^2): voxelization bit-exact
+    against the oracle (rows, point -> voxel, CSR, f64 features), per-voxel
+    Gaussian parameters within the north-star bounds, and a tile crop of the
+    bench's first view against the oracle's planes."""
+    from oracle import voxel as OV
+    from paper_2409_16504_b200.voxelgrid import voxelize_adaptive
+    cloud, views = scenes.config2()
+    pc = PointCloud(cloud.positions, cloud.colors)
+    got = voxelize_adaptive(pc)
+    ref = OV.voxelize(cloud.positions, cloud.colors)
+    assert np.array_equal(got.grid.coords.cpu().numpy(), ref["coords"])
+    assert np.array_equal(got.point_to_voxel.cpu().numpy(), ref["point_to_voxel"])
+    assert np.array_equal(got.source_order.cpu().numpy(), ref["source_order"])
+    assert np.array_equal(got.source_offsets.cpu().numpy(), ref["source_offsets"])
+    assert np.array_equal(got.grid.feats.cpu().numpy(), ref["feats"])
+    est = ON.estimate(cloud.positions, cloud.colors, weights.as_oracle_layers(), 3)
+    check_params(estimate_neural(pc, weights), est)
+    fb = render_frame(pc, weights, Camera.of(views[0]), ("rgb", "normal"))
+    check_properties(fb)
+    check_crop(fb, est, views[0], (30, 34), (28, 36))
 
 
 def test_config3_sparse_noisy_views(weights):
