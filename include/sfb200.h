@@ -92,6 +92,17 @@ int sfb_set_graphs(sfb_ctx *ctx, int on);
  * evaluations per tile. NULL disables. */
 int sfb_set_debug_counters(sfb_ctx *ctx, int64_t *dev_counters);
 int sfb_stage_times(sfb_ctx *ctx, int32_t *stage_ids, float *ms, int32_t cap, int32_t *n_out);
+/* Parity export of the fused frame (sfb_frame / sfb_frame_rgba), for tests:
+ * device buffers of `capacity` >= points rows receive the rank -> point order
+ * (source, rasterizer.py:105), the runs of identical geometry (start rank,
+ * point count, tile rect x0 x1 y0 y1 of _raster_kernels.py:123-130; the
+ * first sfb_stats.runs entries), and per UNet level l < levels the level's
+ * coordinates (3 capacity) and tap-major kernel map (27 capacity, rows in
+ * the level's own order; sparsenet.py:201-207). Frames run eagerly while set;
+ * capacity 0 disables. */
+int sfb_set_frame_debug(sfb_ctx *ctx, int64_t capacity, int64_t *source, int32_t *run_start,
+                        int32_t *run_count, int32_t *run_rect, int32_t levels,
+                        int32_t *level_coords, int32_t *level_maps);
 
 /* ---- voxelization (voxelgrid.py:125-168, voxelize_adaptive) ------------- */
 /* bbox of (n,3) device positions -> host lo_hi[6] = (lo xyz, hi xyz). The
@@ -131,6 +142,16 @@ int sfb_pool(sfb_ctx *ctx, const int32_t *coords, const float *feats, int64_t m,
              int32_t stride, int32_t *parent_coords, float *parent_feats,
              int32_t *child_to_parent, int64_t *m_parent_host);
 
+/* pool_2x2x2 on float64 features (the reference API's dtype): same parents
+ * and child->parent map, means summed in child-row order as np.add.at. */
+int sfb_pool_f64(sfb_ctx *ctx, const int32_t *coords, const double *feats, int64_t m, int32_t c,
+                 int32_t stride, int32_t *parent_coords, double *parent_feats,
+                 int32_t *child_to_parent, int64_t *m_parent_host);
+/* SparseVoxelGrid.lookup (voxelgrid.py:88-94): row of each (nq,3) query in
+ * the canonical grid (m,3), -1 where unoccupied; rows (nq,) int64. */
+int sfb_lookup(sfb_ctx *ctx, const int32_t *coords, int64_t m, const int32_t *query, int64_t nq,
+               int64_t *rows);
+
 /* ---- P2ENet (sparsenet.py:187-287, 310-341) ------------------------------ */
 /* Parse a P2EN weight blob (host bytes, sparsenet.py:344-434 layout) and
  * upload the packed per-layer operands; replaces load_weights/NetworkWeights. */
@@ -152,8 +173,8 @@ int sfb_transposed_conv(sfb_ctx *ctx, int layer, const int32_t *parent_coords,
 /* Full UNet + head on a voxelized cloud: raw (m0,14) float32 per voxel. */
 int sfb_unet_forward(sfb_ctx *ctx, const int32_t *coords, const double *feats9, int64_t m0,
                      float *raw_out);
-/* activate_head per row (sparsenet.py:310-341), float64 outputs. */
-int sfb_activate_head(sfb_ctx *ctx, const float *raw, int64_t m, double voxel_scale,
+/* activate_head per row (sparsenet.py:310-341): float64 raw in, float64 out. */
+int sfb_activate_head(sfb_ctx *ctx, const double *raw, int64_t m, double voxel_scale,
                       double *delta, double *sigma, double *quat, double *opacity,
                       double *normal);
 

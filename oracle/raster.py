@@ -43,6 +43,7 @@ def lib():
         _lib.oracle_bin_fill.argtypes = [P, P, P, I, I, I, I, I, I, I, I, P, P]
         _lib.oracle_forward.argtypes = [I, I, I, I, I, I, I, P, P, P, P, P, P, P, P, P, P,
                                         D, ctypes.c_int, P, P]
+        _lib.oracle_forward_stream.argtypes = [I, I, I, I] + [P] * 9 + [D, ctypes.c_int, P, P, P]
         _lib.oracle_backward.argtypes = [I, I, I, I, I, P, P, P, P, P, P, P, P, P, D,
                                          ctypes.c_int, ctypes.c_int, P, P, P, P, P, P]
     return _lib
@@ -142,6 +143,45 @@ def render(splats: dict, cam, mode="rgb", background=(0.0, 0.0, 0.0), tile=16,
                          _p(prep["opac"]), _p(prep["attr"]), float(alpha_max), int(bool(terminate)),
                          _p(out), _p(trans))
     fb = compose(out, trans, mode, background)
+    fb["prep"] = prep
+    return fb
+
+
+def render_stream(splats: dict, cam, modes=("rgb", "normal"), background=(0.0, 0.0, 0.0),
+                  tile=16, alpha_max=ALPHA_MAX, terminate=True) -> dict:
+    """Full-frame tiled render (rasterizer.py:152-166) of one or two attribute
+    modes in one pass, without materialising the CSR: the per-tile entry
+    lists are generated in rank order on the fly (oracle_forward_stream), so
+    the random-init frames of configs 2-5 render in seconds. Planes are
+    identical to ``render`` (pinned against it and the reference goldens in
+    tests/test_oracle.py)."""
+    prep = prepare(splats, cam, modes[0], tile, ty_window=(0, 0))   # sort + radius, no bins
+    src = prep["source"]
+    attrs = []
+    for m in modes:
+        if m == "rgb":
+            attrs.append(_c(np.asarray(splats["colors"], dtype=np.float64)[src]))
+        elif m == "normal":
+            attrs.append(_c(np.asarray(splats["normals"], dtype=np.float64)[src]))
+        else:
+            a = np.zeros((src.size, 3))
+            a[:, 0] = prep["depth"]
+            attrs.append(a)
+    w, h = int(cam.width), int(cam.height)
+    outs = [np.zeros((h, w, 3)) for _ in modes]
+    trans = np.ones((h, w))
+    inv = prep["inv"]
+    lib().oracle_forward_stream(w, h, tile, src.size, _p(prep["sx"]), _p(prep["sy"]),
+                                _p(prep["radius"]), _p(_c(inv[:, 0])), _p(_c(inv[:, 1])),
+                                _p(_c(inv[:, 2])), _p(prep["opac"]), _p(attrs[0]),
+                                _p(attrs[1]) if len(modes) > 1 else None, float(alpha_max),
+                                int(bool(terminate)), _p(outs[0]),
+                                _p(outs[1]) if len(modes) > 1 else None, _p(trans))
+    fb = {}
+    for m, out in zip(modes, outs):
+        fb.update({k: v for k, v in compose(out, trans, m, background).items()
+                   if k in (m, "transmittance")})
+    fb["source"] = src
     fb["prep"] = prep
     return fb
 

@@ -254,3 +254,83 @@ void oracle_backward(int64_t width, int64_t height, int64_t tile, int64_t ntx, i
             }
     }
 }
+
+/* bin_tiles + forward_kernel without materialising the CSR (full frames at
+ * configs 2-5, whose random-init CSR holds ~1e9 entries). Per tile row, the
+ * ranks whose tile range covers the row are collected in rank order — the
+ * order bin_tiles scatters them in (_raster_kernels.py:137-142) — then each
+ * tile of the row blends the ranks whose column range covers it, with
+ * forward_kernel's per-pixel rules (_raster_kernels.py:146-201). With
+ * terminate, a tile stops once every pixel has T < cutoff: forward_kernel
+ * skips each later entry per pixel at that point, so the planes are
+ * identical. attr2 (optional) is blended with the same weights in the same
+ * pass (alpha and T do not depend on the attribute). */
+void oracle_forward_stream(int64_t width, int64_t height, int64_t tile, int64_t k,
+                           const double *sx, const double *sy, const double *radius,
+                           const double *inv_a, const double *inv_b, const double *inv_c,
+                           const double *opac, const double *attr, const double *attr2,
+                           double alpha_max, int terminate, double *out, double *out2,
+                           double *trans) {
+    int64_t ntx = (width + tile - 1) / tile, nty = (height + tile - 1) / tile;
+    double ft = (double)tile;
+    int64_t *rx0 = (int64_t *)malloc(sizeof(int64_t) * (k > 0 ? k : 1));
+    int64_t *rx1 = (int64_t *)malloc(sizeof(int64_t) * (k > 0 ? k : 1));
+    int64_t *ry0 = (int64_t *)malloc(sizeof(int64_t) * (k > 0 ? k : 1));
+    int64_t *ry1 = (int64_t *)malloc(sizeof(int64_t) * (k > 0 ? k : 1));
+    int64_t *row = (int64_t *)malloc(sizeof(int64_t) * (k > 0 ? k : 1));
+#pragma omp parallel for schedule(static)
+    for (int64_t i = 0; i < k; ++i)
+        tile_range(sx[i], sy[i], radius[i], ft, ntx, nty, &rx0[i], &rx1[i], &ry0[i], &ry1[i]);
+    for (int64_t ty = 0; ty < nty; ++ty) {
+        int64_t nrow = 0;
+        for (int64_t i = 0; i < k; ++i)
+            if (ry0[i] <= ty && ty <= ry1[i] && rx0[i] <= rx1[i]) row[nrow++] = i;
+#pragma omp parallel for schedule(dynamic, 1)
+        for (int64_t tx = 0; tx < ntx; ++tx) {
+            int64_t x_end = imin((tx + 1) * tile, width), y_end = imin((ty + 1) * tile, height);
+            int64_t npix = (x_end - tx * tile) * (y_end - ty * tile), nsat = 0;
+            for (int64_t e = 0; e < nrow; ++e) {
+                int64_t s = row[e];
+                if (tx < rx0[s] || tx > rx1[s]) continue;
+                double rad = radius[s] + 1.0, rr = rad * rad;
+                double mx = sx[s], my = sy[s];
+                double ia = inv_a[s], ib = inv_b[s], ic = inv_c[s], op = opac[s];
+                int64_t px0 = imax(tx * tile, (int64_t)ceil(mx - rad));
+                int64_t px1 = imin(x_end - 1, (int64_t)floor(mx + rad));
+                int64_t py0 = imax(ty * tile, (int64_t)ceil(my - rad));
+                int64_t py1 = imin(y_end - 1, (int64_t)floor(my + rad));
+                for (int64_t py = py0; py <= py1; ++py) {
+                    double dy = (double)py - my;
+                    for (int64_t px = px0; px <= px1; ++px) {
+                        int64_t pix = py * width + px;
+                        double tr = trans[pix];
+                        if (terminate && tr < TRANS_CUTOFF) continue;
+                        double dx = (double)px - mx;
+                        if (dx * dx + dy * dy > rr) continue;
+                        double q = ia * dx * dx + 2.0 * ib * dx * dy + ic * dy * dy;
+                        double alpha = op * exp(-0.5 * q);
+                        if (alpha > alpha_max) alpha = alpha_max;
+                        if (alpha < ALPHA_CUTOFF) continue;
+                        double w = tr * alpha;
+                        out[3 * pix] += w * attr[3 * s];
+                        out[3 * pix + 1] += w * attr[3 * s + 1];
+                        out[3 * pix + 2] += w * attr[3 * s + 2];
+                        if (attr2) {
+                            out2[3 * pix] += w * attr2[3 * s];
+                            out2[3 * pix + 1] += w * attr2[3 * s + 1];
+                            out2[3 * pix + 2] += w * attr2[3 * s + 2];
+                        }
+                        trans[pix] = tr * (1.0 - alpha);
+                        if (terminate && trans[pix] < TRANS_CUTOFF) ++nsat;
+                    }
+                }
+                if (terminate && nsat == npix) break;
+            }
+        }
+    }
+    free(rx0);
+    free(rx1);
+    free(ry0);
+    free(ry1);
+    free(row);
+}

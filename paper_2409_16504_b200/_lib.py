@@ -62,12 +62,15 @@ SIGNATURES = {
     "sfb_set_graphs": [P, ctypes.c_int],
     "sfb_set_debug_counters": [P, P],
     "sfb_stage_times": [P, P, P, I32, ctypes.POINTER(I32)],
+    "sfb_set_frame_debug": [P, I64, P, P, P, P, I32, P, P],
     "sfb_bbox": [P, P, I64, P],
     "sfb_bbox_async": [P, P, I64, P],
     "sfb_voxelize": [P, P, P, I64, D, P, P, P, P, P, P, P, ctypes.POINTER(I64)],
     "sfb_kernel_map": [P, P, I64, I32, I32, P],
     "sfb_transposed_map": [P, P, I64, I32, P, I64, P, P],
     "sfb_pool": [P, P, P, I64, I32, I32, P, P, P, ctypes.POINTER(I64)],
+    "sfb_pool_f64": [P, P, P, I64, I32, I32, P, P, P, ctypes.POINTER(I64)],
+    "sfb_lookup": [P, P, I64, P, I64, P],
     "sfb_net_load": [P, P, ctypes.c_size_t],
     "sfb_net_set_mode": [P, ctypes.c_int],
     "sfb_layer_set": [P, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int, P, P],
@@ -141,12 +144,18 @@ class Context:
         self.net_token = None
 
     def call(self, name: str, *args):
+        """Run one entry point on torch's current stream. The context's scratch
+        arena is reused by every call, so the library orders a call issued on
+        a different stream after the previous call's work (an event recorded
+        at the end of each call, waited on when the stream changes); the lock
+        keeps set-stream + call atomic across host threads."""
         import torch
         stream = torch.cuda.current_stream(self.device).cuda_stream
-        self.lib.sfb_set_stream(self.handle, P(stream))
-        rc = getattr(self.lib, name)(self.handle, *args)
+        with self.lock:
+            self.lib.sfb_set_stream(self.handle, P(stream))
+            rc = getattr(self.lib, name)(self.handle, *args)
+            msg = self.lib.sfb_last_error(self.handle).decode(errors="replace") if rc else ""
         if rc != SFB_OK:
-            msg = self.lib.sfb_last_error(self.handle).decode(errors="replace")
             if rc == SFB_ERR_ARG:
                 raise ValueError(msg)
             raise SfbError(f"{name}: {msg} (code {rc})")

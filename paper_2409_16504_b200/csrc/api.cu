@@ -21,15 +21,34 @@ const void *write_params_func();
 
 namespace {
 
+void record_done(sfb_ctx *ctx) {
+    if (cudaEventRecord(ctx->done_event, ctx->stream) == cudaSuccess) {
+        ctx->done_stream = ctx->stream;
+        ctx->done_valid = true;
+    } else {
+        cudaGetLastError();
+    }
+}
+
 template <class F>
 int guard(sfb_ctx *ctx, F &&f) {
     if (!ctx) return SFB_ERR_ARG;
     try {
         SFB_CUDA(cudaSetDevice(ctx->device));
+        // the arena is reset and reused below: order this call after the
+        // previous call's kernels when they went to another stream
+        if (ctx->done_valid && ctx->done_stream != ctx->stream)
+            SFB_CUDA(cudaStreamWaitEvent(ctx->stream, ctx->done_event, 0));
         ctx->arena.reset();
         ctx->n_marks = 0;
         ctx->mark(ST_BEGIN);
-        f();
+        try {
+            f();
+        } catch (...) {
+            record_done(ctx);   // whatever was enqueued before the error
+            throw;
+        }
+        record_done(ctx);
         ctx->last_error.clear();
         return SFB_OK;
     } catch (const Error &e) {
@@ -109,9 +128,6 @@ VoxelSplats neural_voxels(sfb_ctx *ctx, const double *pos, const double *col, in
     o.order = ctx->arena.alloc<int32_t>(n);
     o.offsets = ctx->arena.alloc<int32_t>(n + 1);
     voxelize_run(ctx, pos, col, n, host, P, o, C);
-#ifdef SFB_WHATIF_DUP_VOX   // what-if builds only (tools/abn.sh): the stage's marginal cost
-    voxelize_run(ctx, pos, col, n, host, P, o, C);
-#endif
     ctx->mark(ST_VOXELIZE);
     float *raw = ctx->arena.alloc<float>(14 * n);
     unet_run(ctx, o.coords, o.feats, n, host, P, C, raw);
@@ -220,6 +236,7 @@ int sfb_ctx_create(int device, sfb_ctx **out) {
         cudaMallocHost(&ctx->pinned, 4096) != cudaSuccess ||
         cudaStreamCreateWithFlags(&ctx->capture_stream, cudaStreamNonBlocking) != cudaSuccess ||
         cudaEventCreateWithFlags(&ctx->fork_event, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&ctx->done_event, cudaEventDisableTiming) != cudaSuccess ||
         cudaStreamCreateWithFlags(&ctx->side_stream, cudaStreamNonBlocking) != cudaSuccess) {
         delete ctx;
         return SFB_ERR_CUDA;
@@ -260,6 +277,25 @@ int sfb_set_timing(sfb_ctx *ctx, int on) {
 int sfb_set_debug_counters(sfb_ctx *ctx, int64_t *dev_counters) {
     if (!ctx) return SFB_ERR_ARG;
     ctx->debug_counters = dev_counters;
+    return SFB_OK;
+}
+
+int sfb_set_frame_debug(sfb_ctx *ctx, int64_t capacity, int64_t *source, int32_t *run_start,
+                        int32_t *run_count, int32_t *run_rect, int32_t levels,
+                        int32_t *level_coords, int32_t *level_maps) {
+    if (!ctx || capacity < 0 || levels < 0) return SFB_ERR_ARG;
+    FrameDebug D;
+    if (capacity > 0) {
+        D.cap = capacity;
+        D.source = source;
+        D.run_start = run_start;
+        D.run_count = run_count;
+        D.run_rect = run_rect;
+        D.levels = levels;
+        D.level_coords = level_coords;
+        D.level_maps = level_maps;
+    }
+    ctx->frame_debug = D;
     return SFB_OK;
 }
 
@@ -372,6 +408,32 @@ int sfb_pool(sfb_ctx *ctx, const int32_t *coords, const float *feats, int64_t m,
     });
 }
 
+int sfb_pool_f64(sfb_ctx *ctx, const int32_t *coords, const double *feats, int64_t m, int32_t c,
+                 int32_t stride, int32_t *parent_coords, double *parent_feats, int32_t *c2p,
+                 int64_t *m_parent_host) {
+    return guard(ctx, [&] {
+        FrameParams host{};
+        coords_layout(ctx, coords, m, host);
+        FrameParams *P = params(ctx, host);
+        DevCounts *C = new_counts(ctx);
+        *reinterpret_cast<int64_t *>(ctx->pinned) = m;
+        SFB_CUDA(cudaMemcpyAsync(&C->m[0], ctx->pinned, sizeof(int64_t), cudaMemcpyHostToDevice,
+                                 ctx->stream));
+        pool_build(ctx, coords, &C->m[0], m, stride, host, P, feats, c, c, parent_coords,
+                   parent_feats, c, c2p, &C->m[1]);
+        ctx->read_back(&C->m[1], sizeof(int64_t));
+        *m_parent_host = ctx->pinned[0];
+    });
+}
+
+int sfb_lookup(sfb_ctx *ctx, const int32_t *coords, int64_t m, const int32_t *query, int64_t nq,
+               int64_t *rows) {
+    return guard(ctx, [&] {
+        SFB_REQUIRE((coords || m == 0) && (query || nq == 0) && (rows || nq == 0), "null argument");
+        lookup_run(ctx, coords, m, query, nq, rows);
+    });
+}
+
 int sfb_net_load(sfb_ctx *ctx, const void *blob, size_t nbytes) {
     return guard(ctx, [&] {
         net_load(ctx, blob, nbytes);
@@ -445,7 +507,7 @@ int sfb_unet_forward(sfb_ctx *ctx, const int32_t *coords, const double *feats9, 
     });
 }
 
-int sfb_activate_head(sfb_ctx *ctx, const float *raw, int64_t m, double scale, double *delta,
+int sfb_activate_head(sfb_ctx *ctx, const double *raw, int64_t m, double scale, double *delta,
                       double *sigma, double *quat, double *opacity, double *normal) {
     return guard(ctx, [&] { activate_run(ctx, raw, m, scale, delta, sigma, quat, opacity, normal); });
 }
@@ -591,8 +653,10 @@ static int frame_impl(sfb_ctx *ctx, const double *positions, const double *color
         FrameParams host = camera_params(cam, bg);
         if (rgba) plane_mask = apply_shading(host, shading);
         voxel_layout(lo_hi_host, s, host);
-        const int key_bits = host.total <= 32 ? ((host.total + 7) / 8) * 8 : 64;
-        if (!ctx->use_graphs || ctx->timing) {
+        // the graph bakes in the voxel-key radix pass count (8-bit digits) and the
+        // key width (32 / 64 bit): key on the pass count in both ranges
+        const int key_bits = ((std::max(host.total, 1) + 7) / 8) * 8;
+        if (!ctx->use_graphs || ctx->timing || ctx->frame_debug.cap > 0) {
             FrameParams *P = ctx->arena.alloc<FrameParams>(1);
             enqueue_frame(ctx, positions, colors, n, host, P, cam, opts, plane_mask, rgb, normal,
                           depth, trans, rgba);

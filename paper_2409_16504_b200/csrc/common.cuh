@@ -120,6 +120,17 @@ struct Net {
 };
 
 struct DevCounts;
+
+// Parity export of the fused frame (sfb_set_frame_debug): caller device
+// buffers of `cap` (>= points) rows; frames run eagerly while set
+struct FrameDebug {
+    int64_t cap = 0;
+    int64_t *source = nullptr;                                        // (cap) rank -> point
+    int32_t *run_start = nullptr, *run_count = nullptr, *run_rect = nullptr;   // (cap) (cap) (4 cap)
+    int32_t levels = 0;
+    int32_t *level_coords = nullptr;   // (levels, 3 cap) the UNet's per-level coordinates
+    int32_t *level_maps = nullptr;     // (levels, 27, cap) its tap-major kernel maps
+};
 }  // namespace sfb
 
 struct sfb_frame_graph;
@@ -144,6 +155,7 @@ struct sfb_ctx {
     std::vector<sfb_frame_graph *> graphs;
     int64_t graph_nodes = 0;
     int64_t *debug_counters = nullptr;   // compositor per-tile counters (diagnostics)
+    sfb::FrameDebug frame_debug;         // fused-frame parity export (tests)
     sfb::DevCounts *last_counts = nullptr;   // device counts of the last call
     // launch-size hints (host copies of the counts of the last eager frame):
     // every kernel loops over its device count, so hints only size grids
@@ -154,6 +166,11 @@ struct sfb_ctx {
         return g < bound ? g : bound;
     }
     int num_sms = 148;
+    // end of the previous call's work (its scratch arena lives on): a call on
+    // another stream waits for it first (api.cu guard)
+    cudaEvent_t done_event = nullptr;
+    cudaStream_t done_stream = nullptr;
+    bool done_valid = false;
     std::string last_error;
     sfb_stats stats{};
     // pinned host staging for small D2H reads (sizes, bbox)
@@ -182,6 +199,7 @@ struct sfb_ctx {
         for (auto &e : side_ev)
             if (e) cudaEventDestroy(e);
         if (fork_event) cudaEventDestroy(fork_event);
+        if (done_event) cudaEventDestroy(done_event);
     }
     // read `count` int64 values back from device (one sync)
     void read_back(const void *dev, size_t bytes) {
@@ -280,6 +298,10 @@ template <class K>
 int dsort_pairs(sfb_ctx *ctx, K *k0, uint32_t *v0, K *k1, uint32_t *v1, const int64_t *d_n,
                 int64_t n_fixed, int bits);
 void write_params(sfb_ctx *ctx, const FrameParams &host, FrameParams *dev);
+// cudaFuncAttributeMaxDynamicSharedMemorySize for `func` on the current
+// device, set once per (device, kernel) under a lock (kernel attributes are
+// per device; several host threads may launch the first frame concurrently)
+void set_max_dyn_smem(const void *func, int bytes);
 
 // ---- cross-file launchers (defined in the .cu files) ----------------------
 
@@ -303,6 +325,12 @@ void pool_build(sfb_ctx *ctx, const int32_t *coords, const int64_t *d_m, int64_t
                 int stride, const FrameParams &host, const FrameParams *P, const float *feats,
                 int c, int ld_in, int32_t *parent_coords, float *parent_feats, int ld_out,
                 int32_t *child_to_parent, int64_t *d_mp);
+void pool_build(sfb_ctx *ctx, const int32_t *coords, const int64_t *d_m, int64_t m_bound,
+                int stride, const FrameParams &host, const FrameParams *P, const double *feats,
+                int c, int ld_in, int32_t *parent_coords, double *parent_feats, int ld_out,
+                int32_t *child_to_parent, int64_t *d_mp);
+void lookup_run(sfb_ctx *ctx, const int32_t *coords, int64_t m, const int32_t *query, int64_t nq,
+                int64_t *rows);
 void coords_layout(sfb_ctx *ctx, const int32_t *coords, int64_t m, FrameParams &P);
 // children of a level grouped by their tap under the parent, each bucket
 // padded to whole 128-row tiles (the tap-bucketed transposed conv)
@@ -351,7 +379,7 @@ void net_load(sfb_ctx *ctx, const void *blob, size_t n);
 // per-voxel raw head (M0 x 14) float32 into `raw`; M0 = C->m[0] (device), bound m_bound
 void unet_run(sfb_ctx *ctx, const int32_t *coords, const double *feats9, int64_t m_bound,
               const FrameParams &host, const FrameParams *P, DevCounts *C, float *raw);
-void activate_run(sfb_ctx *ctx, const float *raw, int64_t m, double scale, double *delta,
+void activate_run(sfb_ctx *ctx, const double *raw, int64_t m, double scale, double *delta,
                   double *sigma, double *quat, double *opac, double *normal);
 void conv_layer(sfb_ctx *ctx, const NetLayer &L, const float *in, int ld_in, const int32_t *nbr,
                 int64_t nbr_ld, const int64_t *d_m, int64_t m_bound, int relu, float *out,

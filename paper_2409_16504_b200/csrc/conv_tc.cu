@@ -160,10 +160,7 @@ struct TcShape {
     // one stage: measured on config 2, a second stage buys no overlap the
     // co-resident CTAs of other items do not already give, and halving the
     // shared memory raises residency (0.379 vs 0.403 ms/frame with 8 lanes)
-#ifndef SFB_TC_MAX_STAGES
-#define SFB_TC_MAX_STAGES 1
-#endif
-    static constexpr int STAGES = (STAGE_FLOATS * 4 * 2 <= 200 * 1024) ? SFB_TC_MAX_STAGES : 1;
+    static constexpr int STAGES = 1;
     // single stage with small weight tiles: the weights alone get a second
     // buffer, so batch k+1's tiles (TMA) are in flight while batch k is staged
     // and multiplied
@@ -561,12 +558,7 @@ void launch_tc(sfb_ctx *ctx, const NetLayer &L, const float *in, int ld_in, cons
                int ld_out, int64_t m_grid, const int32_t *row_map, const int32_t *tap_off,
                int csplit_req) {
     using S = TcShape<KP, NP, BF>;
-    static bool attr = false;
-    if (!attr) {
-        SFB_CUDA(cudaFuncSetAttribute(k_conv_tc<KP, NP, BF>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      S::smem_bytes(32)));
-        attr = true;
-    }
+    set_max_dyn_smem(reinterpret_cast<const void *>(k_conv_tc<KP, NP, BF>), S::smem_bytes(32));
     const int64_t tiles_bound = (m_grid + kM - 1) / kM;
     // Split-K. csplit_req > 1: the splits of a tile form a thread-block
     // cluster (size fixed by the caller from the layer's place in the

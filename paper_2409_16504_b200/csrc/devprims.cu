@@ -5,6 +5,9 @@
 // as one CUDA graph (the P2ENet level sizes, kept splats, runs and tile
 // entries are all data-dependent).
 #include <algorithm>
+#include <mutex>
+#include <set>
+#include <tuple>
 
 #include "common.cuh"
 #include "scan.cuh"
@@ -13,9 +16,7 @@ namespace sfb {
 
 constexpr int kScanBlocks = 148;
 constexpr int kScanThreads = 1024;
-#ifndef SFB_SCAN_GRID
-#define SFB_SCAN_GRID (2 * 148)
-#endif
+constexpr int kScanGrid = 2 * 148;
 
 // ------------------------------------------------------------------ scan
 __device__ __forceinline__ int64_t chunk_of(int64_t n, int blocks) {
@@ -256,7 +257,7 @@ void dscan3(sfb_ctx *ctx, const int32_t *in0, const int32_t *in1, const int32_t 
     auto *status = static_cast<unsigned long long *>(ctx->arena.alloc_bytes(bytes));
     SFB_CUDA(cudaMemsetAsync(status, 0, bytes, ctx->stream));
     Scan3 S{{in0, in1, in2}, {out0, out1, out2}, {tot0, tot1, tot2}};
-    const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(tiles, SFB_SCAN_GRID));
+    const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(tiles, kScanGrid));
     k_scan3_lb<<<grid, kScanThreads, 0, ctx->stream>>>(S, d_n, n_fixed, status, tiles,
                                                        reinterpret_cast<unsigned int *>(status + 3 * tiles));
     SFB_CHECK_LAUNCH();
@@ -271,7 +272,7 @@ void dscan(sfb_ctx *ctx, const int32_t *in, int32_t *out, const int64_t *d_n, in
     auto *status = static_cast<unsigned long long *>(ctx->arena.alloc_bytes(bytes));
     SFB_CUDA(cudaMemsetAsync(status, 0, bytes, ctx->stream));
     auto *ticket = reinterpret_cast<unsigned int *>(status + tiles);
-    const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(tiles, SFB_SCAN_GRID));
+    const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(tiles, kScanGrid));
     k_scan_lb<<<grid, kScanThreads, 0, ctx->stream>>>(in, out, d_n, n_fixed, total_out,
                                                       inclusive ? 1 : 0, status, ticket);
     SFB_CHECK_LAUNCH();
@@ -283,6 +284,17 @@ __global__ void k_write_params(FrameParams p, FrameParams *dst) { *dst = p; }
 void write_params(sfb_ctx *ctx, const FrameParams &host, FrameParams *dev) {
     k_write_params<<<1, 1, 0, ctx->stream>>>(host, dev);
     SFB_CHECK_LAUNCH();
+}
+
+void set_max_dyn_smem(const void *func, int bytes) {
+    static std::mutex mu;
+    static std::set<std::tuple<int, const void *, int>> done;
+    int dev = 0;
+    SFB_CUDA(cudaGetDevice(&dev));
+    std::lock_guard<std::mutex> lock(mu);
+    if (done.count({dev, func, bytes})) return;
+    SFB_CUDA(cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+    done.insert({dev, func, bytes});
 }
 
 const void *write_params_func() { return reinterpret_cast<const void *>(&k_write_params); }
@@ -307,11 +319,9 @@ constexpr int kRsWarps = kRsThreads / 32;
 
 // blocks that take part in a pass: at least one 256-item sub-tile each, at
 // most kRsBlocks (small sorts spread thin: one sub-tile per block)
-#ifndef SFB_RS_MIN_ITEMS
-#define SFB_RS_MIN_ITEMS 256
-#endif
+constexpr int kRsMinItems = 256;
 __device__ __forceinline__ int rs_blocks(int64_t n) {
-    int64_t b = (n + SFB_RS_MIN_ITEMS - 1) / SFB_RS_MIN_ITEMS;
+    int64_t b = (n + kRsMinItems - 1) / kRsMinItems;
     return (int)max((int64_t)1, min(b, (int64_t)kRsBlocks));
 }
 

@@ -21,10 +21,7 @@ static constexpr unsigned long long kEmpty = ~0ull;
 // kernel-map lookups are misses, and a linear-probing miss costs
 // (1 + 1/(1-a)^2)/2 probes at load a (A/B on config 2: 4x gives 0.286 vs
 // 0.290 ms/frame and 0.779 vs 0.787 ms latency against 2x)
-#ifndef SFB_HASH_SPREAD
-#define SFB_HASH_SPREAD 4
-#endif
-static constexpr int kHashSpread = SFB_HASH_SPREAD;
+static constexpr int kHashSpread = 4;
 
 __device__ __forceinline__ uint32_t hash64(unsigned long long k) {
     k ^= k >> 33;
@@ -216,26 +213,29 @@ __global__ void k_pool_segments(const K *__restrict__ keys, const uint32_t *__re
     }
 }
 
-// thread per (parent, channel): ordered float32 mean of its children
-__global__ void k_pool_means(const float *__restrict__ feats, int ld_in, int c,
+// thread per (parent, channel): ordered mean of its children in child-row
+// order (np.add.at, voxelgrid.py:181-183), float32 in the network, float64
+// through the pool_2x2x2 API
+template <class T>
+__global__ void k_pool_means(const T *__restrict__ feats, int ld_in, int c,
                              const uint32_t *__restrict__ child_rows,
                              const int32_t *__restrict__ seg_start, const int64_t *__restrict__ d_mp,
-                             float *__restrict__ out, int ld_out) {
+                             T *__restrict__ out, int ld_out) {
     const int64_t mp = *d_mp;
     SFB_FOR(idx, mp * c) {
         const int64_t v = idx / c;
         const int ch = (int)(idx % c);
         const int32_t b = seg_start[v], e = seg_start[v + 1];
-        float acc = 0.f;
-        for (int32_t j = b; j < e; ++j) acc = __fadd_rn(acc, feats[(int64_t)child_rows[j] * ld_in + ch]);
-        out[v * ld_out + ch] = __fdiv_rn(acc, (float)(e - b));
+        T acc = T(0);
+        for (int32_t j = b; j < e; ++j) acc = acc + feats[(int64_t)child_rows[j] * ld_in + ch];
+        out[v * ld_out + ch] = acc / (T)(e - b);
     }
 }
 
-template <class K>
+template <class K, class T>
 static void pool_typed(sfb_ctx *ctx, const int32_t *coords, const int64_t *d_m, int64_t m_bound,
-                       int stride, const FrameParams *P, int key_bits, const float *feats, int c,
-                       int ld_in, int32_t *parent_coords, float *parent_feats, int ld_out,
+                       int stride, const FrameParams *P, int key_bits, const T *feats, int c,
+                       int ld_in, int32_t *parent_coords, T *parent_feats, int ld_out,
                        int32_t *child_to_parent, int64_t *d_mp) {
     cudaStream_t st = ctx->stream;
     const int64_t S = 2 * (int64_t)stride;
@@ -255,23 +255,62 @@ static void pool_typed(sfb_ctx *ctx, const int32_t *coords, const int64_t *d_m, 
                                           child_to_parent, d_mp);
     SFB_CHECK_LAUNCH();
     if (feats && c > 0) {
-        k_pool_means<<<dgrid(m_bound * c, 256), 256, 0, st>>>(feats, ld_in, c, vs, seg, d_mp,
-                                                               parent_feats, ld_out);
+        k_pool_means<T><<<dgrid(m_bound * c, 256), 256, 0, st>>>(feats, ld_in, c, vs, seg, d_mp,
+                                                                  parent_feats, ld_out);
         SFB_CHECK_LAUNCH();
     }
+}
+
+template <class T>
+static void pool_build_t(sfb_ctx *ctx, const int32_t *coords, const int64_t *d_m, int64_t m_bound,
+                         int stride, const FrameParams &host, const FrameParams *P, const T *feats,
+                         int c, int ld_in, int32_t *parent_coords, T *parent_feats, int ld_out,
+                         int32_t *child_to_parent, int64_t *d_mp) {
+    const int bits = host.total > 0 ? host.total : 1;
+    if (host.total <= 32)
+        pool_typed<uint32_t, T>(ctx, coords, d_m, m_bound, stride, P, bits, feats, c, ld_in,
+                                parent_coords, parent_feats, ld_out, child_to_parent, d_mp);
+    else
+        pool_typed<unsigned long long, T>(ctx, coords, d_m, m_bound, stride, P, bits, feats, c, ld_in,
+                                          parent_coords, parent_feats, ld_out, child_to_parent, d_mp);
 }
 
 void pool_build(sfb_ctx *ctx, const int32_t *coords, const int64_t *d_m, int64_t m_bound,
                 int stride, const FrameParams &host, const FrameParams *P, const float *feats,
                 int c, int ld_in, int32_t *parent_coords, float *parent_feats, int ld_out,
                 int32_t *child_to_parent, int64_t *d_mp) {
-    const int bits = host.total > 0 ? host.total : 1;
-    if (host.total <= 32)
-        pool_typed<uint32_t>(ctx, coords, d_m, m_bound, stride, P, bits, feats, c, ld_in,
-                             parent_coords, parent_feats, ld_out, child_to_parent, d_mp);
-    else
-        pool_typed<unsigned long long>(ctx, coords, d_m, m_bound, stride, P, bits, feats, c, ld_in,
-                                       parent_coords, parent_feats, ld_out, child_to_parent, d_mp);
+    pool_build_t<float>(ctx, coords, d_m, m_bound, stride, host, P, feats, c, ld_in, parent_coords,
+                        parent_feats, ld_out, child_to_parent, d_mp);
+}
+
+void pool_build(sfb_ctx *ctx, const int32_t *coords, const int64_t *d_m, int64_t m_bound,
+                int stride, const FrameParams &host, const FrameParams *P, const double *feats,
+                int c, int ld_in, int32_t *parent_coords, double *parent_feats, int ld_out,
+                int32_t *child_to_parent, int64_t *d_mp) {
+    pool_build_t<double>(ctx, coords, d_m, m_bound, stride, host, P, feats, c, ld_in, parent_coords,
+                         parent_feats, ld_out, child_to_parent, d_mp);
+}
+
+// ---------------------------------------------------------------- lookup
+// SparseVoxelGrid.lookup (voxelgrid.py:88-94): row of each query coordinate
+// in the grid's canonical order, -1 where unoccupied (hash probe instead of
+// searchsorted; identical result since rows are unique)
+__global__ void k_lookup(const int32_t *__restrict__ q, int64_t nq, HashTable h,
+                         int64_t *__restrict__ rows) {
+    const uint32_t mask = *h.mask;
+    SFB_FOR(i, nq) rows[i] = hash_find(h, mask, q[3 * i], q[3 * i + 1], q[3 * i + 2]);
+}
+
+void lookup_run(sfb_ctx *ctx, const int32_t *coords, int64_t m, const int32_t *query, int64_t nq,
+                int64_t *rows) {
+    if (nq == 0) return;
+    if (m == 0) {
+        SFB_CUDA(cudaMemsetAsync(rows, 0xff, sizeof(int64_t) * nq, ctx->stream));
+        return;
+    }
+    HashTable h = hash_build(ctx, coords, nullptr, m);
+    k_lookup<<<dgrid(nq, 256), 256, 0, ctx->stream>>>(query, nq, h, rows);
+    SFB_CHECK_LAUNCH();
 }
 
 // ---------------------------------------------------------------- fast pooling

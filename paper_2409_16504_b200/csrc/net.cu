@@ -153,6 +153,10 @@ void layer_set(sfb_ctx *ctx, int kind, int kernel, int cin, int cout, const floa
 constexpr int kRows = 32;
 constexpr int kThreads = 256;
 constexpr int kMaxOut = 16;  // kRows * cout / kThreads for cout <= 128
+// transposed convs are tap-bucketed (one weight tap per 128-row tile) from 16
+// tiles up (A/B on config 2, 8 frames in flight: 0.316 vs 0.336 ms/frame for a
+// 64-tile threshold, same latency); tinier levels split the taps over a cluster
+constexpr int64_t kTconvBucketRows = 16 * 128;
 
 __global__ void __launch_bounds__(kThreads)
 k_conv_simt(const float *__restrict__ in, int ld_in, const int32_t *__restrict__ nbr, int64_t nbr_ld,
@@ -283,12 +287,7 @@ static void launch_narrow(sfb_ctx *ctx, const NetLayer &L, const float *in, int 
                           int64_t nbr_ld, const int64_t *d_m, int64_t m_bound, int relu, float *out,
                           int ld_out, int64_t m_grid) {
     constexpr size_t smem = sizeof(float) * TAPS * CIN * COUT;
-    static bool attr = false;
-    if (!attr) {
-        SFB_CUDA(cudaFuncSetAttribute(k_conv_narrow<CIN, COUT, TAPS, PARTS>,
-                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        attr = true;
-    }
+    set_max_dyn_smem(reinterpret_cast<const void *>(k_conv_narrow<CIN, COUT, TAPS, PARTS>), (int)smem);
     k_conv_narrow<CIN, COUT, TAPS, PARTS><<<dgrid(m_grid * PARTS, 128, 8), 128, smem, ctx->stream>>>(
         in, ld_in, nbr, nbr_ld, d_m, m_bound, L.w, L.b, relu, out, ld_out);
     SFB_CHECK_LAUNCH();
@@ -298,23 +297,11 @@ void conv_layer(sfb_ctx *ctx, const NetLayer &L, const float *in, int ld_in, con
                 int64_t nbr_ld, const int64_t *d_m, int64_t m_bound, int relu, float *out,
                 int ld_out, int64_t m_grid, int csplit) {
     if (m_bound == 0) return;
-#ifdef SFB_WHATIF_NO_CONV   // A/B builds only (tools/ab_*): measure the convs' share
-    return;
-#endif
     if (m_grid < 0) m_grid = m_bound;
-#ifndef SFB_L0_TC
     if (ctx->net_mode != SFB_NET_TC_BF16 && L.cin == 9 && L.cout == 16 && L.taps == 27) {
         launch_narrow<9, 16, 27, 1>(ctx, L, in, ld_in, nbr, nbr_ld, d_m, m_bound, relu, out, ld_out, m_grid);
         return;
     }
-#endif
-#ifdef SFB_L1_NARROW   // A/B builds only: slower for 16 -> 32 (0.304-0.309 vs 0.297 ms/frame)
-    if (ctx->net_mode != SFB_NET_TC_BF16 && L.cin == 16 && L.cout == 32 && L.taps == 27) {
-        launch_narrow<16, 32, 27, SFB_L1_NARROW>(ctx, L, in, ld_in, nbr, nbr_ld, d_m, m_bound, relu, out,
-                                                 ld_out, m_grid);
-        return;
-    }
-#endif
     if (ctx->net_mode != SFB_NET_SIMT_F32 && L.w_tc) {
         conv_layer_tc(ctx, L, in, ld_in, nbr, nbr_ld, d_m, m_bound, relu, out, ld_out, m_grid,
                       nullptr, nullptr, csplit);
@@ -323,12 +310,7 @@ void conv_layer(sfb_ctx *ctx, const NetLayer &L, const float *in, int ld_in, con
     SFB_REQUIRE(kRows * L.cout <= kMaxOut * kThreads, "conv: cout > 128 unsupported");
     size_t smem = sizeof(float) * ((size_t)kRows * L.cin + (size_t)L.cin * L.cout);
     SFB_REQUIRE(smem <= 200 * 1024, "conv: channels too wide for one CTA");
-    static bool attr = false;
-    if (!attr) {
-        SFB_CUDA(cudaFuncSetAttribute(k_conv_simt, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      200 * 1024));
-        attr = true;
-    }
+    set_max_dyn_smem(reinterpret_cast<const void *>(k_conv_simt), 200 * 1024);
     k_conv_simt<<<dgrid(m_grid, kRows, 4), kThreads, smem, ctx->stream>>>(
         in, ld_in, nbr, nbr_ld, d_m, m_bound, L.taps, L.cin, L.cout, L.w, L.b, relu, out, ld_out);
     SFB_CHECK_LAUNCH();
@@ -383,10 +365,7 @@ void tconv_layer(sfb_ctx *ctx, const NetLayer &L, const float *in, int ld_in,
         // only tiny levels split the 8 taps over a cluster instead (A/B on
         // config 2 with 8 frames in flight: 0.316 vs 0.336 ms/frame for a
         // 64-tile threshold, same latency)
-#ifndef SFB_TCONV_BUCKET_ROWS
-#define SFB_TCONV_BUCKET_ROWS (16 * 128)
-#endif
-        if (tb && m_grid >= SFB_TCONV_BUCKET_ROWS) {
+        if (tb && m_grid >= kTconvBucketRows) {
             conv_layer_tc(ctx, L, in, ld_in, tb->src, 0, tb->d_rows, tb->rows_bound, relu, out,
                           ld_out, tb->rows_grid, tb->perm, tb->off);
             return;
@@ -511,7 +490,8 @@ __device__ __forceinline__ double logaddexp0(double x) {
     return tmp;  // NaN
 }
 
-__device__ __forceinline__ void activate_row(const float *r, double scale, double *delta,
+template <class R>
+__device__ __forceinline__ void activate_row(const R *r, double scale, double *delta,
                                              double *sigma, double *q, double *opac,
                                              double *normal) {
     double x[14];
@@ -547,7 +527,7 @@ __device__ __forceinline__ void activate_row(const float *r, double scale, doubl
     }
 }
 
-__global__ void k_activate(const float *__restrict__ raw, int64_t m, double scale, double *delta,
+__global__ void k_activate(const double *__restrict__ raw, int64_t m, double scale, double *delta,
                            double *sigma, double *quat, double *opac, double *normal) {
     int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (i >= m) return;
@@ -555,7 +535,7 @@ __global__ void k_activate(const float *__restrict__ raw, int64_t m, double scal
                  normal + 3 * i);
 }
 
-void activate_run(sfb_ctx *ctx, const float *raw, int64_t m, double scale, double *delta,
+void activate_run(sfb_ctx *ctx, const double *raw, int64_t m, double scale, double *delta,
                   double *sigma, double *quat, double *opac, double *normal) {
     SFB_REQUIRE(scale > 0, "voxel_scale must be positive");
     if (m == 0) return;
@@ -611,42 +591,8 @@ __global__ void k_feats_to_f32(const double *__restrict__ f, const int64_t *__re
 // frames in flight: {1, 1, 4, 8} gives 0.337 ms/frame vs 0.364 for {2, 4, 8,
 // device} at the same single-frame latency — with concurrent frames the extra
 // CTAs and the partial-sum reduction cost more than the parallelism they buy.
-#ifndef SFB_L0_SPLIT
-#define SFB_L0_SPLIT 1
-#endif
-#ifndef SFB_L1_SPLIT
-#define SFB_L1_SPLIT 1
-#endif
-#ifndef SFB_L2_SPLIT
-#define SFB_L2_SPLIT 4
-#endif
-#ifndef SFB_L3_SPLIT
-#define SFB_L3_SPLIT 8
-#endif
-constexpr int kLevelSplit[4] = {SFB_L0_SPLIT, SFB_L1_SPLIT, SFB_L2_SPLIT, SFB_L3_SPLIT};
-
-// What-if builds only (tools/abn.sh): run a part twice to measure its marginal
-// cost in the concurrent-lane throughput (results unchanged: each part is a
-// pure function of buffers it does not write)
-#ifdef SFB_WHATIF_DUP_CONV
-#define SFB_DUP_CONV(x) x; x
-#else
-#define SFB_DUP_CONV(x) x
-#endif
-#ifdef SFB_WHATIF_DUP_STRUCT
-#define SFB_DUP_STRUCT(x) x; x
-#else
-#define SFB_DUP_STRUCT(x) x
-#endif
-#ifdef SFB_WHATIF_DUP_POOL
-#define SFB_DUP_POOL(x) x; x
-#else
-#define SFB_DUP_POOL(x) x
-#endif
-
-#ifndef SFB_TCONV_SPLIT
-#define SFB_TCONV_SPLIT 8
-#endif
+constexpr int kLevelSplit[4] = {1, 1, 4, 8};
+constexpr int kTconvSplit = 8;
 
 void unet_run(sfb_ctx *ctx, const int32_t *coords0, const double *feats9, int64_t mb,
               const FrameParams &host, const FrameParams *P, DevCounts *C, float *raw) {
@@ -675,8 +621,8 @@ void unet_run(sfb_ctx *ctx, const int32_t *coords0, const double *feats9, int64_
     // level 0: hash + kernel map on the critical path
     HashTable h0;
     nbr[0] = ctx->arena.alloc<int32_t>((size_t)kern[0] * kern[0] * kern[0] * mb);
-    SFB_DUP_STRUCT(h0 = hash_build(ctx, coords[0], &C->m[0], mb, mg[0]);
-                   kernel_map_build(ctx, h0, coords[0], &C->m[0], mb, 1, kern[0], nbr[0], mg[0]));
+    h0 = hash_build(ctx, coords[0], &C->m[0], mb, mg[0]);
+    kernel_map_build(ctx, h0, coords[0], &C->m[0], mb, 1, kern[0], nbr[0], mg[0]);
     // side branch: the coordinate structure of every coarser level (parents,
     // children, taps, hash = the pooling table, kernel map) depends only on
     // coordinates, so it runs concurrently with the convolutions; event l
@@ -689,10 +635,9 @@ void unet_run(sfb_ctx *ctx, const int32_t *coords0, const double *feats9, int64_
             int32_t *pc = ctx->arena.alloc<int32_t>((size_t)mb * 3);
             const int k = kern[l + 1];
             nbr[l + 1] = ctx->arena.alloc<int32_t>((size_t)k * k * k * mb);
-            SFB_DUP_STRUCT(ps[l] = pool_structure(ctx, coords[l], &C->m[l], mb, mg[l], 1 << l, pc,
-                                                  &C->m[l + 1]);
-                           kernel_map_build(ctx, ps[l].table, pc, &C->m[l + 1], mb, 2 << l, k,
-                                            nbr[l + 1], mg[l + 1]));
+            ps[l] = pool_structure(ctx, coords[l], &C->m[l], mb, mg[l], 1 << l, pc, &C->m[l + 1]);
+            kernel_map_build(ctx, ps[l].table, pc, &C->m[l + 1], mb, 2 << l, k, nbr[l + 1],
+                             mg[l + 1]);
             coords[l + 1] = pc;
             SFB_CUDA(cudaEventRecord(ctx->side_ev[l], ctx->stream));
         }
@@ -708,44 +653,49 @@ void unet_run(sfb_ctx *ctx, const int32_t *coords0, const double *feats9, int64_
     for (int l = 0; l < L; ++l) {
         cat[l] = ctx->arena.alloc<float>((size_t)mb * width[l]);
         const int up = dec[L - 1 - l];
-        SFB_DUP_CONV(conv_layer(ctx, net.layers[layer], pin[l], enc[l], nbr[l], mb, &C->m[l], mb, 1,
-                                cat[l] + up, width[l], mg[l], kLevelSplit[std::min(l, 3)]));
+        conv_layer(ctx, net.layers[layer], pin[l], enc[l], nbr[l], mb, &C->m[l], mb, 1, cat[l] + up,
+                   width[l], mg[l], kLevelSplit[std::min(l, 3)]);
         ++layer;
         pin[l + 1] = ctx->arena.alloc<float>((size_t)mb * enc[l + 1]);
         SFB_CUDA(cudaStreamWaitEvent(st, ctx->side_ev[l], 0));   // level l+1 structure ready
-        SFB_DUP_POOL(pool_means(ctx, ps[l], &C->m[l + 1], mg[l + 1], cat[l] + up, enc[l + 1], width[l],
-                                pin[l + 1], enc[l + 1]));
+        pool_means(ctx, ps[l], &C->m[l + 1], mg[l + 1], cat[l] + up, enc[l + 1], width[l],
+                   pin[l + 1], enc[l + 1]);
     }
     float *bott = ctx->arena.alloc<float>((size_t)mb * enc[L + 1]);
-    SFB_DUP_CONV(conv_layer(ctx, net.layers[layer], pin[L], enc[L], nbr[L], mb, &C->m[L], mb, 1, bott,
-                            enc[L + 1], mg[L], kLevelSplit[std::min(L, 3)]));
+    conv_layer(ctx, net.layers[layer], pin[L], enc[L], nbr[L], mb, &C->m[L], mb, 1, bott,
+               enc[L + 1], mg[L], kLevelSplit[std::min(L, 3)]);
     ++layer;
     const float *coarse = bott;
     int ld_coarse = enc[L + 1];
     for (int l = L - 1; l >= 0; --l) {
-        SFB_DUP_CONV(tconv_layer(ctx, net.layers[layer], coarse, ld_coarse, ps[l].c2p, ps[l].tap, &C->m[l],
-                                 mb, 1, cat[l], width[l], mg[l], ps[l].tmap, &ps[l].buckets, SFB_TCONV_SPLIT));
+        tconv_layer(ctx, net.layers[layer], coarse, ld_coarse, ps[l].c2p, ps[l].tap, &C->m[l], mb,
+                    1, cat[l], width[l], mg[l], ps[l].tmap, &ps[l].buckets, kTconvSplit);
         ++layer;
         coarse = cat[l];
         ld_coarse = width[l];
     }
+    const FrameDebug &D = ctx->frame_debug;
+    if (D.cap > 0 && D.level_coords && D.level_maps) {   // parity export (eager frames only)
+        SFB_REQUIRE(mb <= D.cap, "frame debug buffers are smaller than the cloud");
+        for (int l = 0; l <= L && l < D.levels; ++l) {
+            const int taps = kern[l] * kern[l] * kern[l];
+            SFB_REQUIRE(taps <= 27, "frame debug export holds up to 27 taps per level");
+            SFB_CUDA(cudaMemcpyAsync(D.level_coords + (size_t)l * 3 * D.cap, coords[l],
+                                     sizeof(int32_t) * 3 * mb, cudaMemcpyDeviceToDevice, st));
+            for (int t = 0; t < taps; ++t)
+                SFB_CUDA(cudaMemcpyAsync(D.level_maps + ((size_t)l * 27 + t) * D.cap,
+                                         nbr[l] + (size_t)t * mb, sizeof(int32_t) * mb,
+                                         cudaMemcpyDeviceToDevice, st));
+        }
+    }
     const NetLayer &h1 = net.layers[layer], &h2 = net.layers[layer + 1];
     size_t smem = sizeof(float) * ((size_t)kHeadRows * (h1.cin + h1.cout) + (size_t)h1.cin * h1.cout +
                                    (size_t)h1.cout * 14);
-    static bool attr = false;
-    if (!attr) {
-        SFB_CUDA(cudaFuncSetAttribute(k_head_mlp, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      200 * 1024));
-        attr = true;
-    }
+    set_max_dyn_smem(reinterpret_cast<const void *>(k_head_mlp), 200 * 1024);
     SFB_REQUIRE(smem <= 200 * 1024, "head MLP too wide");
     if (h1.cin == 32 && h1.cout == 64 && width[0] % 4 == 0) {
         k_head_row<32, 64><<<dgrid(mg[0], 128, 4), 128, 0, st>>>(cat[0], width[0], &C->m[0], h1.w,
                                                                  h1.b, h2.w, h2.b, raw);
-#ifdef SFB_WHATIF_DUP_HEAD   // what-if builds only (tools/abn.sh)
-        k_head_row<32, 64><<<dgrid(mg[0], 128, 4), 128, 0, st>>>(cat[0], width[0], &C->m[0], h1.w,
-                                                                 h1.b, h2.w, h2.b, raw);
-#endif
         SFB_CHECK_LAUNCH();
         return;
     }

@@ -40,13 +40,8 @@ constexpr int kWin = 2048;     // rank window of the merge
 // (two independent per-pixel chains per thread), 7 CTAs per SM; A/B on
 // config 2 with 8 frames in flight: 0.308 ms/frame vs 0.316 for 256 threads x
 // one pixel (64 threads x 4 pixels: 0.34, register-starved)
-#ifndef SFB_KCT
-#define SFB_KCT 128
-#endif
-constexpr int kCT = SFB_KCT;   // compositor threads per CTA
-#ifndef SFB_COMP_MINB
-#define SFB_COMP_MINB 7
-#endif
+constexpr int kCT = 128;       // compositor threads per CTA
+constexpr int kCompMinBlocks = 7;
 constexpr int kChunk = 64;     // runs per compositing chunk
 
 // ------------------------------------------------------------ 1. projection
@@ -889,7 +884,7 @@ __device__ __forceinline__ float3 horner3(const float4 *__restrict__ v, int m, f
 // MASK: the planes accumulated (SFB_PLANE_*), a compile-time constant so
 // unused accumulators and branches disappear from the hot loop
 template <int NPIX, int MASK>
-__global__ void __launch_bounds__(kCT, SFB_COMP_MINB) k_composite(CompParams P) {
+__global__ void __launch_bounds__(kCT, kCompMinBlocks) k_composite(CompParams P) {
     constexpr uint32_t NONE = 0xffffffffu;
     __shared__ uint32_t bitmap[kWin / 32];
     __shared__ uint32_t list[kWin];
@@ -1214,6 +1209,8 @@ __global__ void __launch_bounds__(kCT, SFB_COMP_MINB) k_composite(CompParams P) 
 }
 
 // ------------------------------------------------------------ driver
+__global__ void k_widen(const uint32_t *__restrict__ a, int64_t n, int64_t *__restrict__ b);
+
 // voxel-level depth order (see k_vdepth_keys): fills src (rank -> point) and
 // the rank-ordered colours; returns the sorted kept voxels, their exact depth
 // bits, rank offsets and point counts, and the device count of kept voxels
@@ -1270,9 +1267,6 @@ void render_run(sfb_ctx *ctx, const RenderInputs &in, const FrameParams *FP, int
     const int64_t nt = ntx * nty, ns = nsx * nsy;
     const int64_t n = in.n_points;
     Proj P = project_inputs(ctx, in, FP);
-#ifdef SFB_WHATIF_DUP_PROJ
-    P = project_inputs(ctx, in, FP);
-#endif
     ctx->mark(ST_PROJECT);
     const int64_t nb = n > 0 ? n : 1;
     const bool want_rgb = plane_mask & SFB_PLANE_RGB, want_n = plane_mask & SFB_PLANE_NORMAL;
@@ -1360,10 +1354,6 @@ void render_run(sfb_ctx *ctx, const RenderInputs &in, const FrameParams *FP, int
         SFB_CHECK_LAUNCH();
         // stable sort by tile id keeps each tile's runs in rank order
         const int fbits = bits_for((uint64_t)nt), sbits = bits_for((uint64_t)ns);
-#ifdef SFB_WHATIF_DUP_BIN   // what-if builds only: sorting the sorted lists again is idempotent
-        dsort_pairs<uint32_t>(ctx, fkey, fval, fkey2, fval2, &C->ef, ebound, fbits);
-        dsort_pairs<uint32_t>(ctx, skey, sval, skey2, sval2, &C->es, ebound, sbits);
-#endif
         f_ids = dsort_pairs<uint32_t>(ctx, fkey, fval, fkey2, fval2, &C->ef, ebound, fbits) ? fval2 : fval;
         const uint32_t *fk = (f_ids == fval2) ? fkey2 : fkey;
         s_ids = dsort_pairs<uint32_t>(ctx, skey, sval, skey2, sval2, &C->es, ebound, sbits) ? sval2 : sval;
@@ -1406,10 +1396,7 @@ void render_run(sfb_ctx *ctx, const RenderInputs &in, const FrameParams *FP, int
     CP.rgba = rgba;
     CP.dbg = ctx->debug_counters;
     const int cm = plane_mask & 7;
-#ifndef SFB_WHATIF_COMP_REPS   // what-if builds only (tools/abn.sh): the stage's marginal cost
-#define SFB_WHATIF_COMP_REPS 1
-#endif
-    for (int rep = 0; rep < SFB_WHATIF_COMP_REPS; ++rep) {
+    {
     constexpr int kNpixMid = (256 + kCT - 1) / kCT, kNpixMax = (1024 + kCT - 1) / kCT;
 #define SFB_COMP_CASE(M)                                                          \
     if (cm == M) {                                                                \
@@ -1423,6 +1410,18 @@ void render_run(sfb_ctx *ctx, const RenderInputs &in, const FrameParams *FP, int
 #undef SFB_COMP_CASE
     SFB_CHECK_LAUNCH();
     ctx->mark(ST_COMPOSITE);
+    const FrameDebug &D = ctx->frame_debug;
+    if (D.cap > 0 && D.source && n > 0) {   // parity export: rank order and runs
+        SFB_REQUIRE(nb <= D.cap, "frame debug buffers are smaller than the cloud");
+        k_widen<<<dgrid(nb, 256), 256, 0, st>>>(src, nb, D.source);
+        SFB_CHECK_LAUNCH();
+        if (D.run_start) SFB_CUDA(cudaMemcpyAsync(D.run_start, R.start, sizeof(int32_t) * nb,
+                                                  cudaMemcpyDeviceToDevice, st));
+        if (D.run_count) SFB_CUDA(cudaMemcpyAsync(D.run_count, R.count, sizeof(int32_t) * nb,
+                                                  cudaMemcpyDeviceToDevice, st));
+        if (D.run_rect) SFB_CUDA(cudaMemcpyAsync(D.run_rect, R.rect, sizeof(int4) * nb,
+                                                 cudaMemcpyDeviceToDevice, st));
+    }
 }
 
 // ------------------------------------------------------------ debug CSR (bin_tiles parity)

@@ -6,10 +6,6 @@
 //   float64 sums (bit-identical to np.add.at, which walks points in increasing
 //   index) -> 9 feature channels.
 // HBM-bound integer/byte work; no tensor cores.
-#ifdef SFB_VOX_CUB_SORT   // A/B builds only
-#include <cub/cub.cuh>
-#endif
-
 #include "common.cuh"
 #include "scan.cuh"
 
@@ -154,43 +150,6 @@ __global__ void k_keygen(const double *__restrict__ pos, int64_t n, const FrameP
     }
 }
 
-template <class K>
-__global__ void k_heads(const K *__restrict__ keys, int64_t n, int32_t *__restrict__ flag) {
-    SFB_FOR(j, n) flag[j] = (j == 0 || keys[j] != keys[j - 1]) ? 1 : 0;
-}
-
-template <class K>
-__global__ void k_segments(const K *__restrict__ keys, const uint32_t *__restrict__ vals,
-                           const int32_t *__restrict__ incl, int64_t n,
-                           const FrameParams *__restrict__ P, int32_t *__restrict__ coords,
-                           int64_t *__restrict__ pkeys, int32_t *__restrict__ p2v,
-                           int32_t *__restrict__ order, int32_t *__restrict__ offsets,
-                           DevCounts *__restrict__ C) {
-    const int bx = P->bits[0], by = P->bits[1];
-    SFB_FOR(j, n) {
-        int32_t v = incl[j] - 1;
-        uint32_t i = vals[j];
-        order[j] = (int32_t)i;
-        p2v[i] = v;
-
-        if (j == n - 1) {
-            offsets[v + 1] = (int32_t)n;
-            C->m[0] = v + 1;
-        }
-        if (j == 0 || incl[j - 1] != incl[j]) {
-            uint64_t k = (uint64_t)keys[j];
-            int64_t x = (int64_t)(k & ((1ull << bx) - 1)) + P->lo[0];
-            int64_t y = (int64_t)((k >> bx) & ((1ull << by) - 1)) + P->lo[1];
-            int64_t z = (int64_t)(k >> (bx + by)) + P->lo[2];
-            coords[3 * v + 0] = (int32_t)x;
-            coords[3 * v + 1] = (int32_t)y;
-            coords[3 * v + 2] = (int32_t)z;
-            pkeys[v] = pack_key(x, y, z);
-            offsets[v] = (int32_t)j;
-        }
-    }
-}
-
 // Segmentation of the sorted point keys in one pass (np.unique's sorted keys,
 // inverse and CSR of voxelgrid.py:146, 165-168): head flags from adjacent
 // keys, their inclusive scan by decoupled look-back (tiles in ticket order),
@@ -323,33 +282,15 @@ static void voxelize_typed(sfb_ctx *ctx, const double *pos, const double *col, i
     cudaStream_t st = ctx->stream;
     K *keys = ctx->arena.alloc<K>(n), *keys2 = ctx->arena.alloc<K>(n);
     uint32_t *vals = ctx->arena.alloc<uint32_t>(n), *vals2 = ctx->arena.alloc<uint32_t>(n);
-    int32_t *flag = ctx->arena.alloc<int32_t>(n);
     const unsigned g = dgrid(n, 256);
     k_keygen<K><<<g, 256, 0, st>>>(pos, n, P, keys, vals);
     SFB_CHECK_LAUNCH();
-#ifndef SFB_VOX_CUB_SORT
     // the library's own stable LSD sort (devprims.cu: 8-bit digits, 1024-item
     // sub-tiles ranked with __match_any_sync, small shared memory so its CTAs
-    // share SMs with the other lanes' kernels); A/B on config 2 against CUB's
-    // onesweep: 0.291 vs 0.298 ms/frame throughput, 0.787 vs 0.790 ms latency
+    // share SMs with the other lanes' kernels)
     const bool second = dsort_pairs<K>(ctx, keys, vals, keys2, vals2, nullptr, n, key_bits);
     K *ks = second ? keys2 : keys;
     uint32_t *vs = second ? vals2 : vals;
-#else
-    // CUB onesweep (A/B builds only)
-    size_t tb = 0;
-    cub::DeviceRadixSort::SortPairs(nullptr, tb, keys, keys2, vals, vals2, (int)n, 0, key_bits, st);
-    void *tmp = ctx->arena.alloc_bytes(tb);
-    SFB_CUDA(cub::DeviceRadixSort::SortPairs(tmp, tb, keys, keys2, vals, vals2, (int)n, 0, key_bits, st));
-    K *ks = keys2;
-    uint32_t *vs = vals2;
-#endif
-#ifdef SFB_VOX_UNFUSED_SEGMENTS   // the three-launch form (A/B builds)
-    k_heads<K><<<g, 256, 0, st>>>(ks, n, flag);
-    dscan(ctx, flag, flag, nullptr, n, nullptr, true);
-    k_segments<K><<<g, 256, 0, st>>>(ks, vs, flag, n, P, out.coords, out.keys, out.p2v, out.order,
-                                     out.offsets, C);
-#else
     {
         const int64_t tiles = (n + kSegTile - 1) / kSegTile;
         const size_t bytes = sizeof(unsigned long long) * (size_t)(tiles + 1);
@@ -360,7 +301,6 @@ static void voxelize_typed(sfb_ctx *ctx, const double *pos, const double *col, i
                                                         out.order, out.offsets, C, status,
                                                         reinterpret_cast<unsigned int *>(status + tiles));
     }
-#endif
     SFB_CHECK_LAUNCH();
     const int64_t vwarps = (ctx->grid_bound(n, ctx->hint_m[0]) + 4) / 5;
     k_voxel_feats<<<dgrid(32 * vwarps, 256), 256, 0, st>>>(pos, col, out.order, out.offsets,

@@ -20,12 +20,15 @@ class DegenerateCloudError(ValueError):
 
 
 class PointCloud:
-    """positions (N,3) float64 world units; colors (N,3) float64 in [0,1]."""
+    """positions (N,3) float64 world units; colors (N,3) float64 in [0,1];
+    normals optional (N,3) unit rows (pcio.py:39-83). Arrays may be host numpy
+    or torch tensors (CUDA tensors stay on the device)."""
 
     def __init__(self, positions, colors, normals=None, validate: bool = True):
         self.positions = _f64(positions)
         self.colors = _f64(colors)
         self.normals = None if normals is None else _f64(normals)
+        self._bbox = None
         if self.positions.ndim != 2 or self.positions.shape[1] != 3:
             raise ValueError(f"positions must be (N, 3), got {tuple(self.positions.shape)}")
         if tuple(self.colors.shape) != tuple(self.positions.shape):
@@ -34,9 +37,39 @@ class PointCloud:
             lo, hi = float(self.colors.min()), float(self.colors.max())
             if lo < 0.0 or hi > 1.0:
                 raise ValueError("color channels must lie in [0, 1]")
+        if self.normals is not None:
+            if tuple(self.normals.shape) != tuple(self.positions.shape):
+                raise ValueError("normals must match positions shape")
+            if validate and self.normals.shape[0]:
+                if isinstance(self.normals, torch.Tensor):
+                    dev = float((self.normals.norm(dim=1) - 1.0).abs().max())
+                else:
+                    dev = float(np.max(np.abs(np.linalg.norm(self.normals, axis=1) - 1.0)))
+                if dev > 1e-6:
+                    raise ValueError("normals must be unit length (within 1e-6)")
 
     def __len__(self) -> int:
         return int(self.positions.shape[0])
+
+    @property
+    def bbox(self):
+        """(min, max) corners as float64 numpy (3,) arrays; cached after first
+        use (pcio.py:73-80). Device clouds reduce on the GPU (sfb_bbox)."""
+        if self._bbox is None:
+            if len(self) == 0:
+                raise EmptyCloudError("empty cloud has no bbox")
+            if isinstance(self.positions, torch.Tensor) and self.positions.is_cuda:
+                from .voxelgrid import device_bbox
+                lo_hi = device_bbox(self.positions)
+                self._bbox = (lo_hi[:3].copy(), lo_hi[3:].copy())
+            else:
+                p = self.positions.numpy() if isinstance(self.positions, torch.Tensor) else self.positions
+                self._bbox = (p.min(axis=0), p.max(axis=0))
+        return self._bbox
+
+    def with_positions(self, positions) -> "PointCloud":
+        """Same colours and normals at new positions (pcio.py:82-83)."""
+        return PointCloud(positions, self.colors, self.normals)
 
     @property
     def on_device(self) -> bool:

@@ -74,15 +74,22 @@ def stage(cloud, lane: int = 0) -> StagedCloud:
     if slot[5]:   # staged but not yet rendered: its data would be overwritten
         raise RuntimeError(f"both staging buffers of lane {lane} hold unrendered clouds: render "
                            "a staged cloud of this lane (or stage on another lane) first")
-    st["k"] ^= 1
     ply = isinstance(cloud, PlyBody)
     n = len(cloud) if ply else int(cloud.positions.shape[0])
     if n == 0:
         raise EmptyCloudError("empty cloud has no bbox")
-    if slot[0] is None or slot[0].shape[0] < n:
+    st["k"] ^= 1
+    grow = slot[0] is None or slot[0].shape[0] < n
+    grow_ply = ply and (slot[3] is None or slot[3].numel() < cloud.raw.numel())
+    if (grow or grow_ply) and slot[2] is not None:
+        # the last frame that read these buffers may still be running on its
+        # stream: the caching allocator could hand the freed blocks to the
+        # next allocation of another stream, so wait before dropping them
+        slot[2].synchronize()
+    if grow:
         slot[0] = torch.empty((n, 3), dtype=torch.float64, device=dev)
         slot[1] = torch.empty((n, 3), dtype=torch.float64, device=dev)
-    if ply and (slot[3] is None or slot[3].numel() < cloud.raw.numel()):
+    if grow_ply:
         slot[3] = torch.empty(cloud.raw.numel(), dtype=torch.uint8, device=dev)
     if slot[4] is None:
         slot[4] = torch.empty(6, dtype=torch.int64).pin_memory()
@@ -154,11 +161,14 @@ def render_frame(cloud: PointCloud, weights: NetworkWeights, cam: Camera,
     for p in planes:
         mask |= _PLANE_BIT[p]
     c, o = cam.struct(), options.struct()
-    ctx.call("sfb_frame", _lib.ptr(pos), _lib.ptr(col), n, s, lo_hi.ctypes.data_as(_lib.P),
-             _lib.ctypes.byref(c), _lib.ctypes.byref(o), mask, bg.ctypes.data_as(_lib.P),
-             _lib.ptr(rgb), _lib.ptr(nrm), _lib.ptr(dep), _lib.ptr(trans))
-    if slot is not None:   # the staging buffer is free once this frame is done
-        slot[2] = torch.cuda.current_stream().record_event()
+    try:
+        ctx.call("sfb_frame", _lib.ptr(pos), _lib.ptr(col), n, s, lo_hi.ctypes.data_as(_lib.P),
+                 _lib.ctypes.byref(c), _lib.ctypes.byref(o), mask, bg.ctypes.data_as(_lib.P),
+                 _lib.ptr(rgb), _lib.ptr(nrm), _lib.ptr(dep), _lib.ptr(trans))
+    finally:
+        if slot is not None:   # the staging buffer is free once this frame (or the
+            # part of it that was enqueued before an error) is done
+            slot[2] = torch.cuda.current_stream().record_event()
     if rgb is None:
         rgb = torch.zeros((int(cam.height), int(cam.width), 3), dtype=torch.float32,
                           device=pos.device)
@@ -168,3 +178,37 @@ def render_frame(cloud: PointCloud, weights: NetworkWeights, cam: Camera,
 def stats(lane: int = 0) -> dict:
     """Sizes of the last call (kept splats, runs, pyramid entries, voxels per level)."""
     return _lib.context(lane=lane).stats()
+
+
+def render_frame_debug(cloud, weights: NetworkWeights, cam: Camera, planes=("rgb", "normal"),
+                       background=(0.0, 0.0, 0.0), options: RenderOptions = None,
+                       levels: int = 4, lane: int = 0):
+    """``render_frame`` plus the fused path's internal order, for parity tests:
+    ``source`` (rank -> point over the kept points, rasterizer.py:105), the runs
+    of identical geometry (start rank, point count, tile rect x0 x1 y0 y1 of
+    _raster_kernels.py:123-130) and, per UNet level, the level coordinates and
+    27-tap kernel map in the level's own row order (sparsenet.py:201-207)."""
+    ctx = ensure_loaded(weights, lane)
+    n = len(cloud)
+    dev = torch.device("cuda", torch.cuda.current_device())
+    source = torch.empty(n, dtype=torch.int64, device=dev)
+    rs = torch.empty(n, dtype=torch.int32, device=dev)
+    rc = torch.empty(n, dtype=torch.int32, device=dev)
+    rr = torch.empty((n, 4), dtype=torch.int32, device=dev)
+    lc = torch.empty((levels, n, 3), dtype=torch.int32, device=dev)
+    lm = torch.empty((levels, 27, n), dtype=torch.int32, device=dev)
+    ctx.lib.sfb_set_frame_debug(ctx.handle, n, _lib.ptr(source), _lib.ptr(rs), _lib.ptr(rc),
+                                _lib.ptr(rr), levels, _lib.ptr(lc), _lib.ptr(lm))
+    try:
+        fb = render_frame(cloud, weights, cam, planes, background, options, lane=lane)
+        torch.cuda.synchronize()
+    finally:
+        ctx.lib.sfb_set_frame_debug(ctx.handle, 0, None, None, None, None, 0, None, None)
+    st = ctx.stats()
+    kept, runs = st["kept"], st["runs"]
+    vox = st["voxels"]
+    out = {"source": source[:kept], "run_start": rs[:runs], "run_count": rc[:runs],
+           "run_rect": rr[:runs], "kept": kept, "runs": runs,
+           "level_coords": [lc[l, :vox[l]] for l in range(levels) if vox[l] > 0],
+           "level_maps": [lm[l, :, :vox[l]] for l in range(levels) if vox[l] > 0]}
+    return fb, out

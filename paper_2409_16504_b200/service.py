@@ -130,11 +130,13 @@ def render_pose_frame(cloud: PointCloud, weights: NetworkWeights, pose: PoseMess
         out = torch.empty((pose.height, pose.width, 4), dtype=torch.uint8, device=pos.device)
     c, o = cam.struct(), options.struct()
     sh = _shading(pose.mode, pose.light_dir, ambient, diffuse)
-    ctx.call("sfb_frame_rgba", _lib.ptr(pos), _lib.ptr(col), n, s, lo_hi.ctypes.data_as(_lib.P),
-             _lib.ctypes.byref(c), _lib.ctypes.byref(o), _lib.ctypes.byref(sh),
-             bg.ctypes.data_as(_lib.P), _lib.ptr(out))
-    if slot is not None:
-        slot[2] = torch.cuda.current_stream().record_event()
+    try:
+        ctx.call("sfb_frame_rgba", _lib.ptr(pos), _lib.ptr(col), n, s, lo_hi.ctypes.data_as(_lib.P),
+                 _lib.ctypes.byref(c), _lib.ctypes.byref(o), _lib.ctypes.byref(sh),
+                 bg.ctypes.data_as(_lib.P), _lib.ptr(out))
+    finally:
+        if slot is not None:   # staging buffer free once the enqueued work is done
+            slot[2] = torch.cuda.current_stream().record_event()
     return out
 
 

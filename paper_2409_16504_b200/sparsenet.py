@@ -140,11 +140,13 @@ class HeadOutput:
 
 
 def activate_head(raw, voxel_scale: float) -> HeadOutput:
-    """Bounded splat parameters from raw head outputs (sparsenet.py:310-341), float64."""
+    """Bounded splat parameters from raw head outputs (sparsenet.py:310-341):
+    float64 in (the reference's dtype; float32 raw from the UNet widens
+    exactly), float64 out."""
     if isinstance(raw, torch.Tensor):
-        r = raw.to(device="cuda", dtype=torch.float32)
+        r = raw.to(device="cuda", dtype=torch.float64)
     else:
-        r = torch.from_numpy(np.asarray(raw, dtype=np.float32)).cuda()
+        r = torch.from_numpy(np.asarray(raw, dtype=np.float64)).cuda()
     if r.shape[-1] != HEAD_CHANNELS:
         raise ValueError(f"raw head output must have {HEAD_CHANNELS} channels")
     if voxel_scale <= 0:

@@ -41,7 +41,10 @@ class SparseVoxelGrid:
     """Device sparse voxel tensor in canonical (packed-key) row order.
 
     coords (M,3) int32 CUDA, feats (M,C) CUDA (float64 at level 0, float32
-    inside the network), stride, scale_to_world.
+    inside the network), stride, scale_to_world. Constructed without ``keys``
+    (the reference constructor, voxelgrid.py:57-79), rows are validated and
+    sorted by packed key on the device, duplicates rejected; the library's own
+    producers (voxelize_adaptive) pass their canonical keys and skip that.
     """
 
     coords: torch.Tensor
@@ -49,6 +52,41 @@ class SparseVoxelGrid:
     stride: int = 1
     scale_to_world: float = 1.0
     keys: torch.Tensor = field(default=None, repr=False)
+
+    def __post_init__(self):
+        if self.keys is not None:
+            return
+        c = to_device(self.coords, torch.int32) if not isinstance(self.coords, torch.Tensor) \
+            else self.coords.to(device="cuda", dtype=torch.int32)
+        f = self.feats
+        if not isinstance(f, torch.Tensor):
+            f = to_device(np.asarray(f, dtype=np.float64), torch.float64)
+        else:
+            f = f.to("cuda")
+            if not f.is_floating_point():
+                f = f.to(torch.float64)
+        if f.ndim == 1:                      # scalar channel shorthand
+            f = f[:, None]
+        if c.ndim != 2 or c.shape[1] != 3:
+            raise ValueError(f"coords must be (M, 3), got {tuple(c.shape)}")
+        if f.shape[0] != c.shape[0]:
+            raise ValueError("feats row count must match coords")
+        if self.stride < 1 or (self.stride & (self.stride - 1)) != 0:
+            raise ValueError(f"stride must be a power of two, got {self.stride}")
+        if self.scale_to_world <= 0:
+            raise ValueError("scale_to_world must be positive")
+        if c.numel() and bool((c % self.stride != 0).any()):
+            raise ValueError(f"all coordinates must be multiples of stride {self.stride}")
+        c64 = c.to(torch.int64)
+        if c64.numel() and bool((c64.abs() >= COORD_LIMIT).any()):
+            raise ValueError(f"voxel coordinates must satisfy |c| < {COORD_LIMIT}")
+        keys = ((c64[:, 2] + _BIAS) << 42) | ((c64[:, 1] + _BIAS) << 21) | (c64[:, 0] + _BIAS)
+        keys, order = torch.sort(keys, stable=True)
+        if keys.numel() > 1 and bool((keys[1:] == keys[:-1]).any()):
+            raise ValueError("duplicate voxel coordinates")
+        self.coords = c[order].contiguous()
+        self.feats = f[order].contiguous()
+        self.keys = keys
 
     def __len__(self) -> int:
         return int(self.coords.shape[0])
@@ -80,6 +118,25 @@ class SparseVoxelGrid:
         return cls(to_device(coords[order], torch.int32), to_device(feats[order], feat_dtype),
                    stride, scale_to_world, to_device(keys, torch.int64))
 
+    def lookup(self, coords) -> torch.Tensor:
+        """Row index of each query coordinate, or -1 where unoccupied
+        (voxelgrid.py:88-94), int64 on the device; a GPU hash probe."""
+        q = coords if isinstance(coords, torch.Tensor) else torch.from_numpy(
+            np.ascontiguousarray(np.atleast_2d(np.asarray(coords, dtype=np.int64))))
+        q = q.to("cuda")
+        if q.ndim == 1:
+            q = q[None, :]
+        if q.ndim != 2 or q.shape[1] != 3:
+            raise ValueError(f"query coords must be (K, 3), got {tuple(q.shape)}")
+        if q.numel() and bool((q.to(torch.int64).abs() >= COORD_LIMIT).any()):
+            raise ValueError(f"voxel coordinates must satisfy |c| < {COORD_LIMIT}")
+        q = q.to(torch.int32).contiguous()
+        nq = int(q.shape[0])
+        rows = torch.empty(nq, dtype=torch.int64, device=q.device)
+        _lib.context().call("sfb_lookup", _lib.ptr(self.coords), len(self), _lib.ptr(q), nq,
+                            _lib.ptr(rows))
+        return rows
+
     def kernel_map(self, kernel: int = 3) -> torch.Tensor:
         """(M, k^3) int32 neighbour rows for a stride-``self.stride`` conv, -1 = empty
         (the tap lookups of sparsenet.py:201-207)."""
@@ -98,6 +155,12 @@ class VoxelizedCloud:
     source_offsets: torch.Tensor   # (M+1,) int32
     s: float = 0.0
     bbox: tuple = None
+
+    @property
+    def source_indices(self) -> list:
+        """Per-voxel tensors of contributing original point indices (voxelgrid.py:109-116)."""
+        off = self.source_offsets.cpu().tolist()
+        return [self.source_order[off[i]:off[i + 1]] for i in range(len(self.grid))]
 
     def reconstructed_positions(self) -> torch.Tensor:
         g = self.grid
@@ -162,38 +225,43 @@ def voxelize_adaptive(cloud: PointCloud) -> VoxelizedCloud:
     return VoxelizedCloud(grid, p2v, order, offsets[:m + 1], s, tuple(lo_hi))
 
 
+def _pool(grid: SparseVoxelGrid):
+    m = len(grid)
+    c = grid.channel_count
+    dev = grid.coords.device
+    f64 = grid.feats.dtype == torch.float64
+    f = grid.feats.contiguous() if f64 else grid.feats.to(torch.float32).contiguous()
+    pc = torch.empty((m, 3), dtype=torch.int32, device=dev)
+    pf = torch.empty((m, c), dtype=f.dtype, device=dev)
+    c2p = torch.empty(m, dtype=torch.int32, device=dev)
+    mp = _lib.I64(0)
+    _lib.context().call("sfb_pool_f64" if f64 else "sfb_pool", _lib.ptr(grid.coords), _lib.ptr(f),
+                        m, c, grid.stride, _lib.ptr(pc), _lib.ptr(pf), _lib.ptr(c2p),
+                        _lib.ctypes.byref(mp))
+    mp = mp.value
+    parent = SparseVoxelGrid(pc[:mp], pf[:mp], grid.stride * 2, grid.scale_to_world,
+                             pack_keys_device(pc[:mp]))
+    return parent, c2p
+
+
+def pack_keys_device(coords: torch.Tensor) -> torch.Tensor:
+    """Packed int64 keys of canonical device coords (voxelgrid.py:22-27)."""
+    c = coords.to(torch.int64)
+    return ((c[:, 2] + _BIAS) << 42) | ((c[:, 1] + _BIAS) << 21) | (c[:, 0] + _BIAS)
+
+
 def pool_2x2x2(grid: SparseVoxelGrid) -> SparseVoxelGrid:
     """Mean of occupied children per stride-doubled parent (voxelgrid.py:171-185).
 
-    Features are pooled in float32 (the network's storage type)."""
-    m = len(grid)
-    c = grid.channel_count
-    f = grid.feats.to(torch.float32).contiguous()
-    dev = grid.coords.device
-    pc = torch.empty((m, 3), dtype=torch.int32, device=dev)
-    pf = torch.empty((m, c), dtype=torch.float32, device=dev)
-    c2p = torch.empty(m, dtype=torch.int32, device=dev)
-    mp = _lib.I64(0)
-    _lib.context().call("sfb_pool", _lib.ptr(grid.coords), _lib.ptr(f), m, c, grid.stride,
-                        _lib.ptr(pc), _lib.ptr(pf), _lib.ptr(c2p), _lib.ctypes.byref(mp))
-    mp = mp.value
-    return SparseVoxelGrid(pc[:mp], pf[:mp], grid.stride * 2, grid.scale_to_world)
+    float64 features (the reference's dtype) are pooled in float64 with the
+    children summed in child-row order (np.add.at); float32 network features
+    stay float32."""
+    return _pool(grid)[0]
 
 
 def pool_with_parents(grid: SparseVoxelGrid):
     """pool_2x2x2 plus the child -> parent row map (used by tests)."""
-    m = len(grid)
-    c = grid.channel_count
-    f = grid.feats.to(torch.float32).contiguous()
-    dev = grid.coords.device
-    pc = torch.empty((m, 3), dtype=torch.int32, device=dev)
-    pf = torch.empty((m, c), dtype=torch.float32, device=dev)
-    c2p = torch.empty(m, dtype=torch.int32, device=dev)
-    mp = _lib.I64(0)
-    _lib.context().call("sfb_pool", _lib.ptr(grid.coords), _lib.ptr(f), m, c, grid.stride,
-                        _lib.ptr(pc), _lib.ptr(pf), _lib.ptr(c2p), _lib.ctypes.byref(mp))
-    mp = mp.value
-    return SparseVoxelGrid(pc[:mp], pf[:mp], grid.stride * 2, grid.scale_to_world), c2p
+    return _pool(grid)
 
 
 def transposed_map(parent: SparseVoxelGrid, targets: torch.Tensor):

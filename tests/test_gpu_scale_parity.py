@@ -1,0 +1,73 @@
+"""Exactness of the FUSED frame path (what bench.py times) at the BASELINE
+configs' full sizes, full frames, against the CPU oracle (tests/parity_util.py):
+
+* the fused voxel-level depth order == the oracle's stable argsort of depth
+  over the same Gaussians (rasterizer.py:105), bit for bit, for every view;
+* every rank's tile rect and therefore bin_tiles' tile offsets
+  (_raster_kernels.py:108-143), bit for bit;
+* the UNet's per-level coordinates and 27-tap kernel maps (sparsenet.py:201-207)
+  against the oracle's canonical pooling, bit for bit (configs 2 and 3);
+* planes within 2e-3 max-abs per channel with ZERO pixels over, both on
+  identical Gaussians (renderer parity) and end to end (cloud -> planes with
+  the GPU's fp32-accurate P2ENet against the oracle's float64 one).
+
+The measured values per config/view are in profiles/parity_r02.json
+(tools/parity_report.py)."""
+import numpy as np
+import pytest
+
+from oracle import net as ON
+from paper_2409_16504_b200 import netplan, scenes
+from paper_2409_16504_b200.pcio import PointCloud
+from parity_util import frame_parity, gpu_splats_np
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def weights():
+    return netplan.init_random(netplan.NetworkPlan(), 0)
+
+
+def check(rec, where):
+    o = rec["order"]
+    assert o["order_exact"], (where, o)
+    assert o["runs_contiguous"] and o["rects_exact"] and o["offsets_exact"], (where, o)
+    for kind in ("renderer", "e2e"):
+        for plane, s in rec[kind].items():
+            assert s["over"] == 0 and s["max_abs"] <= 2e-3, (where, kind, plane, s,
+                                                             rec.get("e2e_over_pixels"))
+    if "levels" in rec:
+        assert rec["levels"]["exact"], (where, rec["levels"])
+
+
+def run_config(cloud, views, weights, which, levels_on=(0,)):
+    pc = PointCloud(cloud.positions, cloud.colors)
+    est = ON.estimate(cloud.positions, cloud.colors, weights.as_oracle_layers(), 3)
+    sp = gpu_splats_np(pc, weights)
+    for k in which:
+        rec = frame_parity(pc, cloud, weights, views[k], est=est, gpu_sp=sp,
+                           levels=k in levels_on)
+        print(k, rec["order"], rec["renderer"], rec["e2e"])
+        check(rec, k)
+
+
+def test_config2_all_eight_views(weights):
+    cloud, views = scenes.config2()
+    run_config(cloud, views, weights, range(len(views)))
+
+
+def test_config3_views(weights):
+    cloud, views = scenes.config3()
+    run_config(cloud, views, weights, (0, 5, 9, 13))
+
+
+@pytest.mark.parametrize("frame", [0, 37, 63])
+def test_config4_frames(weights, frame):
+    cloud, views = scenes.config4_frame(frame)
+    run_config(cloud, views, weights, (0,), levels_on=())
+
+
+def test_config5_views(weights):
+    cloud, views = scenes.config5()
+    run_config(cloud, views, weights, (3, 17), levels_on=())
