@@ -49,11 +49,15 @@ def parse():
     ap.add_argument("--steps", type=int, default=2000)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
-    ap.add_argument("--config", choices=("c2", "c1"), default="c2")
+    ap.add_argument("--config", choices=("c2", "c1", "c4", "c5"), default="c2",
+                    help="c2: the headline workload (BASELINE configs[1]); c4: the 64-frame "
+                         "sequence, frames block-sharded over ranks; c5: the 2048^3 scene, 32 "
+                         "views round-robin over ranks (both also report gather-inclusive fps)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-profile", action="store_true", help="skip the CUPTI launch count")
-    ap.add_argument("--cpu-rows", type=int, default=2, help="tile rows in the CPU sample")
+    ap.add_argument("--cpu-frames", type=int, default=1,
+                    help="full config-2 frames of the CPU port timed for cpu_baseline")
     ap.add_argument("--lanes", type=int, default=8, help="frames in flight per GPU (streams)")
     ap.add_argument("--net-mode", choices=("tc_tf32x3", "tc_bf16", "simt_f32"), default="tc_tf32x3",
                     help="P2ENet arithmetic (tc_tf32x3: fp32-accurate parity mode)")
@@ -89,31 +93,36 @@ def peaks():
 
 
 # ---------------------------------------------------------------- CPU oracle leg
-def cpu_frame_sample(cloud, view, weights, rows):
-    """One frame of the CPU oracle port: full P2ENet (voxelize, UNet, head) and
-    the full projection/sort/support-radius prepare, then binning + blending of
-    `rows` tile rows in the middle of the image, extrapolated to all rows."""
+def cpu_frame(cloud, view, weights, threads):
+    """One WHOLE frame of the CPU port of the reference path (tests-only
+    restatement, oracle/): voxelize + UNet + head (estimators.py:214-231, numpy
+    BLAS), then render rgb and normal (rasterizer.py:152-166: projection, sort,
+    support radius, bin_tiles + forward_kernel over all tile rows, in bands of 8
+    rows for bounded memory; C/OpenMP on `threads` threads). Nothing is
+    extrapolated."""
     from oracle import net as ON
     from oracle import raster as OR
     t0 = time.perf_counter()
     est = ON.estimate(cloud.positions, cloud.colors, weights.as_oracle_layers(),
                       weights.plan.levels)
     t1 = time.perf_counter()
-    nty = -(-int(view.height) // 16)
-    lo = max(0, nty // 2 - rows // 2)
-    win = (lo, min(nty, lo + rows))
-    prep = OR.prepare(est, view, "rgb", 16, ty_window=(0, 0))       # prepare without bins
-    t2 = time.perf_counter()
     for mode in ("rgb", "normal"):
-        OR.render(est, view, mode, ty_window=win)
-    t3 = time.perf_counter()
-    # render() redoes prepare per mode; charge its windowed bin+blend only
-    bin_blend = (t3 - t2) - 2 * (t2 - t1)
-    bin_blend = max(bin_blend, 0.0)
-    total = (t1 - t0) + 2 * (t2 - t1) + bin_blend * nty / (win[1] - win[0])
-    del prep
-    return dict(seconds=total, p2enet_s=t1 - t0, prepare_s=t2 - t1,
-                bin_blend_sample_s=bin_blend, rows=win[1] - win[0], nty=nty)
+        OR.render_banded(est, view, mode)
+    t2 = time.perf_counter()
+    return dict(seconds=t2 - t0, p2enet_s=t1 - t0, render_s=t2 - t1)
+
+
+def cpu_env():
+    """Thread settings of the CPU legs (set before numpy / the oracle load)."""
+    cores = os.cpu_count()
+    for k in ("OMP_NUM_THREADS", "OPENBLAS_NUM_THREADS"):
+        os.environ.setdefault(k, str(cores))
+    cpu = ""
+    try:
+        cpu = [ln.split(":", 1)[1].strip() for ln in open("/proc/cpuinfo") if "model name" in ln][0]
+    except (OSError, IndexError):
+        pass
+    return cores, cpu
 
 
 def workload_config(name, cloud, views):
@@ -130,39 +139,43 @@ def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    os.environ.setdefault("OMP_NUM_THREADS", str(os.cpu_count()))
+    cores, cpu = cpu_env()
     from oracle import raster as OR
-    from paper_2409_16504_b200 import netplan
+    from paper_2409_16504_b200 import netplan, scenes
     OR.build()
-    cloud, views = workload(args.config)
+    name = args.config if args.config in ("c1", "c2") else "c2"
+    cloud, views = workload(name)
     w = netplan.init_random(netplan.NetworkPlan(), 0)
-    # one frame sample takes seconds of CPU time, so the arm is time-boxed:
-    # at most one warm-up, then samples until K are done or the budget
-    # (SFB_REF_BUDGET_S, default 150 s) is spent — at least one
-    for i in range(min(args.warmup, 1)):
-        cpu_frame_sample(cloud, views[i % len(views)], w, args.cpu_rows)
-    budget = float(os.environ.get("SFB_REF_BUDGET_S", "150"))
-    secs = []
+    # warm-up on a small frame (numpy / OpenMP / page-in), then whole frames of
+    # the workload until K are done or the time budget (SFB_REF_BUDGET_S,
+    # default 300 s) is spent — at least one
+    if args.warmup:
+        c1, v1 = scenes.config1(n_dirs=4000)
+        cpu_frame(c1, v1[0], w, cores)
+    budget = float(os.environ.get("SFB_REF_BUDGET_S", "300"))
+    recs = []
     t_start = time.perf_counter()
     for i in range(args.steps):
-        secs.append(cpu_frame_sample(cloud, views[i % len(views)], w, args.cpu_rows)["seconds"])
+        recs.append(cpu_frame(cloud, views[i % len(views)], w, cores))
         if time.perf_counter() - t_start > budget:
             break
-    tot = sum(secs)
-    value = len(secs) / tot
-    cores = os.cpu_count()
-    sample = (f"oracle port (numpy + C/OpenMP restatement of the reference), per step: full "
-              f"P2ENet + projection/sort/prepare of one {args.config} frame, rgb+normal "
-              f"bin/blend of {args.cpu_rows} of 64 tile rows, extrapolated to the frame")
+    tot = sum(r["seconds"] for r in recs)
+    value = len(recs) / tot
+    sample = (f"oracle port (numpy + C/OpenMP restatement of the reference path), {len(recs)} "
+              f"whole {name} frame(s): P2ENet {np.mean([r['p2enet_s'] for r in recs]):.2f} s + "
+              f"render rgb+normal over all tile rows {np.mean([r['render_s'] for r in recs]):.2f} s "
+              f"per frame; {cores} threads on {cpu or 'unknown CPU'}")
     print(json.dumps({
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": 1e3 * tot / len(secs), "steps_sampled": len(secs),
+        "ms_per_step": 1e3 * tot / len(recs), "steps_sampled": len(recs),
         "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": workload_config(args.config, cloud, views),
+        "config": workload_config(name, cloud, views),
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port",
-                         "sample": sample},
+                         "sample": sample, "cpu": cpu,
+                         "p2enet_s": float(np.mean([r["p2enet_s"] for r in recs])),
+                         "render_s": float(np.mean([r["render_s"] for r in recs]))},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }), flush=True)
 
@@ -338,13 +351,21 @@ def run_ours(args):
     torch.cuda.synchronize()
     lat_ms = max_over_ranks(sum(a.elapsed_time(b) for a, b in evs) / n_lat)
 
-    # ---- timed region: throughput, frames overlapped over the lanes
+    # ---- timed region: throughput, frames overlapped over the lanes. The
+    # clock sampler (50 ms period) watches a >= 1 s window of this same load
+    # around it: the timed K frames take only milliseconds
     barrier()
     clocks = ClockSampler(local)
     time.sleep(0.5)   # nvidia-smi needs a moment before its first sample
     clocks.mark()
+    t_mark = time.perf_counter()
+    while time.perf_counter() - t_mark < 0.5:   # load before the timed region
+        run_batch(lanes * copies, dev_clouds)
+    barrier()
     ms, host_s = run_batch(args.steps, dev_clouds)
     barrier()
+    while time.perf_counter() - t_mark < 1.0:   # and after it
+        run_batch(lanes * copies, dev_clouds)
     clk = clocks.stop()
     ms_max = max_over_ranks(ms)
     value = world * args.steps / (ms_max / 1e3)
@@ -464,13 +485,16 @@ def run_ours(args):
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
-        os.environ.setdefault("OMP_NUM_THREADS", str(os.cpu_count()))
-        s = cpu_frame_sample(cloud, views[0], weights, args.cpu_rows)
-        cpu = {"value": 1.0 / s["seconds"], "unit": UNIT, "cores": os.cpu_count(), "kind": "port",
-               "sample": (f"oracle port: full P2ENet {s['p2enet_s']:.2f}s + prepare "
-                          f"{s['prepare_s']:.2f}s x2 modes + rgb/normal bin+blend of "
-                          f"{s['rows']}/{s['nty']} tile rows {s['bin_blend_sample_s']:.2f}s "
-                          f"extrapolated; {s['seconds']:.1f} s/frame")}
+        cores, cpu_name = cpu_env()
+        recs = [cpu_frame(cloud, views[i % len(views)], weights, cores)
+                for i in range(max(1, args.cpu_frames))]
+        tot = sum(r["seconds"] for r in recs)
+        cpu = {"value": len(recs) / tot, "unit": UNIT, "cores": cores, "kind": "port",
+               "cpu": cpu_name,
+               "sample": (f"oracle port, {len(recs)} whole frame(s) of this workload: P2ENet "
+                          f"{np.mean([r['p2enet_s'] for r in recs]):.2f} s + render rgb+normal "
+                          f"(all tile rows) {np.mean([r['render_s'] for r in recs]):.2f} s; "
+                          f"{tot / len(recs):.1f} s/frame on {cores} threads")}
 
     if rank == 0:
         line = {
@@ -497,10 +521,171 @@ def run_ours(args):
         dist.destroy_process_group()
 
 
+# ---------------------------------------------------------------- sharded jobs (c4 / c5)
+def sharded_job(n_units, policy, render_unit, rank, world, lanes=1):
+    """This rank's shard of a job of independent units:
+    ``render_unit(u, lane)`` renders unit u and returns its planes; units go
+    round the lanes (streams). No data-path collective; the planes are
+    gathered afterwards (shard.gather_planes)."""
+    from paper_2409_16504_b200.shard import shard
+    return {u: render_unit(u, i % lanes)
+            for i, u in enumerate(shard(n_units, rank, world, policy))}
+
+
+def run_units(args):
+    """c4 (64-frame sequence, frames block-sharded) / c5 (2048^3 scene, 32
+    views round-robin): every rank renders its own units end to end (P2ENet +
+    splat per unit). ``value`` = units/s from device time (max over ranks);
+    ``gather`` = units/s of the wall-clock job including each rank's
+    device->host copies of its planes (``local``) and the planes of every
+    unit delivered to rank 0's host memory (``to_rank0``: NCCL point-to-point
+    over NVLink, then rank 0's copies), max over ranks."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2409_16504_b200 import netplan, scenes
+    from paper_2409_16504_b200.gaussians import Camera
+    from paper_2409_16504_b200.pcio import PointCloud
+    from paper_2409_16504_b200.pipeline import render_frame, stats
+    from paper_2409_16504_b200.shard import gather_planes, max_over_ranks, shard
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    weights = netplan.init_random(netplan.NetworkPlan(), 0)
+    from paper_2409_16504_b200 import sparsenet
+    sparsenet.set_mode(args.net_mode)
+    if args.config == "c4":
+        n_units, policy = 64, "block"
+        mine = shard(n_units, rank, world, policy)
+        clouds, cams = {}, {}
+        for u in mine:
+            c, v = scenes.config4_frame(u)
+            clouds[u] = PointCloud(torch.from_numpy(c.positions).cuda(),
+                                   torch.from_numpy(c.colors).cuda(), validate=False)
+            cams[u] = Camera.of(v[0])
+        points = int(np.mean([len(clouds[u]) for u in mine]))
+        desc = (f"c4: 64-frame sequence of the 5-ellipsoid union (scenes.config4_frame, ~{points} "
+                f"pts/frame), one 1024x1024 view per frame, frames block-sharded over ranks")
+    else:
+        c, views = scenes.config5()
+        n_units, policy = len(views), "round_robin"
+        mine = shard(n_units, rank, world, policy)
+        dev = PointCloud(torch.from_numpy(c.positions).cuda(), torch.from_numpy(c.colors).cuda(),
+                         validate=False)
+        clouds = {u: dev for u in mine}
+        cams = {u: Camera.of(views[u]) for u in mine}
+        points = len(c)
+        desc = (f"c5: 2048^3 terrain + 50 boxes ({points} pts, scenes.config5), 32 views at "
+                f"1920x1080 round-robin over ranks, P2ENet + splat per view")
+    lanes = max(1, min(args.lanes, len(mine) or 1))
+    streams = [torch.cuda.Stream() for _ in range(lanes)]
+    downs = [torch.cuda.Stream() for _ in range(lanes)]
+    outs = {}
+    for u in mine:
+        H, W = cams[u].height, cams[u].width
+        outs[u] = (torch.empty((H, W, 3), dtype=torch.float32, device="cuda"),
+                   torch.empty((H, W, 3), dtype=torch.float32, device="cuda"),
+                   None, torch.empty((H, W), dtype=torch.float32, device="cuda"))
+    host = {u: tuple(torch.empty(t.shape, dtype=t.dtype).pin_memory()
+                     for t in (outs[u][0], outs[u][1], outs[u][3])) for u in mine}
+
+    def render_unit(u, lane):
+        with torch.cuda.stream(streams[lane]):
+            fb = render_frame(clouds[u], weights, cams[u], ("rgb", "normal"), out=outs[u],
+                              lane=lane)
+        return (fb.rgb, fb.normal, fb.transmittance)
+
+    def job(copy_back=False):
+        cur = torch.cuda.current_stream()
+        for st in streams:
+            st.wait_stream(cur)
+        planes = sharded_job(n_units, policy, render_unit, rank, world, lanes)
+        if copy_back:   # each rank's planes into pinned host memory, per lane
+            for i, u in enumerate(mine):
+                lane = i % lanes
+                downs[lane].wait_stream(streams[lane])
+                with torch.cuda.stream(downs[lane]):
+                    for h, t in zip(host[u], planes[u]):
+                        h.copy_(t, non_blocking=True)
+        for st in streams + downs:
+            cur.wait_stream(st)
+        return planes
+
+    for _ in range(max(args.warmup, 3)):   # eager -> capture -> replay per (lane, unit)
+        job(copy_back=True)
+    barrier()
+    clocks = ClockSampler(local)
+    time.sleep(0.5)
+    clocks.mark()
+    t_mark = time.perf_counter()
+    while time.perf_counter() - t_mark < 0.5:
+        job()
+    barrier()
+    start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    start.record()
+    reps = max(1, args.steps // max(1, n_units))
+    for _ in range(reps):
+        job()
+    end.record()
+    end.synchronize()
+    ms = max_over_ranks(start.elapsed_time(end))
+    barrier()
+    while time.perf_counter() - t_mark < 1.0:
+        job()
+    clk = clocks.stop()
+    # gather-inclusive wall clock (host timer around the whole job, max over ranks)
+    barrier()
+    t0 = time.perf_counter()
+    planes = job(copy_back=True)
+    torch.cuda.synchronize()
+    t_local = max_over_ranks(time.perf_counter() - t0)
+    barrier()
+    t0 = time.perf_counter()
+    planes = job()
+    merged = gather_planes(planes, dst=0, host=True)
+    t_rank0 = max_over_ranks(time.perf_counter() - t0)
+    st = stats()
+    if rank == 0:
+        assert sorted(merged) == list(range(n_units)), "gather lost or duplicated units"
+        per_unit = sum(t.nbytes for t in merged[0])
+        total_units = n_units * reps
+        print(json.dumps({
+            "metric": METRIC, "value": total_units / (ms / 1e3), "unit": UNIT, "n_gpus": world,
+            "steps": total_units, "warmup": args.warmup, "ms_per_step": ms / total_units,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic",
+            "config": {"workload": desc, "points": points, "units": n_units, "policy": policy,
+                       "parallelism": f"units x{world} (no collective on the data path)",
+                       "lanes_per_gpu": lanes, "passes_timed": reps},
+            "gather": {"local_units_per_s": n_units / t_local,
+                       "to_rank0_units_per_s": n_units / t_rank0,
+                       "bytes_per_unit": per_unit,
+                       "note": "wall clock of one pass including the device->host copies of "
+                               "every unit's rgb+normal+T f32 planes (local: each rank into its "
+                               "own pinned memory; to_rank0: all planes in rank 0's host "
+                               "memory via NCCL p2p + copies)"},
+            "clocks": clk, "stats": st,
+        }), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
 def main():
     args = parse()
     if args.impl == "reference":
         run_reference(args)
+    elif args.config in ("c4", "c5"):
+        run_units(args)
     else:
         run_ours(args)
 

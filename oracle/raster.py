@@ -147,6 +147,38 @@ def render(splats: dict, cam, mode="rgb", background=(0.0, 0.0, 0.0), tile=16,
     return fb
 
 
+def render_banded(splats: dict, cam, mode="rgb", background=(0.0, 0.0, 0.0), tile=16,
+                  alpha_max=ALPHA_MAX, terminate=True, band_rows=8) -> dict:
+    """The reference render (rasterizer.py:152-166) over the WHOLE frame with
+    bounded memory: _prepare's projection, sort and support radius once, then
+    bin_tiles + forward_kernel per band of ``band_rows`` tile rows (the full
+    random-init config-2 CSR would hold ~1.6e9 int64 ids). Every tile is
+    binned and blended exactly as in one full pass; planes are identical to
+    ``render``. This is the CPU reference arm's timed frame (bench.py)."""
+    prep = prepare(splats, cam, mode, tile, ty_window=(0, 0))
+    w, h = int(cam.width), int(cam.height)
+    ntx, nty = prep["ntx"], prep["nty"]
+    out = np.zeros((h, w, 3))
+    trans = np.ones((h, w))
+    sx, sy, radius = prep["sx"], prep["sy"], prep["radius"]
+    inv = prep["inv"]
+    ia, ib, ic = _c(inv[:, 0]), _c(inv[:, 1]), _c(inv[:, 2])
+    offsets = np.zeros(ntx * nty + 1, dtype=np.int64)
+    for lo in range(0, nty, band_rows):
+        hi = min(nty, lo + band_rows)
+        e = lib().oracle_bin_count(_p(sx), _p(sy), _p(radius), sx.size, tile, ntx, nty, lo, hi,
+                                   0, ntx, _p(offsets))
+        ids = np.empty(e, dtype=np.int64)
+        lib().oracle_bin_fill(_p(sx), _p(sy), _p(radius), sx.size, tile, ntx, nty, lo, hi, 0, ntx,
+                              _p(offsets), _p(ids))
+        lib().oracle_forward(w, h, tile, ntx, nty, lo, hi, _p(offsets), _p(ids), _p(sx), _p(sy),
+                             _p(radius), _p(ia), _p(ib), _p(ic), _p(prep["opac"]),
+                             _p(prep["attr"]), float(alpha_max), int(bool(terminate)), _p(out),
+                             _p(trans))
+        del ids
+    return compose(out, trans, mode, background)
+
+
 def render_stream(splats: dict, cam, modes=("rgb", "normal"), background=(0.0, 0.0, 0.0),
                   tile=16, alpha_max=ALPHA_MAX, terminate=True) -> dict:
     """Full-frame tiled render (rasterizer.py:152-166) of one or two attribute

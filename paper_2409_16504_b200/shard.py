@@ -69,3 +69,58 @@ def gather_results(results: dict):
                 raise RuntimeError(f"unit {k} rendered by two ranks")
             merged[k] = v
     return merged
+
+
+def _dtype(name: str):
+    return getattr(torch, name.split(".")[-1])
+
+
+def _to_host(t: torch.Tensor) -> torch.Tensor:
+    if not t.is_cuda:
+        return t
+    h = torch.empty(t.shape, dtype=t.dtype, pin_memory=True)
+    h.copy_(t, non_blocking=True)
+    return h
+
+
+def gather_planes(frames: dict, dst: int = 0, host: bool = True):
+    """The final gather of a sharded job: ``frames`` maps each unit this rank
+    rendered to a tuple of plane tensors; rank ``dst`` receives every rank's
+    planes point to point over the default process group (NCCL: device
+    tensors over NVLink; gloo: host tensors) and returns {unit: planes} for
+    the whole job, as pinned host tensors when ``host`` (one device->host copy
+    per plane); other ranks return None. Raises if two ranks rendered the
+    same unit."""
+    if not _ready() or dist.get_world_size() == 1:
+        out = {u: tuple(_to_host(t) if host else t for t in ts) for u, ts in frames.items()}
+        if host and torch.cuda.is_available():
+            torch.cuda.synchronize()
+        return out
+    world, rank = dist.get_world_size(), dist.get_rank()
+    meta = {u: [(tuple(t.shape), str(t.dtype)) for t in ts] for u, ts in frames.items()}
+    metas = [None] * world if rank == dst else None
+    dist.gather_object(meta, metas, dst=dst)
+    if rank != dst:
+        reqs = [dist.isend(t.contiguous(), dst) for u in sorted(frames) for t in frames[u]]
+        for r in reqs:
+            r.wait()
+        return None
+    dev = "cuda" if dist.get_backend() == "nccl" else "cpu"
+    out = dict(frames)
+    reqs = []
+    for src in range(world):
+        if src == dst:
+            continue
+        for u in sorted(metas[src]):
+            if u in out:
+                raise RuntimeError(f"unit {u} rendered by two ranks")
+            bufs = tuple(torch.empty(s, dtype=_dtype(d), device=dev) for s, d in metas[src][u])
+            reqs += [dist.irecv(b, src) for b in bufs]
+            out[u] = bufs
+    for r in reqs:
+        r.wait()
+    if host:
+        out = {u: tuple(_to_host(t) for t in ts) for u, ts in out.items()}
+        if dev == "cuda":
+            torch.cuda.synchronize()
+    return out

@@ -120,7 +120,7 @@ def level_parity(dbg: dict, vox_coords: np.ndarray) -> dict:
         ok_set = gc.shape == coords.shape and np.array_equal(np.sort(OV.pack(gc)), keys)
         ok_map = False
         if ok_set:
-            perm = OV.lookup(keys, OV.pack(gc))      # fused row -> canonical row
+            perm = OV.lookup(keys, gc)               # fused row -> canonical row
             ref = OV.kernel_map(coords, keys, stride)   # (m, 27) canonical
             want = ref[perm]                             # canonical neighbour of each fused row
             got = np.where(gm.T >= 0, perm[np.maximum(gm.T, 0)], -1)
@@ -161,33 +161,78 @@ def frame_parity(pc, cloud, weights, view, est=None, gpu_sp=None, levels=True) -
     return rec
 
 
-def explain_pixels(over, got, same, ref, gpu_sp, est, view, limit=8) -> dict:
+def replay_pixel(prep, x, y, alpha_max=OR.ALPHA_MAX, tile=16):
+    """forward_kernel's blend sequence at one pixel (_raster_kernels.py:146-201)
+    from a prepared frame: [(rank, point, alpha, T before)] of every splat that
+    changes the pixel, in rank order, until T < 1/255."""
+    tx, ty = x // tile, y // tile
+    sx, sy, rad = prep["sx"], prep["sy"], prep["radius"]
+    rect = tile_rects(sx, sy, rad, int(prep["ntx"]) * tile, int(prep["nty"]) * tile, tile)
+    r1 = rad + 1.0
+    with np.errstate(invalid="ignore", over="ignore"):
+        hit = ((rect[:, 0] <= tx) & (tx <= rect[:, 1]) & (rect[:, 2] <= ty) & (ty <= rect[:, 3])
+               & (np.ceil(sx - r1) <= x) & (x <= np.floor(sx + r1))
+               & (np.ceil(sy - r1) <= y) & (y <= np.floor(sy + r1)))
+        dx, dy = x - sx, y - sy
+        hit &= ~(dx * dx + dy * dy > r1 * r1)
+    ranks = np.nonzero(hit)[0]
+    inv = prep["inv"]
+    seq, t = [], 1.0
+    for r in ranks.tolist():
+        if t < OR.CUTOFF:
+            break
+        q = inv[r, 0] * dx[r] * dx[r] + 2.0 * inv[r, 1] * dx[r] * dy[r] + inv[r, 2] * dy[r] * dy[r]
+        a = min(prep["opac"][r] * np.exp(-0.5 * q), alpha_max)
+        if a < OR.CUTOFF:
+            continue
+        seq.append((r, int(prep["source"][r]), float(a), t))
+        t *= 1.0 - a
+    return seq
+
+
+def classify(sg, so, p2v, depth_g, depth_o):
+    """First divergence of two blend sequences (GPU Gaussians vs oracle
+    Gaussians through the same oracle renderer)."""
+    for k in range(max(len(sg), len(so))):
+        if k >= len(sg) or k >= len(so):
+            longer, tb = (sg, "gpu") if len(sg) > len(so) else (so, "oracle")
+            return {"step": k, "kind": "T_cutoff", "longer": tb, "T_before": longer[k][3]}
+        (rg, pg, ag, tg), (ro, po, ao, to) = sg[k], so[k]
+        if pg != po:
+            kind = "order"
+            if pg not in [e[1] for e in so] or po not in [e[1] for e in sg]:
+                miss = pg if pg not in [e[1] for e in so] else po
+                a = ag if miss == pg else ao
+                kind = "alpha_cutoff" if a < 2.0 / 255.0 else "order"
+            return {"step": k, "kind": kind, "gpu_point": pg, "oracle_point": po,
+                    "gpu_voxel": int(p2v[pg]), "oracle_voxel": int(p2v[po]),
+                    "depth_gpu": [float(depth_g[pg]), float(depth_g[po])],
+                    "depth_oracle": [float(depth_o[pg]), float(depth_o[po])],
+                    "alpha": [ag, ao], "T_before": [tg, to]}
+        if abs(ag - ao) > 1e-3:
+            return {"step": k, "kind": "alpha", "point": pg, "alpha": [ag, ao]}
+    return {"kind": "none"}
+
+
+def explain_pixels(over, got, same, ref, gpu_sp, est, view, limit=6) -> dict:
     """Attribute end-to-end pixels over 2e-3: renderer (GPU vs oracle on the
     GPU's own Gaussians) or parameters (oracle renderer on GPU vs oracle
-    Gaussians). For a few pixels, the front-most splats whose order differs
-    between the two parameter sets are listed with their depth gap."""
+    Gaussians); for a few pixels, the first divergence of the two blend
+    sequences (order swap / alpha or T crossing the 1/255 cutoff)."""
     ys, xs = np.nonzero(over)
     ren = max(float(np.abs(got[p][ys, xs] - same[p][ys, xs]).max()) for p in PLANES)
     par = max(float(np.abs(same[p][ys, xs] - ref[p][ys, xs]).max()) for p in PLANES)
-    pg = OR.project(gpu_sp["centers"], gpu_sp["quaternions"], gpu_sp["scales"], view)
-    po = OR.project(est["centers"], est["quaternions"], est["scales"], view)
-    samples = []
+    pg, po = same["prep"], ref["prep"]
+    p2v = est["vox"]["point_to_voxel"]
+    dg = np.zeros(len(p2v))
+    dg[pg["source"]] = pg["depth"]
+    do = np.zeros(len(p2v))
+    do[po["source"]] = po["depth"]
+    kinds, samples = {}, []
     for y, x in list(zip(ys.tolist(), xs.tolist()))[:limit]:
-        # splats whose 3-sigma box covers the pixel, in each depth order
-        def covering(pr, op):
-            r = pr["radius"]
-            hit = pr["keep"] & (np.abs(pr["sx"] - x) <= r) & (np.abs(pr["sy"] - y) <= r)
-            idx = np.nonzero(hit)[0]
-            return idx[np.lexsort((idx, pr["depth"][idx]))][:64]
-        a, b = covering(pg, gpu_sp), covering(po, est)
-        k = int(np.argmax(a[: min(a.size, b.size)] != b[: min(a.size, b.size)])) \
-            if a.size and b.size and not np.array_equal(a[:min(a.size, b.size)], b[:min(a.size, b.size)]) else -1
-        item = {"y": y, "x": x, "first_order_difference": k}
-        if k >= 0:
-            i, j = int(a[k]), int(b[k])
-            item.update({"gpu_point": i, "oracle_point": j,
-                         "depth_gap_gpu": float(pg["depth"][j] - pg["depth"][i]),
-                         "depth_gap_oracle": float(po["depth"][i] - po["depth"][j])})
-        samples.append(item)
+        c = classify(replay_pixel(pg, x, y), replay_pixel(po, x, y), p2v, dg, do)
+        c.update(y=y, x=x)
+        kinds[c["kind"]] = kinds.get(c["kind"], 0) + 1
+        samples.append(c)
     return {"count": int(over.sum()), "renderer_max_abs_there": ren,
-            "parameter_effect_max_abs_there": par, "samples": samples}
+            "parameter_effect_max_abs_there": par, "kinds_of_sampled": kinds, "samples": samples}

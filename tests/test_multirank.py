@@ -1,9 +1,11 @@
-"""The N>1 path on CPU: two gloo ranks shard the views of a scene and the
-frames of a sequence (paper_2409_16504_b200.shard, as bench.py does under
-torchrun), render their units independently and gather to rank 0; the merged
-result must equal a serial run and cover every unit exactly once. The
-renderer here is the CPU oracle standing in for a GPU (no data-path
-collective exists, so the host logic is what differs between N=1 and N>1)."""
+"""The N>1 path on CPU: two gloo ranks run bench.py's sharded job
+(bench.sharded_job -> paper_2409_16504_b200.shard.gather_planes, exactly the
+code bench.py runs under torchrun for configs 4 and 5) and the view sharding
+of config 2 (shard + max_over_ranks + gather_results). The per-unit renderer
+is a CPU function here (the oracle's render of a small scene): no data-path
+collective exists, so the sharding, the gather of every unit's planes to
+rank 0 and the max-over-ranks timing are what differ between N=1 and N>1.
+The merged result must equal a serial run and cover every unit exactly once."""
 import hashlib
 import os
 import socket
@@ -90,3 +92,49 @@ def test_two_gloo_ranks_match_serial(tmp_path, policy):
     est, views = _scene()
     serial = sorted((u, _render_digest(est, v)) for u, v in enumerate(views))
     assert merged == serial                          # every view once, identical planes
+
+
+def _planes(est, view):
+    from oracle import raster as OR
+    import torch
+    fb = OR.render_stream(est, view, ("rgb", "normal"))
+    return tuple(torch.from_numpy(np.ascontiguousarray(fb[k], dtype=np.float32))
+                 for k in ("rgb", "normal", "transmittance"))
+
+
+def _bench_worker(rank, world, port, policy, out_dir):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import bench
+        from paper_2409_16504_b200.shard import gather_planes
+        est, views = _scene()
+        planes = bench.sharded_job(len(views), policy, lambda u, lane: _planes(est, views[u]),
+                                   rank, world, lanes=2)
+        merged = gather_planes(planes, dst=0, host=True)
+        t = max_over_ranks(float(10 - rank))
+        if rank == 0:
+            import torch
+            torch.save({"t": t, "planes": merged, "mine": sorted(planes)},
+                       Path(out_dir, f"bench_{policy}.pt"))
+        else:
+            assert merged is None
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("policy", ["round_robin", "block"])
+def test_bench_sharded_job_gathers_every_unit(tmp_path, policy):
+    import torch
+    world = 2
+    mp.spawn(_bench_worker, args=(world, _free_port(), policy, str(tmp_path)), nprocs=world,
+             join=True)
+    got = torch.load(Path(tmp_path, f"bench_{policy}.pt"))
+    assert got["t"] == 10.0
+    assert got["mine"] == shard(6, 0, world, policy)
+    est, views = _scene()
+    assert sorted(got["planes"]) == list(range(len(views)))
+    for u, v in enumerate(views):
+        want = _planes(est, v)
+        for a, b in zip(got["planes"][u], want):
+            assert torch.equal(a, b), u
