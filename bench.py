@@ -587,7 +587,9 @@ def run_units(args):
         points = len(c)
         desc = (f"c5: 2048^3 terrain + 50 boxes ({points} pts, scenes.config5), 32 views at "
                 f"1920x1080 round-robin over ranks, P2ENet + splat per view")
-    lanes = max(1, min(args.lanes, len(mine) or 1))
+    # c5 frames are ~20x larger (5.6 M points): fewer frames in flight already
+    # overlap, and each lane's scratch arena is sized for the whole cloud
+    lanes = max(1, min(args.lanes if args.config == "c4" else min(args.lanes, 2), len(mine) or 1))
     streams = [torch.cuda.Stream() for _ in range(lanes)]
     downs = [torch.cuda.Stream() for _ in range(lanes)]
     outs = {}
@@ -598,6 +600,13 @@ def run_units(args):
                    None, torch.empty((H, W), dtype=torch.float32, device="cuda"))
     host = {u: tuple(torch.empty(t.shape, dtype=t.dtype).pin_memory()
                      for t in (outs[u][0], outs[u][1], outs[u][3])) for u in mine}
+    # rank 0's pinned destination of every unit's planes for the gather
+    shape_of = {u: (cams[u].height, cams[u].width) for u in mine}
+    ref_hw = next(iter(shape_of.values()))
+    gather_out = ({u: (torch.empty(ref_hw + (3,), dtype=torch.float32).pin_memory(),
+                       torch.empty(ref_hw + (3,), dtype=torch.float32).pin_memory(),
+                       torch.empty(ref_hw, dtype=torch.float32).pin_memory())
+                   for u in range(n_units)} if rank == 0 else None)
 
     def render_unit(u, lane):
         with torch.cuda.stream(streams[lane]):
@@ -652,7 +661,7 @@ def run_units(args):
     barrier()
     t0 = time.perf_counter()
     planes = job()
-    merged = gather_planes(planes, dst=0, host=True)
+    merged = gather_planes(planes, dst=0, host=True, out=gather_out)
     t_rank0 = max_over_ranks(time.perf_counter() - t0)
     st = stats()
     if rank == 0:

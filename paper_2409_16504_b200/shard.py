@@ -83,19 +83,27 @@ def _to_host(t: torch.Tensor) -> torch.Tensor:
     return h
 
 
-def gather_planes(frames: dict, dst: int = 0, host: bool = True):
+def gather_planes(frames: dict, dst: int = 0, host: bool = True, out: dict = None):
     """The final gather of a sharded job: ``frames`` maps each unit this rank
     rendered to a tuple of plane tensors; rank ``dst`` receives every rank's
     planes point to point over the default process group (NCCL: device
     tensors over NVLink; gloo: host tensors) and returns {unit: planes} for
     the whole job, as pinned host tensors when ``host`` (one device->host copy
     per plane); other ranks return None. Raises if two ranks rendered the
-    same unit."""
+    same unit. ``out`` (rank dst): preallocated pinned host tensors per unit
+    to copy into instead of fresh allocations."""
+    def to_host(u, ts):
+        if out is not None and u in out:
+            for h, t in zip(out[u], ts):
+                h.copy_(t, non_blocking=True)
+            return out[u]
+        return tuple(_to_host(t) for t in ts)
+
     if not _ready() or dist.get_world_size() == 1:
-        out = {u: tuple(_to_host(t) if host else t for t in ts) for u, ts in frames.items()}
+        res = {u: (to_host(u, ts) if host else ts) for u, ts in frames.items()}
         if host and torch.cuda.is_available():
             torch.cuda.synchronize()
-        return out
+        return res
     world, rank = dist.get_world_size(), dist.get_rank()
     meta = {u: [(tuple(t.shape), str(t.dtype)) for t in ts] for u, ts in frames.items()}
     metas = [None] * world if rank == dst else None
@@ -106,21 +114,21 @@ def gather_planes(frames: dict, dst: int = 0, host: bool = True):
             r.wait()
         return None
     dev = "cuda" if dist.get_backend() == "nccl" else "cpu"
-    out = dict(frames)
+    got = dict(frames)
     reqs = []
     for src in range(world):
         if src == dst:
             continue
         for u in sorted(metas[src]):
-            if u in out:
+            if u in got:
                 raise RuntimeError(f"unit {u} rendered by two ranks")
             bufs = tuple(torch.empty(s, dtype=_dtype(d), device=dev) for s, d in metas[src][u])
             reqs += [dist.irecv(b, src) for b in bufs]
-            out[u] = bufs
+            got[u] = bufs
     for r in reqs:
         r.wait()
     if host:
-        out = {u: tuple(_to_host(t) for t in ts) for u, ts in out.items()}
+        got = {u: to_host(u, ts) for u, ts in got.items()}
         if dev == "cuda":
             torch.cuda.synchronize()
-    return out
+    return got

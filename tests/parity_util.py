@@ -190,35 +190,62 @@ def replay_pixel(prep, x, y, alpha_max=OR.ALPHA_MAX, tile=16):
     return seq
 
 
-def classify(sg, so, p2v, depth_g, depth_o):
-    """First divergence of two blend sequences (GPU Gaussians vs oracle
-    Gaussians through the same oracle renderer)."""
+def classify(sg, so, p2v, depth_g, depth_o, alpha_of):
+    """First divergence of two blend sequences at one pixel (GPU Gaussians vs
+    oracle Gaussians, both through the oracle renderer). ``alpha_of(set,
+    point)`` gives a point's alpha at the pixel under either parameter set.
+    kinds: ``alpha_cutoff`` — a splat (with its whole run: a voxel's points
+    share alpha) has alpha >= 1/255 under one set and < 1/255 under the other;
+    ``T_cutoff`` — T crosses 1/255 one splat earlier under one set; ``order``
+    — two splats blend in a different order; ``alpha`` — same splat, alphas
+    differ by more than 1e-3."""
+    c = OR.CUTOFF
     for k in range(max(len(sg), len(so))):
         if k >= len(sg) or k >= len(so):
-            longer, tb = (sg, "gpu") if len(sg) > len(so) else (so, "oracle")
-            return {"step": k, "kind": "T_cutoff", "longer": tb, "T_before": longer[k][3]}
+            longer = "gpu" if len(sg) > len(so) else "oracle"
+            short = so if longer == "gpu" else sg
+            t_short = short[-1][3] * (1.0 - short[-1][2]) if short else 1.0
+            t_long = (sg if longer == "gpu" else so)[k][3]
+            return {"step": k, "kind": "T_cutoff", "longer": longer,
+                    "T_gpu": t_long if longer == "gpu" else t_short,
+                    "T_oracle": t_short if longer == "gpu" else t_long,
+                    "straddle": bool(min(t_long, t_short) < c <= max(t_long, t_short)),
+                    "rel_gap": abs(t_long - t_short) / c}
         (rg, pg, ag, tg), (ro, po, ao, to) = sg[k], so[k]
         if pg != po:
-            kind = "order"
-            if pg not in [e[1] for e in so] or po not in [e[1] for e in sg]:
-                miss = pg if pg not in [e[1] for e in so] else po
-                a = ag if miss == pg else ao
-                kind = "alpha_cutoff" if a < 2.0 / 255.0 else "order"
-            return {"step": k, "kind": kind, "gpu_point": pg, "oracle_point": po,
+            in_o = {e[1] for e in so}
+            in_g = {e[1] for e in sg}
+            if pg not in in_o or po not in in_g:
+                miss = pg if pg not in in_o else po
+                a_g, a_o = alpha_of("gpu", miss), alpha_of("oracle", miss)
+                return {"step": k, "kind": "alpha_cutoff", "point": miss, "voxel": int(p2v[miss]),
+                        "alpha_gpu": a_g, "alpha_oracle": a_o,
+                        "straddle": bool(min(a_g, a_o) < c <= max(a_g, a_o)),
+                        "rel_gap": abs(a_g - a_o) / c}
+            return {"step": k, "kind": "order", "gpu_point": pg, "oracle_point": po,
                     "gpu_voxel": int(p2v[pg]), "oracle_voxel": int(p2v[po]),
                     "depth_gpu": [float(depth_g[pg]), float(depth_g[po])],
-                    "depth_oracle": [float(depth_o[pg]), float(depth_o[po])],
-                    "alpha": [ag, ao], "T_before": [tg, to]}
+                    "depth_oracle": [float(depth_o[pg]), float(depth_o[po])]}
         if abs(ag - ao) > 1e-3:
             return {"step": k, "kind": "alpha", "point": pg, "alpha": [ag, ao]}
     return {"kind": "none"}
 
 
-def explain_pixels(over, got, same, ref, gpu_sp, est, view, limit=6) -> dict:
+def _alpha_at(prep, rank_of, point, x, y, alpha_max=OR.ALPHA_MAX):
+    r = rank_of.get(point)
+    if r is None:
+        return 0.0
+    dx, dy = x - prep["sx"][r], y - prep["sy"][r]
+    inv = prep["inv"][r]
+    q = inv[0] * dx * dx + 2.0 * inv[1] * dx * dy + inv[2] * dy * dy
+    return float(min(prep["opac"][r] * np.exp(-0.5 * q), alpha_max))
+
+
+def explain_pixels(over, got, same, ref, gpu_sp, est, view, limit=200) -> dict:
     """Attribute end-to-end pixels over 2e-3: renderer (GPU vs oracle on the
     GPU's own Gaussians) or parameters (oracle renderer on GPU vs oracle
-    Gaussians); for a few pixels, the first divergence of the two blend
-    sequences (order swap / alpha or T crossing the 1/255 cutoff)."""
+    Gaussians), and for each pixel (up to ``limit``) the first divergence of
+    the two blend sequences (``classify``)."""
     ys, xs = np.nonzero(over)
     ren = max(float(np.abs(got[p][ys, xs] - same[p][ys, xs]).max()) for p in PLANES)
     par = max(float(np.abs(same[p][ys, xs] - ref[p][ys, xs]).max()) for p in PLANES)
@@ -228,11 +255,21 @@ def explain_pixels(over, got, same, ref, gpu_sp, est, view, limit=6) -> dict:
     dg[pg["source"]] = pg["depth"]
     do = np.zeros(len(p2v))
     do[po["source"]] = po["depth"]
+    rank_g = {int(p): r for r, p in enumerate(pg["source"])} if over.sum() else {}
+    rank_o = {int(p): r for r, p in enumerate(po["source"])} if over.sum() else {}
     kinds, samples = {}, []
     for y, x in list(zip(ys.tolist(), xs.tolist()))[:limit]:
-        c = classify(replay_pixel(pg, x, y), replay_pixel(po, x, y), p2v, dg, do)
+        def alpha_of(which, point):
+            return _alpha_at(pg if which == "gpu" else po, rank_g if which == "gpu" else rank_o,
+                             point, x, y)
+        c = classify(replay_pixel(pg, x, y), replay_pixel(po, x, y), p2v, dg, do, alpha_of)
         c.update(y=y, x=x)
         kinds[c["kind"]] = kinds.get(c["kind"], 0) + 1
         samples.append(c)
     return {"count": int(over.sum()), "renderer_max_abs_there": ren,
-            "parameter_effect_max_abs_there": par, "kinds_of_sampled": kinds, "samples": samples}
+            "parameter_effect_max_abs_there": par, "kinds": kinds,
+            "all_threshold_crossings": all(c["kind"] in ("alpha_cutoff", "T_cutoff")
+                                           and c["straddle"] and c["rel_gap"] < 1e-3
+                                           for c in samples),
+            "max_rel_gap": max((c.get("rel_gap", 0.0) for c in samples), default=0.0),
+            "samples": samples}
