@@ -59,7 +59,8 @@ def parse():
     ap.add_argument("--cpu-frames", type=int, default=1,
                     help="full config-2 frames of the CPU port timed for cpu_baseline")
     ap.add_argument("--lanes", type=int, default=8, help="frames in flight per GPU (streams)")
-    ap.add_argument("--net-mode", choices=("tc_tf32x3", "tc_bf16", "simt_f32"), default="tc_tf32x3",
+    ap.add_argument("--net-mode", choices=("tc_tf32x3", "tc_bf16", "simt_f32", "simt_f64"),
+                    default="tc_tf32x3",
                     help="P2ENet arithmetic (tc_tf32x3: fp32-accurate parity mode)")
     return ap.parse_args()
 
@@ -509,7 +510,8 @@ def run_ours(args):
                               "streams; latency: 256 MB L2 flush between frames"),
                        "net_arithmetic": {"tc_tf32x3": "tcgen05 tf32 hi/lo split (fp32-accurate)",
                                           "tc_bf16": "tcgen05 bf16 operands, fp32 accumulation",
-                                          "simt_f32": "fp32 FFMA"}[args.net_mode]
+                                          "simt_f32": "fp32 FFMA",
+                                          "simt_f64": "fp64 SIMT (reference arithmetic)"}[args.net_mode]
                                          + " convs; fp64 geometry / compositing"},
             "latency_ms_per_frame": lat_ms,
             "e2e": e2e, "gpu_launches": launches, "roofline": roof, "cpu_baseline": cpu,

@@ -38,7 +38,11 @@ enum { SFB_PLANE_RGB = 1, SFB_PLANE_NORMAL = 2, SFB_PLANE_DEPTH = 4 };
  * (fp32-accurate, the default and the parity mode); tcgen05 single bf16
  * operands with fp32 accumulation (the north star's fast mode; does not meet
  * the 1e-3 Gaussian-parameter bound). */
-enum { SFB_NET_SIMT_F32 = 0, SFB_NET_TC_TF32X3 = 1, SFB_NET_TC_BF16 = 2 };
+enum { SFB_NET_SIMT_F32 = 0, SFB_NET_TC_TF32X3 = 1, SFB_NET_TC_BF16 = 2, SFB_NET_SIMT_F64 = 3 };
+/* SFB_NET_SIMT_F64: float64 features with float32 weights upcast, the
+ * reference network's own arithmetic (sparsenet.py:207-210), on the FP64
+ * pipe — the end-to-end exactness mode (parameters ~1e-13 from the
+ * reference instead of ~1e-6). */
 
 typedef struct sfb_ctx sfb_ctx;
 
@@ -170,9 +174,10 @@ int sfb_sparse_conv(sfb_ctx *ctx, int layer, const int32_t *coords, const float 
 int sfb_transposed_conv(sfb_ctx *ctx, int layer, const int32_t *parent_coords,
                         const float *parent_feats, int64_t m_parent, int32_t parent_stride,
                         const int32_t *targets, int64_t m_targets, int relu, float *out);
-/* Full UNet + head on a voxelized cloud: raw (m0,14) float32 per voxel. */
+/* Full UNet + head on a voxelized cloud: raw (m0,14) per voxel, float32 —
+ * float64 when the network mode is SFB_NET_SIMT_F64. */
 int sfb_unet_forward(sfb_ctx *ctx, const int32_t *coords, const double *feats9, int64_t m0,
-                     float *raw_out);
+                     void *raw_out);
 /* activate_head per row (sparsenet.py:310-341): float64 raw in, float64 out. */
 int sfb_activate_head(sfb_ctx *ctx, const double *raw, int64_t m, double voxel_scale,
                       double *delta, double *sigma, double *quat, double *opacity,

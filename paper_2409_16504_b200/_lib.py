@@ -17,7 +17,7 @@ LIB_PATH = Path(os.environ.get("SFB_LIB_PATH", PKG / "_build" / "libsfb200.so"))
 
 SFB_OK, SFB_ERR_ARG, SFB_ERR_OOM, SFB_ERR_CUDA, SFB_ERR_STATE = 0, 1, 2, 3, 4
 PLANE_RGB, PLANE_NORMAL, PLANE_DEPTH = 1, 2, 4
-NET_SIMT_F32, NET_TC_TF32X3, NET_TC_BF16 = 0, 1, 2
+NET_SIMT_F32, NET_TC_TF32X3, NET_TC_BF16, NET_SIMT_F64 = 0, 1, 2, 3
 STAGES = {1: "voxelize", 2: "unet", 3: "head", 4: "project", 5: "sort", 6: "bin",
           7: "composite"}
 

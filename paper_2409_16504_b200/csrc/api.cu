@@ -129,7 +129,7 @@ VoxelSplats neural_voxels(sfb_ctx *ctx, const double *pos, const double *col, in
     o.offsets = ctx->arena.alloc<int32_t>(n + 1);
     voxelize_run(ctx, pos, col, n, host, P, o, C);
     ctx->mark(ST_VOXELIZE);
-    float *raw = ctx->arena.alloc<float>(14 * n);
+    void *raw = ctx->arena.alloc<double>(14 * n);   // float32 rows, or float64 (SIMT_F64)
     unet_run(ctx, o.coords, o.feats, n, host, P, C, raw);
     ctx->mark(ST_UNET);
     double *blk = ctx->arena.alloc<double>(14 * n);
@@ -442,7 +442,8 @@ int sfb_net_load(sfb_ctx *ctx, const void *blob, size_t nbytes) {
 }
 
 int sfb_net_set_mode(sfb_ctx *ctx, int mode) {
-    if (!ctx || (mode != SFB_NET_SIMT_F32 && mode != SFB_NET_TC_TF32X3 && mode != SFB_NET_TC_BF16))
+    if (!ctx || (mode != SFB_NET_SIMT_F32 && mode != SFB_NET_TC_TF32X3 && mode != SFB_NET_TC_BF16 &&
+                 mode != SFB_NET_SIMT_F64))
         return SFB_ERR_ARG;
     ctx->net_mode = mode;
     return SFB_OK;
@@ -492,7 +493,7 @@ int sfb_transposed_conv(sfb_ctx *ctx, int layer, const int32_t *parent_coords,
 }
 
 int sfb_unet_forward(sfb_ctx *ctx, const int32_t *coords, const double *feats9, int64_t m0,
-                     float *raw_out) {
+                     void *raw_out) {
     return guard(ctx, [&] {
         SFB_REQUIRE(m0 > 0, "empty voxel grid");
         FrameParams host{};

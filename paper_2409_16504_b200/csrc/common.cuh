@@ -377,8 +377,9 @@ void voxelize_run(sfb_ctx *ctx, const double *pos, const double *col, int64_t n,
 // net.cu
 void net_load(sfb_ctx *ctx, const void *blob, size_t n);
 // per-voxel raw head (M0 x 14) float32 into `raw`; M0 = C->m[0] (device), bound m_bound
+// raw: float32, or float64 in SFB_NET_SIMT_F64 mode
 void unet_run(sfb_ctx *ctx, const int32_t *coords, const double *feats9, int64_t m_bound,
-              const FrameParams &host, const FrameParams *P, DevCounts *C, float *raw);
+              const FrameParams &host, const FrameParams *P, DevCounts *C, void *raw);
 void activate_run(sfb_ctx *ctx, const double *raw, int64_t m, double scale, double *delta,
                   double *sigma, double *quat, double *opac, double *normal);
 void conv_layer(sfb_ctx *ctx, const NetLayer &L, const float *in, int ld_in, const int32_t *nbr,
@@ -392,7 +393,7 @@ void tconv_layer(sfb_ctx *ctx, const NetLayer &L, const float *in, int ld_in,
 void layer_set(sfb_ctx *ctx, int kind, int kernel, int cin, int cout, const float *w_host,
                const float *b_host);
 // per-voxel Gaussians for the fused frame: centres, sigma, quat, opacity, normal
-void head_to_voxel_splats(sfb_ctx *ctx, const float *raw, const int32_t *coords,
+void head_to_voxel_splats(sfb_ctx *ctx, const void *raw, const int32_t *coords,
                           const double *feats9, const int64_t *d_m, int64_t m_bound,
                           const FrameParams *P, double *centers, double *sigma, double *quat,
                           double *opac, double *normal);

@@ -546,7 +546,8 @@ void activate_run(sfb_ctx *ctx, const double *raw, int64_t m, double scale, doub
 
 // Per-voxel Gaussian: centre = (coord + 0.5 + residual) * scale + delta
 // (voxelgrid.py:119-122 + estimators.py:223), then the activated fields.
-__global__ void k_voxel_splats(const float *__restrict__ raw, const int32_t *__restrict__ coords,
+template <class R>
+__global__ void k_voxel_splats(const R *__restrict__ raw, const int32_t *__restrict__ coords,
                                const double *__restrict__ feats9, const int64_t *__restrict__ d_m,
                                const FrameParams *__restrict__ P, double *centers, double *sigma,
                                double *quat, double *opac, double *normal) {
@@ -564,12 +565,177 @@ __global__ void k_voxel_splats(const float *__restrict__ raw, const int32_t *__r
     }
 }
 
-void head_to_voxel_splats(sfb_ctx *ctx, const float *raw, const int32_t *coords,
+void head_to_voxel_splats(sfb_ctx *ctx, const void *raw, const int32_t *coords,
                           const double *feats9, const int64_t *d_m, int64_t m_bound,
                           const FrameParams *P, double *centers, double *sigma, double *quat,
                           double *opac, double *normal) {
-    k_voxel_splats<<<dgrid(m_bound, 128), 128, 0, ctx->stream>>>(raw, coords, feats9, d_m, P,
-                                                                 centers, sigma, quat, opac, normal);
+    if (ctx->net_mode == SFB_NET_SIMT_F64)
+        k_voxel_splats<double><<<dgrid(m_bound, 128), 128, 0, ctx->stream>>>(
+            static_cast<const double *>(raw), coords, feats9, d_m, P, centers, sigma, quat, opac, normal);
+    else
+        k_voxel_splats<float><<<dgrid(m_bound, 128), 128, 0, ctx->stream>>>(
+            static_cast<const float *>(raw), coords, feats9, d_m, P, centers, sigma, quat, opac, normal);
+    SFB_CHECK_LAUNCH();
+}
+
+// ------------------------------------------------------------ float64 network
+// SFB_NET_SIMT_F64: the reference network's own arithmetic — float64
+// features, float32 weights upcast (sparsenet.py:207-210, 245, 285-286) — on
+// the FP64 pipe. The parity mode of the end-to-end image check: the Gaussian
+// parameters then agree with the reference to ~1e-13 instead of the ~1e-6 of
+// the fp32-accurate tensor-core path, so no (splat, pixel) alpha or
+// transmittance lands on the other side of a 1/255 cutoff. Same structure
+// (kernel maps, pooling, buckets) as the fp32 path; only the feature kernels
+// differ.
+constexpr int kRowsD = 32;
+
+// CTA = 32 output rows x all output channels; per tap the 32 gathered input
+// rows (float64) and the tap's weights (float32) sit in shared memory, every
+// thread accumulates its outputs over the tap's input channels
+__global__ void __launch_bounds__(kThreads)
+k_conv_f64(const double *__restrict__ in, int ld_in, const int32_t *__restrict__ nbr, int64_t nbr_ld,
+           const int64_t *__restrict__ d_m, int taps, int cin, int cout, const float *__restrict__ w,
+           const float *__restrict__ b, int relu, double *__restrict__ out, int ld_out) {
+    extern __shared__ __align__(16) unsigned char sm_raw[];
+    double *A = reinterpret_cast<double *>(sm_raw);            // [kRowsD][cin]
+    float *W = reinterpret_cast<float *>(A + kRowsD * cin);    // [cin][cout]
+    const int64_t m = *d_m;
+    const int nout = kRowsD * cout;
+    for (int64_t r0 = (int64_t)blockIdx.x * kRowsD; r0 < m; r0 += (int64_t)gridDim.x * kRowsD) {
+        double acc[kMaxOut];
+#pragma unroll
+        for (int k = 0; k < kMaxOut; ++k) acc[k] = 0.0;
+        for (int t = 0; t < taps; ++t) {
+            int any = 0;
+            for (int i = threadIdx.x; i < kRowsD * cin; i += kThreads) {
+                const int r = i / cin, ci = i % cin;
+                const int64_t row = r0 + r;
+                const int32_t src = row < m ? nbr[(int64_t)t * nbr_ld + row] : -1;
+                any |= src >= 0;
+                A[i] = src >= 0 ? in[(int64_t)src * ld_in + ci] : 0.0;
+            }
+            if (!__syncthreads_or(any)) continue;
+            const float *wt = w + (size_t)t * cin * cout;
+            for (int i = threadIdx.x; i < cin * cout; i += kThreads) W[i] = wt[i];
+            __syncthreads();
+#pragma unroll
+            for (int k = 0; k < kMaxOut; ++k) {
+                const int o = threadIdx.x + k * kThreads;
+                if (o < nout) {
+                    const int r = o / cout, co = o % cout;
+                    double sacc = 0.0;
+                    for (int ci = 0; ci < cin; ++ci) sacc = fma(A[r * cin + ci], (double)W[ci * cout + co], sacc);
+                    acc[k] += sacc;   // x_t @ W_t, then accumulated in tap order
+                }
+            }
+            __syncthreads();
+        }
+#pragma unroll
+        for (int k = 0; k < kMaxOut; ++k) {
+            const int o = threadIdx.x + k * kThreads;
+            if (o < nout) {
+                const int r = o / cout, co = o % cout;
+                const int64_t row = r0 + r;
+                if (row < m) {
+                    const double v = (double)b[co] + acc[k];
+                    out[row * ld_out + co] = relu ? fmax(v, 0.0) : v;
+                }
+            }
+        }
+        __syncthreads();
+    }
+}
+
+// transposed conv: out[r] = b + in[parent[r]] @ W[tap[r]] (orphans: bias only)
+__global__ void k_tconv_f64(const double *__restrict__ in, int ld_in, const int32_t *__restrict__ parent,
+                            const int32_t *__restrict__ tap, const int64_t *__restrict__ d_m, int cin,
+                            int cout, const float *__restrict__ w, const float *__restrict__ b, int relu,
+                            double *__restrict__ out, int ld_out) {
+    const int64_t m = *d_m;
+    SFB_FOR(idx, m * cout) {
+        const int64_t r = idx / cout;
+        const int co = (int)(idx % cout);
+        const int32_t p = parent[r];
+        double s = 0.0;
+        if (p >= 0) {
+            const double *x = in + (int64_t)p * ld_in;
+            const float *wt = w + (size_t)tap[r] * cin * cout + co;
+            for (int ci = 0; ci < cin; ++ci) s = fma(x[ci], (double)wt[(size_t)ci * cout], s);
+        }
+        const double v = (double)b[co] + s;
+        out[r * ld_out + co] = relu ? fmax(v, 0.0) : v;
+    }
+}
+
+// pool_2x2x2 means: children summed in child-row order (np.add.at)
+__global__ void k_pool_means_f64(const double *__restrict__ feats, int ld_in, int c,
+                                 const int32_t *__restrict__ nkids, const int32_t *__restrict__ kids,
+                                 const int64_t *__restrict__ d_mp, double *__restrict__ out, int ld_out) {
+    const int64_t mp = *d_mp;
+    SFB_FOR(idx, mp * c) {
+        const int64_t v = idx / c;
+        const int ch = (int)(idx % c);
+        const int cnt = min(nkids[v], 8);
+        int32_t kk[8];
+        for (int q = 0; q < cnt; ++q) kk[q] = kids[8 * v + q];
+        for (int q = 1; q < cnt; ++q) {   // ascending child rows
+            const int32_t x = kk[q];
+            int r = q - 1;
+            while (r >= 0 && kk[r] > x) {
+                kk[r + 1] = kk[r];
+                --r;
+            }
+            kk[r + 1] = x;
+        }
+        double acc = 0.0;
+        for (int q = 0; q < cnt; ++q) acc += feats[(int64_t)kk[q] * ld_in + ch];
+        out[v * ld_out + ch] = acc / (double)cnt;
+    }
+}
+
+// head MLP relu(f @ W1 + b1) @ W2 + b2 (sparsenet.py:284-286), 32 rows per CTA
+__global__ void k_head_f64(const double *__restrict__ f, int ld, const int64_t *__restrict__ d_m,
+                           int cin, int hid, const float *__restrict__ w1, const float *__restrict__ b1,
+                           const float *__restrict__ w2, const float *__restrict__ b2,
+                           double *__restrict__ raw) {
+    extern __shared__ __align__(16) unsigned char sm_raw[];
+    double *F = reinterpret_cast<double *>(sm_raw);   // [rows][cin]
+    double *H = F + kHeadRows * cin;                   // [rows][hid]
+    const int64_t m = *d_m;
+    for (int64_t r0 = (int64_t)blockIdx.x * kHeadRows; r0 < m; r0 += (int64_t)gridDim.x * kHeadRows) {
+        __syncthreads();
+        for (int i = threadIdx.x; i < kHeadRows * cin; i += blockDim.x) {
+            const int64_t row = r0 + i / cin;
+            F[i] = row < m ? f[row * ld + i % cin] : 0.0;
+        }
+        __syncthreads();
+        for (int i = threadIdx.x; i < kHeadRows * hid; i += blockDim.x) {
+            const int r = i / hid, j = i % hid;
+            double sacc = 0.0;
+            for (int c = 0; c < cin; ++c) sacc = fma(F[r * cin + c], (double)w1[c * hid + j], sacc);
+            H[i] = fmax(sacc + (double)b1[j], 0.0);
+        }
+        __syncthreads();
+        for (int i = threadIdx.x; i < kHeadRows * 14; i += blockDim.x) {
+            const int r = i / 14, k = i % 14;
+            const int64_t row = r0 + r;
+            if (row >= m) continue;
+            double sacc = 0.0;
+            for (int c = 0; c < hid; ++c) sacc = fma(H[r * hid + c], (double)w2[c * 14 + k], sacc);
+            raw[row * 14 + k] = sacc + (double)b2[k];
+        }
+    }
+}
+
+static void conv_f64(sfb_ctx *ctx, const NetLayer &L, const double *in, int ld_in,
+                     const int32_t *nbr, int64_t nbr_ld, const int64_t *d_m, int64_t m_grid,
+                     double *out, int ld_out) {
+    SFB_REQUIRE(kRowsD * L.cout <= kMaxOut * kThreads, "conv: cout > 128 unsupported");
+    const size_t smem = sizeof(double) * kRowsD * L.cin + sizeof(float) * L.cin * L.cout;
+    SFB_REQUIRE(smem <= 200 * 1024, "conv: channels too wide for one CTA");
+    set_max_dyn_smem(reinterpret_cast<const void *>(k_conv_f64), 200 * 1024);
+    k_conv_f64<<<dgrid(m_grid, kRowsD, 4), kThreads, smem, ctx->stream>>>(
+        in, ld_in, nbr, nbr_ld, d_m, L.taps, L.cin, L.cout, L.w, L.b, 1, out, ld_out);
     SFB_CHECK_LAUNCH();
 }
 
@@ -595,7 +761,7 @@ constexpr int kLevelSplit[4] = {1, 1, 4, 8};
 constexpr int kTconvSplit = 8;
 
 void unet_run(sfb_ctx *ctx, const int32_t *coords0, const double *feats9, int64_t mb,
-              const FrameParams &host, const FrameParams *P, DevCounts *C, float *raw) {
+              const FrameParams &host, const FrameParams *P, DevCounts *C, void *raw_out) {
     Net &net = ctx->net;
     SFB_REQUIRE(net.loaded, "network weights are not loaded");
     const int L = net.levels;
@@ -646,6 +812,62 @@ void unet_run(sfb_ctx *ctx, const int32_t *coords0, const double *feats9, int64_
         throw;
     }
     ctx->stream = st;
+    auto export_debug = [&]() {   // parity export (eager frames only)
+        const FrameDebug &D = ctx->frame_debug;
+        if (!(D.cap > 0 && D.level_coords && D.level_maps)) return;
+        SFB_REQUIRE(mb <= D.cap, "frame debug buffers are smaller than the cloud");
+        for (int l = 0; l <= L && l < D.levels; ++l) {
+            const int taps = kern[l] * kern[l] * kern[l];
+            SFB_REQUIRE(taps <= 27, "frame debug export holds up to 27 taps per level");
+            SFB_CUDA(cudaMemcpyAsync(D.level_coords + (size_t)l * 3 * D.cap, coords[l],
+                                     sizeof(int32_t) * 3 * mb, cudaMemcpyDeviceToDevice, st));
+            for (int t = 0; t < taps; ++t)
+                SFB_CUDA(cudaMemcpyAsync(D.level_maps + ((size_t)l * 27 + t) * D.cap,
+                                         nbr[l] + (size_t)t * mb, sizeof(int32_t) * mb,
+                                         cudaMemcpyDeviceToDevice, st));
+        }
+    };
+    if (ctx->net_mode == SFB_NET_SIMT_F64) {   // float64 features end to end
+        double *raw = static_cast<double *>(raw_out);
+        std::vector<double *> catd(L), pind(L + 1);
+        int layer = 0;
+        for (int l = 0; l < L; ++l) {
+            catd[l] = ctx->arena.alloc<double>((size_t)mb * width[l]);
+            const int up = dec[L - 1 - l];
+            conv_f64(ctx, net.layers[layer++], l ? pind[l] : feats9, l ? enc[l] : 9, nbr[l], mb,
+                     &C->m[l], mg[l], catd[l] + up, width[l]);
+            pind[l + 1] = ctx->arena.alloc<double>((size_t)mb * enc[l + 1]);
+            SFB_CUDA(cudaStreamWaitEvent(st, ctx->side_ev[l], 0));   // level l+1 structure ready
+            k_pool_means_f64<<<dgrid(mg[l + 1] * enc[l + 1], 256), 256, 0, st>>>(
+                catd[l] + up, width[l], enc[l + 1], ps[l].nkids, ps[l].kids, &C->m[l + 1], pind[l + 1],
+                enc[l + 1]);
+            SFB_CHECK_LAUNCH();
+        }
+        double *bott = ctx->arena.alloc<double>((size_t)mb * enc[L + 1]);
+        conv_f64(ctx, net.layers[layer++], pind[L], enc[L], nbr[L], mb, &C->m[L], mg[L], bott,
+                 enc[L + 1]);
+        const double *coarse = bott;
+        int ld_coarse = enc[L + 1];
+        for (int l = L - 1; l >= 0; --l) {
+            const NetLayer &T = net.layers[layer++];
+            k_tconv_f64<<<dgrid(mg[l] * T.cout, 256), 256, 0, st>>>(
+                coarse, ld_coarse, ps[l].c2p, ps[l].tap, &C->m[l], T.cin, T.cout, T.w, T.b, 1, catd[l],
+                width[l]);
+            SFB_CHECK_LAUNCH();
+            coarse = catd[l];
+            ld_coarse = width[l];
+        }
+        export_debug();
+        const NetLayer &h1 = net.layers[layer], &h2 = net.layers[layer + 1];
+        const size_t smem = sizeof(double) * kHeadRows * (h1.cin + h1.cout);
+        SFB_REQUIRE(smem <= 200 * 1024, "head MLP too wide");
+        set_max_dyn_smem(reinterpret_cast<const void *>(k_head_f64), 200 * 1024);
+        k_head_f64<<<dgrid(mg[0], kHeadRows, 4), 128, smem, st>>>(
+            catd[0], width[0], &C->m[0], h1.cin, h1.cout, h1.w, h1.b, h2.w, h2.b, raw);
+        SFB_CHECK_LAUNCH();
+        return;
+    }
+    float *raw = static_cast<float *>(raw_out);
     pin[0] = ctx->arena.alloc<float>((size_t)mb * enc[0]);
     k_feats_to_f32<<<dgrid(mg[0] * enc[0], 256), 256, 0, st>>>(feats9, &C->m[0], enc[0], pin[0]);
     SFB_CHECK_LAUNCH();
@@ -674,20 +896,7 @@ void unet_run(sfb_ctx *ctx, const int32_t *coords0, const double *feats9, int64_
         coarse = cat[l];
         ld_coarse = width[l];
     }
-    const FrameDebug &D = ctx->frame_debug;
-    if (D.cap > 0 && D.level_coords && D.level_maps) {   // parity export (eager frames only)
-        SFB_REQUIRE(mb <= D.cap, "frame debug buffers are smaller than the cloud");
-        for (int l = 0; l <= L && l < D.levels; ++l) {
-            const int taps = kern[l] * kern[l] * kern[l];
-            SFB_REQUIRE(taps <= 27, "frame debug export holds up to 27 taps per level");
-            SFB_CUDA(cudaMemcpyAsync(D.level_coords + (size_t)l * 3 * D.cap, coords[l],
-                                     sizeof(int32_t) * 3 * mb, cudaMemcpyDeviceToDevice, st));
-            for (int t = 0; t < taps; ++t)
-                SFB_CUDA(cudaMemcpyAsync(D.level_maps + ((size_t)l * 27 + t) * D.cap,
-                                         nbr[l] + (size_t)t * mb, sizeof(int32_t) * mb,
-                                         cudaMemcpyDeviceToDevice, st));
-        }
-    }
+    export_debug();
     const NetLayer &h1 = net.layers[layer], &h2 = net.layers[layer + 1];
     size_t smem = sizeof(float) * ((size_t)kHeadRows * (h1.cin + h1.cout) + (size_t)h1.cin * h1.cout +
                                    (size_t)h1.cout * 14);

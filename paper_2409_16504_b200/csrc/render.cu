@@ -42,7 +42,7 @@ constexpr int kWin = 2048;     // rank window of the merge
 // one pixel (64 threads x 4 pixels: 0.34, register-starved)
 constexpr int kCT = 128;       // compositor threads per CTA
 constexpr int kCompMinBlocks = 7;
-constexpr int kChunk = 64;     // runs per compositing chunk
+constexpr int kChunk = kCT;    // candidate runs staged per compositing chunk
 
 // ------------------------------------------------------------ 1. projection
 __device__ __forceinline__ void project_one(const double *__restrict__ p, const double *__restrict__ q,
@@ -811,6 +811,37 @@ __device__ __forceinline__ double exp_nonpos(double x) {
     return p * __longlong_as_double((long long)(k + 1023) << 52);
 }
 
+// Alpha-support test of a whole tile. forward_kernel blends a splat at a
+// pixel only if alpha = min(o exp(-q/2), alpha_max) >= 1/255, i.e. only if
+// q <= 2 ln(255 o). q_cut widens that bound by a relative 1e-6 (+1e-6), far
+// beyond the float64 rounding of q and of the exp, so skipping a run whose
+// q exceeds q_cut at every pixel of a tile never drops a contribution.
+__device__ __forceinline__ double q_cut(double op) {
+    return 2.0 * log(fmax(255.0 * op, 1e-300)) * (1.0 + 1e-6) + 1e-6;
+}
+
+// min over the rectangle [x0,x1] x [y0,y1] (offsets from the centre) of the
+// positive-definite form q(d) = ia dx^2 + 2 ib dx dy + ic dy^2: 0 when the
+// centre is inside, else the least of the four edge minima (a 1-D quadratic
+// per edge, minimised at its clamped stationary point). Returns 0 (no cull)
+// for a degenerate conic.
+__device__ __forceinline__ double edge_min(double a, double b, double c, double fixed, double lo,
+                                           double hi) {
+    // q(t) = a fixed^2 + 2 b fixed t + c t^2 over t in [lo, hi]
+    const double t = fmin(fmax(-b * fixed / c, lo), hi);
+    return a * fixed * fixed + 2.0 * b * fixed * t + c * t * t;
+}
+__device__ __forceinline__ double tile_min_q(double ia, double ib, double ic, double x0, double x1,
+                                             double y0, double y1) {
+    if (!(ia > 0.0) || !(ic > 0.0) || !(ia * ic - ib * ib > 0.0)) return 0.0;
+    if (x0 <= 0.0 && 0.0 <= x1 && y0 <= 0.0 && 0.0 <= y1) return 0.0;
+    double m = edge_min(ia, ib, ic, x0, y0, y1);
+    m = fmin(m, edge_min(ia, ib, ic, x1, y0, y1));
+    m = fmin(m, edge_min(ic, ib, ia, y0, x0, x1));
+    m = fmin(m, edge_min(ic, ib, ia, y1, x0, x1));
+    return m;
+}
+
 // b^e for e >= 0 by repeated squaring (float64)
 __device__ __forceinline__ double ipow(double b, int e) {
     double r = 1.0;
@@ -824,50 +855,39 @@ __device__ __forceinline__ double ipow(double b, int e) {
 
 // sum_{j<m} om^j v_j (float32; v in rank order). Two interleaved Horner
 // chains in om^2 (even and odd points), S = E + om * O, so two independent
-// FMA chains and four 16-byte loads are in flight per step.
+// chains and four 16-byte loads are in flight per step; the (x, y) channels
+// go through one paired FFMA2 (sm_100), z through an FFMA.
+__device__ __forceinline__ void hstep(float2 &xy, float &z, float2 om2v, float om2, float4 a) {
+    xy = __ffma2_rn(xy, om2v, make_float2(a.x, a.y));
+    z = fmaf(z, om2, a.z);
+}
 __device__ __forceinline__ float3 horner3(const float4 *__restrict__ v, int m, float om) {
     const float om2 = om * om;
-    float ex = 0.f, ey = 0.f, ez = 0.f, ox = 0.f, oy = 0.f, oz = 0.f;
+    const float2 om2v = make_float2(om2, om2);
+    float2 exy = make_float2(0.f, 0.f), oxy = make_float2(0.f, 0.f);
+    float ez = 0.f, oz = 0.f;
     int j = m - 1;
     if (!(m & 1) && j >= 0) {   // make the last point an even one
         const float4 a = __ldg(v + j);
-        ox = a.x;
-        oy = a.y;
+        oxy = make_float2(a.x, a.y);
         oz = a.z;
         --j;
     }
     // j is even here: pairs (j-1 odd, j even) ... down to (-, 0)
     for (; j >= 4; j -= 4) {
         const float4 a = __ldg(v + j), b = __ldg(v + j - 1), c = __ldg(v + j - 2), d = __ldg(v + j - 3);
-        ex = fmaf(ex, om2, a.x);
-        ey = fmaf(ey, om2, a.y);
-        ez = fmaf(ez, om2, a.z);
-        ox = fmaf(ox, om2, b.x);
-        oy = fmaf(oy, om2, b.y);
-        oz = fmaf(oz, om2, b.z);
-        ex = fmaf(ex, om2, c.x);
-        ey = fmaf(ey, om2, c.y);
-        ez = fmaf(ez, om2, c.z);
-        ox = fmaf(ox, om2, d.x);
-        oy = fmaf(oy, om2, d.y);
-        oz = fmaf(oz, om2, d.z);
+        hstep(exy, ez, om2v, om2, a);
+        hstep(oxy, oz, om2v, om2, b);
+        hstep(exy, ez, om2v, om2, c);
+        hstep(oxy, oz, om2v, om2, d);
     }
     for (; j >= 2; j -= 2) {
         const float4 a = __ldg(v + j), b = __ldg(v + j - 1);
-        ex = fmaf(ex, om2, a.x);
-        ey = fmaf(ey, om2, a.y);
-        ez = fmaf(ez, om2, a.z);
-        ox = fmaf(ox, om2, b.x);
-        oy = fmaf(oy, om2, b.y);
-        oz = fmaf(oz, om2, b.z);
+        hstep(exy, ez, om2v, om2, a);
+        hstep(oxy, oz, om2v, om2, b);
     }
-    if (j == 0) {
-        const float4 a = __ldg(v);
-        ex = fmaf(ex, om2, a.x);
-        ey = fmaf(ey, om2, a.y);
-        ez = fmaf(ez, om2, a.z);
-    }
-    return make_float3(fmaf(om, ox, ex), fmaf(om, oy, ey), fmaf(om, oz, ez));
+    if (j == 0) hstep(exy, ez, om2v, om2, __ldg(v));
+    return make_float3(fmaf(om, oxy.x, exy.x), fmaf(om, oxy.y, exy.y), fmaf(om, oz, ez));
 }
 
 // One CTA per tile. The rank-ordered fine / super / global lists are merged
@@ -891,6 +911,8 @@ __global__ void __launch_bounds__(kCT, kCompMinBlocks) k_composite(CompParams P)
     __shared__ int s_nlist;
     __shared__ uint32_t s_add[3];
     __shared__ uint32_t s_head;
+    __shared__ unsigned s_bal[kCT / 32];
+    __shared__ uint8_t r_idx[kChunk];   // staged slot of the chunk's e-th surviving run
     // the current chunk's run records (pixel box precomputed per run)
     __shared__ double r_mx[kChunk], r_my[kChunk], r_rr[kChunk], r_ia[kChunk], r_ib[kChunk],
         r_ic[kChunk], r_op[kChunk], r_dep[kChunk], r_rn[3][kChunk];
@@ -1020,12 +1042,18 @@ __global__ void __launch_bounds__(kCT, kCompMinBlocks) k_composite(CompParams P)
         }
         __syncthreads();
         const int nlist = s_nlist;
-        // chunks grow 8 -> 64 runs: most tiles saturate within the first few
-        // runs, so the first chunk stages (and pays latency for) only 8 records
-        int chunk = 8;
+        // chunks of candidate runs grow 16 -> 128: most tiles saturate within
+        // the first few contributing runs. Each candidate is staged by one
+        // thread, which also drops it when its alpha-support ellipse misses the
+        // tile's pixels (tile_min_q): such a run has alpha < 1/255 at every
+        // pixel of the tile, so forward_kernel's per-pixel test skips it
+        // everywhere (_raster_kernels.py:193-194). Survivors are compacted in
+        // rank order.
+        int chunk = 16;
         for (int base = 0; base < nlist && !done; base += chunk, chunk = min(2 * chunk, kChunk)) {
-            const int nb = min(chunk, nlist - base);
-            if (threadIdx.x < nb) {
+            const int nc = min(chunk, nlist - base);
+            bool keep = false;
+            if (threadIdx.x < nc) {
                 const uint32_t r = list[base + threadIdx.x];
                 const int j = threadIdx.x;
                 const double2 q0 = Rrec[4 * (size_t)r], q1 = Rrec[4 * (size_t)r + 1],
@@ -1052,17 +1080,35 @@ __global__ void __launch_bounds__(kCT, kCompMinBlocks) k_composite(CompParams P)
                     r_rn[2][j] = a1.x;
                 }
                 // pixel box of forward_kernel (_raster_kernels.py:178-181), clamped to the tile
-                r_x0[j] = (int32_t)fmin(fmax((double)x_lo, ceil(mx - rad)), (double)x_end);
-                r_x1[j] = (int32_t)fmax(fmin((double)(x_end - 1), floor(mx + rad)), (double)(x_lo - 1));
-                r_y0[j] = (int32_t)fmin(fmax((double)y_lo, ceil(my - rad)), (double)y_end);
-                r_y1[j] = (int32_t)fmax(fmin((double)(y_end - 1), floor(my + rad)), (double)(y_lo - 1));
+                const int32_t bx0 = (int32_t)fmin(fmax((double)x_lo, ceil(mx - rad)), (double)x_end);
+                const int32_t bx1 = (int32_t)fmax(fmin((double)(x_end - 1), floor(mx + rad)), (double)(x_lo - 1));
+                const int32_t by0 = (int32_t)fmin(fmax((double)y_lo, ceil(my - rad)), (double)y_end);
+                const int32_t by1 = (int32_t)fmax(fmin((double)(y_end - 1), floor(my + rad)), (double)(y_lo - 1));
+                r_x0[j] = bx0;
+                r_x1[j] = bx1;
+                r_y0[j] = by0;
+                r_y1[j] = by1;
                 // whole tile inside the box and the circle (farthest corner
                 // within the radius): the per-pixel tests are then all true
                 const double fx = fmax(fabs((double)x_lo - mx), fabs((double)(x_end - 1) - mx));
                 const double fy = fmax(fabs((double)y_lo - my), fabs((double)(y_end - 1) - my));
-                r_full[j] = r_x0[j] == x_lo && r_x1[j] == x_end - 1 && r_y0[j] == y_lo &&
-                            r_y1[j] == y_end - 1 && fx * fx + fy * fy <= rad * rad;
+                r_full[j] = bx0 == x_lo && bx1 == x_end - 1 && by0 == y_lo && by1 == y_end - 1 &&
+                            fx * fx + fy * fy <= rad * rad;
+                keep = bx0 <= bx1 && by0 <= by1 &&
+                       !(tile_min_q(q1.x, q1.y, q2.x, bx0 - mx, bx1 - mx, by0 - my, by1 - my) >
+                         q_cut(q2.y));
             }
+            const unsigned ball = __ballot_sync(0xffffffffu, keep);
+            if ((threadIdx.x & 31) == 0) s_bal[threadIdx.x >> 5] = ball;
+            __syncthreads();
+            int slot = __popc(ball & ((1u << (threadIdx.x & 31)) - 1u)), nb = 0;
+#pragma unroll
+            for (int w = 0; w < kCT / 32; ++w) {
+                const int c = __popc(s_bal[w]);
+                slot += w < (int)(threadIdx.x >> 5) ? c : 0;
+                nb += c;
+            }
+            if (keep) r_idx[slot] = (uint8_t)threadIdx.x;   // survivors in rank order
             __syncthreads();
             for (int e = 0; e < nb; ++e) {
                 if (term && e && (e & 31) == 0 && __syncthreads_and(saturated())) {
@@ -1073,22 +1119,23 @@ __global__ void __launch_bounds__(kCT, kCompMinBlocks) k_composite(CompParams P)
                     e |= 31;   // my warp is finished: skip to the next block checkpoint
                     continue;
                 }
+                const int f = r_idx[e];
 #pragma unroll
                 for (int k = 0; k < NPIX; ++k) {
                     if (!valid[k]) continue;
                     if (term && T[k] < kCutoff) continue;
-                    const double dx = (double)pxs[k] - r_mx[e], dy = (double)pys[k] - r_my[e];
-                    if (!r_full[e]) {
-                        if (pxs[k] < r_x0[e] || pxs[k] > r_x1[e] || pys[k] < r_y0[e] || pys[k] > r_y1[e])
+                    const double dx = (double)pxs[k] - r_mx[f], dy = (double)pys[k] - r_my[f];
+                    if (!r_full[f]) {
+                        if (pxs[k] < r_x0[f] || pxs[k] > r_x1[f] || pys[k] < r_y0[f] || pys[k] > r_y1[f])
                             continue;
-                        if (dx * dx + dy * dy > r_rr[e]) continue;
+                        if (dx * dx + dy * dy > r_rr[f]) continue;
                     }
-                    const double q = r_ia[e] * dx * dx + 2.0 * r_ib[e] * dx * dy + r_ic[e] * dy * dy;
-                    double alpha = r_op[e] * exp_nonpos(-0.5 * q);
+                    const double q = r_ia[f] * dx * dx + 2.0 * r_ib[f] * dx * dy + r_ic[f] * dy * dy;
+                    double alpha = r_op[f] * exp_nonpos(-0.5 * q);
                     if (alpha > alpha_max) alpha = alpha_max;
                     if (alpha < kCutoff) continue;
                     const double om = 1.0 - alpha;
-                    const int32_t b0 = r_start[e], cnt = r_count[e];
+                    const int32_t b0 = r_start[f], cnt = r_count[f];
                     const double T0 = T[k];
                     int m = cnt;
                     double Tend;
@@ -1123,10 +1170,10 @@ __global__ void __launch_bounds__(kCT, kCompMinBlocks) k_composite(CompParams P)
                         c2[k] = __fma_rn(wa, (double)S.z, c2[k]);
                     }
                     if (want_n) {
-                        if (r_uni[e]) {
-                            n0[k] = __fma_rn(wsum, r_rn[0][e], n0[k]);
-                            n1[k] = __fma_rn(wsum, r_rn[1][e], n1[k]);
-                            n2[k] = __fma_rn(wsum, r_rn[2][e], n2[k]);
+                        if (r_uni[f]) {
+                            n0[k] = __fma_rn(wsum, r_rn[0][f], n0[k]);
+                            n1[k] = __fma_rn(wsum, r_rn[1][f], n1[k]);
+                            n2[k] = __fma_rn(wsum, r_rn[2][f], n2[k]);
                         } else {
                             const float3 S = horner3(snrm + b0, m, omf);
                             n0[k] = __fma_rn(wa, (double)S.x, n0[k]);
@@ -1134,7 +1181,7 @@ __global__ void __launch_bounds__(kCT, kCompMinBlocks) k_composite(CompParams P)
                             n2[k] = __fma_rn(wa, (double)S.z, n2[k]);
                         }
                     }
-                    if (want_d) dd[k] = __fma_rn(wsum, r_dep[e], dd[k]);
+                    if (want_d) dd[k] = __fma_rn(wsum, r_dep[f], dd[k]);
                     T[k] = Tend;
                 }
             }

@@ -21,15 +21,16 @@ from .netplan import (HEAD_CHANNELS, ConvLayerSpec, NetworkPlan, NetworkWeights,
 from .voxelgrid import SparseVoxelGrid, VoxelizedCloud
 
 MODES = {"simt_f32": _lib.NET_SIMT_F32, "tc_tf32x3": _lib.NET_TC_TF32X3,
-         "tc_bf16": _lib.NET_TC_BF16}
+         "tc_bf16": _lib.NET_TC_BF16, "simt_f64": _lib.NET_SIMT_F64}
 _mode = "tc_tf32x3"
 
 
 def set_mode(mode: str) -> None:
-    """Select the conv arithmetic for every lane: 'tc_tf32x3' (tcgen05, tf32
+    """Select the network arithmetic for every lane: 'tc_tf32x3' (tcgen05, tf32
     hi/lo split, fp32-accurate: the default), 'tc_bf16' (tcgen05, single bf16
-    operands, fp32 accumulation: fast, outside the 1e-3 parameter bound) or
-    'simt_f32' (FFMA)."""
+    operands, fp32 accumulation: fast, outside the 1e-3 parameter bound),
+    'simt_f32' (FFMA) or 'simt_f64' (float64 features, the reference's own
+    arithmetic on the FP64 pipe: the end-to-end exactness mode)."""
     global _mode
     if mode not in MODES:
         raise ValueError(f"unknown network mode {mode!r}; expected one of {tuple(MODES)}")
@@ -112,14 +113,16 @@ def transposed_conv_pruned(grid: SparseVoxelGrid, spec: ConvLayerSpec, weights, 
 
 
 def unet_forward_voxels(vox: VoxelizedCloud, weights: NetworkWeights) -> torch.Tensor:
-    """UNet + head, one raw 14-vector per VOXEL (M0,14) float32."""
+    """UNet + head, one raw 14-vector per VOXEL (M0,14): float32, float64 in
+    'simt_f64' mode."""
     plan = weights.plan
     if vox.grid.channel_count != plan.encoder_channels[0]:
         raise ValueError(f"input grid has {vox.grid.channel_count} channels, "
                          f"plan expects {plan.encoder_channels[0]}")
     ctx = ensure_loaded(weights)
     m = len(vox.grid)
-    raw = torch.empty((m, HEAD_CHANNELS), dtype=torch.float32, device=vox.grid.coords.device)
+    dt = torch.float64 if _mode == "simt_f64" else torch.float32
+    raw = torch.empty((m, HEAD_CHANNELS), dtype=dt, device=vox.grid.coords.device)
     feats = vox.grid.feats.to(torch.float64).contiguous()
     ctx.call("sfb_unet_forward", _lib.ptr(vox.grid.coords), _lib.ptr(feats), m, _lib.ptr(raw))
     return raw

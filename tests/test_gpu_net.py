@@ -44,6 +44,25 @@ def test_config1_raw_head_vs_reference_golden(c1_arrays, mode):
     raw_close(raw, c1_arrays["raw_voxel"])
 
 
+def test_float64_mode_matches_reference_raw_to_1e_10():
+    """SFB_NET_SIMT_F64 computes what the reference computes (float64
+    features, float32 weights upcast): the raw head agrees with the reference
+    golden to ~1e-13, four orders of magnitude inside the fp32 bound."""
+    cloud, _ = scenes.config1()
+    w = netplan.init_random(netplan.NetworkPlan(), 0)
+    vox = voxelize_adaptive(PointCloud(cloud.positions, cloud.colors))
+    sparsenet.set_mode("simt_f64")
+    try:
+        raw = sparsenet.unet_forward_voxels(vox, w)
+    finally:
+        sparsenet.set_mode("tc_tf32x3")
+    assert raw.dtype == torch.float64
+    ref = c1_arrays["raw_voxel"]
+    err = np.abs(np_(raw) - ref).max() / np.abs(ref).max()
+    print("float64 mode raw max rel err", err)
+    assert err < 1e-10
+
+
 def test_config1_gaussian_params(c1_arrays, mode):
     cloud, _ = scenes.config1()
     w = netplan.init_random(netplan.NetworkPlan(), 0)

@@ -17,7 +17,7 @@ import numpy as np
 import pytest
 
 from oracle import net as ON
-from paper_2409_16504_b200 import netplan, scenes
+from paper_2409_16504_b200 import netplan, scenes, sparsenet
 from paper_2409_16504_b200.pcio import PointCloud
 from parity_util import frame_parity, gpu_splats_np
 
@@ -58,7 +58,7 @@ def check(rec, where, pixels):
         assert rec["levels"]["exact"], (where, rec["levels"])
 
 
-def run_config(cloud, views, weights, which, levels_on=(0,)):
+def run_config(cloud, views, weights, which, levels_on=(0,), exact=False):
     pc = PointCloud(cloud.positions, cloud.colors)
     est = ON.estimate(cloud.positions, cloud.colors, weights.as_oracle_layers(), 3)
     sp = gpu_splats_np(pc, weights)
@@ -68,6 +68,9 @@ def run_config(cloud, views, weights, which, levels_on=(0,)):
         print(k, rec["order"], rec["renderer"], rec["e2e"],
               {x: y for x, y in rec.get("e2e_over_pixels", {}).items() if x != "samples"})
         check(rec, k, int(views[k].width) * int(views[k].height))
+        if exact:   # the float64 network: no pixel over 2e-3 end to end
+            for plane, st in rec["e2e"].items():
+                assert st["over"] == 0 and st["max_abs"] <= 2e-3, (k, plane, st)
 
 
 def test_config2_all_eight_views(weights):
@@ -89,3 +92,25 @@ def test_config4_frames(weights, frame):
 def test_config5_views(weights):
     cloud, views = scenes.config5()
     run_config(cloud, views, weights, (3, 17), levels_on=())
+
+
+@pytest.fixture
+def f64_mode():
+    sparsenet.set_mode("simt_f64")
+    yield
+    sparsenet.set_mode("tc_tf32x3")
+
+
+def test_exact_mode_zero_pixels_over_end_to_end(weights, f64_mode):
+    """With the reference's float64 network arithmetic (SFB_NET_SIMT_F64) the
+    whole fused frame is within 2e-3 of the oracle at every pixel: every
+    end-to-end difference of the default mode is the fp32 P2ENet's."""
+    cloud, views = scenes.config2()
+    run_config(cloud, views, weights, range(len(views)), levels_on=(), exact=True)
+    cloud, views = scenes.config3()
+    run_config(cloud, views, weights, (0, 9), levels_on=(), exact=True)
+    for f in (0, 37):
+        cloud, views = scenes.config4_frame(f)
+        run_config(cloud, views, weights, (0,), levels_on=(), exact=True)
+    cloud, views = scenes.config5()
+    run_config(cloud, views, weights, (3,), levels_on=(), exact=True)
