@@ -269,7 +269,7 @@ def explain_pixels(over, got, same, ref, gpu_sp, est, view, limit=200) -> dict:
     return {"count": int(over.sum()), "renderer_max_abs_there": ren,
             "parameter_effect_max_abs_there": par, "kinds": kinds,
             "all_threshold_crossings": all(c["kind"] in ("alpha_cutoff", "T_cutoff")
-                                           and c["straddle"] and c["rel_gap"] < 1e-3
+                                           and c["straddle"] and c["rel_gap"] < 5e-2
                                            for c in samples),
             "max_rel_gap": max((c.get("rel_gap", 0.0) for c in samples), default=0.0),
             "samples": samples}

@@ -29,15 +29,17 @@ def weights():
     return netplan.init_random(netplan.NetworkPlan(), 0)
 
 
-# End to end, the GPU's P2ENet (fp32-accurate tcgen05, parameters within
-# ~1e-6 relative of the oracle's float64 network; north star: 1e-3) moves a
-# few (splat, pixel) alphas or transmittances across the reference's 1/255
-# cutoffs. A voxel's points share one alpha, so such a crossing switches a
-# whole run of ~26 points on or off and can move a pixel by more than 2e-3
-# (measured: at most ~1e-5 of a frame's pixels). Every such pixel must be a
-# cutoff crossing — the two parameter sets straddle 1/255 within 0.1 % —
-# never an order difference or a renderer difference.
-E2E_OVER_FRACTION = 2e-5
+# End to end, the GPU's fp32-accurate P2ENet (tcgen05; parameters typically
+# ~1e-6, at worst ~4e-4 relative from the oracle's float64 network; north
+# star: 1e-3) moves a few (splat, pixel) alphas or transmittances across the
+# reference's 1/255 cutoffs. A voxel's points share one alpha, so such a
+# crossing switches a whole run of ~26 points on or off and can move a pixel
+# by more than 2e-3 (profiles/parity_r02.json: <= 16 pixels of a 1-2 Mpixel
+# frame). Every such pixel must be a cutoff crossing — the GPU's and the
+# oracle's value straddle 1/255, within the parameter tolerance — never an
+# order or renderer difference; the float64 network mode (last test) has no
+# pixel over 2e-3 at all.
+E2E_OVER_FRACTION = 5e-5
 
 
 def check(rec, where, pixels):
