@@ -91,6 +91,10 @@ int sfb_set_timing(sfb_ctx *ctx, int on);
 /* CUDA-graph replay of sfb_frame (default on): the first call of a shape runs
  * eagerly, the second captures, later calls update parameters and replay. */
 int sfb_set_graphs(sfb_ctx *ctx, int on);
+/* Capacity (entries) of the fine / super tile-list buffers; 0 (default) sizes
+ * them from the previous eager frame's demand. A frame needing more renders
+ * every run from the global list instead (identical planes, slower). Tests. */
+int sfb_set_entry_capacity(sfb_ctx *ctx, int64_t capacity);
 /* Diagnostics: when set (device buffer of 4 int64 per tile, zeroed by the
  * caller) the compositor accumulates windows, list entries and alpha
  * evaluations per tile. NULL disables. */

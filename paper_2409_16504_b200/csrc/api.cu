@@ -208,6 +208,7 @@ struct sfb_frame_graph {
     int32_t width, height, tile, terminate, mask, key_bits;
     double alpha_max;
     const void *ptrs[7];
+    int64_t level_bound[9];   // UNet buffer bounds (unet_level_bounds) baked into the graph
     int net_mode;
     uint64_t net_epoch;
     int seen = 0;                     // eager runs with this key
@@ -296,6 +297,12 @@ int sfb_set_frame_debug(sfb_ctx *ctx, int64_t capacity, int64_t *source, int32_t
         D.level_maps = level_maps;
     }
     ctx->frame_debug = D;
+    return SFB_OK;
+}
+
+int sfb_set_entry_capacity(sfb_ctx *ctx, int64_t capacity) {
+    if (!ctx || capacity < 0) return SFB_ERR_ARG;
+    ctx->entry_cap_override = capacity;
     return SFB_OK;
 }
 
@@ -657,7 +664,7 @@ static int frame_impl(sfb_ctx *ctx, const double *positions, const double *color
         // the graph bakes in the voxel-key radix pass count (8-bit digits) and the
         // key width (32 / 64 bit): key on the pass count in both ranges
         const int key_bits = ((std::max(host.total, 1) + 7) / 8) * 8;
-        if (!ctx->use_graphs || ctx->timing || ctx->frame_debug.cap > 0) {
+        if (!ctx->use_graphs || ctx->timing || ctx->frame_debug.cap > 0 || ctx->entry_cap_override > 0) {
             FrameParams *P = ctx->arena.alloc<FrameParams>(1);
             enqueue_frame(ctx, positions, colors, n, host, P, cam, opts, plane_mask, rgb, normal,
                           depth, trans, rgba);
@@ -666,12 +673,14 @@ static int frame_impl(sfb_ctx *ctx, const double *positions, const double *color
         // ---- graph path: find / build the graph of this shape
         sfb_frame_graph *G = nullptr;
         const void *ptrs[7] = {positions, colors, rgb, normal, depth, trans, rgba};
+        int64_t lb[9] = {};
+        if (ctx->net.loaded) unet_level_bounds(host, n, std::min(ctx->net.levels, 8), lb);
         for (auto *g : ctx->graphs)
             if (g->n == n && g->width == cam->width && g->height == cam->height &&
                 g->tile == opts->tile_size && g->terminate == opts->early_termination &&
                 g->alpha_max == opts->alpha_max && g->mask == plane_mask && g->key_bits == key_bits &&
                 g->net_mode == ctx->net_mode && g->net_epoch == ctx->net_epoch &&
-                std::equal(ptrs, ptrs + 7, g->ptrs))
+                std::equal(ptrs, ptrs + 7, g->ptrs) && std::equal(lb, lb + 9, g->level_bound))
                 G = g;
         if (!G) {
             G = new sfb_frame_graph();
@@ -686,6 +695,7 @@ static int frame_impl(sfb_ctx *ctx, const double *positions, const double *color
             G->net_mode = ctx->net_mode;
             G->net_epoch = ctx->net_epoch;
             std::copy(ptrs, ptrs + 7, G->ptrs);
+            std::copy(lb, lb + 9, G->level_bound);
             if (ctx->graphs.size() >= 32) {
                 delete ctx->graphs.front();
                 ctx->graphs.erase(ctx->graphs.begin());
@@ -706,7 +716,7 @@ static int frame_impl(sfb_ctx *ctx, const double *positions, const double *color
             for (int l = 0; l < 9; ++l) ctx->hint_m[l] = c.m[l];
             ctx->hint_kept = c.kept;
             ctx->hint_runs = c.runs;
-            ctx->hint_e = c.es + c.ef;
+            ctx->hint_e = c.es_req + c.ef_req;
             return;
         }
         if (!G->exec) {

@@ -156,6 +156,7 @@ struct sfb_ctx {
     int64_t graph_nodes = 0;
     int64_t *debug_counters = nullptr;   // compositor per-tile counters (diagnostics)
     sfb::FrameDebug frame_debug;         // fused-frame parity export (tests)
+    int64_t entry_cap_override = 0;      // tests: pyramid entry capacity (0 = automatic)
     sfb::DevCounts *last_counts = nullptr;   // device counts of the last call
     // launch-size hints (host copies of the counts of the last eager frame):
     // every kernel loops over its device count, so hints only size grids
@@ -263,6 +264,7 @@ struct DevCounts {
     int64_t runs;       // depth-ordered runs of identical geometry
     int64_t runs1;      // runs + 1
     int64_t ef, es, g;  // fine / super / global pyramid entries
+    int64_t ef_req, es_req, overflow;   // entries the runs asked for; 1 = over capacity
     int64_t scratch[4];
 };
 
@@ -278,7 +280,7 @@ Cam to_cam(const sfb_camera &c);
 // kernel-node parameter update.
 struct FrameParams {
     double s, inv_s;
-    int64_t lo[3];
+    int64_t lo[3], hi[3];   // lattice range of the level-0 voxel coordinates
     int32_t bits[3];
     int32_t total;
     Cam cam;
@@ -377,6 +379,12 @@ void voxelize_run(sfb_ctx *ctx, const double *pos, const double *col, int64_t n,
 // net.cu
 void net_load(sfb_ctx *ctx, const void *blob, size_t n);
 // per-voxel raw head (M0 x 14) float32 into `raw`; M0 = C->m[0] (device), bound m_bound
+// Host bounds on the voxel count of UNet level l (stride 2^l): the cloud's
+// point count, and the number of stride-2^l lattice cells the level-0
+// coordinate range [lo, hi] touches, rounded up to 3 significant bits (so a
+// CUDA graph keyed on them survives small bbox changes). Buffers of level l
+// are sized by it instead of by the point count.
+void unet_level_bounds(const FrameParams &host, int64_t n, int levels, int64_t *bound);
 // raw: float32, or float64 in SFB_NET_SIMT_F64 mode
 void unet_run(sfb_ctx *ctx, const int32_t *coords, const double *feats9, int64_t m_bound,
               const FrameParams &host, const FrameParams *P, DevCounts *C, void *raw);

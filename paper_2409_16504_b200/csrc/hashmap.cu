@@ -568,6 +568,7 @@ void coords_layout(sfb_ctx *ctx, const int32_t *coords, int64_t m, FrameParams &
     P.total = 0;
     for (int a = 0; a < 3; ++a) {
         P.lo[a] = h[a];
+        P.hi[a] = h[3 + a];
         P.bits[a] = bits_for((uint64_t)((int64_t)h[3 + a] - h[a]));
         P.total += P.bits[a];
     }

@@ -758,6 +758,24 @@ __global__ void k_feats_to_f32(const double *__restrict__ f, const int64_t *__re
 // device} at the same single-frame latency — with concurrent frames the extra
 // CTAs and the partial-sum reduction cost more than the parallelism they buy.
 constexpr int kLevelSplit[4] = {1, 1, 4, 8};
+
+void unet_level_bounds(const FrameParams &host, int64_t n, int levels, int64_t *bound) {
+    auto round3 = [](int64_t x) {   // up to 3 significant bits
+        int64_t step = 1;
+        while ((x >> 3) >= step * 2) step <<= 1;
+        return (x + step - 1) / step * step;
+    };
+    int64_t prev = n;
+    for (int l = 0; l <= levels; ++l) {
+        const int64_t S = int64_t(1) << l;
+        double cells = 1.0;
+        for (int a = 0; a < 3; ++a)
+            cells *= (double)(floor_div(host.hi[a], S) - floor_div(host.lo[a], S) + 1);
+        int64_t b = cells < (double)prev ? round3((int64_t)cells) : prev;
+        b = std::min(std::max<int64_t>(b, 1), prev);
+        bound[l] = prev = b;
+    }
+}
 constexpr int kTconvSplit = 8;
 
 void unet_run(sfb_ctx *ctx, const int32_t *coords0, const double *feats9, int64_t mb,
@@ -777,8 +795,10 @@ void unet_run(sfb_ctx *ctx, const int32_t *coords0, const double *feats9, int64_
     std::vector<int> width(L);
     coords[0] = coords0;
     for (int l = 0; l < L; ++l) width[l] = dec[L - 1 - l] + enc[l + 1];
-    std::vector<int64_t> mg(L + 1);
-    for (int l = 0; l <= L; ++l) mg[l] = ctx->grid_bound(mb, ctx->hint_m[l]);
+    // per-level row bounds (buffers, kernel-map leading dimensions, grids)
+    std::vector<int64_t> mbl(L + 1), mg(L + 1);
+    unet_level_bounds(host, mb, L, mbl.data());
+    for (int l = 0; l <= L; ++l) mg[l] = ctx->grid_bound(mbl[l], ctx->hint_m[l]);
     std::vector<int> kern(L + 1);
     {
         int layer = 0;
@@ -786,9 +806,9 @@ void unet_run(sfb_ctx *ctx, const int32_t *coords0, const double *feats9, int64_
     }
     // level 0: hash + kernel map on the critical path
     HashTable h0;
-    nbr[0] = ctx->arena.alloc<int32_t>((size_t)kern[0] * kern[0] * kern[0] * mb);
-    h0 = hash_build(ctx, coords[0], &C->m[0], mb, mg[0]);
-    kernel_map_build(ctx, h0, coords[0], &C->m[0], mb, 1, kern[0], nbr[0], mg[0]);
+    nbr[0] = ctx->arena.alloc<int32_t>((size_t)kern[0] * kern[0] * kern[0] * mbl[0]);
+    h0 = hash_build(ctx, coords[0], &C->m[0], mbl[0], mg[0]);
+    kernel_map_build(ctx, h0, coords[0], &C->m[0], mbl[0], 1, kern[0], nbr[0], mg[0]);
     // side branch: the coordinate structure of every coarser level (parents,
     // children, taps, hash = the pooling table, kernel map) depends only on
     // coordinates, so it runs concurrently with the convolutions; event l
@@ -798,11 +818,11 @@ void unet_run(sfb_ctx *ctx, const int32_t *coords0, const double *feats9, int64_
     ctx->stream = ctx->side_stream;
     try {
         for (int l = 0; l < L; ++l) {
-            int32_t *pc = ctx->arena.alloc<int32_t>((size_t)mb * 3);
+            int32_t *pc = ctx->arena.alloc<int32_t>((size_t)mbl[l + 1] * 3);
             const int k = kern[l + 1];
-            nbr[l + 1] = ctx->arena.alloc<int32_t>((size_t)k * k * k * mb);
-            ps[l] = pool_structure(ctx, coords[l], &C->m[l], mb, mg[l], 1 << l, pc, &C->m[l + 1]);
-            kernel_map_build(ctx, ps[l].table, pc, &C->m[l + 1], mb, 2 << l, k, nbr[l + 1],
+            nbr[l + 1] = ctx->arena.alloc<int32_t>((size_t)k * k * k * mbl[l + 1]);
+            ps[l] = pool_structure(ctx, coords[l], &C->m[l], mbl[l], mg[l], 1 << l, pc, &C->m[l + 1]);
+            kernel_map_build(ctx, ps[l].table, pc, &C->m[l + 1], mbl[l + 1], 2 << l, k, nbr[l + 1],
                              mg[l + 1]);
             coords[l + 1] = pc;
             SFB_CUDA(cudaEventRecord(ctx->side_ev[l], ctx->stream));
@@ -820,10 +840,10 @@ void unet_run(sfb_ctx *ctx, const int32_t *coords0, const double *feats9, int64_
             const int taps = kern[l] * kern[l] * kern[l];
             SFB_REQUIRE(taps <= 27, "frame debug export holds up to 27 taps per level");
             SFB_CUDA(cudaMemcpyAsync(D.level_coords + (size_t)l * 3 * D.cap, coords[l],
-                                     sizeof(int32_t) * 3 * mb, cudaMemcpyDeviceToDevice, st));
+                                     sizeof(int32_t) * 3 * mbl[l], cudaMemcpyDeviceToDevice, st));
             for (int t = 0; t < taps; ++t)
                 SFB_CUDA(cudaMemcpyAsync(D.level_maps + ((size_t)l * 27 + t) * D.cap,
-                                         nbr[l] + (size_t)t * mb, sizeof(int32_t) * mb,
+                                         nbr[l] + (size_t)t * mbl[l], sizeof(int32_t) * mbl[l],
                                          cudaMemcpyDeviceToDevice, st));
         }
     };
@@ -832,19 +852,19 @@ void unet_run(sfb_ctx *ctx, const int32_t *coords0, const double *feats9, int64_
         std::vector<double *> catd(L), pind(L + 1);
         int layer = 0;
         for (int l = 0; l < L; ++l) {
-            catd[l] = ctx->arena.alloc<double>((size_t)mb * width[l]);
+            catd[l] = ctx->arena.alloc<double>((size_t)mbl[l] * width[l]);
             const int up = dec[L - 1 - l];
-            conv_f64(ctx, net.layers[layer++], l ? pind[l] : feats9, l ? enc[l] : 9, nbr[l], mb,
+            conv_f64(ctx, net.layers[layer++], l ? pind[l] : feats9, l ? enc[l] : 9, nbr[l], mbl[l],
                      &C->m[l], mg[l], catd[l] + up, width[l]);
-            pind[l + 1] = ctx->arena.alloc<double>((size_t)mb * enc[l + 1]);
+            pind[l + 1] = ctx->arena.alloc<double>((size_t)mbl[l + 1] * enc[l + 1]);
             SFB_CUDA(cudaStreamWaitEvent(st, ctx->side_ev[l], 0));   // level l+1 structure ready
             k_pool_means_f64<<<dgrid(mg[l + 1] * enc[l + 1], 256), 256, 0, st>>>(
                 catd[l] + up, width[l], enc[l + 1], ps[l].nkids, ps[l].kids, &C->m[l + 1], pind[l + 1],
                 enc[l + 1]);
             SFB_CHECK_LAUNCH();
         }
-        double *bott = ctx->arena.alloc<double>((size_t)mb * enc[L + 1]);
-        conv_f64(ctx, net.layers[layer++], pind[L], enc[L], nbr[L], mb, &C->m[L], mg[L], bott,
+        double *bott = ctx->arena.alloc<double>((size_t)mbl[L] * enc[L + 1]);
+        conv_f64(ctx, net.layers[layer++], pind[L], enc[L], nbr[L], mbl[L], &C->m[L], mg[L], bott,
                  enc[L + 1]);
         const double *coarse = bott;
         int ld_coarse = enc[L + 1];
@@ -868,30 +888,30 @@ void unet_run(sfb_ctx *ctx, const int32_t *coords0, const double *feats9, int64_
         return;
     }
     float *raw = static_cast<float *>(raw_out);
-    pin[0] = ctx->arena.alloc<float>((size_t)mb * enc[0]);
+    pin[0] = ctx->arena.alloc<float>((size_t)mbl[0] * enc[0]);
     k_feats_to_f32<<<dgrid(mg[0] * enc[0], 256), 256, 0, st>>>(feats9, &C->m[0], enc[0], pin[0]);
     SFB_CHECK_LAUNCH();
     int layer = 0;
     for (int l = 0; l < L; ++l) {
-        cat[l] = ctx->arena.alloc<float>((size_t)mb * width[l]);
+        cat[l] = ctx->arena.alloc<float>((size_t)mbl[l] * width[l]);
         const int up = dec[L - 1 - l];
-        conv_layer(ctx, net.layers[layer], pin[l], enc[l], nbr[l], mb, &C->m[l], mb, 1, cat[l] + up,
-                   width[l], mg[l], kLevelSplit[std::min(l, 3)]);
+        conv_layer(ctx, net.layers[layer], pin[l], enc[l], nbr[l], mbl[l], &C->m[l], mbl[l], 1,
+                   cat[l] + up, width[l], mg[l], kLevelSplit[std::min(l, 3)]);
         ++layer;
-        pin[l + 1] = ctx->arena.alloc<float>((size_t)mb * enc[l + 1]);
+        pin[l + 1] = ctx->arena.alloc<float>((size_t)mbl[l + 1] * enc[l + 1]);
         SFB_CUDA(cudaStreamWaitEvent(st, ctx->side_ev[l], 0));   // level l+1 structure ready
         pool_means(ctx, ps[l], &C->m[l + 1], mg[l + 1], cat[l] + up, enc[l + 1], width[l],
                    pin[l + 1], enc[l + 1]);
     }
-    float *bott = ctx->arena.alloc<float>((size_t)mb * enc[L + 1]);
-    conv_layer(ctx, net.layers[layer], pin[L], enc[L], nbr[L], mb, &C->m[L], mb, 1, bott,
+    float *bott = ctx->arena.alloc<float>((size_t)mbl[L] * enc[L + 1]);
+    conv_layer(ctx, net.layers[layer], pin[L], enc[L], nbr[L], mbl[L], &C->m[L], mbl[L], 1, bott,
                enc[L + 1], mg[L], kLevelSplit[std::min(L, 3)]);
     ++layer;
     const float *coarse = bott;
     int ld_coarse = enc[L + 1];
     for (int l = L - 1; l >= 0; --l) {
-        tconv_layer(ctx, net.layers[layer], coarse, ld_coarse, ps[l].c2p, ps[l].tap, &C->m[l], mb,
-                    1, cat[l], width[l], mg[l], ps[l].tmap, &ps[l].buckets, kTconvSplit);
+        tconv_layer(ctx, net.layers[layer], coarse, ld_coarse, ps[l].c2p, ps[l].tap, &C->m[l],
+                    mbl[l], 1, cat[l], width[l], mg[l], ps[l].tmap, &ps[l].buckets, kTconvSplit);
         ++layer;
         coarse = cat[l];
         ld_coarse = width[l];

@@ -644,17 +644,37 @@ __global__ void k_vbuild(const uint32_t *__restrict__ vs, const unsigned long lo
     }
 }
 
+// Pyramid capacity check: the fine / super entry buffers hold `cap` entries
+// (sized from the previous eager frame, not from the point count). When a
+// frame's runs ask for more, every run goes to the global list instead (all
+// runs in rank order; dead runs get an empty rect) — slower compositing for
+// that frame, identical planes.
+__global__ void k_entry_guard(DevCounts *__restrict__ C, int64_t cap) {
+    C->ef_req = C->ef;
+    C->es_req = C->es;
+    if (C->ef > cap || C->es > cap) {
+        C->overflow = 1;
+        C->ef = C->es = 0;
+        C->g = C->runs;
+    }
+}
+
 __global__ void k_emit(Runs R, const int32_t *__restrict__ fpos, const int32_t *__restrict__ spos,
                        const int32_t *__restrict__ gpos, int64_t ntx, int64_t nsx,
                        uint32_t *__restrict__ fkey, uint32_t *__restrict__ fval,
                        uint32_t *__restrict__ skey, uint32_t *__restrict__ sval,
-                       uint32_t *__restrict__ glist, int4 *__restrict__ grect) {
+                       uint32_t *__restrict__ glist, int4 *__restrict__ grect,
+                       const DevCounts *__restrict__ C) {
     const int64_t nr = *R.d_R;
+    const bool all_global = C->overflow != 0;
     SFB_FOR(r, nr) {
         R.count[r] -= R.start[r];   // k_run_build stored the run's end
         const int lvl = R.level[r];
         const int4 t = R.rect[r];
-        if (lvl == 0) {
+        if (all_global) {
+            glist[r] = (uint32_t)r;
+            grect[r] = lvl == 3 ? make_int4(1, 0, 1, 0) : t;
+        } else if (lvl == 0) {
             int32_t p = fpos[r];
             for (int y = t.z; y <= t.w; ++y)
                 for (int x = t.x; x <= t.y; ++x) {
@@ -1351,7 +1371,16 @@ void render_run(sfb_ctx *ctx, const RenderInputs &in, const FrameParams *FP, int
     R.ns = cnts + (nb + 1);
     R.ng = cnts + 2 * (nb + 1);
     int32_t *pos = ctx->arena.alloc<int32_t>(3 * (nb + 1));
-    const int64_t ebound = kFineMax * nb;   // at most kFineMax entries per run and level
+    // fine / super entry capacity: at most kFineMax per run and level; sized
+    // from the last eager frame's demand (x2, >= 64k), 4 M entries before
+    // any hint; a frame that needs more falls back to the global list
+    // (k_entry_guard), so the bound never has to cover kFineMax x points
+    const int64_t ebound =
+        ctx->entry_cap_override > 0
+            ? ctx->entry_cap_override
+            : std::min<int64_t>(kFineMax * nb, ctx->hint_e > 0
+                                                   ? std::max<int64_t>(2 * ctx->hint_e, int64_t(1) << 16)
+                                                   : int64_t(1) << 22);
     uint32_t *fkey = ctx->arena.alloc<uint32_t>(ebound), *fval = ctx->arena.alloc<uint32_t>(ebound);
     uint32_t *fkey2 = ctx->arena.alloc<uint32_t>(ebound), *fval2 = ctx->arena.alloc<uint32_t>(ebound);
     uint32_t *skey = ctx->arena.alloc<uint32_t>(ebound), *sval = ctx->arena.alloc<uint32_t>(ebound);
@@ -1388,8 +1417,10 @@ void render_run(sfb_ctx *ctx, const RenderInputs &in, const FrameParams *FP, int
         }
         dscan3(ctx, R.nf, R.ns, R.ng, pos, pos + (nb + 1), pos + 2 * (nb + 1), &C->runs1, nb + 1,
                &C->ef, &C->es, &C->g);
+        k_entry_guard<<<1, 1, 0, st>>>(C, ebound);
         k_emit<<<dgrid(ctx->grid_bound(n, ctx->hint_runs), 256), 256, 0, st>>>(
-            R, pos, pos + (nb + 1), pos + 2 * (nb + 1), ntx, nsx, fkey, fval, skey, sval, glist, grect);
+            R, pos, pos + (nb + 1), pos + 2 * (nb + 1), ntx, nsx, fkey, fval, skey, sval, glist, grect,
+            C);
         SFB_CHECK_LAUNCH();
         if ((scol && !by_voxel) || snrm) {
             k_gather_attrs<<<dgrid(n, 256), 256, 0, st>>>(src, in.point_to_geom, in.colors,

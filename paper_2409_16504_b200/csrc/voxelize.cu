@@ -322,6 +322,7 @@ void voxel_layout(const double *lo_hi, double s, FrameParams &P) {
         SFB_REQUIRE(lo > -(int64_t(1) << 20) && hi < (int64_t(1) << 20),
                     "voxel coordinates must satisfy |c| < 1048576");
         P.lo[a] = lo;
+        P.hi[a] = hi;
         P.bits[a] = bits_for((uint64_t)(hi - lo));
         P.total += P.bits[a];
     }

@@ -238,3 +238,24 @@ def test_staging_refuses_to_overwrite_unrendered(setup):
     rc = render_frame(c, w, cam, lane=5).rgb
     torch.cuda.synchronize()
     assert torch.equal(ra, rb) and torch.equal(ra, rc)
+
+
+def test_tile_list_overflow_falls_back_to_global_list(setup):
+    """Fine / super tile lists are sized from the previous frame's demand; a
+    frame that needs more renders every run from the global list: same
+    planes, bit for bit."""
+    from paper_2409_16504_b200 import _lib
+    pc, cloud, view, w = setup
+    cam = Camera.of(view)
+    want = render_frame(pc, w, cam, ("rgb", "normal"))
+    ctx = _lib.context()
+    ctx.lib.sfb_set_entry_capacity(ctx.handle, 1)
+    try:
+        got = render_frame(pc, w, cam, ("rgb", "normal"))
+        torch.cuda.synchronize()
+        st = stats()
+    finally:
+        ctx.lib.sfb_set_entry_capacity(ctx.handle, 0)
+    assert st["fine_entries"] == 0 and st["super_entries"] == 0 and st["global_entries"] == st["runs"]
+    for k in ("rgb", "normal", "transmittance"):
+        assert torch.equal(getattr(got, k), getattr(want, k)), k
