@@ -40,15 +40,20 @@ def main():
     ap.add_argument("out", nargs="?", default=str(ROOT / "gpurun_out" / "parity.json"))
     ap.add_argument("--c4-frames", type=int, default=64)
     ap.add_argument("--c5-views", type=int, default=32)
+    ap.add_argument("--c3-views", type=int, default=16)
+    ap.add_argument("--net-mode", default="tc_tf32x3",
+                    help="tc_tf32x3 (default, the bench's) or simt_f64 (the reference's float64 arithmetic)")
     a = ap.parse_args()
+    from paper_2409_16504_b200 import sparsenet
+    sparsenet.set_mode(a.net_mode)
     w = netplan.init_random(netplan.NetworkPlan(), 0)
-    rep = {"tolerance": 2e-3, "configs": {}}
+    rep = {"tolerance": 2e-3, "net_mode": a.net_mode, "configs": {}}
     cloud, views = scenes.config1()
     rep["configs"]["c1"] = run(cloud, views, w, range(len(views)), "c1")
     cloud, views = scenes.config2()
     rep["configs"]["c2"] = run(cloud, views, w, range(len(views)), "c2")
     cloud, views = scenes.config3()
-    rep["configs"]["c3"] = run(cloud, views, w, range(len(views)), "c3")
+    rep["configs"]["c3"] = run(cloud, views, w, range(min(a.c3_views, len(views))), "c3")
     c4 = []
     for f in range(a.c4_frames):
         cloud, views = scenes.config4_frame(f)
