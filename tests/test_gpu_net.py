@@ -133,7 +133,7 @@ def test_transposed_conv_children_and_orphans():
             want[i] += g[pidx[i]] @ w.reshape(8, 6, 4)[tap[i]].astype(np.float64)
     # the output grid is canonical (sorted by packed key, voxelgrid.py:72-79):
     # compare row by coordinate
-    rows = np_(out.lookup(kids))
+    rows = out.lookup(kids).cpu().numpy()
     assert (rows >= 0).all()
     got = np_(out.feats)[rows]
     np.testing.assert_allclose(got, want, rtol=0, atol=1e-5)
