@@ -24,7 +24,10 @@
 //    tiles go to a workspace and a deterministic reduce kernel sums them in
 //    split order, adds the bias and applies ReLU (bitwise run-to-run stable).
 #include <cooperative_groups.h>
+#include <cuda.h>   // CUtensorMap (the encode entry point comes through the runtime)
 #include <cuda_bf16.h>
+
+#include <mutex>
 
 #include "common.cuh"
 
@@ -101,6 +104,19 @@ __device__ __forceinline__ void tma_bulk_g2s(void *dst, const void *src, uint32_
         : "memory");
 }
 
+// TMA row gather (sm_100 tile::gather4): rows r0..r3 of the 2D feature
+// tensor behind `tm` (box = KP columns x 1 row), columns from `col`, land as
+// four consecutive KP-float rows at `dst`; rows past the tensor read as zeros
+__device__ __forceinline__ void tma_gather4(void *dst, const CUtensorMap *tm, int col, int r0, int r1,
+                                           int r2, int r3, uint64_t *bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cta.global.tile::gather4.mbarrier::complete_tx::bytes "
+        "[%0], [%1, {%2, %3, %4, %5, %6}], [%7];" ::"r"(smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(tm)), "r"(col), "r"(r0), "r"(r1), "r"(r2), "r"(r3),
+        "r"(smem_u32(bar))
+        : "memory");
+}
+
 __device__ __forceinline__ void mma_tf32(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t idesc,
                                          uint32_t accumulate) {
     asm volatile(
@@ -169,8 +185,15 @@ struct TcShape {
     // the stage buffers double as the cluster split-K reduction tile [kM][NP]
     static constexpr int BUF_FLOATS = STAGES * STAGE_FLOATS + B_EXTRA > kM * NP ? STAGES * STAGE_FLOATS + B_EXTRA
                                                                                  : kM * NP;
+    // TMA-staged A rows (fp32 tf32x3 path, KP <= 64): a ring of RS raw stages
+    // of TAPB x 128 gathered rows, filled RS-1 batches ahead by gather4
+    static constexpr bool TMA_OK = !BF && KP <= 64;
+    static constexpr int RS = KP <= 32 ? 3 : 2;
+    static constexpr int RAW_FLOATS = TMA_OK ? RS * TAPB * kM * KP : 0;
+    static constexpr int RAW_OFF = (BUF_FLOATS * 4 + 1023) / 1024 * 1024 / 4;   // floats, 1 KB aligned
+    static constexpr int BAR_OFF = RAW_OFF + RAW_FLOATS;
     // + the kernel-map rows of one item's taps, sized per launch (src_rows)
-    static constexpr int SMEM = BUF_FLOATS * 4 + 1024 + 64;
+    static constexpr int SMEM = BAR_OFF * 4 + 1024 + 128;
     static constexpr int smem_bytes(int src_rows) { return SMEM + src_rows * kM * 4; }
     // two accumulators (tap t in buffer t % 2): the epilogue of tap t-1 reads
     // one while the MMAs of tap t write the other
@@ -202,7 +225,8 @@ k_conv_tc(const float *__restrict__ in, int ld_in, int cin, const int32_t *__res
           const float *__restrict__ wtc, const float *__restrict__ bias, int cout, int relu,
           float *__restrict__ out, int ld_out, float *__restrict__ partial,
           const int32_t *__restrict__ row_map, const int32_t *__restrict__ tap_off,
-          int cluster_splits, int src_rows, int vec4) {
+          int cluster_splits, int src_rows, int vec4, const __grid_constant__ CUtensorMap tmA,
+          int tma, int oob_row) {
     // cluster mode (cluster_splits > 1): the splits of a tile are the CTAs of
     // one thread-block cluster; partial tiles meet in distributed shared
     // memory and each CTA reduces a slice of the tile's rows in split order —
@@ -215,11 +239,13 @@ k_conv_tc(const float *__restrict__ in, int ld_in, int cin, const int32_t *__res
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     float *stage_base = reinterpret_cast<float *>(
         (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-    uint64_t *bar_full = reinterpret_cast<uint64_t *>(stage_base + S::BUF_FLOATS);
+    float *raw = stage_base + S::RAW_OFF;   // TMA ring [RS][TAPB][kM][KP]
+    uint64_t *bar_full = reinterpret_cast<uint64_t *>(stage_base + S::BAR_OFF);
     uint64_t *bar_done = bar_full + 2;   // indexed by batch parity (i & 1), phase i >> 1
-    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(bar_done + 2);
+    uint64_t *raw_full = bar_done + 2;   // [RS]: stage s's rows landed
+    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(raw_full + 4);
     // kernel-map rows of this item's taps: s_src[t - t0][tid]
-    int32_t (*s_src)[kM] = reinterpret_cast<int32_t (*)[kM]>(stage_base + S::BUF_FLOATS + 16);
+    int32_t (*s_src)[kM] = reinterpret_cast<int32_t (*)[kM]>(stage_base + S::BAR_OFF + 32);
 
     const int tid = threadIdx.x, warp = tid >> 5;
     const int64_t m = d_m ? *d_m : m_fixed;
@@ -236,8 +262,10 @@ k_conv_tc(const float *__restrict__ in, int ld_in, int cin, const int32_t *__res
             mbar_init(&bar_full[s], 1);
             mbar_init(&bar_done[s], 1);
         }
+        for (int s = 0; s < 4; ++s) mbar_init(&raw_full[s], 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
+    const bool use_tma = S::TMA_OK && tma != 0;
     if (warp == 0) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
                          smem_u32(tmem_slot)),
@@ -331,8 +359,40 @@ k_conv_tc(const float *__restrict__ in, int ld_in, int cin, const int32_t *__res
                 }
             }
         };
+        // TMA mode: warp 0 gathers the rows of the item's batches RS ahead into
+        // the raw ring (all threads track the batch sequence, only warp 0
+        // issues); the threads then read their rows from shared memory instead
+        // of holding a register prefetch
+        uint32_t pmask = mask;
+        const int g0 = issued;   // global batch index of this item's first batch
+        int npref = 0;
+        auto prefetch = [&]() {
+            int pt[TB], pn = 0;
+            while (pmask && pn < TB) {
+                pt[pn++] = t0 + __ffs(pmask) - 1;
+                pmask &= pmask - 1;
+            }
+            if (pn == 0) return;
+            const int stg = (g0 + npref++) % S::RS;
+            if (warp == 0) {
+                if (tid == 0) mbar_expect_tx(&raw_full[stg], (uint32_t)(pn * kM * KP * 4));
+                __syncwarp();
+                float *dst = raw + (size_t)stg * TB * kM * KP;
+                for (int q = 0; q < pn; ++q) {
+                    const int32_t *sr = s_src[pt[q] - t0] + 4 * tid;
+                    const int r0 = sr[0] >= 0 ? sr[0] : oob_row, r1 = sr[1] >= 0 ? sr[1] : oob_row,
+                              r2 = sr[2] >= 0 ? sr[2] : oob_row, r3 = sr[3] >= 0 ? sr[3] : oob_row;
+                    tma_gather4(dst + (size_t)q * kM * KP + (size_t)4 * tid * KP, &tmA, 0, r0, r1, r2, r3,
+                                &raw_full[stg]);
+                }
+            }
+        };
         take();
-        if (nxt_n) fetch();
+        if (use_tma) {
+            for (int k = 0; k < S::RS; ++k) prefetch();
+        } else if (nxt_n) {
+            fetch();
+        }
         // weights: with two stages, batch k+1's tiles are fetched (TMA) as soon
         // as batch k-1 has drained, so their latency hides behind batch k
         auto b_slot = [&](int slot) {   // weight buffer of a slot
@@ -367,6 +427,23 @@ k_conv_tc(const float *__restrict__ in, int ld_in, int cin, const int32_t *__res
                 mbar_wait(&bar_done[j & 1], (j >> 1) & 1);
             }
             if (tid == 0 && ((S::STAGES == 1 && !S::BDB) || item_issued == 0)) load_w(cur_t, cur_n, ws);
+            if (use_tma) {   // this batch's rows, gathered RS batches ago
+                const int stg = issued % S::RS;
+                mbar_wait(&raw_full[stg], (uint32_t)(issued / S::RS) & 1u);
+                const float *src = raw + (size_t)stg * TB * kM * KP + (size_t)tid * KP;
+#pragma unroll
+                for (int q = 0; q < TB; ++q) {
+                    if (q >= cur_n) break;
+#pragma unroll
+                    for (int k = 0; k < KP; k += 4) {
+                        const float4 f = *reinterpret_cast<const float4 *>(src + (size_t)q * kM * KP + k);
+                        v[q][k] = f.x;
+                        v[q][k + 1] = f.y;
+                        v[q][k + 2] = f.z;
+                        v[q][k + 3] = f.w;
+                    }
+                }
+            }
             // my row of each tap of the batch in the canonical layout: bf16, or tf32 hi/lo
 #pragma unroll
             for (int q = 0; q < TB; ++q) {
@@ -406,12 +483,13 @@ k_conv_tc(const float *__restrict__ in, int ld_in, int cin, const int32_t *__res
                 }
             }
             take();
-            if (nxt_n) fetch();   // next batch's rows, in flight from here
+            if (nxt_n && !use_tma) fetch();   // next batch's rows, in flight from here
             // next batch's weights: its slot was last read by batch issued-1,
             // complete since the wait above
             if (S::BDB && tid == 0 && nxt_n) load_w(nxt_t, nxt_n, (issued + 1) & 1);
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
             __syncthreads();   // also orders the last drain's TMEM reads before these MMAs
+            if (use_tma) prefetch();   // batch issued + RS into the stage just read
             if (tid == 0) {
                 mbar_wait(&bar_full[ws], use & 1);
                 asm volatile("tcgen05.fence::after_thread_sync;");

@@ -347,15 +347,6 @@ __device__ __forceinline__ double support_radius(double a, double b, double c, d
     return sqrt(fmax(sup, 0.0) * lam) + 1e-9;
 }
 
-// Alpha-support test of a whole tile. forward_kernel blends a splat at a
-// pixel only if alpha = min(o exp(-q/2), alpha_max) >= 1/255, i.e. only if
-// q <= 2 ln(255 o). q_cut widens that bound by a relative 1e-6 (+1e-6), far
-// beyond the float64 rounding of q and of the exp, so skipping a run whose
-// q exceeds q_cut at every pixel of a tile never drops a contribution.
-__device__ __forceinline__ double q_cut(double op) {
-    return 2.0 * log(fmax(255.0 * op, 1e-300)) * (1.0 + 1e-6) + 1e-6;
-}
-
 struct TileRect {
     int32_t x0, x1, y0, y1;
 };
@@ -414,8 +405,7 @@ struct Runs {
     RunRec *rec;
     RunAux *aux;
     int32_t *start, *count;
-    int4 *rect;    // bin_tiles' tile range (_raster_kernels.py:123-130), as the reference
-    int4 *brect;   // the part of it the alpha-support ellipse can reach: what is binned
+    int4 *rect;
     uint8_t *level;  // 0 fine, 1 super, 2 global, 3 dead
     int32_t *nf, *ns, *ng;  // per-run entry counts
     const int64_t *d_R;
@@ -438,27 +428,8 @@ __device__ __forceinline__ void run_geometry(Runs &R, int64_t r, int64_t g, cons
     q.ic = a / det;
     q.op = op;
     q.rad = rad;
-    const TileRect t0 = tile_rect(P.sx[g], P.sy[g], rad, ft, ntx, nty);
-    R.rect[r] = make_int4(t0.x0, t0.x1, t0.y0, t0.y1);
-    // a pixel takes the splat only where alpha >= 1/255, i.e. q <= 2 ln(255 o):
-    // inside the ellipse whose axis-aligned half-extents are sqrt(qmax a) and
-    // sqrt(qmax c) (a, c = the screen covariance diagonal). Bin the tiles of
-    // that box (widened by q_cut's margin) within the reference range; the
-    // runs left out of a tile have alpha < 1/255 at all of its pixels.
-    TileRect t = t0;
-    {
-        const double qc = q_cut(op);
-        if (qc > 0.0) {
-            const double hx = sqrt(qc * a) * (1.0 + 1e-6) + 1e-6, hy = sqrt(qc * c) * (1.0 + 1e-6) + 1e-6;
-            const TileRect ex = tile_rect(P.sx[g], P.sy[g], hx, ft, ntx, nty);
-            const TileRect ey = tile_rect(P.sx[g], P.sy[g], hy, ft, ntx, nty);
-            t.x0 = max(t0.x0, ex.x0);
-            t.x1 = min(t0.x1, ex.x1);
-            t.y0 = max(t0.y0, ey.y0);
-            t.y1 = min(t0.y1, ey.y1);
-        }
-    }
-    R.brect[r] = make_int4(t.x0, t.x1, t.y0, t.y1);
+    const TileRect t = tile_rect(P.sx[g], P.sy[g], rad, ft, ntx, nty);
+    R.rect[r] = make_int4(t.x0, t.x1, t.y0, t.y1);
     int lvl = 3, nf = 0, ns = 0, ng = 0;
     const bool live = !(op < kCutoff) && !(alpha_max < kCutoff) && t.x0 <= t.x1 && t.y0 <= t.y1;
     if (live) {
@@ -699,7 +670,7 @@ __global__ void k_emit(Runs R, const int32_t *__restrict__ fpos, const int32_t *
     SFB_FOR(r, nr) {
         R.count[r] -= R.start[r];   // k_run_build stored the run's end
         const int lvl = R.level[r];
-        const int4 t = R.brect[r];
+        const int4 t = R.rect[r];
         if (all_global) {
             glist[r] = (uint32_t)r;
             grect[r] = lvl == 3 ? make_int4(1, 0, 1, 0) : t;
@@ -860,6 +831,15 @@ __device__ __forceinline__ double exp_nonpos(double x) {
     return p * __longlong_as_double((long long)(k + 1023) << 52);
 }
 
+// Alpha-support test of a whole tile. forward_kernel blends a splat at a
+// pixel only if alpha = min(o exp(-q/2), alpha_max) >= 1/255, i.e. only if
+// q <= 2 ln(255 o). q_cut widens that bound by a relative 1e-6 (+1e-6), far
+// beyond the float64 rounding of q and of the exp, so skipping a run whose
+// q exceeds q_cut at every pixel of a tile never drops a contribution.
+__device__ __forceinline__ double q_cut(double op) {
+    return 2.0 * log(fmax(255.0 * op, 1e-300)) * (1.0 + 1e-6) + 1e-6;
+}
+
 // min over the rectangle [x0,x1] x [y0,y1] (offsets from the centre) of the
 // positive-definite form q(d) = ia dx^2 + 2 ib dx dy + ic dy^2: 0 when the
 // centre is inside, else the least of the four edge minima (a 1-D quadratic
@@ -951,14 +931,15 @@ __global__ void __launch_bounds__(kCT, kCompMinBlocks) k_composite(CompParams P)
     __shared__ int s_nlist;
     __shared__ uint32_t s_add[3];
     __shared__ uint32_t s_head;
-    // each warp stages its own chunk of 32 candidate runs (record + the pixel
-    // box clamped to the warp's quadrant)
-    constexpr int NW = kCT / 32;
-    __shared__ double s_mx[NW][32], s_my[NW][32], s_rr[NW][32], s_ia[NW][32], s_ib[NW][32],
-        s_ic[NW][32], s_op[NW][32], s_dep[NW][32], s_rn[NW][3][32];
-    __shared__ int32_t s_x0[NW][32], s_x1[NW][32], s_y0[NW][32], s_y1[NW][32], s_start[NW][32],
-        s_count[NW][32];
-    __shared__ uint8_t s_uni[NW][32], s_full[NW][32];   // full: box and circle cover the quadrant
+    __shared__ unsigned s_bal[kCT / 32];
+    __shared__ uint8_t r_idx[kChunk];   // staged slot of the chunk's e-th surviving run
+    // the current chunk's run records (pixel box precomputed per run)
+    __shared__ double r_mx[kChunk], r_my[kChunk], r_rr[kChunk], r_ia[kChunk], r_ib[kChunk],
+        r_ic[kChunk], r_op[kChunk], r_dep[kChunk], r_rn[3][kChunk];
+    __shared__ int32_t r_x0[kChunk], r_x1[kChunk], r_y0[kChunk], r_y1[kChunk], r_start[kChunk],
+        r_count[kChunk];
+    __shared__ uint8_t r_uni[kChunk];
+    __shared__ uint8_t r_full[kChunk];   // run's pixel box and circle cover the whole tile
 
     const int64_t t = blockIdx.x;
     const uint32_t ntx32 = (uint32_t)P.ntx;   // 32-bit division: the grid is < 2^31 tiles
@@ -972,22 +953,15 @@ __global__ void __launch_bounds__(kCT, kCompMinBlocks) k_composite(CompParams P)
     constexpr bool want_d = MASK & SFB_PLANE_DEPTH;
     const bool term = P.terminate;
 
-    // warp w owns quadrant (w & 1, w >> 1) of the tile: h x h pixels, NPIX
-    // per lane; every warp walks the tile's candidate runs on its own (no
-    // block barrier inside the blend loop) and culls them against its quadrant
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int h = (TS + 1) >> 1;
-    const int32_t qx0 = x_lo + (warp & 1) * h, qy0 = y_lo + (warp >> 1) * h;
-    const int32_t qx1 = min(qx0 + h, x_end), qy1 = min(qy0 + h, y_end);   // exclusive
     int32_t pxs[NPIX], pys[NPIX];
     bool valid[NPIX];
     double T[NPIX], c0[NPIX], c1[NPIX], c2[NPIX], n0[NPIX], n1[NPIX], n2[NPIX], dd[NPIX];
 #pragma unroll
     for (int k = 0; k < NPIX; ++k) {
-        const uint32_t p = lane + k * 32;
-        pxs[k] = (int32_t)(qx0 + p % (uint32_t)h);
-        pys[k] = (int32_t)(qy0 + p / (uint32_t)h);
-        valid[k] = p < (uint32_t)(h * h) && pxs[k] < qx1 && pys[k] < qy1;
+        const uint32_t p = threadIdx.x + k * kCT;
+        pxs[k] = (int32_t)(x_lo + p % (uint32_t)TS);
+        pys[k] = (int32_t)(y_lo + p / (uint32_t)TS);
+        valid[k] = p < TS * TS && pxs[k] < x_end && pys[k] < y_end;
         T[k] = 1.0;
         c0[k] = c1[k] = c2[k] = n0[k] = n1[k] = n2[k] = dd[k] = 0.0;
     }
@@ -1088,83 +1062,100 @@ __global__ void __launch_bounds__(kCT, kCompMinBlocks) k_composite(CompParams P)
         }
         __syncthreads();
         const int nlist = s_nlist;
-        // this warp: candidates in chunks of 32 (one per lane staged, culled
-        // against the quadrant: outside the pixel box, or the alpha-support
-        // ellipse misses the quadrant => alpha < 1/255 at all of its pixels,
-        // so forward_kernel would skip the run there, _raster_kernels.py:193-194)
-        bool wdone = term && __all_sync(0xffffffffu, saturated());
-        for (int base = 0; base < nlist && !wdone; base += 32) {
-            const int nc = min(32, nlist - base);
+        // chunks of candidate runs grow 16 -> 128: most tiles saturate within
+        // the first few contributing runs. Each candidate is staged by one
+        // thread, which also drops it when its alpha-support ellipse misses the
+        // tile's pixels (tile_min_q): such a run has alpha < 1/255 at every
+        // pixel of the tile, so forward_kernel's per-pixel test skips it
+        // everywhere (_raster_kernels.py:193-194). Survivors are compacted in
+        // rank order.
+        int chunk = 16;
+        for (int base = 0; base < nlist && !done; base += chunk, chunk = min(2 * chunk, kChunk)) {
+            const int nc = min(chunk, nlist - base);
             bool keep = false;
-            if (lane < nc) {
-                const uint32_t r = list[base + lane];
+            if (threadIdx.x < nc) {
+                const uint32_t r = list[base + threadIdx.x];
+                const int j = threadIdx.x;
                 const double2 q0 = Rrec[4 * (size_t)r], q1 = Rrec[4 * (size_t)r + 1],
                               q2 = Rrec[4 * (size_t)r + 2], q3 = Rrec[4 * (size_t)r + 3];
+                const double2 a0 = Raux[3 * (size_t)r], a1 = Raux[3 * (size_t)r + 1],
+                              a2 = Raux[3 * (size_t)r + 2];
                 const double mx = q0.x, my = q0.y;
                 const double rad = q3.x + 1.0;
-                // pixel box of forward_kernel (_raster_kernels.py:178-181), clamped to the quadrant
-                const int32_t bx0 = (int32_t)fmin(fmax((double)qx0, ceil(mx - rad)), (double)qx1);
-                const int32_t bx1 = (int32_t)fmax(fmin((double)(qx1 - 1), floor(mx + rad)), (double)(qx0 - 1));
-                const int32_t by0 = (int32_t)fmin(fmax((double)qy0, ceil(my - rad)), (double)qy1);
-                const int32_t by1 = (int32_t)fmax(fmin((double)(qy1 - 1), floor(my + rad)), (double)(qy0 - 1));
+                r_mx[j] = mx;
+                r_my[j] = my;
+                r_rr[j] = rad * rad;
+                r_ia[j] = q1.x;
+                r_ib[j] = q1.y;
+                r_ic[j] = q2.x;
+                r_op[j] = q2.y;
+                r_dep[j] = q3.y;
+                // RunAux as double2: {rn0, rn1}, {rn2, (start, count)}, {(uni, pad), -}
+                r_start[j] = __double2loint(a1.y);
+                r_count[j] = __double2hiint(a1.y);
+                r_uni[j] = (uint8_t)__double2loint(a2.x);
+                if (want_n) {
+                    r_rn[0][j] = a0.x;
+                    r_rn[1][j] = a0.y;
+                    r_rn[2][j] = a1.x;
+                }
+                // pixel box of forward_kernel (_raster_kernels.py:178-181), clamped to the tile
+                const int32_t bx0 = (int32_t)fmin(fmax((double)x_lo, ceil(mx - rad)), (double)x_end);
+                const int32_t bx1 = (int32_t)fmax(fmin((double)(x_end - 1), floor(mx + rad)), (double)(x_lo - 1));
+                const int32_t by0 = (int32_t)fmin(fmax((double)y_lo, ceil(my - rad)), (double)y_end);
+                const int32_t by1 = (int32_t)fmax(fmin((double)(y_end - 1), floor(my + rad)), (double)(y_lo - 1));
+                r_x0[j] = bx0;
+                r_x1[j] = bx1;
+                r_y0[j] = by0;
+                r_y1[j] = by1;
+                // whole tile inside the box and the circle (farthest corner
+                // within the radius): the per-pixel tests are then all true
+                const double fx = fmax(fabs((double)x_lo - mx), fabs((double)(x_end - 1) - mx));
+                const double fy = fmax(fabs((double)y_lo - my), fabs((double)(y_end - 1) - my));
+                r_full[j] = bx0 == x_lo && bx1 == x_end - 1 && by0 == y_lo && by1 == y_end - 1 &&
+                            fx * fx + fy * fy <= rad * rad;
                 keep = bx0 <= bx1 && by0 <= by1 &&
                        !(tile_min_q(q1.x, q1.y, q2.x, bx0 - mx, bx1 - mx, by0 - my, by1 - my) >
                          q_cut(q2.y));
-                if (keep) {
-                    const double2 a0 = Raux[3 * (size_t)r], a1 = Raux[3 * (size_t)r + 1],
-                                  a2 = Raux[3 * (size_t)r + 2];
-                    s_mx[warp][lane] = mx;
-                    s_my[warp][lane] = my;
-                    s_rr[warp][lane] = rad * rad;
-                    s_ia[warp][lane] = q1.x;
-                    s_ib[warp][lane] = q1.y;
-                    s_ic[warp][lane] = q2.x;
-                    s_op[warp][lane] = q2.y;
-                    s_dep[warp][lane] = q3.y;
-                    // RunAux as double2: {rn0, rn1}, {rn2, (start, count)}, {(uni, pad), -}
-                    s_start[warp][lane] = __double2loint(a1.y);
-                    s_count[warp][lane] = __double2hiint(a1.y);
-                    s_uni[warp][lane] = (uint8_t)__double2loint(a2.x);
-                    if (want_n) {
-                        s_rn[warp][0][lane] = a0.x;
-                        s_rn[warp][1][lane] = a0.y;
-                        s_rn[warp][2][lane] = a1.x;
-                    }
-                    s_x0[warp][lane] = bx0;
-                    s_x1[warp][lane] = bx1;
-                    s_y0[warp][lane] = by0;
-                    s_y1[warp][lane] = by1;
-                    // whole quadrant inside the box and the circle (farthest
-                    // corner within the radius): the per-pixel tests all pass
-                    const double fx = fmax(fabs((double)qx0 - mx), fabs((double)(qx1 - 1) - mx));
-                    const double fy = fmax(fabs((double)qy0 - my), fabs((double)(qy1 - 1) - my));
-                    s_full[warp][lane] = bx0 == qx0 && bx1 == qx1 - 1 && by0 == qy0 &&
-                                         by1 == qy1 - 1 && fx * fx + fy * fy <= rad * rad;
-                }
             }
-            unsigned todo = __ballot_sync(0xffffffffu, keep);
-            __syncwarp();
-            while (todo) {   // survivors in rank order
-                const int f = __ffs(todo) - 1;
-                todo &= todo - 1;
+            const unsigned ball = __ballot_sync(0xffffffffu, keep);
+            if ((threadIdx.x & 31) == 0) s_bal[threadIdx.x >> 5] = ball;
+            __syncthreads();
+            int slot = __popc(ball & ((1u << (threadIdx.x & 31)) - 1u)), nb = 0;
+#pragma unroll
+            for (int w = 0; w < kCT / 32; ++w) {
+                const int c = __popc(s_bal[w]);
+                slot += w < (int)(threadIdx.x >> 5) ? c : 0;
+                nb += c;
+            }
+            if (keep) r_idx[slot] = (uint8_t)threadIdx.x;   // survivors in rank order
+            __syncthreads();
+            for (int e = 0; e < nb; ++e) {
+                if (term && e && (e & 31) == 0 && __syncthreads_and(saturated())) {
+                    done = true;
+                    break;
+                }
+                if (term && __all_sync(0xffffffffu, saturated())) {
+                    e |= 31;   // my warp is finished: skip to the next block checkpoint
+                    continue;
+                }
+                const int f = r_idx[e];
 #pragma unroll
                 for (int k = 0; k < NPIX; ++k) {
                     if (!valid[k]) continue;
                     if (term && T[k] < kCutoff) continue;
-                    const double dx = (double)pxs[k] - s_mx[warp][f], dy = (double)pys[k] - s_my[warp][f];
-                    if (!s_full[warp][f]) {
-                        if (pxs[k] < s_x0[warp][f] || pxs[k] > s_x1[warp][f] || pys[k] < s_y0[warp][f] ||
-                            pys[k] > s_y1[warp][f])
+                    const double dx = (double)pxs[k] - r_mx[f], dy = (double)pys[k] - r_my[f];
+                    if (!r_full[f]) {
+                        if (pxs[k] < r_x0[f] || pxs[k] > r_x1[f] || pys[k] < r_y0[f] || pys[k] > r_y1[f])
                             continue;
-                        if (dx * dx + dy * dy > s_rr[warp][f]) continue;
+                        if (dx * dx + dy * dy > r_rr[f]) continue;
                     }
-                    const double q = s_ia[warp][f] * dx * dx + 2.0 * s_ib[warp][f] * dx * dy +
-                                     s_ic[warp][f] * dy * dy;
-                    double alpha = s_op[warp][f] * exp_nonpos(-0.5 * q);
+                    const double q = r_ia[f] * dx * dx + 2.0 * r_ib[f] * dx * dy + r_ic[f] * dy * dy;
+                    double alpha = r_op[f] * exp_nonpos(-0.5 * q);
                     if (alpha > alpha_max) alpha = alpha_max;
                     if (alpha < kCutoff) continue;
                     const double om = 1.0 - alpha;
-                    const int32_t b0 = s_start[warp][f], cnt = s_count[warp][f];
+                    const int32_t b0 = r_start[f], cnt = r_count[f];
                     const double T0 = T[k];
                     int m = cnt;
                     double Tend;
@@ -1199,10 +1190,10 @@ __global__ void __launch_bounds__(kCT, kCompMinBlocks) k_composite(CompParams P)
                         c2[k] = __fma_rn(wa, (double)S.z, c2[k]);
                     }
                     if (want_n) {
-                        if (s_uni[warp][f]) {
-                            n0[k] = __fma_rn(wsum, s_rn[warp][0][f], n0[k]);
-                            n1[k] = __fma_rn(wsum, s_rn[warp][1][f], n1[k]);
-                            n2[k] = __fma_rn(wsum, s_rn[warp][2][f], n2[k]);
+                        if (r_uni[f]) {
+                            n0[k] = __fma_rn(wsum, r_rn[0][f], n0[k]);
+                            n1[k] = __fma_rn(wsum, r_rn[1][f], n1[k]);
+                            n2[k] = __fma_rn(wsum, r_rn[2][f], n2[k]);
                         } else {
                             const float3 S = horner3(snrm + b0, m, omf);
                             n0[k] = __fma_rn(wa, (double)S.x, n0[k]);
@@ -1210,16 +1201,14 @@ __global__ void __launch_bounds__(kCT, kCompMinBlocks) k_composite(CompParams P)
                             n2[k] = __fma_rn(wa, (double)S.z, n2[k]);
                         }
                     }
-                    if (want_d) dd[k] = __fma_rn(wsum, s_dep[warp][f], dd[k]);
+                    if (want_d) dd[k] = __fma_rn(wsum, r_dep[f], dd[k]);
                     T[k] = Tend;
                 }
             }
-            __syncwarp();   // the staging slots are rewritten by the next chunk
-            if (term) wdone = __all_sync(0xffffffffu, saturated());
+            if (done) break;
+            if (term) done = __syncthreads_and(saturated());
+            else __syncthreads();
         }
-        // a next rank window only if some quadrant is still open
-        done = term ? __syncthreads_and(wdone) : false;
-        if (!done) __syncthreads();   // list[] is rebuilt by the next window
         ws = min(ws * 2, kWin);
         if (P.dbg && threadIdx.x == 0) {
             atomicAdd((unsigned long long *)&P.dbg[4 * t + 0], 1ull);
@@ -1376,7 +1365,6 @@ void render_run(sfb_ctx *ctx, const RenderInputs &in, const FrameParams *FP, int
     R.count = ctx->arena.alloc<int32_t>(nb);
 
     R.rect = ctx->arena.alloc<int4>(nb);
-    R.brect = ctx->arena.alloc<int4>(nb);
     R.level = ctx->arena.alloc<uint8_t>(nb);
     int32_t *cnts = ctx->arena.alloc<int32_t>(3 * (nb + 1));
     R.nf = cnts;
@@ -1453,7 +1441,7 @@ void render_run(sfb_ctx *ctx, const RenderInputs &in, const FrameParams *FP, int
     // tile offsets by binary search in the sorted keys (no histogram / scan),
     // and the super-list rects in list order, in one launch
     k_tile_index<<<dgrid(std::max<int64_t>(ebound, nt + ns + 2), 256), 256, 0, st>>>(
-        fk_sorted, &C->ef, sk_sorted, &C->es, s_ids, R.brect, nt, ns, f_off, s_off, srect);
+        fk_sorted, &C->ef, sk_sorted, &C->es, s_ids, R.rect, nt, ns, f_off, s_off, srect);
     SFB_CHECK_LAUNCH();
     ctx->mark(ST_BIN);
 
@@ -1487,14 +1475,12 @@ void render_run(sfb_ctx *ctx, const RenderInputs &in, const FrameParams *FP, int
     CP.dbg = ctx->debug_counters;
     const int cm = plane_mask & 7;
     {
-    // pixels per lane: each of the 4 warps owns an h x h quadrant, h = ceil(TS / 2)
-    const int hq = (TS + 1) / 2;
-    static_assert(kCT == 128, "the compositor's quadrant split assumes 4 warps per tile");
+    constexpr int kNpixMid = (256 + kCT - 1) / kCT, kNpixMax = (1024 + kCT - 1) / kCT;
 #define SFB_COMP_CASE(M)                                                          \
     if (cm == M) {                                                                \
-        if (hq * hq <= 32) k_composite<1, M><<<(unsigned)nt, kCT, 0, st>>>(CP);   \
-        else if (hq * hq <= 64) k_composite<2, M><<<(unsigned)nt, kCT, 0, st>>>(CP); \
-        else k_composite<8, M><<<(unsigned)nt, kCT, 0, st>>>(CP);                 \
+        if (TS * TS <= kCT) k_composite<1, M><<<(unsigned)nt, kCT, 0, st>>>(CP);  \
+        else if (TS * TS <= 256) k_composite<kNpixMid, M><<<(unsigned)nt, kCT, 0, st>>>(CP); \
+        else k_composite<kNpixMax, M><<<(unsigned)nt, kCT, 0, st>>>(CP);          \
     }
     SFB_COMP_CASE(0) SFB_COMP_CASE(1) SFB_COMP_CASE(2) SFB_COMP_CASE(3)
     SFB_COMP_CASE(4) SFB_COMP_CASE(5) SFB_COMP_CASE(6) SFB_COMP_CASE(7)
