@@ -380,14 +380,18 @@ def run_ours(args):
     ctx = _lib.context()
     ctx.set_timing(True)
     stage_acc = {}
+    comp_by_view = {}
     n_stage = min(args.steps, 16)
     for i in range(n_stage):
         flush.zero_()
         render_frame(dev_clouds[0], weights, view_of(i), planes, out=outs[0][0])
         for k, v in ctx.stage_times().items():
             stage_acc[k] = stage_acc.get(k, 0.0) + v
+            if k == "composite":   # the compositor's cost depends on the view
+                comp_by_view.setdefault(unit_of(i, rank, world, len(cams)), []).append(v)
     ctx.set_timing(False)
     stage_ms = {k: v / n_stage for k, v in stage_acc.items()}
+    comp_by_view = {u: sum(v) / len(v) for u, v in sorted(comp_by_view.items())}
 
     # ---- e2e: public API with pinned HOST buffers, copies inside every step
     e2e = None
@@ -520,7 +524,8 @@ def run_ours(args):
                                          + " convs; fp64 geometry / compositing"},
             "latency_ms_per_frame": lat_ms,
             "e2e": e2e, "gpu_launches": launches, "roofline": roof, "cpu_baseline": cpu,
-            "clocks": clk, "stages_ms_eager": stage_ms, "stats": st,
+            "clocks": clk, "stages_ms_eager": stage_ms, "composite_ms_by_view": comp_by_view,
+            "stats": st,
             "host_enqueue_ms_per_step": 1e3 * host_s / args.steps,
         }
         print(json.dumps(line), flush=True)

@@ -157,6 +157,7 @@ struct sfb_ctx {
     int64_t *debug_counters = nullptr;   // compositor per-tile counters (diagnostics)
     sfb::FrameDebug frame_debug;         // fused-frame parity export (tests)
     int64_t entry_cap_override = 0;      // tests: pyramid entry capacity (0 = automatic)
+    bool conv_tma = true;                // tcgen05 convs stage A rows by TMA gather4
     sfb::DevCounts *last_counts = nullptr;   // device counts of the last call
     // launch-size hints (host copies of the counts of the last eager frame):
     // every kernel loops over its device count, so hints only size grids

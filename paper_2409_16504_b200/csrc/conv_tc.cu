@@ -630,6 +630,41 @@ __global__ void k_prep_weights_bf16(const float *__restrict__ w, int taps, int c
 int pad_k(int c) { return c <= 16 ? 16 : (c <= 32 ? 32 : (c <= 64 ? 64 : 128)); }
 int pad_n(int c) { return c <= 16 ? 16 : (c <= 32 ? 32 : (c <= 64 ? 64 : (c <= 128 ? 128 : 256))); }
 
+// cuTensorMapEncodeTiled through the runtime's driver entry point (the
+// library links only the static cudart)
+using EncodeTiled = CUresult (*)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, void *,
+                                 const cuuint64_t *, const cuuint64_t *, const cuuint32_t *,
+                                 const cuuint32_t *, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                 CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+EncodeTiled encode_tiled() {
+    static EncodeTiled fn = nullptr;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        void *p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<EncodeTiled>(p);
+    });
+    return fn;
+}
+
+// Row-gather tensor map of a feature matrix [rows x ld] fp32: box = KP columns
+// x 1 row (tile::gather4 takes 4 row indices); false when not expressible
+bool feature_map(CUtensorMap *tm, const float *base, int ld, int64_t rows, int KP) {
+    EncodeTiled enc = encode_tiled();
+    if (!enc || rows < 1 || rows >= (int64_t(1) << 31) || (ld % 4) != 0 || ld < KP ||
+        (reinterpret_cast<uintptr_t>(base) & 15) != 0)
+        return false;
+    const cuuint64_t dims[2] = {(cuuint64_t)ld, (cuuint64_t)rows};
+    const cuuint64_t strides[1] = {(cuuint64_t)ld * 4};
+    const cuuint32_t box[2] = {(cuuint32_t)KP, 1u};
+    const cuuint32_t es[2] = {1u, 1u};
+    return enc(tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float *>(base), dims, strides, box, es,
+               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+               CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 template <int KP, int NP, bool BF>
 void launch_tc(sfb_ctx *ctx, const NetLayer &L, const float *in, int ld_in, const int32_t *nbr,
                int64_t nbr_ld, const int64_t *d_m, int64_t m_bound, int relu, float *out,
@@ -649,6 +684,11 @@ void launch_tc(sfb_ctx *ctx, const NetLayer &L, const float *in, int ld_in, cons
     // cluster; with device-chosen splits the split may be 1, so all taps
     const int src_rows = tap_off ? 1 : (csplit >= 1 ? (L.taps + csplit - 1) / csplit : std::min(L.taps, 32));
     const int vec4 = (L.cin % 4 == 0 && ld_in % 4 == 0 && (reinterpret_cast<uintptr_t>(in) & 15) == 0) ? 1 : 0;
+    // A rows by TMA gather (tcgen05 tf32x3 path, full-width rows, multi-tap items)
+    CUtensorMap tm{};
+    const int tma = (S::TMA_OK && !tap_off && L.cin == KP && ctx->conv_tma &&
+                     feature_map(&tm, in, ld_in, m_bound, KP)) ? 1 : 0;
+    const int oob_row = (int)std::min<int64_t>(m_bound, INT32_MAX);
     if (csplit > 1) {
         const int64_t m_tiles = (m_bound + kM - 1) / kM;   // grid covers the device count's bound
         cudaLaunchConfig_t cfg{};
@@ -666,7 +706,8 @@ void launch_tc(sfb_ctx *ctx, const NetLayer &L, const float *in, int ld_in, cons
         const float *wts = BF ? reinterpret_cast<const float *>(L.w_bf16) : L.w_tc;
         SFB_CUDA(cudaLaunchKernelEx(&cfg, k_conv_tc<KP, NP, BF>, in, ld_in, L.cin, nbr, nbr_ld, d_m,
                                     m_bound, L.taps, wts, L.b, L.cout, relu, out, ld_out,
-                                    static_cast<float *>(nullptr), row_map, tap_off, csplit, src_rows, vec4));
+                                    static_cast<float *>(nullptr), row_map, tap_off, csplit, src_rows, vec4,
+                                    tm, tma, oob_row));
         return;
     }
     const int64_t work_bound = (tap_off || csplit == 1)
@@ -678,7 +719,7 @@ void launch_tc(sfb_ctx *ctx, const NetLayer &L, const float *in, int ld_in, cons
     const float *wts = BF ? reinterpret_cast<const float *>(L.w_bf16) : L.w_tc;
     k_conv_tc<KP, NP, BF><<<grid, kThreadsTC, S::smem_bytes(src_rows), ctx->stream>>>(
         in, ld_in, L.cin, nbr, nbr_ld, d_m, m_bound, L.taps, wts, L.b, L.cout, relu, out, ld_out,
-        partial, row_map, tap_off, csplit == 1 ? 1 : 0, src_rows, vec4);
+        partial, row_map, tap_off, csplit == 1 ? 1 : 0, src_rows, vec4, tm, tma, oob_row);
     SFB_CHECK_LAUNCH();
     if (tap_off || csplit == 1) return;   // no split-K partials
     k_splitk_reduce<<<dgrid(std::min<int64_t>(m_grid, kMaxPartialRows) * L.cout, 256), 256, 0,

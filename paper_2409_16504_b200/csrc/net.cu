@@ -282,73 +282,6 @@ k_conv_narrow(const float *__restrict__ in, int ld_in, const int32_t *__restrict
     }
 }
 
-// The same layer with the taps split over TS consecutive lanes (TS | 32):
-// each lane accumulates its contiguous block of taps (tap then channel order),
-// the blocks are summed by a fixed shuffle tree — TS x less serial latency per
-// row (27 dependent gather rounds -> 27 / TS) at the same FFMA count.
-constexpr int kNarrowTapSplit = 4;
-template <int CIN, int COUT, int TAPS, int TS>
-__global__ void __launch_bounds__(128)
-k_conv_narrow_ts(const float *__restrict__ in, int ld_in, const int32_t *__restrict__ nbr,
-                 int64_t nbr_ld, const int64_t *__restrict__ d_m, int64_t m_fixed,
-                 const float *__restrict__ w, const float *__restrict__ b, int relu,
-                 float *__restrict__ out, int ld_out) {
-    constexpr int TPER = (TAPS + TS - 1) / TS;
-    extern __shared__ __align__(16) float sW[];   // [TAPS][CIN][COUT]
-    for (int i = threadIdx.x; i < TAPS * CIN * COUT; i += blockDim.x) sW[i] = w[i];
-    __syncthreads();
-    const int64_t m = d_m ? *d_m : m_fixed;
-    const int part = threadIdx.x % TS;
-    const int t0 = part * TPER, t1 = min(TAPS, t0 + TPER);
-    // grid-stride over rows; the TS lanes of a row run the same trip count
-    // (the shuffle tree needs all of them)
-    const int64_t rows_per_iter = ((int64_t)gridDim.x * blockDim.x) / TS;
-    const int64_t trips = (m + rows_per_iter - 1) / rows_per_iter;
-    int64_t row = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) / TS;
-    for (int64_t it = 0; it < trips; ++it, row += rows_per_iter) {
-        const bool live = row < m;
-        float acc[COUT];
-#pragma unroll
-        for (int c = 0; c < COUT; ++c) acc[c] = 0.f;
-        if (live) {
-            int32_t src[TPER];
-#pragma unroll
-            for (int q = 0; q < TPER; ++q) src[q] = t0 + q < t1 ? nbr[(int64_t)(t0 + q) * nbr_ld + row] : -1;
-#pragma unroll
-            for (int q = 0; q < TPER; ++q) {
-                if (src[q] < 0) continue;
-                float x[CIN];
-#pragma unroll
-                for (int c = 0; c < CIN; ++c) x[c] = __ldg(in + (int64_t)src[q] * ld_in + c);
-#pragma unroll
-                for (int ci = 0; ci < CIN; ++ci) {
-                    const float4 *wr = reinterpret_cast<const float4 *>(sW + ((t0 + q) * CIN + ci) * COUT);
-#pragma unroll
-                    for (int k = 0; k < COUT / 4; ++k) {
-                        const float4 wv = wr[k];
-                        acc[4 * k] = fmaf(x[ci], wv.x, acc[4 * k]);
-                        acc[4 * k + 1] = fmaf(x[ci], wv.y, acc[4 * k + 1]);
-                        acc[4 * k + 2] = fmaf(x[ci], wv.z, acc[4 * k + 2]);
-                        acc[4 * k + 3] = fmaf(x[ci], wv.w, acc[4 * k + 3]);
-                    }
-                }
-            }
-        }
-#pragma unroll
-        for (int o = TS / 2; o; o >>= 1)
-#pragma unroll
-            for (int c = 0; c < COUT; ++c) acc[c] += __shfl_down_sync(0xffffffffu, acc[c], o, TS);
-        if (live && part == 0) {
-            float *dst = out + row * (int64_t)ld_out;
-#pragma unroll
-            for (int c = 0; c < COUT; ++c) {
-                const float v = acc[c] + b[c];
-                dst[c] = relu ? fmaxf(v, 0.f) : v;
-            }
-        }
-    }
-}
-
 template <int CIN, int COUT, int TAPS, int PARTS>
 static void launch_narrow(sfb_ctx *ctx, const NetLayer &L, const float *in, int ld_in, const int32_t *nbr,
                           int64_t nbr_ld, const int64_t *d_m, int64_t m_bound, int relu, float *out,
@@ -366,15 +299,6 @@ void conv_layer(sfb_ctx *ctx, const NetLayer &L, const float *in, int ld_in, con
     if (m_bound == 0) return;
     if (m_grid < 0) m_grid = m_bound;
     if (ctx->net_mode != SFB_NET_TC_BF16 && L.cin == 9 && L.cout == 16 && L.taps == 27) {
-        if (kNarrowTapSplit > 1) {
-            constexpr int TS = kNarrowTapSplit;
-            constexpr size_t smem = sizeof(float) * 27 * 9 * 16;
-            set_max_dyn_smem(reinterpret_cast<const void *>(k_conv_narrow_ts<9, 16, 27, TS>), (int)smem);
-            k_conv_narrow_ts<9, 16, 27, TS><<<dgrid(m_grid * TS, 128, 8), 128, smem, ctx->stream>>>(
-                in, ld_in, nbr, nbr_ld, d_m, m_bound, L.w, L.b, relu, out, ld_out);
-            SFB_CHECK_LAUNCH();
-            return;
-        }
         launch_narrow<9, 16, 27, 1>(ctx, L, in, ld_in, nbr, nbr_ld, d_m, m_bound, relu, out, ld_out, m_grid);
         return;
     }

@@ -108,8 +108,8 @@ def test_raster_cases(golden):
 
 
 def test_frame_kats_rgba8():
-    """frames.json payload SHA-256s; RGBA8 must match the oracle byte-for-byte
-    except where a sub-2e-3 difference crosses a rounding boundary."""
+    """frames.json payload SHA-256s: the GPU planes quantised to RGBA8 reproduce
+    the reference's payloads byte for byte."""
     arrays, cases = kat_cases()
     sp = gpu_splats(arrays)
     for case in cases:
@@ -125,6 +125,7 @@ def test_frame_kats_rgba8():
         else:
             rgba = OR.to_rgba(fb["rgb"], fb["transmittance"])
         ok = hashlib.sha256(rgba.tobytes()).hexdigest() == case["payload_sha256"]
+        assert ok, f"{case['name']}: RGBA8 payload differs from frames.json"   # byte-exact
         if not ok:
             ref = OR.render(arrays, cam, "rgb")
             refn = OR.render(arrays, cam, "normal")
