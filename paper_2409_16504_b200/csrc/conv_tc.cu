@@ -117,6 +117,18 @@ __device__ __forceinline__ void tma_gather4(void *dst, const CUtensorMap *tm, in
         : "memory");
 }
 
+// 16-byte asynchronous global -> shared copy (LDGSTS); src_bytes = 0 zero-fills
+__device__ __forceinline__ void cp_async16(void *dst, const void *src, uint32_t src_bytes) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(smem_u32(dst)), "l"(src),
+                 "r"(src_bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+    asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+
 __device__ __forceinline__ void mma_tf32(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t idesc,
                                          uint32_t accumulate) {
     asm volatile(
@@ -265,7 +277,13 @@ k_conv_tc(const float *__restrict__ in, int ld_in, int cin, const int32_t *__res
         for (int s = 0; s < 4; ++s) mbar_init(&raw_full[s], 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
-    const bool use_tma = S::TMA_OK && tma != 0;
+    // A-row staging: 0 = register prefetch one batch ahead; 1 = TMA gather4
+    // into the shared ring, RS batches ahead; 2 = each thread's own row by
+    // cp.async (LDGSTS) into the ring, RS batches ahead (no barrier: a thread
+    // only reads the row it copied)
+    const bool use_tma = S::TMA_OK && tma == 1;
+    const bool use_cpa = S::TMA_OK && tma == 2;
+    const bool use_ring = use_tma || use_cpa;
     if (warp == 0) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
                          smem_u32(tmem_slot)),
@@ -372,6 +390,21 @@ k_conv_tc(const float *__restrict__ in, int ld_in, int cin, const int32_t *__res
                 pt[pn++] = t0 + __ffs(pmask) - 1;
                 pmask &= pmask - 1;
             }
+            if (use_cpa) {   // my row of each tap of the batch; an empty group past the last batch
+                if (pn > 0) {
+                    const int stg = (g0 + npref++) % S::RS;
+                    float *dst = raw + (size_t)stg * TB * kM * KP + (size_t)tid * KP;
+                    for (int q = 0; q < pn; ++q) {
+                        const int32_t r = s_src[pt[q] - t0][tid];
+                        const float *src = r >= 0 ? in + (int64_t)r * ld_in : in;
+#pragma unroll
+                        for (int k = 0; k < KP; k += 4)
+                            cp_async16(dst + (size_t)q * kM * KP + k, src + k, r >= 0 ? 16u : 0u);
+                    }
+                }
+                cp_async_commit();
+                return;
+            }
             if (pn == 0) return;
             const int stg = (g0 + npref++) % S::RS;
             if (warp == 0) {
@@ -388,7 +421,7 @@ k_conv_tc(const float *__restrict__ in, int ld_in, int cin, const int32_t *__res
             }
         };
         take();
-        if (use_tma) {
+        if (use_ring) {
             for (int k = 0; k < S::RS; ++k) prefetch();
         } else if (nxt_n) {
             fetch();
@@ -427,9 +460,10 @@ k_conv_tc(const float *__restrict__ in, int ld_in, int cin, const int32_t *__res
                 mbar_wait(&bar_done[j & 1], (j >> 1) & 1);
             }
             if (tid == 0 && ((S::STAGES == 1 && !S::BDB) || item_issued == 0)) load_w(cur_t, cur_n, ws);
-            if (use_tma) {   // this batch's rows, gathered RS batches ago
+            if (use_ring) {   // this batch's rows, fetched RS batches ago
                 const int stg = issued % S::RS;
-                mbar_wait(&raw_full[stg], (uint32_t)(issued / S::RS) & 1u);
+                if (use_tma) mbar_wait(&raw_full[stg], (uint32_t)(issued / S::RS) & 1u);
+                else cp_async_wait<S::RS - 1>();   // my oldest group: this batch
                 const float *src = raw + (size_t)stg * TB * kM * KP + (size_t)tid * KP;
 #pragma unroll
                 for (int q = 0; q < TB; ++q) {
@@ -483,13 +517,13 @@ k_conv_tc(const float *__restrict__ in, int ld_in, int cin, const int32_t *__res
                 }
             }
             take();
-            if (nxt_n && !use_tma) fetch();   // next batch's rows, in flight from here
+            if (nxt_n && !use_ring) fetch();   // next batch's rows, in flight from here
             // next batch's weights: its slot was last read by batch issued-1,
             // complete since the wait above
             if (S::BDB && tid == 0 && nxt_n) load_w(nxt_t, nxt_n, (issued + 1) & 1);
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
             __syncthreads();   // also orders the last drain's TMEM reads before these MMAs
-            if (use_tma) prefetch();   // batch issued + RS into the stage just read
+            if (use_ring) prefetch();   // batch issued + RS into the stage just read
             if (tid == 0) {
                 mbar_wait(&bar_full[ws], use & 1);
                 asm volatile("tcgen05.fence::after_thread_sync;");
@@ -686,8 +720,11 @@ void launch_tc(sfb_ctx *ctx, const NetLayer &L, const float *in, int ld_in, cons
     const int vec4 = (L.cin % 4 == 0 && ld_in % 4 == 0 && (reinterpret_cast<uintptr_t>(in) & 15) == 0) ? 1 : 0;
     // A rows by TMA gather (tcgen05 tf32x3 path, full-width rows, multi-tap items)
     CUtensorMap tm{};
-    const int tma = (S::TMA_OK && !tap_off && L.cin == KP && ctx->conv_tma &&
-                     feature_map(&tm, in, ld_in, m_bound, KP)) ? 1 : 0;
+    int tma = 0;
+    if (S::TMA_OK && !tap_off && L.cin == KP && vec4) {
+        if (ctx->conv_stage == 1 && feature_map(&tm, in, ld_in, m_bound, KP)) tma = 1;
+        else if (ctx->conv_stage == 2) tma = 2;
+    }
     const int oob_row = (int)std::min<int64_t>(m_bound, INT32_MAX);
     if (csplit > 1) {
         const int64_t m_tiles = (m_bound + kM - 1) / kM;   // grid covers the device count's bound
