@@ -95,6 +95,11 @@ int sfb_set_graphs(sfb_ctx *ctx, int on);
  * them from the previous eager frame's demand. A frame needing more renders
  * every run from the global list instead (identical planes, slower). Tests. */
 int sfb_set_entry_capacity(sfb_ctx *ctx, int64_t capacity);
+/* How the tcgen05 convs stage their gathered A rows: 0 register prefetch one
+ * tap batch ahead (default, fastest measured), 1 TMA tile::gather4 into a
+ * shared-memory ring RS batches ahead, 2 per-thread cp.async ring. Results are
+ * bitwise identical across modes. */
+int sfb_set_conv_staging(sfb_ctx *ctx, int mode);
 /* Diagnostics: when set (device buffer of 4 int64 per tile, zeroed by the
  * caller) the compositor accumulates windows, list entries and alpha
  * evaluations per tile. NULL disables. */

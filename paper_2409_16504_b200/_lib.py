@@ -61,6 +61,7 @@ SIGNATURES = {
     "sfb_set_timing": [P, ctypes.c_int],
     "sfb_set_graphs": [P, ctypes.c_int],
     "sfb_set_entry_capacity": [P, I64],
+    "sfb_set_conv_staging": [P, ctypes.c_int],
     "sfb_set_debug_counters": [P, P],
     "sfb_stage_times": [P, P, P, I32, ctypes.POINTER(I32)],
     "sfb_set_frame_debug": [P, I64, P, P, P, P, I32, P, P],

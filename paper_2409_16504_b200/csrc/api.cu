@@ -300,6 +300,13 @@ int sfb_set_frame_debug(sfb_ctx *ctx, int64_t capacity, int64_t *source, int32_t
     return SFB_OK;
 }
 
+int sfb_set_conv_staging(sfb_ctx *ctx, int mode) {
+    if (!ctx || mode < 0 || mode > 2) return SFB_ERR_ARG;
+    ctx->conv_stage = mode;
+    ++ctx->net_epoch;   // frame graphs captured with another staging are stale
+    return SFB_OK;
+}
+
 int sfb_set_entry_capacity(sfb_ctx *ctx, int64_t capacity) {
     if (!ctx || capacity < 0) return SFB_ERR_ARG;
     ctx->entry_cap_override = capacity;

@@ -157,9 +157,9 @@ struct sfb_ctx {
     int64_t *debug_counters = nullptr;   // compositor per-tile counters (diagnostics)
     sfb::FrameDebug frame_debug;         // fused-frame parity export (tests)
     int64_t entry_cap_override = 0;      // tests: pyramid entry capacity (0 = automatic)
-    // tcgen05 conv A-row staging: 0 register prefetch, 1 TMA gather4 ring,
-    // 2 cp.async ring (conv_tc.cu; A/B-selected)
-    int conv_stage = 2;
+    // tcgen05 conv A-row staging: 0 register prefetch (default: fastest, A/B in
+    // DESIGN.md §4), 1 TMA gather4 ring, 2 cp.async ring (sfb_set_conv_staging)
+    int conv_stage = 0;
     sfb::DevCounts *last_counts = nullptr;   // device counts of the last call
     // launch-size hints (host copies of the counts of the last eager frame):
     // every kernel loops over its device count, so hints only size grids

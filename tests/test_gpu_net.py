@@ -219,3 +219,22 @@ def test_bf16_mode_conv_bounded_error(kernel, stride, cin, cout):
     err = np.abs(np_(out.feats) - ref)
     assert (err <= 2.0 ** -7 * mag + 1e-6).all(), err.max()
     assert err.max() > 1e-4   # really bf16
+
+
+@pytest.mark.parametrize("mode", [1, 2])
+def test_conv_staging_modes_bitwise_identical(mode):
+    """The tcgen05 conv's A rows staged by TMA tile::gather4 (1) or a cp.async
+    ring (2) instead of the default register prefetch: the same MMA operands,
+    so the UNet output is bitwise identical."""
+    from paper_2409_16504_b200 import _lib
+    cloud, _ = scenes.config1()
+    w = netplan.init_random(netplan.NetworkPlan(), 0)
+    vox = voxelize_adaptive(PointCloud(cloud.positions, cloud.colors))
+    ref = sparsenet.unet_forward_voxels(vox, w)
+    ctx = _lib.context()
+    ctx.lib.sfb_set_conv_staging(ctx.handle, mode)
+    try:
+        got = sparsenet.unet_forward_voxels(vox, w)
+    finally:
+        ctx.lib.sfb_set_conv_staging(ctx.handle, 0)
+    assert torch.equal(got, ref)
