@@ -56,6 +56,8 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-profile", action="store_true", help="skip the CUPTI launch count")
+    ap.add_argument("--view", type=int, default=-1,
+                    help="render only this view (profiling runs; default: views round-robin)")
     ap.add_argument("--cpu-frames", type=int, default=1,
                     help="full config-2 frames of the CPU port timed for cpu_baseline")
     ap.add_argument("--lanes", type=int, default=8, help="frames in flight per GPU (streams)")
@@ -273,7 +275,7 @@ def run_ours(args):
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")   # 256 MB > 126 MB L2
 
     def view_of(i):   # views round-robin over ranks
-        return cams[unit_of(i, rank, world, len(cams))]
+        return cams[args.view if args.view >= 0 else unit_of(i, rank, world, len(cams))]
 
     rgba_out = None   # render_pose leg: one RGBA8 device frame per (lane, input copy)
     # device->host read-backs of the e2e legs: one stream per lane, so a frame's
@@ -388,7 +390,8 @@ def run_ours(args):
         for k, v in ctx.stage_times().items():
             stage_acc[k] = stage_acc.get(k, 0.0) + v
             if k == "composite":   # the compositor's cost depends on the view
-                comp_by_view.setdefault(unit_of(i, rank, world, len(cams)), []).append(v)
+                vid = args.view if args.view >= 0 else unit_of(i, rank, world, len(cams))
+                comp_by_view.setdefault(vid, []).append(v)
     ctx.set_timing(False)
     stage_ms = {k: v / n_stage for k, v in stage_acc.items()}
     comp_by_view = {u: sum(v) / len(v) for u, v in sorted(comp_by_view.items())}
