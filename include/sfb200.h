@@ -86,7 +86,9 @@ int sfb_version(void);
 /* Stage timing with CUDA events on the context stream (off by default):
  * after a call, sfb_stage_times returns (stage id, ms) per completed stage:
  * 1 voxelize, 2 unet, 3 head, 4 project, 5 depth sort, 6 runs+binning,
- * 7 composite. Synchronises on the recorded events. */
+ * 7 composite (in the frame), 8 four more back-to-back compositor launches
+ * (the kernel's own duration, free of eager launch gaps; same output),
+ * 9 untimed. Synchronises on the recorded events. */
 int sfb_set_timing(sfb_ctx *ctx, int on);
 /* CUDA-graph replay of sfb_frame (default on): the first call of a shape runs
  * eagerly, the second captures, later calls update parameters and replay. */

@@ -19,7 +19,8 @@ SFB_OK, SFB_ERR_ARG, SFB_ERR_OOM, SFB_ERR_CUDA, SFB_ERR_STATE = 0, 1, 2, 3, 4
 PLANE_RGB, PLANE_NORMAL, PLANE_DEPTH = 1, 2, 4
 NET_SIMT_F32, NET_TC_TF32X3, NET_TC_BF16, NET_SIMT_F64 = 0, 1, 2, 3
 STAGES = {1: "voxelize", 2: "unet", 3: "head", 4: "project", 5: "sort", 6: "bin",
-          7: "composite"}
+          7: "composite", 8: "composite_reps", 9: "untimed"}
+COMPOSITE_REPS = 4   # render.cu kCompReps: back-to-back compositor launches in stage timing
 
 P = ctypes.c_void_p
 I64 = ctypes.c_int64

@@ -215,7 +215,8 @@ struct sfb_ctx {
 namespace sfb {
 
 // stage ids reported by sfb_stage_times
-enum Stage { ST_BEGIN = 0, ST_VOXELIZE, ST_UNET, ST_HEAD, ST_PROJECT, ST_SORT, ST_BIN, ST_COMPOSITE };
+enum Stage { ST_BEGIN = 0, ST_VOXELIZE, ST_UNET, ST_HEAD, ST_PROJECT, ST_SORT, ST_BIN, ST_COMPOSITE,
+             ST_COMPOSITE_REPS, ST_BEGIN_REPS };
 
 inline unsigned grid_for(int64_t n, int block, int64_t cap = 1 << 20) {
     int64_t g = (n + block - 1) / block;

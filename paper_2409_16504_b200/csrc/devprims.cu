@@ -430,144 +430,12 @@ k_rs_downsweep(const K *__restrict__ kin, const uint32_t *__restrict__ vin, K *_
     }
 }
 
-// ------------------------------------------------------------------ onesweep
-// Stable LSD radix with one launch per 8-bit pass: every tile of 1024 items
-// (block, ticket order) ranks its items per digit in item order, publishes
-// its per-digit counts and looks back over the preceding tiles (decoupled
-// look-back, one digit per thread) for its per-digit offsets; the digit bases
-// come from one histogram of every pass's digits taken before the first pass.
-// Replaces upsweep + downsweep per pass (and their O(blocks) offset loops).
-constexpr int kOsThreads = 256, kOsIpt = 4, kOsTile = kOsThreads * kOsIpt;
-constexpr bool kRsOnesweep = true;
-
-template <class K>
-__global__ void __launch_bounds__(kOsThreads)
-k_os_hist(const K *__restrict__ keys, const int64_t *__restrict__ d_n, int64_t n_fixed, int passes,
-          uint32_t *__restrict__ ghist, unsigned long long *__restrict__ status0) {
-    __shared__ uint32_t h[8][256];
-    for (int i = threadIdx.x; i < 8 * 256; i += kOsThreads) (&h[0][0])[i] = 0u;
-    __syncthreads();
-    const int64_t n = d_n ? *d_n : n_fixed;
-    const int64_t tiles = (n + kOsTile - 1) / kOsTile;
-    SFB_FOR(i, tiles * 256) status0[i] = 0ull;   // pass 0's look-back words
-    SFB_FOR(i, n) {
-        const K k = keys[i];
-        for (int p = 0; p < passes; ++p) atomicAdd(&h[p][(uint32_t)(k >> (8 * p)) & 255u], 1u);
-    }
-    __syncthreads();
-    for (int p = 0; p < passes; ++p)
-        if (h[p][threadIdx.x]) atomicAdd(&ghist[p * 256 + threadIdx.x], h[p][threadIdx.x]);
-}
-
-template <class K, bool HAS_VALS>
-__global__ void __launch_bounds__(kOsThreads)
-k_os_pass(const K *__restrict__ kin, const uint32_t *__restrict__ vin, K *__restrict__ kout,
-          uint32_t *__restrict__ vout, const int64_t *__restrict__ d_n, int64_t n_fixed, int shift,
-          const uint32_t *__restrict__ ghist, unsigned long long *__restrict__ status,
-          unsigned long long *__restrict__ status_next, unsigned int *__restrict__ ticket) {
-    __shared__ int32_t wcnt[kRsWarps][256];
-    __shared__ int32_t base[256];
-    __shared__ int32_t s_warp[32];
-    __shared__ int s_tile;
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int64_t n = d_n ? *d_n : n_fixed;
-    const int64_t ntiles = (n + kOsTile - 1) / kOsTile;
-    const int32_t gbase = block_excl_scan((int32_t)ghist[threadIdx.x], s_warp, nullptr);
-    for (int w = 0; w < kRsWarps; ++w) wcnt[w][threadIdx.x] = 0;
-    if (threadIdx.x == 0) s_tile = (int)atomicAdd(ticket, 1u);
-    __syncthreads();
-    const int64_t tile = s_tile;
-    if (tile >= ntiles) return;
-    if (status_next) status_next[tile * 256 + threadIdx.x] = 0ull;   // the next pass's words
-    const uint32_t lt = (1u << lane) - 1u;
-    K key[kOsIpt];
-    uint32_t val[kOsIpt], dg[kOsIpt];
-    int32_t lr[kOsIpt];
-    const int64_t wbase = tile * kOsTile + (int64_t)warp * 32 * kOsIpt;
-#pragma unroll
-    for (int q = 0; q < kOsIpt; ++q) {
-        const int64_t i = wbase + q * 32 + lane;
-        const bool ok = i < n;
-        key[q] = ok ? kin[i] : K(0);
-        val[q] = (HAS_VALS && ok) ? vin[i] : 0u;
-        dg[q] = ok ? ((uint32_t)(key[q] >> shift) & 255u) : 256u;
-    }
-#pragma unroll
-    for (int q = 0; q < kOsIpt; ++q) {   // rounds in item order
-        const uint32_t d = dg[q];
-        const uint32_t peers = __match_any_sync(0xffffffffu, d);
-        const int r = __popc(peers & lt);
-        lr[q] = d < 256u ? wcnt[warp][d] + r : 0;
-        __syncwarp();
-        if (d < 256u && r == 0) wcnt[warp][d] += __popc(peers);
-        __syncwarp();
-    }
-    __syncthreads();
-    // per digit (thread = digit): exclusive prefix over the warps, tile count
-    int32_t tot = 0;
-#pragma unroll
-    for (int w = 0; w < kRsWarps; ++w) {
-        const int32_t c = wcnt[w][threadIdx.x];
-        wcnt[w][threadIdx.x] = tot;
-        tot += c;
-    }
-    // decoupled look-back for this digit's count in the preceding tiles
-    unsigned long long *mine = status + tile * 256 + threadIdx.x;
-    int32_t prefix = 0;
-    if (tile == 0) {
-        atomicExch(mine, kLbInc | (uint32_t)tot);
-    } else {
-        atomicExch(mine, kLbAgg | (uint32_t)tot);
-        for (int64_t t = tile - 1;; --t) {
-            unsigned long long v = lb_load(status + t * 256 + threadIdx.x);
-            while ((v >> 32) == 0) v = lb_load(status + t * 256 + threadIdx.x);
-            prefix += (int32_t)(uint32_t)v;
-            if ((v >> 32) == 2) break;
-        }
-        atomicExch(mine, kLbInc | (uint32_t)(prefix + tot));
-    }
-    base[threadIdx.x] = gbase + prefix;
-    __syncthreads();
-#pragma unroll
-    for (int q = 0; q < kOsIpt; ++q) {
-        const uint32_t d = dg[q];
-        if (d < 256u) {
-            const int32_t pos = base[d] + wcnt[warp][d] + lr[q];
-            kout[pos] = key[q];
-            if (HAS_VALS) vout[pos] = val[q];
-        }
-    }
-}
-
 // Stable LSD sort of (key, val) over bits [0, bits). Result ends in (k0, v0)
 // if the pass count is even, else in (k1, v1); returns which (0/1).
 template <class K>
 int dsort_pairs(sfb_ctx *ctx, K *k0, uint32_t *v0, K *k1, uint32_t *v1, const int64_t *d_n,
                 int64_t n_fixed, int bits) {
     const int passes = (bits + 7) / 8;
-    if (kRsOnesweep && passes <= 8) {
-        const int64_t tiles = std::max<int64_t>(1, (n_fixed + kOsTile - 1) / kOsTile);
-        uint32_t *ghist = ctx->arena.alloc<uint32_t>(passes * 256 + passes);   // + tickets
-        unsigned int *tickets = ghist + passes * 256;
-        auto *st = ctx->arena.alloc<unsigned long long>(2 * tiles * 256);
-        SFB_CUDA(cudaMemsetAsync(ghist, 0, sizeof(uint32_t) * (passes * 256 + passes), ctx->stream));
-        k_os_hist<K><<<dgrid(n_fixed, kOsThreads, 1), kOsThreads, 0, ctx->stream>>>(k0, d_n, n_fixed,
-                                                                                  passes, ghist, st);
-        for (int p = 0; p < passes; ++p) {
-            K *ki = (p & 1) ? k1 : k0, *ko = (p & 1) ? k0 : k1;
-            uint32_t *vi = (p & 1) ? v1 : v0, *vo = (p & 1) ? v0 : v1;
-            unsigned long long *cur = st + (p & 1) * tiles * 256;
-            unsigned long long *nxt = p + 1 < passes ? st + ((p + 1) & 1) * tiles * 256 : nullptr;
-            if (v0)
-                k_os_pass<K, true><<<(unsigned)tiles, kOsThreads, 0, ctx->stream>>>(
-                    ki, vi, ko, vo, d_n, n_fixed, 8 * p, ghist + p * 256, cur, nxt, tickets + p);
-            else
-                k_os_pass<K, false><<<(unsigned)tiles, kOsThreads, 0, ctx->stream>>>(
-                    ki, nullptr, ko, nullptr, d_n, n_fixed, 8 * p, ghist + p * 256, cur, nxt, tickets + p);
-        }
-        SFB_CHECK_LAUNCH();
-        return passes & 1;
-    }
     int32_t *hist = ctx->arena.alloc<int32_t>(256 * kRsBlocks);
     for (int p = 0; p < passes; ++p) {
         K *ki = (p & 1) ? k1 : k0, *ko = (p & 1) ? k0 : k1;
