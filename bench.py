@@ -350,9 +350,9 @@ def run_ours(args):
         with torch.cuda.stream(streams[0]):
             streams[0].wait_stream(torch.cuda.current_stream())
         evs[i][0].record(streams[0])
-        with torch.cuda.stream(streams[0]):
-            render_frame(dev_clouds[i % copies], weights, view_of(i), planes,
-                         out=outs[0][i % copies], lane=0)
+        with torch.cuda.stream(streams[0]):   # lane 0's input copies (graphs captured in warm-up)
+            k = (i * lanes) % copies
+            render_frame(dev_clouds[k], weights, view_of(i), planes, out=outs[0][k], lane=0)
         evs[i][1].record(streams[0])
         torch.cuda.current_stream().wait_stream(streams[0])
     torch.cuda.synchronize()

@@ -936,7 +936,7 @@ __global__ void __launch_bounds__(kCT, kCompMinBlocks) k_composite(CompParams P)
     __shared__ uint8_t r_idx[kChunk];   // staged slot of the chunk's e-th surviving run
     // the current chunk's run records (pixel box precomputed per run)
     __shared__ double r_mx[kChunk], r_my[kChunk], r_rr[kChunk], r_ia[kChunk], r_ib[kChunk],
-        r_ic[kChunk], r_op[kChunk], r_dep[kChunk], r_rn[3][kChunk], r_qc[kChunk];
+        r_ic[kChunk], r_op[kChunk], r_dep[kChunk], r_rn[3][kChunk];
     __shared__ int32_t r_x0[kChunk], r_x1[kChunk], r_y0[kChunk], r_y1[kChunk], r_start[kChunk],
         r_count[kChunk];
     __shared__ uint8_t r_uni[kChunk];
@@ -1115,10 +1115,9 @@ __global__ void __launch_bounds__(kCT, kCompMinBlocks) k_composite(CompParams P)
                 const double fy = fmax(fabs((double)y_lo - my), fabs((double)(y_end - 1) - my));
                 r_full[j] = bx0 == x_lo && bx1 == x_end - 1 && by0 == y_lo && by1 == y_end - 1 &&
                             fx * fx + fy * fy <= rad * rad;
-                const double qc = q_cut(q2.y);
-                r_qc[j] = qc;
                 keep = bx0 <= bx1 && by0 <= by1 &&
-                       !(tile_min_q(q1.x, q1.y, q2.x, bx0 - mx, bx1 - mx, by0 - my, by1 - my) > qc);
+                       !(tile_min_q(q1.x, q1.y, q2.x, bx0 - mx, bx1 - mx, by0 - my, by1 - my) >
+                         q_cut(q2.y));
             }
             const unsigned ball = __ballot_sync(0xffffffffu, keep);
             if ((threadIdx.x & 31) == 0) s_bal[threadIdx.x >> 5] = ball;
@@ -1153,7 +1152,6 @@ __global__ void __launch_bounds__(kCT, kCompMinBlocks) k_composite(CompParams P)
                         if (dx * dx + dy * dy > r_rr[f]) continue;
                     }
                     const double q = r_ia[f] * dx * dx + 2.0 * r_ib[f] * dx * dy + r_ic[f] * dy * dy;
-                    if (q > r_qc[f]) continue;   // alpha < 1/255 here: no exp needed
                     double alpha = r_op[f] * exp_nonpos(-0.5 * q);
                     if (alpha > alpha_max) alpha = alpha_max;
                     if (alpha < kCutoff) continue;
