@@ -41,7 +41,7 @@ constexpr int kWin = 2048;     // rank window of the merge
 // config 2 with 8 frames in flight: 0.308 ms/frame vs 0.316 for 256 threads x
 // one pixel (64 threads x 4 pixels: 0.34, register-starved)
 constexpr int kCT = 128;       // compositor threads per CTA
-constexpr int kCompMinBlocks = 7;
+constexpr int kCompMinBlocks = 8;
 constexpr int kCompReps = 4;   // timed re-launches of the compositor in stage-timing mode
 constexpr int kChunk = kCT;    // candidate runs staged per compositing chunk
 
@@ -809,9 +809,13 @@ struct CompParams {
 // scaled by 2^k through the exponent bits. Within ~1 ulp like the libm exp
 // (the reference's numba kernel uses LLVM's), at ~25 instructions instead of
 // the ~50 of the general-purpose CUDA exp with its special-case paths.
+// Branch-free (the compositor evaluates it for both of a thread's pixels in
+// one straight-line block): x is clamped to [-708, 0] (x > 0 only through
+// rounding of a degenerate conic, where the result is 1 to within rounding)
+// and 0 is selected below -708 (alpha < 1/255 there anyway).
 __device__ __forceinline__ double exp_nonpos(double x) {
-    if (x < -708.0) return 0.0;   // below the smallest normal: alpha < 1/255 anyway
-    if (x > 0.0) return exp(x);   // q < 0 only through rounding of a degenerate conic
+    const bool under = x < -708.0;
+    x = fmin(fmax(x, -708.0), 0.0);
     const double kd = rint(x * 1.4426950408889634);
     const double r = __fma_rn(-kd, 6.93147180369123816490e-01, x);
     const double rr = __fma_rn(-kd, 1.90821492927058770002e-10, r);
@@ -829,7 +833,7 @@ __device__ __forceinline__ double exp_nonpos(double x) {
     p = __fma_rn(p, rr, 1.0);
     p = __fma_rn(p, rr, 1.0);
     const int k = (int)kd;   // in [-1022, 0]: 2^k is a normal double
-    return p * __longlong_as_double((long long)(k + 1023) << 52);
+    return under ? 0.0 : p * __longlong_as_double((long long)(k + 1023) << 52);
 }
 
 // Alpha-support test of a whole tile. forward_kernel blends a splat at a
@@ -911,6 +915,14 @@ __device__ __forceinline__ float3 horner3(const float4 *__restrict__ v, int m, f
     return make_float3(fmaf(om, oxy.x, exy.x), fmaf(om, oxy.y, exy.y), fmaf(om, oz, ez));
 }
 
+// Colour / normal / depth accumulators of the compositor (T and every
+// alpha / cutoff decision stay float64)
+using CompAcc = float;
+__device__ __forceinline__ double acc_fma(double w, double v, double c) { return __fma_rn(w, v, c); }
+__device__ __forceinline__ float acc_fma(double w, double v, float c) {
+    return __fmaf_rn((float)w, (float)v, c);
+}
+
 // One CTA per tile. The rank-ordered fine / super / global lists are merged
 // in rank windows (bitmap + ordered compaction), candidate runs are staged
 // in chunks, and every pixel blends each covering run in closed form: a
@@ -956,7 +968,8 @@ __global__ void __launch_bounds__(kCT, kCompMinBlocks) k_composite(CompParams P)
 
     int32_t pxs[NPIX], pys[NPIX];
     bool valid[NPIX];
-    double T[NPIX], c0[NPIX], c1[NPIX], c2[NPIX], n0[NPIX], n1[NPIX], n2[NPIX], dd[NPIX];
+    double T[NPIX];
+    CompAcc c0[NPIX], c1[NPIX], c2[NPIX], n0[NPIX], n1[NPIX], n2[NPIX], dd[NPIX];
 #pragma unroll
     for (int k = 0; k < NPIX; ++k) {
         const uint32_t p = threadIdx.x + k * kCT;
@@ -980,9 +993,17 @@ __global__ void __launch_bounds__(kCT, kCompMinBlocks) k_composite(CompParams P)
     const double alpha_max = P.alpha_max;
     const uint32_t *ids[3] = {P.f_ids, P.s_ids, P.g_ids};
     // list positions as 32-bit (the entry lists are int32-indexed)
-    int32_t cur[3] = {P.f_off[t], P.s_off[st], 0};
-    const int32_t end[3] = {P.f_off[t + 1], P.s_off[st + 1], (int32_t)*P.d_G};
-    int ws = 128;  // rank window grows 128 -> 2048: most tiles saturate in the first
+    // list cursors and ends are CTA-uniform: kept in shared memory (registers
+    // go to the per-pixel state)
+    __shared__ int32_t cur[3], end[3];
+    if (threadIdx.x < 3) {
+        const int s = threadIdx.x;
+        cur[s] = s == 0 ? P.f_off[t] : s == 1 ? P.s_off[st] : 0;
+        end[s] = s == 0 ? P.f_off[t + 1] : s == 1 ? P.s_off[st + 1] : (int32_t)*P.d_G;
+    }
+    __syncthreads();
+    __shared__ int s_ws;   // rank window size: 128 -> 2048 (most tiles saturate in the first)
+    if (threadIdx.x == 0) s_ws = 128;
     bool done = false;
     while (!done) {
         // the window's first 256-rank slice (ids and, in list order, rects)
@@ -994,7 +1015,7 @@ __global__ void __launch_bounds__(kCT, kCompMinBlocks) k_composite(CompParams P)
         for (int s = 0; s < 3; ++s) {
             const int32_t idx = cur[s] + (int32_t)threadIdx.x;
             id[s] = idx < end[s] ? ids[s][idx] : NONE;
-            if (s && idx < end[s]) rc[s - 1] = (s == 1 ? P.s_rect : P.g_rect)[idx];
+            if (s) rc[s - 1] = idx < end[s] ? (s == 1 ? P.s_rect : P.g_rect)[idx] : make_int4(1, 0, 1, 0);
         }
         if (threadIdx.x == 0) s_head = min(id[0], min(id[1], id[2]));
         for (int i = threadIdx.x; i < kWin / 32; i += kCT) bitmap[i] = 0;
@@ -1002,6 +1023,7 @@ __global__ void __launch_bounds__(kCT, kCompMinBlocks) k_composite(CompParams P)
         __syncthreads();
         const uint32_t w0 = s_head;
         if (w0 == NONE) break;
+        const int ws = s_ws;   // written again only after the compaction's barrier
         const uint32_t w1 = w0 + (uint32_t)ws;
         // one 256-rank slice of the window at a time: 3 id loads + 2 rect
         // loads in flight per thread, few registers (occupancy)
@@ -1013,11 +1035,10 @@ __global__ void __launch_bounds__(kCT, kCompMinBlocks) k_composite(CompParams P)
                     id[s] = idx < end[s] ? ids[s][idx] : NONE;
                 }
 #pragma unroll
-                for (int s = 1; s < 3; ++s)
-                    if (id[s] < w1) {   // rects stored in list order: no dependent load
-                        const int32_t idx = cur[s] + k * kCT + (int32_t)threadIdx.x;
-                        rc[s - 1] = (s == 1 ? P.s_rect : P.g_rect)[idx];
-                    }
+                for (int s = 1; s < 3; ++s) {   // rects stored in list order: no dependent load
+                    const int32_t idx = cur[s] + k * kCT + (int32_t)threadIdx.x;
+                    rc[s - 1] = idx < end[s] ? (s == 1 ? P.s_rect : P.g_rect)[idx] : make_int4(1, 0, 1, 0);
+                }
             }
 #pragma unroll
             for (int s = 0; s < 3; ++s) {
@@ -1034,8 +1055,8 @@ __global__ void __launch_bounds__(kCT, kCompMinBlocks) k_composite(CompParams P)
             }
         }
         __syncthreads();
-#pragma unroll
-        for (int s = 0; s < 3; ++s) cur[s] += (int32_t)s_add[s];
+        // read again only after the compaction's barrier
+        if (threadIdx.x < 3) cur[threadIdx.x] += (int32_t)s_add[threadIdx.x];
         // ordered compaction of the bitmap by warp 0 (2 words per lane)
         if (threadIdx.x < 32) {
             const int lane = threadIdx.x;
@@ -1141,20 +1162,33 @@ __global__ void __launch_bounds__(kCT, kCompMinBlocks) k_composite(CompParams P)
                     continue;
                 }
                 const int f = r_idx[e];
+                // the pixels' tests and alphas in one branch-free block (two
+                // independent float64 chains interleave), then the blends
+                double al[NPIX];
+                bool use[NPIX];
+                {
+                    const double mx = r_mx[f], my = r_my[f], ia = r_ia[f], ib = r_ib[f], ic = r_ic[f];
+                    const double op = r_op[f];
+                    const bool full = r_full[f];
+#pragma unroll
+                    for (int k = 0; k < NPIX; ++k) {
+                        const double dx = (double)pxs[k] - mx, dy = (double)pys[k] - my;
+                        bool ok = valid[k] && !(term && T[k] < kCutoff);
+                        if (!full)   // forward_kernel's pixel box and circle (_raster_kernels.py:178-184)
+                            ok = ok && !(pxs[k] < r_x0[f] || pxs[k] > r_x1[f] || pys[k] < r_y0[f] ||
+                                         pys[k] > r_y1[f]) &&
+                                 !(dx * dx + dy * dy > r_rr[f]);
+                        const double q = ia * dx * dx + 2.0 * ib * dx * dy + ic * dy * dy;
+                        double alpha = op * exp_nonpos(-0.5 * q);
+                        if (alpha > alpha_max) alpha = alpha_max;
+                        use[k] = ok && !(alpha < kCutoff);
+                        al[k] = alpha;
+                    }
+                }
 #pragma unroll
                 for (int k = 0; k < NPIX; ++k) {
-                    if (!valid[k]) continue;
-                    if (term && T[k] < kCutoff) continue;
-                    const double dx = (double)pxs[k] - r_mx[f], dy = (double)pys[k] - r_my[f];
-                    if (!r_full[f]) {
-                        if (pxs[k] < r_x0[f] || pxs[k] > r_x1[f] || pys[k] < r_y0[f] || pys[k] > r_y1[f])
-                            continue;
-                        if (dx * dx + dy * dy > r_rr[f]) continue;
-                    }
-                    const double q = r_ia[f] * dx * dx + 2.0 * r_ib[f] * dx * dy + r_ic[f] * dy * dy;
-                    double alpha = r_op[f] * exp_nonpos(-0.5 * q);
-                    if (alpha > alpha_max) alpha = alpha_max;
-                    if (alpha < kCutoff) continue;
+                    if (!use[k]) continue;
+                    const double alpha = al[k];
                     const double om = 1.0 - alpha;
                     const int32_t b0 = r_start[f], cnt = r_count[f];
                     const double T0 = T[k];
@@ -1186,23 +1220,23 @@ __global__ void __launch_bounds__(kCT, kCompMinBlocks) k_composite(CompParams P)
                     const float omf = (float)om;
                     if (want_rgb) {
                         const float3 S = horner3(scol + b0, m, omf);
-                        c0[k] = __fma_rn(wa, (double)S.x, c0[k]);
-                        c1[k] = __fma_rn(wa, (double)S.y, c1[k]);
-                        c2[k] = __fma_rn(wa, (double)S.z, c2[k]);
+                        c0[k] = acc_fma(wa, S.x, c0[k]);
+                        c1[k] = acc_fma(wa, S.y, c1[k]);
+                        c2[k] = acc_fma(wa, S.z, c2[k]);
                     }
                     if (want_n) {
                         if (r_uni[f]) {
-                            n0[k] = __fma_rn(wsum, r_rn[0][f], n0[k]);
-                            n1[k] = __fma_rn(wsum, r_rn[1][f], n1[k]);
-                            n2[k] = __fma_rn(wsum, r_rn[2][f], n2[k]);
+                            n0[k] = acc_fma(wsum, r_rn[0][f], n0[k]);
+                            n1[k] = acc_fma(wsum, r_rn[1][f], n1[k]);
+                            n2[k] = acc_fma(wsum, r_rn[2][f], n2[k]);
                         } else {
                             const float3 S = horner3(snrm + b0, m, omf);
-                            n0[k] = __fma_rn(wa, (double)S.x, n0[k]);
-                            n1[k] = __fma_rn(wa, (double)S.y, n1[k]);
-                            n2[k] = __fma_rn(wa, (double)S.z, n2[k]);
+                            n0[k] = acc_fma(wa, S.x, n0[k]);
+                            n1[k] = acc_fma(wa, S.y, n1[k]);
+                            n2[k] = acc_fma(wa, S.z, n2[k]);
                         }
                     }
-                    if (want_d) dd[k] = __fma_rn(wsum, r_dep[f], dd[k]);
+                    if (want_d) dd[k] = acc_fma(wsum, r_dep[f], dd[k]);
                     T[k] = Tend;
                 }
             }
@@ -1210,7 +1244,7 @@ __global__ void __launch_bounds__(kCT, kCompMinBlocks) k_composite(CompParams P)
             if (term) done = __syncthreads_and(saturated());
             else __syncthreads();
         }
-        ws = min(ws * 2, kWin);
+        if (threadIdx.x == 0) s_ws = min(s_ws * 2, kWin);
         if (P.dbg && threadIdx.x == 0) {
             atomicAdd((unsigned long long *)&P.dbg[4 * t + 0], 1ull);
             atomicAdd((unsigned long long *)&P.dbg[4 * t + 1], (unsigned long long)nlist);
