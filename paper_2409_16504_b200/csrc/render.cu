@@ -923,6 +923,33 @@ __device__ __forceinline__ float acc_fma(double w, double v, float c) {
     return __fmaf_rn((float)w, (float)v, c);
 }
 
+// The same sums for two pixels that blend the same m points of a run (the
+// usual case: a thread's two pixels share the tile's runs): one load of each
+// point feeds both pixels, one Horner chain per pixel ((x, y) paired FFMA2s,
+// the two pixels' z in a third).
+__device__ __forceinline__ void horner3x2(const float4 *__restrict__ v, int m, float om0, float om1,
+                                          float3 &S0, float3 &S1) {
+    const float2 o0 = make_float2(om0, om0), o1 = make_float2(om1, om1), oz = make_float2(om0, om1);
+    float2 xy0 = make_float2(0.f, 0.f), xy1 = make_float2(0.f, 0.f), z = make_float2(0.f, 0.f);
+    auto step = [&](const float4 a) {
+        const float2 axy = make_float2(a.x, a.y);
+        xy0 = __ffma2_rn(xy0, o0, axy);
+        xy1 = __ffma2_rn(xy1, o1, axy);
+        z = __ffma2_rn(z, oz, make_float2(a.z, a.z));
+    };
+    int j = m - 1;
+    for (; j >= 3; j -= 4) {
+        const float4 a = __ldg(v + j), b = __ldg(v + j - 1), c = __ldg(v + j - 2), d = __ldg(v + j - 3);
+        step(a);
+        step(b);
+        step(c);
+        step(d);
+    }
+    for (; j >= 0; --j) step(__ldg(v + j));
+    S0 = make_float3(xy0.x, xy0.y, z.x);
+    S1 = make_float3(xy1.x, xy1.y, z.y);
+}
+
 // One CTA per tile. The rank-ordered fine / super / global lists are merged
 // in rank windows (bitmap + ordered compaction), candidate runs are staged
 // in chunks, and every pixel blends each covering run in closed form: a
@@ -1185,12 +1212,19 @@ __global__ void __launch_bounds__(kCT, kCompMinBlocks) k_composite(CompParams P)
                         al[k] = alpha;
                     }
                 }
+                // per pixel: points blended (m) and the weights, in float64
+                int mm[NPIX];
+                double wa[NPIX], wsum[NPIX];
+                float omf[NPIX];
+                const int32_t b0 = r_start[f], cnt = r_count[f];
 #pragma unroll
                 for (int k = 0; k < NPIX; ++k) {
+                    mm[k] = 0;
+                    wa[k] = wsum[k] = 0.0;
+                    omf[k] = 0.f;
                     if (!use[k]) continue;
                     const double alpha = al[k];
                     const double om = 1.0 - alpha;
-                    const int32_t b0 = r_start[f], cnt = r_count[f];
                     const double T0 = T[k];
                     int m = cnt;
                     double Tend;
@@ -1215,29 +1249,56 @@ __global__ void __launch_bounds__(kCT, kCompMinBlocks) k_composite(CompParams P)
                         atomicAdd((unsigned long long *)&P.dbg[4 * t + 2], 1ull);
                         atomicAdd((unsigned long long *)&P.dbg[4 * t + 3], (unsigned long long)m);
                     }
-                    const double wa = T0 * alpha;    // weight of the run's first point
-                    const double wsum = T0 - Tend;   // total weight of its m points
-                    const float omf = (float)om;
-                    if (want_rgb) {
-                        const float3 S = horner3(scol + b0, m, omf);
-                        c0[k] = acc_fma(wa, S.x, c0[k]);
-                        c1[k] = acc_fma(wa, S.y, c1[k]);
-                        c2[k] = acc_fma(wa, S.z, c2[k]);
-                    }
-                    if (want_n) {
-                        if (r_uni[f]) {
-                            n0[k] = acc_fma(wsum, r_rn[0][f], n0[k]);
-                            n1[k] = acc_fma(wsum, r_rn[1][f], n1[k]);
-                            n2[k] = acc_fma(wsum, r_rn[2][f], n2[k]);
-                        } else {
-                            const float3 S = horner3(snrm + b0, m, omf);
-                            n0[k] = acc_fma(wa, S.x, n0[k]);
-                            n1[k] = acc_fma(wa, S.y, n1[k]);
-                            n2[k] = acc_fma(wa, S.z, n2[k]);
+                    mm[k] = m;
+                    wa[k] = T0 * alpha;    // weight of the run's first point
+                    wsum[k] = T0 - Tend;   // total weight of its m points
+                    omf[k] = (float)om;
+                    T[k] = Tend;
+                }
+                // colour (and non-uniform normal) sums: pixel pairs with the
+                // same m share the loads of the run's points
+                auto sums = [&](const float4 *__restrict__ v, CompAcc *a0, CompAcc *a1, CompAcc *a2) {
+#pragma unroll
+                    for (int k = 0; k < NPIX; k += 2) {
+                        if (k + 1 < NPIX && use[k] && use[k + 1] && mm[k] == mm[k + 1]) {
+                            float3 S0, S1;
+                            horner3x2(v, mm[k], omf[k], omf[k + 1], S0, S1);
+                            a0[k] = acc_fma(wa[k], S0.x, a0[k]);
+                            a1[k] = acc_fma(wa[k], S0.y, a1[k]);
+                            a2[k] = acc_fma(wa[k], S0.z, a2[k]);
+                            a0[k + 1] = acc_fma(wa[k + 1], S1.x, a0[k + 1]);
+                            a1[k + 1] = acc_fma(wa[k + 1], S1.y, a1[k + 1]);
+                            a2[k + 1] = acc_fma(wa[k + 1], S1.z, a2[k + 1]);
+                            continue;
+                        }
+#pragma unroll
+                        for (int u = k; u < k + 2 && u < NPIX; ++u) {
+                            if (!use[u]) continue;
+                            const float3 S = horner3(v, mm[u], omf[u]);
+                            a0[u] = acc_fma(wa[u], S.x, a0[u]);
+                            a1[u] = acc_fma(wa[u], S.y, a1[u]);
+                            a2[u] = acc_fma(wa[u], S.z, a2[u]);
                         }
                     }
-                    if (want_d) dd[k] = acc_fma(wsum, r_dep[f], dd[k]);
-                    T[k] = Tend;
+                };
+                if (want_rgb) sums(scol + b0, c0, c1, c2);
+                if (want_n) {
+                    if (r_uni[f]) {
+#pragma unroll
+                        for (int k = 0; k < NPIX; ++k) {
+                            if (!use[k]) continue;
+                            n0[k] = acc_fma(wsum[k], r_rn[0][f], n0[k]);
+                            n1[k] = acc_fma(wsum[k], r_rn[1][f], n1[k]);
+                            n2[k] = acc_fma(wsum[k], r_rn[2][f], n2[k]);
+                        }
+                    } else {
+                        sums(snrm + b0, n0, n1, n2);
+                    }
+                }
+                if (want_d) {
+#pragma unroll
+                    for (int k = 0; k < NPIX; ++k)
+                        if (use[k]) dd[k] = acc_fma(wsum[k], r_dep[f], dd[k]);
                 }
             }
             if (done) break;
