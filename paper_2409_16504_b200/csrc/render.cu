@@ -867,17 +867,6 @@ __device__ __forceinline__ double tile_min_q(double ia, double ib, double ic, do
     return m;
 }
 
-// b^e for e >= 0 by repeated squaring (float64)
-__device__ __forceinline__ double ipow(double b, int e) {
-    double r = 1.0;
-    while (e) {
-        if (e & 1) r = r * b;
-        b = b * b;
-        e >>= 1;
-    }
-    return r;
-}
-
 // sum_{j<m} om^j v_j (float32; v in rank order). Two interleaved Horner
 // chains in om^2 (even and odd points), S = E + om * O, so two independent
 // chains and four 16-byte loads are in flight per step; the (x, y) channels
@@ -1217,6 +1206,25 @@ __global__ void __launch_bounds__(kCT, kCompMinBlocks) k_composite(CompParams P)
                 double wa[NPIX], wsum[NPIX];
                 float omf[NPIX];
                 const int32_t b0 = r_start[f], cnt = r_count[f];
+                // (1-alpha)^e for all pixels in one square-and-multiply loop
+                // (e is the run's: uniform across the warp)
+                double pw[NPIX];
+                {
+                    double bb[NPIX];
+#pragma unroll
+                    for (int k = 0; k < NPIX; ++k) {
+                        pw[k] = 1.0;
+                        bb[k] = 1.0 - al[k];
+                    }
+                    for (int ex = term ? cnt - 1 : cnt; ex; ex >>= 1) {
+                        if (ex & 1) {
+#pragma unroll
+                            for (int k = 0; k < NPIX; ++k) pw[k] = pw[k] * bb[k];
+                        }
+#pragma unroll
+                        for (int k = 0; k < NPIX; ++k) bb[k] = bb[k] * bb[k];
+                    }
+                }
 #pragma unroll
                 for (int k = 0; k < NPIX; ++k) {
                     mm[k] = 0;
@@ -1229,7 +1237,7 @@ __global__ void __launch_bounds__(kCT, kCompMinBlocks) k_composite(CompParams P)
                     int m = cnt;
                     double Tend;
                     if (term) {
-                        const double Tl = T0 * ipow(om, cnt - 1);   // T before the last point
+                        const double Tl = T0 * pw[k];   // T before the last point
                         if (Tl >= kCutoff * (1.0 + 1e-12)) {
                             Tend = Tl * om;
                         } else {   // the run crosses the cutoff: exact per-point iteration
@@ -1243,7 +1251,7 @@ __global__ void __launch_bounds__(kCT, kCompMinBlocks) k_composite(CompParams P)
                             Tend = Tt;
                         }
                     } else {
-                        Tend = T0 * ipow(om, cnt);
+                        Tend = T0 * pw[k];
                     }
                     if (P.dbg) {
                         atomicAdd((unsigned long long *)&P.dbg[4 * t + 2], 1ull);

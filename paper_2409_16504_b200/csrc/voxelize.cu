@@ -150,6 +150,36 @@ __global__ void k_keygen(const double *__restrict__ pos, int64_t n, const FrameP
     }
 }
 
+// keys of at most 32 bits: one 64-bit word per point, (index << 32) | key, so
+// each radix pass scatters one 8-byte word instead of a key and a value
+__global__ void k_keygen_packed(const double *__restrict__ pos, int64_t n,
+                                const FrameParams *__restrict__ P, unsigned long long *__restrict__ kv) {
+    const double s = P->s;
+    const int bx = P->bits[0], bxy = P->bits[0] + P->bits[1];
+    const int64_t lx = P->lo[0], ly = P->lo[1], lz = P->lo[2];
+    SFB_FOR(i, n) {
+        int64_t ix = (int64_t)floor(__dmul_rn(pos[3 * i + 0], s)) - lx;
+        int64_t iy = (int64_t)floor(__dmul_rn(pos[3 * i + 1], s)) - ly;
+        int64_t iz = (int64_t)floor(__dmul_rn(pos[3 * i + 2], s)) - lz;
+        kv[i] = ((unsigned long long)i << 32) |
+                (uint32_t)(((uint64_t)iz << bxy) | ((uint64_t)iy << bx) | (uint64_t)ix);
+    }
+}
+
+// sorted (key, point) readers of k_vox_segments: split arrays or packed words
+template <class K>
+struct SplitKV {
+    const K *k;
+    const uint32_t *v;
+    __device__ __forceinline__ K key(int64_t i) const { return k[i]; }
+    __device__ __forceinline__ uint32_t val(int64_t i) const { return v[i]; }
+};
+struct PackedKV {
+    const unsigned long long *p;
+    __device__ __forceinline__ uint32_t key(int64_t i) const { return (uint32_t)p[i]; }
+    __device__ __forceinline__ uint32_t val(int64_t i) const { return (uint32_t)(p[i] >> 32); }
+};
+
 // Segmentation of the sorted point keys in one pass (np.unique's sorted keys,
 // inverse and CSR of voxelgrid.py:146, 165-168): head flags from adjacent
 // keys, their inclusive scan by decoupled look-back (tiles in ticket order),
@@ -158,9 +188,9 @@ __global__ void k_keygen(const double *__restrict__ pos, int64_t n, const FrameP
 // kernel, a scan and a segment kernel (and the flag array's round trips).
 constexpr int kSegThreads = 1024, kSegItems = 4, kSegTile = kSegThreads * kSegItems;
 
-template <class K>
+template <class K, class KV>
 __global__ void __launch_bounds__(kSegThreads)
-k_vox_segments(const K *__restrict__ keys, const uint32_t *__restrict__ vals, int64_t n,
+k_vox_segments(const KV kv, int64_t n,
                const FrameParams *__restrict__ P, int32_t *__restrict__ coords,
                int64_t *__restrict__ pkeys, int32_t *__restrict__ p2v, int32_t *__restrict__ order,
                int32_t *__restrict__ offsets, DevCounts *__restrict__ C,
@@ -184,8 +214,8 @@ k_vox_segments(const K *__restrict__ keys, const uint32_t *__restrict__ vals, in
             const int64_t i = base + k * kSegThreads + threadIdx.x;
             f[k] = 0;
             if (i < n) {
-                key[k] = keys[i];
-                f[k] = (i == 0 || key[k] != keys[i - 1]) ? 1 : 0;
+                key[k] = kv.key(i);
+                f[k] = (i == 0 || key[k] != kv.key(i - 1)) ? 1 : 0;
             }
             s_val[k * kSegThreads + threadIdx.x] = f[k];
         }
@@ -215,7 +245,7 @@ k_vox_segments(const K *__restrict__ keys, const uint32_t *__restrict__ vals, in
             const int64_t j = base + k * kSegThreads + threadIdx.x;
             if (j >= n) continue;
             const int32_t vox = s_val[k * kSegThreads + threadIdx.x] - 1;
-            const uint32_t i = vals[j];
+            const uint32_t i = kv.val(j);
             order[j] = (int32_t)i;
             p2v[i] = vox;
             if (j == n - 1) {
@@ -280,26 +310,41 @@ template <class K>
 static void voxelize_typed(sfb_ctx *ctx, const double *pos, const double *col, int64_t n,
                            const FrameParams *P, int key_bits, VoxelOut &out, DevCounts *C) {
     cudaStream_t st = ctx->stream;
-    K *keys = ctx->arena.alloc<K>(n), *keys2 = ctx->arena.alloc<K>(n);
-    uint32_t *vals = ctx->arena.alloc<uint32_t>(n), *vals2 = ctx->arena.alloc<uint32_t>(n);
     const unsigned g = dgrid(n, 256);
-    k_keygen<K><<<g, 256, 0, st>>>(pos, n, P, keys, vals);
-    SFB_CHECK_LAUNCH();
     // the library's own stable LSD sort (devprims.cu: 8-bit digits, 1024-item
     // sub-tiles ranked with __match_any_sync, small shared memory so its CTAs
-    // share SMs with the other lanes' kernels)
-    const bool second = dsort_pairs<K>(ctx, keys, vals, keys2, vals2, nullptr, n, key_bits);
-    K *ks = second ? keys2 : keys;
-    uint32_t *vs = second ? vals2 : vals;
+    // share SMs with the other lanes' kernels) on the key bits only: equal
+    // keys keep ascending point order
+    constexpr bool packed = sizeof(K) == 4;
+    SplitKV<K> skv{};
+    PackedKV pkv{};
+    if (packed) {
+        auto *w = ctx->arena.alloc<unsigned long long>(n), *w2 = ctx->arena.alloc<unsigned long long>(n);
+        k_keygen_packed<<<g, 256, 0, st>>>(pos, n, P, w);
+        SFB_CHECK_LAUNCH();
+        pkv.p = dsort_pairs<unsigned long long>(ctx, w, nullptr, w2, nullptr, nullptr, n, key_bits) ? w2 : w;
+    } else {
+        K *keys = ctx->arena.alloc<K>(n), *keys2 = ctx->arena.alloc<K>(n);
+        uint32_t *vals = ctx->arena.alloc<uint32_t>(n), *vals2 = ctx->arena.alloc<uint32_t>(n);
+        k_keygen<K><<<g, 256, 0, st>>>(pos, n, P, keys, vals);
+        SFB_CHECK_LAUNCH();
+        const bool second = dsort_pairs<K>(ctx, keys, vals, keys2, vals2, nullptr, n, key_bits);
+        skv.k = second ? keys2 : keys;
+        skv.v = second ? vals2 : vals;
+    }
     {
         const int64_t tiles = (n + kSegTile - 1) / kSegTile;
         const size_t bytes = sizeof(unsigned long long) * (size_t)(tiles + 1);
         auto *status = static_cast<unsigned long long *>(ctx->arena.alloc_bytes(bytes));
         SFB_CUDA(cudaMemsetAsync(status, 0, bytes, st));
         const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(tiles, 2 * 148));
-        k_vox_segments<K><<<grid, kSegThreads, 0, st>>>(ks, vs, n, P, out.coords, out.keys, out.p2v,
-                                                        out.order, out.offsets, C, status,
-                                                        reinterpret_cast<unsigned int *>(status + tiles));
+        auto *ticket = reinterpret_cast<unsigned int *>(status + tiles);
+        if (packed)
+            k_vox_segments<uint32_t><<<grid, kSegThreads, 0, st>>>(pkv, n, P, out.coords, out.keys, out.p2v,
+                                                               out.order, out.offsets, C, status, ticket);
+        else
+            k_vox_segments<K><<<grid, kSegThreads, 0, st>>>(skv, n, P, out.coords, out.keys, out.p2v,
+                                                        out.order, out.offsets, C, status, ticket);
     }
     SFB_CHECK_LAUNCH();
     const int64_t vwarps = (ctx->grid_bound(n, ctx->hint_m[0]) + 4) / 5;
