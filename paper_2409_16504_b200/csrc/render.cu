@@ -388,6 +388,15 @@ __global__ void k_run_heads(const uint32_t *__restrict__ src, const int64_t *__r
     }
 }
 
+// Alpha-support test of a whole tile. forward_kernel blends a splat at a
+// pixel only if alpha = min(o exp(-q/2), alpha_max) >= 1/255, i.e. only if
+// q <= 2 ln(255 o). q_cut widens that bound by a relative 1e-6 (+1e-6), far
+// beyond the float64 rounding of q and of the exp, so skipping a run whose
+// q exceeds q_cut at every pixel of a tile never drops a contribution.
+__device__ __forceinline__ double q_cut(double op) {
+    return 2.0 * log(fmax(255.0 * op, 1e-300)) * (1.0 + 1e-6) + 1e-6;
+}
+
 // What the compositor stages per candidate run, packed so a run costs a few
 // 16-byte loads: geometry (conic, centre, opacity, support radius, depth)
 // and the attribute side (first normal, point range, uniform-normal flag).
@@ -398,8 +407,10 @@ struct __align__(16) RunAux {
     double rn[3];          // normal of the run's first point
     int32_t start, count;  // the run's points in rank order
     int32_t uni, pad;      // 1 when every point of the run has the same normal
+    double qcut;           // q_cut(opacity): the run's alpha-support bound
 };
-static_assert(sizeof(RunAux) == 48 && offsetof(RunAux, start) == 24 && offsetof(RunAux, uni) == 32,
+static_assert(sizeof(RunAux) == 48 && offsetof(RunAux, start) == 24 && offsetof(RunAux, uni) == 32 &&
+                  offsetof(RunAux, qcut) == 40,
               "the compositor stages RunAux as three double2 loads");
 
 struct Runs {
@@ -707,6 +718,7 @@ __global__ void k_stage_runs(Runs R, const uint32_t *__restrict__ src, const int
         const int64_t g0 = p2g ? p2g[i0] : (int64_t)i0;
         R.rec[r].dep = gdepth[g0];
         RunAux &x = R.aux[r];
+        x.qcut = q_cut(R.rec[r].op);
         x.start = R.start[r];
         x.count = R.count[r];
         x.pad = 0;
@@ -836,14 +848,6 @@ __device__ __forceinline__ double exp_nonpos(double x) {
     return under ? 0.0 : p * __longlong_as_double((long long)(k + 1023) << 52);
 }
 
-// Alpha-support test of a whole tile. forward_kernel blends a splat at a
-// pixel only if alpha = min(o exp(-q/2), alpha_max) >= 1/255, i.e. only if
-// q <= 2 ln(255 o). q_cut widens that bound by a relative 1e-6 (+1e-6), far
-// beyond the float64 rounding of q and of the exp, so skipping a run whose
-// q exceeds q_cut at every pixel of a tile never drops a contribution.
-__device__ __forceinline__ double q_cut(double op) {
-    return 2.0 * log(fmax(255.0 * op, 1e-300)) * (1.0 + 1e-6) + 1e-6;
-}
 
 // min over the rectangle [x0,x1] x [y0,y1] (offsets from the centre) of the
 // positive-definite form q(d) = ia dx^2 + 2 ib dx dy + ic dy^2: 0 when the
@@ -957,7 +961,6 @@ __global__ void __launch_bounds__(kCT, kCompMinBlocks) k_composite(CompParams P)
     constexpr uint32_t NONE = 0xffffffffu;
     __shared__ uint32_t bitmap[kWin / 32];
     __shared__ uint32_t list[kWin];
-    __shared__ int s_nlist;
     __shared__ uint32_t s_add[3];
     __shared__ uint32_t s_head;
     __shared__ unsigned s_bal[kCT / 32];
@@ -1073,33 +1076,34 @@ __global__ void __launch_bounds__(kCT, kCompMinBlocks) k_composite(CompParams P)
         __syncthreads();
         // read again only after the compaction's barrier
         if (threadIdx.x < 3) cur[threadIdx.x] += (int32_t)s_add[threadIdx.x];
-        // ordered compaction of the bitmap by warp 0 (2 words per lane)
-        if (threadIdx.x < 32) {
-            const int lane = threadIdx.x;
+        // ordered compaction of the bitmap by all threads: every warp forms
+        // the words' prefix counts (2 words per lane, shuffle scan), then
+        // each thread places the set bits among its rank positions
+        // p = tid + kCT k (a warp's 32 positions are one word)
+        int nlist;
+        {
+            const int lane = threadIdx.x & 31;
             const int nw = ws / 32;
-            uint32_t wa = 2 * lane < nw ? bitmap[2 * lane] : 0u;
-            uint32_t wb = 2 * lane + 1 < nw ? bitmap[2 * lane + 1] : 0u;
-            int ca = __popc(wa), cb = __popc(wb);
+            const uint32_t wa = 2 * lane < nw ? bitmap[2 * lane] : 0u;
+            const uint32_t wb = 2 * lane + 1 < nw ? bitmap[2 * lane + 1] : 0u;
+            const int ca = __popc(wa), cb = __popc(wb);
             int incl = ca + cb;
             for (int o = 1; o < 32; o <<= 1) {
-                int v = __shfl_up_sync(0xffffffffu, incl, o);
+                const int v = __shfl_up_sync(0xffffffffu, incl, o);
                 if (lane >= o) incl += v;
             }
-            int pos = incl - ca - cb;
-            while (wa) {
-                int b = __ffs(wa) - 1;
-                wa &= wa - 1;
-                list[pos++] = w0 + 64 * lane + b;
+            const int pre = incl - ca - cb;   // set bits before word 2 * lane
+            nlist = __shfl_sync(0xffffffffu, incl, 31);
+            for (int p0 = threadIdx.x & ~31; p0 < ws; p0 += kCT) {
+                const int wi = p0 >> 5;   // warp-uniform
+                const int base = __shfl_sync(0xffffffffu, pre, wi >> 1) +
+                                 ((wi & 1) ? __shfl_sync(0xffffffffu, ca, wi >> 1) : 0);
+                const uint32_t word = (wi & 1) ? __shfl_sync(0xffffffffu, wb, wi >> 1)
+                                               : __shfl_sync(0xffffffffu, wa, wi >> 1);
+                if ((word >> lane) & 1u) list[base + __popc(word & ((1u << lane) - 1u))] = w0 + p0 + lane;
             }
-            while (wb) {
-                int b = __ffs(wb) - 1;
-                wb &= wb - 1;
-                list[pos++] = w0 + 64 * lane + 32 + b;
-            }
-            if (lane == 31) s_nlist = incl;
         }
         __syncthreads();
-        const int nlist = s_nlist;
         // chunks of candidate runs grow 16 -> 128: most tiles saturate within
         // the first few contributing runs. Each candidate is staged by one
         // thread, which also drops it when its alpha-support ellipse misses the
@@ -1128,7 +1132,7 @@ __global__ void __launch_bounds__(kCT, kCompMinBlocks) k_composite(CompParams P)
                 r_ic[j] = q2.x;
                 r_op[j] = q2.y;
                 r_dep[j] = q3.y;
-                // RunAux as double2: {rn0, rn1}, {rn2, (start, count)}, {(uni, pad), -}
+                // RunAux as double2: {rn0, rn1}, {rn2, (start, count)}, {(uni, pad), qcut}
                 r_start[j] = __double2loint(a1.y);
                 r_count[j] = __double2hiint(a1.y);
                 r_uni[j] = (uint8_t)__double2loint(a2.x);
@@ -1154,7 +1158,7 @@ __global__ void __launch_bounds__(kCT, kCompMinBlocks) k_composite(CompParams P)
                             fx * fx + fy * fy <= rad * rad;
                 keep = bx0 <= bx1 && by0 <= by1 &&
                        !(tile_min_q(q1.x, q1.y, q2.x, bx0 - mx, bx1 - mx, by0 - my, by1 - my) >
-                         q_cut(q2.y));
+                         a2.y);   // q_cut(opacity), precomputed per run
             }
             const unsigned ball = __ballot_sync(0xffffffffu, keep);
             if ((threadIdx.x & 31) == 0) s_bal[threadIdx.x >> 5] = ball;
