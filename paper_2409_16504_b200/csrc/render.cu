@@ -853,21 +853,25 @@ __device__ __forceinline__ double exp_nonpos(double x) {
 // positive-definite form q(d) = ia dx^2 + 2 ib dx dy + ic dy^2: 0 when the
 // centre is inside, else the least of the four edge minima (a 1-D quadratic
 // per edge, minimised at its clamped stationary point). Returns 0 (no cull)
-// for a degenerate conic.
-__device__ __forceinline__ double edge_min(double a, double b, double c, double fixed, double lo,
-                                           double hi) {
+// for a degenerate conic. The stationary point is fixed * slope with the
+// slope -b/c divided once per pair of parallel edges (its rounding moves the
+// evaluated point by ~1e-16 relative: q changes quadratically, far inside
+// q_cut's 1e-6 margin).
+__device__ __forceinline__ double edge_min(double a, double b, double c, double slope, double fixed,
+                                           double lo, double hi) {
     // q(t) = a fixed^2 + 2 b fixed t + c t^2 over t in [lo, hi]
-    const double t = fmin(fmax(-b * fixed / c, lo), hi);
+    const double t = fmin(fmax(slope * fixed, lo), hi);
     return a * fixed * fixed + 2.0 * b * fixed * t + c * t * t;
 }
 __device__ __forceinline__ double tile_min_q(double ia, double ib, double ic, double x0, double x1,
                                              double y0, double y1) {
     if (!(ia > 0.0) || !(ic > 0.0) || !(ia * ic - ib * ib > 0.0)) return 0.0;
     if (x0 <= 0.0 && 0.0 <= x1 && y0 <= 0.0 && 0.0 <= y1) return 0.0;
-    double m = edge_min(ia, ib, ic, x0, y0, y1);
-    m = fmin(m, edge_min(ia, ib, ic, x1, y0, y1));
-    m = fmin(m, edge_min(ic, ib, ia, y0, x0, x1));
-    m = fmin(m, edge_min(ic, ib, ia, y1, x0, x1));
+    const double sx = -ib / ic, sy = -ib / ia;
+    double m = edge_min(ia, ib, ic, sx, x0, y0, y1);
+    m = fmin(m, edge_min(ia, ib, ic, sx, x1, y0, y1));
+    m = fmin(m, edge_min(ic, ib, ia, sy, y0, x0, x1));
+    m = fmin(m, edge_min(ic, ib, ia, sy, y1, x0, x1));
     return m;
 }
 
