@@ -47,25 +47,37 @@ def main():
     from paper_2409_16504_b200 import sparsenet
     sparsenet.set_mode(a.net_mode)
     w = netplan.init_random(netplan.NetworkPlan(), 0)
-    rep = {"tolerance": 2e-3, "net_mode": a.net_mode, "configs": {}}
+    what = {
+        "tc_tf32x3": "Full-frame parity of the fused GPU frame (sfb_frame, what bench.py times) vs the CPU "
+                     "oracle, every BASELINE config, default network mode tc_tf32x3 (tools/parity_report.py, "
+                     "tests/parity_util.py). order/rects/offsets: fused rank order and per-rank tile ranges vs "
+                     "the oracle's _prepare/bin_tiles on the same Gaussians; renderer: planes vs the oracle "
+                     "renderer on the same Gaussians; e2e: GPU cloud->planes vs oracle cloud->planes; "
+                     "e2e_over_pixels: every end-to-end pixel over 2e-3 classified by replaying both blend "
+                     "sequences.",
+        "simt_f64": "Full-frame parity of the fused GPU frame vs the CPU oracle in the float64 network mode "
+                    "(SFB_NET_SIMT_F64, the reference's own arithmetic) (tools/parity_report.py --net-mode "
+                    "simt_f64).",
+    }.get(a.net_mode, a.net_mode)
+    rep = {"what": what, "net_mode": a.net_mode, "tolerance": 2e-3, "frames": {}}
     cloud, views = scenes.config1()
-    rep["configs"]["c1"] = run(cloud, views, w, range(len(views)), "c1")
+    rep["frames"]["c1"] = run(cloud, views, w, range(len(views)), "c1")
     cloud, views = scenes.config2()
-    rep["configs"]["c2"] = run(cloud, views, w, range(len(views)), "c2")
+    rep["frames"]["c2"] = run(cloud, views, w, range(len(views)), "c2")
     cloud, views = scenes.config3()
-    rep["configs"]["c3"] = run(cloud, views, w, range(min(a.c3_views, len(views))), "c3")
+    rep["frames"]["c3"] = run(cloud, views, w, range(min(a.c3_views, len(views))), "c3")
     c4 = []
     for f in range(a.c4_frames):
         cloud, views = scenes.config4_frame(f)
         r = run(cloud, views, w, (0,), f"c4 frame {f}", levels_for=())
         r[0]["frame"] = f
         c4 += r
-    rep["configs"]["c4"] = c4
+    rep["frames"]["c4"] = c4
     cloud, views = scenes.config5()
-    rep["configs"]["c5"] = run(cloud, views, w, range(min(a.c5_views, len(views))), "c5",
+    rep["frames"]["c5"] = run(cloud, views, w, range(min(a.c5_views, len(views))), "c5",
                                levels_for=(0,))
     summ = {}
-    for name, recs in rep["configs"].items():
+    for name, recs in rep["frames"].items():
         summ[name] = {
             "frames": len(recs),
             "order_exact": all(r["order"]["order_exact"] for r in recs),
