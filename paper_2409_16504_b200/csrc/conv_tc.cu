@@ -206,7 +206,12 @@ struct TcShape {
     static constexpr int BAR_OFF = RAW_OFF + RAW_FLOATS;
     // + the kernel-map rows of one item's taps, sized per launch (src_rows)
     static constexpr int SMEM = BAR_OFF * 4 + 1024 + 128;
-    static constexpr int smem_bytes(int src_rows) { return SMEM + src_rows * kM * 4; }
+    // the ring is only laid out for the ring staging modes: register-prefetch
+    // CTAs (the default) take the buffers + barriers + kernel-map rows only,
+    // so more of them (and other lanes' kernels) fit on an SM
+    static constexpr int smem_bytes(int src_rows, bool ring = true) {
+        return (ring ? SMEM : RAW_OFF * 4 + 1024 + 128) + src_rows * kM * 4;
+    }
     // two accumulators (tap t in buffer t % 2): the epilogue of tap t-1 reads
     // one while the MMAs of tap t write the other
     static constexpr uint32_t TMEM_COLS = 2 * NP <= 32 ? 32 : (2 * NP <= 64 ? 64 : (2 * NP <= 128 ? 128 : 256));
@@ -251,13 +256,21 @@ k_conv_tc(const float *__restrict__ in, int ld_in, int cin, const int32_t *__res
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     float *stage_base = reinterpret_cast<float *>(
         (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-    float *raw = stage_base + S::RAW_OFF;   // TMA ring [RS][TAPB][kM][KP]
-    uint64_t *bar_full = reinterpret_cast<uint64_t *>(stage_base + S::BAR_OFF);
+    // A-row staging: 0 = register prefetch one batch ahead; 1 = TMA gather4
+    // into the shared ring, RS batches ahead; 2 = each thread's own row by
+    // cp.async (LDGSTS) into the ring, RS batches ahead (no barrier: a thread
+    // only reads the row it copied)
+    const bool use_tma = S::TMA_OK && tma == 1;
+    const bool use_cpa = S::TMA_OK && tma == 2;
+    const bool use_ring = use_tma || use_cpa;
+    float *raw = stage_base + S::RAW_OFF;   // TMA ring [RS][TAPB][kM][KP] (ring modes only)
+    const int bar_off = use_ring ? S::BAR_OFF : S::RAW_OFF;
+    uint64_t *bar_full = reinterpret_cast<uint64_t *>(stage_base + bar_off);
     uint64_t *bar_done = bar_full + 2;   // indexed by batch parity (i & 1), phase i >> 1
     uint64_t *raw_full = bar_done + 2;   // [RS]: stage s's rows landed
     uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(raw_full + 4);
     // kernel-map rows of this item's taps: s_src[t - t0][tid]
-    int32_t (*s_src)[kM] = reinterpret_cast<int32_t (*)[kM]>(stage_base + S::BAR_OFF + 32);
+    int32_t (*s_src)[kM] = reinterpret_cast<int32_t (*)[kM]>(stage_base + bar_off + 32);
 
     const int tid = threadIdx.x, warp = tid >> 5;
     const int64_t m = d_m ? *d_m : m_fixed;
@@ -277,13 +290,6 @@ k_conv_tc(const float *__restrict__ in, int ld_in, int cin, const int32_t *__res
         for (int s = 0; s < 4; ++s) mbar_init(&raw_full[s], 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
-    // A-row staging: 0 = register prefetch one batch ahead; 1 = TMA gather4
-    // into the shared ring, RS batches ahead; 2 = each thread's own row by
-    // cp.async (LDGSTS) into the ring, RS batches ahead (no barrier: a thread
-    // only reads the row it copied)
-    const bool use_tma = S::TMA_OK && tma == 1;
-    const bool use_cpa = S::TMA_OK && tma == 2;
-    const bool use_ring = use_tma || use_cpa;
     if (warp == 0) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
                          smem_u32(tmem_slot)),
@@ -731,7 +737,7 @@ void launch_tc(sfb_ctx *ctx, const NetLayer &L, const float *in, int ld_in, cons
         cudaLaunchConfig_t cfg{};
         cfg.gridDim = dim3((unsigned)(std::max<int64_t>(1, std::min(tiles_bound, m_tiles)) * csplit));
         cfg.blockDim = dim3(kThreadsTC);
-        cfg.dynamicSmemBytes = S::smem_bytes(src_rows);
+        cfg.dynamicSmemBytes = S::smem_bytes(src_rows, tma != 0);
         cfg.stream = ctx->stream;
         cudaLaunchAttribute at[1];
         at[0].id = cudaLaunchAttributeClusterDimension;
@@ -754,7 +760,7 @@ void launch_tc(sfb_ctx *ctx, const NetLayer &L, const float *in, int ld_in, cons
     float *partial = ctx->arena.alloc<float>((size_t)std::min<int64_t>(kMaxPartialRows,
                                                                        32 * m_bound) * NP);
     const float *wts = BF ? reinterpret_cast<const float *>(L.w_bf16) : L.w_tc;
-    k_conv_tc<KP, NP, BF><<<grid, kThreadsTC, S::smem_bytes(src_rows), ctx->stream>>>(
+    k_conv_tc<KP, NP, BF><<<grid, kThreadsTC, S::smem_bytes(src_rows, tma != 0), ctx->stream>>>(
         in, ld_in, L.cin, nbr, nbr_ld, d_m, m_bound, L.taps, wts, L.b, L.cout, relu, out, ld_out,
         partial, row_map, tap_off, csplit == 1 ? 1 : 0, src_rows, vec4, tm, tma, oob_row);
     SFB_CHECK_LAUNCH();
