@@ -35,15 +35,18 @@ constexpr double kCutoff = 1.0 / 255.0;
 constexpr int kFineMax = 16;   // tiles per run at the fine level
 constexpr int kSuper = 8;      // tiles per super-tile edge
 constexpr int kSuperMax = 16;  // super tiles per run at the middle level
-constexpr int kWin = 2048;     // rank window of the merge
+constexpr int kWin = 512;      // rank window of the merge
 // compositor CTA: 128 threads, two pixels each for the default 16x16 tile
-// (two independent per-pixel chains per thread), 7 CTAs per SM; A/B on
+// (two independent per-pixel chains per thread), 8 CTAs per SM; A/B on
 // config 2 with 8 frames in flight: 0.308 ms/frame vs 0.316 for 256 threads x
-// one pixel (64 threads x 4 pixels: 0.34, register-starved)
+// one pixel (64 threads x 4 pixels: 0.34, register-starved). The rank window
+// (512) and the chunk (64 runs) keep its shared memory at ~14 KB: the rest of
+// the SM's 256 KB stays L1 for the runs' colour reads (0.0615 vs 0.0625 ms
+// with a 2048-rank window and 128-run chunks)
 constexpr int kCT = 128;       // compositor threads per CTA
 constexpr int kCompMinBlocks = 8;
 constexpr int kCompReps = 4;   // timed re-launches of the compositor in stage-timing mode
-constexpr int kChunk = kCT;    // candidate runs staged per compositing chunk
+constexpr int kChunk = 64;     // candidate runs staged per compositing chunk
 
 // ------------------------------------------------------------ 1. projection
 __device__ __forceinline__ void project_one(const double *__restrict__ p, const double *__restrict__ q,
@@ -1025,7 +1028,7 @@ __global__ void __launch_bounds__(kCT, kCompMinBlocks) k_composite(CompParams P)
         end[s] = s == 0 ? P.f_off[t + 1] : s == 1 ? P.s_off[st + 1] : (int32_t)*P.d_G;
     }
     __syncthreads();
-    __shared__ int s_ws;   // rank window size: 128 -> 2048 (most tiles saturate in the first)
+    __shared__ int s_ws;   // rank window size: 128 -> kWin (most tiles saturate in the first)
     if (threadIdx.x == 0) s_ws = 128;
     bool done = false;
     while (!done) {
@@ -1108,7 +1111,7 @@ __global__ void __launch_bounds__(kCT, kCompMinBlocks) k_composite(CompParams P)
             }
         }
         __syncthreads();
-        // chunks of candidate runs grow 16 -> 128: most tiles saturate within
+        // chunks of candidate runs grow 16 -> kChunk: most tiles saturate within
         // the first few contributing runs. Each candidate is staged by one
         // thread, which also drops it when its alpha-support ellipse misses the
         // tile's pixels (tile_min_q): such a run has alpha < 1/255 at every
