@@ -127,10 +127,11 @@ VoxelSplats neural_voxels(sfb_ctx *ctx, const double *pos, const double *col, in
     o.p2v = ctx->arena.alloc<int32_t>(n);
     o.order = ctx->arena.alloc<int32_t>(n);
     o.offsets = ctx->arena.alloc<int32_t>(n + 1);
+    if (ctx->net_mode != SFB_NET_SIMT_F64) o.feats32 = ctx->arena.alloc<float>(9 * n);
     voxelize_run(ctx, pos, col, n, host, P, o, C);
     ctx->mark(ST_VOXELIZE);
     void *raw = ctx->arena.alloc<double>(14 * n);   // float32 rows, or float64 (SIMT_F64)
-    unet_run(ctx, o.coords, o.feats, n, host, P, C, raw);
+    unet_run(ctx, o.coords, o.feats, n, host, P, C, raw, o.feats32);
     ctx->mark(ST_UNET);
     double *blk = ctx->arena.alloc<double>(14 * n);
     V.c = blk;

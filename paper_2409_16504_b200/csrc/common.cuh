@@ -372,6 +372,7 @@ struct VoxelOut {
     double *feats;
     int64_t *keys;
     int32_t *p2v, *order, *offsets;
+    float *feats32 = nullptr;   // optional: the (M, 9) features also as float32 (UNet input)
 };
 void bbox_run(sfb_ctx *ctx, const double *pos, int64_t n, double *lo_hi_host);
 void bbox_async_run(sfb_ctx *ctx, const double *pos, int64_t n, uint64_t *ordered_host);
@@ -390,8 +391,10 @@ void net_load(sfb_ctx *ctx, const void *blob, size_t n);
 // are sized by it instead of by the point count.
 void unet_level_bounds(const FrameParams &host, int64_t n, int levels, int64_t *bound);
 // raw: float32, or float64 in SFB_NET_SIMT_F64 mode
+// feats32: the level-0 features already as float32 (voxelization writes them), or null
 void unet_run(sfb_ctx *ctx, const int32_t *coords, const double *feats9, int64_t m_bound,
-              const FrameParams &host, const FrameParams *P, DevCounts *C, void *raw);
+              const FrameParams &host, const FrameParams *P, DevCounts *C, void *raw,
+              const float *feats32 = nullptr);
 void activate_run(sfb_ctx *ctx, const double *raw, int64_t m, double scale, double *delta,
                   double *sigma, double *quat, double *opac, double *normal);
 void conv_layer(sfb_ctx *ctx, const NetLayer &L, const float *in, int ld_in, const int32_t *nbr,

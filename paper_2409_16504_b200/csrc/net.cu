@@ -780,7 +780,8 @@ void unet_level_bounds(const FrameParams &host, int64_t n, int levels, int64_t *
 constexpr int kTconvSplit = 8;
 
 void unet_run(sfb_ctx *ctx, const int32_t *coords0, const double *feats9, int64_t mb,
-              const FrameParams &host, const FrameParams *P, DevCounts *C, void *raw_out) {
+              const FrameParams &host, const FrameParams *P, DevCounts *C, void *raw_out,
+              const float *feats32) {
     Net &net = ctx->net;
     SFB_REQUIRE(net.loaded, "network weights are not loaded");
     const int L = net.levels;
@@ -889,9 +890,13 @@ void unet_run(sfb_ctx *ctx, const int32_t *coords0, const double *feats9, int64_
         return;
     }
     float *raw = static_cast<float *>(raw_out);
-    pin[0] = ctx->arena.alloc<float>((size_t)mbl[0] * enc[0]);
-    k_feats_to_f32<<<dgrid(mg[0] * enc[0], 256), 256, 0, st>>>(feats9, &C->m[0], enc[0], pin[0]);
-    SFB_CHECK_LAUNCH();
+    if (feats32 && enc[0] == 9) {
+        pin[0] = const_cast<float *>(feats32);
+    } else {
+        pin[0] = ctx->arena.alloc<float>((size_t)mbl[0] * enc[0]);
+        k_feats_to_f32<<<dgrid(mg[0] * enc[0], 256), 256, 0, st>>>(feats9, &C->m[0], enc[0], pin[0]);
+        SFB_CHECK_LAUNCH();
+    }
     int layer = 0;
     for (int l = 0; l < L; ++l) {
         cat[l] = ctx->arena.alloc<float>((size_t)mbl[l] * width[l]);

@@ -560,6 +560,7 @@ __device__ __forceinline__ int32_t count_below(const int32_t *__restrict__ lst, 
 // thead[rank] = 1 where a tie group's merged order switches voxel (its first
 // rank included): the predecessor of p in the group is the largest group
 // point index below p, found with the same per-voxel binary searches.
+template <int G>   // lanes per voxel (32: one warp; 8 / 16: several voxels per warp)
 __global__ void k_vranks(const int32_t *__restrict__ order, const int32_t *__restrict__ goff,
                          const int32_t *__restrict__ off, const unsigned long long *__restrict__ full,
                          const uint32_t *__restrict__ vs, const int64_t *__restrict__ d_kg,
@@ -569,16 +570,16 @@ __global__ void k_vranks(const int32_t *__restrict__ order, const int32_t *__res
     // the voxel's offsets are loaded once, the point reads / rank writes
     // are coalesced, only the colour gather is random
     const int64_t KG = *d_kg;
-    const int lane = threadIdx.x & 31;
-    const int64_t w0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-    const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    const int lane = threadIdx.x % G;
+    const int64_t w0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) / G;
+    const int64_t nw = ((int64_t)gridDim.x * blockDim.x) / G;
     for (int64_t i = w0; i < KG; i += nw) {
         const uint32_t v = vs[i];
         const int32_t s0 = goff[v], s1 = goff[v + 1];
         int64_t gs, ge;
         const bool tie = tie_group(full, i, KG, gs, ge);
         const int64_t base = tie ? (int64_t)off[gs] : (int64_t)off[i];
-        for (int32_t s = s0 + lane; s < s1; s += 32) {
+        for (int32_t s = s0 + lane; s < s1; s += G) {
             const int32_t p = order[s];
             const int32_t w = s - s0;
             int64_t rank = base + w;
@@ -915,7 +916,7 @@ __device__ __forceinline__ float3 horner3(const float4 *__restrict__ v, int m, f
     return make_float3(fmaf(om, oxy.x, exy.x), fmaf(om, oxy.y, exy.y), fmaf(om, oz, ez));
 }
 
-// Colour / normal / depth accumulators of the compositor (T and every
+// Colour / normal accumulators of the compositor (T, the depth sums and every
 // alpha / cutoff decision stay float64)
 using CompAcc = float;
 __device__ __forceinline__ double acc_fma(double w, double v, double c) { return __fma_rn(w, v, c); }
@@ -995,7 +996,8 @@ __global__ void __launch_bounds__(kCT, kCompMinBlocks) k_composite(CompParams P)
     int32_t pxs[NPIX], pys[NPIX];
     bool valid[NPIX];
     double T[NPIX];
-    CompAcc c0[NPIX], c1[NPIX], c2[NPIX], n0[NPIX], n1[NPIX], n2[NPIX], dd[NPIX];
+    CompAcc c0[NPIX], c1[NPIX], c2[NPIX], n0[NPIX], n1[NPIX], n2[NPIX];
+    double dd[NPIX];   // depth keeps float64 sums: its values are O(scene depth), not O(1)
 #pragma unroll
     for (int k = 0; k < NPIX; ++k) {
         const uint32_t p = threadIdx.x + k * kCT;
@@ -1430,7 +1432,7 @@ static void voxel_order(sfb_ctx *ctx, const RenderInputs &in, const Proj &P, Dev
     k_vcounts<<<gv, 256, 0, st>>>(vs, d_kg, in.geom_offsets, cnt, vpos);
     SFB_CHECK_LAUNCH();
     dscan(ctx, cnt, off, d_kg, nbg, &C->kept, false);
-    k_vranks<<<dgrid(32 * ctx->grid_bound(nbg, ctx->hint_m[0]), 256), 256, 0, st>>>(
+    k_vranks<32><<<dgrid(32 * ctx->grid_bound(nbg, ctx->hint_m[0]), 256), 256, 0, st>>>(
         in.geom_order, in.geom_offsets, off, full, vs, d_kg, in.colors, scol, src, thead);
     SFB_CHECK_LAUNCH();
 }

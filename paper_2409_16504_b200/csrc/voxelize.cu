@@ -276,7 +276,8 @@ k_vox_segments(const KV kv, int64_t n,
 __global__ void k_voxel_feats(const double *__restrict__ pos, const double *__restrict__ col,
                               const int32_t *__restrict__ order, const int32_t *__restrict__ offsets,
                               const int32_t *__restrict__ coords, const DevCounts *__restrict__ C,
-                              const FrameParams *__restrict__ P, double *__restrict__ feats) {
+                              const FrameParams *__restrict__ P, double *__restrict__ feats,
+                              float *__restrict__ feats32) {
     const int64_t m = C->m[0];
     const double s = P->s;
     const int lane = threadIdx.x & 31;
@@ -298,10 +299,16 @@ __global__ void k_voxel_feats(const double *__restrict__ pos, const double *__re
         double *f = feats + 9 * v;
         if (ch < 3) {
             double res = __dsub_rn(mean, __dadd_rn((double)coords[3 * v + ch], 0.5));
-            f[ch] = __ddiv_rn(mean, s);
-            f[6 + ch] = fmin(fmax(res, -0.5), 0.5);
+            const double a = __ddiv_rn(mean, s), r = fmin(fmax(res, -0.5), 0.5);
+            f[ch] = a;
+            f[6 + ch] = r;
+            if (feats32) {   // the UNet's float32 input, same rounding as a separate cast
+                feats32[9 * v + ch] = (float)a;
+                feats32[9 * v + 6 + ch] = (float)r;
+            }
         } else {
             f[ch] = mean;
+            if (feats32) feats32[9 * v + ch] = (float)mean;
         }
     }
 }
@@ -349,7 +356,7 @@ static void voxelize_typed(sfb_ctx *ctx, const double *pos, const double *col, i
     SFB_CHECK_LAUNCH();
     const int64_t vwarps = (ctx->grid_bound(n, ctx->hint_m[0]) + 4) / 5;
     k_voxel_feats<<<dgrid(32 * vwarps, 256), 256, 0, st>>>(pos, col, out.order, out.offsets,
-                                                          out.coords, C, P, out.feats);
+                                                          out.coords, C, P, out.feats, out.feats32);
     SFB_CHECK_LAUNCH();
 }
 

@@ -74,3 +74,37 @@ if rep.exists():
     d["k_composite"] = {"dram_bytes_per_launch": rd + wr, "read": rd, "write": wr,
                         "source": f"profiles/{tag}_composite_ncu.txt"}
     tj.write_text(json.dumps(d, indent=1) + "\n")
+
+# ---- tcgen05 conv launches (tools/conv_profile.sh): the last frame's convs
+cp = go / f"conv_ncu_{tag}.csv"
+if cp.exists():
+    rows = [r for r in csv.reader(open(cp)) if len(r) > 10]
+    h = rows[0]
+    ix = {k: h.index(k) for k in ("ID", "Kernel Name", "Metric Name", "Metric Value", "Grid Size")}
+    per = {}
+    for r in rows[1:]:
+        d = per.setdefault(int(r[ix["ID"]]), {"k": r[ix["Kernel Name"]], "grid": r[ix["Grid Size"]]})
+        d[r[ix["Metric Name"]]] = r[ix["Metric Value"]]
+    ids = sorted(per)
+    starts = [i for i in ids if per[i]["k"].startswith("void k_conv_narrow")]
+    # a complete frame: from the second-to-last level-0 conv to the last
+    # (the launch cap may cut the last frame short)
+    last = ([i for i in ids if starts[-2] <= i < starts[-1]] if len(starts) >= 2
+            else [i for i in ids if i >= starts[-1]] if starts else ids)
+    f = lambda d, m: float(d.get(m, "0").replace(",", "") or 0)
+    lines = [f"# ncu of the convolution launches of one steady-state config-2 frame (view 0), tag {tag}",
+             "# (tools/conv_profile.sh: --clock-control none --cache-control none, launches serialised, lanes 1)",
+             "# tensor% = sm__pipe_tensor_cycles_active (avg over SMs / busiest SM), tmem = smsp__inst_executed_pipe_tmem.sum,",
+             "# warps% = sm__warps_active; smem-occ = CTAs per SM allowed by shared memory",
+             f"{'kernel':34s} {'grid':>6s} {'us':>6s} {'tensor% avg':>11s} {'max':>6s} {'tmem inst':>9s} {'DRAM MB':>8s} {'warps%':>6s} {'smem-occ':>8s} {'cluster':>7s}"]
+    for i in last:
+        d = per[i]
+        name = d["k"].split("(")[0].replace("void ", "").replace("(anonymous namespace)::", "")[:34]
+        lines.append(f"{name:34s} {d['grid'].strip('()').split(',')[0]:>6s} {f(d, 'gpu__time_duration.sum') / 1000:6.1f} "
+                     f"{f(d, 'sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active'):11.2f} "
+                     f"{f(d, 'sm__pipe_tensor_cycles_active.max.pct_of_peak_sustained_active'):6.1f} "
+                     f"{f(d, 'smsp__inst_executed_pipe_tmem.sum'):9.0f} "
+                     f"{(f(d, 'dram__bytes_read.sum') + f(d, 'dram__bytes_write.sum')) / 1e6:8.2f} "
+                     f"{f(d, 'sm__warps_active.avg.pct_of_peak_sustained_active'):6.1f} "
+                     f"{f(d, 'launch__occupancy_limit_shared_mem'):8.0f} {f(d, 'launch__cluster_dim_x'):7.0f}")
+    (out / f"{tag}_conv_ncu.txt").write_text("\n".join(lines) + "\n")
