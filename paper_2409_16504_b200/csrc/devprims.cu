@@ -362,6 +362,25 @@ k_rs_downsweep(const K *__restrict__ kin, const uint32_t *__restrict__ vin, K *_
     const int64_t n = d_n ? *d_n : n_fixed;
     const int nb = rs_blocks(n);
     if ((int)blockIdx.x >= nb) return;
+    const int64_t ch = chunk_of(n, nb);
+    const int64_t b0 = blockIdx.x * ch, b1 = min(n, b0 + ch);
+    constexpr int SUB = kRsThreads * kRsIpt;
+    // sub-tile loads (warp w owns items [w * 32 * kRsIpt, ...)): the first
+    // sub-tile's are issued before the offset prologue, each next one's
+    // before the current one is ranked, so their latency hides
+    auto load = [&](int64_t t0, K *key, uint32_t *val) {
+        const int64_t wbase = t0 + (int64_t)warp * 32 * kRsIpt;
+#pragma unroll
+        for (int q = 0; q < kRsIpt; ++q) {
+            const int64_t i = wbase + q * 32 + lane;
+            const bool ok = i < b1;
+            key[q] = ok ? kin[i] : K(0);
+            val[q] = (HAS_VALS && ok) ? vin[i] : 0u;
+        }
+    };
+    K key[kRsIpt];
+    uint32_t val[kRsIpt];
+    load(b0, key, val);
     {
         int32_t tot = 0, pre = 0;
 #pragma unroll 8
@@ -376,23 +395,17 @@ k_rs_downsweep(const K *__restrict__ kin, const uint32_t *__restrict__ vin, K *_
     }
     for (int w = 0; w < kRsWarps; ++w) wcnt[w][threadIdx.x] = 0;
     __syncthreads();
-    const int64_t ch = chunk_of(n, nb);
-    const int64_t b0 = blockIdx.x * ch, b1 = min(n, b0 + ch);
     const uint32_t lt = (1u << lane) - 1u;
-    constexpr int SUB = kRsThreads * kRsIpt;
     for (int64_t t0 = b0; t0 < b1; t0 += SUB) {
-        K key[kRsIpt];
-        uint32_t val[kRsIpt], dg[kRsIpt];
+        uint32_t dg[kRsIpt];
         int32_t lr[kRsIpt];
         const int64_t wbase = t0 + (int64_t)warp * 32 * kRsIpt;
 #pragma unroll
-        for (int q = 0; q < kRsIpt; ++q) {
-            const int64_t i = wbase + q * 32 + lane;
-            const bool ok = i < b1;
-            key[q] = ok ? kin[i] : K(0);
-            val[q] = (HAS_VALS && ok) ? vin[i] : 0u;
-            dg[q] = ok ? ((uint32_t)(key[q] >> shift) & 255u) : 256u;
-        }
+        for (int q = 0; q < kRsIpt; ++q)
+            dg[q] = wbase + q * 32 + lane < b1 ? ((uint32_t)(key[q] >> shift) & 255u) : 256u;
+        K nkey[kRsIpt];
+        uint32_t nval[kRsIpt];
+        if (t0 + SUB < b1) load(t0 + SUB, nkey, nval);
 #pragma unroll
         for (int q = 0; q < kRsIpt; ++q) {   // rounds in item order
             const uint32_t d = dg[q];
@@ -426,6 +439,11 @@ k_rs_downsweep(const K *__restrict__ kin, const uint32_t *__restrict__ vin, K *_
         run[threadIdx.x] += tot;
 #pragma unroll
         for (int w = 0; w < kRsWarps; ++w) wcnt[w][threadIdx.x] = 0;
+#pragma unroll
+        for (int q = 0; q < kRsIpt; ++q) {
+            key[q] = nkey[q];
+            val[q] = nval[q];
+        }
         __syncthreads();
     }
 }
