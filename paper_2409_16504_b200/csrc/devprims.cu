@@ -313,7 +313,7 @@ Cam to_cam(const sfb_camera &c) {
 }
 
 // ------------------------------------------------------------------ radix sort
-constexpr int kRsBlocks = 148;
+constexpr int kRsBlocks = 148;   // a multiple of 4 (the offset prologue reads kRsBlocks / 4 per round)
 constexpr int kRsThreads = 256;
 constexpr int kRsWarps = kRsThreads / 32;
 
@@ -383,11 +383,16 @@ k_rs_downsweep(const K *__restrict__ kin, const uint32_t *__restrict__ vin, K *_
     load(b0, key, val);
     {
         int32_t tot = 0, pre = 0;
-#pragma unroll 8
-        for (int b = 0; b < nb; ++b) {
-            const int32_t c = hist[b * 256 + threadIdx.x];
-            tot += c;
-            pre += b < (int)blockIdx.x ? c : 0;
+        constexpr int R = kRsBlocks / 4;   // 37 loads in flight: <= 4 rounds
+        for (int b = 0; b < nb; b += R) {
+            int32_t c[R];
+#pragma unroll
+            for (int u = 0; u < R; ++u) c[u] = b + u < nb ? hist[(b + u) * 256 + threadIdx.x] : 0;
+#pragma unroll
+            for (int u = 0; u < R; ++u) {
+                tot += c[u];
+                pre += b + u < (int)blockIdx.x ? c[u] : 0;
+            }
         }
         __shared__ int32_t s_warp[32];
         const int32_t base = block_excl_scan(tot, s_warp, nullptr);
