@@ -270,6 +270,9 @@ struct DevCounts {
     int64_t ef, es, g;  // fine / super / global pyramid entries
     int64_t ef_req, es_req, overflow;   // entries the runs asked for; 1 = over capacity
     int64_t scratch[4];
+    // kept depths' range as atomicMax words (zero = identity): zr[0] = ~min
+    // bits, zr[1] = max bits (depth > 0, so the bits order like the values)
+    unsigned long long zr[2];
 };
 
 struct Cam {
@@ -447,7 +450,7 @@ void render_run(sfb_ctx *ctx, const RenderInputs &in, const FrameParams *FP, int
 void project_run(sfb_ctx *ctx, const double *centers, const double *quats, const double *scales,
                  const int64_t *d_n, int64_t n_bound, const FrameParams *FP, double z_near,
                  double dilation, double *sx, double *sy, double *depth, double *ca, double *cb,
-                 double *cc, double *radius, uint8_t *keep);
+                 double *cc, double *radius, uint8_t *keep, unsigned long long *zr = nullptr);
 void render_backward_run(sfb_ctx *ctx, const RenderInputs &in, const FrameParams *FP, int64_t width,
                          int64_t height, const sfb_render_options &opts, int mode, DevCounts *C,
                          const double *upstream, double *d_centers, double *d_scales,

@@ -404,19 +404,32 @@ __global__ void k_pool_means_fast(const float *__restrict__ feats, int ld_in, in
         const int64_t v = idx / c;
         const int ch = (int)(idx % c);
         const int cnt = min(nkids[v], 8);
+        // all 8 slots loaded at once (absent ones padded past any row), sorted
+        // by a fixed compare-exchange network (registers, no local memory),
+        // then every child's row gathered at once: one round trip per step
+        // instead of one per child
         int32_t kk[8];
-        for (int q = 0; q < cnt; ++q) kk[q] = kids[8 * v + q];
-        for (int q = 1; q < cnt; ++q) {   // ascending child rows
-            const int32_t x = kk[q];
-            int r = q - 1;
-            while (r >= 0 && kk[r] > x) {
-                kk[r + 1] = kk[r];
-                --r;
-            }
-            kk[r + 1] = x;
-        }
+#pragma unroll
+        for (int q = 0; q < 8; ++q) kk[q] = q < cnt ? kids[8 * v + q] : INT32_MAX;
+        auto cx = [&](int a, int b) {
+            const int32_t lo = min(kk[a], kk[b]), hi = max(kk[a], kk[b]);
+            kk[a] = lo;
+            kk[b] = hi;
+        };
+        // Batcher's odd-even merge sort for 8 (19 exchanges): ascending child rows
+        cx(0, 1); cx(2, 3); cx(4, 5); cx(6, 7);
+        cx(0, 2); cx(1, 3); cx(4, 6); cx(5, 7);
+        cx(1, 2); cx(5, 6);
+        cx(0, 4); cx(1, 5); cx(2, 6); cx(3, 7);
+        cx(2, 4); cx(3, 5);
+        cx(1, 2); cx(3, 4); cx(5, 6);
+        float f[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) f[q] = q < cnt ? feats[(int64_t)kk[q] * ld_in + ch] : 0.f;
         float acc = 0.f;
-        for (int q = 0; q < cnt; ++q) acc = __fadd_rn(acc, feats[(int64_t)kk[q] * ld_in + ch]);
+#pragma unroll
+        for (int q = 0; q < 8; ++q)
+            if (q < cnt) acc = __fadd_rn(acc, f[q]);
         out[v * ld_out + ch] = __fdiv_rn(acc, (float)cnt);
     }
 }

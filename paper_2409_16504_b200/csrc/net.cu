@@ -232,7 +232,12 @@ k_conv_narrow(const float *__restrict__ in, int ld_in, const int32_t *__restrict
     constexpr int CO = COUT / PARTS;
     static_assert(CO % 4 == 0, "outputs per thread must be a multiple of 4");
     extern __shared__ __align__(16) float sW[];   // [TAPS][CIN][COUT]
-    for (int i = threadIdx.x; i < TAPS * CIN * COUT; i += blockDim.x) sW[i] = w[i];
+    static_assert((TAPS * CIN * COUT) % 4 == 0, "16-byte weight staging");
+    // weights staged with 16-byte loads, 8 in flight per thread (a rolled
+    // scalar loop waits ~30 round trips before the first FMA)
+#pragma unroll 8
+    for (int i = threadIdx.x; i < TAPS * CIN * COUT / 4; i += blockDim.x)
+        reinterpret_cast<float4 *>(sW)[i] = __ldg(reinterpret_cast<const float4 *>(w) + i);
     __syncthreads();
     const int64_t m = d_m ? *d_m : m_fixed;
     SFB_FOR(item, m * PARTS) {
@@ -448,9 +453,15 @@ __global__ void __launch_bounds__(128)
 k_head_row(const float *__restrict__ f, int ld, const int64_t *__restrict__ d_m,
            const float *__restrict__ w1, const float *__restrict__ b1, const float *__restrict__ w2,
            const float *__restrict__ b2, float *__restrict__ raw) {
-    __shared__ float W1[CIN * HID], B1[HID], W2[HID * 14], B2[14];
-    for (int i = threadIdx.x; i < CIN * HID; i += blockDim.x) W1[i] = w1[i];
-    for (int i = threadIdx.x; i < HID * 14; i += blockDim.x) W2[i] = w2[i];
+    __shared__ __align__(16) float W1[CIN * HID], B1[HID], W2[HID * 14], B2[14];
+    // 16-byte weight staging, all loads in flight (see k_conv_narrow)
+    static_assert((CIN * HID) % 4 == 0 && (HID * 14) % 4 == 0, "16-byte weight staging");
+#pragma unroll
+    for (int i = threadIdx.x; i < CIN * HID / 4; i += 128)
+        reinterpret_cast<float4 *>(W1)[i] = __ldg(reinterpret_cast<const float4 *>(w1) + i);
+#pragma unroll
+    for (int i = threadIdx.x; i < HID * 14 / 4; i += 128)
+        reinterpret_cast<float4 *>(W2)[i] = __ldg(reinterpret_cast<const float4 *>(w2) + i);
     for (int i = threadIdx.x; i < HID; i += blockDim.x) B1[i] = b1[i];
     if (threadIdx.x < 14) B2[threadIdx.x] = b2[threadIdx.x];
     __syncthreads();

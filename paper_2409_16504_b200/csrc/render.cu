@@ -118,22 +118,47 @@ __global__ void k_project(const double *__restrict__ centers, const double *__re
                           double dil, double *__restrict__ sx, double *__restrict__ sy,
                           double *__restrict__ depth, double *__restrict__ ca,
                           double *__restrict__ cb, double *__restrict__ cc,
-                          double *__restrict__ rad3, uint8_t *__restrict__ keep) {
+                          double *__restrict__ rad3, uint8_t *__restrict__ keep,
+                          unsigned long long *__restrict__ zr) {
     const int64_t n = d_n ? *d_n : n_fixed;
     const Cam C = FP->cam;
-    SFB_FOR(i, n)
-    project_one(centers + 3 * i, quats + 4 * i, scales + 3 * i, C, z_near, dil, sx + i, sy + i,
-                depth + i, ca + i, cb + i, cc + i, rad3 + i, keep + i);
+    // the kept depths' range for the depth-order keys, reduced here (zr:
+    // DevCounts words, zero-initialised per frame) instead of a second pass
+    unsigned long long lo = ~0ull, hi = 0ull;
+    for (int64_t i0 = blockIdx.x * (int64_t)blockDim.x; i0 < n; i0 += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t i = i0 + threadIdx.x;
+        if (i < n) {
+            project_one(centers + 3 * i, quats + 4 * i, scales + 3 * i, C, z_near, dil, sx + i, sy + i,
+                        depth + i, ca + i, cb + i, cc + i, rad3 + i, keep + i);
+            if (zr && keep[i]) {
+                const unsigned long long b = (unsigned long long)__double_as_longlong(depth[i]);
+                lo = b < lo ? b : lo;
+                hi = b > hi ? b : hi;
+            }
+        }
+    }
+    if (zr) {
+        for (int o = 16; o; o >>= 1) {
+            const unsigned long long l2 = __shfl_xor_sync(0xffffffffu, lo, o);
+            const unsigned long long h2 = __shfl_xor_sync(0xffffffffu, hi, o);
+            lo = l2 < lo ? l2 : lo;
+            hi = h2 > hi ? h2 : hi;
+        }
+        if ((threadIdx.x & 31) == 0 && hi) {
+            atomicMax(&zr[0], ~lo);
+            atomicMax(&zr[1], hi);
+        }
+    }
 }
 
 void project_run(sfb_ctx *ctx, const double *centers, const double *quats, const double *scales,
                  const int64_t *d_n, int64_t n_bound, const FrameParams *FP, double z_near,
                  double dilation, double *sx, double *sy, double *depth, double *ca, double *cb,
-                 double *cc, double *radius, uint8_t *keep) {
+                 double *cc, double *radius, uint8_t *keep, unsigned long long *zr) {
     if (n_bound == 0) return;
     k_project<<<dgrid(n_bound, 128), 128, 0, ctx->stream>>>(centers, quats, scales, d_n, n_bound, FP,
                                                             z_near, dilation, sx, sy, depth, ca, cb,
-                                                            cc, radius, keep);
+                                                            cc, radius, keep, zr);
     SFB_CHECK_LAUNCH();
 }
 
@@ -143,7 +168,8 @@ struct Proj {
     uint8_t *keep;
 };
 
-static Proj project_inputs(sfb_ctx *ctx, const RenderInputs &in, const FrameParams *FP) {
+static Proj project_inputs(sfb_ctx *ctx, const RenderInputs &in, const FrameParams *FP,
+                           unsigned long long *zr = nullptr) {
     Proj P;
     const int64_t n = in.n_geom;   // bound
     double *blk = ctx->arena.alloc<double>(7 * (size_t)(n > 0 ? n : 1));
@@ -156,7 +182,7 @@ static Proj project_inputs(sfb_ctx *ctx, const RenderInputs &in, const FramePara
     P.r3 = blk + 6 * n;
     P.keep = ctx->arena.alloc<uint8_t>(n > 0 ? n : 1);
     project_run(ctx, in.centers, in.quats, in.scales, in.d_n_geom, n, FP, 0.01, 0.3, P.sx, P.sy,
-                P.depth, P.a, P.b, P.c, P.r3, P.keep);
+                P.depth, P.a, P.b, P.c, P.r3, P.keep, zr);
     return P;
 }
 
@@ -171,38 +197,11 @@ __device__ __forceinline__ unsigned long long dbits(double d) {
     return (unsigned long long)__double_as_longlong(d);
 }
 
-__global__ void k_depth_range(const Proj P, const int64_t *__restrict__ d_ng, int64_t ng_fixed,
-                              unsigned long long *__restrict__ mm) {
-    const int64_t ng = d_ng ? *d_ng : ng_fixed;
-    unsigned long long lo = ~0ull, hi = 0ull;
-    SFB_FOR(g, ng)
-    if (P.keep[g]) {
-        const unsigned long long b = dbits(P.depth[g]);   // depth > z_near > 0
-        lo = b < lo ? b : lo;
-        hi = b > hi ? b : hi;
-    }
-    for (int o = 16; o; o >>= 1) {
-        const unsigned long long l2 = __shfl_xor_sync(0xffffffffu, lo, o);
-        const unsigned long long h2 = __shfl_xor_sync(0xffffffffu, hi, o);
-        lo = l2 < lo ? l2 : lo;
-        hi = h2 > hi ? h2 : hi;
-    }
-    if ((threadIdx.x & 31) == 0) {
-        atomicMin(&mm[0], lo);
-        atomicMax(&mm[1], hi);
-    }
-}
-
-__global__ void k_init_range(unsigned long long *mm) {
-    mm[0] = ~0ull;
-    mm[1] = 0ull;
-}
-
 __global__ void k_depth_keys(int64_t n, const int32_t *__restrict__ p2g, const Proj P,
-                             const unsigned long long *__restrict__ mm, uint32_t *__restrict__ keys,
+                             const unsigned long long *__restrict__ zr, uint32_t *__restrict__ keys,
                              uint32_t *__restrict__ vals, int64_t *__restrict__ d_kept) {
-    const double zmin = __longlong_as_double((long long)mm[0]);
-    const double zmax = __longlong_as_double((long long)mm[1]);
+    const double zmin = __longlong_as_double((long long)~zr[0]);
+    const double zmax = __longlong_as_double((long long)zr[1]);
     const double scale = zmax > zmin ? 4294967294.0 / (zmax - zmin) : 0.0;
     SFB_FOR(i, ((n + 31) & ~int64_t(31))) {
         bool k = false;
@@ -267,15 +266,18 @@ k_depth_fixup(const uint32_t *__restrict__ keys, uint32_t *__restrict__ src,
     const int64_t K = *d_kept, H = *n_heads;
     for (int64_t gi = blockIdx.x; gi < H; gi += gridDim.x) {
         const int64_t h = heads[gi];
-        if (threadIdx.x == 0) {
-            int64_t lo = h, hi = K;   // first index with key > keys[h]
-            const uint32_t kh = keys[h];
-            while (lo < hi) {
-                const int64_t mid = (lo + hi) >> 1;
-                if (keys[mid] <= kh) lo = mid + 1;
-                else hi = mid;
-            }
-            s_end = lo;
+        // group end = first index after h with another key: all threads test
+        // 256 positions per round (groups are short: one round, instead of a
+        // ~15-step serial binary search by one thread)
+        const uint32_t kh = keys[h];
+        if (threadIdx.x == 0) s_end = K;
+        __syncthreads();
+        for (int64_t base = h + 1; base < K; base += blockDim.x) {
+            const int64_t i = base + threadIdx.x;
+            if (i < K && keys[i] != kh) atomicMin((unsigned long long *)&s_end, (unsigned long long)i);
+            __syncthreads();
+            if (s_end < K || base + (int64_t)blockDim.x >= K) break;
+            __syncthreads();
         }
         __syncthreads();
         const int64_t e = s_end, cnt = e - h;
@@ -319,11 +321,7 @@ static uint32_t *depth_order(sfb_ctx *ctx, const RenderInputs &in, const Proj &P
     const int64_t n = in.n_points;
     uint32_t *k0 = ctx->arena.alloc<uint32_t>(n), *k1 = ctx->arena.alloc<uint32_t>(n);
     uint32_t *v0 = ctx->arena.alloc<uint32_t>(n), *v1 = ctx->arena.alloc<uint32_t>(n);
-    auto *mm = ctx->arena.alloc<unsigned long long>(2);
-    k_init_range<<<1, 1, 0, ctx->stream>>>(mm);
-    k_depth_range<<<dgrid(ctx->grid_bound(in.n_geom, in.d_n_geom ? ctx->hint_m[0] : 0), 256), 256, 0,
-                    ctx->stream>>>(P, in.d_n_geom, in.n_geom, mm);
-    k_depth_keys<<<dgrid(n, 256), 256, 0, ctx->stream>>>(n, in.point_to_geom, P, mm, k0, v0, &C->kept);
+    k_depth_keys<<<dgrid(n, 256), 256, 0, ctx->stream>>>(n, in.point_to_geom, P, C->zr, k0, v0, &C->kept);
     SFB_CHECK_LAUNCH();
     // stable by point index within equal keys (devprims.cu radix sort)
     const bool second = dsort_pairs<uint32_t>(ctx, k0, v0, k1, v1, nullptr, n, 32);
@@ -500,12 +498,12 @@ __global__ void k_run_build(const uint32_t *__restrict__ src, DevCounts *__restr
 // M0 voxels instead of the N points replaces an 800k-key sort by a ~30k one,
 // and runs come out per voxel (one run per voxel outside tie groups).
 __global__ void k_vdepth_keys(const int64_t *__restrict__ d_ng, const Proj P,
-                              const unsigned long long *__restrict__ mm, uint32_t *__restrict__ keys,
+                              const unsigned long long *__restrict__ zr, uint32_t *__restrict__ keys,
                               uint32_t *__restrict__ vals, int32_t *__restrict__ vpos,
                               int64_t *__restrict__ d_kept_geom) {
     const int64_t ng = *d_ng;
-    const double zmin = __longlong_as_double((long long)mm[0]);
-    const double zmax = __longlong_as_double((long long)mm[1]);
+    const double zmin = __longlong_as_double((long long)~zr[0]);
+    const double zmax = __longlong_as_double((long long)zr[1]);
     // 24-bit monotone quantisation (3 radix passes over ~30k voxels; exact
     // order restored inside equal-key groups by the fix-up), culled last
     const double scale = zmax > zmin ? 16777214.0 / (zmax - zmin) : 0.0;
@@ -1408,11 +1406,9 @@ static void voxel_order(sfb_ctx *ctx, const RenderInputs &in, const Proj &P, Dev
     uint32_t *k0 = ctx->arena.alloc<uint32_t>(nbg), *k1 = ctx->arena.alloc<uint32_t>(nbg);
     uint32_t *v0 = ctx->arena.alloc<uint32_t>(nbg), *v1 = ctx->arena.alloc<uint32_t>(nbg);
     vpos = ctx->arena.alloc<int32_t>(nbg);
-    auto *mm = ctx->arena.alloc<unsigned long long>(2);
     d_kg = &C->scratch[3];
-    k_init_range<<<1, 1, 0, st>>>(mm);
-    k_depth_range<<<gv, 256, 0, st>>>(P, in.d_n_geom, in.n_geom, mm);
-    k_vdepth_keys<<<gv, 256, 0, st>>>(in.d_n_geom, P, mm, k0, v0, vpos, d_kg);
+    // the depth range came with the projection (DevCounts::zr)
+    k_vdepth_keys<<<gv, 256, 0, st>>>(in.d_n_geom, P, C->zr, k0, v0, vpos, d_kg);
     SFB_CHECK_LAUNCH();
     // stable by voxel id within equal quantised keys; culled voxels (key ~0) last
     const bool second = dsort_pairs<uint32_t>(ctx, k0, v0, k1, v1, in.d_n_geom, nbg, 24);
@@ -1450,7 +1446,7 @@ void render_run(sfb_ctx *ctx, const RenderInputs &in, const FrameParams *FP, int
     const int64_t nsx = (ntx + kSuper - 1) / kSuper, nsy = (nty + kSuper - 1) / kSuper;
     const int64_t nt = ntx * nty, ns = nsx * nsy;
     const int64_t n = in.n_points;
-    Proj P = project_inputs(ctx, in, FP);
+    Proj P = project_inputs(ctx, in, FP, C->zr);
     ctx->mark(ST_PROJECT);
     const int64_t nb = n > 0 ? n : 1;
     const bool want_rgb = plane_mask & SFB_PLANE_RGB, want_n = plane_mask & SFB_PLANE_NORMAL;
@@ -1687,7 +1683,7 @@ static Csr build_csr(sfb_ctx *ctx, const RenderInputs &in, const FrameParams *FP
     R.ntx = (width + tile - 1) / tile;
     R.nty = (height + tile - 1) / tile;
     const int64_t nt = R.ntx * R.nty;
-    R.P = project_inputs(ctx, in, FP);
+    R.P = project_inputs(ctx, in, FP, C->zr);
     R.toff = ctx->arena.alloc<int32_t>(nt + 1);
     SFB_CUDA(cudaMemsetAsync(R.toff, 0, sizeof(int32_t) * (nt + 1), st));
     if (in.n_points > 0) {
