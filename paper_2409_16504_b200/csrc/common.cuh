@@ -240,10 +240,15 @@ __host__ __device__ inline bool key_in_range(int64_t x, int64_t y, int64_t z) {
     const int64_t L = int64_t(1) << 20;
     return x > -L && x < L && y > -L && y < L && z > -L && z < L;
 }
-// Python floor division by a positive power of two
+// Python floor division by a positive power of two (every caller divides by
+// a lattice stride): an arithmetic shift, not a 64-bit integer division
 __host__ __device__ inline int64_t floor_div(int64_t a, int64_t d) {
-    int64_t q = a / d;
-    return (a % d != 0 && a < 0) ? q - 1 : q;
+#ifdef __CUDA_ARCH__
+    const int sh = __ffsll(d) - 1;
+#else
+    const int sh = __builtin_ctzll((unsigned long long)d);
+#endif
+    return a >> sh;
 }
 
 // grid-stride loop over a count that may live in device memory

@@ -130,7 +130,8 @@ __global__ void k_transposed_lookup(const int32_t *__restrict__ targets,
             p[a] = floor_div(t[a], ps) * ps;
         }
         const int half = ps / 2;
-        tap[r] = (int32_t)(((t[2] - p[2]) / half) * 4 + ((t[1] - p[1]) / half) * 2 + (t[0] - p[0]) / half);
+        tap[r] = (int32_t)(floor_div(t[2] - p[2], half) * 4 + floor_div(t[1] - p[1], half) * 2 +
+                           floor_div(t[0] - p[0], half));
         parent[r] = hash_find(h, mask, p[0], p[1], p[2]);
     }
 }
@@ -152,7 +153,7 @@ __device__ __forceinline__ void parent_layout(const FrameParams *P, int64_t S, i
     for (int a = 0; a < 3; ++a) {
         const int64_t lo = P->lo[a], hi = lo + ((int64_t)1 << P->bits[a]) - 1;
         plo[a] = floor_div(lo, S) * S;
-        const int64_t span = (floor_div(hi, S) * S - plo[a]) / S;
+        const int64_t span = floor_div(floor_div(hi, S) * S - plo[a], S);
         int b = 0;
         while (b < 63 && (span >> b) != 0) ++b;
         pbits[a] = b;
@@ -170,7 +171,7 @@ __global__ void k_parent_keys(const int32_t *__restrict__ coords, const int64_t 
     SFB_FOR(j, m) {
         uint64_t q[3];
 #pragma unroll
-        for (int a = 0; a < 3; ++a) q[a] = (uint64_t)((floor_div(coords[3 * j + a], S) * S - plo[a]) / S);
+        for (int a = 0; a < 3; ++a) q[a] = (uint64_t)floor_div(floor_div(coords[3 * j + a], S) * S - plo[a], S);
         keys[j] = (K)((q[2] << (pb[0] + pb[1])) | (q[1] << pb[0]) | q[0]);
         vals[j] = (uint32_t)j;
     }
@@ -483,9 +484,17 @@ __global__ void k_tap_scatter(const int32_t *__restrict__ tap, const int32_t *__
         off[threadIdx.x] = o[threadIdx.x];
         if (threadIdx.x == 8) *d_rows = o[8];
     }
+    const int lane = threadIdx.x & 31;
     SFB_FOR(j, m) {
+        // one atomic per (warp, tap): the 8 bucket cursors are hot
         const int32_t t = tap[j];
-        const int32_t pos = o[t] + atomicAdd(&cur[t], 1);
+        const unsigned act = __activemask();
+        const unsigned peers = __match_any_sync(act, t);
+        const int leader = __ffs(peers) - 1;
+        int32_t b = 0;
+        if (lane == leader) b = atomicAdd(&cur[t], __popc(peers));
+        b = __shfl_sync(peers, b, leader);
+        const int32_t pos = o[t] + b + __popc(peers & ((1u << lane) - 1u));
         perm[pos] = (int32_t)j;
         src[pos] = c2p[j];
     }

@@ -399,7 +399,7 @@ __global__ void k_child_tap(const int32_t *__restrict__ coords, const int64_t *_
         int64_t d[3];
         for (int a = 0; a < 3; ++a) {
             int64_t c = coords[3 * r + a];
-            d[a] = (c - floor_div(c, ps) * ps) / cs;
+            d[a] = floor_div(c - floor_div(c, ps) * ps, cs);
         }
         tap[r] = (int32_t)(d[2] * 4 + d[1] * 2 + d[0]);
     }
