@@ -108,3 +108,36 @@ if cp.exists():
                      f"{f(d, 'sm__warps_active.avg.pct_of_peak_sustained_active'):6.1f} "
                      f"{f(d, 'launch__occupancy_limit_shared_mem'):8.0f} {f(d, 'launch__cluster_dim_x'):7.0f}")
     (out / f"{tag}_conv_ncu.txt").write_text("\n".join(lines) + "\n")
+
+# ---- every launch of one frame in issue order (from the SM-cost capture)
+sp = go / f"smlaunch_{tag}.csv"
+if sp.exists():
+    rows = [r for r in csv.reader(open(sp)) if len(r) > 10]
+    h = rows[0]
+    ix = {k: h.index(k) for k in ("ID", "Kernel Name", "Metric Name", "Metric Value", "Grid Size", "Block Size")}
+    per = {}
+    for r in rows[1:]:
+        d = per.setdefault(int(r[ix["ID"]]), {"k": r[ix["Kernel Name"]], "g": r[ix["Grid Size"]],
+                                              "b": r[ix["Block Size"]]})
+        d[r[ix["Metric Name"]]] = r[ix["Metric Value"]]
+    ids = sorted(per)
+    starts = [i for i in ids if "k_bbox_init" in per[i]["k"]]
+    if len(starts) >= 2:
+        a, b = starts[-2], starts[-1]
+        fr = [i for i in ids if a <= i < b]
+        num = lambda d, m: float(d.get(m, "0").replace(",", "") or 0)
+        tot = sum(num(per[i], "gpu__time_duration.sum") / 1000 for i in fr)
+        lines = ["# every kernel launch of one config-2 frame (view 0), in issue order: ncu --metrics gpu__time_duration.sum,",
+                 "# sm__cycles_active.sum,sm__warps_active --clock-control none --cache-control none (launches serialised;",
+                 "# per-launch times are cold-start + serialised, so compare SHARES, not absolutes, with bench.py's timings)",
+                 f"# tag {tag}, command: python bench.py --steps 2 --warmup 1 --lanes 1 --no-e2e --no-cpu --no-profile --view 0",
+                 f"{'#':>3s} {'us':>7s} {'share%':>6s} {'grid':>6s} {'block':>5s} {'warps%':>6s}  kernel"]
+        for n, i in enumerate(fr):
+            d = per[i]
+            t = num(d, "gpu__time_duration.sum") / 1000
+            name = d["k"].split("(")[0].replace("void ", "").replace("(anonymous namespace)::", "")
+            lines.append(f"{n:3d} {t:7.1f} {100 * t / tot:6.1f} {d['g'].strip('()').split(',')[0]:>6s} "
+                         f"{d['b'].strip('()').split(',')[0]:>5s} "
+                         f"{num(d, 'sm__warps_active.avg.pct_of_peak_sustained_active'):6.1f}  {name}")
+        lines.append(f"total {tot:.1f} us serialised over {len(fr)} launches")
+        (out / f"{tag}_launches.txt").write_text("\n".join(lines) + "\n")
