@@ -243,7 +243,7 @@ k_conv_tc(const float *__restrict__ in, int ld_in, int cin, const int32_t *__res
           float *__restrict__ out, int ld_out, float *__restrict__ partial,
           const int32_t *__restrict__ row_map, const int32_t *__restrict__ tap_off,
           int cluster_splits, int src_rows, int vec4, const __grid_constant__ CUtensorMap tmA,
-          int tma, int oob_row) {
+          int tma, int oob_row, int khalf) {
     // cluster mode (cluster_splits > 1): the splits of a tile are the CTAs of
     // one thread-block cluster; partial tiles meet in distributed shared
     // memory and each CTA reduces a slice of the tile's rows in split order —
@@ -326,11 +326,11 @@ k_conv_tc(const float *__restrict__ in, int ld_in, int cin, const int32_t *__res
         const int64_t row0 = (wi / splits) * kM;
         const int split = (int)(wi % splits);
         int t0 = split * tps, t1 = min(taps, t0 + tps);
-        if (tap_off) {   // the bucket of this tile
+        if (tap_off) {   // the bucket of this tile (khalf: its two K halves)
             int tb = 0;
             while (tb < 7 && row0 >= tap_off[tb + 1]) ++tb;
-            t0 = tb;
-            t1 = tb + 1;
+            t0 = khalf ? 2 * tb : tb;
+            t1 = t0 + (khalf ? 2 : 1);
         }
         const int64_t row = row0 + tid;
 #pragma unroll
@@ -339,7 +339,8 @@ k_conv_tc(const float *__restrict__ in, int ld_in, int cin, const int32_t *__res
         // coalesced loads) and OR the per-tap occupancy over the tile
         uint32_t mymask = 0;
         for (int t = t0; t < t1; ++t) {
-            const int32_t src = row < m ? nbr[(tap_off ? 0 : (int64_t)t * nbr_ld) + row] : -1;
+            const int tr = khalf ? t >> 1 : t;   // the real tap of a K-half pseudo-tap
+            const int32_t src = row < m ? nbr[(tap_off ? 0 : (int64_t)tr * nbr_ld) + row] : -1;
             s_src[t - t0][tid] = src;
             mymask |= (src >= 0 ? 1u : 0u) << (t - t0);
         }
@@ -366,12 +367,15 @@ k_conv_tc(const float *__restrict__ in, int ld_in, int cin, const int32_t *__res
 #pragma unroll
             for (int q = 0; q < TB; ++q) {
                 const int32_t src = q < nxt_n ? s_src[nxt_t[q] - t0][tid] : -1;
-                const float *x = src >= 0 ? in + (int64_t)src * ld_in : nullptr;
+                // khalf: pseudo-tap t reads channels [64 (t & 1), +64) of the row
+                const int koff = khalf && q < nxt_n ? 64 * (nxt_t[q] & 1) : 0;
+                const int cin_q = cin - koff;
+                const float *x = src >= 0 ? in + (int64_t)src * ld_in + koff : nullptr;
                 if (vec4) {   // 16-byte rows (cin, ld_in multiples of 4, aligned base)
 #pragma unroll
                     for (int k = 0; k < KP; k += 4) {
-                        const float4 f = (x && k < cin) ? __ldg(reinterpret_cast<const float4 *>(x + k))
-                                                        : make_float4(0.f, 0.f, 0.f, 0.f);
+                        const float4 f = (x && k < cin_q) ? __ldg(reinterpret_cast<const float4 *>(x + k))
+                                                          : make_float4(0.f, 0.f, 0.f, 0.f);
                         v[q][k] = f.x;
                         v[q][k + 1] = f.y;
                         v[q][k + 2] = f.z;
@@ -379,7 +383,7 @@ k_conv_tc(const float *__restrict__ in, int ld_in, int cin, const int32_t *__res
                     }
                 } else {
 #pragma unroll
-                    for (int k = 0; k < KP; ++k) v[q][k] = (x && k < cin) ? __ldg(x + k) : 0.f;
+                    for (int k = 0; k < KP; ++k) v[q][k] = (x && k < cin_q) ? __ldg(x + k) : 0.f;
                 }
             }
         };
@@ -709,7 +713,7 @@ template <int KP, int NP, bool BF>
 void launch_tc(sfb_ctx *ctx, const NetLayer &L, const float *in, int ld_in, const int32_t *nbr,
                int64_t nbr_ld, const int64_t *d_m, int64_t m_bound, int relu, float *out,
                int ld_out, int64_t m_grid, const int32_t *row_map, const int32_t *tap_off,
-               int csplit_req) {
+               int csplit_req, int khalf = 0) {
     using S = TcShape<KP, NP, BF>;
     set_max_dyn_smem(reinterpret_cast<const void *>(k_conv_tc<KP, NP, BF>), S::smem_bytes(32));
     const int64_t tiles_bound = (m_grid + kM - 1) / kM;
@@ -722,12 +726,14 @@ void launch_tc(sfb_ctx *ctx, const NetLayer &L, const float *in, int ld_in, cons
     const int csplit = tap_off ? 1 : (csplit_req > 8 ? 8 : csplit_req);
     // taps one work item can cover: one per bucket tile; taps/csplit in a
     // cluster; with device-chosen splits the split may be 1, so all taps
-    const int src_rows = tap_off ? 1 : (csplit >= 1 ? (L.taps + csplit - 1) / csplit : std::min(L.taps, 32));
+    const int taps_eff = khalf ? 2 * L.taps : L.taps;   // khalf: pseudo-taps of 64 channels
+    const int src_rows = tap_off ? (khalf ? 2 : 1)
+                                 : (csplit >= 1 ? (taps_eff + csplit - 1) / csplit : std::min(taps_eff, 32));
     const int vec4 = (L.cin % 4 == 0 && ld_in % 4 == 0 && (reinterpret_cast<uintptr_t>(in) & 15) == 0) ? 1 : 0;
     // A rows by TMA gather (tcgen05 tf32x3 path, full-width rows, multi-tap items)
     CUtensorMap tm{};
     int tma = 0;
-    if (S::TMA_OK && !tap_off && L.cin == KP && vec4) {
+    if (S::TMA_OK && !tap_off && !khalf && L.cin == KP && vec4) {
         if (ctx->conv_stage == 1 && feature_map(&tm, in, ld_in, m_bound, KP)) tma = 1;
         else if (ctx->conv_stage == 2) tma = 2;
     }
@@ -746,27 +752,27 @@ void launch_tc(sfb_ctx *ctx, const NetLayer &L, const float *in, int ld_in, cons
         at[0].val.clusterDim.z = 1;
         cfg.attrs = at;
         cfg.numAttrs = 1;
-        const float *wts = BF ? reinterpret_cast<const float *>(L.w_bf16) : L.w_tc;
+        const float *wts = BF ? reinterpret_cast<const float *>(L.w_bf16) : khalf ? L.w_tc_k2 : L.w_tc;
         SFB_CUDA(cudaLaunchKernelEx(&cfg, k_conv_tc<KP, NP, BF>, in, ld_in, L.cin, nbr, nbr_ld, d_m,
-                                    m_bound, L.taps, wts, L.b, L.cout, relu, out, ld_out,
+                                    m_bound, taps_eff, wts, L.b, L.cout, relu, out, ld_out,
                                     static_cast<float *>(nullptr), row_map, tap_off, csplit, src_rows, vec4,
-                                    tm, tma, oob_row));
+                                    tm, tma, oob_row, khalf));
         return;
     }
     const int64_t work_bound = (tap_off || csplit == 1)
                                    ? tiles_bound
-                                   : tiles_bound * choose_splits(tiles_bound, L.taps, kSplitTarget);
+                                   : tiles_bound * choose_splits(tiles_bound, taps_eff, kSplitTarget);
     const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(work_bound, kSplitTarget));
     float *partial = ctx->arena.alloc<float>((size_t)std::min<int64_t>(kMaxPartialRows,
                                                                        32 * m_bound) * NP);
-    const float *wts = BF ? reinterpret_cast<const float *>(L.w_bf16) : L.w_tc;
+    const float *wts = BF ? reinterpret_cast<const float *>(L.w_bf16) : khalf ? L.w_tc_k2 : L.w_tc;
     k_conv_tc<KP, NP, BF><<<grid, kThreadsTC, S::smem_bytes(src_rows, tma != 0), ctx->stream>>>(
-        in, ld_in, L.cin, nbr, nbr_ld, d_m, m_bound, L.taps, wts, L.b, L.cout, relu, out, ld_out,
-        partial, row_map, tap_off, csplit == 1 ? 1 : 0, src_rows, vec4, tm, tma, oob_row);
+        in, ld_in, L.cin, nbr, nbr_ld, d_m, m_bound, taps_eff, wts, L.b, L.cout, relu, out, ld_out,
+        partial, row_map, tap_off, csplit == 1 ? 1 : 0, src_rows, vec4, tm, tma, oob_row, khalf);
     SFB_CHECK_LAUNCH();
     if (tap_off || csplit == 1) return;   // no split-K partials
     k_splitk_reduce<<<dgrid(std::min<int64_t>(m_grid, kMaxPartialRows) * L.cout, 256), 256, 0,
-                      ctx->stream>>>(partial, d_m, m_bound, L.taps, NP, L.b, L.cout, relu, out,
+                      ctx->stream>>>(partial, d_m, m_bound, taps_eff, NP, L.b, L.cout, relu, out,
                                      ld_out);
     SFB_CHECK_LAUNCH();
 }
@@ -783,6 +789,24 @@ bool conv_tc_supported(const NetLayer &L) {
     return stage + 2048 <= 200 * 1024;
 }
 
+// W[t][ci][co] -> per pseudo-tap p = 2t + h the [hi | lo] tiles of [NP x 64]
+// covering input channels [64h, 64h + 64) (K-split transposed convs)
+__global__ void k_prep_weights_k2(const float *__restrict__ w, int taps, int cin, int cout, int NP,
+                                  float *__restrict__ wtc) {
+    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    const int64_t per = (int64_t)NP * 64;
+    if (i >= 2 * taps * per) return;
+    const int pt = (int)(i / per), t = pt >> 1, h = pt & 1;
+    const int rem = (int)(i % per);
+    const int n = rem / 64, k = rem % 64, ci = 64 * h + k;
+    const float x = (n < cout && ci < cin) ? w[((size_t)t * cin + ci) * cout + n] : 0.f;
+    const float hi = tf32_round(x), lo = tf32_round(x - hi);
+    float *base = wtc + (size_t)pt * 2 * per;
+    const int off = core_off(n, k, 64);
+    base[off] = hi;
+    base[per + off] = lo;
+}
+
 void prepare_tc_weights(sfb_ctx *ctx, NetLayer &L) {
     L.cin_pad = pad_k(L.cin);
     L.cout_pad = pad_n(L.cout);
@@ -791,6 +815,11 @@ void prepare_tc_weights(sfb_ctx *ctx, NetLayer &L) {
     int64_t total = (int64_t)L.taps * L.cin_pad * L.cout_pad;
     k_prep_weights<<<grid_for(total, 256), 256, 0, ctx->stream>>>(L.w, L.taps, L.cin, L.cout,
                                                                   L.cin_pad, L.cout_pad, L.w_tc);
+    if (L.kind == 1 && L.cin_pad == 128) {
+        SFB_CUDA(cudaMalloc(&L.w_tc_k2, n * sizeof(float)));
+        k_prep_weights_k2<<<grid_for(total, 256), 256, 0, ctx->stream>>>(L.w, L.taps, L.cin, L.cout,
+                                                                         L.cout_pad, L.w_tc_k2);
+    }
     SFB_CUDA(cudaMalloc(&L.w_bf16, (size_t)total * sizeof(uint16_t)));
     k_prep_weights_bf16<<<grid_for(total, 256), 256, 0, ctx->stream>>>(L.w, L.taps, L.cin, L.cout,
                                                                        L.cin_pad, L.cout_pad, L.w_bf16);
@@ -802,6 +831,20 @@ void conv_layer_tc(sfb_ctx *ctx, const NetLayer &L, const float *in, int ld_in, 
                    int ld_out, int64_t m_grid, const int32_t *row_map, const int32_t *tap_off,
                    int csplit) {
     const bool bf = ctx->net_mode == SFB_NET_TC_BF16;
+    // 128-wide transposed convs as two 64-wide K halves (both the bucketed
+    // and the 8-tap map path, so they stay bitwise equal): half the staged
+    // tile (one 128-KB+ CTA per SM otherwise), the halves summed in fp32 registers
+    if (!bf && L.kind == 1 && L.cin_pad == 128 && L.w_tc_k2) {
+        if (L.cout_pad == 16)
+            return launch_tc<64, 16, false>(ctx, L, in, ld_in, nbr, nbr_ld, d_m, m_bound, relu, out, ld_out,
+                                            m_grid, row_map, tap_off, csplit, 1);
+        if (L.cout_pad == 32)
+            return launch_tc<64, 32, false>(ctx, L, in, ld_in, nbr, nbr_ld, d_m, m_bound, relu, out, ld_out,
+                                            m_grid, row_map, tap_off, csplit, 1);
+        if (L.cout_pad == 64)
+            return launch_tc<64, 64, false>(ctx, L, in, ld_in, nbr, nbr_ld, d_m, m_bound, relu, out, ld_out,
+                                            m_grid, row_map, tap_off, csplit, 1);
+    }
 #define SFB_TC_CASE(K, N)                                                                 \
     if (L.cin_pad == K && L.cout_pad == N) {                                              \
         if (bf)                                                                           \

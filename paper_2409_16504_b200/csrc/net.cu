@@ -105,6 +105,7 @@ void net_load(sfb_ctx *ctx, const void *blob, size_t nbytes) {
                 prepare_tc_weights(ctx, L);
                 fresh.allocations.push_back(L.w_tc);
                 fresh.allocations.push_back(L.w_bf16);
+                if (L.w_tc_k2) fresh.allocations.push_back(L.w_tc_k2);
             }
         SFB_CUDA(cudaStreamSynchronize(ctx->stream));
     } catch (...) {
@@ -129,7 +130,7 @@ void layer_set(sfb_ctx *ctx, int kind, int kernel, int cin, int cout, const floa
     if (kind == 0) SFB_REQUIRE(kernel >= 1 && (kernel & 1), "conv kernels must be odd");
     if (kind == 1) SFB_REQUIRE(kernel == 2, "transposed_conv kernel is fixed at 2");
     NetLayer &L = ctx->adhoc;
-    for (void *p : {(void *)L.w, (void *)L.b, (void *)L.w_tc, (void *)L.w_bf16})
+    for (void *p : {(void *)L.w, (void *)L.b, (void *)L.w_tc, (void *)L.w_bf16, (void *)L.w_tc_k2})
         if (p) cudaFree(p);
     L = NetLayer{};
     L.kind = kind;
