@@ -102,8 +102,8 @@ struct NetLayer {
     // tcgen05 operands (split tf32 hi/lo, K-major per tap, padded)
     float *w_tc = nullptr;
     uint16_t *w_bf16 = nullptr;   // single bf16 operands, same canonical layout (fast mode)
-    // transposed convs with Cin > 64: the same split operands as two 64-wide
-    // K halves per tap (pseudo-taps 2t, 2t+1), so a CTA stages half the tile
+    // transposed convs with Cin > 32: the same split operands as two K halves
+    // per tap (pseudo-taps 2t, 2t+1), so a CTA stages half the tile
     float *w_tc_k2 = nullptr;
     int cin_pad = 0, cout_pad = 0;
 };

@@ -367,8 +367,8 @@ k_conv_tc(const float *__restrict__ in, int ld_in, int cin, const int32_t *__res
 #pragma unroll
             for (int q = 0; q < TB; ++q) {
                 const int32_t src = q < nxt_n ? s_src[nxt_t[q] - t0][tid] : -1;
-                // khalf: pseudo-tap t reads channels [64 (t & 1), +64) of the row
-                const int koff = khalf && q < nxt_n ? 64 * (nxt_t[q] & 1) : 0;
+                // khalf: pseudo-tap t reads channels [KP (t & 1), +KP) of the row
+                const int koff = khalf && q < nxt_n ? KP * (nxt_t[q] & 1) : 0;
                 const int cin_q = cin - koff;
                 const float *x = src >= 0 ? in + (int64_t)src * ld_in + koff : nullptr;
                 if (vec4) {   // 16-byte rows (cin, ld_in multiples of 4, aligned base)
@@ -789,20 +789,21 @@ bool conv_tc_supported(const NetLayer &L) {
     return stage + 2048 <= 200 * 1024;
 }
 
-// W[t][ci][co] -> per pseudo-tap p = 2t + h the [hi | lo] tiles of [NP x 64]
-// covering input channels [64h, 64h + 64) (K-split transposed convs)
-__global__ void k_prep_weights_k2(const float *__restrict__ w, int taps, int cin, int cout, int NP,
-                                  float *__restrict__ wtc) {
+// W[t][ci][co] -> per pseudo-tap p = 2t + h the [hi | lo] tiles of [NP x H]
+// covering input channels [H h, H h + H) (K-split transposed convs, H = half
+// the padded input width)
+__global__ void k_prep_weights_k2(const float *__restrict__ w, int taps, int cin, int cout, int H,
+                                  int NP, float *__restrict__ wtc) {
     int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    const int64_t per = (int64_t)NP * 64;
+    const int64_t per = (int64_t)NP * H;
     if (i >= 2 * taps * per) return;
     const int pt = (int)(i / per), t = pt >> 1, h = pt & 1;
     const int rem = (int)(i % per);
-    const int n = rem / 64, k = rem % 64, ci = 64 * h + k;
+    const int n = rem / H, k = rem % H, ci = H * h + k;
     const float x = (n < cout && ci < cin) ? w[((size_t)t * cin + ci) * cout + n] : 0.f;
     const float hi = tf32_round(x), lo = tf32_round(x - hi);
     float *base = wtc + (size_t)pt * 2 * per;
-    const int off = core_off(n, k, 64);
+    const int off = core_off(n, k, H);
     base[off] = hi;
     base[per + off] = lo;
 }
@@ -815,10 +816,10 @@ void prepare_tc_weights(sfb_ctx *ctx, NetLayer &L) {
     int64_t total = (int64_t)L.taps * L.cin_pad * L.cout_pad;
     k_prep_weights<<<grid_for(total, 256), 256, 0, ctx->stream>>>(L.w, L.taps, L.cin, L.cout,
                                                                   L.cin_pad, L.cout_pad, L.w_tc);
-    if (L.kind == 1 && L.cin_pad == 128) {
+    if (L.kind == 1 && L.cin_pad >= 64) {
         SFB_CUDA(cudaMalloc(&L.w_tc_k2, n * sizeof(float)));
-        k_prep_weights_k2<<<grid_for(total, 256), 256, 0, ctx->stream>>>(L.w, L.taps, L.cin, L.cout,
-                                                                         L.cout_pad, L.w_tc_k2);
+        k_prep_weights_k2<<<grid_for(total, 256), 256, 0, ctx->stream>>>(
+            L.w, L.taps, L.cin, L.cout, L.cin_pad / 2, L.cout_pad, L.w_tc_k2);
     }
     SFB_CUDA(cudaMalloc(&L.w_bf16, (size_t)total * sizeof(uint16_t)));
     k_prep_weights_bf16<<<grid_for(total, 256), 256, 0, ctx->stream>>>(L.w, L.taps, L.cin, L.cout,
@@ -831,19 +832,17 @@ void conv_layer_tc(sfb_ctx *ctx, const NetLayer &L, const float *in, int ld_in, 
                    int ld_out, int64_t m_grid, const int32_t *row_map, const int32_t *tap_off,
                    int csplit) {
     const bool bf = ctx->net_mode == SFB_NET_TC_BF16;
-    // 128-wide transposed convs as two 64-wide K halves (both the bucketed
+    // 64- and 128-wide transposed convs as two K halves (both the bucketed
     // and the 8-tap map path, so they stay bitwise equal): half the staged
-    // tile (one 128-KB+ CTA per SM otherwise), the halves summed in fp32 registers
-    if (!bf && L.kind == 1 && L.cin_pad == 128 && L.w_tc_k2) {
-        if (L.cout_pad == 16)
-            return launch_tc<64, 16, false>(ctx, L, in, ld_in, nbr, nbr_ld, d_m, m_bound, relu, out, ld_out,
-                                            m_grid, row_map, tap_off, csplit, 1);
-        if (L.cout_pad == 32)
-            return launch_tc<64, 32, false>(ctx, L, in, ld_in, nbr, nbr_ld, d_m, m_bound, relu, out, ld_out,
-                                            m_grid, row_map, tap_off, csplit, 1);
-        if (L.cout_pad == 64)
-            return launch_tc<64, 64, false>(ctx, L, in, ld_in, nbr, nbr_ld, d_m, m_bound, relu, out, ld_out,
-                                            m_grid, row_map, tap_off, csplit, 1);
+    // tile per CTA, the halves summed in fp32 registers
+    if (!bf && L.kind == 1 && L.cin_pad >= 64 && L.w_tc_k2) {
+#define SFB_TC_K2(K, N)                                                                         \
+        if (L.cin_pad == 2 * K && L.cout_pad == N)                                              \
+            return launch_tc<K, N, false>(ctx, L, in, ld_in, nbr, nbr_ld, d_m, m_bound, relu, out, \
+                                          ld_out, m_grid, row_map, tap_off, csplit, 1);
+        SFB_TC_K2(64, 16) SFB_TC_K2(64, 32) SFB_TC_K2(64, 64)
+        SFB_TC_K2(32, 16) SFB_TC_K2(32, 32) SFB_TC_K2(32, 64)
+#undef SFB_TC_K2
     }
 #define SFB_TC_CASE(K, N)                                                                 \
     if (L.cin_pad == K && L.cout_pad == N) {                                              \
