@@ -95,9 +95,18 @@ __global__ void k_kernel_map(const int32_t *__restrict__ coords, const int64_t *
     const int64_t m = d_m ? *d_m : m_fixed;
     const uint32_t mask = *h.mask;
     const int taps = kernel * kernel * kernel, k2 = kernel * kernel, rad = kernel / 2;
+    const bool narrow = m * taps < (int64_t(1) << 31);   // 32-bit index arithmetic (the usual case)
     SFB_FOR(idx, m * taps) {
-        const int64_t r = idx % m;
-        const int t = (int)(idx / m);
+        int64_t r;
+        int t;
+        if (narrow) {   // 32-bit division: a 64-bit one is ~4x the instructions
+            const uint32_t i32 = (uint32_t)idx, m32 = (uint32_t)m;
+            t = (int)(i32 / m32);
+            r = (int64_t)(i32 - (uint32_t)t * m32);
+        } else {
+            r = idx % m;
+            t = (int)(idx / m);
+        }
         const int a = t / k2, b = (t / kernel) % kernel, c = t % kernel;  // (dz, dy, dx)
         const int64_t x = coords[3 * r] + (int64_t)(c - rad) * stride;
         const int64_t y = coords[3 * r + 1] + (int64_t)(b - rad) * stride;
@@ -402,8 +411,9 @@ __global__ void k_pool_means_fast(const float *__restrict__ feats, int ld_in, in
                                   int ld_out) {
     const int64_t mp = *d_mp;
     SFB_FOR(idx, mp * c) {
-        const int64_t v = idx / c;
-        const int ch = (int)(idx % c);
+        // channel counts are small: 32-bit quotient when the index fits
+        const int64_t v = idx < (int64_t(1) << 31) ? (int64_t)((uint32_t)idx / (uint32_t)c) : idx / c;
+        const int ch = (int)(idx - v * c);
         const int cnt = min(nkids[v], 8);
         // all 8 slots loaded at once (absent ones padded past any row), sorted
         // by a fixed compare-exchange network (registers, no local memory),
