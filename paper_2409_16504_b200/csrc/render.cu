@@ -557,13 +557,15 @@ __device__ __forceinline__ int32_t count_below(const int32_t *__restrict__ lst, 
 // CSR slot -> rank: src[rank] = point, colours gathered in rank order.
 // thead[rank] = 1 where a tie group's merged order switches voxel (its first
 // rank included): the predecessor of p in the group is the largest group
-// point index below p, found with the same per-voxel binary searches.
+// point index below p, found with the same per-voxel binary searches. Also
+// records every sorted voxel's group bounds (gspan) for the run builders.
 template <int G>   // lanes per voxel (32: one warp; 8 / 16: several voxels per warp)
 __global__ void k_vranks(const int32_t *__restrict__ order, const int32_t *__restrict__ goff,
                          const int32_t *__restrict__ off, const unsigned long long *__restrict__ full,
                          const uint32_t *__restrict__ vs, const int64_t *__restrict__ d_kg,
                          const double *__restrict__ colors, float4 *__restrict__ scol,
-                         uint32_t *__restrict__ src, int32_t *__restrict__ thead) {
+                         uint32_t *__restrict__ src, int32_t *__restrict__ thead,
+                         int2 *__restrict__ gspan) {
     // one warp per sorted kept voxel, lanes over its points (CSR slots):
     // the voxel's offsets are loaded once, the point reads / rank writes
     // are coalesced, only the colour gather is random
@@ -576,6 +578,7 @@ __global__ void k_vranks(const int32_t *__restrict__ order, const int32_t *__res
         const int32_t s0 = goff[v], s1 = goff[v + 1];
         int64_t gs, ge;
         const bool tie = tie_group(full, i, KG, gs, ge);
+        if (lane == 0) gspan[i] = make_int2((int32_t)gs, (int32_t)ge);
         const int64_t base = tie ? (int64_t)off[gs] : (int64_t)off[i];
         for (int32_t s = s0 + lane; s < s1; s += G) {
             const int32_t p = order[s];
@@ -605,14 +608,15 @@ __global__ void k_vranks(const int32_t *__restrict__ order, const int32_t *__res
 
 // Runs per sorted voxel: 1 outside tie groups; the first voxel of a tie
 // group holds the group's block count (inclusive scan of thead over ranks).
-__global__ void k_vblocks(const unsigned long long *__restrict__ full, const int64_t *__restrict__ d_kg,
+__global__ void k_vblocks(const int2 *__restrict__ gspan, const int64_t *__restrict__ d_kg,
                           const int32_t *__restrict__ off, const int32_t *__restrict__ cnt,
                           const int32_t *__restrict__ hincl, int32_t *__restrict__ nblk) {
     const int64_t KG = *d_kg;
     SFB_FOR(i, KG) {
-        int64_t gs, ge;
+        const int2 sp = gspan[i];
+        const int64_t gs = sp.x, ge = sp.y;
         int32_t b = 1;
-        if (tie_group(full, i, KG, gs, ge)) {
+        if (ge - gs > 1) {
             b = 0;
             if (gs == i) {
                 const int64_t j0 = off[gs], j1 = off[ge - 1] + cnt[ge - 1];
@@ -626,7 +630,7 @@ __global__ void k_vblocks(const unsigned long long *__restrict__ full, const int
 // Run records. x < KG: one run per non-tie sorted voxel; x < K: a tie-group
 // head rank starts run ro[group] + (heads of the group before it), ending at
 // the next head or the group end.
-__global__ void k_vbuild(const uint32_t *__restrict__ vs, const unsigned long long *__restrict__ full,
+__global__ void k_vbuild(const uint32_t *__restrict__ vs, const int2 *__restrict__ gspan,
                          DevCounts *__restrict__ C, const int64_t *__restrict__ d_kg,
                          const int32_t *__restrict__ off, const int32_t *__restrict__ cnt,
                          const int32_t *__restrict__ ro, const int32_t *__restrict__ vpos,
@@ -637,8 +641,7 @@ __global__ void k_vbuild(const uint32_t *__restrict__ vs, const unsigned long lo
     const int64_t KG = *d_kg, K = C->kept;
     if (blockIdx.x == 0 && threadIdx.x == 0) C->runs1 = C->runs + 1;
     SFB_FOR(x, max(KG, K)) {
-        int64_t gs, ge;
-        if (x < KG && !tie_group(full, x, KG, gs, ge)) {
+        if (x < KG && gspan[x].y - gspan[x].x == 1) {
             const int64_t r = ro[x];
             R.start[r] = off[x];
             R.count[r] = off[x] + cnt[x];   // run end; k_emit subtracts the start
@@ -646,7 +649,8 @@ __global__ void k_vbuild(const uint32_t *__restrict__ vs, const unsigned long lo
         }
         if (x < K && thead[x]) {
             const int32_t g = p2g[src[x]];
-            tie_group(full, vpos[g], KG, gs, ge);
+            const int2 sp = gspan[vpos[g]];
+            const int64_t gs = sp.x, ge = sp.y;
             const int64_t j0 = off[gs], j1 = off[ge - 1] + cnt[ge - 1];
             const int64_t r = ro[gs] + (hincl[x] - (j0 > 0 ? hincl[j0 - 1] : 0)) - 1;
             int64_t e = x + 1;
@@ -1399,7 +1403,7 @@ __global__ void k_widen(const uint32_t *__restrict__ a, int64_t n, int64_t *__re
 static void voxel_order(sfb_ctx *ctx, const RenderInputs &in, const Proj &P, DevCounts *C,
                         uint32_t *src, float4 *scol, uint32_t *&vs, unsigned long long *&full,
                         int32_t *&off, int32_t *&cnt, int64_t *&d_kg, int32_t *&vpos,
-                        int32_t *thead) {
+                        int32_t *thead, int2 *&gspan) {
     cudaStream_t st = ctx->stream;
     const int64_t nbg = in.n_geom > 0 ? in.n_geom : 1;
     const unsigned gv = dgrid(ctx->grid_bound(nbg, ctx->hint_m[0]), 256);
@@ -1428,8 +1432,9 @@ static void voxel_order(sfb_ctx *ctx, const RenderInputs &in, const Proj &P, Dev
     k_vcounts<<<gv, 256, 0, st>>>(vs, d_kg, in.geom_offsets, cnt, vpos);
     SFB_CHECK_LAUNCH();
     dscan(ctx, cnt, off, d_kg, nbg, &C->kept, false);
+    gspan = ctx->arena.alloc<int2>(nbg);
     k_vranks<32><<<dgrid(32 * ctx->grid_bound(nbg, ctx->hint_m[0]), 256), 256, 0, st>>>(
-        in.geom_order, in.geom_offsets, off, full, vs, d_kg, in.colors, scol, src, thead);
+        in.geom_order, in.geom_offsets, off, full, vs, d_kg, in.colors, scol, src, thead, gspan);
     SFB_CHECK_LAUNCH();
 }
 
@@ -1459,11 +1464,12 @@ void render_run(sfb_ctx *ctx, const RenderInputs &in, const FrameParams *FP, int
     int32_t *voff = nullptr, *vcnt = nullptr;
     int64_t *d_kg = nullptr;
     int32_t *vpos = nullptr, *thead = nullptr;
+    int2 *gspan = nullptr;
     uint32_t *src;
     if (by_voxel) {
         src = ctx->arena.alloc<uint32_t>(nb);
         thead = ctx->arena.alloc<int32_t>(nb);
-        voxel_order(ctx, in, P, C, src, scol, vs, vfull, voff, vcnt, d_kg, vpos, thead);
+        voxel_order(ctx, in, P, C, src, scol, vs, vfull, voff, vcnt, d_kg, vpos, thead, gspan);
     } else {
         src = n > 0 ? depth_order(ctx, in, P, C) : ctx->arena.alloc<uint32_t>(1);
     }
@@ -1512,10 +1518,10 @@ void render_run(sfb_ctx *ctx, const RenderInputs &in, const FrameParams *FP, int
             int32_t *hincl = head;   // inclusive count of tie-group run heads per rank
             dscan(ctx, thead, hincl, &C->kept, n, nullptr, true);
             int32_t *nblk = ctx->arena.alloc<int32_t>(in.n_geom + 1);   // then run offsets
-            k_vblocks<<<gv, 256, 0, st>>>(vfull, d_kg, voff, vcnt, hincl, nblk);
+            k_vblocks<<<gv, 256, 0, st>>>(gspan, d_kg, voff, vcnt, hincl, nblk);
             SFB_CHECK_LAUNCH();
             dscan(ctx, nblk, nblk, d_kg, in.n_geom, &C->runs, false);
-            k_vbuild<<<dgrid(n, 256), 256, 0, st>>>(vs, vfull, C, d_kg, voff, vcnt, nblk, vpos, thead,
+            k_vbuild<<<dgrid(n, 256), 256, 0, st>>>(vs, gspan, C, d_kg, voff, vcnt, nblk, vpos, thead,
                                                    hincl, src, in.point_to_geom, P, in.opac,
                                                    (double)TS, ntx, nty, opts.alpha_max, R);
             SFB_CHECK_LAUNCH();
