@@ -60,7 +60,7 @@ def parse():
                     help="render only this view (profiling runs; default: views round-robin)")
     ap.add_argument("--cpu-frames", type=int, default=1,
                     help="full config-2 frames of the CPU port timed for cpu_baseline")
-    ap.add_argument("--lanes", type=int, default=8, help="frames in flight per GPU (streams)")
+    ap.add_argument("--lanes", type=int, default=12, help="frames in flight per GPU (streams)")
     ap.add_argument("--net-mode", choices=("tc_tf32x3", "tc_bf16", "simt_f32", "simt_f64"),
                     default="tc_tf32x3",
                     help="P2ENet arithmetic (tc_tf32x3: fp32-accurate parity mode)")
