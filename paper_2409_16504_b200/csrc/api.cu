@@ -40,6 +40,7 @@ int guard(sfb_ctx *ctx, F &&f) {
         if (ctx->done_valid && ctx->done_stream != ctx->stream)
             SFB_CUDA(cudaStreamWaitEvent(ctx->stream, ctx->done_event, 0));
         ctx->arena.reset();
+        ctx->feats_pending = false;
         ctx->n_marks = 0;
         ctx->mark(ST_BEGIN);
         try {
@@ -128,7 +129,7 @@ VoxelSplats neural_voxels(sfb_ctx *ctx, const double *pos, const double *col, in
     o.order = ctx->arena.alloc<int32_t>(n);
     o.offsets = ctx->arena.alloc<int32_t>(n + 1);
     if (ctx->net_mode != SFB_NET_SIMT_F64) o.feats32 = ctx->arena.alloc<float>(9 * n);
-    voxelize_run(ctx, pos, col, n, host, P, o, C);
+    voxelize_run(ctx, pos, col, n, host, P, o, C, true);
     ctx->mark(ST_VOXELIZE);
     void *raw = ctx->arena.alloc<double>(14 * n);   // float32 rows, or float64 (SIMT_F64)
     unet_run(ctx, o.coords, o.feats, n, host, P, C, raw, o.feats32);

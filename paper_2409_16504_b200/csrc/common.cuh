@@ -153,8 +153,9 @@ struct sfb_ctx {
     // side branch of the frame (coordinate structure of the UNet levels runs
     // concurrently with the convolutions): its stream and fork/join events
     cudaStream_t side_stream = nullptr;
-    static constexpr int kSideEvents = 10;
-    cudaEvent_t side_ev[kSideEvents] = {};
+    static constexpr int kSideEvents = 12;   // UNet levels + fork, and the last two:
+    cudaEvent_t side_ev[kSideEvents] = {};     // voxel-feature sums fork / join
+    bool feats_pending = false;   // voxel features still being summed on the side stream
     std::vector<sfb_frame_graph *> graphs;
     int64_t graph_nodes = 0;
     int64_t *debug_counters = nullptr;   // compositor per-tile counters (diagnostics)
@@ -389,8 +390,12 @@ void bbox_run(sfb_ctx *ctx, const double *pos, int64_t n, double *lo_hi_host);
 void bbox_async_run(sfb_ctx *ctx, const double *pos, int64_t n, uint64_t *ordered_host);
 void voxel_layout(const double *lo_hi, double s, FrameParams &P);
 // voxel count lands in C->m[0] (device)
+// feats_on_side: the per-voxel feature sums go to the side stream (they only
+// feed the first convolution, so the level-0 hash and kernel map overlap
+// them); ctx->feats_pending tells unet_run to join before it
 void voxelize_run(sfb_ctx *ctx, const double *pos, const double *col, int64_t n,
-                  const FrameParams &host, const FrameParams *P, VoxelOut &out, DevCounts *C);
+                  const FrameParams &host, const FrameParams *P, VoxelOut &out, DevCounts *C,
+                  bool feats_on_side = false);
 
 // net.cu
 void net_load(sfb_ctx *ctx, const void *blob, size_t n);

@@ -315,7 +315,8 @@ __global__ void k_voxel_feats(const double *__restrict__ pos, const double *__re
 
 template <class K>
 static void voxelize_typed(sfb_ctx *ctx, const double *pos, const double *col, int64_t n,
-                           const FrameParams *P, int key_bits, VoxelOut &out, DevCounts *C) {
+                           const FrameParams *P, int key_bits, VoxelOut &out, DevCounts *C,
+                           bool feats_on_side) {
     cudaStream_t st = ctx->stream;
     const unsigned g = dgrid(n, 256);
     // the library's own stable LSD sort (devprims.cu: 8-bit digits, 1024-item
@@ -355,9 +356,20 @@ static void voxelize_typed(sfb_ctx *ctx, const double *pos, const double *col, i
     }
     SFB_CHECK_LAUNCH();
     const int64_t vwarps = (ctx->grid_bound(n, ctx->hint_m[0]) + 4) / 5;
-    k_voxel_feats<<<dgrid(32 * vwarps, 256), 256, 0, st>>>(pos, col, out.order, out.offsets,
+    cudaStream_t fs = st;
+    if (feats_on_side) {   // fork: the sums need only the segmentation above
+        cudaEvent_t fork = ctx->side_ev[sfb_ctx::kSideEvents - 2];
+        SFB_CUDA(cudaEventRecord(fork, st));
+        SFB_CUDA(cudaStreamWaitEvent(ctx->side_stream, fork, 0));
+        fs = ctx->side_stream;
+    }
+    k_voxel_feats<<<dgrid(32 * vwarps, 256), 256, 0, fs>>>(pos, col, out.order, out.offsets,
                                                           out.coords, C, P, out.feats, out.feats32);
     SFB_CHECK_LAUNCH();
+    if (feats_on_side) {
+        SFB_CUDA(cudaEventRecord(ctx->side_ev[sfb_ctx::kSideEvents - 1], fs));
+        ctx->feats_pending = true;
+    }
 }
 
 // Host half of voxelize_adaptive's key setup: s and the per-axis ranges are
@@ -381,12 +393,13 @@ void voxel_layout(const double *lo_hi, double s, FrameParams &P) {
 }
 
 void voxelize_run(sfb_ctx *ctx, const double *pos, const double *col, int64_t n,
-                  const FrameParams &host, const FrameParams *P, VoxelOut &out, DevCounts *C) {
+                  const FrameParams &host, const FrameParams *P, VoxelOut &out, DevCounts *C,
+                  bool feats_on_side) {
     SFB_REQUIRE(n >= 2, "voxelization needs at least 2 points");
     SFB_REQUIRE(n < (int64_t(1) << 31), "at most 2^31-1 points per cloud");
     const int bits = host.total > 0 ? host.total : 1;
-    if (host.total <= 32) voxelize_typed<uint32_t>(ctx, pos, col, n, P, bits, out, C);
-    else voxelize_typed<unsigned long long>(ctx, pos, col, n, P, bits, out, C);
+    if (host.total <= 32) voxelize_typed<uint32_t>(ctx, pos, col, n, P, bits, out, C, feats_on_side);
+    else voxelize_typed<unsigned long long>(ctx, pos, col, n, P, bits, out, C, feats_on_side);
 }
 
 }  // namespace sfb
