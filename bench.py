@@ -36,6 +36,11 @@ from pathlib import Path
 
 import numpy as np
 
+# Frames in flight run on 12 lanes x 3 streams (main, side, aux) each: with the
+# default 8 hardware work queues, streams share queues and a frame's side-stream
+# kernels queue behind other lanes' work. Must be set before CUDA initialises.
+os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")
+
 ROOT = Path(__file__).resolve().parent
 sys.path.insert(0, str(ROOT))
 

@@ -240,7 +240,8 @@ int sfb_ctx_create(int device, sfb_ctx **out) {
         cudaStreamCreateWithFlags(&ctx->capture_stream, cudaStreamNonBlocking) != cudaSuccess ||
         cudaEventCreateWithFlags(&ctx->fork_event, cudaEventDisableTiming) != cudaSuccess ||
         cudaEventCreateWithFlags(&ctx->done_event, cudaEventDisableTiming) != cudaSuccess ||
-        cudaStreamCreateWithFlags(&ctx->side_stream, cudaStreamNonBlocking) != cudaSuccess) {
+        cudaStreamCreateWithFlags(&ctx->side_stream, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaStreamCreateWithFlags(&ctx->aux_stream, cudaStreamNonBlocking) != cudaSuccess) {
         delete ctx;
         return SFB_ERR_CUDA;
     }

@@ -153,8 +153,13 @@ struct sfb_ctx {
     // side branch of the frame (coordinate structure of the UNet levels runs
     // concurrently with the convolutions): its stream and fork/join events
     cudaStream_t side_stream = nullptr;
-    static constexpr int kSideEvents = 12;   // UNet levels + fork, and the last two:
-    cudaEvent_t side_ev[kSideEvents] = {};     // voxel-feature sums fork / join
+    cudaStream_t aux_stream = nullptr;   // the voxel feature sums, beside both
+    // events: UNet levels + fork (0..L), then the voxel-feature sums' fork /
+    // join and the binning stage's fork / join (the last four)
+    static constexpr int kSideEvents = 14;
+    static constexpr int kEvFeatsFork = kSideEvents - 4, kEvFeatsJoin = kSideEvents - 3;
+    static constexpr int kEvBinFork = kSideEvents - 2, kEvBinJoin = kSideEvents - 1;
+    cudaEvent_t side_ev[kSideEvents] = {};
     bool feats_pending = false;   // voxel features still being summed on the side stream
     std::vector<sfb_frame_graph *> graphs;
     int64_t graph_nodes = 0;
@@ -204,6 +209,7 @@ struct sfb_ctx {
             if (e) cudaEventDestroy(e);
         if (capture_stream) cudaStreamDestroy(capture_stream);
         if (side_stream) cudaStreamDestroy(side_stream);
+        if (aux_stream) cudaStreamDestroy(aux_stream);
         for (auto &e : side_ev)
             if (e) cudaEventDestroy(e);
         if (fork_event) cudaEventDestroy(fork_event);
@@ -390,7 +396,7 @@ void bbox_run(sfb_ctx *ctx, const double *pos, int64_t n, double *lo_hi_host);
 void bbox_async_run(sfb_ctx *ctx, const double *pos, int64_t n, uint64_t *ordered_host);
 void voxel_layout(const double *lo_hi, double s, FrameParams &P);
 // voxel count lands in C->m[0] (device)
-// feats_on_side: the per-voxel feature sums go to the side stream (they only
+// feats_on_side: the per-voxel feature sums go to the aux stream (they only
 // feed the first convolution, so the level-0 hash and kernel map overlap
 // them); ctx->feats_pending tells unet_run to join before it
 void voxelize_run(sfb_ctx *ctx, const double *pos, const double *col, int64_t n,

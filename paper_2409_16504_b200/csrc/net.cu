@@ -798,7 +798,7 @@ void unet_run(sfb_ctx *ctx, const int32_t *coords0, const double *feats9, int64_
     SFB_REQUIRE(net.loaded, "network weights are not loaded");
     const int L = net.levels;
     SFB_REQUIRE(L + 1 <= 9, "at most 8 UNet levels");
-    SFB_REQUIRE(L <= sfb_ctx::kSideEvents - 3, "too many UNet levels for the side branch");
+    SFB_REQUIRE(L < sfb_ctx::kEvFeatsFork, "too many UNet levels for the side branch");
     const auto &enc = net.enc;
     const auto &dec = net.dec;
     cudaStream_t st = ctx->stream;
@@ -818,20 +818,22 @@ void unet_run(sfb_ctx *ctx, const int32_t *coords0, const double *feats9, int64_
         int layer = 0;
         for (int l = 0; l <= L; ++l) kern[l] = net.layers[layer++].kernel;
     }
+    // side branch fork point: the coordinate structure of the coarser levels
+    // needs only the level-0 coordinates, so it starts with the level-0 hash
+    SFB_CUDA(cudaEventRecord(ctx->side_ev[L], st));
     // level 0: hash + kernel map on the critical path
     HashTable h0;
     nbr[0] = ctx->arena.alloc<int32_t>((size_t)kern[0] * kern[0] * kern[0] * mbl[0]);
     h0 = hash_build(ctx, coords[0], &C->m[0], mbl[0], mg[0]);
     kernel_map_build(ctx, h0, coords[0], &C->m[0], mbl[0], 1, kern[0], nbr[0], mg[0]);
-    if (ctx->feats_pending) {   // join the voxel-feature sums (voxelize_run on the side stream)
-        SFB_CUDA(cudaStreamWaitEvent(st, ctx->side_ev[sfb_ctx::kSideEvents - 1], 0));
+    if (ctx->feats_pending) {   // join the voxel-feature sums (voxelize_run on the aux stream)
+        SFB_CUDA(cudaStreamWaitEvent(st, ctx->side_ev[sfb_ctx::kEvFeatsJoin], 0));
         ctx->feats_pending = false;
     }
     // side branch: the coordinate structure of every coarser level (parents,
     // children, taps, hash = the pooling table, kernel map) depends only on
-    // coordinates, so it runs concurrently with the convolutions; event l
-    // marks "level l+1 structure and kernel map ready"
-    SFB_CUDA(cudaEventRecord(ctx->side_ev[L], st));
+    // coordinates, so it runs concurrently with the level-0 kernel map and
+    // the convolutions; event l marks "level l+1 structure and kernel map ready"
     SFB_CUDA(cudaStreamWaitEvent(ctx->side_stream, ctx->side_ev[L], 0));
     ctx->stream = ctx->side_stream;
     try {

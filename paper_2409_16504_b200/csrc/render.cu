@@ -1546,16 +1546,28 @@ void render_run(sfb_ctx *ctx, const RenderInputs &in, const FrameParams *FP, int
                                                           in.normals, &C->kept, scol, snrm);
             SFB_CHECK_LAUNCH();
         }
-        k_stage_runs<<<dgrid(ctx->grid_bound(n, ctx->hint_runs), 256), 256, 0, st>>>(
-            R, src, in.point_to_geom, in.normals, P.depth, want_n ? 1 : 0);
-        SFB_CHECK_LAUNCH();
-        // stable sort by tile id keeps each tile's runs in rank order
+        // side stream: the run staging and the super-tile list sort run beside
+        // the fine-tile list sort (all three need only k_emit's output)
         const int fbits = bits_for((uint64_t)nt), sbits = bits_for((uint64_t)ns);
-        f_ids = dsort_pairs<uint32_t>(ctx, fkey, fval, fkey2, fval2, &C->ef, ebound, fbits) ? fval2 : fval;
-        const uint32_t *fk = (f_ids == fval2) ? fkey2 : fkey;
-        s_ids = dsort_pairs<uint32_t>(ctx, skey, sval, skey2, sval2, &C->es, ebound, sbits) ? sval2 : sval;
+        SFB_CUDA(cudaEventRecord(ctx->side_ev[sfb_ctx::kEvBinFork], st));
+        SFB_CUDA(cudaStreamWaitEvent(ctx->side_stream, ctx->side_ev[sfb_ctx::kEvBinFork], 0));
+        ctx->stream = ctx->side_stream;
+        try {
+            k_stage_runs<<<dgrid(ctx->grid_bound(n, ctx->hint_runs), 256), 256, 0, ctx->stream>>>(
+                R, src, in.point_to_geom, in.normals, P.depth, want_n ? 1 : 0);
+            SFB_CHECK_LAUNCH();
+            // stable sort by tile id keeps each tile's runs in rank order
+            s_ids = dsort_pairs<uint32_t>(ctx, skey, sval, skey2, sval2, &C->es, ebound, sbits) ? sval2 : sval;
+            SFB_CUDA(cudaEventRecord(ctx->side_ev[sfb_ctx::kEvBinJoin], ctx->stream));
+        } catch (...) {
+            ctx->stream = st;
+            throw;
+        }
+        ctx->stream = st;
         sk_sorted = (s_ids == sval2) ? skey2 : skey;
-        fk_sorted = fk;
+        f_ids = dsort_pairs<uint32_t>(ctx, fkey, fval, fkey2, fval2, &C->ef, ebound, fbits) ? fval2 : fval;
+        fk_sorted = (f_ids == fval2) ? fkey2 : fkey;
+        SFB_CUDA(cudaStreamWaitEvent(st, ctx->side_ev[sfb_ctx::kEvBinJoin], 0));
     }
     // tile offsets by binary search in the sorted keys (no histogram / scan),
     // and the super-list rects in list order, in one launch

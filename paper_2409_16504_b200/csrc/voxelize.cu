@@ -358,16 +358,16 @@ static void voxelize_typed(sfb_ctx *ctx, const double *pos, const double *col, i
     const int64_t vwarps = (ctx->grid_bound(n, ctx->hint_m[0]) + 4) / 5;
     cudaStream_t fs = st;
     if (feats_on_side) {   // fork: the sums need only the segmentation above
-        cudaEvent_t fork = ctx->side_ev[sfb_ctx::kSideEvents - 2];
+        cudaEvent_t fork = ctx->side_ev[sfb_ctx::kEvFeatsFork];
         SFB_CUDA(cudaEventRecord(fork, st));
-        SFB_CUDA(cudaStreamWaitEvent(ctx->side_stream, fork, 0));
-        fs = ctx->side_stream;
+        SFB_CUDA(cudaStreamWaitEvent(ctx->aux_stream, fork, 0));
+        fs = ctx->aux_stream;
     }
     k_voxel_feats<<<dgrid(32 * vwarps, 256), 256, 0, fs>>>(pos, col, out.order, out.offsets,
                                                           out.coords, C, P, out.feats, out.feats32);
     SFB_CHECK_LAUNCH();
     if (feats_on_side) {
-        SFB_CUDA(cudaEventRecord(ctx->side_ev[sfb_ctx::kSideEvents - 1], fs));
+        SFB_CUDA(cudaEventRecord(ctx->side_ev[sfb_ctx::kEvFeatsJoin], fs));
         ctx->feats_pending = true;
     }
 }
