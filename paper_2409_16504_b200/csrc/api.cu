@@ -46,7 +46,15 @@ int guard(sfb_ctx *ctx, F &&f) {
         try {
             f();
         } catch (...) {
-            record_done(ctx);   // whatever was enqueued before the error
+            // whatever was enqueued before the error, including work still
+            // forked on the side / aux streams (joined here so the next call's
+            // arena reuse is ordered after it); errors are ignored on this path
+            for (cudaStream_t s : {ctx->side_stream, ctx->aux_stream}) {
+                if (s && cudaEventRecord(ctx->side_ev[sfb_ctx::kEvFeatsJoin], s) == cudaSuccess)
+                    cudaStreamWaitEvent(ctx->stream, ctx->side_ev[sfb_ctx::kEvFeatsJoin], 0);
+            }
+            cudaGetLastError();
+            record_done(ctx);
             throw;
         }
         record_done(ctx);
