@@ -30,6 +30,17 @@ void record_done(sfb_ctx *ctx) {
     }
 }
 
+// Join whatever the side / aux streams still hold into ctx->stream (error
+// paths: an abandoned capture must not end with unjoined streams, and the next
+// call's arena reuse must be ordered after forked work). Errors are ignored.
+void join_forked(sfb_ctx *ctx) {
+    for (cudaStream_t s : {ctx->side_stream, ctx->aux_stream}) {
+        if (s && cudaEventRecord(ctx->side_ev[sfb_ctx::kEvFeatsJoin], s) == cudaSuccess)
+            cudaStreamWaitEvent(ctx->stream, ctx->side_ev[sfb_ctx::kEvFeatsJoin], 0);
+    }
+    cudaGetLastError();
+}
+
 template <class F>
 int guard(sfb_ctx *ctx, F &&f) {
     if (!ctx) return SFB_ERR_ARG;
@@ -46,14 +57,7 @@ int guard(sfb_ctx *ctx, F &&f) {
         try {
             f();
         } catch (...) {
-            // whatever was enqueued before the error, including work still
-            // forked on the side / aux streams (joined here so the next call's
-            // arena reuse is ordered after it); errors are ignored on this path
-            for (cudaStream_t s : {ctx->side_stream, ctx->aux_stream}) {
-                if (s && cudaEventRecord(ctx->side_ev[sfb_ctx::kEvFeatsJoin], s) == cudaSuccess)
-                    cudaStreamWaitEvent(ctx->stream, ctx->side_ev[sfb_ctx::kEvFeatsJoin], 0);
-            }
-            cudaGetLastError();
+            join_forked(ctx);   // whatever was enqueued before the error
             record_done(ctx);
             throw;
         }
@@ -755,6 +759,7 @@ static int frame_impl(sfb_ctx *ctx, const double *positions, const double *color
                 // drop the capture, run this frame eagerly (growing the arena),
                 // capture on the next call
                 ctx->arena.no_grow = false;
+                join_forked(ctx);   // side / aux branches of the abandoned capture
                 cudaGraph_t junk = nullptr;
                 cudaStreamEndCapture(ctx->stream, &junk);
                 if (junk) cudaGraphDestroy(junk);
@@ -767,6 +772,7 @@ static int frame_impl(sfb_ctx *ctx, const double *positions, const double *color
                 return;
             } catch (...) {
                 ctx->arena.no_grow = false;
+                join_forked(ctx);
                 cudaGraph_t junk = nullptr;
                 cudaStreamEndCapture(ctx->stream, &junk);
                 if (junk) cudaGraphDestroy(junk);
