@@ -36,7 +36,7 @@ from pathlib import Path
 
 import numpy as np
 
-# Frames in flight run on 12 lanes x 3 streams (main, side, aux) each: with the
+# Frames in flight run on 10 lanes x 3 streams (main, side, aux) each: with the
 # default 8 hardware work queues, streams share queues and a frame's side-stream
 # kernels queue behind other lanes' work. Must be set before CUDA initialises.
 os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")
@@ -65,7 +65,7 @@ def parse():
                     help="render only this view (profiling runs; default: views round-robin)")
     ap.add_argument("--cpu-frames", type=int, default=1,
                     help="full config-2 frames of the CPU port timed for cpu_baseline")
-    ap.add_argument("--lanes", type=int, default=12, help="frames in flight per GPU (streams)")
+    ap.add_argument("--lanes", type=int, default=10, help="frames in flight per GPU (streams)")
     ap.add_argument("--e2e-lanes", type=int, default=8,
                     help="frames in flight in the e2e (host-buffer) legs (PCIe-bound; 20-frame "
                          "runs: 4/6/8/12 lanes 0.876/0.871/0.873/0.870-0.908 ms, 12 with outliers); "
