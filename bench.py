@@ -66,6 +66,8 @@ def parse():
     ap.add_argument("--cpu-frames", type=int, default=1,
                     help="full config-2 frames of the CPU port timed for cpu_baseline")
     ap.add_argument("--lanes", type=int, default=10, help="frames in flight per GPU (streams)")
+    ap.add_argument("--stage-ahead", type=int, default=2,
+                    help="host clouds: uploads enqueued this many frames ahead (< e2e lanes)")
     ap.add_argument("--e2e-lanes", type=int, default=8,
                     help="frames in flight in the e2e (host-buffer) legs (PCIe-bound; 20-frame "
                          "runs: 4/6/8/12 lanes 0.876/0.871/0.873/0.870-0.908 ms, 12 with outliers); "
@@ -333,7 +335,7 @@ def run_ours(args):
         # engine has ~2 frames of work queued and host hiccups do not idle it
         # (frames i and i+ahead must not share a lane: a lane has two staging buffers)
         nl = active[0]
-        ahead = 2 if nl >= 3 else 1
+        ahead = min(args.stage_ahead, nl - 1) if nl >= 3 else 1
         staged = [stage(cloud_list[j % copies], j % nl) for j in range(min(ahead, n_frames))] \
             if host_in else []
         for i in range(n_frames):
